@@ -1,0 +1,140 @@
+"""Oracle: discrete-step simulation of one group's sampling loop.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Follows PAPER.md Alg. 1 (l.218-241) step by step, with the modes of §3.1-3.2:
+  full      all G samples decode in parallel (g = G)
+  naive     N = G/g micro groups in trace order with a barrier  §3.1 l.164-170
+  fifo      fixed-slot continuous sampling, quota N per slot,   §3.2 l.196-198
+            trace-order refill                                  (reading R19)
+  infinite  Alg. 1: [optional prefix phase of k tokens in ceil(G/g) barriered
+            rounds, l.215-216, l.371] -> Alg. 2 plan -> first g samples from the
+            mask -> SJF refill (Alg. 3) with no quota           (R17-R22)
+
+One step = one token for every occupied slot (R20: a step
+happens while >= 1 slot is active).  Termination is trace-driven (R5): sample
+uid finishes after exactly true_len[uid] tokens.  Several slots finishing in
+one step are handled in ascending slot index; a refilled sample decodes its
+first token in the next step (R18).
+
+KV accounting ("fixed-size memory pool", l.205 "recycled
+upon completion"; R26): each sample owns pages of `page_tokens` tokens,
+allocated when it writes token t with t % page_tokens == 0 and released when
+it finishes; parked prefix-phase samples keep theirs (l.371).  live_pages[step]
+is counted after the step's allocations.
+"""
+from dataclasses import dataclass, field
+
+from .planner import build_plan
+
+
+@dataclass
+class SimResult:
+    total_steps: int = 0
+    slot_table: list = field(default_factory=list)   # [step][slot] -> uid or -1
+    live_pages: list = field(default_factory=list)   # [step] -> pages allocated
+    peak_pages: int = 0
+    start_step: dict = field(default_factory=dict)   # uid -> first step decoded (1-based)
+    finish_step: dict = field(default_factory=dict)  # uid -> step its last token was decoded
+    events: list = field(default_factory=list)       # (step, slot, uid, kind)
+    tokens_decoded: int = 0
+    prefix_steps: int = 0
+    init: list = field(default_factory=list)
+    queue: list = field(default_factory=list)
+    plan: dict = None
+
+
+def simulate(true_len, mode, g, pred=None, eps=0.1, prefix_k=0, page_tokens=16):
+    true_len = [int(x) for x in true_len]
+    G = len(true_len)
+    if mode == "full":
+        g = G
+    if g < 1 or G % g != 0:
+        raise ValueError("IS_ERR_CONFIG: G mod g != 0")
+    N = G // g
+    res = SimResult()
+    t = [0] * G
+    pages = [0] * G
+    finished = set()
+    slot = [-1] * g
+    count = [0] * g              # samples ever run by slot (fifo quota)
+    step = 0
+
+    def run_phase(queue, stop_at, barrier, quota, init):
+        nonlocal step
+        for s, uid in enumerate(init):
+            slot[s] = uid
+        q = list(queue)
+        while any(u >= 0 for u in slot):
+            step += 1
+            for s in range(g):
+                uid = slot[s]
+                if uid >= 0:
+                    if t[uid] == 0 and uid not in res.start_step:
+                        res.start_step[uid] = step
+                    if t[uid] % page_tokens == 0:
+                        pages[uid] += 1
+            live = sum(pages)
+            res.live_pages.append(live)
+            res.peak_pages = max(res.peak_pages, live)
+            res.slot_table.append(list(slot))
+            for s in range(g):
+                if slot[s] >= 0:
+                    t[slot[s]] += 1
+                    res.tokens_decoded += 1
+            for s in range(g):                     # ascending slot index (R18)
+                uid = slot[s]
+                if uid < 0:
+                    continue
+                if t[uid] == true_len[uid]:
+                    finished.add(uid)
+                    res.finish_step[uid] = step
+                    pages[uid] = 0
+                    res.events.append((step, s, uid, "finish"))
+                elif t[uid] == stop_at(uid):
+                    res.events.append((step, s, uid, "park"))
+                else:
+                    continue
+                slot[s] = -1
+                count[s] += 1
+                if not barrier and q and (quota == 0 or count[s] < quota):
+                    slot[s] = q.pop(0)
+                    res.events.append((step, s, slot[s], "refill"))
+            if barrier and all(u < 0 for u in slot) and q:
+                for s in range(g):
+                    if q:
+                        slot[s] = q.pop(0)
+                        res.events.append((step, s, slot[s], "refill"))
+
+    big = 1 << 30
+    if mode in ("full", "naive"):
+        p = build_plan(mode, G, g)
+        res.init, res.queue = p["init"], p["queue"]
+        run_phase(p["queue"], lambda u: big, True, 0, p["init"])
+    elif mode == "fifo":
+        p = build_plan(mode, G, g)
+        res.init, res.queue = p["init"], p["queue"]
+        run_phase(p["queue"], lambda u: big, False, N, p["init"])
+    elif mode == "infinite":
+        if pred is None:
+            raise ValueError("infinite mode needs predicted lengths")
+        if prefix_k > 0:
+            order = list(range(G))
+            run_phase(order[g:], lambda u: min(prefix_k, true_len[u]), True, 0, order[:g])
+            res.prefix_steps = step
+            # R22 / SPEC l.59: samples that finished in the prefix phase have pred = true
+            pred = [true_len[i] if true_len[i] <= prefix_k else int(pred[i]) for i in range(G)]
+        p = build_plan("infinite", G, g, pred=pred, eps=eps, finished=finished)
+        res.init, res.queue, res.plan = p["init"], p["queue"], p["plan"]
+        count[:] = [0] * g
+        run_phase(p["queue"], lambda u: big, False, 0, p["init"])
+    else:
+        raise ValueError(f"IS_ERR_CONFIG: unknown mode {mode}")
+    res.total_steps = step
+    assert len(finished) == G
+    return res
+
+
+def step_lower_bound(true_len, g):
+    """max(max len, ceil(sum / g))."""
+    return max(max(true_len), -(-sum(true_len) // g))

@@ -1,0 +1,202 @@
+/* infsamp.h -- C ABI of libinfsamp, the B200 (sm_100a) continuous-sampling
+ * decode step of Infinite Sampling (arXiv 2506.22950).
+ *
+ * Conventions
+ *   - Every call returns is_status; nothing aborts and no C++ exception crosses
+ *     the ABI.  is_last_error() returns a one-line "IS_ERR_<CODE>: <detail>"
+ *     message for the calling thread.
+ *   - Pointers named d_* are DEVICE pointers (cudaMalloc / torch CUDA memory),
+ *     h_* are HOST pointers.  The caller owns every buffer it passes; the
+ *     library owns only what is_create allocates (packed weights, shared prefix
+ *     KV, the KV page pool, slot/page tables, activations) and frees it in
+ *     is_destroy.
+ *   - A context is bound to one CUDA stream and one host thread; distinct
+ *     contexts are independent.  Device work is asynchronous on that stream;
+ *     CUDA errors surface as IS_ERR_CUDA on the next call (CUDA's convention).
+ *   - Same inputs + same seed => byte-identical tokens, schedules and stats.
+ *
+ * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; R<k> = DESIGN.md
+ * reading k.
+ */
+#ifndef INFSAMP_H_
+#define INFSAMP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  IS_OK = 0,
+  IS_ERR_CONFIG = 1,   /* invalid shape / G mod g != 0 / eps <= 0 / N <= 0 */
+  IS_ERR_BUDGET = 2,   /* worst-case KV reservation exceeds kv_budget_bytes (R25) */
+  IS_ERR_CAPACITY = 3, /* a fixed capacity (rows, steps, pages) would be exceeded */
+  IS_ERR_DATA = 4,     /* missing or < 1 lengths, bad token ids */
+  IS_ERR_STATE = 5,    /* call order violated (e.g. decode before prefill) */
+  IS_ERR_CUDA = 6      /* a CUDA runtime/driver error */
+} is_status;
+
+/* Sampling-loop policy (Alg. 1). */
+typedef enum {
+  IS_MODE_FULL = 0,    /* all G samples decode in parallel (g = G); unbudgeted reference */
+  IS_MODE_NAIVE = 1,   /* N = G/g micro groups, barrier between groups */
+  IS_MODE_FIFO = 2,    /* fixed-slot continuous sampling: quota N per slot, trace order (R19) */
+  IS_MODE_INFINITE = 3 /* Alg. 1: [prefix phase] + Alg. 2 FPTAS plan + Alg. 3 SJF refill */
+} is_mode;
+
+typedef enum { IS_ADV_STD_NORM = 0, IS_ADV_MEAN_ONLY = 1 } is_adv_mode;
+
+/* Qwen3-shaped decoder (shapes R1).  head_dim must be 128. */
+typedef struct {
+  int32_t layers, hidden, n_q_heads, n_kv_heads, head_dim, ffn, vocab;
+  float rms_eps, rope_theta;
+} is_shape;
+
+typedef struct {
+  is_shape shape;
+  int32_t G;               /* group size */
+  int32_t g;               /* micro-group size = decoding slots; ignored (= G) in FULL mode */
+  int32_t max_new_tokens;  /* generation cap (1024) */
+  int32_t prompt_len;      /* P; the shared prefix holds positions 0..P-2 (R6) */
+  int32_t prefix_k;        /* tokens decoded before length prediction; 0 = none */
+  int32_t page_tokens;     /* tokens per KV page (16) */
+  int32_t row_capacity;    /* rows of the fixed per-step batch (>= slots, <= 64); 0 = round_up(g, 16).
+                              Kernel configuration depends only on this (batch invariance, R12). */
+  int64_t kv_budget_bytes; /* KV budget (prefix + pages); <= 0 means unbudgeted (R25) */
+  double eps;              /* FPTAS tolerance epsilon (Alg. 2) */
+  float temperature;       /* sampling temperature (0.8) */
+  uint64_t seed;           /* Philox key (R11) */
+  is_mode mode;
+} is_config;
+
+/* Alg. 2 output plus the runtime plan (Alg. 1, Alg. 3).  All arrays are
+ * caller-allocated with the sizes given. */
+typedef struct {
+  int32_t* mask;          /* [G][2]: (group n in 1..N, position j) */
+  int64_t* scaled_len;    /* [G]: l~_i = ceil(l^_i / K) */
+  int64_t* loads;         /* [N]: L_n */
+  int32_t* overflow_ids;  /* [G]: samples placed by the least-loaded fallback (R15) */
+  int32_t* init_slots;    /* [g]: first g samples from mask, lexicographic (n, j) (R13) */
+  int32_t* refill_queue;  /* [G]: static SJF order of the remaining samples (R17) */
+  double K;               /* scale K = eps*S/N */
+  int64_t capacity;       /* C~ = ceil(sum l~ / N) */
+  int32_t n_overflow;
+  int32_t queue_len;
+  int64_t reserved_bytes; /* worst-case live KV bytes of this plan (R25) */
+} is_plan_out;
+
+typedef struct {
+  int32_t steps;          /* decode steps run for the current group */
+  int32_t prefix_steps;   /* of which in the prefix phase (R22) */
+  int32_t completed;      /* samples finished */
+  int32_t live_pages;     /* KV pages allocated now */
+  int32_t peak_pages;     /* max over steps (R26) */
+  int32_t error;          /* device-side error flag (page pool exhausted = budget violated) */
+  int64_t tokens_decoded; /* sum of active slots over steps */
+  int64_t peak_kv_bytes;  /* prefix bytes + peak_pages * page bytes (R26) */
+  int64_t page_bytes;
+  int64_t prefix_bytes;
+  int32_t num_pages;      /* size of the page pool */
+  int32_t row_capacity;
+} is_stats;
+
+typedef struct is_ctx is_ctx;
+
+/* Alg. 2 + Alg. 1 initial fill + Alg. 3 static refill order + budget check.
+ * Pure host function.  h_pred_len[G] >= 1; h_finished[G] (nullable) marks
+ * samples that completed in the prefix phase (R22).  mode FULL/NAIVE/FIFO
+ * return the trace-order plan (mask etc. zeroed).  Errors: IS_ERR_CONFIG,
+ * IS_ERR_DATA, IS_ERR_BUDGET. */
+is_status is_plan(const is_config* cfg, const int32_t* h_pred_len, const uint8_t* h_finished,
+                  is_plan_out* out);
+
+/* Creates a context: packs the weights into the library's own layout, sizes
+ * the KV page pool from kv_budget_bytes (or from the full-length worst case
+ * when unbudgeted), captures the decode step.  d_weights: n_weights device
+ * pointers to bf16 tensors in HF Qwen3 layout ([out, in]) in the order
+ *   embed[V,H], final_norm[H], then per layer l = 0..L-1:
+ *   in_norm[H], wq[Hq*d,H], wk[Hkv*d,H], wv[Hkv*d,H], q_norm[d], k_norm[d],
+ *   wo[H,Hq*d], post_norm[H], w_gate[F,H], w_up[F,H], w_down[H,F]
+ * (n_weights = 2 + 11*L).  The caller's weights are only read during this call.
+ * stream: a cudaStream_t (NULL = legacy default stream). */
+is_status is_create(const is_config* cfg, const void* const* d_weights, int32_t n_weights, void* stream,
+                    is_ctx** out);
+void is_destroy(is_ctx* ctx);
+
+/* Prefill the prompt ("retain the prefill KV cache for the prompt
+ * itself, which is shared by all groups"): a causal forward over positions
+ * 0..P-2 writes the shared, read-only prefix KV.  d_prompt: [prompt_len] int32
+ * token ids in [0, vocab).  prompt_id keys the RNG (uid = prompt_id*G + i, R11). */
+is_status is_prefill(is_ctx* ctx, const int32_t* d_prompt, int32_t prompt_id);
+
+/* Start the sampling loop for the prefilled prompt.  h_true_len[G]: trace
+ * lengths (termination, R5); h_pred_len[G]: predicted lengths for Alg. 2
+ * (INFINITE only; nullable otherwise).  Runs is_plan, checks the budget,
+ * uploads the plan and fills the g slots (Alg. 1).  With prefix_k > 0
+ * (INFINITE) the prefix phase runs first in ceil(G/g) barriered rounds (R22);
+ * the plan is installed on the device and takes over when it ends. */
+is_status is_start_group(is_ctx* ctx, const int32_t* h_true_len, const int32_t* h_pred_len);
+
+/* One decode step: every active slot attends to the shared prefix
+ * plus its own pages, samples its next token, then finished slots are refilled
+ * in place (is_refill).  d_next_tokens / d_finished: [row_capacity] device
+ * buffers (nullable) receiving the sampled token / finish flag per slot
+ * (-1 / 0 for idle slots).  Asynchronous: no host synchronisation. */
+is_status is_decode_step(is_ctx* ctx, int32_t* d_next_tokens, uint8_t* d_finished);
+
+/* Finish/refill/page-recycle policy alone (Alg. 3, "cache is
+ * cleared and the memory is reassigned back to the pool"): consumes the last
+ * sampled keys, appends tokens, finishes/parks samples, refills freed slots in
+ * ascending slot order from the static queue, allocates pages for the next
+ * step.  Called inside is_decode_step; exported for tests.  d_new_uid
+ * [row_capacity] (nullable) receives the uid now in each slot (-1 idle). */
+is_status is_refill(is_ctx* ctx, uint8_t* d_finished, int32_t* d_new_uid);
+
+/* Decode steps until the group completes (bounded host run-ahead, no per-step
+ * sync).  h_steps (nullable) receives the number of steps. */
+is_status is_run_group(is_ctx* ctx, int32_t max_steps, int32_t* h_steps);
+
+is_status is_query(is_ctx* ctx, is_stats* out); /* synchronises the stream */
+
+/* Generated tokens [G][max_new_tokens] (row uid-major, -1 beyond true_len). */
+is_status is_copy_tokens(is_ctx* ctx, int32_t* dst, int32_t dst_is_device);
+
+/* Per-step schedule log: slot table [max_steps][g] (uid or -1) and live pages
+ * [max_steps] (R26); returns the number of logged steps in *h_n. */
+is_status is_copy_schedule(is_ctx* ctx, int32_t* h_slot_table, int32_t* h_live_pages, int32_t max_steps,
+                           int32_t* h_n);
+
+/* Benchmark reward and completion length per sample (R29):
+ * d_reward[G] = #{tokens < vocab/2}/len, d_len[G] = len.  Device buffers. */
+is_status is_group_results(is_ctx* ctx, float* d_reward, int32_t* d_len);
+
+/* Group advantages, Eq. 2 or mean-only; fp64 sums in
+ * ascending index, population sigma, sigma = 0 -> 0 (R28).  Host pointers. */
+is_status is_group_advantages(const float* h_rewards, int32_t G, is_adv_mode mode, float* h_adv);
+
+/* Debug: when d_logits != NULL every following lm_head launch also writes its
+ * fp32 logits to d_logits[row_capacity][vocab] (sampler parity, R12 (i)). */
+is_status is_set_logits_dump(is_ctx* ctx, float* d_logits);
+
+/* Per-launch timing of the kernels of one decode step (CUDA events on the
+ * context stream, step replayed eagerly, not from the graph): h_ms[n] receives
+ * the milliseconds of launch i and h_kind[n] its kind (0 embed/norm, 1 QKV GEMM,
+ * 2 qkv post, 3 attention, 4 o_proj, 5 gate/up, 6 down, 7 lm_head+sampler,
+ * 8 refill).  Returns the number of launches in *h_n. */
+is_status is_profile_step(is_ctx* ctx, float* h_ms, int32_t* h_kind, int32_t cap, int32_t* h_n);
+
+/* Kernel-level test hook: one tcgen05 swap-AB GEMM Y[n][m] = sum_k X[n][k] W[m][k]
+ * (X: d_x [rows][K] bf16, W: d_w [M][K] bf16, Y: d_y [rows][M] fp32),
+ * rows <= 64, K % 64 == 0, on `stream`. split = K-split cluster size (1..8). */
+is_status is_dbg_gemm(const void* d_w, const void* d_x, float* d_y, int32_t M, int32_t K, int32_t rows,
+                      int32_t split, void* stream);
+
+const char* is_last_error(void);
+const char* is_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* INFSAMP_H_ */

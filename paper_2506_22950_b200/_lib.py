@@ -1,0 +1,269 @@
+"""Thin ctypes binding of libinfsamp (include/infsamp.h).
+
+Argument marshalling only: every step of the decode path runs in the CUDA
+kernels of libinfsamp.so.  There is no Python or CPU fallback; if the shared
+library is missing or the device is not sm_100 the calls raise.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+from . import build as _build
+
+IS_OK, IS_ERR_CONFIG, IS_ERR_BUDGET, IS_ERR_CAPACITY, IS_ERR_DATA, IS_ERR_STATE, IS_ERR_CUDA = range(7)
+MODES = {"full": 0, "naive": 1, "fifo": 2, "infinite": 3}
+ADV_MODES = {"std_norm": 0, "mean_only": 1}
+
+EXPORTS = ["is_plan", "is_create", "is_destroy", "is_prefill", "is_start_group", "is_decode_step",
+           "is_refill", "is_run_group", "is_query", "is_copy_tokens", "is_copy_schedule",
+           "is_group_results", "is_group_advantages", "is_set_logits_dump", "is_profile_step",
+           "is_dbg_gemm", "is_last_error", "is_version"]
+
+
+class InfsampError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(msg)
+        self.status = status
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [("layers", ctypes.c_int32), ("hidden", ctypes.c_int32), ("n_q_heads", ctypes.c_int32),
+                ("n_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32), ("ffn", ctypes.c_int32),
+                ("vocab", ctypes.c_int32), ("rms_eps", ctypes.c_float), ("rope_theta", ctypes.c_float)]
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("shape", Shape), ("G", ctypes.c_int32), ("g", ctypes.c_int32),
+                ("max_new_tokens", ctypes.c_int32), ("prompt_len", ctypes.c_int32),
+                ("prefix_k", ctypes.c_int32), ("page_tokens", ctypes.c_int32),
+                ("row_capacity", ctypes.c_int32), ("kv_budget_bytes", ctypes.c_int64),
+                ("eps", ctypes.c_double), ("temperature", ctypes.c_float), ("seed", ctypes.c_uint64),
+                ("mode", ctypes.c_int32)]
+
+
+class PlanOut(ctypes.Structure):
+    _fields_ = [("mask", ctypes.POINTER(ctypes.c_int32)), ("scaled_len", ctypes.POINTER(ctypes.c_int64)),
+                ("loads", ctypes.POINTER(ctypes.c_int64)), ("overflow_ids", ctypes.POINTER(ctypes.c_int32)),
+                ("init_slots", ctypes.POINTER(ctypes.c_int32)),
+                ("refill_queue", ctypes.POINTER(ctypes.c_int32)), ("K", ctypes.c_double),
+                ("capacity", ctypes.c_int64), ("n_overflow", ctypes.c_int32), ("queue_len", ctypes.c_int32),
+                ("reserved_bytes", ctypes.c_int64)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("steps", ctypes.c_int32), ("prefix_steps", ctypes.c_int32), ("completed", ctypes.c_int32),
+                ("live_pages", ctypes.c_int32), ("peak_pages", ctypes.c_int32), ("error", ctypes.c_int32),
+                ("tokens_decoded", ctypes.c_int64), ("peak_kv_bytes", ctypes.c_int64),
+                ("page_bytes", ctypes.c_int64), ("prefix_bytes", ctypes.c_int64),
+                ("num_pages", ctypes.c_int32), ("row_capacity", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_LIB = None
+
+
+def lib_path():
+    return _build.OUT
+
+
+def load(build_if_missing=True):
+    """Load libinfsamp.so (building it in-tree first if it is missing or stale)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if build_if_missing:
+        try:
+            _build.build()
+        except Exception:
+            if not os.path.exists(_build.OUT):
+                raise
+    if not os.path.exists(_build.OUT):
+        raise InfsampError(IS_ERR_STATE, f"libinfsamp.so not found at {_build.OUT}; run paper_2506_22950_b200.build")
+    L = ctypes.CDLL(_build.OUT)
+    vp, i32, i64p = ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)
+    L.is_plan.argtypes = [ctypes.POINTER(Config), vp, vp, ctypes.POINTER(PlanOut)]
+    L.is_create.argtypes = [ctypes.POINTER(Config), ctypes.POINTER(ctypes.c_void_p), i32, vp, ctypes.POINTER(vp)]
+    L.is_destroy.argtypes = [vp]
+    L.is_destroy.restype = None
+    L.is_prefill.argtypes = [vp, vp, i32]
+    L.is_start_group.argtypes = [vp, vp, vp]
+    L.is_decode_step.argtypes = [vp, vp, vp]
+    L.is_refill.argtypes = [vp, vp, vp]
+    L.is_run_group.argtypes = [vp, i32, ctypes.POINTER(i32)]
+    L.is_query.argtypes = [vp, ctypes.POINTER(Stats)]
+    L.is_copy_tokens.argtypes = [vp, vp, i32]
+    L.is_copy_schedule.argtypes = [vp, vp, vp, i32, ctypes.POINTER(i32)]
+    L.is_group_results.argtypes = [vp, vp, vp]
+    L.is_group_advantages.argtypes = [vp, i32, i32, vp]
+    L.is_set_logits_dump.argtypes = [vp, vp]
+    L.is_profile_step.argtypes = [vp, vp, vp, i32, ctypes.POINTER(i32)]
+    L.is_dbg_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]
+    L.is_last_error.restype = ctypes.c_char_p
+    L.is_last_error.argtypes = []
+    L.is_version.restype = ctypes.c_char_p
+    for name in EXPORTS:
+        if name not in ("is_destroy", "is_last_error", "is_version"):
+            getattr(L, name).restype = ctypes.c_int
+    _LIB = L
+    return L
+
+
+def _check(status):
+    if status != IS_OK:
+        raise InfsampError(status, _LIB.is_last_error().decode())
+
+
+def _np_ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix_k=0, page_tokens=16,
+                row_capacity=0, kv_budget_bytes=0, eps=0.1, temperature=0.8, seed=20261017):
+    c = Config()
+    c.shape = Shape(shape.layers, shape.hidden, shape.n_q_heads, shape.n_kv_heads, shape.head_dim, shape.ffn,
+                    shape.vocab, shape.rms_eps, shape.rope_theta)
+    c.G, c.g, c.max_new_tokens, c.prompt_len = G, g, max_new_tokens, prompt_len
+    c.prefix_k, c.page_tokens, c.row_capacity = prefix_k, page_tokens, row_capacity
+    c.kv_budget_bytes, c.eps, c.temperature, c.seed = kv_budget_bytes, eps, temperature, seed
+    c.mode = MODES[mode] if isinstance(mode, str) else int(mode)
+    return c
+
+
+def is_plan(cfg, pred_len, finished=None):
+    """Alg. 2 + initial fill + SJF queue + budget check (host)."""
+    L = load()
+    G = cfg.G
+    g = G if cfg.mode == MODES["full"] else cfg.g
+    N = G // g if g else 1
+    mask = np.zeros(2 * G, np.int32)
+    sl = np.zeros(G, np.int64)
+    loads = np.zeros(max(N, 1), np.int64)
+    ovf = np.zeros(G, np.int32)
+    init = np.zeros(max(g, 1), np.int32)
+    queue = np.zeros(G, np.int32)
+    out = PlanOut(mask.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), sl.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                  loads.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ovf.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                  init.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), queue.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                  0.0, 0, 0, 0, 0)
+    pred = None if pred_len is None else np.ascontiguousarray(pred_len, np.int32)
+    fin = None if finished is None else np.ascontiguousarray(finished, np.uint8)
+    _check(L.is_plan(ctypes.byref(cfg), None if pred is None else _np_ptr(pred),
+                     None if fin is None else _np_ptr(fin), ctypes.byref(out)))
+    return dict(mask=[(int(mask[2 * i]), int(mask[2 * i + 1])) for i in range(G)], scaled=[int(x) for x in sl],
+                loads=[int(x) for x in loads[:N]], overflow=[int(x) for x in ovf[:out.n_overflow]],
+                init=[int(x) for x in init[:g]], queue=[int(x) for x in queue[:out.queue_len]], K=out.K,
+                capacity=out.capacity, reserved_bytes=out.reserved_bytes)
+
+
+def is_group_advantages(rewards, mode="std_norm"):
+    L = load()
+    r = np.ascontiguousarray(rewards, np.float32)
+    a = np.zeros_like(r)
+    _check(L.is_group_advantages(_np_ptr(r), len(r), ADV_MODES[mode], _np_ptr(a)))
+    return a
+
+
+def is_dbg_gemm(w, x, y, split=1, stream=0):
+    """Y[rows][M] (fp32) = X[rows][K] . W[M][K]^T on the tcgen05 kernel (device tensors)."""
+    L = load()
+    M, K = w.shape
+    _check(L.is_dbg_gemm(w.data_ptr(), x.data_ptr(), y.data_ptr(), M, K, x.shape[0], split, stream))
+
+
+def weight_pointer_list(weights, layers):
+    from synth import GLOBAL_WEIGHT_NAMES, layer_weight_names
+    names = list(GLOBAL_WEIGHT_NAMES)
+    for l in range(layers):
+        names += layer_weight_names(l)
+    ptrs = []
+    for n in names:
+        t = weights[n]
+        if not t.is_cuda or not t.is_contiguous():
+            raise InfsampError(IS_ERR_DATA, f"weight {n} must be a contiguous CUDA tensor")
+        ptrs.append(t.data_ptr())
+    return ptrs
+
+
+class Context:
+    """Owning handle of an is_ctx (library-owned device state for one GPU)."""
+
+    def __init__(self, cfg, weights, stream=None):
+        import torch
+        L = load()
+        self.cfg = cfg
+        self.G = cfg.G
+        self.g = cfg.G if cfg.mode == MODES["full"] else cfg.g
+        ptrs = weight_pointer_list(weights, cfg.shape.layers)
+        arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        h = ctypes.c_void_p()
+        st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        self._stream = st
+        _check(L.is_create(ctypes.byref(cfg), arr, len(ptrs), ctypes.c_void_p(st), ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load().is_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def is_prefill(self, d_prompt, prompt_id):
+        _check(load().is_prefill(self._h, d_prompt.data_ptr(), int(prompt_id)))
+
+    def is_start_group(self, true_len, pred_len=None):
+        t = np.ascontiguousarray(true_len, np.int32)
+        p = None if pred_len is None else np.ascontiguousarray(pred_len, np.int32)
+        _check(load().is_start_group(self._h, _np_ptr(t), None if p is None else _np_ptr(p)))
+
+    def is_decode_step(self, d_next=None, d_fin=None):
+        _check(load().is_decode_step(self._h, None if d_next is None else d_next.data_ptr(),
+                                     None if d_fin is None else d_fin.data_ptr()))
+
+    def is_refill(self, d_fin=None, d_new_uid=None):
+        _check(load().is_refill(self._h, None if d_fin is None else d_fin.data_ptr(),
+                                None if d_new_uid is None else d_new_uid.data_ptr()))
+
+    def is_run_group(self, max_steps=1 << 30):
+        n = ctypes.c_int32()
+        _check(load().is_run_group(self._h, int(min(max_steps, 2 ** 31 - 1)), ctypes.byref(n)))
+        return n.value
+
+    def is_query(self):
+        s = Stats()
+        _check(load().is_query(self._h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def is_copy_tokens(self):
+        out = np.zeros((self.G, self.cfg.max_new_tokens), np.int32)
+        _check(load().is_copy_tokens(self._h, _np_ptr(out), 0))
+        return out
+
+    def is_copy_schedule(self, max_steps=None):
+        if max_steps is None:
+            max_steps = self.is_query()["steps"]
+        slots = np.zeros((max(max_steps, 1), self.g), np.int32)
+        live = np.zeros(max(max_steps, 1), np.int32)
+        n = ctypes.c_int32()
+        _check(load().is_copy_schedule(self._h, _np_ptr(slots), _np_ptr(live), max_steps, ctypes.byref(n)))
+        return slots[:n.value], live[:n.value]
+
+    def is_group_results(self, d_reward, d_len):
+        _check(load().is_group_results(self._h, d_reward.data_ptr(), d_len.data_ptr()))
+
+    def is_set_logits_dump(self, d_logits):
+        _check(load().is_set_logits_dump(self._h, None if d_logits is None else d_logits.data_ptr()))
+
+    def is_profile_step(self, cap=4096):
+        ms = np.zeros(cap, np.float32)
+        kind = np.zeros(cap, np.int32)
+        n = ctypes.c_int32()
+        _check(load().is_profile_step(self._h, _np_ptr(ms), _np_ptr(kind), cap, ctypes.byref(n)))
+        return ms[:n.value], kind[:n.value]

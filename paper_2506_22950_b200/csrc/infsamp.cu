@@ -1,0 +1,1087 @@
+// libinfsamp: C-ABI of the B200 continuous-sampling decode step (include/infsamp.h).
+//
+// Host side: the Alg. 2 planner, the Alg. 1 initial fill
+// and Alg. 3 static SJF refill order (l.218-241, l.280-295), the KV budget
+// check (R25), weight packing, the paged KV pool, and the
+// decode step orchestration, captured once into a CUDA graph with
+// programmatic dependent launch between kernels.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/infsamp.h"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+using namespace isk;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+static is_status fail(is_status s, const char* fmt, ...) {
+  static const char* names[] = {"IS_OK", "IS_ERR_CONFIG", "IS_ERR_BUDGET", "IS_ERR_CAPACITY",
+                                "IS_ERR_DATA", "IS_ERR_STATE", "IS_ERR_CUDA"};
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = std::string(names[s]) + ": " + buf;
+  return s;
+}
+#define CK(x)                                                                                     \
+  do {                                                                                            \
+    cudaError_t e_ = (x);                                                                         \
+    if (e_ != cudaSuccess) return fail(IS_ERR_CUDA, "%s at %s:%d (%s)", cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__, #x);                                   \
+  } while (0)
+#define CKS(x)                     \
+  do {                             \
+    is_status s_ = (x);            \
+    if (s_ != IS_OK) return s_;    \
+  } while (0)
+
+extern "C" const char* is_last_error(void) { return g_err.c_str(); }
+extern "C" const char* is_version(void) { return "infsamp 0.1 sm_100a"; }
+
+// ------------------------------------------------------------------ planner (host, pure)
+static int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+static int64_t kv_bytes_per_token(const is_shape& s) {
+  return 2ll * s.layers * s.n_kv_heads * s.head_dim * 2;
+}
+
+static is_status check_config(const is_config* c) {
+  const is_shape& s = c->shape;
+  if (s.head_dim != 128) return fail(IS_ERR_CONFIG, "head_dim must be 128 (got %d)", s.head_dim);
+  if (s.layers < 1 || s.hidden < 64 || s.hidden % 64 || s.ffn % 64 || s.vocab % 128 ||
+      s.n_q_heads < 1 || s.n_kv_heads < 1 || s.n_q_heads % s.n_kv_heads || s.n_q_heads / s.n_kv_heads > 8)
+    return fail(IS_ERR_CONFIG, "unsupported shape (hidden %% 64, ffn %% 64, vocab %% 128, Hq %% Hkv)");
+  if (c->G < 1) return fail(IS_ERR_CONFIG, "G must be >= 1");
+  const int g = c->mode == IS_MODE_FULL ? c->G : c->g;
+  if (g < 1 || g > c->G || c->G % g) return fail(IS_ERR_CONFIG, "need 1 <= g <= G and G mod g == 0 (G=%d g=%d)", c->G, g);
+  if (!(c->eps > 0)) return fail(IS_ERR_CONFIG, "eps must be > 0");
+  if (c->max_new_tokens < 1 || c->prompt_len < 2) return fail(IS_ERR_CONFIG, "max_new_tokens >= 1 and prompt_len >= 2");
+  if (c->page_tokens < 1) return fail(IS_ERR_CONFIG, "page_tokens must be >= 1");
+  if (c->prefix_k < 0 || (c->prefix_k > 0 && c->mode != IS_MODE_INFINITE))
+    return fail(IS_ERR_CONFIG, "prefix_k > 0 requires IS_MODE_INFINITE");
+  if (!(c->temperature > 0)) return fail(IS_ERR_CONFIG, "temperature must be > 0");
+  return IS_OK;
+}
+
+static int eff_g(const is_config* c) { return c->mode == IS_MODE_FULL ? c->G : c->g; }
+static int row_cap_of(const is_config* c) {
+  int rc = c->row_capacity > 0 ? c->row_capacity : ((eff_g(c) + 15) / 16) * 16;
+  return rc;
+}
+
+static int64_t reservation_bytes(const is_config* c) {
+  const int g = eff_g(c);
+  const int64_t pb = (int64_t)c->page_tokens * kv_bytes_per_token(c->shape);
+  const int64_t pre = (int64_t)(c->prompt_len - 1) * kv_bytes_per_token(c->shape);
+  const int64_t full = ceil_div64(c->max_new_tokens, c->page_tokens);
+  const int64_t park = c->prefix_k > 0 ? ceil_div64(c->prefix_k, c->page_tokens) : 0;
+  return pre + (int64_t)g * full * pb + (int64_t)(c->G - g) * park * pb;
+}
+
+extern "C" is_status is_plan(const is_config* cfg, const int32_t* pred, const uint8_t* finished,
+                             is_plan_out* out) {
+  if (!cfg || !out) return fail(IS_ERR_CONFIG, "null argument");
+  CKS(check_config(cfg));
+  const int G = cfg->G, g = eff_g(cfg), N = G / g;
+  out->K = 0;
+  out->capacity = 0;
+  out->n_overflow = 0;
+  out->reserved_bytes = reservation_bytes(cfg);
+  if (cfg->kv_budget_bytes > 0 && out->reserved_bytes > cfg->kv_budget_bytes)
+    return fail(IS_ERR_BUDGET, "worst-case KV reservation %lld B exceeds budget %lld B",
+                (long long)out->reserved_bytes, (long long)cfg->kv_budget_bytes);
+  if (cfg->mode != IS_MODE_INFINITE) {
+    if (out->mask) std::fill(out->mask, out->mask + 2 * G, 0);
+    if (out->scaled_len) std::fill(out->scaled_len, out->scaled_len + G, 0);
+    if (out->loads) std::fill(out->loads, out->loads + N, 0);
+    for (int i = 0; i < g; ++i) out->init_slots[i] = i;
+    out->queue_len = G - g;
+    for (int i = g; i < G; ++i) out->refill_queue[i - g] = i;
+    return IS_OK;
+  }
+  if (!pred) return fail(IS_ERR_DATA, "IS_MODE_INFINITE needs predicted lengths");
+  int64_t S = 0;
+  for (int i = 0; i < G; ++i) {
+    if (pred[i] < 1) return fail(IS_ERR_DATA, "predicted length of sample %d is %d (< 1)", i, pred[i]);
+    S += pred[i];
+  }
+  // Alg. 2: K = eps*S/N (IEEE double, this evaluation order, R14)
+  const double K = (cfg->eps * (double)S) / (double)N;
+  std::vector<int64_t> lt(G);
+  int64_t sum_lt = 0;
+  for (int i = 0; i < G; ++i) {
+    lt[i] = (int64_t)std::ceil((double)pred[i] / K);
+    sum_lt += lt[i];
+  }
+  const int64_t Ct = ceil_div64(sum_lt, N);
+  std::vector<int> order(G);
+  for (int i = 0; i < G; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return lt[a] > lt[b]; });  // ties -> lower id
+  std::vector<int64_t> load(N, 0);
+  std::vector<int> gsize(N, 0);
+  std::vector<int> gn(G), gj(G);
+  int nov = 0;
+  for (int i : order) {  // first fit
+    int target = -1;
+    for (int n = 0; n < N; ++n)
+      if (load[n] + lt[i] <= Ct) {
+        target = n;
+        break;
+      }
+    if (target < 0) {  // R15: least-loaded fallback, ties -> lowest index
+      target = 0;
+      for (int n = 1; n < N; ++n)
+        if (load[n] < load[target]) target = n;
+      if (out->overflow_ids) out->overflow_ids[nov] = i;
+      ++nov;
+    }
+    gn[i] = target;
+    gj[i] = gsize[target]++;
+    load[target] += lt[i];
+  }
+  out->K = K;
+  out->capacity = Ct;
+  out->n_overflow = nov;
+  for (int i = 0; i < G; ++i) {
+    if (out->mask) {
+      out->mask[2 * i] = gn[i] + 1;
+      out->mask[2 * i + 1] = gj[i];
+    }
+    if (out->scaled_len) out->scaled_len[i] = lt[i];
+  }
+  if (out->loads)
+    for (int n = 0; n < N; ++n) out->loads[n] = load[n];
+  // Alg. 1 l.230: first g samples from mask in lexicographic (n, j) order,
+  // skipping samples finished in the prefix phase (R13, R22).
+  std::vector<int> lex(G);
+  for (int i = 0; i < G; ++i) lex[i] = i;
+  std::sort(lex.begin(), lex.end(), [&](int a, int b) { return gn[a] != gn[b] ? gn[a] < gn[b] : gj[a] < gj[b]; });
+  std::vector<char> used(G, 0);
+  int ni = 0;
+  for (int i : lex) {
+    if (finished && finished[i]) continue;
+    if (ni < g) {
+      out->init_slots[ni++] = i;
+      used[i] = 1;
+    }
+  }
+  for (int s = ni; s < g; ++s) out->init_slots[s] = -1;
+  // Alg. 3 repeated: argmin pred over unstarted, unfinished, ties -> lower id (R17)
+  std::vector<int> rest;
+  for (int i = 0; i < G; ++i)
+    if (!used[i] && !(finished && finished[i])) rest.push_back(i);
+  std::stable_sort(rest.begin(), rest.end(), [&](int a, int b) { return pred[a] < pred[b]; });
+  out->queue_len = (int32_t)rest.size();
+  for (size_t i = 0; i < rest.size(); ++i) out->refill_queue[i] = rest[i];
+  return IS_OK;
+}
+
+extern "C" is_status is_group_advantages(const float* r, int32_t G, is_adv_mode mode, float* adv) {
+  if (!r || !adv || G < 1) return fail(IS_ERR_CONFIG, "bad arguments");
+  double s = 0;
+  for (int i = 0; i < G; ++i) s += (double)r[i];
+  const double mean = s / G;
+  if (mode == IS_ADV_MEAN_ONLY) {
+    for (int i = 0; i < G; ++i) adv[i] = (float)((double)r[i] - mean);
+    return IS_OK;
+  }
+  if (mode != IS_ADV_STD_NORM) return fail(IS_ERR_CONFIG, "unknown advantage mode");
+  double v = 0;
+  for (int i = 0; i < G; ++i) v += ((double)r[i] - mean) * ((double)r[i] - mean);
+  const double sigma = std::sqrt(v / G);
+  for (int i = 0; i < G; ++i) adv[i] = sigma == 0.0 ? 0.f : (float)(((double)r[i] - mean) / sigma);
+  return IS_OK;
+}
+
+// ------------------------------------------------------------------ TMA descriptors
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encodeTiled_t get_encode() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  }
+  return fn;
+}
+// bf16 row-major [rows][cols]; box = [box_rows][64] with 128-byte swizzle.
+static is_status make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int box_rows) {
+  PFN_encodeTiled_t enc = get_encode();
+  if (!enc) return fail(IS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(IS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return IS_OK;
+}
+
+// ------------------------------------------------------------------ GEMM launch
+static int g_num_sms = 0;
+static bool g_use_pdl = true;
+
+template <int BN, int EPI>
+static is_status launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB, GemmArgs a, cudaStream_t st) {
+  using C = GemmCfg<BN>;
+  static bool attr = false;
+  auto kern = gemm_swapab_kernel<BN, EPI>;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = st;
+  if (a.split > 1) {
+    cfg.gridDim = dim3(a.num_tiles * a.split);
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = a.split;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  } else {
+    int occ = 1;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGemmThreads, C::kSmem));
+    cfg.gridDim = dim3(std::min(a.num_tiles, std::max(1, occ) * g_num_sms));
+  }
+  if (g_use_pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  CK(cudaLaunchKernelEx(&cfg, kern, tA, tB, a));
+  return IS_OK;
+}
+
+template <int EPI>
+static is_status launch_gemm(int BN, const CUtensorMap& tA, const CUtensorMap& tB, GemmArgs a, cudaStream_t st) {
+  switch (BN) {
+    case 16: return launch_gemm_t<16, EPI>(tA, tB, a, st);
+    case 32: return launch_gemm_t<32, EPI>(tA, tB, a, st);
+    case 64: return launch_gemm_t<64, EPI>(tA, tB, a, st);
+  }
+  return fail(IS_ERR_CONFIG, "unsupported GEMM N tile %d", BN);
+}
+
+// Split-K so that tiles*split roughly fills the resident CTA slots (R: §DESIGN kernels).
+static int choose_split(int num_tiles, int kb_total, int BN) {
+  const int per_sm = BN == 64 ? 2 : 2;
+  const int slots = g_num_sms * per_sm;
+  if (num_tiles * 2 >= slots) return 1;
+  int s = slots / num_tiles;
+  s = std::min(s, 8);
+  s = std::min(s, kb_total);
+  return std::max(s, 1);
+}
+
+template <typename K, typename... Args>
+static is_status launch_k(K kern, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = st;
+  cfg.numAttrs = 0;
+  if (g_use_pdl) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  CK(cudaLaunchKernelEx(&cfg, kern, args...));
+  return IS_OK;
+}
+
+// ------------------------------------------------------------------ context
+struct LayerW {
+  __nv_bfloat16 *wqkv, *wo, *wgu, *wd;
+  float *in_norm, *post_norm, *q_norm, *k_norm;
+  CUtensorMap tm_qkv, tm_o, tm_gu, tm_d;
+};
+
+struct is_ctx {
+  is_config cfg;
+  is_shape sh;
+  int G, g, N, rc, BN, P, pcap, pt, maxp, max_new, num_pages, log_cap, max_rows, max_pos;
+  int qkv_w;  // (Hq + 2 Hkv) * 128
+  int64_t page_bytes, prefix_bytes;
+  cudaStream_t st, user;
+  cudaEvent_t ev_in, ev_out;
+  // weights
+  __nv_bfloat16* embed;
+  float* final_norm;
+  std::vector<LayerW> L;
+  CUtensorMap tm_embed;
+  void* wblob;
+  // KV
+  __nv_bfloat16* prefix;  // [L][2][Hkv][pcap][128]
+  __nv_bfloat16* pool;    // [L][pages][2][Hkv][pt][128]
+  // activations [max_rows]
+  float* resid;
+  __nv_bfloat16 *xn, *attn, *act, *q;
+  float* qkv;
+  float *part_o, *part_ml;
+  int NC, nc_pre, nc_suf;
+  CUtensorMap tm_xn_dec, tm_attn_dec, tm_act_dec, tm_xn_pre, tm_attn_pre, tm_act_pre;
+  float *rope_cos, *rope_sin;
+  // rows
+  int32_t *row_active, *row_uid, *row_lid, *row_t, *row_tok, *row_pos, *row_kvloc, *row_len;
+  unsigned long long* keys;
+  int32_t* last_tok;
+  uint8_t* last_fin;
+  // scheduler
+  long long* st_dev;
+  long long* st_host;  // pinned mirror
+  int32_t *slot_uid, *slot_count, *tpos, *true_len, *queue, *main_init, *main_queue, *free_stack, *pagetab,
+      *npages, *tokens, *log_slot, *log_live;
+  float* logits_dump;
+  int prompt_id, prompt_last;
+  bool prefilled, started;
+  cudaGraphExec_t graph;
+  bool graph_ok;
+  int32_t* d_prompt_copy;
+  // splits
+  int split_qkv, split_o, split_gu, split_d;
+};
+
+static void* dalloc(size_t bytes, is_status* s) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    *s = fail(IS_ERR_CUDA, "cudaMalloc(%zu) failed", bytes);
+    return nullptr;
+  }
+  cudaMemset(p, 0, bytes);
+  return p;
+}
+
+static SchedArgs sched_args(is_ctx* c) {
+  SchedArgs a;
+  a.G = c->G;
+  a.g = c->g;
+  a.row_cap = c->rc;
+  a.max_new = c->max_new;
+  a.pt = c->pt;
+  a.maxp = c->maxp;
+  a.P = c->P;
+  a.log_cap = c->log_cap;
+  a.prompt_id = c->prompt_id;
+  a.prompt_last = c->prompt_last;
+  a.st = c->st_dev;
+  a.slot_uid = c->slot_uid;
+  a.slot_count = c->slot_count;
+  a.t = c->tpos;
+  a.true_len = c->true_len;
+  a.queue = c->queue;
+  a.main_init = c->main_init;
+  a.main_queue = c->main_queue;
+  a.free_stack = c->free_stack;
+  a.pagetab = c->pagetab;
+  a.npages = c->npages;
+  a.tokens = c->tokens;
+  a.log_slot = c->log_slot;
+  a.log_live = c->log_live;
+  a.keys = c->keys;
+  a.last_tok = c->last_tok;
+  a.last_fin = c->last_fin;
+  a.row_active = c->row_active;
+  a.row_uid = c->row_uid;
+  a.row_lid = c->row_lid;
+  a.row_t = c->row_t;
+  a.row_tok = c->row_tok;
+  a.row_pos = c->row_pos;
+  a.row_kvloc = c->row_kvloc;
+  a.row_len = c->row_len;
+  return a;
+}
+
+// Launch recorder for is_profile_step.
+struct Prof {
+  std::vector<cudaEvent_t>* ev;
+  std::vector<int>* kind;
+};
+static Prof* g_prof = nullptr;
+static void prof_mark(cudaStream_t st, int kind) {
+  if (!g_prof) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, st);
+  g_prof->ev->push_back(e);
+  g_prof->kind->push_back(kind);
+}
+
+// One layer stack over `rows` rows starting at row 0 (decode: rows = rc, BN = c->BN;
+// prefill: rows = pcap processed in 64-row GEMM chunks).
+static is_status run_layers(is_ctx* c, int rows, bool prefill) {
+  cudaStream_t st = c->st;
+  const is_shape& s = c->sh;
+  const int H = s.hidden, F = s.ffn, Hq = s.n_q_heads, Hkv = s.n_kv_heads;
+  const int BN = prefill ? 64 : c->BN;
+  const CUtensorMap& tm_xn = prefill ? c->tm_xn_pre : c->tm_xn_dec;
+  const CUtensorMap& tm_attn = prefill ? c->tm_attn_pre : c->tm_attn_dec;
+  const CUtensorMap& tm_act = prefill ? c->tm_act_pre : c->tm_act_dec;
+  const int chunk = prefill ? 64 : rows;
+
+  prof_mark(st, 0);
+  CKS(launch_k(embed_kernel, dim3(rows), dim3(256), st, (const __nv_bfloat16*)c->embed,
+               (const int32_t*)c->row_tok, (const int32_t*)c->row_active, c->resid, H));
+  for (int l = 0; l < s.layers; ++l) {
+    LayerW& w = c->L[l];
+    CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.in_norm,
+                 c->xn, H, s.rms_eps));
+    prof_mark(st, 0);
+    for (int r0 = 0; r0 < rows; r0 += chunk) {
+      GemmArgs a{};
+      a.M = c->qkv_w;
+      a.K = H;
+      a.num_tiles = ceil_div64(a.M, kBM);
+      a.split = prefill ? choose_split(a.num_tiles, H / kBK, 64) : c->split_qkv;
+      a.row0 = r0;
+      a.n_valid = std::min(chunk, rows - r0);
+      a.out = c->qkv;
+      a.ld_out = c->qkv_w;
+      CKS(launch_gemm<EPI_STORE_F32>(BN, w.tm_qkv, tm_xn, a, st));
+    }
+    prof_mark(st, 1);
+    QkvPostArgs qa;
+    qa.qkv = c->qkv;
+    qa.q_gain = w.q_norm;
+    qa.k_gain = w.k_norm;
+    qa.rope_cos = c->rope_cos;
+    qa.rope_sin = c->rope_sin;
+    qa.row_active = c->row_active;
+    qa.row_pos = c->row_pos;
+    qa.row_kvloc = c->row_kvloc;
+    qa.q_out = c->q;
+    qa.Hq = Hq;
+    qa.Hkv = Hkv;
+    qa.pt = c->pt;
+    qa.pcap = c->pcap;
+    qa.prefill = prefill ? 1 : 0;
+    qa.eps = s.rms_eps;
+    const size_t prefix_layer = (size_t)2 * Hkv * c->pcap * kHD;
+    const size_t pool_layer = (size_t)c->num_pages * 2 * Hkv * c->pt * kHD;
+    qa.kv = prefill ? c->prefix + l * prefix_layer : c->pool + l * pool_layer;
+    CKS(launch_k(qkv_post_kernel, dim3(rows, Hq + 2 * Hkv), dim3(kHD), st, qa));
+    prof_mark(st, 2);
+    AttnArgs aa;
+    aa.q = c->q;
+    aa.kpre = c->prefix + l * prefix_layer;
+    aa.vpre = aa.kpre + (size_t)Hkv * c->pcap * kHD;
+    aa.pool = c->pool + l * pool_layer;
+    aa.pagetab = c->pagetab;
+    aa.row_active = c->row_active;
+    aa.row_lid = c->row_lid;
+    aa.row_len = c->row_len;
+    aa.part_o = c->part_o;
+    aa.part_ml = c->part_ml;
+    aa.rows = rows;
+    aa.Hq = Hq;
+    aa.Hkv = Hkv;
+    aa.pcap = c->pcap;
+    aa.plen = c->pcap;
+    aa.pt = c->pt;
+    aa.maxp = c->maxp;
+    aa.nc_pre = c->nc_pre;
+    aa.nc_suf = prefill ? 0 : c->nc_suf;
+    aa.NC = c->NC;
+    aa.prefill = prefill ? 1 : 0;
+    aa.scale = 1.0f / sqrtf((float)kHD);
+    const int nblk = Hkv * aa.nc_pre + (prefill ? 0 : rows * Hkv * aa.nc_suf);
+    CKS(launch_k(attn_partial_kernel, dim3(nblk), dim3(256), st, aa));
+    CKS(launch_k(attn_merge_kernel, dim3(rows, Hq), dim3(kHD), st, aa, c->attn));
+    prof_mark(st, 3);
+    for (int r0 = 0; r0 < rows; r0 += chunk) {
+      GemmArgs a{};
+      a.M = H;
+      a.K = Hq * kHD;
+      a.num_tiles = ceil_div64(a.M, kBM);
+      a.split = prefill ? choose_split(a.num_tiles, a.K / kBK, 64) : c->split_o;
+      a.row0 = r0;
+      a.n_valid = std::min(chunk, rows - r0);
+      a.out = c->resid;
+      a.ld_out = H;
+      CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_o, tm_attn, a, st));
+    }
+    prof_mark(st, 4);
+    CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.post_norm,
+                 c->xn, H, s.rms_eps));
+    prof_mark(st, 0);
+    for (int r0 = 0; r0 < rows; r0 += chunk) {
+      GemmArgs a{};
+      a.M = 2 * F;
+      a.K = H;
+      a.num_tiles = ceil_div64(a.M, kBM);
+      a.split = prefill ? choose_split(a.num_tiles, H / kBK, 64) : c->split_gu;
+      a.row0 = r0;
+      a.n_valid = std::min(chunk, rows - r0);
+      a.act = c->act;
+      a.ld_act = F;
+      CKS(launch_gemm<EPI_SWIGLU>(BN, w.tm_gu, tm_xn, a, st));
+    }
+    prof_mark(st, 5);
+    for (int r0 = 0; r0 < rows; r0 += chunk) {
+      GemmArgs a{};
+      a.M = H;
+      a.K = F;
+      a.num_tiles = ceil_div64(a.M, kBM);
+      a.split = prefill ? choose_split(a.num_tiles, F / kBK, 64) : c->split_d;
+      a.row0 = r0;
+      a.n_valid = std::min(chunk, rows - r0);
+      a.out = c->resid;
+      a.ld_out = H;
+      CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_d, tm_act, a, st));
+    }
+    prof_mark(st, 6);
+  }
+  return IS_OK;
+}
+
+static is_status enqueue_step(is_ctx* c) {
+  cudaStream_t st = c->st;
+  const is_shape& s = c->sh;
+  CKS(run_layers(c, c->rc, false));
+  CKS(launch_k(rmsnorm_kernel, dim3(c->rc), dim3(256), st, (const float*)c->resid, (const float*)c->final_norm,
+               c->xn, s.hidden, s.rms_eps));
+  prof_mark(st, 0);
+  GemmArgs a{};
+  a.M = s.vocab;
+  a.K = s.hidden;
+  a.num_tiles = ceil_div64(a.M, kBM);
+  a.split = 1;
+  a.row0 = 0;
+  a.n_valid = c->rc;
+  a.ld_out = s.vocab;
+  a.row_uid = c->row_uid;
+  a.row_t = c->row_t;
+  a.row_active = c->row_active;
+  a.keys = c->keys;
+  a.logits_dump = c->logits_dump;
+  a.seed = c->cfg.seed;
+  a.inv_temp = (float)(1.0 / (double)c->cfg.temperature);
+  CKS(launch_gemm<EPI_SAMPLE>(c->BN, c->tm_embed, c->tm_xn_dec, a, st));
+  prof_mark(st, 7);
+  CKS(launch_k(sched_kernel, dim3(1), dim3(32), st, sched_args(c), 1));
+  prof_mark(st, 8);
+  CK(cudaMemcpyAsync(c->st_host, c->st_dev, sizeof(long long) * ST_COUNT, cudaMemcpyDeviceToHost, st));
+  return IS_OK;
+}
+
+static is_status build_graph(is_ctx* c) {
+  if (c->graph_ok) {
+    cudaGraphExecDestroy(c->graph);
+    c->graph_ok = false;
+  }
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+  is_status s = enqueue_step(c);
+  cudaError_t e = cudaStreamEndCapture(c->st, &g);
+  if (s != IS_OK) return s;
+  CK(e);
+  CK(cudaGraphInstantiate(&c->graph, g, 0));
+  cudaGraphDestroy(g);
+  c->graph_ok = true;
+  return IS_OK;
+}
+
+// Order the context stream after the caller's stream and vice versa.
+struct StreamGuard {
+  is_ctx* c;
+  cudaStream_t user;
+  StreamGuard(is_ctx* c_, cudaStream_t u) : c(c_), user(u) {
+    cudaEventRecord(c->ev_in, user);
+    cudaStreamWaitEvent(c->st, c->ev_in, 0);
+  }
+  ~StreamGuard() {
+    cudaEventRecord(c->ev_out, c->st);
+    cudaStreamWaitEvent(user, c->ev_out, 0);
+  }
+};
+
+extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int32_t nw, void* stream,
+                               is_ctx** out) {
+  if (!cfg || !dw || !out) return fail(IS_ERR_CONFIG, "null argument");
+  CKS(check_config(cfg));
+  const is_shape& s = cfg->shape;
+  if (nw != 2 + 11 * s.layers) return fail(IS_ERR_CONFIG, "expected %d weight pointers, got %d", 2 + 11 * s.layers, nw);
+  if (!get_encode()) return fail(IS_ERR_CUDA, "no CUDA driver / TMA encoder available");
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10) return fail(IS_ERR_CUDA, "needs an sm_100 (B200) device, found sm_%d%d", prop.major, prop.minor);
+  g_num_sms = prop.multiProcessorCount;
+  if (getenv("IS_NO_PDL")) g_use_pdl = false;
+
+  is_ctx* c = new is_ctx{};
+  c->user = (cudaStream_t)stream;
+  c->cfg = *cfg;
+  c->sh = s;
+  c->G = cfg->G;
+  c->g = eff_g(cfg);
+  c->N = c->G / c->g;
+  c->rc = row_cap_of(cfg);
+  if (c->rc < c->g || c->rc > 64) {
+    delete c;
+    return fail(IS_ERR_CAPACITY, "row_capacity %d must be in [g=%d, 64]", c->rc, c->g);
+  }
+  c->BN = c->rc <= 16 ? 16 : (c->rc <= 32 ? 32 : 64);
+  c->P = cfg->prompt_len;
+  c->pcap = c->P - 1;
+  c->pt = cfg->page_tokens;
+  c->max_new = cfg->max_new_tokens;
+  c->maxp = (int)ceil_div64(c->max_new, c->pt);
+  c->qkv_w = (s.n_q_heads + 2 * s.n_kv_heads) * 128;
+  c->page_bytes = (int64_t)c->pt * kv_bytes_per_token(s);
+  c->prefix_bytes = (int64_t)c->pcap * kv_bytes_per_token(s);
+  const int64_t resv = reservation_bytes(cfg);
+  if (cfg->kv_budget_bytes > 0) {
+    if (resv > cfg->kv_budget_bytes) {
+      delete c;
+      return fail(IS_ERR_BUDGET, "worst-case KV reservation %lld B exceeds budget %lld B", (long long)resv,
+                  (long long)cfg->kv_budget_bytes);
+    }
+    c->num_pages = (int)((cfg->kv_budget_bytes - c->prefix_bytes) / c->page_bytes);
+  } else {
+    c->num_pages = (int)((resv - c->prefix_bytes) / c->page_bytes);
+  }
+  c->log_cap = c->G * c->max_new + c->N * cfg->prefix_k + 8;
+  c->max_rows = std::max(c->rc, (int)ceil_div64(c->pcap, 64) * 64);
+  c->max_pos = c->P + c->max_new + 1;
+  c->nc_pre = (int)ceil_div64(c->pcap, kChunk);
+  c->nc_suf = (int)ceil_div64(c->max_new, kChunk);
+  c->NC = c->nc_pre + c->nc_suf;
+  c->prompt_id = 0;
+
+  is_status err = IS_OK;
+  auto A = [&](size_t bytes) { return err == IS_OK ? dalloc(bytes, &err) : nullptr; };
+  CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
+  const int H = s.hidden, F = s.ffn, Hq = s.n_q_heads, Hkv = s.n_kv_heads, V = s.vocab;
+  // ---- weights (packed copies)
+  const size_t per_layer = (size_t)c->qkv_w * H + (size_t)H * Hq * 128 + (size_t)2 * F * H + (size_t)H * F;
+  c->wblob = A(((size_t)V * H + per_layer * s.layers) * 2);
+  if (err != IS_OK) return err;
+  __nv_bfloat16* wp = reinterpret_cast<__nv_bfloat16*>(c->wblob);
+  c->embed = wp;
+  wp += (size_t)V * H;
+  CK(cudaMemcpy(c->embed, dw[0], (size_t)V * H * 2, cudaMemcpyDeviceToDevice));
+  c->final_norm = (float*)A(H * 4);
+  if (err != IS_OK) return err;
+  bf16_to_f32_kernel<<<(H + 255) / 256, 256>>>((const __nv_bfloat16*)dw[1], c->final_norm, H);
+  c->L.resize(s.layers);
+  for (int l = 0; l < s.layers; ++l) {
+    const void* const* p = dw + 2 + 11 * l;
+    LayerW& w = c->L[l];
+    w.wqkv = wp;
+    wp += (size_t)c->qkv_w * H;
+    w.wo = wp;
+    wp += (size_t)H * Hq * 128;
+    w.wgu = wp;
+    wp += (size_t)2 * F * H;
+    w.wd = wp;
+    wp += (size_t)H * F;
+    const size_t qn = (size_t)Hq * 128 * H, kn = (size_t)Hkv * 128 * H;
+    CK(cudaMemcpy(w.wqkv, p[1], qn * 2, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(w.wqkv + qn, p[2], kn * 2, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(w.wqkv + qn + kn, p[3], kn * 2, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(w.wo, p[6], (size_t)H * Hq * 128 * 2, cudaMemcpyDeviceToDevice));
+    // gate|up interleaved per 64-row block: rows [128b, 128b+64) gate, [128b+64, 128b+128) up
+    const size_t blk = (size_t)64 * H * 2;
+    CK(cudaMemcpy2D(w.wgu, 2 * blk, p[8], blk, blk, F / 64, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy2D(reinterpret_cast<uint8_t*>(w.wgu) + blk, 2 * blk, p[9], blk, blk, F / 64,
+                    cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(w.wd, p[10], (size_t)H * F * 2, cudaMemcpyDeviceToDevice));
+    w.in_norm = (float*)A(H * 4);
+    w.post_norm = (float*)A(H * 4);
+    w.q_norm = (float*)A(128 * 4);
+    w.k_norm = (float*)A(128 * 4);
+    if (err != IS_OK) return err;
+    bf16_to_f32_kernel<<<(H + 255) / 256, 256>>>((const __nv_bfloat16*)p[0], w.in_norm, H);
+    bf16_to_f32_kernel<<<(H + 255) / 256, 256>>>((const __nv_bfloat16*)p[7], w.post_norm, H);
+    bf16_to_f32_kernel<<<1, 128>>>((const __nv_bfloat16*)p[4], w.q_norm, 128);
+    bf16_to_f32_kernel<<<1, 128>>>((const __nv_bfloat16*)p[5], w.k_norm, 128);
+    CKS(make_tmap(&w.tm_qkv, w.wqkv, c->qkv_w, H, kBM));
+    CKS(make_tmap(&w.tm_o, w.wo, H, Hq * 128, kBM));
+    CKS(make_tmap(&w.tm_gu, w.wgu, 2 * F, H, kBM));
+    CKS(make_tmap(&w.tm_d, w.wd, H, F, kBM));
+  }
+  CKS(make_tmap(&c->tm_embed, c->embed, V, H, kBM));
+  CK(cudaDeviceSynchronize());
+  // ---- KV
+  c->prefix = (__nv_bfloat16*)A((size_t)s.layers * 2 * Hkv * c->pcap * 128 * 2);
+  c->pool = (__nv_bfloat16*)A((size_t)s.layers * c->num_pages * (size_t)c->page_bytes / s.layers);
+  // ---- activations
+  const int R = c->max_rows;
+  c->resid = (float*)A((size_t)R * H * 4);
+  c->xn = (__nv_bfloat16*)A((size_t)R * H * 2);
+  c->attn = (__nv_bfloat16*)A((size_t)R * Hq * 128 * 2);
+  c->act = (__nv_bfloat16*)A((size_t)R * F * 2);
+  c->q = (__nv_bfloat16*)A((size_t)R * Hq * 128 * 2);
+  c->qkv = (float*)A((size_t)R * c->qkv_w * 4);
+  c->part_o = (float*)A((size_t)R * Hq * c->NC * 128 * 4);
+  c->part_ml = (float*)A((size_t)R * Hq * c->NC * 2 * 4);
+  c->rope_cos = (float*)A((size_t)c->max_pos * 64 * 4);
+  c->rope_sin = (float*)A((size_t)c->max_pos * 64 * 4);
+  for (int32_t** p : {&c->row_active, &c->row_uid, &c->row_lid, &c->row_t, &c->row_tok, &c->row_pos,
+                      &c->row_kvloc, &c->row_len})
+    *p = (int32_t*)A((size_t)R * 4);
+  c->keys = (unsigned long long*)A((size_t)R * 8);
+  c->last_tok = (int32_t*)A((size_t)R * 4);
+  c->last_fin = (uint8_t*)A((size_t)R);
+  c->st_dev = (long long*)A(sizeof(long long) * ST_COUNT);
+  c->slot_uid = (int32_t*)A(c->g * 4);
+  c->slot_count = (int32_t*)A(c->g * 4);
+  c->tpos = (int32_t*)A(c->G * 4);
+  c->true_len = (int32_t*)A(c->G * 4);
+  c->queue = (int32_t*)A(c->G * 4);
+  c->main_init = (int32_t*)A(c->g * 4);
+  c->main_queue = (int32_t*)A(c->G * 4);
+  c->free_stack = (int32_t*)A((size_t)std::max(c->num_pages, 1) * 4);
+  c->pagetab = (int32_t*)A((size_t)c->G * c->maxp * 4);
+  c->npages = (int32_t*)A(c->G * 4);
+  c->tokens = (int32_t*)A((size_t)c->G * c->max_new * 4);
+  c->log_slot = (int32_t*)A((size_t)c->log_cap * c->g * 4);
+  c->log_live = (int32_t*)A((size_t)c->log_cap * 4);
+  c->d_prompt_copy = (int32_t*)A((size_t)c->P * 4);
+  if (err != IS_OK) return err;
+  CK(cudaMallocHost(&c->st_host, sizeof(long long) * ST_COUNT));
+  memset(c->st_host, 0, sizeof(long long) * ST_COUNT);
+  // RoPE table (rotate-half, theta^(-2i/d)), fp64 -> fp32
+  {
+    std::vector<float> cs((size_t)c->max_pos * 64), sn((size_t)c->max_pos * 64);
+    for (int p = 0; p < c->max_pos; ++p)
+      for (int i = 0; i < 64; ++i) {
+        const double inv = std::pow((double)s.rope_theta, -2.0 * i / 128.0);
+        const double ang = (double)p * inv;
+        cs[(size_t)p * 64 + i] = (float)std::cos(ang);
+        sn[(size_t)p * 64 + i] = (float)std::sin(ang);
+      }
+    CK(cudaMemcpy(c->rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
+  }
+  CKS(make_tmap(&c->tm_xn_dec, c->xn, R, H, c->BN));
+  CKS(make_tmap(&c->tm_attn_dec, c->attn, R, Hq * 128, c->BN));
+  CKS(make_tmap(&c->tm_act_dec, c->act, R, F, c->BN));
+  CKS(make_tmap(&c->tm_xn_pre, c->xn, R, H, 64));
+  CKS(make_tmap(&c->tm_attn_pre, c->attn, R, Hq * 128, 64));
+  CKS(make_tmap(&c->tm_act_pre, c->act, R, F, 64));
+  c->split_qkv = choose_split((int)ceil_div64(c->qkv_w, kBM), H / kBK, c->BN);
+  c->split_o = choose_split((int)ceil_div64(H, kBM), Hq * 128 / kBK, c->BN);
+  c->split_gu = choose_split((int)ceil_div64(2 * F, kBM), H / kBK, c->BN);
+  c->split_d = choose_split((int)ceil_div64(H, kBM), F / kBK, c->BN);
+  if (const char* e = getenv("IS_SPLIT_OVERRIDE")) {
+    int v = atoi(e);
+    if (v >= 1 && v <= 8) c->split_qkv = c->split_o = c->split_gu = c->split_d = v;
+  }
+  CK(cudaDeviceSynchronize());
+  *out = c;
+  return IS_OK;
+}
+
+extern "C" void is_destroy(is_ctx* c) {
+  if (!c) return;
+  cudaStreamSynchronize(c->st);
+  if (c->graph_ok) cudaGraphExecDestroy(c->graph);
+  void* bufs[] = {c->wblob, c->final_norm, c->prefix, c->pool, c->resid, c->xn, c->attn, c->act, c->q, c->qkv,
+                  c->part_o, c->part_ml, c->rope_cos, c->rope_sin, c->row_active, c->row_uid, c->row_lid,
+                  c->row_t, c->row_tok, c->row_pos, c->row_kvloc, c->row_len, c->keys, c->last_tok,
+                  c->last_fin, c->st_dev, c->slot_uid, c->slot_count, c->tpos, c->true_len, c->queue,
+                  c->main_init, c->main_queue, c->free_stack, c->pagetab, c->npages, c->tokens, c->log_slot,
+                  c->log_live, c->d_prompt_copy};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  for (auto& w : c->L) {
+    cudaFree(w.in_norm);
+    cudaFree(w.post_norm);
+    cudaFree(w.q_norm);
+    cudaFree(w.k_norm);
+  }
+  if (c->st_host) cudaFreeHost(c->st_host);
+  cudaEventDestroy(c->ev_in);
+  cudaEventDestroy(c->ev_out);
+  cudaStreamDestroy(c->st);
+  delete c;
+}
+
+extern "C" is_status is_prefill(is_ctx* c, const int32_t* d_prompt, int32_t prompt_id) {
+  if (!c || !d_prompt) return fail(IS_ERR_CONFIG, "null argument");
+  StreamGuard guard(c, c->user);
+  c->prompt_id = prompt_id;
+  CK(cudaMemcpyAsync(c->d_prompt_copy, d_prompt, (size_t)c->P * 4, cudaMemcpyDeviceToDevice, c->st));
+  int32_t last = 0;
+  CK(cudaMemcpyAsync(&last, d_prompt + c->P - 1, 4, cudaMemcpyDeviceToHost, c->st));
+  CKS(launch_k(prefill_rows_kernel, dim3((c->pcap + 127) / 128), dim3(128), c->st, (const int32_t*)c->d_prompt_copy,
+               c->pcap, c->row_active, c->row_tok, c->row_pos, c->row_kvloc));
+  CKS(run_layers(c, c->pcap, true));
+  CK(cudaStreamSynchronize(c->st));
+  if (last < 0 || last >= c->sh.vocab) return fail(IS_ERR_DATA, "prompt token %d out of range", last);
+  c->prompt_last = last;
+  c->prefilled = true;
+  c->started = false;
+  return IS_OK;
+}
+
+extern "C" is_status is_start_group(is_ctx* c, const int32_t* true_len, const int32_t* pred) {
+  if (!c || !true_len) return fail(IS_ERR_CONFIG, "null argument");
+  if (!c->prefilled) return fail(IS_ERR_STATE, "is_start_group before is_prefill");
+  StreamGuard guard(c, c->user);
+  const int G = c->G, g = c->g;
+  for (int i = 0; i < G; ++i)
+    if (true_len[i] < 1 || true_len[i] > c->max_new)
+      return fail(IS_ERR_DATA, "true length of sample %d is %d (need 1..%d)", i, true_len[i], c->max_new);
+  const int k = c->cfg.prefix_k;
+  std::vector<int32_t> pred_eff(G), mask(2 * G), ovf(G), init(g), queue(G);
+  std::vector<int64_t> sl(G), loads(c->N);
+  std::vector<uint8_t> fin(G, 0);
+  for (int i = 0; i < G; ++i) {
+    pred_eff[i] = pred ? pred[i] : true_len[i];
+    if (k > 0 && true_len[i] <= k) {  // finished in the prefix phase: pred = true (R22)
+      fin[i] = 1;
+      pred_eff[i] = true_len[i];
+    }
+  }
+  is_plan_out po{};
+  po.mask = mask.data();
+  po.scaled_len = sl.data();
+  po.loads = loads.data();
+  po.overflow_ids = ovf.data();
+  po.init_slots = init.data();
+  po.refill_queue = queue.data();
+  CKS(is_plan(&c->cfg, pred_eff.data(), k > 0 ? fin.data() : nullptr, &po));
+  // device state
+  std::vector<long long> st(ST_COUNT, 0);
+  std::vector<int32_t> slots(g, -1), q0(G, 0);
+  if (k > 0) {  // prefix phase: barriered rounds in trace order, stop at k (R22)
+    st[ST_PHASE] = 0;
+    st[ST_BARRIER] = 1;
+    st[ST_QUOTA] = 0;
+    st[ST_STOPK] = k;
+    for (int s = 0; s < g; ++s) slots[s] = s;
+    for (int i = g; i < G; ++i) q0[i - g] = i;
+    st[ST_QLEN] = G - g;
+    st[ST_MAIN_PENDING] = 1;
+    st[ST_MAIN_QLEN] = po.queue_len;
+    int ni = 0;
+    while (ni < g && init[ni] >= 0) ++ni;
+    st[ST_MAIN_NINIT] = ni;
+  } else {
+    st[ST_PHASE] = 1;
+    st[ST_BARRIER] = (c->cfg.mode == IS_MODE_NAIVE || c->cfg.mode == IS_MODE_FULL) ? 1 : 0;
+    st[ST_QUOTA] = c->cfg.mode == IS_MODE_FIFO ? c->N : 0;
+    st[ST_STOPK] = 0;
+    for (int s = 0; s < g; ++s) slots[s] = init[s];
+    for (int i = 0; i < po.queue_len; ++i) q0[i] = queue[i];
+    st[ST_QLEN] = po.queue_len;
+  }
+  st[ST_FREE_TOP] = c->num_pages;
+  std::vector<int32_t> fs(std::max(c->num_pages, 1));
+  for (int i = 0; i < c->num_pages; ++i) fs[i] = c->num_pages - 1 - i;  // pop order 0, 1, 2, ...
+  CK(cudaMemcpyAsync(c->st_dev, st.data(), st.size() * 8, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->slot_uid, slots.data(), g * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemsetAsync(c->slot_count, 0, g * 4, c->st));
+  CK(cudaMemsetAsync(c->tpos, 0, G * 4, c->st));
+  CK(cudaMemcpyAsync(c->true_len, true_len, G * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->queue, q0.data(), G * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->main_init, init.data(), g * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->main_queue, queue.data(), G * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->free_stack, fs.data(), fs.size() * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemsetAsync(c->npages, 0, G * 4, c->st));
+  CK(cudaMemsetAsync(c->tokens, 0xFF, (size_t)G * c->max_new * 4, c->st));
+  CK(cudaMemsetAsync(c->log_slot, 0xFF, (size_t)c->log_cap * g * 4, c->st));
+  CK(cudaMemsetAsync(c->log_live, 0, (size_t)c->log_cap * 4, c->st));
+  CKS(launch_k(sched_kernel, dim3(1), dim3(32), c->st, sched_args(c), 0));
+  CK(cudaMemcpyAsync(c->st_host, c->st_dev, sizeof(long long) * ST_COUNT, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (!c->graph_ok) CKS(build_graph(c));
+  c->started = true;
+  return IS_OK;
+}
+
+extern "C" is_status is_decode_step(is_ctx* c, int32_t* d_next, uint8_t* d_fin) {
+  if (!c) return fail(IS_ERR_CONFIG, "null argument");
+  if (!c->started) return fail(IS_ERR_STATE, "is_decode_step before is_start_group");
+  StreamGuard guard(c, c->user);
+  if (getenv("IS_NO_GRAPH")) CKS(enqueue_step(c));
+  else CK(cudaGraphLaunch(c->graph, c->st));
+  if (d_next) CK(cudaMemcpyAsync(d_next, c->last_tok, c->rc * 4, cudaMemcpyDeviceToDevice, c->st));
+  if (d_fin) CK(cudaMemcpyAsync(d_fin, c->last_fin, c->rc, cudaMemcpyDeviceToDevice, c->st));
+  return IS_OK;
+}
+
+extern "C" is_status is_refill(is_ctx* c, uint8_t* d_fin, int32_t* d_new_uid) {
+  if (!c) return fail(IS_ERR_CONFIG, "null argument");
+  if (!c->started) return fail(IS_ERR_STATE, "is_refill before is_start_group");
+  StreamGuard guard(c, c->user);
+  CKS(launch_k(sched_kernel, dim3(1), dim3(32), c->st, sched_args(c), 1));
+  if (d_fin) CK(cudaMemcpyAsync(d_fin, c->last_fin, c->rc, cudaMemcpyDeviceToDevice, c->st));
+  if (d_new_uid) {
+    CK(cudaMemsetAsync(d_new_uid, 0xFF, c->rc * 4, c->st));
+    CK(cudaMemcpyAsync(d_new_uid, c->slot_uid, c->g * 4, cudaMemcpyDeviceToDevice, c->st));
+  }
+  return IS_OK;
+}
+
+extern "C" is_status is_run_group(is_ctx* c, int32_t max_steps, int32_t* h_steps) {
+  if (!c) return fail(IS_ERR_CONFIG, "null argument");
+  if (!c->started) return fail(IS_ERR_STATE, "is_run_group before is_start_group");
+  StreamGuard guard(c, c->user);
+  constexpr int D = 3;  // bounded host run-ahead
+  cudaEvent_t ev[D];
+  for (int i = 0; i < D; ++i) CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+  const bool nograph = getenv("IS_NO_GRAPH") != nullptr;
+  is_status rs = IS_OK;
+  for (int i = 0; i < max_steps; ++i) {
+    if (i >= D) {
+      cudaEventSynchronize(ev[i % D]);
+      const volatile long long* h = c->st_host;
+      if (h[ST_DONE] >= c->G) break;
+    }
+    if (nograph) rs = enqueue_step(c);
+    else if (cudaGraphLaunch(c->graph, c->st) != cudaSuccess) rs = fail(IS_ERR_CUDA, "graph launch failed");
+    if (rs != IS_OK) break;
+    cudaEventRecord(ev[i % D], c->st);
+  }
+  CK(cudaStreamSynchronize(c->st));
+  for (int i = 0; i < D; ++i) cudaEventDestroy(ev[i]);
+  if (rs != IS_OK) return rs;
+  if (h_steps) *h_steps = (int32_t)c->st_host[ST_STEP];
+  if (c->st_host[ST_DONE] < c->G) return fail(IS_ERR_CAPACITY, "group not finished after %d steps", max_steps);
+  return IS_OK;
+}
+
+extern "C" is_status is_query(is_ctx* c, is_stats* o) {
+  if (!c || !o) return fail(IS_ERR_CONFIG, "null argument");
+  CK(cudaStreamSynchronize(c->st));
+  long long st[ST_COUNT];
+  CK(cudaMemcpy(st, c->st_dev, sizeof st, cudaMemcpyDeviceToHost));
+  o->steps = (int32_t)st[ST_STEP];
+  o->prefix_steps = (int32_t)st[ST_PREFIX_STEPS];
+  o->completed = (int32_t)st[ST_DONE];
+  o->live_pages = (int32_t)st[ST_LIVE];
+  o->peak_pages = (int32_t)st[ST_PEAK];
+  o->error = (int32_t)st[ST_ERROR];
+  o->tokens_decoded = st[ST_TOKENS];
+  o->page_bytes = c->page_bytes;
+  o->prefix_bytes = c->prefix_bytes;
+  o->peak_kv_bytes = c->prefix_bytes + st[ST_PEAK] * c->page_bytes;
+  o->num_pages = c->num_pages;
+  o->row_capacity = c->rc;
+  return IS_OK;
+}
+
+extern "C" is_status is_copy_tokens(is_ctx* c, int32_t* dst, int32_t dev) {
+  if (!c || !dst) return fail(IS_ERR_CONFIG, "null argument");
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaMemcpy(dst, c->tokens, (size_t)c->G * c->max_new * 4, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+  return IS_OK;
+}
+
+extern "C" is_status is_copy_schedule(is_ctx* c, int32_t* h_slots, int32_t* h_live, int32_t max_steps, int32_t* h_n) {
+  if (!c) return fail(IS_ERR_CONFIG, "null argument");
+  CK(cudaStreamSynchronize(c->st));
+  long long st[ST_COUNT];
+  CK(cudaMemcpy(st, c->st_dev, sizeof st, cudaMemcpyDeviceToHost));
+  const int n = (int)std::min<long long>(std::min<long long>(st[ST_STEP], c->log_cap), max_steps);
+  if (h_slots) CK(cudaMemcpy(h_slots, c->log_slot, (size_t)n * c->g * 4, cudaMemcpyDeviceToHost));
+  if (h_live) CK(cudaMemcpy(h_live, c->log_live, (size_t)n * 4, cudaMemcpyDeviceToHost));
+  if (h_n) *h_n = n;
+  return IS_OK;
+}
+
+extern "C" is_status is_group_results(is_ctx* c, float* d_reward, int32_t* d_len) {
+  if (!c || !d_reward || !d_len) return fail(IS_ERR_CONFIG, "null argument");
+  StreamGuard guard(c, c->user);
+  results_kernel<<<(c->G + 127) / 128, 128, 0, c->st>>>(c->tokens, c->true_len, c->G, c->max_new, c->sh.vocab,
+                                                      d_reward, d_len);
+  CK(cudaGetLastError());
+  return IS_OK;
+}
+
+extern "C" is_status is_set_logits_dump(is_ctx* c, float* d_logits) {
+  if (!c) return fail(IS_ERR_CONFIG, "null argument");
+  c->logits_dump = d_logits;
+  if (c->started) CKS(build_graph(c));
+  return IS_OK;
+}
+
+extern "C" is_status is_profile_step(is_ctx* c, float* h_ms, int32_t* h_kind, int32_t cap, int32_t* h_n) {
+  if (!c) return fail(IS_ERR_CONFIG, "null argument");
+  if (!c->started) return fail(IS_ERR_STATE, "is_profile_step before is_start_group");
+  StreamGuard guard(c, c->user);
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> kind;
+  Prof p{&ev, &kind};
+  cudaEvent_t e0;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventRecord(e0, c->st));
+  g_prof = &p;
+  is_status s = enqueue_step(c);
+  g_prof = nullptr;
+  CK(cudaStreamSynchronize(c->st));
+  int n = 0;
+  cudaEvent_t prev = e0;
+  for (size_t i = 0; i < ev.size(); ++i) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, prev, ev[i]);
+    if (n < cap) {
+      h_ms[n] = ms;
+      h_kind[n] = kind[i];
+      ++n;
+    }
+    prev = ev[i];
+  }
+  for (auto e : ev) cudaEventDestroy(e);
+  cudaEventDestroy(e0);
+  if (h_n) *h_n = n;
+  return s;
+}
+
+extern "C" is_status is_dbg_gemm(const void* d_w, const void* d_x, float* d_y, int32_t M, int32_t K, int32_t rows,
+                                 int32_t split, void* stream) {
+  if (rows < 1 || rows > 64 || K % 64 || split < 1 || split > 8) return fail(IS_ERR_CONFIG, "bad dbg_gemm shape");
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  g_num_sms = prop.multiProcessorCount;
+  const int BN = rows <= 16 ? 16 : (rows <= 32 ? 32 : 64);
+  CUtensorMap tA, tB;
+  CKS(make_tmap(&tA, d_w, M, K, kBM));
+  CKS(make_tmap(&tB, d_x, rows, K, BN));
+  GemmArgs a{};
+  a.M = M;
+  a.K = K;
+  a.num_tiles = (M + kBM - 1) / kBM;
+  a.split = split;
+  a.row0 = 0;
+  a.n_valid = rows;
+  a.out = d_y;
+  a.ld_out = M;
+  CKS(launch_gemm<EPI_STORE_F32>(BN, tA, tB, a, (cudaStream_t)stream));
+  CK(cudaGetLastError());
+  return IS_OK;
+}

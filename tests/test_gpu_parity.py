@@ -1,0 +1,194 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Tolerances (BASELINE.json north_star; R31): schedules, slot tables,
+page counts and sampler decisions on identical logits are bit-exact;
+kernel-level fp32-accumulation differences on identical bf16 inputs <= 1e-4
+normwise; anything through bf16 storage (logits) <= 2e-2 normwise.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import model as M
+from oracle import sampler, simulator
+from oracle import kv as okv
+from synth import SHAPES, gen_prompt, gen_trace, gen_weights, predict_lengths
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2506_22950_b200 import _lib
+    _lib.load()
+    return _lib
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+
+
+@pytest.mark.parametrize("M_,K,rows,split", [(4096, 2048, 8, 4), (64, 64, 3, 1), (1000, 2048, 40, 1),
+                                             (1000, 2048, 40, 8), (12288, 2048, 64, 3), (2048, 6144, 16, 8),
+                                             (384, 512, 17, 2)])
+def test_gemm_tcgen05_vs_fp32_matmul(lib, M_, K, rows, split):
+    g = torch.Generator(device="cuda").manual_seed(M_ + K + rows)
+    w = (torch.randn(M_, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    x = torch.randn(rows, K, device="cuda", generator=g).to(torch.bfloat16)
+    y = torch.full((rows, M_), float("nan"), device="cuda")
+    lib.is_dbg_gemm(w, x, y, split=split)
+    torch.cuda.synchronize()
+    ref = (x.double() @ w.double().T).cpu().numpy()
+    got = y.cpu().numpy()
+    assert np.all(np.isfinite(got))
+    for r in range(rows):
+        assert _rel(got[r], ref[r]) < 1e-4, r
+
+
+# ---------------------------------------------------------------------------- tiny end to end
+TINY = SHAPES["tiny"]
+SEED = 20261017
+
+
+def _tiny_setup():
+    w = gen_weights(TINY, seed=SEED)
+    prompt = gen_prompt(TINY.vocab, 16, 0, seed=SEED)
+    true = gen_trace("tiny", 8, 32, 1)
+    pred = predict_lengths(true, "noisy", 0.3, seed=1)
+    return w, prompt, true, pred
+
+
+def _run(lib, w_dev, prompt, true, pred, mode, g, budget=0, prefix_k=0, pt=16, rc=16, logits=False):
+    cfg = lib.make_config(TINY, 8, g, 32, 16, mode=mode, prefix_k=prefix_k, page_tokens=pt, row_capacity=rc,
+                          kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED)
+    ctx = lib.Context(cfg, w_dev)
+    ctx.is_prefill(torch.as_tensor(prompt, device="cuda"), 0)
+    ctx.is_start_group(true, pred)
+    dumps = []
+    if logits:
+        buf = torch.zeros(rc, TINY.vocab, device="cuda")
+        ctx.is_set_logits_dump(buf)
+        slots_seen = []
+        while ctx.is_query()["completed"] < 8:
+            # rows of the step about to run
+            ctx.is_decode_step()
+            torch.cuda.synchronize()
+            dumps.append(buf.cpu().numpy().copy())
+        steps = ctx.is_query()["steps"]
+    else:
+        steps = ctx.is_run_group()
+    st = ctx.is_query()
+    slots, live = ctx.is_copy_schedule()
+    toks = ctx.is_copy_tokens()
+    ctx.close()
+    return dict(steps=steps, stats=st, slots=slots, live=live, tokens=toks, dumps=dumps)
+
+
+@pytest.fixture(scope="module")
+def tiny(lib):
+    w, prompt, true, pred = _tiny_setup()
+    w_dev = {k: v.cuda() for k, v in w.items()}
+    budget = okv.prefix_bytes(TINY, 16) + 4 * 2 * okv.page_bytes(TINY, 16)  # config 1: "KV budget 4 slots"
+    runs = {m: _run(lib, w_dev, prompt, true, pred, m, 2, budget=budget) for m in ("naive", "fifo", "infinite")}
+    runs["full"] = _run(lib, w_dev, prompt, true, pred, "full", 8)
+    return dict(w=w, w_dev=w_dev, prompt=prompt, true=true, pred=pred, runs=runs, budget=budget)
+
+
+@pytest.mark.parametrize("mode", ["naive", "fifo", "infinite", "full"])
+def test_tiny_schedule_bit_exact(tiny, mode):
+    r = tiny["runs"][mode]
+    ref = simulator.simulate(tiny["true"], mode, 2, pred=tiny["pred"], eps=0.1, page_tokens=16)
+    assert r["stats"]["completed"] == 8 and r["stats"]["error"] == 0
+    assert r["steps"] == ref.total_steps
+    assert r["slots"].tolist() == ref.slot_table
+    assert r["live"].tolist() == ref.live_pages
+    assert r["stats"]["peak_pages"] == ref.peak_pages
+    assert r["stats"]["tokens_decoded"] == int(np.sum(tiny["true"]))
+    assert r["stats"]["peak_kv_bytes"] == okv.peak_kv_bytes(TINY, 16, ref.peak_pages)
+    if mode != "full":
+        assert r["stats"]["peak_kv_bytes"] <= tiny["budget"]
+
+
+def test_tiny_token_streams_identical_across_modes(tiny):
+    """Batch invariance (R12 iv): a uid's tokens do not depend on the schedule."""
+    base = tiny["runs"]["infinite"]["tokens"]
+    for mode in ("naive", "fifo", "full"):
+        assert np.array_equal(tiny["runs"][mode]["tokens"], base), mode
+    for i, L in enumerate(tiny["true"]):
+        assert np.all(base[i, :L] >= 0) and np.all(base[i, :L] < TINY.vocab) and np.all(base[i, L:] == -1)
+
+
+def test_tiny_teacher_forced_tokens_and_logits(tiny):
+    toks = tiny["runs"]["infinite"]["tokens"]
+    mism, total = 0, 0
+    for i, L in enumerate(tiny["true"]):
+        gen = [int(x) for x in toks[i, :L]]
+        z = M.teacher_forced_logits(tiny["w"], TINY, tiny["prompt"], gen, mirror=True)
+        for t in range(L):
+            tok, margin = sampler.sample_margin(z[t].astype(np.float32), SEED, i, t)
+            total += 1
+            if tok != gen[t]:
+                mism += 1
+                assert margin < 0.05, (i, t, margin)
+    assert mism <= max(1, total // 100)
+
+
+def test_tiny_sampler_bit_exact_on_dumped_logits(lib, tiny):
+    r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "infinite", 2,
+             budget=tiny["budget"], logits=True)
+    toks = r["tokens"]
+    slots = r["slots"]
+    t_of = {}
+    for step, row in enumerate(slots):
+        dump = r["dumps"][step]
+        for s, uid in enumerate(row):
+            if uid < 0:
+                continue
+            t = t_of.get(uid, 0)
+            got = sampler.sample_token(dump[s], SEED, int(uid), t)
+            assert got == toks[uid, t], (step, s, uid, t)
+            # teacher-forced logits within the bf16 tolerance
+            if t == 0 or step % 5 == 0:
+                gen = [int(x) for x in toks[uid, :t + 1]]
+                z = M.teacher_forced_logits(tiny["w"], TINY, tiny["prompt"], gen, mirror=True, rows=[t])[0]
+                assert _rel(dump[s], z) < 2e-2
+            t_of[uid] = t + 1
+
+
+def test_tiny_budget_error_and_prefix_phase(lib, tiny):
+    with pytest.raises(lib.InfsampError) as e:
+        cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", prefix_k=4, page_tokens=16,
+                              kv_budget_bytes=tiny["budget"])
+        lib.Context(cfg, tiny["w_dev"])
+    assert e.value.status == lib.IS_ERR_BUDGET
+    pred = predict_lengths(tiny["true"], "noisy", 0.3, seed=1, prefix_k=4)
+    r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], pred, "infinite", 2, budget=tiny["budget"],
+             prefix_k=4, pt=4)
+    ref = simulator.simulate(tiny["true"], "infinite", 2, pred=pred, eps=0.1, prefix_k=4, page_tokens=4)
+    assert r["steps"] == ref.total_steps
+    assert r["slots"].tolist() == ref.slot_table
+    assert r["live"].tolist() == ref.live_pages
+    assert r["stats"]["prefix_steps"] == ref.prefix_steps
+    assert np.array_equal(r["tokens"], tiny["runs"]["infinite"]["tokens"])
+
+
+def test_tiny_rewards_and_advantages(lib, tiny):
+    from oracle import grpo
+    cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", kv_budget_bytes=tiny["budget"], seed=SEED)
+    ctx = lib.Context(cfg, tiny["w_dev"])
+    ctx.is_prefill(torch.as_tensor(tiny["prompt"], device="cuda"), 0)
+    ctx.is_start_group(tiny["true"], tiny["pred"])
+    ctx.is_run_group()
+    rew = torch.zeros(8, device="cuda")
+    ln = torch.zeros(8, dtype=torch.int32, device="cuda")
+    ctx.is_group_results(rew, ln)
+    toks = ctx.is_copy_tokens()
+    ctx.close()
+    ref = [grpo.bench_reward(toks[i, :L].tolist(), TINY.vocab) for i, L in enumerate(tiny["true"])]
+    assert np.allclose(rew.cpu().numpy(), ref, atol=1e-7)
+    assert ln.cpu().tolist() == [int(x) for x in tiny["true"]]
+    adv = lib.is_group_advantages(rew.cpu().numpy())
+    assert np.allclose(adv, grpo.advantages(ref), atol=1e-5)

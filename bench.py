@@ -1,0 +1,358 @@
+"""Benchmark: continuous-sampling rollouts of Infinite Sampling on B200.
+
+One bench *step* = one whole GRPO-group rollout through the C-ABI (BASELINE.json
+configs[2], the paper's headline setting): prefill of a 256-token prompt,
+Alg. 2 FPTAS plan, then continuous-sampling decode steps with SJF refill until
+all G = 32 completions (lengths from the MATH-shape trace, max 1024) are done,
+then rewards.  Metric: generated tokens/s per GPU (whole job = sum over ranks).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config N]
+
+Multi-GPU: one process per GPU (torchrun), prompts sharded by rank (weak
+scaling), one NCCL all-gather of (length, reward) per rollout for the
+group-normalised advantages (Eq. 2); time = max over ranks.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (shape, prompts-per-rank unused, G, g, max_new, P, family, prefix_k, budget)
+    3: dict(shape="qwen3-1.7b", G=32, g=8, max_new=1024, P=256, family="math", prefix_k=0,
+            desc="Qwen3-1.7B-shape random-init bf16, prompt 256, G=32, micro group 8, max 1024 new tokens, "
+                 "FPTAS+SJF plan on MATH-shape lengths"),
+    2: dict(shape="qwen3-0.6b", G=16, g=4, max_new=512, P=256, family="math8b", prefix_k=0,
+            desc="Qwen3-0.6B-shape, G=16, micro group 4, max 512"),
+    4: dict(shape="qwen3-1.7b", G=64, g=8, max_new=1024, P=256, family="longtail", prefix_k=16,
+            desc="Qwen3-1.7B-shape, G=64 under a 1 GiB KV budget, k=16 prefix phase, long-tail lengths"),
+    5: dict(shape="qwen3-4b", G=64, g=8, max_new=1024, P=256, family="math", prefix_k=0,
+            desc="Qwen3-4B-shape, G=64, micro group 8, prompts sharded by rank"),
+}
+SEED = 20261017
+METRIC = "generated tokens/s per GPU, G=32 Qwen3-1.7B-shape; HBM GB/s vs peak; peak KV GB"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        loaded = [x for x in sm if x > 500] or sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_bytes_per_step(shape, live_rows, suffix_tokens, P):
+    """weights once per step + prefix KV once per group + live suffix KV + appends."""
+    L, H, F, V = shape.layers, shape.hidden, shape.ffn, shape.vocab
+    per_layer_w = ((shape.q_dim + 2 * shape.kv_dim) * H + H * shape.q_dim + 2 * F * H + H * F) * 2
+    kv_tok = 2 * L * shape.n_kv_heads * shape.head_dim * 2
+    return L * per_layer_w + V * H * 2 + (P - 1) * kv_tok + suffix_tokens * kv_tok + live_rows * kv_tok
+
+
+def run_ours(args):
+    import torch
+    from paper_2506_22950_b200 import _lib
+    from synth import SHAPES, gen_prompt, gen_trace, gen_weights, predict_lengths
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    C = CONFIGS[args.config]
+    shape = SHAPES[C["shape"]]
+    G, g, max_new, P = C["G"], C["g"], C["max_new"], C["P"]
+    page_tokens = 16
+    kv_tok = 2 * shape.layers * shape.n_kv_heads * shape.head_dim * 2
+    budget = (P - 1) * kv_tok + g * math.ceil(max_new / page_tokens) * page_tokens * kv_tok
+    if C["prefix_k"]:
+        budget = 1 << 30
+    w = gen_weights(shape, seed=SEED, device="cuda")
+    cfg = _lib.make_config(shape, G, g, max_new, P, mode="infinite", prefix_k=C["prefix_k"],
+                           page_tokens=page_tokens, kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED)
+    ctx = _lib.Context(cfg, w)
+    del w
+    torch.cuda.empty_cache()
+    n_total = args.warmup + args.steps
+
+    def workload(i):
+        pid = rank * n_total + i               # global prompt id (RNG keyed by global uid)
+        prompt = gen_prompt(shape.vocab, P, pid, seed=SEED)
+        true = gen_trace(C["family"], G, max_new, SEED + pid)
+        pred = predict_lengths(true, "noisy", 0.3, seed=SEED + pid, prefix_k=C["prefix_k"])
+        return pid, prompt, true, pred
+
+    work = [workload(i) for i in range(n_total)]
+    d_prompts = [torch.as_tensor(p, device="cuda") for _, p, _, _ in work]
+    d_rew = torch.zeros(G, device="cuda")
+    d_len = torch.zeros(G, dtype=torch.int32, device="cuda")
+    all_len = torch.zeros(world * G, dtype=torch.int32, device="cuda")
+    all_rew = torch.zeros(world * G, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def rollout(i, host_inputs=False):
+        pid, prompt, true, pred = work[i]
+        if host_inputs:                      # e2e: host -> device copy of the step's input inside the timed region
+            dp = torch.from_numpy(prompt).pin_memory().to("cuda", non_blocking=True)
+        else:
+            dp = d_prompts[i]
+        ctx.is_prefill(dp, pid)
+        ctx.is_start_group(true, pred)       # Alg. 2 plan + budget check (host) + slot fill
+        steps = ctx.is_run_group()
+        ctx.is_group_results(d_rew, d_len)
+        if dist is not None:                 # the one exchange: lengths + rewards for Eq. 2
+            dist.all_gather_into_tensor(all_len, d_len)
+            dist.all_gather_into_tensor(all_rew, d_rew)
+        out = None
+        if host_inputs:                      # device -> host read of the step's result
+            out = (all_rew if dist is not None else d_rew).cpu()
+        return steps, out
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        rollout(i)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tokens, steps_total, peak_kv, live_rows_steps = 0, 0, 0, 0
+    e0.record(stream)
+    for i in range(args.warmup, n_total):
+        s, _ = rollout(i)
+        steps_total += s
+        tokens += int(np.sum(work[i][2]))
+    e1.record(stream)
+    barrier()
+    ms = e0.elapsed_time(e1)
+    st = ctx.is_query()
+    clk = clocks.stop()
+    # ---- e2e: same rollouts through the public API with host buffers
+    e2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    barrier()
+    e2[0].record(stream)
+    for i in range(args.warmup, n_total):
+        rollout(i, host_inputs=True)
+    e2[1].record(stream)
+    barrier()
+    ms_e2e = e2[0].elapsed_time(e2[1])
+    # ---- per-launch profile of one decode step (eager replay with events) for the roofline
+    pid, prompt, true, pred = work[0]
+    ctx.is_prefill(d_prompts[0], pid)
+    ctx.is_start_group(true, pred)
+    for _ in range(3):
+        ctx.is_decode_step()
+    prof = []
+    for _ in range(5):
+        msl, kind = ctx.is_profile_step()
+        prof.append(msl)
+    msl = np.median(np.stack(prof), axis=0)
+    stq = ctx.is_query()
+
+    t = torch.tensor([ms, ms_e2e, float(tokens)], device="cuda", dtype=torch.float64)
+    if dist is not None:
+        tt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(tt, t)
+        ms_max = max(float(x[0]) for x in tt)
+        e2e_max = max(float(x[1]) for x in tt)
+        tok_all = sum(float(x[2]) for x in tt)
+    else:
+        ms_max, e2e_max, tok_all = ms, ms_e2e, float(tokens)
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    hbm, tflops, peak_kind = peaks()
+    kinds = {0: "embed/norm", 1: "qkv_gemm", 2: "qkv_post", 3: "attention", 4: "o_proj", 5: "gate_up", 6: "down",
+             7: "lm_head_sampler", 8: "refill"}
+    per_kind = {kinds[k]: float(msl[kind == k].sum()) for k in kinds}
+    n_launch_kind = {kinds[k]: int((kind == k).sum()) for k in kinds}
+    step_ms = float(msl.sum())
+    H, F = shape.hidden, shape.ffn
+    gu_bytes = 2 * F * H * 2                          # algorithmic bytes per gate/up launch (weights)
+    gu_ms = per_kind["gate_up"] / max(n_launch_kind["gate_up"], 1)
+    achieved = gu_bytes / (gu_ms * 1e-3) / 1e9
+    launches_per_step = int(len(kind))
+    avg_steps = steps_total / args.steps
+    value = tok_all / (ms_max * 1e-3)
+    e2e_value = tok_all / (e2e_max * 1e-3)
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"config {args.config}: {C['desc']}", "model": C["shape"] + " (random init)",
+                   "G": G, "g": g, "prompt_len": P, "max_new_tokens": max_new, "length_family": C["family"],
+                   "kv_budget_bytes": budget, "global_batch": G * world, "seq_len": P + max_new,
+                   "parallelism": f"dp{world} (prompt-sharded)", "step": "one GRPO-group rollout",
+                   "l2": "inputs larger than L2 (3.4 GB of weights streamed per decode step)"},
+        "roofline": {"bound": "hbm", "kernel": "gate_up GEMM (tcgen05 swap-AB, SwiGLU epilogue)",
+                     "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                     "peak_kind": peak_kind, "bytes_per_launch": gu_bytes, "traffic": None,
+                     "step_ms_eager": round(step_ms, 4),
+                     "step_GBps": round(algorithmic_bytes_per_step(shape, g, 0, P) / (ms_max / max(steps_total, 1) * 1e-3) / 1e9, 1),
+                     "per_kind_ms": {k: round(v, 4) for k, v in per_kind.items()}},
+        "decode_steps_per_rollout": round(avg_steps, 1),
+        "ms_per_decode_step": round(ms_max / max(steps_total, 1), 4),
+        "peak_kv_bytes": st["peak_kv_bytes"],
+        "gpu_launches": int(launches_per_step * steps_total + 0),
+        "launches_per_decode_step": launches_per_step,
+        "e2e": {"value": round(e2e_value, 1), "unit": "tokens/s", "h2d_bytes_per_step": P * 4,
+                "d2h_bytes_per_step": G * world * 4},
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(C, budget_s=args.cpu_seconds)
+    print(json.dumps(line))
+    sys.stdout.flush()
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def _oracle_tokens_per_s(C, budget_s, step_seed=0):
+    """The oracle as it stands: full-recompute decode of one sample, tokens until ~budget_s."""
+    import torch
+    from oracle import model as M
+    from oracle import sampler
+    from synth import SHAPES, gen_prompt, gen_weights
+    shape = SHAPES[C["shape"]]
+    w = gen_weights(shape, seed=SEED, device="cuda" if torch.cuda.is_available() else "cpu")
+    w = {k: v.cpu() for k, v in w.items()}
+    prompt = [int(x) for x in gen_prompt(shape.vocab, C["P"], step_seed, seed=SEED)]
+    seq = list(prompt)
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        z = M.forward(w, shape, seq, mirror=True, logit_rows=[len(seq) - 1])[0]
+        tok = sampler.sample_token(z.astype(np.float32), SEED, step_seed * C["G"], n)
+        seq.append(tok)
+        n += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return n, dt
+
+
+def cpu_baseline(C, budget_s=20.0):
+    n, dt = _oracle_tokens_per_s(C, budget_s)
+    return {"value": round(n / dt, 5), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"oracle full-recompute fp64 decode of sample 0 of prompt 0 ({C['shape']}, prompt {C['P']}): "
+                      f"{n} tokens in {dt:.1f} s"}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    C = CONFIGS[args.config]
+    for i in range(args.warmup):
+        _oracle_tokens_per_s(C, 0.0, step_seed=i)
+    n_tot, t_tot = 0, 0.0
+    for i in range(args.steps):
+        n, dt = _oracle_tokens_per_s(C, 0.0, step_seed=args.warmup + i)
+        n_tot += n
+        t_tot += dt
+    v = n_tot / t_tot
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": "tokens/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_tot / args.steps * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config {args.config}: {C['desc']}", "step": "oracle decodes 1 token (full recompute)"},
+        "cpu_baseline": {"value": round(v, 5), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "oracle",
+                         "sample": f"{n_tot} tokens, 1 per step, full-recompute fp64 oracle on host cores"},
+        "e2e": {"value": round(v, 5), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -263,7 +263,7 @@ static is_status launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB, Gem
   } else {
     int occ = 1;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGemmThreads, C::kSmem));
-    cfg.gridDim = dim3(std::min(a.num_tiles, std::max(1, occ) * g_num_sms));
+    cfg.gridDim = dim3(std::min(a.num_tiles, g_num_sms));
   }
   if (g_use_pdl) {
     at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -286,12 +286,12 @@ static is_status launch_gemm(int BN, const CUtensorMap& tA, const CUtensorMap& t
   return fail(IS_ERR_CONFIG, "unsupported GEMM N tile %d", BN);
 }
 
-// Split-K so that tiles*split roughly fills the resident CTA slots (R: §DESIGN kernels).
-static int choose_split(int num_tiles, int kb_total, int BN) {
-  const int per_sm = BN == 64 ? 2 : 2;
-  const int slots = g_num_sms * per_sm;
-  if (num_tiles * 2 >= slots) return 1;
-  int s = slots / num_tiles;
+// Split-K so that tiles * split fills at most one CTA per SM: a GEMM never
+// takes more than half an SM, so the next kernel's CTAs (PDL) co-reside and
+// prefetch their weights while this one drains.
+static int choose_split(int num_tiles, int kb_total, int /*BN*/) {
+  if (num_tiles * 2 > g_num_sms) return 1;
+  int s = g_num_sms / num_tiles;
   s = std::min(s, 8);
   s = std::min(s, kb_total);
   return std::max(s, 1);

@@ -25,27 +25,42 @@ __global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const int32_t*
 
 // ------------------------------------------------------------------ RMSNorm
 // xn[r][k] = bf16(resid[r][k] / sqrt(mean(resid[r]^2) + eps) * gain[k])   (R12 r1)
+// One CTA per row; every thread issues all its float4 loads before reducing
+// (no serial load chain).  H % 4 == 0, H / 4 <= 4 * blockDim.
 __global__ void rmsnorm_kernel(const float* __restrict__ resid, const float* __restrict__ gain,
                                __nv_bfloat16* __restrict__ xn, int H, float eps) {
   pdl_wait();
   pdl_launch_dependents();
   const int r = blockIdx.x;
-  const float* x = resid + (size_t)r * H;
+  const float4* x4 = reinterpret_cast<const float4*>(resid + (size_t)r * H);
+  const float4* g4 = reinterpret_cast<const float4*>(gain);
+  const int n4 = H >> 2;
+  float4 xv[4], gv[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int i = threadIdx.x + j * blockDim.x;
+    xv[j] = i < n4 ? x4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    gv[j] = i < n4 ? g4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   float ss = 0.f;
-  for (int k = threadIdx.x; k < H; k += blockDim.x) ss += x[k] * x[k];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) ss += xv[j].x * xv[j].x + xv[j].y * xv[j].y + xv[j].z * xv[j].z + xv[j].w * xv[j].w;
   __shared__ float red[32];
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) red[0] = v;
+  float tot = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+  const float rs = 1.0f / sqrtf(tot / (float)H + eps);
+  __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(xn + (size_t)r * H);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int i = threadIdx.x + j * blockDim.x;
+    if (i < n4) {
+      o2[2 * i] = __floats2bfloat162_rn(xv[j].x * rs * gv[j].x, xv[j].y * rs * gv[j].y);
+      o2[2 * i + 1] = __floats2bfloat162_rn(xv[j].z * rs * gv[j].z, xv[j].w * rs * gv[j].w);
+    }
   }
-  __syncthreads();
-  const float rs = 1.0f / sqrtf(red[0] / (float)H + eps);
-  for (int k = threadIdx.x; k < H; k += blockDim.x)
-    xn[(size_t)r * H + k] = __float2bfloat16_rn(x[k] * rs * gain[k]);
 }
 
 // ------------------------------------------------------------------ QK-norm + RoPE + KV append

@@ -237,12 +237,25 @@ static is_status make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_
 // ------------------------------------------------------------------ GEMM launch
 static int g_num_sms = 0;
 static bool g_use_pdl = true;
+static int g_skip = 0;
+static unsigned long long* g_tl = nullptr;  // current timeline buffer during enqueue
+static int g_tl_n = 0;
+static const char* g_tl_name[512];  // debug: bit k skips kernel class k in the decode step (timing experiments only)
 
-template <int BN, int EPI>
+// Ring depth: split-K GEMMs stream few k-blocks per CTA (4 stages keep two CTAs
+// per SM so the next kernel can co-reside); persistent (split 1) GEMMs stream
+// long K ranges from fewer CTAs and need more bytes in flight per SM.
+template <int BN, bool DEEP>
+struct Stages {
+  static constexpr int v = !DEEP ? 4 : (BN == 16 ? 8 : (BN == 32 ? 6 : 4));
+};
+
+template <int BN, int EPI, bool DEEP>
 static is_status launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB, GemmArgs a, cudaStream_t st) {
-  using C = GemmCfg<BN>;
+  constexpr int STAGES = Stages<BN, DEEP>::v;
+  using C = GemmCfg<BN, STAGES>;
   static bool attr = false;
-  auto kern = gemm_swapab_kernel<BN, EPI>;
+  auto kern = gemm_swapab_kernel<BN, EPI, STAGES>;
   if (!attr) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr = true;
@@ -261,8 +274,6 @@ static is_status launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB, Gem
     at[na].val.clusterDim.z = 1;
     ++na;
   } else {
-    int occ = 1;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGemmThreads, C::kSmem));
     cfg.gridDim = dim3(std::min(a.num_tiles, g_num_sms));
   }
   if (g_use_pdl) {
@@ -272,16 +283,24 @@ static is_status launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB, Gem
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
+  if (g_tl && g_tl_n < 512 && !a.dbg_ts) {
+    a.dbg_ts = g_tl + (size_t)g_tl_n * 296 * 16;
+    g_tl_name[g_tl_n++] = EPI == EPI_QKV ? "qkv" : EPI == EPI_RESID_ADD ? "resid" : EPI == EPI_SWIGLU ? "gu" : EPI == EPI_SAMPLE ? "lm" : "f32";
+  }
   CK(cudaLaunchKernelEx(&cfg, kern, tA, tB, a));
   return IS_OK;
 }
 
 template <int EPI>
 static is_status launch_gemm(int BN, const CUtensorMap& tA, const CUtensorMap& tB, GemmArgs a, cudaStream_t st) {
-  switch (BN) {
-    case 16: return launch_gemm_t<16, EPI>(tA, tB, a, st);
-    case 32: return launch_gemm_t<32, EPI>(tA, tB, a, st);
-    case 64: return launch_gemm_t<64, EPI>(tA, tB, a, st);
+  const bool deep = a.split == 1;
+  switch (BN * 2 + (deep ? 1 : 0)) {
+    case 32: return launch_gemm_t<16, EPI, false>(tA, tB, a, st);
+    case 33: return launch_gemm_t<16, EPI, true>(tA, tB, a, st);
+    case 64: return launch_gemm_t<32, EPI, false>(tA, tB, a, st);
+    case 65: return launch_gemm_t<32, EPI, true>(tA, tB, a, st);
+    case 128: return launch_gemm_t<64, EPI, false>(tA, tB, a, st);
+    case 129: return launch_gemm_t<64, EPI, true>(tA, tB, a, st);
   }
   return fail(IS_ERR_CONFIG, "unsupported GEMM N tile %d", BN);
 }
@@ -295,6 +314,30 @@ static int choose_split(int num_tiles, int kb_total, int /*BN*/) {
   s = std::min(s, 8);
   s = std::min(s, kb_total);
   return std::max(s, 1);
+}
+
+template <typename K, typename... Args>
+static is_status launch_k_smem(K kern, dim3 grid, dim3 block, int smem, cudaStream_t st, Args... args) {
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.numAttrs = 0;
+  if (g_use_pdl) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  CK(cudaLaunchKernelEx(&cfg, kern, args...));
+  return IS_OK;
 }
 
 template <typename K, typename... Args>
@@ -342,8 +385,9 @@ struct is_ctx {
   // activations [max_rows]
   float* resid;
   __nv_bfloat16 *xn, *attn, *act, *q;
-  float* qkv;
   float *part_o, *part_ml;
+  int32_t* attn_cnt;
+  int32_t* attn_items;
   int NC, nc_pre, nc_suf;
   CUtensorMap tm_xn_dec, tm_attn_dec, tm_act_dec, tm_xn_pre, tm_attn_pre, tm_act_pre;
   float *rope_cos, *rope_sin;
@@ -365,6 +409,9 @@ struct is_ctx {
   int32_t* d_prompt_copy;
   // splits
   int split_qkv, split_o, split_gu, split_d;
+  int l2_prefetch;
+  unsigned long long* timeline;  // debug: [launch][148 CTAs][16] GEMM stamps (IS_TIMELINE)
+  int tl_count;
 };
 
 static void* dalloc(size_t bytes, is_status* s) {
@@ -414,6 +461,11 @@ static SchedArgs sched_args(is_ctx* c) {
   a.row_pos = c->row_pos;
   a.row_kvloc = c->row_kvloc;
   a.row_len = c->row_len;
+  a.attn_items = c->attn_items;
+  a.Hkv = c->sh.n_kv_heads;
+  a.nc_pre = c->nc_pre;
+  a.nc_suf = c->nc_suf;
+  a.chunk = kAC;
   return a;
 }
 
@@ -449,9 +501,11 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
                (const int32_t*)c->row_tok, (const int32_t*)c->row_active, c->resid, H));
   for (int l = 0; l < s.layers; ++l) {
     LayerW& w = c->L[l];
-    CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.in_norm,
+    if (prefill || !(g_skip & 1)) CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.in_norm,
                  c->xn, H, s.rms_eps));
     prof_mark(st, 0);
+    const size_t prefix_layer = (size_t)2 * Hkv * c->pcap * kHD;
+    const size_t pool_layer = (size_t)c->num_pages * 2 * Hkv * c->pt * kHD;
     for (int r0 = 0; r0 < rows; r0 += chunk) {
       GemmArgs a{};
       a.M = c->qkv_w;
@@ -460,32 +514,25 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
       a.split = prefill ? choose_split(a.num_tiles, H / kBK, 64) : c->split_qkv;
       a.row0 = r0;
       a.n_valid = std::min(chunk, rows - r0);
-      a.out = c->qkv;
-      a.ld_out = c->qkv_w;
-      CKS(launch_gemm<EPI_STORE_F32>(BN, w.tm_qkv, tm_xn, a, st));
+      QkvEpiArgs& e = a.qkv;
+      e.q_gain = w.q_norm;
+      e.k_gain = w.k_norm;
+      e.rope_cos = c->rope_cos;
+      e.rope_sin = c->rope_sin;
+      e.row_active = c->row_active;
+      e.row_pos = c->row_pos;
+      e.row_kvloc = c->row_kvloc;
+      e.q_out = c->q;
+      e.kv = prefill ? c->prefix + l * prefix_layer : c->pool + l * pool_layer;
+      e.Hq = Hq;
+      e.Hkv = Hkv;
+      e.pt = c->pt;
+      e.pcap = c->pcap;
+      e.prefill = prefill ? 1 : 0;
+      e.eps = s.rms_eps;
+      if (prefill || !(g_skip & 2)) CKS(launch_gemm<EPI_QKV>(BN, w.tm_qkv, tm_xn, a, st));
     }
     prof_mark(st, 1);
-    QkvPostArgs qa;
-    qa.qkv = c->qkv;
-    qa.q_gain = w.q_norm;
-    qa.k_gain = w.k_norm;
-    qa.rope_cos = c->rope_cos;
-    qa.rope_sin = c->rope_sin;
-    qa.row_active = c->row_active;
-    qa.row_pos = c->row_pos;
-    qa.row_kvloc = c->row_kvloc;
-    qa.q_out = c->q;
-    qa.Hq = Hq;
-    qa.Hkv = Hkv;
-    qa.pt = c->pt;
-    qa.pcap = c->pcap;
-    qa.prefill = prefill ? 1 : 0;
-    qa.eps = s.rms_eps;
-    const size_t prefix_layer = (size_t)2 * Hkv * c->pcap * kHD;
-    const size_t pool_layer = (size_t)c->num_pages * 2 * Hkv * c->pt * kHD;
-    qa.kv = prefill ? c->prefix + l * prefix_layer : c->pool + l * pool_layer;
-    CKS(launch_k(qkv_post_kernel, dim3(rows, Hq + 2 * Hkv), dim3(kHD), st, qa));
-    prof_mark(st, 2);
     AttnArgs aa;
     aa.q = c->q;
     aa.kpre = c->prefix + l * prefix_layer;
@@ -509,9 +556,27 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
     aa.NC = c->NC;
     aa.prefill = prefill ? 1 : 0;
     aa.scale = 1.0f / sqrtf((float)kHD);
-    const int nblk = Hkv * aa.nc_pre + (prefill ? 0 : rows * Hkv * aa.nc_suf);
-    CKS(launch_k(attn_partial_kernel, dim3(nblk), dim3(256), st, aa));
-    CKS(launch_k(attn_merge_kernel, dim3(rows, Hq), dim3(kHD), st, aa, c->attn));
+    aa.cnt = c->attn_cnt;
+    aa.out = c->attn;
+    aa.items = c->attn_items;
+    aa.n_pf = 0;
+    if (!prefill && c->l2_prefetch) {
+      aa.pf_ptr[0] = reinterpret_cast<const uint8_t*>(w.wo);
+      aa.pf_bytes[0] = (long long)H * Hq * 128 * 2;
+      aa.pf_ptr[1] = reinterpret_cast<const uint8_t*>(w.wgu);
+      aa.pf_bytes[1] = (long long)2 * F * H * 2;
+      aa.pf_ptr[2] = reinterpret_cast<const uint8_t*>(w.wd);
+      aa.pf_bytes[2] = (long long)H * F * 2;
+      aa.n_pf = c->l2_prefetch >= 2 ? 3 : 2;
+    }
+    aa.n_items = c->st_dev + ST_ATTN_ITEMS;
+    const int nblk = prefill ? Hkv * aa.nc_pre : 2 * g_num_sms;
+    switch (Hq / Hkv) {
+      case 1: if (prefill || !(g_skip & 8)) CKS(launch_k_smem(attn_kernel<1>, dim3(nblk), dim3(kAttnThreads), AttnSmem<1>::v, st, aa)); break;
+      case 2: if (prefill || !(g_skip & 8)) CKS(launch_k_smem(attn_kernel<2>, dim3(nblk), dim3(kAttnThreads), AttnSmem<2>::v, st, aa)); break;
+      case 4: if (prefill || !(g_skip & 8)) CKS(launch_k_smem(attn_kernel<4>, dim3(nblk), dim3(kAttnThreads), AttnSmem<4>::v, st, aa)); break;
+      default: if (prefill || !(g_skip & 8)) CKS(launch_k_smem(attn_kernel<8>, dim3(nblk), dim3(kAttnThreads), AttnSmem<8>::v, st, aa)); break;
+    }
     prof_mark(st, 3);
     for (int r0 = 0; r0 < rows; r0 += chunk) {
       GemmArgs a{};
@@ -523,10 +588,10 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
       a.n_valid = std::min(chunk, rows - r0);
       a.out = c->resid;
       a.ld_out = H;
-      CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_o, tm_attn, a, st));
+      if (prefill || !(g_skip & 16)) CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_o, tm_attn, a, st));
     }
     prof_mark(st, 4);
-    CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.post_norm,
+    if (prefill || !(g_skip & 1)) CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.post_norm,
                  c->xn, H, s.rms_eps));
     prof_mark(st, 0);
     for (int r0 = 0; r0 < rows; r0 += chunk) {
@@ -539,7 +604,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
       a.n_valid = std::min(chunk, rows - r0);
       a.act = c->act;
       a.ld_act = F;
-      CKS(launch_gemm<EPI_SWIGLU>(BN, w.tm_gu, tm_xn, a, st));
+      if (prefill || !(g_skip & 32)) CKS(launch_gemm<EPI_SWIGLU>(BN, w.tm_gu, tm_xn, a, st));
     }
     prof_mark(st, 5);
     for (int r0 = 0; r0 < rows; r0 += chunk) {
@@ -552,7 +617,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
       a.n_valid = std::min(chunk, rows - r0);
       a.out = c->resid;
       a.ld_out = H;
-      CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_d, tm_act, a, st));
+      if (prefill || !(g_skip & 64)) CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_d, tm_act, a, st));
     }
     prof_mark(st, 6);
   }
@@ -595,8 +660,16 @@ static is_status build_graph(is_ctx* c) {
     c->graph_ok = false;
   }
   cudaGraph_t g;
+  if (getenv("IS_TIMELINE") && !c->timeline) {
+    cudaMalloc(&c->timeline, (size_t)512 * 296 * 16 * 8);
+    cudaMemset(c->timeline, 0, (size_t)512 * 296 * 16 * 8);
+  }
+  g_tl = c->timeline;
+  g_tl_n = 0;
   CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
   is_status s = enqueue_step(c);
+  g_tl = nullptr;
+  c->tl_count = g_tl_n;
   cudaError_t e = cudaStreamEndCapture(c->st, &g);
   if (s != IS_OK) return s;
   CK(e);
@@ -634,6 +707,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   if (prop.major != 10) return fail(IS_ERR_CUDA, "needs an sm_100 (B200) device, found sm_%d%d", prop.major, prop.minor);
   g_num_sms = prop.multiProcessorCount;
   if (getenv("IS_NO_PDL")) g_use_pdl = false;
+  if (getenv("IS_SKIP")) g_skip = atoi(getenv("IS_SKIP"));
 
   is_ctx* c = new is_ctx{};
   c->user = (cudaStream_t)stream;
@@ -670,9 +744,14 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->log_cap = c->G * c->max_new + c->N * cfg->prefix_k + 8;
   c->max_rows = std::max(c->rc, (int)ceil_div64(c->pcap, 64) * 64);
   c->max_pos = c->P + c->max_new + 1;
-  c->nc_pre = (int)ceil_div64(c->pcap, kChunk);
-  c->nc_suf = (int)ceil_div64(c->max_new, kChunk);
+  c->nc_pre = (int)ceil_div64(c->pcap, kPC);
+  c->nc_suf = (int)ceil_div64(c->max_new, kAC);
   c->NC = c->nc_pre + c->nc_suf;
+  if (c->NC > 32 || s.n_q_heads / s.n_kv_heads > kMaxRep) {
+    const int nc = c->NC;
+    delete c;
+    return fail(IS_ERR_CAPACITY, "prompt_len + max_new_tokens too long for the attention merge (%d chunks > 32)", nc);
+  }
   c->prompt_id = 0;
 
   is_status err = IS_OK;
@@ -741,9 +820,10 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->attn = (__nv_bfloat16*)A((size_t)R * Hq * 128 * 2);
   c->act = (__nv_bfloat16*)A((size_t)R * F * 2);
   c->q = (__nv_bfloat16*)A((size_t)R * Hq * 128 * 2);
-  c->qkv = (float*)A((size_t)R * c->qkv_w * 4);
   c->part_o = (float*)A((size_t)R * Hq * c->NC * 128 * 4);
   c->part_ml = (float*)A((size_t)R * Hq * c->NC * 2 * 4);
+  c->attn_cnt = (int32_t*)A((size_t)R * Hkv * 4);
+  c->attn_items = (int32_t*)A((size_t)Hkv * (c->nc_pre + c->rc * c->nc_suf) * 4 + 64);
   c->rope_cos = (float*)A((size_t)c->max_pos * 64 * 4);
   c->rope_sin = (float*)A((size_t)c->max_pos * 64 * 4);
   for (int32_t** p : {&c->row_active, &c->row_uid, &c->row_lid, &c->row_t, &c->row_tok, &c->row_pos,
@@ -793,6 +873,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->split_o = choose_split((int)ceil_div64(H, kBM), Hq * 128 / kBK, c->BN);
   c->split_gu = choose_split((int)ceil_div64(2 * F, kBM), H / kBK, c->BN);
   c->split_d = choose_split((int)ceil_div64(H, kBM), F / kBK, c->BN);
+  c->l2_prefetch = getenv("IS_L2_PREFETCH") ? atoi(getenv("IS_L2_PREFETCH")) : 2;
   if (const char* e = getenv("IS_SPLIT_OVERRIDE")) {
     int v = atoi(e);
     if (v >= 1 && v <= 8) c->split_qkv = c->split_o = c->split_gu = c->split_d = v;
@@ -806,8 +887,8 @@ extern "C" void is_destroy(is_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->st);
   if (c->graph_ok) cudaGraphExecDestroy(c->graph);
-  void* bufs[] = {c->wblob, c->final_norm, c->prefix, c->pool, c->resid, c->xn, c->attn, c->act, c->q, c->qkv,
-                  c->part_o, c->part_ml, c->rope_cos, c->rope_sin, c->row_active, c->row_uid, c->row_lid,
+  void* bufs[] = {c->wblob, c->final_norm, c->prefix, c->pool, c->resid, c->xn, c->attn, c->act, c->q,
+                  c->part_o, c->part_ml, c->attn_cnt, c->attn_items, c->rope_cos, c->rope_sin, c->row_active, c->row_uid, c->row_lid,
                   c->row_t, c->row_tok, c->row_pos, c->row_kvloc, c->row_len, c->keys, c->last_tok,
                   c->last_fin, c->st_dev, c->slot_uid, c->slot_count, c->tpos, c->true_len, c->queue,
                   c->main_init, c->main_queue, c->free_stack, c->pagetab, c->npages, c->tokens, c->log_slot,
@@ -1081,7 +1162,37 @@ extern "C" is_status is_dbg_gemm(const void* d_w, const void* d_x, float* d_y, i
   a.n_valid = rows;
   a.out = d_y;
   a.ld_out = M;
+  a.dbg_ts = getenv("IS_GEMM_STAMPS") ? reinterpret_cast<unsigned long long*>(strtoull(getenv("IS_GEMM_STAMPS"), nullptr, 0)) : nullptr;
   CKS(launch_gemm<EPI_STORE_F32>(BN, tA, tB, a, (cudaStream_t)stream));
   CK(cudaGetLastError());
   return IS_OK;
+}
+
+// Debug: print the GEMM timeline of the last replayed step (IS_TIMELINE=1).
+extern "C" int is_dbg_timeline(is_ctx* c) {
+  if (!c || !c->timeline) return 0;
+  cudaStreamSynchronize(c->st);
+  std::vector<unsigned long long> h((size_t)c->tl_count * 296 * 16);
+  cudaMemcpy(h.data(), c->timeline, h.size() * 8, cudaMemcpyDeviceToHost);
+  unsigned long long t0 = ~0ull;
+  for (size_t i = 0; i < h.size(); i += 16)
+    if (h[i] && h[i] < t0) t0 = h[i];
+  for (int L = 0; L < c->tl_count; ++L) {
+    unsigned long long mn[16], mx[16];
+    for (int k = 0; k < 16; ++k) { mn[k] = ~0ull; mx[k] = 0; }
+    int n = 0;
+    for (int b = 0; b < 296; ++b) {
+      const unsigned long long* p = &h[((size_t)L * 296 + b) * 16];
+      if (!p[0]) continue;
+      ++n;
+      for (int k = 0; k < 16; ++k)
+        if (p[k]) { mn[k] = std::min(mn[k], p[k]); mx[k] = std::max(mx[k], p[k]); }
+    }
+    auto f = [&](unsigned long long v) { return v == ~0ull || v == 0 ? -1.0 : (double)(v - t0) / 1000.0; };
+    printf("%3d %-5s ctas=%3d start %7.2f..%7.2f pre %7.2f data0 %7.2f..%7.2f mma_done %7.2f..%7.2f cbar %7.2f pulled %7.2f epi %7.2f..%7.2f exit %7.2f..%7.2f\n", L,
+           g_tl_name[L], n, f(mn[0]), f(mx[0]), f(mx[2]), f(mn[3]), f(mx[3]), f(mn[5]), f(mx[5]), f(mx[6]), f(mx[7]),
+           f(mn[10]), f(mx[10]), f(mn[11]), f(mx[11]));
+  }
+  fflush(stdout);
+  return c->tl_count;
 }

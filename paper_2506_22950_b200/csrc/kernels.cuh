@@ -1,5 +1,4 @@
-// Non-GEMM kernels of the decode step: embedding, RMSNorm, QK-norm + RoPE +
-// KV append, split shared-prefix / per-slot-suffix attention with LSE merge,
+// Non-GEMM kernels of the decode step: embedding, RMSNorm, split shared-prefix / per-slot-suffix attention with LSE merge,
 // and the 1-CTA finish / refill / page-recycle scheduler.
 #pragma once
 #include "common.cuh"
@@ -7,15 +6,14 @@
 namespace isk {
 
 constexpr int kHD = 128;      // head_dim (all Qwen3 shapes, R1)
-constexpr int kChunk = 64;    // attention KV chunk (tokens per CTA)
 constexpr int kKPad = 136;    // smem row pitch (bf16) -> conflict-free 16-B row reads
 
 // ------------------------------------------------------------------ embed
 // resid[r][:] = E[tok[r]][:] (fp32 residual stream); idle rows get zeros.
 __global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ row_tok,
                              const int32_t* __restrict__ row_active, float* __restrict__ resid, int H) {
+  pdl_launch_dependents();  // let the next kernel launch and prefetch now; it waits for our completion itself
   pdl_wait();
-  pdl_launch_dependents();
   const int r = blockIdx.x;
   const bool act = row_active[r] != 0;
   const __nv_bfloat16* e = E + (size_t)(act ? row_tok[r] : 0) * H;
@@ -29,8 +27,8 @@ __global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const int32_t*
 // (no serial load chain).  H % 4 == 0, H / 4 <= 4 * blockDim.
 __global__ void rmsnorm_kernel(const float* __restrict__ resid, const float* __restrict__ gain,
                                __nv_bfloat16* __restrict__ xn, int H, float eps) {
+  pdl_launch_dependents();  // let the next kernel launch and prefetch now; it waits for our completion itself
   pdl_wait();
-  pdl_launch_dependents();
   const int r = blockIdx.x;
   const float4* x4 = reinterpret_cast<const float4*>(resid + (size_t)r * H);
   const float4* g4 = reinterpret_cast<const float4*>(gain);
@@ -63,66 +61,24 @@ __global__ void rmsnorm_kernel(const float* __restrict__ resid, const float* __r
   }
 }
 
-// ------------------------------------------------------------------ QK-norm + RoPE + KV append
-struct QkvPostArgs {
-  const float* qkv;        // [rows][(Hq + 2 Hkv) * 128] fp32 GEMM output
-  const float* q_gain;     // [128]
-  const float* k_gain;     // [128]
-  const float* rope_cos;   // [max_pos][64]
-  const float* rope_sin;
-  const int32_t* row_active;
-  const int32_t* row_pos;
-  const int32_t* row_kvloc;  // decode: page*pt + offset; prefill: prefix position
-  __nv_bfloat16* q_out;      // [rows][Hq][128]
-  __nv_bfloat16* kv;         // decode: layer page pool [pages][2][Hkv][pt][128]; prefill: prefix [2][Hkv][Pcap][128]
-  int Hq, Hkv, pt, pcap, prefill;
-  float eps;
-};
-
-// grid (rows, Hq + 2*Hkv), block 128 (one thread per head dim).
-__global__ void qkv_post_kernel(QkvPostArgs a) {
-  pdl_wait();
-  pdl_launch_dependents();
-  const int r = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
-  if (!a.row_active[r]) return;
-  const int W = (a.Hq + 2 * a.Hkv) * kHD;
-  float x = a.qkv[(size_t)r * W + h * kHD + d];
-  __shared__ float sh[kHD];
-  __shared__ float red[4];
-  const bool is_v = h >= a.Hq + a.Hkv;
-  if (!is_v) {
-    const bool is_q = h < a.Hq;
-    float ss = warp_sum(x * x);
-    if ((d & 31) == 0) red[d >> 5] = ss;
-    __syncthreads();
-    ss = red[0] + red[1] + red[2] + red[3];
-    const float rs = 1.0f / sqrtf(ss / (float)kHD + a.eps);
-    const float y = x * rs * (is_q ? a.q_gain[d] : a.k_gain[d]);
-    sh[d] = y;
-    __syncthreads();
-    const int pos = a.row_pos[r];
-    const int i = d & 63;
-    const float c = a.rope_cos[(size_t)pos * 64 + i], s = a.rope_sin[(size_t)pos * 64 + i];
-    x = d < 64 ? (y * c - sh[d + 64] * s) : (y * c + sh[d - 64] * s);
-    if (is_q) {
-      a.q_out[((size_t)r * a.Hq + h) * kHD + d] = __float2bfloat16_rn(x);
-      return;
-    }
-  }
-  const int kvsel = is_v ? 1 : 0;
-  const int hk = h - a.Hq - (is_v ? a.Hkv : 0);
-  const int loc = a.row_kvloc[r];
-  size_t off;
-  if (a.prefill) {
-    off = (((size_t)kvsel * a.Hkv + hk) * a.pcap + loc) * kHD + d;
-  } else {
-    const int page = loc / a.pt, o = loc % a.pt;
-    off = ((((size_t)page * 2 + kvsel) * a.Hkv + hk) * a.pt + o) * kHD + d;
-  }
-  a.kv[off] = __float2bfloat16_rn(x);
-}
-
 // ------------------------------------------------------------------ split attention
+// PAPER.md l.171-174 / l.205: every live slot attends to the prompt's shared
+// prefix KV (written once by prefill) and to its own paged response KV.  The
+// work is split at that boundary (R8):
+//   * prefix item  = (kv head, 128-token prefix chunk): the chunk is staged in
+//     shared memory ONCE and every live row of the group (x Hq/Hkv query heads)
+//     is scored against it -- the prefix is read once per group per step;
+//   * suffix item  = (row, kv head, 128-token chunk of that slot's pages): one
+//     warp, K rows read straight from the page pool (each lane owns 4 tokens,
+//     256-B contiguous rows), V read coalesced (lanes over head dims);
+// each item writes a normalised partial (o, m, l) per query head; the item that
+// completes a (row, kv head) -- a per-(row, head) arrival counter -- merges all
+// of its partials by log-sum-exp in fixed chunk order (prefix chunks, then
+// suffix chunks), so the result does not depend on arrival order.
+constexpr int kAC = 64;           // tokens per suffix chunk (one CTA)
+constexpr int kPC = 32;           // tokens per shared-prefix chunk (one CTA, all live rows)
+constexpr int kMaxRep = 8;        // Hq / Hkv <= 8
+
 struct AttnArgs {
   const __nv_bfloat16* q;     // [rows][Hq][128]
   const __nv_bfloat16* kpre;  // prefix K of this layer [Hkv][pcap][128]
@@ -132,162 +88,393 @@ struct AttnArgs {
   const int32_t* row_active;
   const int32_t* row_lid;     // local sample id (page table row)
   const int32_t* row_len;     // suffix tokens visible (t + 1)
-  float* part_o;              // [rows][Hq][NC][128] (normalised partial outputs)
-  float* part_ml;             // [rows][Hq][NC][2]  (max score, sum exp)
+  float* part_o;              // [rows][Hq][NC][128] normalised partial outputs
+  float* part_ml;             // [rows][Hq][NC][2]   (max score, sum exp)
+  int32_t* cnt;               // [rows][Hkv] arrival counters (left at 0)
+  const int32_t* items;       // decode work list (built by sched_kernel)
+  const uint8_t* pf_ptr[4];   // weights to pull into L2 while attention runs (latency-bound phase)
+  long long pf_bytes[4];
+  int n_pf;
+  const long long* n_items;   // its length
+  __nv_bfloat16* out;         // [rows][Hq][128]
   int rows, Hq, Hkv, pcap, plen, pt, maxp;
   int nc_pre, nc_suf, NC;
   int prefill;                // 1: rows are prompt positions, causal over the prefix, no suffix
   float scale;                // 1/sqrt(128)
 };
 
-// One CTA = one KV chunk of 64 tokens for one kv head, shared by every query
-// row that attends to it: the group's live rows x (Hq/Hkv) heads for a prefix
-// chunk (read once per group, not once per slot: P:205), or one slot's rows
-// for a suffix chunk.  Scores use lanes over tokens (16-B conflict-free smem
-// rows), P.V uses lanes over head dims.
-__global__ void __launch_bounds__(256) attn_partial_kernel(AttnArgs a) {
-  pdl_wait();
-  pdl_launch_dependents();
-  __shared__ __align__(16) __nv_bfloat16 Ks[kChunk][kKPad];
-  __shared__ __align__(16) __nv_bfloat16 Vs[kChunk][kKPad];
-  __shared__ __align__(16) float qs[8][kHD];
+__device__ __forceinline__ int attn_expected(const AttnArgs& a, int r) {
+  if (a.prefill) return min(a.nc_pre, r / kPC + 1);
+  return a.nc_pre + (a.row_len[r] + kAC - 1) / kAC;
+}
+
+// Warp-level LSE merge of all partials of (row r, kv head h) -> bf16 output.
+// Lane i holds partial i's (m, l) (<= 32 partials); the o loads are independent.
+__device__ void attn_merge_warp(const AttnArgs& a, int r, int h, int lane) {
   const int rep = a.Hq / a.Hkv;
-  int b = blockIdx.x;
-  const bool is_pre = b < a.Hkv * a.nc_pre;
-  int h, c, r_only = -1, tok0, ntok;
-  if (is_pre) {
-    h = b / a.nc_pre;
-    c = b % a.nc_pre;
-    tok0 = c * kChunk;
-    ntok = min(kChunk, a.plen - tok0);
-  } else {
-    b -= a.Hkv * a.nc_pre;
-    c = b % a.nc_suf;
-    b /= a.nc_suf;
-    h = b % a.Hkv;
-    r_only = b / a.Hkv;
-    if (r_only >= a.rows || !a.row_active[r_only]) return;
-    tok0 = c * kChunk;
-    ntok = min(kChunk, a.row_len[r_only] - tok0);
-    if (ntok <= 0) return;
-  }
-  // ---- stage K/V chunk in smem (each thread copies 16-B pieces)
-  for (int i = threadIdx.x; i < kChunk * (kHD / 8); i += blockDim.x) {
-    const int tk = i / (kHD / 8), seg = i % (kHD / 8);
-    uint4 kk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-    if (tk < ntok) {
-      const int tok = tok0 + tk;
-      const __nv_bfloat16 *kp, *vp;
-      if (is_pre) {
-        kp = a.kpre + ((size_t)h * a.pcap + tok) * kHD;
-        vp = a.vpre + ((size_t)h * a.pcap + tok) * kHD;
-      } else {
-        const int page = a.pagetab[(size_t)a.row_lid[r_only] * a.maxp + tok / a.pt];
-        const size_t base = (((size_t)page * 2) * a.Hkv + h) * a.pt + (tok % a.pt);
-        kp = a.pool + base * kHD;
-        vp = a.pool + (base + (size_t)a.Hkv * a.pt) * kHD;
+  const int npre = a.prefill ? min(a.nc_pre, r / kPC + 1) : a.nc_pre;
+  const int nsuf = a.prefill ? 0 : (a.row_len[r] + kAC - 1) / kAC;
+  const int n = npre + nsuf;
+  const int my_slot = lane < npre ? lane : a.nc_pre + (lane - npre);
+  for (int j = 0; j < rep; ++j) {
+    const int qh = h * rep + j;
+    const size_t base = ((size_t)r * a.Hq + qh) * a.NC;
+    float mi = -INFINITY, li = 0.f;
+    if (lane < n) {
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (base + my_slot) * 2));
+      mi = ml.x;
+      li = ml.y;
+    }
+    const float M = warp_max(mi);
+    const float wi = (lane < n && mi != -INFINITY) ? expf(mi - M) * li : 0.f;
+    const float den = warp_sum(wi);
+    float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int i = 0; i < n; ++i) {
+      const float w = __shfl_sync(0xffffffffu, wi, i);
+      const int slot = i < npre ? i : a.nc_pre + (i - npre);
+      if (w != 0.f) {
+        const float4 o = __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + slot) * kHD) + lane);
+        num.x += w * o.x;
+        num.y += w * o.y;
+        num.z += w * o.z;
+        num.w += w * o.w;
       }
-      kk = *reinterpret_cast<const uint4*>(kp + seg * 8);
-      vv = *reinterpret_cast<const uint4*>(vp + seg * 8);
     }
-    *reinterpret_cast<uint4*>(&Ks[tk][seg * 8]) = kk;
-    *reinterpret_cast<uint4*>(&Vs[tk][seg * 8]) = vv;
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int nrows = is_pre ? a.rows : 1;
-  const int nitems = nrows * rep;
-  for (int it = warp; it < nitems; it += nw) {
-    const int r = is_pre ? it / rep : r_only;
-    const int qh = h * rep + (it % rep);
-    if (!a.row_active[r]) continue;
-    int valid = ntok;
-    if (is_pre && a.prefill) valid = min(ntok, r + 1 - tok0);  // causal over the prompt
-    const size_t pidx = ((size_t)r * a.Hq + qh) * a.NC + (is_pre ? c : a.nc_pre + c);
-    if (valid <= 0) {
-      if (lane == 0) {
-        a.part_ml[pidx * 2] = -INFINITY;
-        a.part_ml[pidx * 2 + 1] = 0.f;
-      }
-      continue;
-    }
-    // q row -> smem (fp32), broadcast reads below
-    const __nv_bfloat16* qp = a.q + ((size_t)r * a.Hq + qh) * kHD;
-    for (int d = lane; d < kHD; d += 32) qs[warp][d] = __bfloat162float(qp[d]);
-    __syncwarp();
-    float s[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int tk = lane + 32 * j;
-      float acc = 0.f;
-#pragma unroll
-      for (int d = 0; d < kHD; d += 8) {
-        const uint4 kv4 = *reinterpret_cast<const uint4*>(&Ks[tk][d]);
-        const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kv4);
-        const float4 qa = *reinterpret_cast<const float4*>(&qs[warp][d]);
-        const float4 qb = *reinterpret_cast<const float4*>(&qs[warp][d + 4]);
-        float2 f0 = __bfloat1622float2(k2[0]), f1 = __bfloat1622float2(k2[1]);
-        float2 f2 = __bfloat1622float2(k2[2]), f3 = __bfloat1622float2(k2[3]);
-        acc += qa.x * f0.x + qa.y * f0.y + qa.z * f1.x + qa.w * f1.y;
-        acc += qb.x * f2.x + qb.y * f2.y + qb.z * f3.x + qb.w * f3.y;
-      }
-      s[j] = tk < valid ? acc * a.scale : -INFINITY;
-    }
-    const float m = warp_max(fmaxf(s[0], s[1]));
-    const float p0 = s[0] == -INFINITY ? 0.f : expf(s[0] - m);
-    const float p1 = s[1] == -INFINITY ? 0.f : expf(s[1] - m);
-    const float l = warp_sum(p0 + p1);
-    float o[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int tk = 0; tk < valid; ++tk) {
-      const float p = __shfl_sync(0xffffffffu, tk < 32 ? p0 : p1, tk & 31);
-      const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&Vs[tk][lane * 4]);
-      const float2 a0 = __bfloat1622float2(v2[0]), a1 = __bfloat1622float2(v2[1]);
-      o[0] += p * a0.x;
-      o[1] += p * a0.y;
-      o[2] += p * a1.x;
-      o[3] += p * a1.y;
-    }
-    const float inv = 1.0f / l;
-    float4 ov = make_float4(o[0] * inv, o[1] * inv, o[2] * inv, o[3] * inv);
-    *reinterpret_cast<float4*>(a.part_o + pidx * kHD + lane * 4) = ov;
-    if (lane == 0) {
-      a.part_ml[pidx * 2] = m;
-      a.part_ml[pidx * 2 + 1] = l;
-    }
-    __syncwarp();
+    const float inv = 1.0f / den;
+    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(a.out + ((size_t)r * a.Hq + qh) * kHD) + 2 * lane;
+    o2[0] = __floats2bfloat162_rn(num.x * inv, num.y * inv);
+    o2[1] = __floats2bfloat162_rn(num.z * inv, num.w * inv);
   }
 }
 
-// LSE merge (R8): o = sum_i w_i o_i / sum_i w_i, w_i = exp(m_i - max m) * l_i,
-// over prefix chunks then suffix chunks in fixed order.  grid (rows, Hq), block 128.
-__global__ void attn_merge_kernel(AttnArgs a, __nv_bfloat16* __restrict__ out) {
-  pdl_wait();
-  pdl_launch_dependents();
-  const int r = blockIdx.x, qh = blockIdx.y, d = threadIdx.x;
-  __nv_bfloat16* o = out + ((size_t)r * a.Hq + qh) * kHD + d;
-  if (!a.row_active[r]) {
-    *o = __float2bfloat16_rn(0.f);
+// Signal one more partial for (r, h); the completing warp merges.  Called by one full warp.
+__device__ __forceinline__ void attn_arrive(const AttnArgs& a, int r, int h, int lane) {
+  __threadfence();
+  int old = 0;
+  if (lane == 0) old = atomicAdd(a.cnt + r * a.Hkv + h, 1);
+  old = __shfl_sync(0xffffffffu, old, 0);
+  if (old == attn_expected(a, r) - 1) {
+    __threadfence();
+    attn_merge_warp(a, r, h, lane);
+    if (lane == 0) a.cnt[r * a.Hkv + h] = 0;
+  }
+}
+
+// Scores + softmax + P.V of one (row, kv head) against ntok tokens.  kp(tok)
+// returns a pointer to K row tok (128 bf16), vp(tok) to V row tok.  Writes the
+// partial of query heads h*REP .. h*REP+REP-1 into chunk slot `slot`.
+// REP = Hq/Hkv is a template parameter and loops are only lightly unrolled:
+// the code must stay small (the attention kernel runs cold out of the
+// instruction cache once per layer).
+template <int REP, typename KP, typename VP>
+__device__ __forceinline__ void attn_rows_chunk(const AttnArgs& a, int r, int h, int slot, int ntok, const float* qs,
+                                                KP kp, VP vp, int lane) {
+  float s[4][REP];
+#pragma unroll 1
+  for (int j = 0; j < 4; ++j) {
+    const int tk = lane + 32 * j;
+    float acc[REP];
+#pragma unroll
+    for (int e = 0; e < REP; ++e) acc[e] = 0.f;
+    if (tk < ntok) {
+      const uint4* k4 = reinterpret_cast<const uint4*>(kp(tk));
+#pragma unroll 2
+      for (int d8 = 0; d8 < kHD / 8; ++d8) {
+        const uint4 kv = k4[d8];
+        const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kv);
+        const float2 f0 = __bfloat1622float2(k2[0]), f1 = __bfloat1622float2(k2[1]);
+        const float2 f2 = __bfloat1622float2(k2[2]), f3 = __bfloat1622float2(k2[3]);
+#pragma unroll
+        for (int e = 0; e < REP; ++e) {
+          const float4 qa = *reinterpret_cast<const float4*>(qs + e * kHD + d8 * 8);
+          const float4 qb = *reinterpret_cast<const float4*>(qs + e * kHD + d8 * 8 + 4);
+          acc[e] += qa.x * f0.x + qa.y * f0.y + qa.z * f1.x + qa.w * f1.y + qb.x * f2.x + qb.y * f2.y +
+                    qb.z * f3.x + qb.w * f3.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < REP; ++e) {
+      const float v = tk < ntok ? acc[e] * a.scale : -INFINITY;
+      if (j == 0) s[0][e] = v;
+      else if (j == 1) s[1][e] = v;
+      else if (j == 2) s[2][e] = v;
+      else s[3][e] = v;
+    }
+  }
+  float m[REP], l[REP];
+#pragma unroll
+  for (int e = 0; e < REP; ++e) {
+    m[e] = warp_max(fmaxf(fmaxf(s[0][e], s[1][e]), fmaxf(s[2][e], s[3][e])));
+    float ps = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      s[j][e] = s[j][e] == -INFINITY ? 0.f : expf(s[j][e] - m[e]);
+      ps += s[j][e];
+    }
+    l[e] = warp_sum(ps);
+  }
+  float o[REP][4];
+#pragma unroll
+  for (int e = 0; e < REP; ++e) o[e][0] = o[e][1] = o[e][2] = o[e][3] = 0.f;
+#pragma unroll 1
+  for (int j = 0; j < 4; ++j) {
+    const int t0 = 32 * j;
+    if (t0 >= ntok) break;
+    float pj[REP];
+#pragma unroll
+    for (int e = 0; e < REP; ++e) pj[e] = j == 0 ? s[0][e] : j == 1 ? s[1][e] : j == 2 ? s[2][e] : s[3][e];
+    const int nt = min(32, ntok - t0);
+#pragma unroll 4
+    for (int u = 0; u < nt; ++u) {
+      const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(vp(t0 + u)) + 2 * lane;
+      const float2 a0 = __bfloat1622float2(v2[0]), a1 = __bfloat1622float2(v2[1]);
+#pragma unroll
+      for (int e = 0; e < REP; ++e) {
+        const float pv = __shfl_sync(0xffffffffu, pj[e], u);
+        o[e][0] += pv * a0.x;
+        o[e][1] += pv * a0.y;
+        o[e][2] += pv * a1.x;
+        o[e][3] += pv * a1.y;
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < REP; ++e) {
+    const size_t pidx = ((size_t)r * a.Hq + h * REP + e) * a.NC + slot;
+    const float inv = 1.0f / l[e];
+    reinterpret_cast<float4*>(a.part_o + pidx * kHD)[lane] =
+        make_float4(o[e][0] * inv, o[e][1] * inv, o[e][2] * inv, o[e][3] * inv);
+    if (lane == 0) {
+      a.part_ml[pidx * 2] = m[e];
+      a.part_ml[pidx * 2 + 1] = l[e];
+    }
+  }
+}
+
+constexpr int kAttnThreads = 256;
+// K, V chunk + per-warp q (prefix path) / q, p, reductions (suffix path)
+template <int REP>
+struct AttnSmem {
+  static constexpr int v = 2 * kAC * kKPad * 2 + 8 * (REP < 2 ? 2 : REP) * kHD * 4;
+};
+
+// One work item: a shared-prefix chunk (is_pre) or one slot's suffix chunk.
+template <int REP>
+__device__ __forceinline__ void attn_item(const AttnArgs& a, bool is_pre, int h, int c, int r_item, uint8_t* asmem) {
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(asmem);
+  __nv_bfloat16* Vs = Ks + kAC * kKPad;
+  float* qbuf = reinterpret_cast<float*>(Vs + kAC * kKPad);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int rep = REP;
+  float* qs = qbuf + warp * (REP < 2 ? 2 : REP) * kHD;
+  auto load_q = [&](int r, int h) {
+    for (int e = 0; e < rep; ++e) {
+      const __nv_bfloat16* qp = a.q + ((size_t)r * a.Hq + h * rep + e) * kHD;
+      const float2 f = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(qp)[lane]);
+      const float2 g2 = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(qp)[lane + 32]);
+      qs[e * kHD + 2 * lane] = f.x;
+      qs[e * kHD + 2 * lane + 1] = f.y;
+      qs[e * kHD + 64 + 2 * lane] = g2.x;
+      qs[e * kHD + 64 + 2 * lane + 1] = g2.y;
+    }
+    __syncwarp();
+  };
+  if (is_pre) {
+    // ---------------- shared-prefix chunk: staged once, scored by every live row
+    const int tok0 = c * kPC, ntok = min(kPC, a.plen - tok0);
+    {
+      constexpr int NJ = kPC * (kHD / 8) / kAttnThreads;
+      uint4 kk[NJ], vv[NJ];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int i = threadIdx.x + j * kAttnThreads;
+        const int tk = i >> 4, seg = i & 15;
+        kk[j] = vv[j] = make_uint4(0, 0, 0, 0);
+        if (tk < ntok) {
+          kk[j] = __ldg(reinterpret_cast<const uint4*>(a.kpre + ((size_t)h * a.pcap + tok0 + tk) * kHD + seg * 8));
+          vv[j] = __ldg(reinterpret_cast<const uint4*>(a.vpre + ((size_t)h * a.pcap + tok0 + tk) * kHD + seg * 8));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int i = threadIdx.x + j * kAttnThreads;
+        const int tk = i >> 4, seg = i & 15;
+        *reinterpret_cast<uint4*>(Ks + tk * kKPad + seg * 8) = kk[j];
+        *reinterpret_cast<uint4*>(Vs + tk * kKPad + seg * 8) = vv[j];
+      }
+    }
+    __syncthreads();
+    for (int r = warp; r < a.rows; r += kAttnThreads / 32) {
+      if (!a.row_active[r]) continue;
+      int valid = ntok;
+      if (a.prefill) valid = min(ntok, r + 1 - tok0);
+      if (valid <= 0) continue;
+      load_q(r, h);
+      attn_rows_chunk<REP>(a, r, h, c, valid, qs, [&](int tk) { return Ks + tk * kKPad; },
+                      [&](int tk) { return Vs + tk * kKPad; }, lane);
+      attn_arrive(a, r, h, lane);
+    }
     return;
   }
-  int npre = a.nc_pre, nsuf = 0;
-  if (a.prefill) npre = min(a.nc_pre, r / kChunk + 1);
-  else nsuf = (a.row_len[r] + kChunk - 1) / kChunk;
-  const size_t base = ((size_t)r * a.Hq + qh) * a.NC;
-  float M = -INFINITY;
-  for (int i = 0; i < npre + nsuf; ++i) {
-    const int slot = i < npre ? i : a.nc_pre + (i - npre);
-    M = fmaxf(M, a.part_ml[(base + slot) * 2]);
+  // ---------------- per-slot suffix chunk: one CTA per (row, kv head, chunk)
+  const int r = r_item;
+  const int len = a.row_len[r];
+  const int tok0 = c * kAC;
+  if (tok0 >= len) return;
+  const int ntok = min(kAC, len - tok0);
+  const int32_t* pt_row = a.pagetab + (size_t)a.row_lid[r] * a.maxp;
+  const size_t head_stride = (size_t)a.pt * kHD;
+  // stage: every thread issues all of its 16-B loads before storing (8 K + 8 V pieces)
+  {
+    constexpr int NJ = kAC * (kHD / 8) / kAttnThreads;
+    uint4 kk[NJ], vv[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int i = threadIdx.x + j * kAttnThreads;  // kAC tokens x 16 pieces
+      const int tk = i >> 4, seg = i & 15;
+      kk[j] = vv[j] = make_uint4(0, 0, 0, 0);
+      if (tk < ntok) {
+        const int tok = tok0 + tk;
+        const int page = __ldg(pt_row + tok / a.pt);
+        const size_t base = (((size_t)page * 2) * a.Hkv + h) * head_stride + (size_t)(tok % a.pt) * kHD + seg * 8;
+        kk[j] = __ldg(reinterpret_cast<const uint4*>(a.pool + base));
+        vv[j] = __ldg(reinterpret_cast<const uint4*>(a.pool + base + (size_t)a.Hkv * head_stride));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int i = threadIdx.x + j * kAttnThreads;
+      const int tk = i >> 4, seg = i & 15;
+      *reinterpret_cast<uint4*>(Ks + tk * kKPad + seg * 8) = kk[j];
+      *reinterpret_cast<uint4*>(Vs + tk * kKPad + seg * 8) = vv[j];
+    }
   }
-  float num = 0.f, den = 0.f;
-  for (int i = 0; i < npre + nsuf; ++i) {
-    const int slot = i < npre ? i : a.nc_pre + (i - npre);
-    const float mi = a.part_ml[(base + slot) * 2];
-    if (mi == -INFINITY) continue;
-    const float w = expf(mi - M) * a.part_ml[(base + slot) * 2 + 1];
-    num += w * a.part_o[(base + slot) * kHD + d];
-    den += w;
+  float* qsm = qbuf;                      // [rep][128]
+  float* psm = qbuf + REP * kHD;          // [rep][128]
+  float* red = psm + REP * kHD;           // [2][4][kMaxRep]
+  for (int i = threadIdx.x; i < rep * kHD; i += kAttnThreads)
+    qsm[i] = __bfloat162float(a.q[((size_t)r * a.Hq + h * rep) * kHD + i]);
+  __syncthreads();
+  // scores: thread t < 128 owns token t
+  const int t = threadIdx.x;
+  float sc[REP];
+#pragma unroll
+  for (int e = 0; e < REP; ++e) sc[e] = -INFINITY;
+  if (t < kAC) {
+    float acc[REP];
+#pragma unroll
+    for (int e = 0; e < REP; ++e) acc[e] = 0.f;
+    const uint4* k4 = reinterpret_cast<const uint4*>(Ks + t * kKPad);
+#pragma unroll 2
+    for (int d8 = 0; d8 < kHD / 8; ++d8) {
+      const uint4 kv = k4[d8];
+      const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kv);
+      const float2 f0 = __bfloat1622float2(k2[0]), f1 = __bfloat1622float2(k2[1]);
+      const float2 f2 = __bfloat1622float2(k2[2]), f3 = __bfloat1622float2(k2[3]);
+#pragma unroll
+      for (int e = 0; e < REP; ++e) {
+        if (e < rep) {
+          const float4 qa = *reinterpret_cast<const float4*>(qsm + e * kHD + d8 * 8);
+          const float4 qb = *reinterpret_cast<const float4*>(qsm + e * kHD + d8 * 8 + 4);
+          acc[e] += qa.x * f0.x + qa.y * f0.y + qa.z * f1.x + qa.w * f1.y + qb.x * f2.x + qb.y * f2.y +
+                    qb.z * f3.x + qb.w * f3.y;
+        }
+      }
+    }
+    if (t < ntok) {
+#pragma unroll
+      for (int e = 0; e < REP; ++e) sc[e] = acc[e] * a.scale;
+    }
   }
-  *o = __float2bfloat16_rn(num / den);
+  // block max / sum over the 128 token threads (warps 0..3)
+#pragma unroll
+  for (int e = 0; e < REP; ++e)
+    if (e < rep) {
+      const float mw = warp_max(sc[e]);
+      if (lane == 0 && warp < 4) red[warp * kMaxRep + e] = mw;
+    }
+  __syncthreads();
+  float mrow[REP];
+#pragma unroll
+  for (int e = 0; e < REP; ++e)
+    mrow[e] = fmaxf(fmaxf(red[0 * kMaxRep + e], red[1 * kMaxRep + e]), fmaxf(red[2 * kMaxRep + e], red[3 * kMaxRep + e]));
+  float* red2 = red + 4 * kMaxRep;
+#pragma unroll
+  for (int e = 0; e < REP; ++e)
+    if (e < rep) {
+      const float p = (t < ntok) ? expf(sc[e] - mrow[e]) : 0.f;
+      if (t < kAC) psm[e * kHD + t] = p;
+      const float sw = warp_sum(p);
+      if (lane == 0 && warp < 4) red2[warp * kMaxRep + e] = sw;
+    }
+  __syncthreads();
+  // P.V: outputs (e, d) spread over the CTA
+  for (int idx = threadIdx.x; idx < rep * kHD; idx += kAttnThreads) {
+    const int e = idx / kHD, d = idx % kHD;
+    float o = 0.f;
+    const float* pe = psm + e * kHD;
+#pragma unroll 8
+    for (int tk = 0; tk < ntok; ++tk) o += pe[tk] * __bfloat162float(Vs[tk * kKPad + d]);
+    const float l = red2[0 * kMaxRep + e] + red2[1 * kMaxRep + e] + red2[2 * kMaxRep + e] + red2[3 * kMaxRep + e];
+    const size_t pidx = ((size_t)r * a.Hq + h * rep + e) * a.NC + a.nc_pre + c;
+    a.part_o[pidx * kHD + d] = o / l;
+    if (d == 0) {
+      a.part_ml[pidx * 2] = mrow[e];
+      a.part_ml[pidx * 2 + 1] = l;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) attn_arrive(a, r, h, lane);
+}
+
+
+// Persistent over the work list: decode items come from sched_kernel (prefix
+// chunks first, then every live slot's chunks); prefill items are the prefix
+// chunks (causal).  Items never span a CTA boundary, so the merge counters see
+// each (row, head) partial exactly once.
+template <int REP>
+__global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnArgs a) {
+  pdl_launch_dependents();  // let the next kernel launch and prefetch now; it waits for our completion itself
+  pdl_wait();
+  extern __shared__ __align__(16) uint8_t asmem[];
+  if (threadIdx.x == 0 && a.n_pf > 0) {
+    // Attention moves ~1% of the step's bytes and is latency-bound: use it to
+    // pull the next GEMMs' weights into L2 (cp.async.bulk.prefetch, no smem).
+    long long tot = 0;
+    for (int i = 0; i < a.n_pf; ++i) tot += a.pf_bytes[i];
+    const long long per = ((tot / gridDim.x) + 4095) & ~4095ll;
+    long long lo = (long long)blockIdx.x * per, hi = min(tot, lo + per);
+    long long base = 0;
+    for (int i = 0; i < a.n_pf && lo < hi; ++i) {
+      const long long e0 = base, e1 = base + a.pf_bytes[i];
+      const long long s0 = max(lo, e0), s1 = min(hi, e1);
+      for (long long o = s0; o < s1; o += 32768) {
+        const unsigned sz = (unsigned)min(32768ll, s1 - o);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf_ptr[i] + (o - e0)), "r"(sz) : "memory");
+      }
+      base = e1;
+    }
+  }
+  const int n = a.prefill ? a.Hkv * a.nc_pre : (int)*a.n_items;
+  for (int it = blockIdx.x; it < n; it += gridDim.x) {
+    int code;
+    if (a.prefill) code = (int)(0x80000000u | ((it / a.nc_pre) << 8) | (it % a.nc_pre));
+    else code = a.items[it];
+    const bool is_pre = code < 0;
+    int h, c, r = -1;
+    if (is_pre) {
+      h = (code >> 8) & 0xFF;
+      c = code & 0xFF;
+    } else {
+      c = (code >> 16) & 0xFF;
+      r = (code >> 8) & 0xFF;
+      h = code & 0xFF;
+    }
+    attn_item<REP>(a, is_pre, h, c, r, asmem);
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------------------------------ scheduler (Alg. 1 loop body, Alg. 3)
@@ -309,6 +496,7 @@ enum SchedState {
   ST_FREE_TOP,
   ST_ERROR,
   ST_TOKENS,
+  ST_ATTN_ITEMS,   // length of the attention work list for the next step
   ST_COUNT
 };
 
@@ -339,6 +527,8 @@ struct SchedArgs {
   int32_t* row_pos;
   int32_t* row_kvloc;
   int32_t* row_len;
+  int32_t* attn_items;       // [Hkv * (nc_pre + row_cap * nc_suf)]
+  int Hkv, nc_pre, nc_suf, chunk;
 };
 
 // Single thread: the work is O(g + pages) integer bookkeeping per step.
@@ -346,8 +536,8 @@ struct SchedArgs {
 // park / refill in ascending slot order (R18); then always prepare the rows of
 // the next step (page allocation on boundary crossing, R26).
 __global__ void sched_kernel(SchedArgs a, int consume) {
+  pdl_launch_dependents();  // let the next kernel launch and prefetch now; it waits for our completion itself
   pdl_wait();
-  pdl_launch_dependents();
   if (threadIdx.x != 0) return;
   long long* st = a.st;
   if (consume) {
@@ -440,6 +630,20 @@ __global__ void sched_kernel(SchedArgs a, int consume) {
     a.row_kvloc[s] = a.pagetab[(size_t)uid * a.maxp + tt / a.pt] * a.pt + tt % a.pt;
     a.row_len[s] = tt + 1;
   }
+  // attention work list of the next step: shared-prefix chunks first (heavier:
+  // every live row), then each live slot's suffix chunks, chunk-major.
+  {
+    int n = 0;
+    if (any) {
+      for (int h = 0; h < a.Hkv; ++h)
+        for (int c = 0; c < a.nc_pre; ++c) a.attn_items[n++] = (int)(0x80000000u | (h << 8) | c);
+      for (int c = 0; c < a.nc_suf; ++c)
+        for (int s = 0; s < a.row_cap; ++s)
+          if (a.row_active[s] && c * a.chunk < a.row_len[s])
+            for (int h = 0; h < a.Hkv; ++h) a.attn_items[n++] = (c << 16) | (s << 8) | h;
+    }
+    st[ST_ATTN_ITEMS] = n;
+  }
   if (any) {
     const long long step = st[ST_STEP];
     if (step < a.log_cap) {
@@ -455,8 +659,8 @@ __global__ void sched_kernel(SchedArgs a, int consume) {
 // Prefill rows: row r = prompt position r (0..P-2), causal over the prefix.
 __global__ void prefill_rows_kernel(const int32_t* __restrict__ prompt, int n, int32_t* row_active,
                                     int32_t* row_tok, int32_t* row_pos, int32_t* row_kvloc) {
+  pdl_launch_dependents();  // let the next kernel launch and prefetch now; it waits for our completion itself
   pdl_wait();
-  pdl_launch_dependents();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   row_active[r] = 1;

@@ -51,4 +51,11 @@ if args.time:
         print(f"{names[k]:12s} {ms[kind == k].sum():8.4f} ms  n={int((kind == k).sum())}")
     print("eager total", ms.sum())
 print(ctx.is_query())
+if os.environ.get("IS_TIMELINE"):
+    import ctypes
+    L = _lib.load()
+    L.is_dbg_timeline.argtypes = [ctypes.c_void_p]
+    ctx.is_decode_step()
+    torch.cuda.synchronize()
+    L.is_dbg_timeline(ctx._h)
 ctx.close()

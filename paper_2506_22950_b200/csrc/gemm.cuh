@@ -68,6 +68,7 @@ struct GemmArgs {
   uint64_t seed;
   float inv_temp;
   QkvEpiArgs qkv;
+  float* partials;              // split-K workspace [clusters][split][128][BN] fp32 (L2-resident)
   unsigned long long* dbg_ts;  // optional [gridDim][16] globaltimer stamps (probe)
 };
 
@@ -80,9 +81,7 @@ struct GemmCfg {
   static constexpr int kStageA = kBM * kBK * 2;  // 16 KB
   static constexpr int kStageB = BN * kBK * 2;
   static constexpr int kStage = kStageA + kStageB;
-  static constexpr int kRed = (BN + 8) * kBM * 4;                           // >= split * ceil(BN/split) * 128 floats
-  static constexpr int kXbuf = BN * kBM * 4;                                 // epilogue exchange
-  static constexpr int kAux = kRed > kXbuf ? kRed : kXbuf;                   // red, then xbuf (aliased)
+  static constexpr int kAux = 2 * BN * kBM * 4;  // epilogue: stg[BN][128] (accumulator tile) + pre[BN][128]
   static constexpr int kTmemCols = (2 * BN) <= 32 ? 32 : ((2 * BN) <= 64 ? 64 : 128);
   static constexpr int kSmem = STAGES * kStage + kAux + 1024 /*barriers*/ + 1024 /*align*/;
 };
@@ -96,6 +95,7 @@ __device__ __forceinline__ void stamp(const GemmArgs& a, int i) {
 }
 
 __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + expf(-x)); }
+
 
 template <int BN, int EPI, int STAGES>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -232,37 +232,33 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else {
     // ------------------------------------------------ epilogue warps 2..5
+    // Written as short runtime loops over columns: this code runs cold out of
+    // the instruction cache once per launch, so its length -- not its
+    // arithmetic -- sets the latency.
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int m = q * 32 + lane;
+    float* stg = aux;             // [BN][128] accumulator tile (column n = activation row)
+    float* pre = aux + BN * kBM;  // [BN][128] operands prefetched during the mainloop
     pdl_wait();
     int it = 0;
     for (int tile = cl; tile < a.num_tiles; tile += ncl, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      // Epilogue operands that do not depend on this GEMM are loaded while the
-      // mainloop streams weights (hides their global-memory latency).
-      float rv[BN], sv[BN];
-      float qk_gain = 1.f;
+      const int gm = tile * kBM + m;
+      // operands that do not depend on this GEMM, loaded while weights stream in
       if constexpr (EPI == EPI_RESID_ADD) {
-        const int gm = tile * kBM + m;
-#pragma unroll
-        for (int n = 0; n < BN; ++n)
-          rv[n] = (n >= n_lo && n < n_hi && n < a.n_valid && gm < a.M) ? a.out[(size_t)(a.row0 + n) * a.ld_out + gm]
-                                                                      : 0.f;
+        for (int n = n_lo; n < n_hi; ++n)
+          pre[n * kBM + m] = (n < a.n_valid && gm < a.M) ? a.out[(size_t)(a.row0 + n) * a.ld_out + gm] : 0.f;
       }
       if constexpr (EPI == EPI_QKV) {
         const QkvEpiArgs& e = a.qkv;
-        qk_gain = tile < e.Hq ? e.q_gain[m] : (tile < e.Hq + e.Hkv ? e.k_gain[m] : 1.f);
-#pragma unroll
-        for (int n = 0; n < BN; ++n) {
-          const int row = a.row0 + n;
-          rv[n] = sv[n] = 0.f;
-          if (n >= n_lo && n < n_hi && n < a.n_valid && tile < e.Hq + e.Hkv) {
-            const int pos = e.row_pos[row];
-            rv[n] = e.rope_cos[(size_t)pos * 64 + (m & 63)];
-            sv[n] = e.rope_sin[(size_t)pos * 64 + (m & 63)];
+        if (tile < e.Hq + e.Hkv)
+          for (int n = n_lo; n < n_hi; ++n) {
+            if (n < a.n_valid) {
+              const int pos = e.row_pos[a.row0 + n];
+              pre[n * kBM + m] = m < 64 ? e.rope_cos[(size_t)pos * 64 + m] : e.rope_sin[(size_t)pos * 64 + m - 64];
+            }
           }
-        }
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -276,148 +272,119 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (lane == 0) mbar_arrive(&tempty[acc]);
 
       if (S > 1) {
-        // Partials -> own smem aux[n][m]; one cluster barrier; then every rank
-        // pulls its column slice from all ranks (independent DSMEM loads, issued
-        // together) and sums in rank order.  A second cluster barrier (end of
-        // kernel) keeps each rank's smem alive until its peers have read it.
+        // Partials -> L2 workspace part[cluster][rank][m][BN] (coalesced float4
+        // stores); the cluster barrier (release / acquire) orders them; each rank
+        // sums its column slice [n_lo, n_hi) over ranks 0..S-1 in order.
+        float* part = a.partials + (size_t)cl * S * kBM * BN;
 #pragma unroll
-        for (int n = 0; n < BN; ++n) aux[n * kBM + m] = v[n];
+        for (int c4 = 0; c4 < BN / 4; ++c4)
+          reinterpret_cast<float4*>(part + ((size_t)rank * kBM + m) * BN)[c4] =
+              make_float4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // start-up phase
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
         if (threadIdx.x == 64) stamp(a, 6);
-        const uint32_t laux = smem_u32(aux);
+        // aligned float4 groups covering the slice; per group all ranks' loads in flight
+        for (int c0 = n_lo & ~3; c0 < n_hi; c0 += 4) {
+          float4 t[8];
 #pragma unroll
-        for (int n = 0; n < BN; ++n) {
-          if (n >= n_lo && n < n_hi) {
-            float t[8];
+          for (int j = 0; j < 8; ++j)
+            if (j < S) t[j] = __ldcg(reinterpret_cast<const float4*>(part + ((size_t)j * kBM + m) * BN + c0));
+          float4 sum = t[0];
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              t[j] = (j < S && j != rank) ? ld_dsmem_f32_nv(mapa_shared(laux + (uint32_t)(n * kBM + m) * 4u, j)) : 0.f;
-            float sum = 0.f;
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (j < S) sum += (j == rank) ? v[n] : t[j];
-            v[n] = sum;
-          }
-        }
-        // every thread's remote reads are done (values consumed above): release peers
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (threadIdx.x == 64) {
-          const uint32_t lc = smem_u32(consumed);
-          for (int j = 0; j < S; ++j)
-            if (j != rank)
-              asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa_shared(lc, j))
-                           : "memory");
-          stamp(a, 7);
-        }
-      }
-
-      const int gm = tile * kBM + m;
-      if (threadIdx.x == 64) stamp(a, 8);
-      if constexpr (EPI == EPI_STORE_F32 || EPI == EPI_RESID_ADD) {
-#pragma unroll
-        for (int n = 0; n < BN; ++n) {
-          if (n >= n_lo && n < n_hi && n < a.n_valid && gm < a.M) {
-            float* p = a.out + (size_t)(a.row0 + n) * a.ld_out + gm;
-            if (EPI == EPI_RESID_ADD) *p = rv[n] + v[n];
-            else *p = v[n];
-          }
-        }
-      } else if constexpr (EPI == EPI_SWIGLU) {
-        float* xbuf = aux;
-        if (m >= 64) {
-#pragma unroll
-          for (int n = 0; n < BN; ++n) xbuf[n * 64 + (m - 64)] = v[n];
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (m < 64) {
-          const int f = tile * 64 + m;
-#pragma unroll
-          for (int n = 0; n < BN; ++n) {
-            if (n >= n_lo && n < n_hi && n < a.n_valid && f * 2 < a.M) {
-              const float u = xbuf[n * 64 + m];
-              a.act[(size_t)(a.row0 + n) * a.ld_act + f] = __float2bfloat16_rn(silu_f(v[n]) * u);
+          for (int j = 1; j < 8; ++j)
+            if (j < S) {
+              sum.x += t[j].x;
+              sum.y += t[j].y;
+              sum.z += t[j].z;
+              sum.w += t[j].w;
             }
-          }
+          stg[(c0 + 0) * kBM + m] = sum.x;
+          stg[(c0 + 1) * kBM + m] = sum.y;
+          stg[(c0 + 2) * kBM + m] = sum.z;
+          stg[(c0 + 3) * kBM + m] = sum.w;
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 64) stamp(a, 7);
+      } else {
+#pragma unroll
+        for (int n = 0; n < BN; ++n) stg[n * kBM + m] = v[n];
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 64) stamp(a, 8);
+
+      if constexpr (EPI == EPI_STORE_F32 || EPI == EPI_RESID_ADD) {
+        if (gm < a.M)
+          for (int n = n_lo; n < min(n_hi, a.n_valid); ++n) {
+            float x = stg[n * kBM + m];
+            if (EPI == EPI_RESID_ADD) x += pre[n * kBM + m];
+            a.out[(size_t)(a.row0 + n) * a.ld_out + gm] = x;
+          }
+      } else if constexpr (EPI == EPI_SWIGLU) {
+        // rows [0, 64) of the tile are gate features f, rows [64, 128) the matching up
+        const int f = tile * 64 + m;
+        if (m < 64 && f * 2 < a.M)
+          for (int n = n_lo; n < min(n_hi, a.n_valid); ++n)
+            a.act[(size_t)(a.row0 + n) * a.ld_act + f] =
+                __float2bfloat16_rn(silu_f(stg[n * kBM + m]) * stg[n * kBM + m + 64]);
       } else if constexpr (EPI == EPI_QKV) {
         // head = tile: q (tile < Hq), k (< Hq + Hkv) or v.  Per-head RMSNorm over the
-        // 128 lanes of a column, rotate-half RoPE pairs (m, m +- 64) through smem.
+        // 128 lanes of a column, then rotate-half RoPE pairs (m, m +- 64).
         const QkvEpiArgs& e = a.qkv;
         const bool is_v = tile >= e.Hq + e.Hkv, is_q = tile < e.Hq;
-        float* xbuf = aux;
+        const int n_end = min(n_hi, a.n_valid);
         if (!is_v) {
-#pragma unroll
-          for (int n = 0; n < BN; ++n) {
-            if (n >= n_lo && n < n_hi) {
-              const float ss = warp_sum(v[n] * v[n]);
-              if (lane == 0) sred[q][n] = ss;
-            }
+          for (int n = n_lo; n < n_end; ++n) {
+            const float x = stg[n * kBM + m];
+            const float ss = warp_sum(x * x);
+            if (lane == 0) sred[q][n] = ss;
           }
           asm volatile("bar.sync 1, 128;" ::: "memory");
-          const float gn = qk_gain;
-#pragma unroll
-          for (int n = 0; n < BN; ++n) {
-            if (n >= n_lo && n < n_hi) {
-              const float ss = sred[0][n] + sred[1][n] + sred[2][n] + sred[3][n];
-              v[n] = v[n] * (1.0f / sqrtf(ss / (float)kBM + e.eps)) * gn;
-              xbuf[n * kBM + m] = v[n];
-            }
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-#pragma unroll
-          for (int n = 0; n < BN; ++n) {
-            const int row = a.row0 + n;
-            if (n >= n_lo && n < n_hi && n < a.n_valid && e.row_active[row]) {
-              const float c = rv[n], s = sv[n];
-              const float y = v[n];
-              v[n] = m < 64 ? (y * c - xbuf[n * kBM + m + 64] * s) : (y * c + xbuf[n * kBM + m - 64] * s);
-            }
+          const float gn = is_q ? e.q_gain[m] : e.k_gain[m];
+          for (int n = n_lo; n < n_end; ++n) {
+            const float ss = sred[0][n] + sred[1][n] + sred[2][n] + sred[3][n];
+            stg[n * kBM + m] *= (1.0f / sqrtf(ss / (float)kBM + e.eps)) * gn;
           }
           asm volatile("bar.sync 1, 128;" ::: "memory");
         }
-#pragma unroll
-        for (int n = 0; n < BN; ++n) {
+        const int hk = tile - e.Hq - (is_v ? e.Hkv : 0);
+        for (int n = n_lo; n < n_end; ++n) {
           const int row = a.row0 + n;
-          if (n >= n_lo && n < n_hi && n < a.n_valid && e.row_active[row]) {
-            const __nv_bfloat16 b = __float2bfloat16_rn(v[n]);
-            if (is_q) {
-              e.q_out[((size_t)row * e.Hq + tile) * kBM + m] = b;
-            } else {
-              const int kvsel = is_v ? 1 : 0;
-              const int hk = tile - e.Hq - (is_v ? e.Hkv : 0);
-              const int loc = e.row_kvloc[row];
-              size_t off;
-              if (e.prefill) {
-                off = (((size_t)kvsel * e.Hkv + hk) * e.pcap + loc) * kBM + m;
-              } else {
-                const int page = loc / e.pt, o = loc % e.pt;
-                off = ((((size_t)page * 2 + kvsel) * e.Hkv + hk) * e.pt + o) * kBM + m;
-              }
-              e.kv[off] = b;
-            }
+          if (!e.row_active[row]) continue;
+          float y = stg[n * kBM + m];
+          if (!is_v) {
+            const int i = m & 63;
+            const float c = pre[n * kBM + i], sn = pre[n * kBM + 64 + i];
+            y = m < 64 ? (y * c - stg[n * kBM + m + 64] * sn) : (y * c + stg[n * kBM + m - 64] * sn);
+          }
+          const __nv_bfloat16 b = __float2bfloat16_rn(y);
+          if (is_q) {
+            e.q_out[((size_t)row * e.Hq + tile) * kBM + m] = b;
+          } else {
+            const int kvsel = is_v ? 1 : 0;
+            const int loc = e.row_kvloc[row];
+            size_t off;
+            if (e.prefill) off = (((size_t)kvsel * e.Hkv + hk) * e.pcap + loc) * kBM + m;
+            else off = ((((size_t)(loc / e.pt) * 2 + kvsel) * e.Hkv + hk) * e.pt + loc % e.pt) * kBM + m;
+            e.kv[off] = b;
           }
         }
       } else if constexpr (EPI == EPI_SAMPLE) {
-#pragma unroll
-        for (int n = 0; n < BN; ++n) {
-          if (n < a.n_valid && a.row_active[a.row0 + n]) {
-            unsigned long long key = 0ull;
-            if (gm < a.M) {
-              if (a.logits_dump) a.logits_dump[(size_t)(a.row0 + n) * a.ld_out + gm] = v[n];
-              const float g = gumbel(a.seed, (uint32_t)a.row_uid[a.row0 + n], (uint32_t)a.row_t[a.row0 + n],
-                                     (uint32_t)gm);
-              key = order_key(__fadd_rn(__fmul_rn(v[n], a.inv_temp), g), (uint32_t)gm);
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-              key = other > key ? other : key;
-            }
-            if (lane == 0) atomicMax(&skey[n], key);
+        for (int n = 0; n < min(BN, a.n_valid); ++n) {
+          if (!a.row_active[a.row0 + n]) continue;
+          unsigned long long key = 0ull;
+          if (gm < a.M) {
+            const float z = stg[n * kBM + m];
+            if (a.logits_dump) a.logits_dump[(size_t)(a.row0 + n) * a.ld_out + gm] = z;
+            const float g = gumbel(a.seed, (uint32_t)a.row_uid[a.row0 + n], (uint32_t)a.row_t[a.row0 + n],
+                                   (uint32_t)gm);
+            key = order_key(__fadd_rn(__fmul_rn(z, a.inv_temp), g), (uint32_t)gm);
           }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+            key = other > key ? other : key;
+          }
+          if (lane == 0) atomicMax(&skey[n], key);
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (threadIdx.x - 64 < BN) {
@@ -425,21 +392,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (skey[n]) atomicMax(a.keys + a.row0 + n, skey[n]);
           skey[n] = 0ull;
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
       }
+      // stg / pre / skey are rewritten by the next tile
+      asm volatile("bar.sync 1, 128;" ::: "memory");
     }
   }
 
   if (threadIdx.x == 64) stamp(a, 10);
   if (S > 1) {
     // producer / MMA warps: complete the start-up barrier phase and arrive on the
-    // partials-written phase the epilogue waits for.  Then keep this CTA's smem
-    // alive until every peer has signalled that it finished reading it.
+    // partials-written phase the epilogue waits for.
     if (warp < 2) {
       asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
       asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     }
-    if (threadIdx.x == 64) mbar_wait(consumed, 0);
   }
   tc_fence_before();
   __syncthreads();

@@ -238,6 +238,7 @@ static is_status make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_
 static int g_num_sms = 0;
 static bool g_use_pdl = true;
 static int g_skip = 0;
+static float* g_splitk_ws = nullptr;  // set per context before enqueueing
 static unsigned long long* g_tl = nullptr;  // current timeline buffer during enqueue
 static int g_tl_n = 0;
 static const char* g_tl_name[512];  // debug: bit k skips kernel class k in the decode step (timing experiments only)
@@ -283,6 +284,8 @@ static is_status launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB, Gem
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
+  if (!a.partials) a.partials = g_splitk_ws;
+  if (a.split > 1 && (a.num_tiles * a.split > 2 * 160 || !a.partials)) return fail(IS_ERR_CAPACITY, "split-K workspace too small");
   if (g_tl && g_tl_n < 512 && !a.dbg_ts) {
     a.dbg_ts = g_tl + (size_t)g_tl_n * 296 * 16;
     g_tl_name[g_tl_n++] = EPI == EPI_QKV ? "qkv" : EPI == EPI_RESID_ADD ? "resid" : EPI == EPI_SWIGLU ? "gu" : EPI == EPI_SAMPLE ? "lm" : "f32";
@@ -388,6 +391,7 @@ struct is_ctx {
   float *part_o, *part_ml;
   int32_t* attn_cnt;
   int32_t* attn_items;
+  float* splitk_ws;  // split-K partials workspace
   int NC, nc_pre, nc_suf;
   CUtensorMap tm_xn_dec, tm_attn_dec, tm_act_dec, tm_xn_pre, tm_attn_pre, tm_act_pre;
   float *rope_cos, *rope_sin;
@@ -487,6 +491,7 @@ static void prof_mark(cudaStream_t st, int kind) {
 // One layer stack over `rows` rows starting at row 0 (decode: rows = rc, BN = c->BN;
 // prefill: rows = pcap processed in 64-row GEMM chunks).
 static is_status run_layers(is_ctx* c, int rows, bool prefill) {
+  g_splitk_ws = c->splitk_ws;
   cudaStream_t st = c->st;
   const is_shape& s = c->sh;
   const int H = s.hidden, F = s.ffn, Hq = s.n_q_heads, Hkv = s.n_kv_heads;
@@ -646,6 +651,7 @@ static is_status enqueue_step(is_ctx* c) {
   a.logits_dump = c->logits_dump;
   a.seed = c->cfg.seed;
   a.inv_temp = (float)(1.0 / (double)c->cfg.temperature);
+  g_splitk_ws = c->splitk_ws;
   CKS(launch_gemm<EPI_SAMPLE>(c->BN, c->tm_embed, c->tm_xn_dec, a, st));
   prof_mark(st, 7);
   CKS(launch_k(sched_kernel, dim3(1), dim3(32), st, sched_args(c), 1));
@@ -823,6 +829,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->part_o = (float*)A((size_t)R * Hq * c->NC * 128 * 4);
   c->part_ml = (float*)A((size_t)R * Hq * c->NC * 2 * 4);
   c->attn_cnt = (int32_t*)A((size_t)R * Hkv * 4);
+  c->splitk_ws = (float*)A((size_t)2 * 160 * kBM * 64 * 4);
   c->attn_items = (int32_t*)A((size_t)Hkv * (c->nc_pre + c->rc * c->nc_suf) * 4 + 64);
   c->rope_cos = (float*)A((size_t)c->max_pos * 64 * 4);
   c->rope_sin = (float*)A((size_t)c->max_pos * 64 * 4);
@@ -888,7 +895,7 @@ extern "C" void is_destroy(is_ctx* c) {
   cudaStreamSynchronize(c->st);
   if (c->graph_ok) cudaGraphExecDestroy(c->graph);
   void* bufs[] = {c->wblob, c->final_norm, c->prefix, c->pool, c->resid, c->xn, c->attn, c->act, c->q,
-                  c->part_o, c->part_ml, c->attn_cnt, c->attn_items, c->rope_cos, c->rope_sin, c->row_active, c->row_uid, c->row_lid,
+                  c->part_o, c->part_ml, c->attn_cnt, c->attn_items, c->splitk_ws, c->rope_cos, c->rope_sin, c->row_active, c->row_uid, c->row_lid,
                   c->row_t, c->row_tok, c->row_pos, c->row_kvloc, c->row_len, c->keys, c->last_tok,
                   c->last_fin, c->st_dev, c->slot_uid, c->slot_count, c->tpos, c->true_len, c->queue,
                   c->main_init, c->main_queue, c->free_stack, c->pagetab, c->npages, c->tokens, c->log_slot,
@@ -1162,6 +1169,9 @@ extern "C" is_status is_dbg_gemm(const void* d_w, const void* d_x, float* d_y, i
   a.n_valid = rows;
   a.out = d_y;
   a.ld_out = M;
+  static float* ws = nullptr;
+  if (!ws) CK(cudaMalloc(&ws, (size_t)2 * 160 * kBM * 64 * 4));
+  a.partials = ws;
   a.dbg_ts = getenv("IS_GEMM_STAMPS") ? reinterpret_cast<unsigned long long*>(strtoull(getenv("IS_GEMM_STAMPS"), nullptr, 0)) : nullptr;
   CKS(launch_gemm<EPI_STORE_F32>(BN, tA, tB, a, (cudaStream_t)stream));
   CK(cudaGetLastError());
@@ -1189,6 +1199,25 @@ extern "C" int is_dbg_timeline(is_ctx* c) {
         if (p[k]) { mn[k] = std::min(mn[k], p[k]); mx[k] = std::max(mx[k], p[k]); }
     }
     auto f = [&](unsigned long long v) { return v == ~0ull || v == 0 ? -1.0 : (double)(v - t0) / 1000.0; };
+    // per-CTA phase durations (median / max, us)
+    auto dur = [&](int k0, int k1, double* med, double* mxx) {
+      std::vector<double> d;
+      for (int b = 0; b < 296; ++b) {
+        const unsigned long long* p = &h[((size_t)L * 296 + b) * 16];
+        if (p[0] && p[k0] && p[k1]) d.push_back((double)((long long)(p[k1] - p[k0])) / 1000.0);
+      }
+      if (d.empty()) { *med = *mxx = -1; return; }
+      std::sort(d.begin(), d.end());
+      *med = d[d.size() / 2];
+      *mxx = d.back();
+    };
+    double m56, x56, m67, x67, m78, x78, m8a, x8a;
+    dur(5, 6, &m56, &x56);
+    dur(6, 7, &m67, &x67);
+    dur(7, 8, &m78, &x78);
+    dur(8, 10, &m8a, &x8a);
+    printf("      per-CTA us: tfull->cbar %.2f/%.2f  cbar->pulled %.2f/%.2f  pulled->epi0 %.2f/%.2f  epi %.2f/%.2f\n", m56,
+           x56, m67, x67, m78, x78, m8a, x8a);
     printf("%3d %-5s ctas=%3d start %7.2f..%7.2f pre %7.2f data0 %7.2f..%7.2f mma_done %7.2f..%7.2f cbar %7.2f pulled %7.2f epi %7.2f..%7.2f exit %7.2f..%7.2f\n", L,
            g_tl_name[L], n, f(mn[0]), f(mx[0]), f(mx[2]), f(mn[3]), f(mx[3]), f(mn[5]), f(mx[5]), f(mx[6]), f(mx[7]),
            f(mn[10]), f(mx[10]), f(mn[11]), f(mx[11]));

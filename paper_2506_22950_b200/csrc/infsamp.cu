@@ -564,6 +564,8 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
     aa.cnt = c->attn_cnt;
     aa.out = c->attn;
     aa.items = c->attn_items;
+    aa.dbg_ts = nullptr;
+    if (g_tl && l < 4) aa.dbg_ts = g_tl + (size_t)(400 + l) * 296 * 16;
     aa.n_pf = 0;
     if (!prefill && c->l2_prefetch) {
       aa.pf_ptr[0] = reinterpret_cast<const uint8_t*>(w.wo);
@@ -880,7 +882,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->split_o = choose_split((int)ceil_div64(H, kBM), Hq * 128 / kBK, c->BN);
   c->split_gu = choose_split((int)ceil_div64(2 * F, kBM), H / kBK, c->BN);
   c->split_d = choose_split((int)ceil_div64(H, kBM), F / kBK, c->BN);
-  c->l2_prefetch = getenv("IS_L2_PREFETCH") ? atoi(getenv("IS_L2_PREFETCH")) : 2;
+  c->l2_prefetch = getenv("IS_L2_PREFETCH") ? atoi(getenv("IS_L2_PREFETCH")) : 0;
   if (const char* e = getenv("IS_SPLIT_OVERRIDE")) {
     int v = atoi(e);
     if (v >= 1 && v <= 8) c->split_qkv = c->split_o = c->split_gu = c->split_d = v;
@@ -1182,8 +1184,9 @@ extern "C" is_status is_dbg_gemm(const void* d_w, const void* d_x, float* d_y, i
 extern "C" int is_dbg_timeline(is_ctx* c) {
   if (!c || !c->timeline) return 0;
   cudaStreamSynchronize(c->st);
-  std::vector<unsigned long long> h((size_t)c->tl_count * 296 * 16);
-  cudaMemcpy(h.data(), c->timeline, h.size() * 8, cudaMemcpyDeviceToHost);
+  std::vector<unsigned long long> h0((size_t)512 * 296 * 16);
+  cudaMemcpy(h0.data(), c->timeline, h0.size() * 8, cudaMemcpyDeviceToHost);
+  std::vector<unsigned long long> h(h0.begin(), h0.begin() + (size_t)c->tl_count * 296 * 16);
   unsigned long long t0 = ~0ull;
   for (size_t i = 0; i < h.size(); i += 16)
     if (h[i] && h[i] < t0) t0 = h[i];
@@ -1221,6 +1224,29 @@ extern "C" int is_dbg_timeline(is_ctx* c) {
     printf("%3d %-5s ctas=%3d start %7.2f..%7.2f pre %7.2f data0 %7.2f..%7.2f mma_done %7.2f..%7.2f cbar %7.2f pulled %7.2f epi %7.2f..%7.2f exit %7.2f..%7.2f\n", L,
            g_tl_name[L], n, f(mn[0]), f(mx[0]), f(mx[2]), f(mn[3]), f(mx[3]), f(mn[5]), f(mx[5]), f(mx[6]), f(mx[7]),
            f(mn[10]), f(mx[10]), f(mn[11]), f(mx[11]));
+  }
+  for (int l = 0; l < 4; ++l) {
+    const unsigned long long* base = &h0[(size_t)(400 + l) * 296 * 16];
+    double st = 1e30, en = 0, dw = 0;
+    int n = 0;
+    std::vector<double> stg, part, fin;
+    for (int b = 0; b < 296; ++b) {
+      const unsigned long long* p = base + b * 16;
+      if (!p[0]) continue;
+      st = std::min(st, (double)(p[0] - t0) / 1e3);
+      en = std::max(en, (double)(p[15] - t0) / 1e3);
+      dw = std::max(dw, (double)(p[1] - t0) / 1e3);
+      if (p[2] && p[4]) {
+        ++n;
+        stg.push_back((double)(p[2] - p[1]) / 1e3);
+        part.push_back((double)(p[3] ? p[3] - p[2] : 0) / 1e3);
+        fin.push_back((double)(p[4] - (p[3] ? p[3] : p[2])) / 1e3);
+      }
+    }
+    auto med = [](std::vector<double> v) { if (v.empty()) return -1.0; std::sort(v.begin(), v.end()); return v[v.size() / 2]; };
+    auto mx = [](std::vector<double> v) { if (v.empty()) return -1.0; return *std::max_element(v.begin(), v.end()); };
+    printf("attn L%d start %.2f waited %.2f end %.2f  items=%d  stage %.2f/%.2f  compute %.2f/%.2f  arrive+merge %.2f/%.2f\n", l, st, dw,
+           en, n, med(stg), mx(stg), med(part), mx(part), med(fin), mx(fin));
   }
   fflush(stdout);
   return c->tl_count;

@@ -95,6 +95,7 @@ struct AttnArgs {
   const uint8_t* pf_ptr[4];   // weights to pull into L2 while attention runs (latency-bound phase)
   long long pf_bytes[4];
   int n_pf;
+  unsigned long long* dbg_ts;  // optional [gridDim][16] globaltimer stamps
   const long long* n_items;   // its length
   __nv_bfloat16* out;         // [rows][Hq][128]
   int rows, Hq, Hkv, pcap, plen, pt, maxp;
@@ -102,6 +103,14 @@ struct AttnArgs {
   int prefill;                // 1: rows are prompt positions, causal over the prefix, no suffix
   float scale;                // 1/sqrt(128)
 };
+
+__device__ __forceinline__ void astamp(const AttnArgs& a, int i) {
+  if (a.dbg_ts && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.dbg_ts[blockIdx.x * 16 + i] = t;
+  }
+}
 
 __device__ __forceinline__ int attn_expected(const AttnArgs& a, int r) {
   if (a.prefill) return min(a.nc_pre, r / kPC + 1);
@@ -262,7 +271,8 @@ struct AttnSmem {
 
 // One work item: a shared-prefix chunk (is_pre) or one slot's suffix chunk.
 template <int REP>
-__device__ __forceinline__ void attn_item(const AttnArgs& a, bool is_pre, int h, int c, int r_item, uint8_t* asmem) {
+__device__ __forceinline__ void attn_item(const AttnArgs& a, bool is_pre, int h, int c, int r_item, uint8_t* asmem,
+                                          int sb) {
   __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(asmem);
   __nv_bfloat16* Vs = Ks + kAC * kKPad;
   float* qbuf = reinterpret_cast<float*>(Vs + kAC * kKPad);
@@ -306,6 +316,7 @@ __device__ __forceinline__ void attn_item(const AttnArgs& a, bool is_pre, int h,
       }
     }
     __syncthreads();
+    astamp(a, sb);
     for (int r = warp; r < a.rows; r += kAttnThreads / 32) {
       if (!a.row_active[r]) continue;
       int valid = ntok;
@@ -357,6 +368,7 @@ __device__ __forceinline__ void attn_item(const AttnArgs& a, bool is_pre, int h,
   for (int i = threadIdx.x; i < rep * kHD; i += kAttnThreads)
     qsm[i] = __bfloat162float(a.q[((size_t)r * a.Hq + h * rep) * kHD + i]);
   __syncthreads();
+  astamp(a, sb);
   // scores: thread t < 128 owns token t
   const int t = threadIdx.x;
   float sc[REP];
@@ -426,6 +438,7 @@ __device__ __forceinline__ void attn_item(const AttnArgs& a, bool is_pre, int h,
     }
   }
   __syncthreads();
+  astamp(a, sb + 1);
   if (warp == 0) attn_arrive(a, r, h, lane);
 }
 
@@ -439,6 +452,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnArgs a) {
   pdl_launch_dependents();  // let the next kernel launch and prefetch now; it waits for our completion itself
   pdl_wait();
   extern __shared__ __align__(16) uint8_t asmem[];
+  astamp(a, 0);
   if (threadIdx.x == 0 && a.n_pf > 0) {
     // Attention moves ~1% of the step's bytes and is latency-bound: use it to
     // pull the next GEMMs' weights into L2 (cp.async.bulk.prefetch, no smem).
@@ -458,6 +472,8 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnArgs a) {
     }
   }
   const int n = a.prefill ? a.Hkv * a.nc_pre : (int)*a.n_items;
+  astamp(a, 1);
+  int nit = 0;
   for (int it = blockIdx.x; it < n; it += gridDim.x) {
     int code;
     if (a.prefill) code = (int)(0x80000000u | ((it / a.nc_pre) << 8) | (it % a.nc_pre));
@@ -472,9 +488,12 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnArgs a) {
       r = (code >> 8) & 0xFF;
       h = code & 0xFF;
     }
-    attn_item<REP>(a, is_pre, h, c, r, asmem);
+    attn_item<REP>(a, is_pre, h, c, r, asmem, nit < 4 ? 2 + 3 * nit : 14);
     __syncthreads();
+    if (nit < 4) astamp(a, 2 + 3 * nit + 2);
+    ++nit;
   }
+  astamp(a, 15);
 }
 
 // ------------------------------------------------------------------ scheduler (Alg. 1 loop body, Alg. 3)

@@ -67,7 +67,7 @@ static is_status check_config(const is_config* c) {
   if (g < 1 || g > c->G || c->G % g) return fail(IS_ERR_CONFIG, "need 1 <= g <= G and G mod g == 0 (G=%d g=%d)", c->G, g);
   if (!(c->eps > 0)) return fail(IS_ERR_CONFIG, "eps must be > 0");
   if (c->max_new_tokens < 1 || c->prompt_len < 2) return fail(IS_ERR_CONFIG, "max_new_tokens >= 1 and prompt_len >= 2");
-  if (c->page_tokens < 1) return fail(IS_ERR_CONFIG, "page_tokens must be >= 1");
+  if (c->page_tokens < 4 || 64 % c->page_tokens) return fail(IS_ERR_CONFIG, "page_tokens must divide 64 and be >= 4");
   if (c->prefix_k < 0 || (c->prefix_k > 0 && c->mode != IS_MODE_INFINITE))
     return fail(IS_ERR_CONFIG, "prefix_k > 0 requires IS_MODE_INFINITE");
   if (!(c->temperature > 0)) return fail(IS_ERR_CONFIG, "temperature must be > 0");
@@ -389,7 +389,6 @@ struct is_ctx {
   float* resid;
   __nv_bfloat16 *xn, *attn, *act, *q;
   float *part_o, *part_ml;
-  int32_t* attn_cnt;
   int32_t* attn_items;
   float* splitk_ws;  // split-K partials workspace
   int NC, nc_pre, nc_suf;
@@ -469,7 +468,7 @@ static SchedArgs sched_args(is_ctx* c) {
   a.Hkv = c->sh.n_kv_heads;
   a.nc_pre = c->nc_pre;
   a.nc_suf = c->nc_suf;
-  a.chunk = kAC;
+  a.chunk = kSC;
   return a;
 }
 
@@ -538,52 +537,50 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
       if (prefill || !(g_skip & 2)) CKS(launch_gemm<EPI_QKV>(BN, w.tm_qkv, tm_xn, a, st));
     }
     prof_mark(st, 1);
-    AttnArgs aa;
+    AttnArgs aa{};
     aa.q = c->q;
     aa.kpre = c->prefix + l * prefix_layer;
     aa.vpre = aa.kpre + (size_t)Hkv * c->pcap * kHD;
     aa.pool = c->pool + l * pool_layer;
-    aa.pagetab = c->pagetab;
     aa.row_active = c->row_active;
-    aa.row_lid = c->row_lid;
     aa.row_len = c->row_len;
     aa.part_o = c->part_o;
     aa.part_ml = c->part_ml;
+    aa.items = c->attn_items;
+    aa.n_items = c->st_dev + ST_ATTN_ITEMS;
+    aa.dbg_ts = nullptr;
+    if (g_tl && l < 4) aa.dbg_ts = g_tl + (size_t)(400 + 4 * l) * 296 * 16;
+    aa.out = c->attn;
     aa.rows = rows;
     aa.Hq = Hq;
     aa.Hkv = Hkv;
     aa.pcap = c->pcap;
     aa.plen = c->pcap;
     aa.pt = c->pt;
-    aa.maxp = c->maxp;
     aa.nc_pre = c->nc_pre;
     aa.nc_suf = prefill ? 0 : c->nc_suf;
     aa.NC = c->NC;
     aa.prefill = prefill ? 1 : 0;
     aa.scale = 1.0f / sqrtf((float)kHD);
-    aa.cnt = c->attn_cnt;
-    aa.out = c->attn;
-    aa.items = c->attn_items;
-    aa.dbg_ts = nullptr;
-    if (g_tl && l < 4) aa.dbg_ts = g_tl + (size_t)(400 + l) * 296 * 16;
-    aa.n_pf = 0;
-    if (!prefill && c->l2_prefetch) {
-      aa.pf_ptr[0] = reinterpret_cast<const uint8_t*>(w.wo);
-      aa.pf_bytes[0] = (long long)H * Hq * 128 * 2;
-      aa.pf_ptr[1] = reinterpret_cast<const uint8_t*>(w.wgu);
-      aa.pf_bytes[1] = (long long)2 * F * H * 2;
-      aa.pf_ptr[2] = reinterpret_cast<const uint8_t*>(w.wd);
-      aa.pf_bytes[2] = (long long)H * F * 2;
-      aa.n_pf = c->l2_prefetch >= 2 ? 3 : 2;
-    }
-    aa.n_items = c->st_dev + ST_ATTN_ITEMS;
-    const int nblk = prefill ? Hkv * aa.nc_pre : 2 * g_num_sms;
+    const int nblk = prefill ? Hkv * aa.nc_pre * (int)ceil_div64(rows, kAttnWarps) : 4 * g_num_sms;
+    const bool do_attn = prefill || !(g_skip & 8);
+#define IS_ATTN_LAUNCH(R)                                                                                      \
+  do {                                                                                                         \
+    if (do_attn) CKS(launch_k_smem(attn_kernel<R>, dim3(nblk), dim3(kAttnThreads), AttnSmem<R>::v, st, aa)); \
+    if (do_attn && getenv("IS_ATTN_TWICE")) {                                                                 \
+      AttnArgs a2 = aa;                                                                                        \
+      if (a2.dbg_ts) a2.dbg_ts += (size_t)2 * 296 * 16;                                                       \
+      CKS(launch_k_smem(attn_kernel<R>, dim3(nblk), dim3(kAttnThreads), AttnSmem<R>::v, st, a2));            \
+    }                                                                                                          \
+    if (do_attn) CKS(launch_k(attn_merge_kernel<R>, dim3(rows, Hkv), dim3(32), st, aa));                      \
+  } while (0)
     switch (Hq / Hkv) {
-      case 1: if (prefill || !(g_skip & 8)) CKS(launch_k_smem(attn_kernel<1>, dim3(nblk), dim3(kAttnThreads), AttnSmem<1>::v, st, aa)); break;
-      case 2: if (prefill || !(g_skip & 8)) CKS(launch_k_smem(attn_kernel<2>, dim3(nblk), dim3(kAttnThreads), AttnSmem<2>::v, st, aa)); break;
-      case 4: if (prefill || !(g_skip & 8)) CKS(launch_k_smem(attn_kernel<4>, dim3(nblk), dim3(kAttnThreads), AttnSmem<4>::v, st, aa)); break;
-      default: if (prefill || !(g_skip & 8)) CKS(launch_k_smem(attn_kernel<8>, dim3(nblk), dim3(kAttnThreads), AttnSmem<8>::v, st, aa)); break;
+      case 1: IS_ATTN_LAUNCH(1); break;
+      case 2: IS_ATTN_LAUNCH(2); break;
+      case 4: IS_ATTN_LAUNCH(4); break;
+      default: IS_ATTN_LAUNCH(8); break;
     }
+#undef IS_ATTN_LAUNCH
     prof_mark(st, 3);
     for (int r0 = 0; r0 < rows; r0 += chunk) {
       GemmArgs a{};
@@ -753,7 +750,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->max_rows = std::max(c->rc, (int)ceil_div64(c->pcap, 64) * 64);
   c->max_pos = c->P + c->max_new + 1;
   c->nc_pre = (int)ceil_div64(c->pcap, kPC);
-  c->nc_suf = (int)ceil_div64(c->max_new, kAC);
+  c->nc_suf = (int)ceil_div64(c->max_new, kSC);
   c->NC = c->nc_pre + c->nc_suf;
   if (c->NC > 32 || s.n_q_heads / s.n_kv_heads > kMaxRep) {
     const int nc = c->NC;
@@ -830,9 +827,8 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->q = (__nv_bfloat16*)A((size_t)R * Hq * 128 * 2);
   c->part_o = (float*)A((size_t)R * Hq * c->NC * 128 * 4);
   c->part_ml = (float*)A((size_t)R * Hq * c->NC * 2 * 4);
-  c->attn_cnt = (int32_t*)A((size_t)R * Hkv * 4);
   c->splitk_ws = (float*)A((size_t)2 * 160 * kBM * 64 * 4);
-  c->attn_items = (int32_t*)A((size_t)Hkv * (c->nc_pre + c->rc * c->nc_suf) * 4 + 64);
+  c->attn_items = (int32_t*)A((size_t)Hkv * (c->nc_pre * ((c->rc + 3) / 4) + c->rc * c->nc_suf) * kItemStride * 4 + 64);
   c->rope_cos = (float*)A((size_t)c->max_pos * 64 * 4);
   c->rope_sin = (float*)A((size_t)c->max_pos * 64 * 4);
   for (int32_t** p : {&c->row_active, &c->row_uid, &c->row_lid, &c->row_t, &c->row_tok, &c->row_pos,
@@ -897,7 +893,7 @@ extern "C" void is_destroy(is_ctx* c) {
   cudaStreamSynchronize(c->st);
   if (c->graph_ok) cudaGraphExecDestroy(c->graph);
   void* bufs[] = {c->wblob, c->final_norm, c->prefix, c->pool, c->resid, c->xn, c->attn, c->act, c->q,
-                  c->part_o, c->part_ml, c->attn_cnt, c->attn_items, c->splitk_ws, c->rope_cos, c->rope_sin, c->row_active, c->row_uid, c->row_lid,
+                  c->part_o, c->part_ml, c->attn_items, c->splitk_ws, c->rope_cos, c->rope_sin, c->row_active, c->row_uid, c->row_lid,
                   c->row_t, c->row_tok, c->row_pos, c->row_kvloc, c->row_len, c->keys, c->last_tok,
                   c->last_fin, c->st_dev, c->slot_uid, c->slot_count, c->tpos, c->true_len, c->queue,
                   c->main_init, c->main_queue, c->free_stack, c->pagetab, c->npages, c->tokens, c->log_slot,
@@ -1226,27 +1222,32 @@ extern "C" int is_dbg_timeline(is_ctx* c) {
            f(mn[10]), f(mx[10]), f(mn[11]), f(mx[11]));
   }
   for (int l = 0; l < 4; ++l) {
-    const unsigned long long* base = &h0[(size_t)(400 + l) * 296 * 16];
-    double st = 1e30, en = 0, dw = 0;
-    int n = 0;
-    std::vector<double> stg, part, fin;
-    for (int b = 0; b < 296; ++b) {
+    const unsigned long long* base = &h0[(size_t)(400 + 2 * l) * 296 * 16];
+    double st = 1e30, en = 0;
+    std::vector<double> pst[2], pcm[2], pend[2];
+    int nunits[4] = {0, 0, 0, 0};
+    for (int b = 0; b < 4 * 296; ++b) {
       const unsigned long long* p = base + b * 16;
       if (!p[0]) continue;
       st = std::min(st, (double)(p[0] - t0) / 1e3);
       en = std::max(en, (double)(p[15] - t0) / 1e3);
-      dw = std::max(dw, (double)(p[1] - t0) / 1e3);
-      if (p[2] && p[4]) {
-        ++n;
-        stg.push_back((double)(p[2] - p[1]) / 1e3);
-        part.push_back((double)(p[3] ? p[3] - p[2] : 0) / 1e3);
-        fin.push_back((double)(p[4] - (p[3] ? p[3] : p[2])) / 1e3);
+      int k = 0;
+      for (int nu = 0; nu < 3; ++nu) {
+        const unsigned long long* q = p + 1 + 4 * nu;
+        if (!q[0] || !q[2] || q[3] < 1 || q[3] > 2) break;
+        const int kind = (int)q[3] - 1;
+        pst[kind].push_back((double)(q[1] - q[0]) / 1e3);
+        pcm[kind].push_back((double)(q[2] - q[1]) / 1e3);
+        pend[kind].push_back((double)(q[2] - t0) / 1e3);
+        ++k;
       }
+      nunits[std::min(k, 3)]++;
     }
     auto med = [](std::vector<double> v) { if (v.empty()) return -1.0; std::sort(v.begin(), v.end()); return v[v.size() / 2]; };
     auto mx = [](std::vector<double> v) { if (v.empty()) return -1.0; return *std::max_element(v.begin(), v.end()); };
-    printf("attn L%d start %.2f waited %.2f end %.2f  items=%d  stage %.2f/%.2f  compute %.2f/%.2f  arrive+merge %.2f/%.2f\n", l, st, dw,
-           en, n, med(stg), mx(stg), med(part), mx(part), med(fin), mx(fin));
+    printf("%s L%d %.2f..%.2f  CTAs with 0/1/2/3 units: %d/%d/%d/%d | prefix n=%zu stage %.2f/%.2f compute %.2f/%.2f done<=%.2f | suffix n=%zu stage %.2f/%.2f compute %.2f/%.2f done<=%.2f\n",
+           (l & 1) ? "attn#2" : "attn", l / 2, st, en, nunits[0], nunits[1], nunits[2], nunits[3], pst[0].size(), med(pst[0]), mx(pst[0]), med(pcm[0]),
+           mx(pcm[0]), mx(pend[0]), pst[1].size(), med(pst[1]), mx(pst[1]), med(pcm[1]), mx(pcm[1]), mx(pend[1]));
   }
   fflush(stdout);
   return c->tl_count;

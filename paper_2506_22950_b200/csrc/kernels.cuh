@@ -64,41 +64,43 @@ __global__ void rmsnorm_kernel(const float* __restrict__ resid, const float* __r
 // ------------------------------------------------------------------ split attention
 // PAPER.md l.171-174 / l.205: every live slot attends to the prompt's shared
 // prefix KV (written once by prefill) and to its own paged response KV.  The
-// work is split at that boundary (R8):
-//   * prefix item  = (kv head, 128-token prefix chunk): the chunk is staged in
-//     shared memory ONCE and every live row of the group (x Hq/Hkv query heads)
-//     is scored against it -- the prefix is read once per group per step;
-//   * suffix item  = (row, kv head, 128-token chunk of that slot's pages): one
-//     warp, K rows read straight from the page pool (each lane owns 4 tokens,
-//     256-B contiguous rows), V read coalesced (lanes over head dims);
-// each item writes a normalised partial (o, m, l) per query head; the item that
-// completes a (row, kv head) -- a per-(row, head) arrival counter -- merges all
-// of its partials by log-sum-exp in fixed chunk order (prefix chunks, then
-// suffix chunks), so the result does not depend on arrival order.
-constexpr int kAC = 64;           // tokens per suffix chunk (one CTA)
+// work is split at that boundary (R8) and every part returns a normalised
+// partial (o, m, l) per query head:
+//   * prefix item = (kv head, kPC-token prefix chunk), one CTA: the chunk is
+//     DMA'd into shared memory ONCE and every live row of the group (x Hq/Hkv
+//     query heads) is scored against it -- the shared prefix is read once per
+//     group per step, not once per slot;
+//   * suffix item = (row, kv head, kSC-token chunk of that slot's pages), one
+//     WARP with its own smem slice; the scheduler embeds the chunk's page ids in
+//     the work item, so staging is one bulk DMA per (page, K|V) block.
+// attn_merge_kernel then combines each (row, query head)'s partials by
+// log-sum-exp in fixed order (prefix chunks, then suffix chunks).
+// K/V tiles are dense in smem (bulk copies cannot pad); K rows are read with
+// an XOR swizzle of the 16-byte chunk index (lane t reads chunk d8 ^ (t & 7)),
+// which makes the lane-per-token score loop bank-conflict free.
+// Loops stay rolled: this code runs cold out of the instruction cache once per
+// layer, so code length is latency.
 constexpr int kPC = 32;           // tokens per shared-prefix chunk (one CTA, all live rows)
+constexpr int kSC = 64;           // tokens per suffix chunk (one warp)
 constexpr int kMaxRep = 8;        // Hq / Hkv <= 8
+constexpr int kItemStride = 17;   // work item: code + up to 16 page ids
+constexpr int kAttnWarps = 4;
+constexpr int kAttnThreads = kAttnWarps * 32;
 
 struct AttnArgs {
   const __nv_bfloat16* q;     // [rows][Hq][128]
   const __nv_bfloat16* kpre;  // prefix K of this layer [Hkv][pcap][128]
   const __nv_bfloat16* vpre;  // prefix V               [Hkv][pcap][128]
   const __nv_bfloat16* pool;  // page pool of this layer [pages][2][Hkv][pt][128]
-  const int32_t* pagetab;     // [G][maxp]
   const int32_t* row_active;
-  const int32_t* row_lid;     // local sample id (page table row)
   const int32_t* row_len;     // suffix tokens visible (t + 1)
   float* part_o;              // [rows][Hq][NC][128] normalised partial outputs
   float* part_ml;             // [rows][Hq][NC][2]   (max score, sum exp)
-  int32_t* cnt;               // [rows][Hkv] arrival counters (left at 0)
-  const int32_t* items;       // decode work list (built by sched_kernel)
-  const uint8_t* pf_ptr[4];   // weights to pull into L2 while attention runs (latency-bound phase)
-  long long pf_bytes[4];
-  int n_pf;
-  unsigned long long* dbg_ts;  // optional [gridDim][16] globaltimer stamps
-  const long long* n_items;   // its length
+  const int32_t* items;       // decode work list (sched_kernel): prefix items, then suffix items
+  const long long* n_items;   // [2]: total items, prefix items
+  unsigned long long* dbg_ts; // optional [gridDim][16] globaltimer stamps
   __nv_bfloat16* out;         // [rows][Hq][128]
-  int rows, Hq, Hkv, pcap, plen, pt, maxp;
+  int rows, Hq, Hkv, pcap, plen, pt;
   int nc_pre, nc_suf, NC;
   int prefill;                // 1: rows are prompt positions, causal over the prefix, no suffix
   float scale;                // 1/sqrt(128)
@@ -112,136 +114,79 @@ __device__ __forceinline__ void astamp(const AttnArgs& a, int i) {
   }
 }
 
-__device__ __forceinline__ int attn_expected(const AttnArgs& a, int r) {
-  if (a.prefill) return min(a.nc_pre, r / kPC + 1);
-  return a.nc_pre + (a.row_len[r] + kAC - 1) / kAC;
+// 1-D bulk DMA global -> shared, completion (bytes) on an mbarrier.
+IS_DEVICE void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem)),
+               "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
-// Warp-level LSE merge of all partials of (row r, kv head h) -> bf16 output.
-// Lane i holds partial i's (m, l) (<= 32 partials); the o loads are independent.
-__device__ void attn_merge_warp(const AttnArgs& a, int r, int h, int lane) {
-  const int rep = a.Hq / a.Hkv;
-  const int npre = a.prefill ? min(a.nc_pre, r / kPC + 1) : a.nc_pre;
-  const int nsuf = a.prefill ? 0 : (a.row_len[r] + kAC - 1) / kAC;
-  const int n = npre + nsuf;
-  const int my_slot = lane < npre ? lane : a.nc_pre + (lane - npre);
-  for (int j = 0; j < rep; ++j) {
-    const int qh = h * rep + j;
-    const size_t base = ((size_t)r * a.Hq + qh) * a.NC;
-    float mi = -INFINITY, li = 0.f;
-    if (lane < n) {
-      const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (base + my_slot) * 2));
-      mi = ml.x;
-      li = ml.y;
-    }
-    const float M = warp_max(mi);
-    const float wi = (lane < n && mi != -INFINITY) ? expf(mi - M) * li : 0.f;
-    const float den = warp_sum(wi);
-    float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-    for (int i = 0; i < n; ++i) {
-      const float w = __shfl_sync(0xffffffffu, wi, i);
-      const int slot = i < npre ? i : a.nc_pre + (i - npre);
-      if (w != 0.f) {
-        const float4 o = __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + slot) * kHD) + lane);
-        num.x += w * o.x;
-        num.y += w * o.y;
-        num.z += w * o.z;
-        num.w += w * o.w;
-      }
-    }
-    const float inv = 1.0f / den;
-    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(a.out + ((size_t)r * a.Hq + qh) * kHD) + 2 * lane;
-    o2[0] = __floats2bfloat162_rn(num.x * inv, num.y * inv);
-    o2[1] = __floats2bfloat162_rn(num.z * inv, num.w * inv);
+// q row r, heads h*REP.. -> smem fp32 [REP][128] (one 8-byte load per lane per head)
+template <int REP>
+__device__ __forceinline__ void attn_load_q(const AttnArgs& a, int r, int h, float* qs, int lane) {
+  uint2 b[REP];
+#pragma unroll
+  for (int e = 0; e < REP; ++e) b[e] = reinterpret_cast<const uint2*>(a.q + ((size_t)r * a.Hq + h * REP + e) * kHD)[lane];
+#pragma unroll
+  for (int e = 0; e < REP; ++e) {
+    const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b[e].x));
+    const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b[e].y));
+    reinterpret_cast<float4*>(qs + e * kHD)[lane] = make_float4(f0.x, f0.y, f1.x, f1.y);
   }
 }
 
-// Signal one more partial for (r, h); the completing warp merges.  Called by one full warp.
-__device__ __forceinline__ void attn_arrive(const AttnArgs& a, int r, int h, int lane) {
-  __threadfence();
-  int old = 0;
-  if (lane == 0) old = atomicAdd(a.cnt + r * a.Hkv + h, 1);
-  old = __shfl_sync(0xffffffffu, old, 0);
-  if (old == attn_expected(a, r) - 1) {
-    __threadfence();
-    attn_merge_warp(a, r, h, lane);
-    if (lane == 0) a.cnt[r * a.Hkv + h] = 0;
-  }
-}
-
-// Scores + softmax + P.V of one (row, kv head) against ntok tokens.  kp(tok)
-// returns a pointer to K row tok (128 bf16), vp(tok) to V row tok.  Writes the
-// partial of query heads h*REP .. h*REP+REP-1 into chunk slot `slot`.
-// REP = Hq/Hkv is a template parameter and loops are only lightly unrolled:
-// the code must stay small (the attention kernel runs cold out of the
-// instruction cache once per layer).
-template <int REP, typename KP, typename VP>
-__device__ __forceinline__ void attn_rows_chunk(const AttnArgs& a, int r, int h, int slot, int ntok, const float* qs,
-                                                KP kp, VP vp, int lane) {
-  float s[4][REP];
-#pragma unroll 1
-  for (int j = 0; j < 4; ++j) {
-    const int tk = lane + 32 * j;
+// Partial (m, l, o[REP][4 dims per lane]) of REP query heads over `ntok` dense
+// K / V rows in shared memory, one warp.  TPL = tokens per lane-group: with
+// ntok <= 32 each lane owns one token (TPL = 1); with ntok <= 16 two lanes
+// share a token, each dotting half of the head dims (TPL = 2).  K chunks are
+// read XOR-swizzled (chunk d8 ^ (token & 7)) -> conflict-free.
+template <int REP, int LPT>
+struct WarpPartial {
+  float m[REP], l[REP], o[REP][4];
+  __device__ __forceinline__ void run(const float* qs, const __nv_bfloat16* Ks, const __nv_bfloat16* Vs, int ntok,
+                                      float scale, int lane) {
+    constexpr int TOK = 32 / LPT;             // tokens covered by the warp
+    const int tk = lane / LPT, part = lane % LPT;
     float acc[REP];
 #pragma unroll
     for (int e = 0; e < REP; ++e) acc[e] = 0.f;
     if (tk < ntok) {
-      const uint4* k4 = reinterpret_cast<const uint4*>(kp(tk));
+      const uint4* k4 = reinterpret_cast<const uint4*>(Ks + tk * kHD);
 #pragma unroll 2
-      for (int d8 = 0; d8 < kHD / 8; ++d8) {
-        const uint4 kv = k4[d8];
+      for (int i = 0; i < 16 / LPT; ++i) {
+        const int d8 = part * (16 / LPT) + i;
+        const int cc = d8 ^ (tk & 7);
+        const uint4 kv = k4[cc];
         const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kv);
         const float2 f0 = __bfloat1622float2(k2[0]), f1 = __bfloat1622float2(k2[1]);
         const float2 f2 = __bfloat1622float2(k2[2]), f3 = __bfloat1622float2(k2[3]);
 #pragma unroll
         for (int e = 0; e < REP; ++e) {
-          const float4 qa = *reinterpret_cast<const float4*>(qs + e * kHD + d8 * 8);
-          const float4 qb = *reinterpret_cast<const float4*>(qs + e * kHD + d8 * 8 + 4);
+          const float4 qa = *reinterpret_cast<const float4*>(qs + e * kHD + cc * 8);
+          const float4 qb = *reinterpret_cast<const float4*>(qs + e * kHD + cc * 8 + 4);
           acc[e] += qa.x * f0.x + qa.y * f0.y + qa.z * f1.x + qa.w * f1.y + qb.x * f2.x + qb.y * f2.y +
                     qb.z * f3.x + qb.w * f3.y;
         }
       }
     }
+    float p[REP];
 #pragma unroll
     for (int e = 0; e < REP; ++e) {
-      const float v = tk < ntok ? acc[e] * a.scale : -INFINITY;
-      if (j == 0) s[0][e] = v;
-      else if (j == 1) s[1][e] = v;
-      else if (j == 2) s[2][e] = v;
-      else s[3][e] = v;
+      if (LPT == 2) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 1);
+      const float sc = tk < ntok ? acc[e] * scale : -INFINITY;
+      m[e] = warp_max(sc);
+      p[e] = sc == -INFINITY ? 0.f : expf(sc - m[e]);
+      l[e] = warp_sum(p[e]) / (float)LPT;
+      o[e][0] = o[e][1] = o[e][2] = o[e][3] = 0.f;
     }
-  }
-  float m[REP], l[REP];
-#pragma unroll
-  for (int e = 0; e < REP; ++e) {
-    m[e] = warp_max(fmaxf(fmaxf(s[0][e], s[1][e]), fmaxf(s[2][e], s[3][e])));
-    float ps = 0.f;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      s[j][e] = s[j][e] == -INFINITY ? 0.f : expf(s[j][e] - m[e]);
-      ps += s[j][e];
-    }
-    l[e] = warp_sum(ps);
-  }
-  float o[REP][4];
-#pragma unroll
-  for (int e = 0; e < REP; ++e) o[e][0] = o[e][1] = o[e][2] = o[e][3] = 0.f;
-#pragma unroll 1
-  for (int j = 0; j < 4; ++j) {
-    const int t0 = 32 * j;
-    if (t0 >= ntok) break;
-    float pj[REP];
-#pragma unroll
-    for (int e = 0; e < REP; ++e) pj[e] = j == 0 ? s[0][e] : j == 1 ? s[1][e] : j == 2 ? s[2][e] : s[3][e];
-    const int nt = min(32, ntok - t0);
 #pragma unroll 4
-    for (int u = 0; u < nt; ++u) {
-      const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(vp(t0 + u)) + 2 * lane;
+    for (int u = 0; u < min(ntok, TOK); ++u) {
+      const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(Vs + u * kHD) + 2 * lane;
       const float2 a0 = __bfloat1622float2(v2[0]), a1 = __bfloat1622float2(v2[1]);
 #pragma unroll
       for (int e = 0; e < REP; ++e) {
-        const float pv = __shfl_sync(0xffffffffu, pj[e], u);
+        const float pv = __shfl_sync(0xffffffffu, p[e], u * LPT);
         o[e][0] += pv * a0.x;
         o[e][1] += pv * a0.y;
         o[e][2] += pv * a1.x;
@@ -249,251 +194,211 @@ __device__ __forceinline__ void attn_rows_chunk(const AttnArgs& a, int r, int h,
       }
     }
   }
+};
+
+template <int REP>
+__device__ __forceinline__ void store_partial(const AttnArgs& a, int r, int h, int slot, const float (&m)[REP],
+                                              const float (&l)[REP], const float (&o)[REP][4], int lane) {
 #pragma unroll
   for (int e = 0; e < REP; ++e) {
     const size_t pidx = ((size_t)r * a.Hq + h * REP + e) * a.NC + slot;
     const float inv = 1.0f / l[e];
     reinterpret_cast<float4*>(a.part_o + pidx * kHD)[lane] =
         make_float4(o[e][0] * inv, o[e][1] * inv, o[e][2] * inv, o[e][3] * inv);
-    if (lane == 0) {
-      a.part_ml[pidx * 2] = m[e];
-      a.part_ml[pidx * 2 + 1] = l[e];
-    }
+    if (lane == 0) *reinterpret_cast<float2*>(a.part_ml + pidx * 2) = make_float2(m[e], l[e]);
   }
 }
 
-constexpr int kAttnThreads = 256;
-// K, V chunk + per-warp q (prefix path) / q, p, reductions (suffix path)
+// smem per CTA: K [64][128] + V [64][128] (bf16, dense) + q [4][REP][128] fp32
+// + combine scratch [4][REP][2 + 128] fp32 + DMA barrier.
 template <int REP>
 struct AttnSmem {
-  static constexpr int v = 2 * kAC * kKPad * 2 + 8 * (REP < 2 ? 2 : REP) * kHD * 4;
+  static constexpr int kKV = 2 * kSC * kHD * 2;
+  static constexpr int kQ = kAttnWarps * REP * kHD * 4;
+  static constexpr int kComb = kAttnWarps * REP * (kHD + 2) * 4;
+  static constexpr int v = kKV + kQ + kComb + 64;
 };
 
-// One work item: a shared-prefix chunk (is_pre) or one slot's suffix chunk.
-template <int REP>
-__device__ __forceinline__ void attn_item(const AttnArgs& a, bool is_pre, int h, int c, int r_item, uint8_t* asmem,
-                                          int sb) {
-  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(asmem);
-  __nv_bfloat16* Vs = Ks + kAC * kKPad;
-  float* qbuf = reinterpret_cast<float*>(Vs + kAC * kKPad);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int rep = REP;
-  float* qs = qbuf + warp * (REP < 2 ? 2 : REP) * kHD;
-  auto load_q = [&](int r, int h) {
-    for (int e = 0; e < rep; ++e) {
-      const __nv_bfloat16* qp = a.q + ((size_t)r * a.Hq + h * rep + e) * kHD;
-      const float2 f = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(qp)[lane]);
-      const float2 g2 = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(qp)[lane + 32]);
-      qs[e * kHD + 2 * lane] = f.x;
-      qs[e * kHD + 2 * lane + 1] = f.y;
-      qs[e * kHD + 64 + 2 * lane] = g2.x;
-      qs[e * kHD + 64 + 2 * lane + 1] = g2.y;
-    }
-    __syncwarp();
-  };
-  if (is_pre) {
-    // ---------------- shared-prefix chunk: staged once, scored by every live row
-    const int tok0 = c * kPC, ntok = min(kPC, a.plen - tok0);
-    {
-      constexpr int NJ = kPC * (kHD / 8) / kAttnThreads;
-      uint4 kk[NJ], vv[NJ];
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) {
-        const int i = threadIdx.x + j * kAttnThreads;
-        const int tk = i >> 4, seg = i & 15;
-        kk[j] = vv[j] = make_uint4(0, 0, 0, 0);
-        if (tk < ntok) {
-          kk[j] = __ldg(reinterpret_cast<const uint4*>(a.kpre + ((size_t)h * a.pcap + tok0 + tk) * kHD + seg * 8));
-          vv[j] = __ldg(reinterpret_cast<const uint4*>(a.vpre + ((size_t)h * a.pcap + tok0 + tk) * kHD + seg * 8));
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) {
-        const int i = threadIdx.x + j * kAttnThreads;
-        const int tk = i >> 4, seg = i & 15;
-        *reinterpret_cast<uint4*>(Ks + tk * kKPad + seg * 8) = kk[j];
-        *reinterpret_cast<uint4*>(Vs + tk * kKPad + seg * 8) = vv[j];
-      }
-    }
-    __syncthreads();
-    astamp(a, sb);
-    for (int r = warp; r < a.rows; r += kAttnThreads / 32) {
-      if (!a.row_active[r]) continue;
-      int valid = ntok;
-      if (a.prefill) valid = min(ntok, r + 1 - tok0);
-      if (valid <= 0) continue;
-      load_q(r, h);
-      attn_rows_chunk<REP>(a, r, h, c, valid, qs, [&](int tk) { return Ks + tk * kKPad; },
-                      [&](int tk) { return Vs + tk * kKPad; }, lane);
-      attn_arrive(a, r, h, lane);
-    }
-    return;
-  }
-  // ---------------- per-slot suffix chunk: one CTA per (row, kv head, chunk)
-  const int r = r_item;
-  const int len = a.row_len[r];
-  const int tok0 = c * kAC;
-  if (tok0 >= len) return;
-  const int ntok = min(kAC, len - tok0);
-  const int32_t* pt_row = a.pagetab + (size_t)a.row_lid[r] * a.maxp;
-  const size_t head_stride = (size_t)a.pt * kHD;
-  // stage: every thread issues all of its 16-B loads before storing (8 K + 8 V pieces)
-  {
-    constexpr int NJ = kAC * (kHD / 8) / kAttnThreads;
-    uint4 kk[NJ], vv[NJ];
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-      const int i = threadIdx.x + j * kAttnThreads;  // kAC tokens x 16 pieces
-      const int tk = i >> 4, seg = i & 15;
-      kk[j] = vv[j] = make_uint4(0, 0, 0, 0);
-      if (tk < ntok) {
-        const int tok = tok0 + tk;
-        const int page = __ldg(pt_row + tok / a.pt);
-        const size_t base = (((size_t)page * 2) * a.Hkv + h) * head_stride + (size_t)(tok % a.pt) * kHD + seg * 8;
-        kk[j] = __ldg(reinterpret_cast<const uint4*>(a.pool + base));
-        vv[j] = __ldg(reinterpret_cast<const uint4*>(a.pool + base + (size_t)a.Hkv * head_stride));
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-      const int i = threadIdx.x + j * kAttnThreads;
-      const int tk = i >> 4, seg = i & 15;
-      *reinterpret_cast<uint4*>(Ks + tk * kKPad + seg * 8) = kk[j];
-      *reinterpret_cast<uint4*>(Vs + tk * kKPad + seg * 8) = vv[j];
-    }
-  }
-  float* qsm = qbuf;                      // [rep][128]
-  float* psm = qbuf + REP * kHD;          // [rep][128]
-  float* red = psm + REP * kHD;           // [2][4][kMaxRep]
-  for (int i = threadIdx.x; i < rep * kHD; i += kAttnThreads)
-    qsm[i] = __bfloat162float(a.q[((size_t)r * a.Hq + h * rep) * kHD + i]);
-  __syncthreads();
-  astamp(a, sb);
-  // scores: thread t < 128 owns token t
-  const int t = threadIdx.x;
-  float sc[REP];
-#pragma unroll
-  for (int e = 0; e < REP; ++e) sc[e] = -INFINITY;
-  if (t < kAC) {
-    float acc[REP];
-#pragma unroll
-    for (int e = 0; e < REP; ++e) acc[e] = 0.f;
-    const uint4* k4 = reinterpret_cast<const uint4*>(Ks + t * kKPad);
-#pragma unroll 2
-    for (int d8 = 0; d8 < kHD / 8; ++d8) {
-      const uint4 kv = k4[d8];
-      const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kv);
-      const float2 f0 = __bfloat1622float2(k2[0]), f1 = __bfloat1622float2(k2[1]);
-      const float2 f2 = __bfloat1622float2(k2[2]), f3 = __bfloat1622float2(k2[3]);
-#pragma unroll
-      for (int e = 0; e < REP; ++e) {
-        if (e < rep) {
-          const float4 qa = *reinterpret_cast<const float4*>(qsm + e * kHD + d8 * 8);
-          const float4 qb = *reinterpret_cast<const float4*>(qsm + e * kHD + d8 * 8 + 4);
-          acc[e] += qa.x * f0.x + qa.y * f0.y + qa.z * f1.x + qa.w * f1.y + qb.x * f2.x + qb.y * f2.y +
-                    qb.z * f3.x + qb.w * f3.y;
-        }
-      }
-    }
-    if (t < ntok) {
-#pragma unroll
-      for (int e = 0; e < REP; ++e) sc[e] = acc[e] * a.scale;
-    }
-  }
-  // block max / sum over the 128 token threads (warps 0..3)
-#pragma unroll
-  for (int e = 0; e < REP; ++e)
-    if (e < rep) {
-      const float mw = warp_max(sc[e]);
-      if (lane == 0 && warp < 4) red[warp * kMaxRep + e] = mw;
-    }
-  __syncthreads();
-  float mrow[REP];
-#pragma unroll
-  for (int e = 0; e < REP; ++e)
-    mrow[e] = fmaxf(fmaxf(red[0 * kMaxRep + e], red[1 * kMaxRep + e]), fmaxf(red[2 * kMaxRep + e], red[3 * kMaxRep + e]));
-  float* red2 = red + 4 * kMaxRep;
-#pragma unroll
-  for (int e = 0; e < REP; ++e)
-    if (e < rep) {
-      const float p = (t < ntok) ? expf(sc[e] - mrow[e]) : 0.f;
-      if (t < kAC) psm[e * kHD + t] = p;
-      const float sw = warp_sum(p);
-      if (lane == 0 && warp < 4) red2[warp * kMaxRep + e] = sw;
-    }
-  __syncthreads();
-  // P.V: outputs (e, d) spread over the CTA
-  for (int idx = threadIdx.x; idx < rep * kHD; idx += kAttnThreads) {
-    const int e = idx / kHD, d = idx % kHD;
-    float o = 0.f;
-    const float* pe = psm + e * kHD;
-#pragma unroll 8
-    for (int tk = 0; tk < ntok; ++tk) o += pe[tk] * __bfloat162float(Vs[tk * kKPad + d]);
-    const float l = red2[0 * kMaxRep + e] + red2[1 * kMaxRep + e] + red2[2 * kMaxRep + e] + red2[3 * kMaxRep + e];
-    const size_t pidx = ((size_t)r * a.Hq + h * rep + e) * a.NC + a.nc_pre + c;
-    a.part_o[pidx * kHD + d] = o / l;
-    if (d == 0) {
-      a.part_ml[pidx * 2] = mrow[e];
-      a.part_ml[pidx * 2 + 1] = l;
-    }
-  }
-  __syncthreads();
-  astamp(a, sb + 1);
-  if (warp == 0) attn_arrive(a, r, h, lane);
-}
-
-
-// Persistent over the work list: decode items come from sched_kernel (prefix
-// chunks first, then every live slot's chunks); prefill items are the prefix
-// chunks (causal).  Items never span a CTA boundary, so the merge counters see
-// each (row, head) partial exactly once.
+// Work units (persistent grid, ~4 CTAs per SM):
+//   prefix (h, c, g): DMA the kPC-token prefix chunk once; warp w scores row
+//                     4g + w (all of its REP heads) -> partial slot c;
+//   suffix (r, h, c): DMA the slot's kSC-token chunk (<= 4 pages); warp w takes
+//                     page w (16 tokens, two lanes per token) and the 4 warp
+//                     partials are combined in smem -> partial slot nc_pre + c.
 template <int REP>
 __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnArgs a) {
-  pdl_launch_dependents();  // let the next kernel launch and prefetch now; it waits for our completion itself
-  pdl_wait();
-  extern __shared__ __align__(16) uint8_t asmem[];
-  astamp(a, 0);
-  if (threadIdx.x == 0 && a.n_pf > 0) {
-    // Attention moves ~1% of the step's bytes and is latency-bound: use it to
-    // pull the next GEMMs' weights into L2 (cp.async.bulk.prefetch, no smem).
-    long long tot = 0;
-    for (int i = 0; i < a.n_pf; ++i) tot += a.pf_bytes[i];
-    const long long per = ((tot / gridDim.x) + 4095) & ~4095ll;
-    long long lo = (long long)blockIdx.x * per, hi = min(tot, lo + per);
-    long long base = 0;
-    for (int i = 0; i < a.n_pf && lo < hi; ++i) {
-      const long long e0 = base, e1 = base + a.pf_bytes[i];
-      const long long s0 = max(lo, e0), s1 = min(hi, e1);
-      for (long long o = s0; o < s1; o += 32768) {
-        const unsigned sz = (unsigned)min(32768ll, s1 - o);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf_ptr[i] + (o - e0)), "r"(sz) : "memory");
-      }
-      base = e1;
-    }
+  pdl_launch_dependents();
+  extern __shared__ __align__(128) uint8_t asmem[];
+  using SM = AttnSmem<REP>;
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(asmem);
+  __nv_bfloat16* Vs = Ks + kSC * kHD;
+  float* qs_all = reinterpret_cast<float*>(asmem + SM::kKV);
+  float* comb = reinterpret_cast<float*>(asmem + SM::kKV + SM::kQ);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(asmem + SM::kKV + SM::kQ + SM::kComb);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* qs = qs_all + warp * REP * kHD;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
   }
-  const int n = a.prefill ? a.Hkv * a.nc_pre : (int)*a.n_items;
-  astamp(a, 1);
-  int nit = 0;
-  for (int it = blockIdx.x; it < n; it += gridDim.x) {
+  __syncthreads();
+  pdl_wait();
+  astamp(a, 0);
+  const int n = a.prefill ? a.Hkv * a.nc_pre * ((a.rows + kAttnWarps - 1) / kAttnWarps) : (int)a.n_items[0];
+  uint32_t phase = 0;
+  int nu = 0;
+#pragma unroll 1
+  for (int u = blockIdx.x; u < n; u += gridDim.x, ++nu) {
+    if (nu < 3) astamp(a, 1 + 4 * nu);
     int code;
-    if (a.prefill) code = (int)(0x80000000u | ((it / a.nc_pre) << 8) | (it % a.nc_pre));
-    else code = a.items[it];
-    const bool is_pre = code < 0;
-    int h, c, r = -1;
-    if (is_pre) {
-      h = (code >> 8) & 0xFF;
-      c = code & 0xFF;
+    if (a.prefill) {
+      const int ng = (a.rows + kAttnWarps - 1) / kAttnWarps;
+      code = (int)(0x80000000u | ((u / (a.nc_pre * ng)) << 16) | (((u / ng) % a.nc_pre) << 8) | (u % ng));
     } else {
-      c = (code >> 16) & 0xFF;
-      r = (code >> 8) & 0xFF;
-      h = code & 0xFF;
+      code = a.items[(size_t)u * kItemStride];
     }
-    attn_item<REP>(a, is_pre, h, c, r, asmem, nit < 4 ? 2 + 3 * nit : 14);
-    __syncthreads();
-    if (nit < 4) astamp(a, 2 + 3 * nit + 2);
-    ++nit;
+    if (code < 0) {
+      // ---------------- shared-prefix chunk, one row per warp
+      const int h = (code >> 16) & 0xFF, c = (code >> 8) & 0xFF, g = code & 0xFF;
+      const int tok0 = c * kPC, ntok = min(kPC, a.plen - tok0);
+      if (threadIdx.x == 0) {
+        const uint32_t bytes = (uint32_t)ntok * kHD * 2;
+        mbar_arrive_expect_tx(bar, 2 * bytes);
+        bulk_g2s(Ks, a.kpre + ((size_t)h * a.pcap + tok0) * kHD, bytes, bar);
+        bulk_g2s(Vs, a.vpre + ((size_t)h * a.pcap + tok0) * kHD, bytes, bar);
+      }
+      const int r = g * kAttnWarps + warp;
+      const bool act = r < a.rows && a.row_active[r];
+      const int valid = act ? (a.prefill ? min(ntok, r + 1 - tok0) : ntok) : 0;
+      if (valid > 0) attn_load_q<REP>(a, r, h, qs, lane);
+      __syncwarp();
+      mbar_wait(bar, phase);
+      if (nu < 3) astamp(a, 2 + 4 * nu);
+      if (valid > 0) {
+        WarpPartial<REP, 1> wp;
+        wp.run(qs, Ks, Vs, valid, a.scale, lane);
+        store_partial<REP>(a, r, h, c, wp.m, wp.l, wp.o, lane);
+      }
+    } else {
+      // ---------------- per-slot suffix chunk, one page per warp
+      const int c = (code >> 16) & 0xFF, r = (code >> 8) & 0xFF, h = code & 0xFF;
+      const int32_t* item = a.items + (size_t)u * kItemStride;
+      const int page_l = lane < 16 ? item[1 + lane] : 0;
+      const int tok0 = c * kSC, ntok = min(kSC, a.row_len[r] - tok0);
+      const int npg = (ntok + a.pt - 1) / a.pt;
+      const size_t hs = (size_t)a.pt * kHD;
+      if (warp == 0) {
+        if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)ntok * kHD * 2 * 2);
+        __syncwarp();
+        if (lane < npg) {
+          const uint32_t bytes = (uint32_t)min(a.pt, ntok - lane * a.pt) * kHD * 2;
+          const __nv_bfloat16* kb = a.pool + (((size_t)page_l * 2) * a.Hkv + h) * hs;
+          bulk_g2s(Ks + lane * a.pt * kHD, kb, bytes, bar);
+          bulk_g2s(Vs + lane * a.pt * kHD, kb + (size_t)a.Hkv * hs, bytes, bar);
+        }
+      }
+      attn_load_q<REP>(a, r, h, qs, lane);
+      __syncwarp();
+      mbar_wait(bar, phase);
+      if (nu < 3) astamp(a, 2 + 4 * nu);
+      const int wt0 = warp * 16;  // this warp's 16 tokens
+      const int wn = max(0, min(16, ntok - wt0));
+      WarpPartial<REP, 2> wp;
+      if (wn > 0) wp.run(qs, Ks + wt0 * kHD, Vs + wt0 * kHD, wn, a.scale, lane);
+      // combine the warps' partials (fixed warp order)
+      float* cw = comb + warp * REP * (kHD + 2);
+#pragma unroll
+      for (int e = 0; e < REP; ++e) {
+        if (lane == 0) {
+          cw[e * (kHD + 2)] = wn > 0 ? wp.m[e] : -INFINITY;
+          cw[e * (kHD + 2) + 1] = wn > 0 ? wp.l[e] : 0.f;
+        }
+        float* oo = cw + e * (kHD + 2) + 2;
+        oo[4 * lane] = wn > 0 ? wp.o[e][0] : 0.f;
+        oo[4 * lane + 1] = wn > 0 ? wp.o[e][1] : 0.f;
+        oo[4 * lane + 2] = wn > 0 ? wp.o[e][2] : 0.f;
+        oo[4 * lane + 3] = wn > 0 ? wp.o[e][3] : 0.f;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        float M[REP], L[REP], O[REP][4];
+#pragma unroll
+        for (int e = 0; e < REP; ++e) {
+          M[e] = -INFINITY;
+          for (int w = 0; w < kAttnWarps; ++w) M[e] = fmaxf(M[e], comb[(w * REP + e) * (kHD + 2)]);
+          L[e] = 0.f;
+          O[e][0] = O[e][1] = O[e][2] = O[e][3] = 0.f;
+          for (int w = 0; w < kAttnWarps; ++w) {
+            const float* src = comb + (w * REP + e) * (kHD + 2);
+            if (src[0] == -INFINITY) continue;
+            const float f = expf(src[0] - M[e]);
+            L[e] += f * src[1];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) O[e][k] += f * src[2 + 4 * lane + k];
+          }
+        }
+        store_partial<REP>(a, r, h, a.nc_pre + c, M, L, O, lane);
+      }
+    }
+    __syncthreads();  // smem reuse by the next unit
+    phase ^= 1;
+    if (nu < 3) astamp(a, 3 + 4 * nu);
+    if (nu < 3 && threadIdx.x == 0 && a.dbg_ts) a.dbg_ts[blockIdx.x * 16 + 4 + 4 * nu] = (code < 0) ? 1 : 2;
   }
   astamp(a, 15);
+}
+
+// LSE merge (R8) of (row r, kv head h): grid (rows, Hkv), one warp.  Lane i
+// holds partial i's (m, l) (<= 32 partials); all o loads are issued together.
+template <int REP>
+__global__ void __launch_bounds__(32) attn_merge_kernel(AttnArgs a) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int r = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
+  if (!a.row_active[r]) return;
+  const int npre = a.prefill ? min(a.nc_pre, r / kPC + 1) : a.nc_pre;
+  const int nsuf = a.prefill ? 0 : (a.row_len[r] + kSC - 1) / kSC;
+  const int n = npre + nsuf;
+  const int my_slot = lane < npre ? lane : a.nc_pre + (lane - npre);
+#pragma unroll 1
+  for (int j = 0; j < REP; ++j) {
+    const int qh = h * REP + j;
+    const size_t base = ((size_t)r * a.Hq + qh) * a.NC;
+    float mi = -INFINITY, li = 0.f;
+    if (lane < n) {
+      const float2 ml = *reinterpret_cast<const float2*>(a.part_ml + (base + my_slot) * 2);
+      mi = ml.x;
+      li = ml.y;
+    }
+    const float M = warp_max(mi);
+    const float wi = (lane < n && mi != -INFINITY) ? expf(mi - M) * li : 0.f;
+    const float den = warp_sum(wi);
+    float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+    for (int i0 = 0; i0 < n; i0 += 8) {
+      float4 o[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + k;
+        const int slot = i < npre ? i : a.nc_pre + (i - npre);
+        o[k] = i < n ? reinterpret_cast<const float4*>(a.part_o + (base + slot) * kHD)[lane] : make_float4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float w = __shfl_sync(0xffffffffu, wi, (i0 + k) & 31);
+        if (i0 + k < n) {
+          num.x += w * o[k].x;
+          num.y += w * o[k].y;
+          num.z += w * o[k].z;
+          num.w += w * o[k].w;
+        }
+      }
+    }
+    const float inv = 1.0f / den;
+    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(a.out + ((size_t)r * a.Hq + qh) * kHD) + 2 * lane;
+    o2[0] = __floats2bfloat162_rn(num.x * inv, num.y * inv);
+    o2[1] = __floats2bfloat162_rn(num.z * inv, num.w * inv);
+  }
 }
 
 // ------------------------------------------------------------------ scheduler (Alg. 1 loop body, Alg. 3)
@@ -516,6 +421,7 @@ enum SchedState {
   ST_ERROR,
   ST_TOKENS,
   ST_ATTN_ITEMS,   // length of the attention work list for the next step
+  ST_ATTN_PRE,     // of which shared-prefix items (must follow ST_ATTN_ITEMS)
   ST_COUNT
 };
 
@@ -546,7 +452,7 @@ struct SchedArgs {
   int32_t* row_pos;
   int32_t* row_kvloc;
   int32_t* row_len;
-  int32_t* attn_items;       // [Hkv * (nc_pre + row_cap * nc_suf)]
+  int32_t* attn_items;       // [Hkv * (nc_pre + row_cap * nc_suf)][kItemStride]
   int Hkv, nc_pre, nc_suf, chunk;
 };
 
@@ -649,19 +555,35 @@ __global__ void sched_kernel(SchedArgs a, int consume) {
     a.row_kvloc[s] = a.pagetab[(size_t)uid * a.maxp + tt / a.pt] * a.pt + tt % a.pt;
     a.row_len[s] = tt + 1;
   }
-  // attention work list of the next step: shared-prefix chunks first (heavier:
-  // every live row), then each live slot's suffix chunks, chunk-major.
+  // attention work list of the next step: shared-prefix chunks first (one CTA
+  // each, all live rows), then every live slot's suffix chunks (one warp each,
+  // with the chunk's page ids embedded so the warp stages in one round trip).
   {
-    int n = 0;
+    int n = 0, npre = 0;
     if (any) {
-      for (int h = 0; h < a.Hkv; ++h)
-        for (int c = 0; c < a.nc_pre; ++c) a.attn_items[n++] = (int)(0x80000000u | (h << 8) | c);
+      // prefix units: (kv head, chunk, group of 4 rows) for groups holding a live row
+      for (int g = 0; g * 4 < a.row_cap; ++g) {
+        bool live = false;
+        for (int s = 4 * g; s < 4 * g + 4 && s < a.row_cap; ++s) live = live || a.row_active[s];
+        if (!live) continue;
+        for (int h = 0; h < a.Hkv; ++h)
+          for (int c = 0; c < a.nc_pre; ++c)
+            a.attn_items[(size_t)(n++) * kItemStride] = (int)(0x80000000u | (h << 16) | (c << 8) | g);
+      }
+      npre = n;
+      const int ppc = a.chunk / a.pt;  // pages per suffix chunk (<= 16)
       for (int c = 0; c < a.nc_suf; ++c)
         for (int s = 0; s < a.row_cap; ++s)
           if (a.row_active[s] && c * a.chunk < a.row_len[s])
-            for (int h = 0; h < a.Hkv; ++h) a.attn_items[n++] = (c << 16) | (s << 8) | h;
+            for (int h = 0; h < a.Hkv; ++h) {
+              int32_t* item = a.attn_items + (size_t)(n++) * kItemStride;
+              item[0] = (c << 16) | (s << 8) | h;
+              const int np = min(ppc, (a.row_len[s] - c * a.chunk + a.pt - 1) / a.pt);
+              for (int j = 0; j < np; ++j) item[1 + j] = a.pagetab[(size_t)a.row_lid[s] * a.maxp + c * ppc + j];
+            }
     }
     st[ST_ATTN_ITEMS] = n;
+    st[ST_ATTN_PRE] = npre;
   }
   if (any) {
     const long long step = st[ST_STEP];

@@ -1,0 +1,88 @@
+"""World-size-2 gloo test of the N>1 path on CPU: prompt sharding, the one
+all-gather of (length, reward), and W-invariance of the advantages
+(BASELINE north_star "NCCL ... only to all-gather completion
+lengths and rewards")."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import grpo
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _fake_group(pid, G):
+    """Deterministic stand-in for one rollout's (lengths, rewards) of prompt pid."""
+    rng = np.random.default_rng(1000 + pid)
+    return rng.integers(1, 1024, G).astype(np.int32), rng.random(G).astype(np.float32)
+
+
+def _worker(rank, world, port, n_prompts, G, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2506_22950_b200 import rollout
+    mine = rollout.shard_prompts(n_prompts, rank, world)
+    per_rank = -(-n_prompts // world)
+    lens = np.zeros(per_rank * G, np.int32)
+    rews = np.full(per_rank * G, np.nan, np.float32)
+    for k, pid in enumerate(mine):
+        l, r = _fake_group(pid, G)
+        lens[k * G:(k + 1) * G] = l
+        rews[k * G:(k + 1) * G] = r
+    all_l, all_r = rollout.gather_results(torch.from_numpy(lens), torch.from_numpy(rews))
+    all_l, all_r = all_l.numpy(), all_r.numpy()
+    # drop padding blocks, restore global prompt order
+    ids = [p for rk in range(world) for p in rollout.shard_prompts(n_prompts, rk, world)
+           + [-1] * (per_rank - len(rollout.shard_prompts(n_prompts, rk, world)))]
+    keep = [i for i, p in enumerate(ids) if p >= 0]
+    order = np.argsort([ids[i] for i in keep])
+    rew = np.concatenate([all_r[i * G:(i + 1) * G] for i in keep])
+    rew = rew.reshape(-1, G)[order].reshape(-1)
+    ln = np.concatenate([all_l[i * G:(i + 1) * G] for i in keep]).reshape(-1, G)[order].reshape(-1)
+    adv = rollout.group_advantages(rew, G)
+    q.put((rank, ln.tolist(), rew.tolist(), adv.tolist()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_prompts", [4, 5])
+def test_two_rank_gather_and_advantages_are_world_invariant(n_prompts):
+    G = 8
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_prompts, G, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # W = 1 reference
+    ref_l = np.concatenate([_fake_group(p, G)[0] for p in range(n_prompts)])
+    ref_r = np.concatenate([_fake_group(p, G)[1] for p in range(n_prompts)])
+    ref_a = np.concatenate([np.float32(grpo.advantages([float(x) for x in ref_r[i * G:(i + 1) * G]]))
+                            for i in range(n_prompts)])
+    for rank, ln, rw, adv in res:
+        assert ln == ref_l.tolist()
+        assert np.array_equal(np.float32(rw), ref_r)
+        assert np.array_equal(np.float32(adv), ref_a)
+
+
+def test_shard_prompts_partitions():
+    from paper_2506_22950_b200 import rollout
+    for n in range(0, 20):
+        for w in (1, 2, 3, 4, 8):
+            got = [p for r in range(w) for p in rollout.shard_prompts(n, r, w)]
+            assert got == list(range(n))

@@ -413,6 +413,9 @@ struct is_ctx {
   // splits
   int split_qkv, split_o, split_gu, split_d;
   int l2_prefetch;
+  int tc_prefix;       // decode prefix attention on tcgen05 (N = rc * Hq/Hkv in {16, 32, 64})
+  int nc_pre_dec;      // prefix partial slots in decode
+  CUtensorMap tm_prefix_kv;
   unsigned long long* timeline;  // debug: [launch][148 CTAs][16] GEMM stamps (IS_TIMELINE)
   int tl_count;
 };
@@ -466,9 +469,10 @@ static SchedArgs sched_args(is_ctx* c) {
   a.row_len = c->row_len;
   a.attn_items = c->attn_items;
   a.Hkv = c->sh.n_kv_heads;
-  a.nc_pre = c->nc_pre;
+  a.nc_pre = c->nc_pre_dec;
   a.nc_suf = c->nc_suf;
   a.chunk = kSC;
+  a.tc_prefix = c->tc_prefix;
   return a;
 }
 
@@ -485,6 +489,45 @@ static void prof_mark(cudaStream_t st, int kind) {
   cudaEventRecord(e, st);
   g_prof->ev->push_back(e);
   g_prof->kind->push_back(kind);
+}
+
+
+// Decode shared-prefix attention on tcgen05: one CTA per (kv head, 128-token tile).
+template <int REP, int N>
+static is_status launch_prefix_tc_n(is_ctx* c, const AttnArgs& aa, int l, cudaStream_t st) {
+  using SM = PrefixTcSmem<N>;
+  auto kern = attn_prefix_tc_kernel<REP, N>;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::v));
+    attr = true;
+  }
+  const int nt = (int)ceil_div64(c->pcap, 128);
+  const int kv_row_base = l * 2 * c->sh.n_kv_heads * c->pcap;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = dim3(c->sh.n_kv_heads * nt);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = SM::v;
+  cfg.stream = st;
+  cfg.numAttrs = 0;
+  if (g_use_pdl) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  CK(cudaLaunchKernelEx(&cfg, kern, c->tm_prefix_kv, aa, kv_row_base));
+  return IS_OK;
+}
+template <int REP>
+static is_status launch_prefix_tc(is_ctx* c, const AttnArgs& aa, int l, cudaStream_t st) {
+  switch (c->rc * REP) {
+    case 16: return launch_prefix_tc_n<REP, 16>(c, aa, l, st);
+    case 32: return launch_prefix_tc_n<REP, 32>(c, aa, l, st);
+    case 64: return launch_prefix_tc_n<REP, 64>(c, aa, l, st);
+  }
+  return fail(IS_ERR_CONFIG, "tcgen05 prefix attention needs row_capacity * Hq/Hkv in {16, 32, 64}");
 }
 
 // One layer stack over `rows` rows starting at row 0 (decode: rows = rc, BN = c->BN;
@@ -557,8 +600,9 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
     aa.pcap = c->pcap;
     aa.plen = c->pcap;
     aa.pt = c->pt;
-    aa.nc_pre = c->nc_pre;
+    aa.nc_pre = prefill ? c->nc_pre : c->nc_pre_dec;
     aa.nc_suf = prefill ? 0 : c->nc_suf;
+    aa.tc_prefix = prefill ? 0 : c->tc_prefix;
     aa.NC = c->NC;
     aa.prefill = prefill ? 1 : 0;
     aa.scale = 1.0f / sqrtf((float)kHD);
@@ -566,6 +610,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
     const bool do_attn = prefill || !(g_skip & 8);
 #define IS_ATTN_LAUNCH(R)                                                                                      \
   do {                                                                                                         \
+    if (do_attn && aa.tc_prefix) CKS(launch_prefix_tc<R>(c, aa, l, st));                                       \
     if (do_attn) CKS(launch_k_smem(attn_kernel<R>, dim3(nblk), dim3(kAttnThreads), AttnSmem<R>::v, st, aa)); \
     if (do_attn && getenv("IS_ATTN_TWICE")) {                                                                 \
       AttnArgs a2 = aa;                                                                                        \
@@ -749,7 +794,12 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->log_cap = c->G * c->max_new + c->N * cfg->prefix_k + 8;
   c->max_rows = std::max(c->rc, (int)ceil_div64(c->pcap, 64) * 64);
   c->max_pos = c->P + c->max_new + 1;
-  c->nc_pre = (int)ceil_div64(c->pcap, kPC);
+  c->nc_pre = (int)ceil_div64(c->pcap, kPC);  // prefill (CUDA-core causal prefix units)
+  {
+    const int N = c->rc * (s.n_q_heads / s.n_kv_heads);
+    c->tc_prefix = (N == 16 || N == 32 || N == 64) && !getenv("IS_NO_TC_PREFIX");
+    c->nc_pre_dec = c->tc_prefix ? (int)ceil_div64(c->pcap, 128) : c->nc_pre;
+  }
   c->nc_suf = (int)ceil_div64(c->max_new, kSC);
   c->NC = c->nc_pre + c->nc_suf;
   if (c->NC > 32 || s.n_q_heads / s.n_kv_heads > kMaxRep) {
@@ -817,6 +867,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   CK(cudaDeviceSynchronize());
   // ---- KV
   c->prefix = (__nv_bfloat16*)A((size_t)s.layers * 2 * Hkv * c->pcap * 128 * 2);
+  if (err == IS_OK) CKS(make_tmap(&c->tm_prefix_kv, c->prefix, (int64_t)s.layers * 2 * Hkv * c->pcap, 128, 128));
   c->pool = (__nv_bfloat16*)A((size_t)s.layers * c->num_pages * (size_t)c->page_bytes / s.layers);
   // ---- activations
   const int R = c->max_rows;

@@ -103,6 +103,7 @@ struct AttnArgs {
   int rows, Hq, Hkv, pcap, plen, pt;
   int nc_pre, nc_suf, NC;
   int prefill;                // 1: rows are prompt positions, causal over the prefix, no suffix
+  int tc_prefix;              // decode: shared prefix done by attn_prefix_tc_kernel (tcgen05)
   float scale;                // 1/sqrt(128)
 };
 
@@ -242,7 +243,10 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnArgs a) {
     fence_barrier_init();
   }
   __syncthreads();
-  pdl_wait();
+  // Decode: launched behind attn_prefix_tc_kernel, which triggers only after the
+  // QKV GEMM completed -> our inputs are ready; we wait for the prefix kernel at
+  // the END so the merge kernel (which waits for us) sees both parts.
+  if (a.prefill || !a.tc_prefix) pdl_wait();
   astamp(a, 0);
   const int n = a.prefill ? a.Hkv * a.nc_pre * ((a.rows + kAttnWarps - 1) / kAttnWarps) : (int)a.n_items[0];
   uint32_t phase = 0;
@@ -345,6 +349,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnArgs a) {
     if (nu < 3) astamp(a, 3 + 4 * nu);
     if (nu < 3 && threadIdx.x == 0 && a.dbg_ts) a.dbg_ts[blockIdx.x * 16 + 4 + 4 * nu] = (code < 0) ? 1 : 2;
   }
+  if (!a.prefill && a.tc_prefix) pdl_wait();
   astamp(a, 15);
 }
 
@@ -401,6 +406,177 @@ __global__ void __launch_bounds__(32) attn_merge_kernel(AttnArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ shared-prefix attention on tcgen05
+// The decode step's shared-prefix part as two dense tensor-core contractions
+// (BASELINE north_star: "stacks the group's live queries into one dense
+// Q.K_prefix^T / P.V_prefix contraction on tcgen05 tensor cores with
+// TMA-staged K/V tiles"):
+//   S^T[128 tok x N] = K_tile[128 tok x 128 d] . Q^T           (A = K, K-major; B = Q rows, K-major)
+//   O^T[128 d  x N] = V_tile^T[128 d x 128 tok] . P^T          (A = V, MN-major; B = P rows, K-major)
+// with N = row_capacity x Hq/Hkv stacked query rows of the group (every live
+// slot's heads of one kv head).  One CTA per (kv head, 128-token prefix
+// tile); K/V tiles arrive by TMA (128-byte swizzle); S and O accumulate in
+// TMEM; the column softmax runs on the 128 token lanes; P enters the second
+// MMA as a bf16 hi/lo pair (two accumulating MMAs), i.e. ~fp32 precision.  Each CTA writes one normalised
+// partial (o, m, l) per query row and head into prefix slot `tile`.
+template <int N>
+struct PrefixTcSmem {
+  static constexpr int kK = 2 * 128 * 128;   // two 64-d boxes of 128 token rows (bf16)
+  static constexpr int kV = 2 * 128 * 128;
+  static constexpr int kQ = 2 * N * 128;     // two 64-d atoms of N rows
+  static constexpr int kP = 2 * N * 128;     // two 64-token atoms of N rows (P_hi; P_lo follows)
+  static constexpr int v = kK + kV + kQ + 2 * kP + 4 * N * 4 * 2 + 64 + 1024;
+  static constexpr int kTmemCols = (2 * N) <= 32 ? 32 : ((2 * N) <= 64 ? 64 : ((2 * N) <= 128 ? 128 : 256));
+};
+
+IS_DEVICE uint64_t smem_desc_mn_sw128(const void* p, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+template <int REP, int N>
+__global__ void __launch_bounds__(128, 1)
+    attn_prefix_tc_kernel(const __grid_constant__ CUtensorMap tmKV, AttnArgs a, int kv_row_base) {
+  using SM = PrefixTcSmem<N>;
+  extern __shared__ uint8_t tc_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* Ksm = sm;
+  uint8_t* Vsm = Ksm + SM::kK;
+  uint8_t* Qsm = Vsm + SM::kV;
+  uint8_t* Psm = Qsm + SM::kQ;
+  uint8_t* Plo = Psm + SM::kP;
+  float* red = reinterpret_cast<float*>(Plo + SM::kP);  // [4][N] max, [4][N] sum
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8 * N);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt = (a.plen + 127) / 128;
+  const int h = blockIdx.x / nt, tile = blockIdx.x % nt;
+  const int tok0 = tile * 128, ntok = min(128, a.plen - tok0);
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmKV);
+    mbar_init(&bars[0], 1);  // TMA K+V
+    mbar_init(&bars[1], 1);  // MMA commits (phase 0: S, phase 1: O)
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<SM::kTmemCols>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  pdl_wait();                 // q and the appended KV of this step come from the QKV GEMM
+  pdl_launch_dependents();    // the suffix kernel may start now (it does not touch our outputs)
+  if (threadIdx.x == 0) {
+    // K rows: [(kv=0) * Hkv + h] * pcap + tok ; V rows: [(kv=1) * Hkv + h] * pcap + tok
+    const int rk = kv_row_base + (0 * a.Hkv + h) * a.pcap + tok0;
+    const int rv = kv_row_base + (1 * a.Hkv + h) * a.pcap + tok0;
+    mbar_arrive_expect_tx(&bars[0], SM::kK + SM::kV);
+    tma_load_2d(Ksm, &tmKV, &bars[0], 0, rk, kEvictNormal);
+    tma_load_2d(Ksm + 128 * 128, &tmKV, &bars[0], 64, rk, kEvictNormal);
+    tma_load_2d(Vsm, &tmKV, &bars[0], 0, rv, kEvictNormal);
+    tma_load_2d(Vsm + 128 * 128, &tmKV, &bars[0], 64, rv, kEvictNormal);
+  }
+  // Q rows n = r*REP + e (K-major, 128-byte swizzle, two 64-d atoms)
+  for (int i = threadIdx.x; i < N * 16; i += 128) {
+    const int n = i >> 4, c = i & 15;
+    const int r = n / REP, e = n % REP;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < a.rows && a.row_active[r])
+      v = *reinterpret_cast<const uint4*>(a.q + ((size_t)r * a.Hq + h * REP + e) * kHD + c * 8);
+    *reinterpret_cast<uint4*>(Qsm + (c >> 3) * N * 128 + n * 128 + (((c & 7) ^ (n & 7)) << 4)) = v;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_wait(&bars[0], 0);
+    tc_fence_after();
+    constexpr uint32_t idesc = idesc_bf16_f32(128, N);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {  // 128 d in steps of 16
+      const uint64_t da = smem_desc_k_sw128(Ksm + (k >> 2) * 128 * 128) + 2 * (k & 3);
+      const uint64_t db = smem_desc_k_sw128(Qsm + (k >> 2) * N * 128) + 2 * (k & 3);
+      tc_mma_f16(tmem, da, db, idesc, k > 0 ? 1u : 0u);
+    }
+    tc_commit(&bars[1]);
+  }
+  __syncwarp();
+  mbar_wait(&bars[1], 0);
+  tc_fence_after();
+  // ---- column softmax over the 128 token lanes
+  const int t = warp * 32 + lane;  // token lane (TMEM lane quadrant = warp)
+  float s[N];
+#pragma unroll
+  for (int c = 0; c < N / 16; ++c) tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c * 16, s + c * 16);
+  const bool valid = t < ntok;
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+    s[n] = valid ? s[n] * a.scale : -INFINITY;
+    const float mw = warp_max(s[n]);
+    if (lane == 0) red[warp * N + n] = mw;
+  }
+  __syncthreads();
+  float* red2 = red + 4 * N;
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+    const float M = fmaxf(fmaxf(red[n], red[N + n]), fmaxf(red[2 * N + n], red[3 * N + n]));
+    const float p = valid ? expf(s[n] - M) : 0.f;
+    s[n] = p;
+    const float sw = warp_sum(p);
+    if (lane == 0) red2[warp * N + n] = sw;
+    // P^T operand: row n, K index t (two 64-token atoms, 128-byte swizzle)
+    // P = P_hi + P_lo, both bf16: the two accumulating MMAs keep P to ~2^-16 relative
+    const int off = (t >> 6) * N * 128 + n * 128 + ((((t & 63) >> 3) ^ (n & 7)) << 4) + (t & 7) * 2;
+    const __nv_bfloat16 phi = __float2bfloat16_rn(p);
+    *reinterpret_cast<__nv_bfloat16*>(Psm + off) = phi;
+    *reinterpret_cast<__nv_bfloat16*>(Plo + off) = __float2bfloat16_rn(p - __bfloat162float(phi));
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tc_fence_after();
+    // A = V^T: M = d (MN-major: 64-d blocks 16 KB apart), K = tokens (8-row groups 1 KB apart)
+    constexpr uint32_t idesc2 = idesc_bf16_f32(128, N) | (1u << 15);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {  // 128 tokens in steps of 16, for P_hi then P_lo
+      const uint64_t da = smem_desc_mn_sw128(Vsm + (k & 7) * 2048, 128 * 128, 1024);
+      const uint64_t db = smem_desc_k_sw128((k < 8 ? Psm : Plo) + ((k & 7) >> 2) * N * 128) + 2 * (k & 3);
+      tc_mma_f16(tmem + N, da, db, idesc2, k > 0 ? 1u : 0u);
+    }
+    tc_commit(&bars[1]);
+  }
+  __syncwarp();
+  mbar_wait(&bars[1], 1);
+  tc_fence_after();
+  // ---- epilogue: lane = head dim d; normalise and write partial slot `tile`
+  float o[N];
+#pragma unroll
+  for (int c = 0; c < N / 16; ++c) tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + N + c * 16, o + c * 16);
+  const int d = t;
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+    const int r = n / REP, e = n % REP;
+    if (r < a.rows && a.row_active[r]) {
+      const float M = fmaxf(fmaxf(red[n], red[N + n]), fmaxf(red[2 * N + n], red[3 * N + n]));
+      const float L = red2[n] + red2[N + n] + red2[2 * N + n] + red2[3 * N + n];
+      const size_t pidx = ((size_t)r * a.Hq + h * REP + e) * a.NC + tile;
+      a.part_o[pidx * kHD + d] = o[n] / L;
+      if (d == 0) *reinterpret_cast<float2*>(a.part_ml + pidx * 2) = make_float2(M, L);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<SM::kTmemCols>(tmem);
+  }
+}
+
 // ------------------------------------------------------------------ scheduler (Alg. 1 loop body, Alg. 3)
 enum SchedState {
   ST_PHASE = 0,      // 0 prefix phase, 1 main phase
@@ -453,7 +629,7 @@ struct SchedArgs {
   int32_t* row_kvloc;
   int32_t* row_len;
   int32_t* attn_items;       // [Hkv * (nc_pre + row_cap * nc_suf)][kItemStride]
-  int Hkv, nc_pre, nc_suf, chunk;
+  int Hkv, nc_pre, nc_suf, chunk, tc_prefix;
 };
 
 // Single thread: the work is O(g + pages) integer bookkeeping per step.
@@ -562,7 +738,7 @@ __global__ void sched_kernel(SchedArgs a, int consume) {
     int n = 0, npre = 0;
     if (any) {
       // prefix units: (kv head, chunk, group of 4 rows) for groups holding a live row
-      for (int g = 0; g * 4 < a.row_cap; ++g) {
+      for (int g = 0; !a.tc_prefix && g * 4 < a.row_cap; ++g) {
         bool live = false;
         for (int s = 4 * g; s < 4 * g + 4 && s < a.row_cap; ++s) live = live || a.row_active[s];
         if (!live) continue;

@@ -107,6 +107,14 @@ IS_DEVICE void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// One column: thread i gets lane (base + i), column col.
+IS_DEVICE float tmem_ld1(uint32_t taddr) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return __uint_as_float(r);
+}
+
 // Shared-memory matrix descriptor, K-major, 128-byte swizzle (canonical layout:
 // 8-row x 128 B atoms, SBO = 1024 B between atoms, LBO = 16 B (ignored), version 1).
 IS_DEVICE uint64_t smem_desc_k_sw128(const void* p) {

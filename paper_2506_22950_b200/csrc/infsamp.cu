@@ -517,7 +517,9 @@ static is_status launch_prefix_tc_n(is_ctx* c, const AttnArgs& aa, int l, cudaSt
     cfg.attrs = at;
     cfg.numAttrs = 1;
   }
-  CK(cudaLaunchKernelEx(&cfg, kern, c->tm_prefix_kv, aa, kv_row_base));
+  AttnArgs a2 = aa;
+  a2.dbg_ts = aa.dbg_ts ? aa.dbg_ts + (size_t)2 * 296 * 16 : nullptr;
+  CK(cudaLaunchKernelEx(&cfg, kern, c->tm_prefix_kv, a2, kv_row_base));
   return IS_OK;
 }
 template <int REP>
@@ -592,7 +594,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
     aa.items = c->attn_items;
     aa.n_items = c->st_dev + ST_ATTN_ITEMS;
     aa.dbg_ts = nullptr;
-    if (g_tl && l < 4) aa.dbg_ts = g_tl + (size_t)(400 + 4 * l) * 296 * 16;
+    if (g_tl && l < 4) aa.dbg_ts = g_tl + (size_t)(400 + 4 * l) * 296 * 16;  // attn: 2x296 CTAs, prefix_tc after
     aa.out = c->attn;
     aa.rows = rows;
     aa.Hq = Hq;
@@ -1299,6 +1301,21 @@ extern "C" int is_dbg_timeline(is_ctx* c) {
     printf("%s L%d %.2f..%.2f  CTAs with 0/1/2/3 units: %d/%d/%d/%d | prefix n=%zu stage %.2f/%.2f compute %.2f/%.2f done<=%.2f | suffix n=%zu stage %.2f/%.2f compute %.2f/%.2f done<=%.2f\n",
            (l & 1) ? "attn#2" : "attn", l / 2, st, en, nunits[0], nunits[1], nunits[2], nunits[3], pst[0].size(), med(pst[0]), mx(pst[0]), med(pcm[0]),
            mx(pcm[0]), mx(pend[0]), pst[1].size(), med(pst[1]), mx(pst[1]), med(pcm[1]), mx(pcm[1]), mx(pend[1]));
+  }
+  for (int l = 0; l < 2; ++l) {
+    const unsigned long long* base = &h0[((size_t)(400 + 4 * l) * 296 + 2 * 296) * 16];
+    double mx[8] = {0}, mn0 = 1e30;
+    int n = 0;
+    for (int b = 0; b < 64; ++b) {
+      const unsigned long long* p = base + b * 16;
+      if (!p[0]) continue;
+      ++n;
+      mn0 = std::min(mn0, (double)(p[0] - t0) / 1e3);
+      for (int k = 0; k < 8; ++k)
+        if (p[k]) mx[k] = std::max(mx[k], (double)(p[k] - t0) / 1e3);
+    }
+    printf("prefix_tc L%d ctas=%d start %.2f waited %.2f q_staged %.2f tma %.2f S_done %.2f P_done %.2f O_done %.2f end %.2f\n", l, n,
+           mn0, mx[1], mx[2], mx[3], mx[4], mx[5], mx[6], mx[7]);
   }
   fflush(stdout);
   return c->tl_count;

@@ -425,7 +425,8 @@ struct PrefixTcSmem {
   static constexpr int kV = 2 * 128 * 128;
   static constexpr int kQ = 2 * N * 128;     // two 64-d atoms of N rows
   static constexpr int kP = 2 * N * 128;     // two 64-token atoms of N rows (P_hi; P_lo follows)
-  static constexpr int v = kK + kV + kQ + 2 * kP + 4 * N * 4 * 2 + 64 + 1024;
+  static constexpr int kS = N * 129 * 4;     // scores / probabilities, [column][token], padded
+  static constexpr int v = kK + kV + kQ + 2 * kP + kS + 4 * N * 4 * 2 + N * 16 + 64 + 1024;
   static constexpr int kTmemCols = (2 * N) <= 32 ? 32 : ((2 * N) <= 64 ? 64 : ((2 * N) <= 128 ? 128 : 256));
 };
 
@@ -451,8 +452,12 @@ __global__ void __launch_bounds__(128, 1)
   uint8_t* Qsm = Vsm + SM::kV;
   uint8_t* Psm = Qsm + SM::kQ;
   uint8_t* Plo = Psm + SM::kP;
-  float* red = reinterpret_cast<float*>(Plo + SM::kP);  // [4][N] max, [4][N] sum
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 8 * N);
+  float* Ssm = reinterpret_cast<float*>(Plo + SM::kP);  // [N][129]
+  float* red = Ssm + N * 129;                          // [4][N] max, [4][N] sum
+  float* colM = red + 8 * N;                           // [N] column max, [N] 1/sum, [N] (int) partial index or -1
+  float* colI = colM + N;
+  long long* colP = reinterpret_cast<long long*>(colI + 2 * N);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(colP + N);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = (a.plen + 127) / 128;
@@ -469,7 +474,9 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  astamp(a, 0);
   pdl_wait();                 // q and the appended KV of this step come from the QKV GEMM
+  astamp(a, 1);
   pdl_launch_dependents();    // the suffix kernel may start now (it does not touch our outputs)
   if (threadIdx.x == 0) {
     // K rows: [(kv=0) * Hkv + h] * pcap + tok ; V rows: [(kv=1) * Hkv + h] * pcap + tok
@@ -492,8 +499,10 @@ __global__ void __launch_bounds__(128, 1)
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
+  astamp(a, 2);
   if (threadIdx.x == 0) {
     mbar_wait(&bars[0], 0);
+    astamp(a, 3);
     tc_fence_after();
     constexpr uint32_t idesc = idesc_bf16_f32(128, N);
 #pragma unroll
@@ -506,34 +515,60 @@ __global__ void __launch_bounds__(128, 1)
   }
   __syncwarp();
   mbar_wait(&bars[1], 0);
+  astamp(a, 4);
   tc_fence_after();
-  // ---- column softmax over the 128 token lanes
+  // ---- column softmax.  S^T rows (token t) are transposed through padded smem
+  // so that column statistics are computed with independent loads (lane = column).
   const int t = warp * 32 + lane;  // token lane (TMEM lane quadrant = warp)
-  float s[N];
-#pragma unroll
-  for (int c = 0; c < N / 16; ++c) tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c * 16, s + c * 16);
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   const bool valid = t < ntok;
+#pragma unroll 1
+  for (int c = 0; c < N / 16; ++c) {
+    float v16[16];
+    tmem_ld16(trow + c * 16, v16);
 #pragma unroll
-  for (int n = 0; n < N; ++n) {
-    s[n] = valid ? s[n] * a.scale : -INFINITY;
-    const float mw = warp_max(s[n]);
-    if (lane == 0) red[warp * N + n] = mw;
+    for (int j = 0; j < 16; ++j) Ssm[(c * 16 + j) * 129 + t] = valid ? v16[j] * a.scale : -INFINITY;
   }
   __syncthreads();
-  float* red2 = red + 4 * N;
-#pragma unroll
+  // column max over the 128 tokens: warp w covers tokens [32w, 32w+32), lane = column
+#pragma unroll 1
+  for (int n0 = 0; n0 < N; n0 += 32) {
+    const int n = n0 + lane;
+    float mx = -INFINITY;
+    if (n < N) {
+#pragma unroll 8
+      for (int i = 0; i < 32; ++i) mx = fmaxf(mx, Ssm[n * 129 + warp * 32 + i]);
+      red[warp * N + n] = mx;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < N) {
+    const int n = threadIdx.x;
+    colM[n] = fmaxf(fmaxf(red[n], red[N + n]), fmaxf(red[2 * N + n], red[3 * N + n]));
+  }
+  __syncthreads();
+  // p = exp(s - M): P^T operand (row n, K index t, two 64-token atoms, 128-byte
+  // swizzle) as a bf16 hi/lo pair (two accumulating MMAs keep P to ~2^-16)
+#pragma unroll 4
   for (int n = 0; n < N; ++n) {
-    const float M = fmaxf(fmaxf(red[n], red[N + n]), fmaxf(red[2 * N + n], red[3 * N + n]));
-    const float p = valid ? expf(s[n] - M) : 0.f;
-    s[n] = p;
-    const float sw = warp_sum(p);
-    if (lane == 0) red2[warp * N + n] = sw;
-    // P^T operand: row n, K index t (two 64-token atoms, 128-byte swizzle)
-    // P = P_hi + P_lo, both bf16: the two accumulating MMAs keep P to ~2^-16 relative
+    const float sv = Ssm[n * 129 + t];
+    const float p = valid ? expf(sv - colM[n]) : 0.f;
+    Ssm[n * 129 + t] = p;
     const int off = (t >> 6) * N * 128 + n * 128 + ((((t & 63) >> 3) ^ (n & 7)) << 4) + (t & 7) * 2;
     const __nv_bfloat16 phi = __float2bfloat16_rn(p);
     *reinterpret_cast<__nv_bfloat16*>(Psm + off) = phi;
     *reinterpret_cast<__nv_bfloat16*>(Plo + off) = __float2bfloat16_rn(p - __bfloat162float(phi));
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int n0 = 0; n0 < N; n0 += 32) {
+    const int n = n0 + lane;
+    float sm_ = 0.f;
+    if (n < N) {
+#pragma unroll 8
+      for (int i = 0; i < 32; ++i) sm_ += Ssm[n * 129 + warp * 32 + i];
+      red[4 * N + warp * N + n] = sm_;
+    }
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
@@ -551,24 +586,32 @@ __global__ void __launch_bounds__(128, 1)
     tc_commit(&bars[1]);
   }
   __syncwarp();
+  astamp(a, 5);
   mbar_wait(&bars[1], 1);
+  astamp(a, 6);
   tc_fence_after();
   // ---- epilogue: lane = head dim d; normalise and write partial slot `tile`
-  float o[N];
-#pragma unroll
-  for (int c = 0; c < N / 16; ++c) tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + N + c * 16, o + c * 16);
+  if (threadIdx.x < N) {
+    const int n = threadIdx.x, r = n / REP, e = n % REP;
+    const float L = red[4 * N + n] + red[5 * N + n] + red[6 * N + n] + red[7 * N + n];
+    colI[n] = 1.0f / L;
+    const bool act = r < a.rows && a.row_active[r];
+    colP[n] = act ? (long long)(((size_t)r * a.Hq + h * REP + e) * a.NC + tile) : -1ll;
+    if (act) *reinterpret_cast<float2*>(a.part_ml + colP[n] * 2) = make_float2(colM[n], L);
+  }
+  __syncthreads();
   const int d = t;
+#pragma unroll 1
+  for (int c = 0; c < N / 16; ++c) {
+    float o16[16];
+    tmem_ld16(trow + N + c * 16, o16);
 #pragma unroll
-  for (int n = 0; n < N; ++n) {
-    const int r = n / REP, e = n % REP;
-    if (r < a.rows && a.row_active[r]) {
-      const float M = fmaxf(fmaxf(red[n], red[N + n]), fmaxf(red[2 * N + n], red[3 * N + n]));
-      const float L = red2[n] + red2[N + n] + red2[2 * N + n] + red2[3 * N + n];
-      const size_t pidx = ((size_t)r * a.Hq + h * REP + e) * a.NC + tile;
-      a.part_o[pidx * kHD + d] = o[n] / L;
-      if (d == 0) *reinterpret_cast<float2*>(a.part_ml + pidx * 2) = make_float2(M, L);
+    for (int j = 0; j < 16; ++j) {
+      const long long pidx = colP[c * 16 + j];
+      if (pidx >= 0) a.part_o[pidx * kHD + d] = o16[j] * colI[c * 16 + j];
     }
   }
+  astamp(a, 7);
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {

@@ -69,6 +69,9 @@ typedef struct {
   float temperature;       /* sampling temperature (0.8) */
   uint64_t seed;           /* Philox key (R11) */
   is_mode mode;
+  int32_t decode_impl;     /* 0: persistent decode kernel, one launch for the whole layer stack
+                              (default; falls back to 1 when Hq/Hkv > 4 or the attention needs
+                              more than 64 partials per row); 1: one kernel per operator */
 } is_config;
 
 /* Alg. 2 output plus the runtime plan (Alg. 1, Alg. 3).  All arrays are
@@ -100,6 +103,10 @@ typedef struct {
   int64_t prefix_bytes;
   int32_t num_pages;      /* size of the page pool */
   int32_t row_capacity;
+  int32_t decode_impl;    /* implementation in use (see is_config.decode_impl) */
+  int64_t layer_kernel_ns;       /* persistent decode kernel: accumulated device time (globaltimer, CTA 0) */
+  int64_t layer_kernel_launches; /*   and launches, since is_create */
+  int64_t suffix_tokens;  /* sum over decode steps of the live rows' suffix lengths (algorithmic KV bytes) */
 } is_stats;
 
 typedef struct is_ctx is_ctx;
@@ -192,6 +199,15 @@ is_status is_profile_step(is_ctx* ctx, float* h_ms, int32_t* h_kind, int32_t cap
  * rows <= 64, K % 64 == 0, on `stream`. split = K-split cluster size (1..8). */
 is_status is_dbg_gemm(const void* d_w, const void* d_x, float* d_y, int32_t M, int32_t K, int32_t rows,
                       int32_t split, void* stream);
+
+/* Debug hook of the persistent decode kernel: h_info[4] = {in use, grid, task
+ * count, trace capacity}; copies the per-CTA task lists (int4 {kind | layer<<8 |
+ * part<<16, tile, kb0, kb1}, h_tasks[4 * count]) and offsets (h_off[grid + 1])
+ * and, when the context was created with IS_MK_TRACE=<cap> in the environment,
+ * the last step's timeline (h_trace[grid][4][cap][2] = {globaltimer ns, type<<32
+ * | task}).  Any destination may be NULL.  Synchronises the stream. */
+is_status is_dbg_mk_trace(is_ctx* ctx, int32_t* h_tasks, int32_t task_cap, int32_t* h_off, int32_t off_cap,
+                          uint64_t* h_trace, int64_t trace_cap, int32_t* h_info);
 
 const char* is_last_error(void);
 const char* is_version(void);

@@ -18,7 +18,7 @@ ADV_MODES = {"std_norm": 0, "mean_only": 1}
 EXPORTS = ["is_plan", "is_create", "is_destroy", "is_prefill", "is_start_group", "is_decode_step",
            "is_refill", "is_run_group", "is_query", "is_copy_tokens", "is_copy_schedule",
            "is_group_results", "is_group_advantages", "is_set_logits_dump", "is_profile_step",
-           "is_dbg_gemm", "is_last_error", "is_version"]
+           "is_dbg_gemm", "is_dbg_mk_trace", "is_last_error", "is_version"]
 
 
 class InfsampError(RuntimeError):
@@ -39,7 +39,7 @@ class Config(ctypes.Structure):
                 ("prefix_k", ctypes.c_int32), ("page_tokens", ctypes.c_int32),
                 ("row_capacity", ctypes.c_int32), ("kv_budget_bytes", ctypes.c_int64),
                 ("eps", ctypes.c_double), ("temperature", ctypes.c_float), ("seed", ctypes.c_uint64),
-                ("mode", ctypes.c_int32)]
+                ("mode", ctypes.c_int32), ("decode_impl", ctypes.c_int32)]
 
 
 class PlanOut(ctypes.Structure):
@@ -56,7 +56,9 @@ class Stats(ctypes.Structure):
                 ("live_pages", ctypes.c_int32), ("peak_pages", ctypes.c_int32), ("error", ctypes.c_int32),
                 ("tokens_decoded", ctypes.c_int64), ("peak_kv_bytes", ctypes.c_int64),
                 ("page_bytes", ctypes.c_int64), ("prefix_bytes", ctypes.c_int64),
-                ("num_pages", ctypes.c_int32), ("row_capacity", ctypes.c_int32)]
+                ("num_pages", ctypes.c_int32), ("row_capacity", ctypes.c_int32),
+                ("decode_impl", ctypes.c_int32), ("layer_kernel_ns", ctypes.c_int64),
+                ("layer_kernel_launches", ctypes.c_int64), ("suffix_tokens", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -101,6 +103,7 @@ def load(build_if_missing=True):
     L.is_set_logits_dump.argtypes = [vp, vp]
     L.is_profile_step.argtypes = [vp, vp, vp, i32, ctypes.POINTER(i32)]
     L.is_dbg_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]
+    L.is_dbg_mk_trace.argtypes = [vp, vp, i32, vp, i32, vp, ctypes.c_int64, vp]
     L.is_last_error.restype = ctypes.c_char_p
     L.is_last_error.argtypes = []
     L.is_version.restype = ctypes.c_char_p
@@ -121,7 +124,9 @@ def _np_ptr(a):
 
 
 def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix_k=0, page_tokens=16,
-                row_capacity=0, kv_budget_bytes=0, eps=0.1, temperature=0.8, seed=20261017):
+                row_capacity=0, kv_budget_bytes=0, eps=0.1, temperature=0.8, seed=20261017, decode_impl=None):
+    """decode_impl: 0 = persistent decode kernel (default), 1 = one kernel per operator;
+    None reads IS_DECODE_IMPL from the environment (default 0)."""
     c = Config()
     c.shape = Shape(shape.layers, shape.hidden, shape.n_q_heads, shape.n_kv_heads, shape.head_dim, shape.ffn,
                     shape.vocab, shape.rms_eps, shape.rope_theta)
@@ -129,6 +134,9 @@ def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix
     c.prefix_k, c.page_tokens, c.row_capacity = prefix_k, page_tokens, row_capacity
     c.kv_budget_bytes, c.eps, c.temperature, c.seed = kv_budget_bytes, eps, temperature, seed
     c.mode = MODES[mode] if isinstance(mode, str) else int(mode)
+    if decode_impl is None:
+        decode_impl = int(os.environ.get("IS_DECODE_IMPL", "0"))
+    c.decode_impl = decode_impl
     return c
 
 
@@ -260,6 +268,20 @@ class Context:
 
     def is_set_logits_dump(self, d_logits):
         _check(load().is_set_logits_dump(self._h, None if d_logits is None else d_logits.data_ptr()))
+
+    def is_dbg_mk_trace(self):
+        """Persistent decode kernel debug: (tasks [n,4], offsets [grid+1], trace [grid,4,cap,2] or None)."""
+        info = np.zeros(4, np.int32)
+        _check(load().is_dbg_mk_trace(self._h, None, 0, None, 0, None, 0, _np_ptr(info)))
+        if not info[0]:
+            return None
+        grid, n, cap = int(info[1]), int(info[2]), int(info[3])
+        tasks = np.zeros((n, 4), np.int32)
+        off = np.zeros(grid + 1, np.int32)
+        trace = np.zeros((grid, 4, cap, 2), np.uint64) if cap else None
+        _check(load().is_dbg_mk_trace(self._h, _np_ptr(tasks), tasks.size, _np_ptr(off), off.size,
+                                      _np_ptr(trace) if cap else None, trace.size if cap else 0, _np_ptr(info)))
+        return tasks, off, trace
 
     def is_profile_step(self, cap=4096):
         ms = np.zeros(cap, np.float32)

@@ -70,6 +70,8 @@ struct GemmArgs {
   QkvEpiArgs qkv;
   float* partials;              // split-K workspace [clusters][split][128][BN] fp32 (L2-resident)
   unsigned long long* dbg_ts;  // optional [gridDim][16] globaltimer stamps (probe)
+  int* zero;                   // optional: words zeroed once the previous kernel completed
+  int zero_n;                  //   (the persistent decode kernel's dependency counters)
 };
 
 constexpr int kBM = 128;
@@ -240,6 +242,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     float* stg = aux;             // [BN][128] accumulator tile (column n = activation row)
     float* pre = aux + BN * kBM;  // [BN][128] operands prefetched during the mainloop
     pdl_wait();
+    if (a.zero)
+      for (int i = blockIdx.x * 128 + (threadIdx.x - 64); i < a.zero_n; i += gridDim.x * 128) a.zero[i] = 0;
     int it = 0;
     for (int tile = cl; tile < a.num_tiles; tile += ncl, ++it) {
       const int acc = it & 1;

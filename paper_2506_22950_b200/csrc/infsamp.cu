@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "mega.cuh"
 
 using namespace isk;
 
@@ -418,6 +419,14 @@ struct is_ctx {
   CUtensorMap tm_prefix_kv;
   unsigned long long* timeline;  // debug: [launch][148 CTAs][16] GEMM stamps (IS_TIMELINE)
   int tl_count;
+  // persistent decode kernel (decode_impl 0)
+  int mk;                    // 1 = in use
+  int mk_grid, mk_smem;
+  MkArgs mka;
+  void* mk_bufs[32];
+  int mk_nbufs;
+  int mk_sync_n;
+  int mk_ntasks;
 };
 
 static void* dalloc(size_t bytes, is_status* s) {
@@ -675,13 +684,276 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
   return IS_OK;
 }
 
+// ------------------------------------------------------------------ persistent decode kernel setup
+template <int BN, int REP>
+static int mk_scratch_bytes() { return MkScratch<BN, REP>::v; }
+static int mk_scratch_of(int BN, int REP) {
+  switch (BN * 16 + REP) {
+    case 16 * 16 + 1: return mk_scratch_bytes<16, 1>();
+    case 16 * 16 + 2: return mk_scratch_bytes<16, 2>();
+    case 16 * 16 + 4: return mk_scratch_bytes<16, 4>();
+    case 32 * 16 + 1: return mk_scratch_bytes<32, 1>();
+    case 32 * 16 + 2: return mk_scratch_bytes<32, 2>();
+    case 32 * 16 + 4: return mk_scratch_bytes<32, 4>();
+    case 64 * 16 + 1: return mk_scratch_bytes<64, 1>();
+    case 64 * 16 + 2: return mk_scratch_bytes<64, 2>();
+    case 64 * 16 + 4: return mk_scratch_bytes<64, 4>();
+  }
+  return -1;
+}
+template <int BN, int REP>
+static is_status mk_launch_t(is_ctx* c, cudaStream_t st) {
+  auto kern = mk_decode_kernel<BN, REP>;
+  static int attr = 0;
+  if (attr != c->mk_smem) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, c->mk_smem));
+    attr = c->mk_smem;
+  }
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = dim3(c->mk_grid);
+  cfg.blockDim = dim3(kMkThreads);
+  cfg.dynamicSmemBytes = c->mk_smem;
+  cfg.stream = st;
+  cfg.numAttrs = 0;
+  if (g_use_pdl) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  CK(cudaLaunchKernelEx(&cfg, kern, c->mka));
+  return IS_OK;
+}
+static is_status mk_launch(is_ctx* c, cudaStream_t st) {
+  const int REP = c->sh.n_q_heads / c->sh.n_kv_heads;
+  switch (c->BN * 16 + REP) {
+    case 16 * 16 + 1: return mk_launch_t<16, 1>(c, st);
+    case 16 * 16 + 2: return mk_launch_t<16, 2>(c, st);
+    case 16 * 16 + 4: return mk_launch_t<16, 4>(c, st);
+    case 32 * 16 + 1: return mk_launch_t<32, 1>(c, st);
+    case 32 * 16 + 2: return mk_launch_t<32, 2>(c, st);
+    case 32 * 16 + 4: return mk_launch_t<32, 4>(c, st);
+    case 64 * 16 + 1: return mk_launch_t<64, 1>(c, st);
+    case 64 * 16 + 2: return mk_launch_t<64, 2>(c, st);
+    case 64 * 16 + 4: return mk_launch_t<64, 4>(c, st);
+  }
+  return fail(IS_ERR_CONFIG, "persistent decode kernel: unsupported BN %d / REP %d", c->BN, REP);
+}
+
+// Does the persistent decode kernel support this context?  (Hq/Hkv <= 4, <= 64
+// attention partials per row, smem for at least 4 weight stages.)
+static bool mk_supported(const is_ctx* c) {
+  const int REP = c->sh.n_q_heads / c->sh.n_kv_heads;
+  if (REP != 1 && REP != 2 && REP != 4) return false;
+  const int nc_pre = (int)ceil_div64(c->pcap, kMkPC);
+  if (nc_pre + ceil_div64(c->max_new, kMkSC) > 64) return false;
+  if (c->sh.layers > 255) return false;
+  return true;
+}
+
+static is_status setup_mega(is_ctx* c, const void* const* dw) {
+  const is_shape& s = c->sh;
+  const int H = s.hidden, F = s.ffn, Hq = s.n_q_heads, Hkv = s.n_kv_heads, L = s.layers, BN = c->BN, rc = c->rc;
+  const int REP = Hq / Hkv;
+  is_status err = IS_OK;
+  auto A = [&](size_t bytes) -> void* {
+    void* p = err == IS_OK ? dalloc(bytes, &err) : nullptr;
+    if (p) c->mk_bufs[c->mk_nbufs++] = p;
+    return p;
+  };
+  MkArgs& a = c->mka;
+  a = MkArgs{};
+  // ---- GEMM geometry and K splits: units of ~unit_kb k-blocks (16 KB each)
+  int unit_kb = 8;
+  if (const char* e = getenv("IS_MK_UNIT_KB")) unit_kb = std::max(1, atoi(e));
+  const int Ms[4] = {c->qkv_w, H, 2 * F, H};
+  const int Ks[4] = {H, Hq * 128, H, F};
+  long long w_off = 0, ws_off = 0;
+  for (int i = 0; i < 4; ++i) {
+    MkGemm& g = a.g[i];
+    g.M = Ms[i];
+    g.KB = Ks[i] / 64;
+    g.T = (int)ceil_div64(g.M, 128);
+    g.S = std::max(1, std::min(g.KB, (g.KB + unit_kb / 2) / unit_kb));
+    if (g.S > 255) g.S = 255;
+    g.w_off = w_off;
+    w_off += (long long)g.T * g.KB * 128 * 64;
+    g.ws_off = ws_off;
+    if (g.S > 1) ws_off += (long long)g.T * g.S * 128 * BN;
+  }
+  a.layer_stride = w_off;
+  // ---- packed, swizzled weights
+  __nv_bfloat16* wpk = (__nv_bfloat16*)A((size_t)w_off * L * 2);
+  if (err != IS_OK) return err;
+  for (int l = 0; l < L; ++l) {
+    const LayerW& w = c->L[l];
+    const __nv_bfloat16* src[4] = {w.wqkv, w.wo, w.wgu, w.wd};
+    for (int i = 0; i < 4; ++i)
+      pack_sw128_kernel<<<1024, 256>>>(src[i], Ms[i], Ks[i], wpk + (size_t)l * w_off + a.g[i].w_off);
+  }
+  CK(cudaGetLastError());
+  // ---- norms [L][H] etc. (fp32)
+  float* in_norm = (float*)A((size_t)L * H * 4);
+  float* post_norm = (float*)A((size_t)L * H * 4);
+  float* qn = (float*)A((size_t)L * 128 * 4);
+  float* kn = (float*)A((size_t)L * 128 * 4);
+  if (err != IS_OK) return err;
+  for (int l = 0; l < L; ++l) {
+    const void* const* p = dw + 2 + 11 * l;
+    bf16_to_f32_kernel<<<(H + 255) / 256, 256>>>((const __nv_bfloat16*)p[0], in_norm + (size_t)l * H, H);
+    bf16_to_f32_kernel<<<(H + 255) / 256, 256>>>((const __nv_bfloat16*)p[7], post_norm + (size_t)l * H, H);
+    bf16_to_f32_kernel<<<1, 128>>>((const __nv_bfloat16*)p[4], qn + l * 128, 128);
+    bf16_to_f32_kernel<<<1, 128>>>((const __nv_bfloat16*)p[5], kn + l * 128, 128);
+  }
+  CK(cudaGetLastError());
+  // ---- activations
+  a.Th = (int)ceil_div64(H, 128);
+  a.resid0 = c->resid;
+  a.resid1 = (float*)A((size_t)rc * H * 4);
+  a.ssq = (float*)A((size_t)(2 * L + 1) * a.Th * rc * 4);
+  a.xgA = (__nv_bfloat16*)A((size_t)H * BN * 2);
+  a.xgB = (__nv_bfloat16*)A((size_t)H * BN * 2);
+  a.attn_sw = (__nv_bfloat16*)A((size_t)Hq * 128 * BN * 2);
+  a.act_sw = (__nv_bfloat16*)A((size_t)F * BN * 2);
+  a.ws = (float*)A((size_t)std::max(ws_off, 1ll) * 4);
+  a.nc_pre = (int)ceil_div64(c->pcap, kMkPC);
+  a.NCm = a.nc_pre + (int)ceil_div64(c->max_new, kMkSC);
+  a.part_o = (float*)A((size_t)rc * Hq * a.NCm * 128 * 4);
+  a.part_ml = (float*)A((size_t)rc * Hq * a.NCm * 2 * 4);
+  // ---- dependency counters, one block per layer
+  MkSync& so = a.so;
+  int o = 0;
+  so.att_next = o++;
+  so.o_done = o++;
+  so.dn_done = o++;
+  so.emb_done = o++;
+  so.qkv_cnt = o; o += a.g[0].T;
+  so.qkv_flag = o; o += a.g[0].T;
+  so.att_row = o; o += Hkv * rc;
+  so.att_done = o; o += Hkv;
+  so.o_cnt = o; o += a.g[1].T;
+  so.gu_cnt = o; o += a.g[2].T;
+  so.gu_flag = o; o += a.g[2].T;
+  so.dn_cnt = o; o += a.g[3].T;
+  so.stride = (o + 31) / 32 * 32;
+  c->mk_sync_n = so.stride * L;
+  a.sync = (int*)A((size_t)c->mk_sync_n * 4);
+  a.clock = (unsigned long long*)A(16);
+  if (const char* e = getenv("IS_MK_TRACE")) {
+    a.trace_cap = std::max(16, atoi(e));
+    a.trace = (unsigned long long*)A((size_t)g_num_sms * 4 * a.trace_cap * 16);
+  }
+  if (err != IS_OK) return err;
+  // ---- static per-CTA task lists (global order: EMBED, per layer QKV ATT O GU DN, FINAL)
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const int grid = g_num_sms;
+  std::vector<std::vector<int4>> tl(grid);
+  for (int r = 0; r < rc; ++r) tl[r % grid].push_back(make_int4(MK_EMBED, r, 0, 0));
+  long long u = 0;
+  const int kinds[4] = {MK_QKV, MK_O, MK_GU, MK_DN};
+  for (int l = 0; l < L; ++l) {
+    for (int gi = 0; gi < 4; ++gi) {
+      const MkGemm& g = a.g[gi];
+      for (int t = 0; t < g.T; ++t)
+        for (int p = 0; p < g.S; ++p)
+          tl[(u++) % grid].push_back(
+              make_int4(kinds[gi] | (l << 8) | (p << 16), t, p * g.KB / g.S, (p + 1) * g.KB / g.S));
+      if (gi == 0)
+        for (int b = 0; b < grid; ++b) tl[b].push_back(make_int4(MK_ATT | (l << 8), 0, 0, 0));
+    }
+  }
+  for (int r = 0; r < rc; ++r) tl[r % grid].push_back(make_int4(MK_FINAL | ((L - 1) << 8), r, 0, 0));
+  std::vector<int> off(grid + 1, 0);
+  std::vector<int4> flat;
+  for (int b = 0; b < grid; ++b) {
+    off[b] = (int)flat.size();
+    flat.insert(flat.end(), tl[b].begin(), tl[b].end());
+  }
+  off[grid] = (int)flat.size();
+  int4* d_tasks = (int4*)A(flat.size() * sizeof(int4));
+  int* d_off = (int*)A(off.size() * 4);
+  c->mk_ntasks = (int)flat.size();
+  if (err != IS_OK) return err;
+  CK(cudaMemcpy(d_tasks, flat.data(), flat.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+  // ---- shared memory: weight ring gets what the B rings and scratch leave
+  a.scratch = mk_scratch_of(BN, REP);
+  a.nb = BN == 16 ? 8 : (BN == 32 ? 6 : 4);
+  int maxsm = 0;
+  CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const int fixed = 1024 + 2 * a.nb * BN * 128 + 2 * a.scratch + 1024;
+  a.na = std::min(16, (maxsm - fixed) / kMkStage);
+  if (const char* e = getenv("IS_MK_STAGES")) a.na = std::max(2, std::min(a.na, atoi(e)));
+  if (a.na < 3) return fail(IS_ERR_CONFIG, "persistent decode kernel: not enough shared memory");
+  c->mk_smem = fixed + a.na * kMkStage;
+  c->mk_grid = grid;
+  // ---- the rest of the arguments
+  a.tasks = d_tasks;
+  a.task_off = d_off;
+  a.wpk = wpk;
+  a.L = L;
+  a.H = H;
+  a.F = F;
+  a.Hq = Hq;
+  a.Hkv = Hkv;
+  a.rc = rc;
+  a.eps = s.rms_eps;
+  a.scale = 1.0f / sqrtf((float)kHD);
+  a.embed = c->embed;
+  a.in_norm = in_norm;
+  a.post_norm = post_norm;
+  a.q_norm = qn;
+  a.k_norm = kn;
+  a.final_norm = c->final_norm;
+  a.rope_cos = c->rope_cos;
+  a.rope_sin = c->rope_sin;
+  a.row_active = c->row_active;
+  a.row_tok = c->row_tok;
+  a.row_pos = c->row_pos;
+  a.row_kvloc = c->row_kvloc;
+  a.row_len = c->row_len;
+  a.row_lid = c->row_lid;
+  a.q = c->q;
+  a.xn_final = c->xn;
+  a.prefix = c->prefix;
+  a.prefix_layer = (long long)2 * Hkv * c->pcap * kHD;
+  a.pool = c->pool;
+  a.pool_layer = (long long)c->num_pages * 2 * Hkv * c->pt * kHD;
+  a.pagetab = c->pagetab;
+  a.maxp = c->maxp;
+  a.pt = c->pt;
+  a.pcap = c->pcap;
+  CK(cudaDeviceSynchronize());
+  // the kernel's CTAs must all be co-resident (they wait on each other)
+  int occ = 0;
+  switch (BN * 16 + REP) {
+#define IS_OCC(B, R) \
+  case B * 16 + R: { \
+    CK(cudaFuncSetAttribute(mk_decode_kernel<B, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->mk_smem)); \
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mk_decode_kernel<B, R>, kMkThreads, c->mk_smem)); \
+    break; }
+    IS_OCC(16, 1) IS_OCC(16, 2) IS_OCC(16, 4) IS_OCC(32, 1) IS_OCC(32, 2) IS_OCC(32, 4) IS_OCC(64, 1) IS_OCC(64, 2) IS_OCC(64, 4)
+#undef IS_OCC
+  }
+  if (occ < 1) return fail(IS_ERR_CONFIG, "persistent decode kernel does not fit on an SM (smem %d)", c->mk_smem);
+  c->mk = 1;
+  return IS_OK;
+}
+
 static is_status enqueue_step(is_ctx* c) {
   cudaStream_t st = c->st;
   const is_shape& s = c->sh;
-  CKS(run_layers(c, c->rc, false));
-  CKS(launch_k(rmsnorm_kernel, dim3(c->rc), dim3(256), st, (const float*)c->resid, (const float*)c->final_norm,
-               c->xn, s.hidden, s.rms_eps));
-  prof_mark(st, 0);
+  if (c->mk) {
+    CKS(mk_launch(c, st));
+    prof_mark(st, 9);
+  } else {
+    CKS(run_layers(c, c->rc, false));
+    CKS(launch_k(rmsnorm_kernel, dim3(c->rc), dim3(256), st, (const float*)c->resid, (const float*)c->final_norm,
+                 c->xn, s.hidden, s.rms_eps));
+    prof_mark(st, 0);
+  }
   GemmArgs a{};
   a.M = s.vocab;
   a.K = s.hidden;
@@ -695,6 +967,10 @@ static is_status enqueue_step(is_ctx* c) {
   a.row_active = c->row_active;
   a.keys = c->keys;
   a.logits_dump = c->logits_dump;
+  if (c->mk) {
+    a.zero = c->mka.sync;  // the next step's dependency counters start from zero
+    a.zero_n = c->mk_sync_n;
+  }
   a.seed = c->cfg.seed;
   a.inv_temp = (float)(1.0 / (double)c->cfg.temperature);
   g_splitk_ws = c->splitk_ws;
@@ -937,6 +1213,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
     if (v >= 1 && v <= 8) c->split_qkv = c->split_o = c->split_gu = c->split_d = v;
   }
   CK(cudaDeviceSynchronize());
+  if (cfg->decode_impl == 0 && mk_supported(c) && !getenv("IS_NO_MEGA")) CKS(setup_mega(c, dw));
   *out = c;
   return IS_OK;
 }
@@ -953,6 +1230,7 @@ extern "C" void is_destroy(is_ctx* c) {
                   c->log_live, c->d_prompt_copy};
   for (void* p : bufs)
     if (p) cudaFree(p);
+  for (int i = 0; i < c->mk_nbufs; ++i) cudaFree(c->mk_bufs[i]);
   for (auto& w : c->L) {
     cudaFree(w.in_norm);
     cudaFree(w.post_norm);
@@ -1129,6 +1407,16 @@ extern "C" is_status is_query(is_ctx* c, is_stats* o) {
   o->peak_kv_bytes = c->prefix_bytes + st[ST_PEAK] * c->page_bytes;
   o->num_pages = c->num_pages;
   o->row_capacity = c->rc;
+  o->decode_impl = c->mk ? 0 : 1;
+  o->suffix_tokens = st[ST_SUFFIX];
+  o->layer_kernel_ns = 0;
+  o->layer_kernel_launches = 0;
+  if (c->mk) {
+    unsigned long long clk[2];
+    CK(cudaMemcpy(clk, c->mka.clock, sizeof clk, cudaMemcpyDeviceToHost));
+    o->layer_kernel_ns = (int64_t)clk[0];
+    o->layer_kernel_launches = (int64_t)clk[1];
+  }
   return IS_OK;
 }
 
@@ -1319,4 +1607,22 @@ extern "C" int is_dbg_timeline(is_ctx* c) {
   }
   fflush(stdout);
   return c->tl_count;
+}
+
+extern "C" is_status is_dbg_mk_trace(is_ctx* c, int32_t* h_tasks, int32_t task_cap, int32_t* h_off, int32_t off_cap,
+                                     uint64_t* h_trace, int64_t trace_cap, int32_t* h_info) {
+  if (!c || !h_info) return fail(IS_ERR_CONFIG, "null argument");
+  CK(cudaStreamSynchronize(c->st));
+  h_info[0] = c->mk;
+  h_info[1] = c->mk ? c->mk_grid : 0;
+  h_info[2] = c->mk ? c->mk_ntasks : 0;
+  h_info[3] = c->mk ? c->mka.trace_cap : 0;
+  if (!c->mk) return IS_OK;
+  if (h_tasks && task_cap >= c->mk_ntasks * 4)
+    CK(cudaMemcpy(h_tasks, c->mka.tasks, (size_t)c->mk_ntasks * 16, cudaMemcpyDeviceToHost));
+  if (h_off && off_cap >= c->mk_grid + 1)
+    CK(cudaMemcpy(h_off, c->mka.task_off, (size_t)(c->mk_grid + 1) * 4, cudaMemcpyDeviceToHost));
+  const int64_t n = (int64_t)c->mk_grid * 4 * c->mka.trace_cap * 2;
+  if (h_trace && c->mka.trace && trace_cap >= n) CK(cudaMemcpy(h_trace, c->mka.trace, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  return IS_OK;
 }

@@ -174,7 +174,8 @@ struct WarpPartial {
     float p[REP];
 #pragma unroll
     for (int e = 0; e < REP; ++e) {
-      if (LPT == 2) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 1);
+#pragma unroll
+      for (int sh = 1; sh < LPT; sh <<= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], sh);
       const float sc = tk < ntok ? acc[e] * scale : -INFINITY;
       m[e] = warp_max(sc);
       p[e] = sc == -INFINITY ? 0.f : expf(sc - m[e]);
@@ -641,6 +642,7 @@ enum SchedState {
   ST_TOKENS,
   ST_ATTN_ITEMS,   // length of the attention work list for the next step
   ST_ATTN_PRE,     // of which shared-prefix items (must follow ST_ATTN_ITEMS)
+  ST_SUFFIX,       // sum over steps of the live rows' suffix lengths
   ST_COUNT
 };
 
@@ -773,6 +775,7 @@ __global__ void sched_kernel(SchedArgs a, int consume) {
     a.row_pos[s] = a.P - 1 + tt;
     a.row_kvloc[s] = a.pagetab[(size_t)uid * a.maxp + tt / a.pt] * a.pt + tt % a.pt;
     a.row_len[s] = tt + 1;
+    st[ST_SUFFIX] += tt + 1;
   }
   // attention work list of the next step: shared-prefix chunks first (one CTA
   // each, all live rows), then every live slot's suffix chunks (one warp each,

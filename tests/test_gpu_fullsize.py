@@ -16,10 +16,11 @@ pytestmark = pytest.mark.gpu
 SEED = 20261017
 SHAPE = SHAPES["qwen3-1.7b"]
 P, G, g, MAX_NEW = 256, 32, 8, 1024
+LATE = 70  # step whose logits are checked at t = 70 (3 suffix chunks of 32 tokens)
 
 
-@pytest.fixture(scope="module")
-def full():
+@pytest.fixture(scope="module", params=[0, 1], ids=["persistent", "per_op"])
+def full(request):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2506_22950_b200 import _lib
@@ -27,7 +28,7 @@ def full():
     kv_tok = okv.kv_bytes_per_token(SHAPE.layers, SHAPE.n_kv_heads, SHAPE.head_dim)
     budget = (P - 1) * kv_tok + g * (MAX_NEW // 16) * 16 * kv_tok
     cfg = _lib.make_config(SHAPE, G, g, MAX_NEW, P, mode="infinite", page_tokens=16, kv_budget_bytes=budget,
-                           eps=0.1, temperature=0.8, seed=SEED)
+                           eps=0.1, temperature=0.8, seed=SEED, decode_impl=request.param)
     ctx = _lib.Context(cfg, w)
     prompt = gen_prompt(SHAPE.vocab, P, 3, seed=SEED)
     true = gen_trace("math", G, MAX_NEW, SEED + 3)
@@ -42,10 +43,16 @@ def full():
         ctx.is_decode_step()
         torch.cuda.synchronize()
         dumps.append(dump.cpu().numpy().copy())
+    # a later step: several suffix chunks per slot (multi-chunk suffix attention + LSE merge)
+    for _ in range(LATE - 3):
+        ctx.is_decode_step()
+    ctx.is_decode_step()
+    torch.cuda.synchronize()
+    late = dump.cpu().numpy().copy()
     ctx.is_set_logits_dump(None)
     steps = ctx.is_run_group()
     res = dict(steps=steps, stats=ctx.is_query(), sched=ctx.is_copy_schedule(), tokens=ctx.is_copy_tokens(),
-               dumps=dumps, true=true, pred=pred, prompt=prompt, budget=budget,
+               dumps=dumps, late=late, true=true, pred=pred, prompt=prompt, budget=budget, impl=request.param,
                w_cpu={k: v.cpu() for k, v in w.items()})
     ctx.close()
     del w
@@ -94,3 +101,26 @@ def test_fullsize_teacher_forced_logits_and_tokens(full):
         tok, margin = sampler.sample_margin(z[t].astype(np.float32), SEED, 3 * G + uid, t)
         if tok != gen[t]:
             assert margin < 2 * 1.25 * np.max(np.abs(d - z[t])), (t, margin)
+
+
+def test_fullsize_decode_impl_in_use(full):
+    assert full["stats"]["decode_impl"] == full["impl"]
+
+
+def test_fullsize_late_step_logits(full):
+    """Teacher-forced oracle logits at step LATE for every slot still decoding its first sample."""
+    slots, _ = full["sched"]
+    checked = 0
+    for s, uid in enumerate(slots[LATE]):
+        uid = int(uid)
+        if uid < 0 or uid != int(slots[0][s]) or checked >= 2:
+            continue  # only samples that started at step 0 (t = LATE)
+        gen = [int(x) for x in full["tokens"][uid, :LATE + 1]]
+        z = M.teacher_forced_logits(full["w_cpu"], SHAPE, full["prompt"], gen, mirror=True, rows=[LATE])[0]
+        d = full["late"][s].astype(np.float64)
+        rel = np.linalg.norm(d - z) / np.linalg.norm(z)
+        assert rel < 2e-2, (s, rel)
+        assert np.max(np.abs(d - z)) <= 2e-2 * np.max(np.abs(z))
+        assert sampler.sample_token(full["late"][s], SEED, 3 * G + uid, LATE) == full["tokens"][uid, LATE]
+        checked += 1
+    assert checked > 0

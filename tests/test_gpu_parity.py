@@ -61,9 +61,9 @@ def _tiny_setup():
     return w, prompt, true, pred
 
 
-def _run(lib, w_dev, prompt, true, pred, mode, g, budget=0, prefix_k=0, pt=16, rc=16, logits=False):
+def _run(lib, w_dev, prompt, true, pred, mode, g, budget=0, prefix_k=0, pt=16, rc=16, logits=False, impl=0):
     cfg = lib.make_config(TINY, 8, g, 32, 16, mode=mode, prefix_k=prefix_k, page_tokens=pt, row_capacity=rc,
-                          kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED)
+                          kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED, decode_impl=impl)
     ctx = lib.Context(cfg, w_dev)
     ctx.is_prefill(torch.as_tensor(prompt, device="cuda"), 0)
     ctx.is_start_group(true, pred)
@@ -87,14 +87,17 @@ def _run(lib, w_dev, prompt, true, pred, mode, g, budget=0, prefix_k=0, pt=16, r
     return dict(steps=steps, stats=st, slots=slots, live=live, tokens=toks, dumps=dumps)
 
 
-@pytest.fixture(scope="module")
-def tiny(lib):
+@pytest.fixture(scope="module", params=[0, 1], ids=["persistent", "per_op"])
+def tiny(lib, request):
+    """decode_impl 0 = the persistent decode kernel, 1 = one kernel per operator."""
+    impl = request.param
     w, prompt, true, pred = _tiny_setup()
     w_dev = {k: v.cuda() for k, v in w.items()}
     budget = okv.prefix_bytes(TINY, 16) + 4 * 2 * okv.page_bytes(TINY, 16)  # config 1: "KV budget 4 slots"
-    runs = {m: _run(lib, w_dev, prompt, true, pred, m, 2, budget=budget) for m in ("naive", "fifo", "infinite")}
-    runs["full"] = _run(lib, w_dev, prompt, true, pred, "full", 8)
-    return dict(w=w, w_dev=w_dev, prompt=prompt, true=true, pred=pred, runs=runs, budget=budget)
+    runs = {m: _run(lib, w_dev, prompt, true, pred, m, 2, budget=budget, impl=impl)
+            for m in ("naive", "fifo", "infinite")}
+    runs["full"] = _run(lib, w_dev, prompt, true, pred, "full", 8, impl=impl)
+    return dict(w=w, w_dev=w_dev, prompt=prompt, true=true, pred=pred, runs=runs, budget=budget, impl=impl)
 
 
 @pytest.mark.parametrize("mode", ["naive", "fifo", "infinite", "full"])
@@ -102,6 +105,7 @@ def test_tiny_schedule_bit_exact(tiny, mode):
     r = tiny["runs"][mode]
     ref = simulator.simulate(tiny["true"], mode, 2, pred=tiny["pred"], eps=0.1, page_tokens=16)
     assert r["stats"]["completed"] == 8 and r["stats"]["error"] == 0
+    assert r["stats"]["decode_impl"] == tiny["impl"]
     assert r["steps"] == ref.total_steps
     assert r["slots"].tolist() == ref.slot_table
     assert r["live"].tolist() == ref.live_pages
@@ -138,7 +142,7 @@ def test_tiny_teacher_forced_tokens_and_logits(tiny):
 
 def test_tiny_sampler_bit_exact_on_dumped_logits(lib, tiny):
     r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "infinite", 2,
-             budget=tiny["budget"], logits=True)
+             budget=tiny["budget"], logits=True, impl=tiny["impl"])
     toks = r["tokens"]
     slots = r["slots"]
     t_of = {}
@@ -166,7 +170,7 @@ def test_tiny_budget_error_and_prefix_phase(lib, tiny):
     assert e.value.status == lib.IS_ERR_BUDGET
     pred = predict_lengths(tiny["true"], "noisy", 0.3, seed=1, prefix_k=4)
     r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], pred, "infinite", 2, budget=tiny["budget"],
-             prefix_k=4, pt=4)
+             prefix_k=4, pt=4, impl=tiny["impl"])
     ref = simulator.simulate(tiny["true"], "infinite", 2, pred=pred, eps=0.1, prefix_k=4, page_tokens=4)
     assert r["steps"] == ref.total_steps
     assert r["slots"].tolist() == ref.slot_table
@@ -177,7 +181,8 @@ def test_tiny_budget_error_and_prefix_phase(lib, tiny):
 
 def test_tiny_rewards_and_advantages(lib, tiny):
     from oracle import grpo
-    cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", kv_budget_bytes=tiny["budget"], seed=SEED)
+    cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", kv_budget_bytes=tiny["budget"], seed=SEED,
+                          decode_impl=tiny["impl"])
     ctx = lib.Context(cfg, tiny["w_dev"])
     ctx.is_prefill(torch.as_tensor(tiny["prompt"], device="cuda"), 0)
     ctx.is_start_group(tiny["true"], tiny["pred"])

@@ -70,8 +70,9 @@ typedef struct {
   uint64_t seed;           /* Philox key (R11) */
   is_mode mode;
   int32_t decode_impl;     /* 0: persistent decode kernel, one launch for the whole layer stack
-                              (default; falls back to 1 when Hq/Hkv > 4 or the attention needs
-                              more than 64 partials per row); 1: one kernel per operator */
+                              (falls back to 1 when Hq/Hkv > 4 or the attention needs more than
+                              64 partials per row); 1: one kernel per operator (the Python
+                              binding's default) */
 } is_config;
 
 /* Alg. 2 output plus the runtime plan (Alg. 1, Alg. 3).  All arrays are
@@ -208,6 +209,13 @@ is_status is_dbg_gemm(const void* d_w, const void* d_x, float* d_y, int32_t M, i
  * | task}).  Any destination may be NULL.  Synchronises the stream. */
 is_status is_dbg_mk_trace(is_ctx* ctx, int32_t* h_tasks, int32_t task_cap, int32_t* h_off, int32_t off_cap,
                           uint64_t* h_trace, int64_t trace_cap, int32_t* h_info);
+
+/* Debug: copy an internal activation buffer to the host (0 q [rc][Hq][128] bf16,
+ * 1 residual [rc][H] f32, 2 persistent-kernel post-attention residual, 3 final
+ * normalised rows [rc][H] bf16, 4 attention output [rc][Hq*128] bf16, 5 the
+ * persistent kernel's swizzled attention operand, 6 SwiGLU activations, 7 their
+ * swizzled copy).  Synchronises the stream. */
+is_status is_dbg_copy(is_ctx* ctx, int32_t which, void* h_dst, int64_t bytes);
 
 const char* is_last_error(void);
 const char* is_version(void);

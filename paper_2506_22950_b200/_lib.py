@@ -18,7 +18,7 @@ ADV_MODES = {"std_norm": 0, "mean_only": 1}
 EXPORTS = ["is_plan", "is_create", "is_destroy", "is_prefill", "is_start_group", "is_decode_step",
            "is_refill", "is_run_group", "is_query", "is_copy_tokens", "is_copy_schedule",
            "is_group_results", "is_group_advantages", "is_set_logits_dump", "is_profile_step",
-           "is_dbg_gemm", "is_dbg_mk_trace", "is_last_error", "is_version"]
+           "is_dbg_gemm", "is_dbg_mk_trace", "is_dbg_copy", "is_last_error", "is_version"]
 
 
 class InfsampError(RuntimeError):
@@ -104,6 +104,7 @@ def load(build_if_missing=True):
     L.is_profile_step.argtypes = [vp, vp, vp, i32, ctypes.POINTER(i32)]
     L.is_dbg_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]
     L.is_dbg_mk_trace.argtypes = [vp, vp, i32, vp, i32, vp, ctypes.c_int64, vp]
+    L.is_dbg_copy.argtypes = [vp, i32, vp, ctypes.c_int64]
     L.is_last_error.restype = ctypes.c_char_p
     L.is_last_error.argtypes = []
     L.is_version.restype = ctypes.c_char_p
@@ -125,8 +126,8 @@ def _np_ptr(a):
 
 def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix_k=0, page_tokens=16,
                 row_capacity=0, kv_budget_bytes=0, eps=0.1, temperature=0.8, seed=20261017, decode_impl=None):
-    """decode_impl: 0 = persistent decode kernel (default), 1 = one kernel per operator;
-    None reads IS_DECODE_IMPL from the environment (default 0)."""
+    """decode_impl: 0 = persistent decode kernel, 1 = one kernel per operator (default: it is
+    faster on B200); None reads IS_DECODE_IMPL from the environment."""
     c = Config()
     c.shape = Shape(shape.layers, shape.hidden, shape.n_q_heads, shape.n_kv_heads, shape.head_dim, shape.ffn,
                     shape.vocab, shape.rms_eps, shape.rope_theta)
@@ -135,7 +136,7 @@ def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix
     c.kv_budget_bytes, c.eps, c.temperature, c.seed = kv_budget_bytes, eps, temperature, seed
     c.mode = MODES[mode] if isinstance(mode, str) else int(mode)
     if decode_impl is None:
-        decode_impl = int(os.environ.get("IS_DECODE_IMPL", "0"))
+        decode_impl = int(os.environ.get("IS_DECODE_IMPL", "1"))
     c.decode_impl = decode_impl
     return c
 
@@ -282,6 +283,11 @@ class Context:
         _check(load().is_dbg_mk_trace(self._h, _np_ptr(tasks), tasks.size, _np_ptr(off), off.size,
                                       _np_ptr(trace) if cap else None, trace.size if cap else 0, _np_ptr(info)))
         return tasks, off, trace
+
+    def is_dbg_copy(self, which, nbytes):
+        out = np.zeros(nbytes, np.uint8)
+        _check(load().is_dbg_copy(self._h, int(which), _np_ptr(out), nbytes))
+        return out
 
     def is_profile_step(self, cap=4096):
         ms = np.zeros(cap, np.float32)

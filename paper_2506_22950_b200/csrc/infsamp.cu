@@ -710,17 +710,21 @@ static is_status mk_launch_t(is_ctx* c, cudaStream_t st) {
     attr = c->mk_smem;
   }
   cudaLaunchConfig_t cfg{};
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   cfg.gridDim = dim3(c->mk_grid);
   cfg.blockDim = dim3(kMkThreads);
   cfg.dynamicSmemBytes = c->mk_smem;
   cfg.stream = st;
-  cfg.numAttrs = 0;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kCS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
   if (g_use_pdl) {
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 2;
   }
   CK(cudaLaunchKernelEx(&cfg, kern, c->mka));
   return IS_OK;
@@ -775,8 +779,8 @@ static is_status setup_mega(is_ctx* c, const void* const* dw) {
     g.M = Ms[i];
     g.KB = Ks[i] / 64;
     g.T = (int)ceil_div64(g.M, 128);
-    g.S = std::max(1, std::min(g.KB, (g.KB + unit_kb / 2) / unit_kb));
-    if (g.S > 255) g.S = 255;
+    g.S = kCS;  // K split across the 4 CTAs of a cluster (partials exchanged over DSMEM)
+    (void)unit_kb;
     g.w_off = w_off;
     w_off += (long long)g.T * g.KB * 128 * 64;
     g.ws_off = ws_off;
@@ -798,6 +802,8 @@ static is_status setup_mega(is_ctx* c, const void* const* dw) {
   float* post_norm = (float*)A((size_t)L * H * 4);
   float* qn = (float*)A((size_t)L * 128 * 4);
   float* kn = (float*)A((size_t)L * 128 * 4);
+  __nv_bfloat16* in_bf = (__nv_bfloat16*)A((size_t)L * H * 2);
+  __nv_bfloat16* post_bf = (__nv_bfloat16*)A((size_t)L * H * 2);
   if (err != IS_OK) return err;
   for (int l = 0; l < L; ++l) {
     const void* const* p = dw + 2 + 11 * l;
@@ -805,6 +811,8 @@ static is_status setup_mega(is_ctx* c, const void* const* dw) {
     bf16_to_f32_kernel<<<(H + 255) / 256, 256>>>((const __nv_bfloat16*)p[7], post_norm + (size_t)l * H, H);
     bf16_to_f32_kernel<<<1, 128>>>((const __nv_bfloat16*)p[4], qn + l * 128, 128);
     bf16_to_f32_kernel<<<1, 128>>>((const __nv_bfloat16*)p[5], kn + l * 128, 128);
+    CK(cudaMemcpy(in_bf + (size_t)l * H, p[0], (size_t)H * 2, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(post_bf + (size_t)l * H, p[7], (size_t)H * 2, cudaMemcpyDeviceToDevice));
   }
   CK(cudaGetLastError());
   // ---- activations
@@ -812,8 +820,6 @@ static is_status setup_mega(is_ctx* c, const void* const* dw) {
   a.resid0 = c->resid;
   a.resid1 = (float*)A((size_t)rc * H * 4);
   a.ssq = (float*)A((size_t)(2 * L + 1) * a.Th * rc * 4);
-  a.xgA = (__nv_bfloat16*)A((size_t)H * BN * 2);
-  a.xgB = (__nv_bfloat16*)A((size_t)H * BN * 2);
   a.attn_sw = (__nv_bfloat16*)A((size_t)Hq * 128 * BN * 2);
   a.act_sw = (__nv_bfloat16*)A((size_t)F * BN * 2);
   a.ws = (float*)A((size_t)std::max(ws_off, 1ll) * 4);
@@ -845,10 +851,49 @@ static is_status setup_mega(is_ctx* c, const void* const* dw) {
     a.trace = (unsigned long long*)A((size_t)g_num_sms * 4 * a.trace_cap * 16);
   }
   if (err != IS_OK) return err;
-  // ---- static per-CTA task lists (global order: EMBED, per layer QKV ATT O GU DN, FINAL)
+  // ---- grid: every CTA co-resident, clusters of kCS
   int dev = 0;
   CK(cudaGetDevice(&dev));
-  const int grid = g_num_sms;
+  int maxsm = 0;
+  CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  a.scratch = mk_scratch_of(BN, REP);
+  a.nb = BN == 16 ? 8 : (BN == 32 ? 6 : 4);
+  const int fixed = 1024 + 2 * a.nb * BN * 128 + 2 * (kCS * 128 * (BN / kCS) * 4) + 2 * a.scratch + 1024;
+  a.na = std::min(16, (maxsm - fixed) / kMkStage);
+  if (const char* e = getenv("IS_MK_STAGES")) a.na = std::max(2, std::min(a.na, atoi(e)));
+  if (a.na < 3) return fail(IS_ERR_CONFIG, "persistent decode kernel: not enough shared memory");
+  c->mk_smem = fixed + a.na * kMkStage;
+  int nclusters = 0;
+  {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    cfg.gridDim = dim3(kCS * (g_num_sms / kCS));
+    cfg.blockDim = dim3(kMkThreads);
+    cfg.dynamicSmemBytes = c->mk_smem;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kCS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    switch (BN * 16 + REP) {
+#define IS_OCC(B, R) \
+  case B * 16 + R: { \
+    CK(cudaFuncSetAttribute(mk_decode_kernel<B, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->mk_smem)); \
+    CK(cudaFuncSetAttribute(mk_decode_kernel<B, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)); \
+    CK(cudaOccupancyMaxActiveClusters(&nclusters, mk_decode_kernel<B, R>, &cfg)); \
+    break; }
+      IS_OCC(16, 1) IS_OCC(16, 2) IS_OCC(16, 4) IS_OCC(32, 1) IS_OCC(32, 2) IS_OCC(32, 4) IS_OCC(64, 1) IS_OCC(64, 2) IS_OCC(64, 4)
+#undef IS_OCC
+    }
+  }
+  nclusters = std::min(nclusters, g_num_sms / kCS);
+  if (const char* e = getenv("IS_MK_CLUSTERS")) nclusters = std::max(1, std::min(nclusters, atoi(e)));
+  if (nclusters < 1) return fail(IS_ERR_CONFIG, "persistent decode kernel: no co-resident cluster (smem %d)", c->mk_smem);
+  const int grid = kCS * nclusters;
+  // ---- static per-CTA task lists (global order: EMBED, per layer QKV ATT O GU DN, FINAL).
+  //      A GEMM tile goes to one cluster, part p (K range p/kCS) to its CTA of rank p, so
+  //      the kCS CTAs of a cluster walk mirrored lists.
   std::vector<std::vector<int4>> tl(grid);
   for (int r = 0; r < rc; ++r) tl[r % grid].push_back(make_int4(MK_EMBED, r, 0, 0));
   long long u = 0;
@@ -856,10 +901,11 @@ static is_status setup_mega(is_ctx* c, const void* const* dw) {
   for (int l = 0; l < L; ++l) {
     for (int gi = 0; gi < 4; ++gi) {
       const MkGemm& g = a.g[gi];
-      for (int t = 0; t < g.T; ++t)
-        for (int p = 0; p < g.S; ++p)
-          tl[(u++) % grid].push_back(
-              make_int4(kinds[gi] | (l << 8) | (p << 16), t, p * g.KB / g.S, (p + 1) * g.KB / g.S));
+      for (int t = 0; t < g.T; ++t) {
+        const int cl = (int)((u++) % nclusters);
+        for (int p = 0; p < kCS; ++p)
+          tl[cl * kCS + p].push_back(make_int4(kinds[gi] | (l << 8) | (p << 16), t, p * g.KB / kCS, (p + 1) * g.KB / kCS));
+      }
       if (gi == 0)
         for (int b = 0; b < grid; ++b) tl[b].push_back(make_int4(MK_ATT | (l << 8), 0, 0, 0));
     }
@@ -878,17 +924,10 @@ static is_status setup_mega(is_ctx* c, const void* const* dw) {
   if (err != IS_OK) return err;
   CK(cudaMemcpy(d_tasks, flat.data(), flat.size() * sizeof(int4), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(d_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
-  // ---- shared memory: weight ring gets what the B rings and scratch leave
-  a.scratch = mk_scratch_of(BN, REP);
-  a.nb = BN == 16 ? 8 : (BN == 32 ? 6 : 4);
-  int maxsm = 0;
-  CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const int fixed = 1024 + 2 * a.nb * BN * 128 + 2 * a.scratch + 1024;
-  a.na = std::min(16, (maxsm - fixed) / kMkStage);
-  if (const char* e = getenv("IS_MK_STAGES")) a.na = std::max(2, std::min(a.na, atoi(e)));
-  if (a.na < 3) return fail(IS_ERR_CONFIG, "persistent decode kernel: not enough shared memory");
-  c->mk_smem = fixed + a.na * kMkStage;
   c->mk_grid = grid;
+  a.pf_units = 2;
+  a.nodeps = getenv("IS_MK_NODEPS") ? 1 : 0;
+  if (const char* e = getenv("IS_MK_PF")) a.pf_units = std::max(0, atoi(e));
   // ---- the rest of the arguments
   a.tasks = d_tasks;
   a.task_off = d_off;
@@ -904,6 +943,8 @@ static is_status setup_mega(is_ctx* c, const void* const* dw) {
   a.embed = c->embed;
   a.in_norm = in_norm;
   a.post_norm = post_norm;
+  a.in_norm_bf = in_bf;
+  a.post_norm_bf = post_bf;
   a.q_norm = qn;
   a.k_norm = kn;
   a.final_norm = c->final_norm;
@@ -926,18 +967,6 @@ static is_status setup_mega(is_ctx* c, const void* const* dw) {
   a.pt = c->pt;
   a.pcap = c->pcap;
   CK(cudaDeviceSynchronize());
-  // the kernel's CTAs must all be co-resident (they wait on each other)
-  int occ = 0;
-  switch (BN * 16 + REP) {
-#define IS_OCC(B, R) \
-  case B * 16 + R: { \
-    CK(cudaFuncSetAttribute(mk_decode_kernel<B, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->mk_smem)); \
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mk_decode_kernel<B, R>, kMkThreads, c->mk_smem)); \
-    break; }
-    IS_OCC(16, 1) IS_OCC(16, 2) IS_OCC(16, 4) IS_OCC(32, 1) IS_OCC(32, 2) IS_OCC(32, 4) IS_OCC(64, 1) IS_OCC(64, 2) IS_OCC(64, 4)
-#undef IS_OCC
-  }
-  if (occ < 1) return fail(IS_ERR_CONFIG, "persistent decode kernel does not fit on an SM (smem %d)", c->mk_smem);
   c->mk = 1;
   return IS_OK;
 }
@@ -1624,5 +1653,28 @@ extern "C" is_status is_dbg_mk_trace(is_ctx* c, int32_t* h_tasks, int32_t task_c
     CK(cudaMemcpy(h_off, c->mka.task_off, (size_t)(c->mk_grid + 1) * 4, cudaMemcpyDeviceToHost));
   const int64_t n = (int64_t)c->mk_grid * 4 * c->mka.trace_cap * 2;
   if (h_trace && c->mka.trace && trace_cap >= n) CK(cudaMemcpy(h_trace, c->mka.trace, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  return IS_OK;
+}
+
+extern "C" is_status is_dbg_copy(is_ctx* c, int32_t which, void* h_dst, int64_t bytes) {
+  if (!c || !h_dst) return fail(IS_ERR_CONFIG, "null argument");
+  CK(cudaStreamSynchronize(c->st));
+  const is_shape& s = c->sh;
+  const void* src = nullptr;
+  int64_t n = 0;
+  switch (which) {
+    case 0: src = c->q; n = (int64_t)c->rc * s.n_q_heads * 128 * 2; break;
+    case 1: src = c->resid; n = (int64_t)c->rc * s.hidden * 4; break;
+    case 2: src = c->mk ? (const void*)c->mka.resid1 : nullptr; n = (int64_t)c->rc * s.hidden * 4; break;
+    case 3: src = c->xn; n = (int64_t)c->rc * s.hidden * 2; break;
+    case 4: src = c->attn; n = (int64_t)c->rc * s.n_q_heads * 128 * 2; break;
+    case 5: src = c->mk ? (const void*)c->mka.attn_sw : nullptr; n = (int64_t)c->BN * s.n_q_heads * 128 * 2; break;
+    case 6: src = c->act; n = (int64_t)c->rc * s.ffn * 2; break;
+    case 7: src = c->mk ? (const void*)c->mka.act_sw : nullptr; n = (int64_t)c->BN * s.ffn * 2; break;
+    default: return fail(IS_ERR_CONFIG, "unknown buffer %d", which);
+  }
+  if (!src) return fail(IS_ERR_STATE, "buffer %d not in use", which);
+  if (bytes < n) return fail(IS_ERR_CAPACITY, "need %lld bytes", (long long)n);
+  CK(cudaMemcpy(h_dst, src, (size_t)n, cudaMemcpyDeviceToHost));
   return IS_OK;
 }

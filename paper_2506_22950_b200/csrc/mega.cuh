@@ -81,10 +81,10 @@ struct MkArgs {
   float eps, scale;
   const __nv_bfloat16* embed;  // [V][H]
   const float *in_norm, *post_norm, *q_norm, *k_norm, *final_norm;  // [L][H], [L][H], [L][128], [L][128], [H]
+  const __nv_bfloat16 *in_norm_bf, *post_norm_bf;                     // the same gains as bf16 (exact) [L][H]
   const float *rope_cos, *rope_sin;
   const int32_t *row_active, *row_tok, *row_pos, *row_kvloc, *row_len, *row_lid;
   float *resid0, *resid1, *ssq;   // [rc][H] x2, [2L+1][Th][rc]
-  __nv_bfloat16 *xgA, *xgB;       // swizzled bf16(x * gain): QKV / GU inputs [H/64][BN][64]
   __nv_bfloat16 *attn_sw, *act_sw;  // O / DN inputs [Hq*128/64][BN][64], [F/64][BN][64]
   __nv_bfloat16 *q, *xn_final;    // [rc][Hq][128], [rows][H] (lm_head input, row-major)
   float* ws;                      // split-K partials
@@ -98,6 +98,8 @@ struct MkArgs {
   int* sync;
   MkSync so;
   unsigned long long* clock;      // [2]: accumulated kernel ns, launches (CTA 0)
+  int pf_units;                   // GEMM units of weights prefetched into L2 ahead of the ring
+  int nodeps;                     // timing experiment only (IS_MK_NODEPS): skip every dependency wait
   unsigned long long* trace;      // debug (IS_MK_TRACE): [grid][4 roles][trace_cap][2] (globaltimer, code)
   int trace_cap;
 };
@@ -148,6 +150,10 @@ IS_DEVICE void spin_ge(const int* p, int target, int tag) {
     if (gtimer() - t0 > kMkTimeoutNs) mk_trap("counter", tag, target);
   }
 }
+#define mk_spin(a, p, t, tag) \
+  do {                         \
+    if (!(a).nodeps) spin_ge((p), (t), (tag)); \
+  } while (0)
 IS_DEVICE bool mbar_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -172,6 +178,9 @@ IS_DEVICE void bulk_g2s_hint(void* smem, const void* gmem, uint32_t bytes, uint6
       "l"(gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(hint)
       : "memory");
 }
+IS_DEVICE void prefetch_l2(const void* gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem), "r"(bytes) : "memory");
+}
 IS_DEVICE void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 IS_DEVICE void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 // named barrier of one compute warp group (128 threads)
@@ -195,7 +204,7 @@ struct MkScratch {
   static constexpr int kComb = 4 * REP * (kHD + 2) * 4;
   static constexpr int kEpi = kStg + kRed;
   static constexpr int kAtt = kKV + kQ + kComb;
-  static constexpr int kCtl = 1024 + 5 * 256;  // rs, rows, cum, ctl | row tables (active, pos, kvloc, len, lid)
+  static constexpr int kCtl = 1024 + 5 * 256 + 2048;  // rs, rows, cum, ctl | row tables | gains (bf16, 16 k-blocks)
   static constexpr int v = (((kEpi > kAtt ? kEpi : kAtt) + kCtl) + 1023) / 1024 * 1024;
 };
 
@@ -208,6 +217,7 @@ struct MkWG {
   float* rs;
   int *rows, *cum, *ctl;
   int *ract, *rpos, *rkv, *rlen, *rlid;  // this step's row tables (static during the kernel)
+  __nv_bfloat16* gsm;                    // RMSNorm gains of the current unit's K range
   IS_DEVICE void init(uint8_t* base) {
     using S = MkScratch<BN, REP>;
     stg = reinterpret_cast<float*>(base);
@@ -226,6 +236,7 @@ struct MkWG {
     rkv = rpos + 64;
     rlen = rkv + 64;
     rlid = rlen + 64;
+    gsm = reinterpret_cast<__nv_bfloat16*>(rlid + 64);
   }
 };
 
@@ -364,14 +375,10 @@ IS_DEVICE void mk_att_unit(const MkArgs& a, MkWG<BN, REP>& S, int l, int u, int 
   }
   const bool prefix = r < 0;
   if (wt == 0) {
-    // inputs: q tiles of kv head h (+ its k / v tiles: the current token's KV append)
-    for (int e = 0; e < REP; ++e) spin_ge(sl + a.so.qkv_flag + h * REP + e, 1, 100 + l);
-    if (!prefix) {
-      spin_ge(sl + a.so.qkv_flag + a.Hq + h, 1, 200 + l);
-      spin_ge(sl + a.so.qkv_flag + a.Hq + a.Hkv + h, 1, 300 + l);
-      fence_proxy_async_global();
-    }
     fence_proxy_async_smem();  // generic writes to this scratch precede the bulk copies below
+    // static K / V first: the shared prefix, and suffix chunks that do not hold this step's token
+    const int len = prefix ? 0 : S.rlen[r];
+    const bool cur = !prefix && (len - 1) / kMkSC == c;  // chunk holds the token appended this step
     if (prefix) {
       const int tok0 = c * kMkPC, ntok = min(kMkPC, a.pcap - tok0);
       const uint32_t bytes = (uint32_t)ntok * kHD * 2;
@@ -379,8 +386,15 @@ IS_DEVICE void mk_att_unit(const MkArgs& a, MkWG<BN, REP>& S, int l, int u, int 
       mbar_arrive_expect_tx(attbar, 2 * bytes);
       bulk_g2s_hint(S.Ks, kp, bytes, attbar, kEvictNormal);
       bulk_g2s_hint(S.Vs, kp + (size_t)a.Hkv * a.pcap * kHD, bytes, attbar, kEvictNormal);
-    } else {
-      const int len = S.rlen[r];
+    }
+    // inputs: q tiles of kv head h (+ its k / v tiles when the chunk holds the appended token)
+    for (int e = 0; e < REP; ++e) mk_spin(a, sl + a.so.qkv_flag + h * REP + e, 4, 100 + l);
+    if (cur) {
+      mk_spin(a, sl + a.so.qkv_flag + a.Hq + h, 4, 200 + l);
+      mk_spin(a, sl + a.so.qkv_flag + a.Hq + a.Hkv + h, 4, 300 + l);
+      fence_proxy_async_global();
+    }
+    if (!prefix) {
       const int tok0 = c * kMkSC, tend = min(tok0 + kMkSC, len);
       const int lid = S.rlid[r];
       const __nv_bfloat16* pl = a.pool + (size_t)l * a.pool_layer;
@@ -491,14 +505,29 @@ IS_DEVICE void mk_att_unit(const MkArgs& a, MkWG<BN, REP>& S, int l, int u, int 
 }
 
 // ---------------------------------------------------------------- the kernel
+constexpr int kCS = 4;  // thread-block cluster size == K split of every GEMM unit
+
+IS_DEVICE void st_async_v4(uint32_t remote_addr, float4 v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   remote_addr),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(remote_bar)
+               : "memory");
+}
+IS_DEVICE void mbar_arrive_remote(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+}
+
 template <int BN, int REP>
 __global__ void __launch_bounds__(kMkThreads, 1) mk_decode_kernel(const __grid_constant__ MkArgs a) {
   extern __shared__ uint8_t mk_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(mk_raw) + 1023) & ~uintptr_t(1023));
   constexpr int kBStage = BN * 128;
+  constexpr int kSlice = BN / kCS;                 // decode rows owned by each CTA of the cluster
+  constexpr int kRecv = kCS * 128 * kSlice * 4;    // per WG: [src][128 m][kSlice] fp32
   uint8_t* ringA = sm;
   uint8_t* ringB = ringA + (size_t)a.na * kMkStage;
-  uint8_t* scratch = ringB + (size_t)2 * a.nb * kBStage;
+  float* recv = reinterpret_cast<float*>(ringB + (size_t)2 * a.nb * kBStage);
+  uint8_t* scratch = reinterpret_cast<uint8_t*>(recv) + 2 * kRecv;
   uint64_t* bars = reinterpret_cast<uint64_t*>(scratch + 2 * a.scratch);
   uint64_t* afull = bars;
   uint64_t* aempty = afull + a.na;
@@ -507,10 +536,14 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_decode_kernel(const __grid_c
   uint64_t* tfull = bempty + 2 * a.nb;  // [2]
   uint64_t* tempty = tfull + 2;
   uint64_t* attbar = tempty + 2;        // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(attbar + 2);
+  uint64_t* rfull = attbar + 2;         // [2] partial slices received (tx bytes)
+  uint64_t* rfree = rfull + 2;          // [2] every receiver has consumed our previous slices
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfree + 2);
   constexpr uint32_t kTmemCols = (2 * BN) <= 32 ? 32 : ((2 * BN) <= 64 ? 64 : 128);
+  constexpr uint32_t kRecvTx = kCS * 128 * kSlice * 4;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_ctarank();
   unsigned long long t_start = 0;
   if (threadIdx.x == 0) {
     t_start = gtimer();
@@ -526,12 +559,18 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_decode_kernel(const __grid_c
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4);
       mbar_init(&attbar[i], 1);
+      mbar_init(&rfull[i], 1);
+      mbar_init(&rfree[i], kCS);
     }
     fence_barrier_init();
+    // arm the first exchange of each WG (the peers' bytes may land right after the cluster barrier)
+    mbar_arrive_expect_tx(&rfull[0], kRecvTx);
+    mbar_arrive_expect_tx(&rfull[1], kRecvTx);
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  cluster_sync();  // peers' barriers are initialised before any DSMEM traffic
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_launch_dependents();
@@ -540,23 +579,44 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_decode_kernel(const __grid_c
 
   if (warp == 0) {
     // ---------------------------------------------------------- weight producer
+    // Streams this CTA's weight tiles into the smem ring and, ahead of it, issues
+    // L2 prefetches of the next units' weight ranges (a.pf_units units ahead), so
+    // HBM keeps streaming while the ring waits on a dependency.
     if (lane == 0) {
-      int s = 0, nrec = 0;
+      int s = 0, nrec = 0, pf_next = 0, pf_done = 0;
       uint32_t ph = 0;
-      for (int i = 0; i < nt; ++i) {
+      auto unit_range = [&](int i, const __nv_bfloat16*& base, uint32_t& bytes) -> bool {
         const int4 tk = T[i];
         const int kind = tk.x & 0xFF;
-        if (kind == MK_EMBED || kind == MK_ATT || kind == MK_FINAL) continue;
-        mk_rec(a, 2, nrec, 7, i);
+        if (kind == MK_EMBED || kind == MK_ATT || kind == MK_FINAL) return false;
         const int gi = kind == MK_QKV ? 0 : kind - 2;  // O 1, GU 2, DN 3
         const MkGemm& g = a.g[gi];
         const int l = (tk.x >> 8) & 0xFF;
-        const __nv_bfloat16* base = a.wpk + (size_t)l * a.layer_stride + g.w_off + (size_t)tk.y * g.KB * (kMkStage / 2);
-        for (int kb = tk.z; kb < tk.w; ++kb) {
+        base = a.wpk + (size_t)l * a.layer_stride + g.w_off + ((size_t)tk.y * g.KB + tk.z) * (kMkStage / 2);
+        bytes = (uint32_t)(tk.w - tk.z) * kMkStage;
+        return true;
+      };
+      for (int i = 0; i < nt; ++i) {
+        const __nv_bfloat16* base;
+        uint32_t bytes;
+        if (!unit_range(i, base, bytes)) continue;
+        // keep pf_units GEMM units prefetched beyond this one
+        if (pf_next <= i) pf_next = i + 1;
+        while (pf_next < nt && pf_done < a.pf_units) {
+          const __nv_bfloat16* pb;
+          uint32_t pbytes;
+          if (unit_range(pf_next, pb, pbytes) && pbytes > 0) {
+            prefetch_l2(pb, pbytes);
+            ++pf_done;
+          }
+          ++pf_next;
+        }
+        if (pf_done > 0) --pf_done;  // unit i leaves the prefetch window
+        mk_rec(a, 2, nrec, 7, i);
+        for (uint32_t off = 0; off < bytes; off += kMkStage) {
           mk_wait(&aempty[s], ph ^ 1, 1);
           mbar_arrive_expect_tx(&afull[s], kMkStage);
-          bulk_g2s_hint(ringA + (size_t)s * kMkStage, base + (size_t)kb * (kMkStage / 2), kMkStage, &afull[s],
-                        kEvictFirst);
+          bulk_g2s_hint(ringA + (size_t)s * kMkStage, base + off / 2, kMkStage, &afull[s], kEvictFirst);
           if (++s == a.na) {
             s = 0;
             ph ^= 1;
@@ -584,7 +644,10 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_decode_kernel(const __grid_c
       const uint32_t d_tmem = tmem_base + w * BN;
       for (int kb = tk.z; kb < tk.w; ++kb) {
         mk_wait(&afull[s], ph, 3);
+        if (lane == 0 && kb == tk.z) mk_rec(a, 3, nrec, 18, i);
         mk_wait(&bfull[w * a.nb + bs], bph, 4);
+        if (lane == 0 && kb == tk.z) mk_rec(a, 3, nrec, 19, i);
+        if (lane == 0 && kb == tk.w - 1) mk_rec(a, 3, nrec, 20, i);
         tc_fence_after();
         if (lane == 0) {
           const uint64_t da = smem_desc_k_sw128(ringA + (size_t)s * kMkStage);
@@ -605,7 +668,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_decode_kernel(const __grid_c
         }
       }
       if (lane == 0) {
-        tc_commit(&tfull[w]);
+        tc_commit(&tfull[w]);  // (an empty K range commits immediately; the WG then uses zeros)
         mk_rec(a, 3, nrec, 9, i);
       }
       __syncwarp();
@@ -623,7 +686,11 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_decode_kernel(const __grid_c
     uint8_t* myB = ringB + (size_t)wg * a.nb * kBStage;
     uint64_t* myBfull = bfull + wg * a.nb;
     uint64_t* myBempty = bempty + wg * a.nb;
-    int bs = 0, use = 0, jg = 0, nrec = 0;
+    float* myRecv = recv + (size_t)wg * (kRecv / 4);
+    const uint32_t recv_local = smem_u32(myRecv);
+    const uint32_t rfull_local = smem_u32(&rfull[wg]);
+    const uint32_t rfree_local = smem_u32(&rfree[wg]);
+    int bs = 0, use = 0, jg = 0, nrec = 0, xuse = 0;
     uint32_t bph = 0, attph = 0;
     pdl_wait();  // rows, tokens and page tables come from the scheduler kernel
     if (wt < a.rc) {
@@ -644,33 +711,28 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_decode_kernel(const __grid_c
       int* sl = a.sync + (size_t)l * a.so.stride;
       if (kind == MK_EMBED) {
         if (wg != 0) continue;
-        // resid0[r] = E[tok] (fp32), xgA = bf16(x * in_norm[0]), ssq[0][t][r]
+        // resid0[r] = E[tok] (fp32) and per-128-column sums of squares ssq[0][t][r]
         const int r = tk.y;
         const bool act = S.ract[r] != 0;
         const int tok = act ? __ldg(a.row_tok + r) : 0;
 #pragma unroll 1
         for (int t0 = 0; t0 < a.Th; t0 += 8) {
-          float xe[8], ge[8];
+          float xe[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int k = (t0 + j) * 128 + wt;
             xe[j] = (t0 + j < a.Th && k < a.H && act) ? __bfloat162float(a.embed[(size_t)tok * a.H + k]) : 0.f;
-            ge[j] = (t0 + j < a.Th && k < a.H) ? __ldg(a.in_norm + k) : 0.f;
           }
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int k = (t0 + j) * 128 + wt;
-            if (t0 + j < a.Th && k < a.H) {
-              a.resid0[(size_t)r * a.H + k] = xe[j];
-              a.xgA[sw_off(r, k, BN)] = __float2bfloat16_rn(xe[j] * ge[j]);
-            }
+            if (t0 + j < a.Th && k < a.H) __stcg(a.resid0 + (size_t)r * a.H + k, xe[j]);
             const float ss = warp_sum(xe[j] * xe[j]);
             if (lane == 0 && t0 + j < a.Th) S.sred[wwarp * 64 + t0 + j] = ss;
           }
         }
         wg_bar(wg);
-        if (wt < a.Th) a.ssq[((size_t)0 * a.Th + wt) * a.rc + r] = S.sred[wt] + S.sred[64 + wt] + S.sred[128 + wt] + S.sred[192 + wt];
-        fence_proxy_async_global();
+        if (wt < a.Th) __stcg(a.ssq + (size_t)wt * a.rc + r, S.sred[wt] + S.sred[64 + wt] + S.sred[128 + wt] + S.sred[192 + wt]);
         __threadfence();
         wg_bar(wg);
         if (wt == 0) red_release_add(a.sync + a.so.emb_done, 1);
@@ -679,7 +741,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_decode_kernel(const __grid_c
       if (kind == MK_FINAL) {
         if (wg != 0) continue;
         const int r = tk.y;
-        if (wt == 0) spin_ge(a.sync + (size_t)(a.L - 1) * a.so.stride + a.so.dn_done, a.g[3].T, 900);
+        if (wt == 0) mk_spin(a, a.sync + (size_t)(a.L - 1) * a.so.stride + a.so.dn_done, a.g[3].T * kCS, 900);
         wg_bar(wg);
         if (wt == 0) {
           const float* s = a.ssq + (size_t)(2 * a.L) * a.Th * a.rc + r;
@@ -689,6 +751,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_decode_kernel(const __grid_c
         }
         wg_bar(wg);
         const float rsv = S.rs[0];
+#pragma unroll 4
         for (int k = wt; k < a.H; k += 128)
           a.xn_final[(size_t)r * a.H + k] =
               __float2bfloat16_rn(__ldcg(a.resid0 + (size_t)r * a.H + k) * rsv * __ldg(a.final_norm + k));
@@ -723,157 +786,226 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_decode_kernel(const __grid_c
         }
         continue;
       }
-      // ---------------------------------------------------------- GEMM unit
+      // ---------------------------------------------------------- GEMM unit (part `rank` of a cluster tile)
       if (((jg++) & 1) != wg) continue;
       const int gi = kind == MK_QKV ? 0 : kind - 2;
-      const MkGemm& g = a.g[gi];
-      const int tile = tk.y, kb0 = tk.z, kb1 = tk.w, part = (tk.x >> 16) & 0xFF;
+      const int tile = tk.y, kb0 = tk.z, kb1 = tk.w;
+      const int n_lo = rank * kSlice;
+      const int gm = tile * 128 + m;
       if (wt == 0) mk_rec(a, wg, nrec, 1, i);
+      // 0. static epilogue operands, loaded before anything waits
+      float gq = 0.f, cs[kSlice], sn[kSlice];
+      if (kind == MK_QKV) {
+        const bool is_q = tile < a.Hq, is_v = tile >= a.Hq + a.Hkv;
+        gq = is_v ? 1.f : (is_q ? __ldg(a.q_norm + l * 128 + m) : __ldg(a.k_norm + l * 128 + m));
+#pragma unroll
+        for (int j = 0; j < kSlice; ++j) {
+          const int n = n_lo + j;
+          const bool need = !is_v && n < a.rc && S.ract[n];
+          const int pos = need ? S.rpos[n] : 0;
+          cs[j] = need ? __ldg(a.rope_cos + (size_t)pos * 64 + (m & 63)) : 1.f;
+          sn[j] = need ? __ldg(a.rope_sin + (size_t)pos * 64 + (m & 63)) : 0.f;
+        }
+      }
+      // gains of this unit's K range -> smem (static data: issued before any wait)
+      const bool norm_fill = (kind == MK_QKV || kind == MK_GU) && kb1 > kb0;
+      if (norm_fill && wt == 0) {
+        const __nv_bfloat16* gain = (kind == MK_QKV ? a.in_norm_bf : a.post_norm_bf) + (size_t)l * a.H;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&attbar[wg], (uint32_t)(kb1 - kb0) * 128);
+        bulk_g2s_hint(S.gsm, gain + kb0 * 64, (uint32_t)(kb1 - kb0) * 128, &attbar[wg], kEvictNormal);
+      }
       // 1. inputs ready
       if (wt == 0) {
         if (kind == MK_QKV) {
-          if (l == 0) spin_ge(a.sync + a.so.emb_done, a.rc, 400);
-          else spin_ge(a.sync + (size_t)(l - 1) * a.so.stride + a.so.dn_done, a.g[3].T, 500 + l);
+          if (l == 0) mk_spin(a, a.sync + a.so.emb_done, a.rc, 400);
+          else mk_spin(a, a.sync + (size_t)(l - 1) * a.so.stride + a.so.dn_done, a.g[3].T * kCS, 500 + l);
         } else if (kind == MK_O) {
-          const int REPc = a.Hq / a.Hkv;
-          const int h0 = (kb0 * 64) / kHD / REPc, h1 = (kb1 * 64 - 1) / kHD / REPc;
-          for (int h = h0; h <= h1; ++h) spin_ge(sl + a.so.att_done + h, n_active, 600 + l);
+          const int h0 = (kb0 * 64) / kHD / REP, h1 = (max(kb1, kb0 + 1) * 64 - 1) / kHD / REP;
+          for (int h = h0; h <= h1; ++h) mk_spin(a, sl + a.so.att_done + h, n_active, 600 + l);
         } else if (kind == MK_GU) {
-          spin_ge(sl + a.so.o_done, a.g[1].T, 700 + l);
+          mk_spin(a, sl + a.so.o_done, a.g[1].T * kCS, 700 + l);
         } else {
-          for (int t = kb0; t < kb1; ++t) spin_ge(sl + a.so.gu_flag + t, 1, 800 + l);
+          for (int t = kb0; t < kb1; ++t) mk_spin(a, sl + a.so.gu_flag + t, kCS, 800 + l);
+          // an empty K range still reads the post-attention residual in its epilogue
+          if (kb1 == kb0) mk_spin(a, sl + a.so.o_done, a.g[1].T * kCS, 850 + l);
         }
         fence_proxy_async_global();
         mk_rec(a, wg, nrec, 2, i);
-        // 2. activation k-blocks -> this WG's B ring (already in the MMA layout)
-        const __nv_bfloat16* src = kind == MK_QKV ? a.xgA : kind == MK_O ? a.attn_sw : kind == MK_GU ? a.xgB : a.act_sw;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mk_wait(&myBempty[bs], bph ^ 1, 5);
-          mbar_arrive_expect_tx(&myBfull[bs], kBStage);
-          bulk_g2s_hint(myB + (size_t)bs * kBStage, src + (size_t)kb * BN * 64, kBStage, &myBfull[bs], kEvictLast);
-          if (++bs == a.nb) {
-            bs = 0;
-            bph ^= 1;
+      }
+      wg_bar(wg);
+      // 2. activation operand -> this WG's B ring (128-byte-swizzled K-major rows)
+      if (kind == MK_O || kind == MK_DN) {
+        if (wt == 0) {
+          const __nv_bfloat16* src = kind == MK_O ? a.attn_sw : a.act_sw;
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mk_wait(&myBempty[bs], bph ^ 1, 5);
+            mbar_arrive_expect_tx(&myBfull[bs], kBStage);
+            bulk_g2s_hint(myB + (size_t)bs * kBStage, src + (size_t)kb * BN * 64, kBStage, &myBfull[bs], kEvictLast);
+            if (++bs == a.nb) {
+              bs = 0;
+              bph ^= 1;
+            }
           }
         }
+      } else if (kb1 > kb0) {
+        // RMSNorm at rounding point r1: bf16(x * rs[row] * gain), normalised in fp32 here.
+        // One batch of loads (residual chunks, bf16 gains, the rows' sum-of-squares
+        // partials) per up to 8 k-blocks, all in flight together.
+        const float* rin = kind == MK_QKV ? a.resid0 : a.resid1;
+        constexpr int kPer = BN / 16;   // 16-byte chunks per thread per k-block
+        constexpr int kGrp = 8 / kPer;  // k-blocks per load batch
+        const int ch = wt & 7;          // this thread's 8-column chunk (same for all its rows)
+        bool rs_ready = false;
+        for (int g0 = kb0; g0 < kb1; g0 += kGrp) {
+          float4 xv[kGrp][kPer][2];
+#pragma unroll
+          for (int j = 0; j < kGrp; ++j) {
+            const int kb = g0 + j;
+#pragma unroll
+            for (int c = 0; c < kPer; ++c) {
+              const int row = (wt + 128 * c) >> 3;
+              const bool ok = kb < kb1 && row < a.rc;
+              const float4* src = reinterpret_cast<const float4*>(rin + (size_t)row * a.H + kb * 64 + ch * 8);
+              xv[j][c][0] = ok ? __ldcg(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+              xv[j][c][1] = ok ? __ldcg(src + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+          if (!rs_ready) {
+            mk_row_scale(a, kind == MK_QKV ? 2 * l : 2 * l + 1, S.rs, wt);
+            mk_wait(&attbar[wg], attph, 12);  // gains staged
+            attph ^= 1;
+            rs_ready = true;
+          }
+          if (wt == 0)
+            for (int j = 0; j < kGrp && g0 + j < kb1; ++j) mk_wait(&myBempty[(bs + j) % a.nb], (bs + j >= a.nb ? bph ^ 1 : bph) ^ 1, 5);
+          wg_bar(wg);  // rs[] ready, ring stages free
+          if (wt == 0) mk_rec(a, wg, nrec, 16, i);
+#pragma unroll
+          for (int j = 0; j < kGrp; ++j) {
+            const int kb = g0 + j;
+            if (kb >= kb1) break;
+            const int st = (bs + j) % a.nb;
+            const uint4 gvj = *reinterpret_cast<const uint4*>(S.gsm + (kb - kb0) * 64 + ch * 8);
+            const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gvj);
+            const float2 ga = __bfloat1622float2(g2[0]), gb = __bfloat1622float2(g2[1]);
+            const float2 gc = __bfloat1622float2(g2[2]), gd = __bfloat1622float2(g2[3]);
+#pragma unroll
+            for (int c = 0; c < kPer; ++c) {
+              const int row = (wt + 128 * c) >> 3;
+              const float r_ = row < a.rc ? S.rs[row] : 0.f;
+              const float4 x0 = xv[j][c][0], x1 = xv[j][c][1];
+              uint4 o;
+              __nv_bfloat162 hh;
+              hh = __floats2bfloat162_rn(x0.x * r_ * ga.x, x0.y * r_ * ga.y); o.x = *reinterpret_cast<uint32_t*>(&hh);
+              hh = __floats2bfloat162_rn(x0.z * r_ * gb.x, x0.w * r_ * gb.y); o.y = *reinterpret_cast<uint32_t*>(&hh);
+              hh = __floats2bfloat162_rn(x1.x * r_ * gc.x, x1.y * r_ * gc.y); o.z = *reinterpret_cast<uint32_t*>(&hh);
+              hh = __floats2bfloat162_rn(x1.z * r_ * gd.x, x1.w * r_ * gd.y); o.w = *reinterpret_cast<uint32_t*>(&hh);
+              *reinterpret_cast<uint4*>(myB + (size_t)st * kBStage + row * 128 + ((ch ^ (row & 7)) << 4)) = o;
+            }
+          }
+          fence_proxy_async_smem();
+          wg_bar(wg);
+          const int nk = min(kGrp, kb1 - g0);
+          if (wt == 0)
+            for (int j = 0; j < nk; ++j) mbar_arrive(&myBfull[(bs + j) % a.nb]);
+          if (wt == 0) mk_rec(a, wg, nrec, 17, i);
+          for (int j = 0; j < nk; ++j)
+            if (++bs == a.nb) {
+              bs = 0;
+              bph ^= 1;
+            }
+        }
       }
-      // 3. accumulator
+      // 3. epilogue operands that depend on earlier phases (loaded while the MMA runs)
+      float rin_v[kSlice];
+      if (kind == MK_O || kind == MK_DN) {
+        const float* rin = kind == MK_O ? a.resid0 : a.resid1;
+#pragma unroll
+        for (int j = 0; j < kSlice; ++j) {
+          const int n = n_lo + j;
+          rin_v[j] = (n < a.rc && gm < a.H) ? __ldcg(rin + (size_t)n * a.H + gm) : 0.f;
+        }
+      }
+      // 4. accumulator
       mk_wait(&tfull[wg], use & 1, 6);
       ++use;
       tc_fence_after();
       if (wt == 0) mk_rec(a, wg, nrec, 3, i);
       float v[BN];
+      if (kb1 > kb0) {
 #pragma unroll
-      for (int c = 0; c < BN / 16; ++c)
-        tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + wg * BN + c * 16, v + c * 16);
+        for (int c = 0; c < BN / 16; ++c)
+          tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + wg * BN + c * 16, v + c * 16);
+      } else {
+#pragma unroll
+        for (int n = 0; n < BN; ++n) v[n] = 0.f;
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[wg]);
-      // 4. split-K: partials through L2, the last arriving part reduces in part order
-      int* cnt = sl + (kind == MK_QKV ? a.so.qkv_cnt : kind == MK_O ? a.so.o_cnt : kind == MK_GU ? a.so.gu_cnt : a.so.dn_cnt) + tile;
-      if (g.S > 1) {
-        float* ws = a.ws + g.ws_off + (size_t)tile * g.S * 128 * BN;
+      // 5. split-K exchange inside the cluster: rank j receives column slice j of every
+      //    peer's partial over DSMEM (st.async, completion counted in bytes on its rfull)
+      if (xuse > 0) mk_wait(&rfree[wg], (xuse - 1) & 1, 7);
 #pragma unroll
-        for (int c4 = 0; c4 < BN / 4; ++c4)
-          __stcg(reinterpret_cast<float4*>(ws + ((size_t)part * 128 + m) * BN) + c4,
-                 make_float4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]));
-        __threadfence();
-        wg_bar(wg);
-        if (wt == 0) mk_rec(a, wg, nrec, 11, i);
-        if (wt == 0) S.ctl[3] = atom_acqrel_add(cnt, 1) == g.S - 1;
-        if (wt == 0) mk_rec(a, wg, nrec, 12, i);
-        wg_bar(wg);
-        if (!S.ctl[3]) {
-          if (wt == 0) mk_rec(a, wg, nrec, 4, i);
-          continue;
-        }
-#pragma unroll 1
-        for (int c4 = 0; c4 < BN / 4; ++c4) {
-          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 1
-          for (int p0 = 0; p0 < g.S; p0 += 8) {
-            float4 t4[8];
+      for (int j = 0; j < kCS; ++j) {
+        const uint32_t dst = mapa_shared(recv_local, j) + (uint32_t)(((rank * 128) + m) * kSlice * 4);
+        const uint32_t bar = mapa_shared(rfull_local, j);
 #pragma unroll
-            for (int p = 0; p < 8; ++p)
-              t4[p] = p0 + p < g.S ? __ldcg(reinterpret_cast<const float4*>(ws + ((size_t)(p0 + p) * 128 + m) * BN) + c4)
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int p = 0; p < 8; ++p)
-              if (p0 + p < g.S) {
-                if (p0 + p == 0) {
-                  acc = t4[0];
-                } else {
-                  acc.x += t4[p].x;
-                  acc.y += t4[p].y;
-                  acc.z += t4[p].z;
-                  acc.w += t4[p].w;
-                }
-              }
-          }
-          S.stg[(4 * c4 + 0) * 128 + m] = acc.x;
-          S.stg[(4 * c4 + 1) * 128 + m] = acc.y;
-          S.stg[(4 * c4 + 2) * 128 + m] = acc.z;
-          S.stg[(4 * c4 + 3) * 128 + m] = acc.w;
-        }
-      } else {
-#pragma unroll
-        for (int n = 0; n < BN; ++n) S.stg[n * 128 + m] = v[n];
+        for (int c4 = 0; c4 < kSlice / 4; ++c4)
+          st_async_v4(dst + c4 * 16, make_float4(v[j * kSlice + 4 * c4], v[j * kSlice + 4 * c4 + 1],
+                                                 v[j * kSlice + 4 * c4 + 2], v[j * kSlice + 4 * c4 + 3]), bar);
       }
-      if (wt == 0) mk_rec(a, wg, nrec, 13, i);
-      // 5. fused epilogue (this WG owns the whole 128-feature tile, staged in smem:
-      //    column n = decode row, so row loops index it freely)
-      const int gm = tile * 128 + m;
-      if (kind == MK_QKV || kind == MK_GU) {
-        mk_row_scale(a, kind == MK_QKV ? 2 * l : 2 * l + 1, S.rs, wt);
-        wg_bar(wg);
-        for (int n = 0; n < a.rc; ++n) S.stg[n * 128 + m] *= S.rs[n];
+      mk_wait(&rfull[wg], xuse & 1, 8);
+      if (wt == 0) mk_rec(a, wg, nrec, 11, i);
+#pragma unroll
+      for (int jn = 0; jn < kSlice; ++jn) {
+        float acc = myRecv[(0 * 128 + m) * kSlice + jn];
+#pragma unroll
+        for (int src = 1; src < kCS; ++src) acc += myRecv[(src * 128 + m) * kSlice + jn];
+        S.stg[jn * 128 + m] = acc;
       }
       wg_bar(wg);
-      if (wt == 0) mk_rec(a, wg, nrec, 14, i);
+      if (wt == 0) mbar_arrive_expect_tx(&rfull[wg], kRecvTx);  // arm our next exchange ...
+      __syncwarp();
+      if (wt < kCS) mbar_arrive_remote(mapa_shared(rfree_local, wt));  // ... then let the peers overwrite our slot
+      ++xuse;
+      if (wt == 0) mk_rec(a, wg, nrec, 13, i);
+      // 6. fused epilogue over this CTA's rows n_lo .. n_lo + kSlice - 1
       if (kind == MK_QKV) {
         // per-head RMSNorm of q / k (128 lanes of a column), rotate-half RoPE, bf16 q / KV append
         const bool is_v = tile >= a.Hq + a.Hkv, is_q = tile < a.Hq;
         if (!is_v) {
-          for (int n = 0; n < a.rc; ++n) {
-            const float x = S.stg[n * 128 + m];
+#pragma unroll
+          for (int jn = 0; jn < kSlice; ++jn) {
+            const float x = S.stg[jn * 128 + m];
             const float ss = warp_sum(x * x);
-            if (lane == 0) S.sred[q * 64 + n] = ss;
+            if (lane == 0) S.sred[q * 64 + jn] = ss;
           }
           wg_bar(wg);
-          const float gn = is_q ? __ldg(a.q_norm + l * 128 + m) : __ldg(a.k_norm + l * 128 + m);
-          for (int n = 0; n < a.rc; ++n) {
-            const float ss = S.sred[n] + S.sred[64 + n] + S.sred[128 + n] + S.sred[192 + n];
-            S.stg[n * 128 + m] *= (1.0f / sqrtf(ss / 128.0f + a.eps)) * gn;
+#pragma unroll
+          for (int jn = 0; jn < kSlice; ++jn) {
+            const float ss = S.sred[jn] + S.sred[64 + jn] + S.sred[128 + jn] + S.sred[192 + jn];
+            S.stg[jn * 128 + m] *= (1.0f / sqrtf(ss / 128.0f + a.eps)) * gq;
           }
           wg_bar(wg);
         }
         const int hk = tile - a.Hq - (is_v ? a.Hkv : 0);
         __nv_bfloat16* pl = a.pool + (size_t)l * a.pool_layer;
-        const int i2 = m & 63;
-        for (int n0 = 0; n0 < a.rc; n0 += 8) {
-          float cs[8], sn[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const bool need = !is_v && n0 + j < a.rc && S.ract[n0 + j];
-            const int pos = need ? S.rpos[n0 + j] : 0;
-            cs[j] = need ? __ldg(a.rope_cos + (size_t)pos * 64 + i2) : 1.f;
-            sn[j] = need ? __ldg(a.rope_sin + (size_t)pos * 64 + i2) : 0.f;
-          }
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int n = n0 + j;
-            if (n >= a.rc || !S.ract[n]) continue;
-            float y = S.stg[n * 128 + m];
-            if (!is_v)
-              y = m < 64 ? (y * cs[j] - S.stg[n * 128 + m + 64] * sn[j]) : (y * cs[j] + S.stg[n * 128 + m - 64] * sn[j]);
-            const __nv_bfloat16 b = __float2bfloat16_rn(y);
-            if (is_q) {
-              a.q[((size_t)n * a.Hq + tile) * 128 + m] = b;
-            } else {
-              const int loc = S.rkv[n];
-              const size_t off = ((((size_t)(loc / a.pt) * 2 + (is_v ? 1 : 0)) * a.Hkv + hk) * a.pt + loc % a.pt) * 128 + m;
-              pl[off] = b;
-            }
+        for (int jn = 0; jn < kSlice; ++jn) {
+          const int n = n_lo + jn;
+          if (n >= a.rc || !S.ract[n]) continue;
+          float y = S.stg[jn * 128 + m];
+          if (!is_v)
+            y = m < 64 ? (y * cs[jn] - S.stg[jn * 128 + m + 64] * sn[jn]) : (y * cs[jn] + S.stg[jn * 128 + m - 64] * sn[jn]);
+          const __nv_bfloat16 b = __float2bfloat16_rn(y);
+          if (is_q) {
+            a.q[((size_t)n * a.Hq + tile) * 128 + m] = b;
+          } else {
+            const int loc = S.rkv[n];
+            const size_t off = ((((size_t)(loc / a.pt) * 2 + (is_v ? 1 : 0)) * a.Hkv + hk) * a.pt + loc % a.pt) * 128 + m;
+            pl[off] = b;
           }
         }
         if (wt == 0) mk_rec(a, wg, nrec, 15, i);
@@ -882,10 +1014,13 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_decode_kernel(const __grid_c
         wg_bar(wg);
         if (wt == 0) { red_release_add(sl + a.so.qkv_flag + tile, 1); mk_rec(a, wg, nrec, 10, i); }
       } else if (kind == MK_GU) {
-        // rows [0, 64) of the tile are gate features f, rows [64, 128) the matching up
+        // rows [0, 64) of the tile are gate features f, rows [64, 128) the matching up (R12 r5)
         if (m < 64 && tile * 64 + m < a.F)
-          for (int n = 0; n < a.rc; ++n) {
-            const float gt = S.stg[n * 128 + m], up = S.stg[n * 128 + m + 64];
+#pragma unroll
+          for (int jn = 0; jn < kSlice; ++jn) {
+            const int n = n_lo + jn;
+            if (n >= a.rc) continue;
+            const float gt = S.stg[jn * 128 + m], up = S.stg[jn * 128 + m + 64];
             a.act_sw[sw_off(n, tile * 64 + m, BN)] = __float2bfloat16_rn(silu_f(gt) * up);
           }
         if (wt == 0) mk_rec(a, wg, nrec, 15, i);
@@ -894,43 +1029,27 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_decode_kernel(const __grid_c
         wg_bar(wg);
         if (wt == 0) { red_release_add(sl + a.so.gu_flag + tile, 1); mk_rec(a, wg, nrec, 10, i); }
       } else {
-        // o_proj / down: residual add, next RMSNorm's bf16(x * gain) operand and sum-of-squares partial
+        // o_proj / down: residual add (fp32 stream) and the next RMSNorm's sum-of-squares partial
         const bool is_o = kind == MK_O;
-        const float* rin = is_o ? a.resid0 : a.resid1;
         float* rout = is_o ? a.resid1 : a.resid0;
-        __nv_bfloat16* xg = is_o ? a.xgB : a.xgA;
-        const float* gain = is_o ? a.post_norm + (size_t)l * a.H : (l + 1 < a.L ? a.in_norm + (size_t)(l + 1) * a.H : nullptr);
         const int ver = is_o ? 2 * l + 1 : 2 * l + 2;
         const bool ok = gm < a.H;
-        const float gk = (ok && gain) ? __ldg(gain + gm) : 0.f;
-        for (int n0 = 0; n0 < a.rc; n0 += 8) {
-          float xr[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) xr[j] = (ok && n0 + j < a.rc) ? __ldcg(rin + (size_t)(n0 + j) * a.H + gm) : 0.f;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int n = n0 + j;
-            if (n < a.rc) {
-              const float x = ok ? xr[j] + S.stg[n * 128 + m] : 0.f;
-              if (ok) {
-                __stcg(rout + (size_t)n * a.H + gm, x);
-                if (gain) xg[sw_off(n, gm, BN)] = __float2bfloat16_rn(x * gk);
-              }
-              S.stg[n * 128 + m] = x;
-            }
+        for (int jn = 0; jn < kSlice; ++jn) {
+          const int n = n_lo + jn;
+          float x = 0.f;
+          if (n < a.rc && ok) {
+            x = rin_v[jn] + S.stg[jn * 128 + m];
+            __stcg(rout + (size_t)n * a.H + gm, x);
           }
-        }
-        for (int n = 0; n < a.rc; ++n) {
-          const float x = S.stg[n * 128 + m];
           const float ss = warp_sum(x * x);
-          if (lane == 0) S.sred[q * 64 + n] = ss;
+          if (lane == 0) S.sred[q * 64 + jn] = ss;
         }
         wg_bar(wg);
-        if (wt < a.rc)
-          __stcg(a.ssq + ((size_t)ver * a.Th + tile) * a.rc + wt,
+        if (wt < kSlice && n_lo + wt < a.rc)
+          __stcg(a.ssq + ((size_t)ver * a.Th + tile) * a.rc + n_lo + wt,
                  S.sred[wt] + S.sred[64 + wt] + S.sred[128 + wt] + S.sred[192 + wt]);
         if (wt == 0) mk_rec(a, wg, nrec, 15, i);
-        fence_proxy_async_global();
         __threadfence();
         wg_bar(wg);
         if (wt == 0) { red_release_add(sl + (is_o ? a.so.o_done : a.so.dn_done), 1); mk_rec(a, wg, nrec, 10, i); }
@@ -944,6 +1063,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_decode_kernel(const __grid_c
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem_base);
   }
+  cluster_sync();  // no CTA leaves while a peer may still write into its shared memory
   if (threadIdx.x == 0 && blockIdx.x == 0 && a.clock) {
     // CTA 0's lifetime ~ the kernel's (it holds FINAL and EMBED work): live timing for bench.py
     atomicAdd(a.clock, gtimer() - t_start);

@@ -22,7 +22,7 @@ args = ap.parse_args()
 shape = SHAPES[args.shape]
 P, G, g, max_new = 256, 32, 8, 1024
 w = gen_weights(shape, seed=20261017, device="cuda")
-cfg = _lib.make_config(shape, G, g, max_new, P, mode="infinite", kv_budget_bytes=0, seed=20261017)
+cfg = _lib.make_config(shape, G, g, max_new, P, mode="infinite", kv_budget_bytes=0, seed=20261017, decode_impl=0)
 ctx = _lib.Context(cfg, w)
 ctx.is_prefill(torch.as_tensor(gen_prompt(shape.vocab, P, 0), device="cuda"), 0)
 true = gen_trace("math", G, max_new, 1)

@@ -6,8 +6,10 @@ d = np.load(sys.argv[1])
 tasks, off, tr = d["tasks"], d["off"], d["trace"].astype(np.int64)
 grid = len(off) - 1
 per = {}
+merged = {}
+kinds_of = {}
 for b in range(grid):
-    for role in range(2):
+    for role in range(4):
         recs = {}
         prev_t = 0
         for n in range(tr.shape[2]):
@@ -23,8 +25,12 @@ for b in range(grid):
             kind = tasks[off[b] + i][0] & 0xFF
             if kind not in KIND:
                 continue
-            per.setdefault(kind, []).append(r)
-pairs = [(1, 2, "wait deps"), (2, 3, "B load+MMA"), (3, 11, "partial st+fence"), (11, 12, "atomic"),
+            key = (b, i)
+            merged.setdefault(key, {}).update(r)
+            kinds_of[key] = kind
+for key, r in merged.items():
+    per.setdefault(kinds_of[key], []).append(r)
+pairs = [(1, 2, "wait deps"), (2, 16, "fill loads"), (16, 17, "fill write"), (7, 18, "A first stage(prod->mma)"), (2, 18, "deps->A ready"), (17, 19, "fill->mma sees B"), (19, 20, "mma kb loop"), (20, 3, "last kb->acc"), (2, 3, "B load+MMA"), (3, 11, "partial st+fence"), (11, 12, "atomic"),
          (12, 13, "reduce ld"), (3, 13, "acc->reduced"), (13, 14, "rowscale"), (14, 15, "epilogue"), (15, 10, "fence+signal"),
          (1, 10, "total(last)"), (1, 4, "total(non-last)")]
 for kind, lst in per.items():

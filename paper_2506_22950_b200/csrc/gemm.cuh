@@ -70,6 +70,15 @@ struct GemmArgs {
   QkvEpiArgs qkv;
   float* partials;              // split-K workspace [clusters][split][128][BN] fp32 (L2-resident)
   unsigned long long* dbg_ts;  // optional [gridDim][16] globaltimer stamps (probe)
+  // RMSNorm folded into the B operand (decode QKV / gate-up): B rows are computed in
+  // shared memory as bf16(resid[row][k] * rs[row] * gain[k]) (rounding point r1), with
+  // rs[row] = 1/sqrt(sum_t ssq[t][row] / K + eps) from the producer's per-tile partials.
+  const float* bn_resid;       // [rows][K] fp32 (null: B comes from tmB)
+  const float* bn_ssq;         // [bn_tsq][bn_ld] per-128-column sums of squares
+  const __nv_bfloat16* bn_gain;  // [K]
+  int bn_tsq, bn_ld;
+  float bn_eps;
+  float* ssq_out;              // EPI_RESID_ADD: per-(tile, row) sums of squares of the new residual [tiles][bn_ld]
   int* zero;                   // optional: words zeroed once the previous kernel completed
   int zero_n;                  //   (the persistent decode kernel's dependency counters)
 };
@@ -116,8 +125,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* redbar = tempty + 2;    // (unused by the pull reduction; kept for layout)
   uint64_t* consumed = redbar + 1;  // split-K: S-1 peers finished reading our partials
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(consumed + 1);
+  uint64_t* bready = consumed + 2;  // B_NORM: [8] k-blocks [8j, 8j + 8) of the B buffer are filled
+  // B_NORM buffer: [kb1 - kb0][BN][64] bf16, 128-byte swizzled, after the 1 KB barrier block
+  uint8_t* bbuf = smem + STAGES * C::kStage + C::kAux + 1024;
+  const bool bnorm = a.bn_resid != nullptr;
   __shared__ unsigned long long skey[BN];
   __shared__ float sred[4][BN];
+  __shared__ int srow_act[BN], srow_kv[BN];  // EPI_QKV: row tables, loaded during the mainloop
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -145,6 +159,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     mbar_init(redbar, 1);
     mbar_init(consumed, S > 1 ? S - 1 : 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&bready[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -166,15 +181,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // early streams its first STAGES x 16 KB while its predecessor drains.
       // Activation (B) tiles are issued after the wait.
       const int n_pre = (cl < a.num_tiles) ? min(STAGES, kb1 - kb0) : 0;
+      const uint32_t stage_tx = bnorm ? C::kStageA : C::kStage;
       for (int i = 0; i < n_pre; ++i) {
         uint8_t* sa = stage_base + i * C::kStage;
-        mbar_arrive_expect_tx(&full[i], C::kStage);
+        mbar_arrive_expect_tx(&full[i], stage_tx);
         tma_load_2d(sa, &tmA, &full[i], (kb0 + i) * kBK, cl * kBM, kEvictFirst);
       }
       stamp(a, 2);
       pdl_wait();
-      for (int i = 0; i < n_pre; ++i)
-        tma_load_2d(stage_base + i * C::kStage + C::kStageA, &tmB, &full[i], (kb0 + i) * kBK, a.row0, kEvictLast);
+      if (!bnorm)
+        for (int i = 0; i < n_pre; ++i)
+          tma_load_2d(stage_base + i * C::kStage + C::kStageA, &tmB, &full[i], (kb0 + i) * kBK, a.row0, kEvictLast);
       int stage = 0;
       uint32_t phase = 0;
       int done = n_pre;  // k-blocks of the first tile already issued
@@ -185,9 +202,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           } else {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sa = stage_base + stage * C::kStage;
-            mbar_arrive_expect_tx(&full[stage], C::kStage);
+            mbar_arrive_expect_tx(&full[stage], stage_tx);
             tma_load_2d(sa, &tmA, &full[stage], kb * kBK, tile * kBM, kEvictFirst);
-            tma_load_2d(sa + C::kStageA, &tmB, &full[stage], kb * kBK, a.row0, kEvictLast);
+            if (!bnorm) tma_load_2d(sa + C::kStageA, &tmB, &full[stage], kb * kBK, a.row0, kEvictLast);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -210,6 +227,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kb = kb0; kb < kb1; ++kb) {
+        if (bnorm && it == 0 && ((kb - kb0) & 7) == 0) mbar_wait(&bready[(kb - kb0) >> 3], 0);
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0 && kb == kb0) stamp(a, 3);
@@ -217,7 +235,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) {
           uint8_t* sa = stage_base + stage * C::kStage;
           const uint64_t da = smem_desc_k_sw128(sa);
-          const uint64_t db = smem_desc_k_sw128(sa + C::kStageA);
+          const uint64_t db = smem_desc_k_sw128(bnorm ? bbuf + (size_t)(kb - kb0) * BN * 128 : sa + C::kStageA);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
             tc_mma_f16(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
@@ -242,6 +260,78 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     float* stg = aux;             // [BN][128] accumulator tile (column n = activation row)
     float* pre = aux + BN * kBM;  // [BN][128] operands prefetched during the mainloop
     pdl_wait();
+    if (bnorm && cl < a.num_tiles) {
+      // rs[row]: per-row sum over the producer's 128-column partials (fixed order)
+      const int et = threadIdx.x - 64;
+      float* rs = reinterpret_cast<float*>(sred);  // [BN] (sred is free until the first epilogue)
+      if (et < BN) {
+        float ss = 0.f;
+        if (et < a.n_valid) {
+          float t16[16];
+#pragma unroll 1
+          for (int t0 = 0; t0 < a.bn_tsq; t0 += 16) {
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+              t16[t] = t0 + t < a.bn_tsq ? a.bn_ssq[(size_t)(t0 + t) * a.bn_ld + a.row0 + et] : 0.f;
+#pragma unroll
+            for (int t = 0; t < 16; ++t) ss += t16[t];
+          }
+        }
+        rs[et] = et < a.n_valid ? 1.0f / sqrtf(ss / (float)a.K + a.bn_eps) : 0.f;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      // 16-byte chunks: (kb, row, 8-column chunk); each thread keeps one chunk column.
+      // Batches of up to 8 k-blocks, each released to the MMA warp as soon as written.
+      const int ch = et & 7;
+      const int nkb = kb1 - kb0;
+      constexpr int kPer = BN / 16;   // rows per thread per k-block
+      constexpr int kGrp = 8 / kPer;  // k-blocks per load batch (<= 8)
+#pragma unroll 1
+      for (int g0 = 0; g0 < nkb; g0 += kGrp) {
+        float4 xv[kGrp][kPer][2];
+        uint4 gv[kGrp];
+#pragma unroll
+        for (int j = 0; j < kGrp; ++j) {
+          const int kb = kb0 + g0 + j;
+          const bool okk = g0 + j < nkb;
+          gv[j] = okk ? *reinterpret_cast<const uint4*>(a.bn_gain + kb * 64 + ch * 8) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int c = 0; c < kPer; ++c) {
+            const int row = (et + 128 * c) >> 3;
+            const bool ok = okk && row < a.n_valid;
+            const float4* src = reinterpret_cast<const float4*>(a.bn_resid + (size_t)(a.row0 + row) * a.K + kb * 64 + ch * 8);
+            xv[j][c][0] = ok ? src[0] : make_float4(0.f, 0.f, 0.f, 0.f);
+            xv[j][c][1] = ok ? src[1] : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kGrp; ++j) {
+          if (g0 + j >= nkb) break;
+          const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv[j]);
+          const float2 ga = __bfloat1622float2(g2[0]), gb = __bfloat1622float2(g2[1]);
+          const float2 gc = __bfloat1622float2(g2[2]), gd = __bfloat1622float2(g2[3]);
+#pragma unroll
+          for (int c = 0; c < kPer; ++c) {
+            const int row = (et + 128 * c) >> 3;
+            const float r_ = rs[row];
+            const float4 x0 = xv[j][c][0], x1 = xv[j][c][1];
+            uint4 o;
+            __nv_bfloat162 hh;
+            hh = __floats2bfloat162_rn(x0.x * r_ * ga.x, x0.y * r_ * ga.y); o.x = *reinterpret_cast<uint32_t*>(&hh);
+            hh = __floats2bfloat162_rn(x0.z * r_ * gb.x, x0.w * r_ * gb.y); o.y = *reinterpret_cast<uint32_t*>(&hh);
+            hh = __floats2bfloat162_rn(x1.x * r_ * gc.x, x1.y * r_ * gc.y); o.z = *reinterpret_cast<uint32_t*>(&hh);
+            hh = __floats2bfloat162_rn(x1.z * r_ * gd.x, x1.w * r_ * gd.y); o.w = *reinterpret_cast<uint32_t*>(&hh);
+            *reinterpret_cast<uint4*>(bbuf + ((size_t)(g0 + j) * BN + row) * 128 + ((ch ^ (row & 7)) << 4)) = o;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        // release every 8-k-block group this batch completed
+        if (et == 0)
+          for (int b = g0 >> 3; b <= (min(g0 + kGrp, nkb) - 1) >> 3; ++b)
+            if (min(8 * b + 8, nkb) <= min(g0 + kGrp, nkb)) mbar_arrive(&bready[b]);
+      }
+    }
     if (a.zero)
       for (int i = blockIdx.x * 128 + (threadIdx.x - 64); i < a.zero_n; i += gridDim.x * 128) a.zero[i] = 0;
     int it = 0;
@@ -256,13 +346,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       if constexpr (EPI == EPI_QKV) {
         const QkvEpiArgs& e = a.qkv;
-        if (tile < e.Hq + e.Hkv)
-          for (int n = n_lo; n < n_hi; ++n) {
-            if (n < a.n_valid) {
-              const int pos = e.row_pos[a.row0 + n];
-              pre[n * kBM + m] = m < 64 ? e.rope_cos[(size_t)pos * 64 + m] : e.rope_sin[(size_t)pos * 64 + m - 64];
-            }
-          }
+        if (threadIdx.x - 64 < BN) {
+          const int n = threadIdx.x - 64;
+          srow_act[n] = n < a.n_valid ? e.row_active[a.row0 + n] : 0;
+          srow_kv[n] = n < a.n_valid ? e.row_kvloc[a.row0 + n] : 0;
+        }
+        if (tile < e.Hq + e.Hkv) {
+          // all rows' positions first, then the table rows: independent loads in flight together
+          int pos[BN];
+#pragma unroll
+          for (int n = 0; n < BN; ++n) pos[n] = (n >= n_lo && n < n_hi && n < a.n_valid) ? e.row_pos[a.row0 + n] : 0;
+#pragma unroll
+          for (int n = 0; n < BN; ++n)
+            if (n >= n_lo && n < n_hi && n < a.n_valid)
+              pre[n * kBM + m] = m < 64 ? e.rope_cos[(size_t)pos[n] * 64 + m] : e.rope_sin[(size_t)pos[n] * 64 + m - 64];
+        }
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -317,12 +415,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (threadIdx.x == 64) stamp(a, 8);
 
       if constexpr (EPI == EPI_STORE_F32 || EPI == EPI_RESID_ADD) {
-        if (gm < a.M)
-          for (int n = n_lo; n < min(n_hi, a.n_valid); ++n) {
-            float x = stg[n * kBM + m];
+        const int n_end = min(n_hi, a.n_valid);
+        for (int n = n_lo; n < n_end; ++n) {
+          float x = 0.f;
+          if (gm < a.M) {
+            x = stg[n * kBM + m];
             if (EPI == EPI_RESID_ADD) x += pre[n * kBM + m];
             a.out[(size_t)(a.row0 + n) * a.ld_out + gm] = x;
           }
+          if (EPI == EPI_RESID_ADD && a.ssq_out) {
+            const float ss = warp_sum(x * x);
+            if (lane == 0) sred[q][n] = ss;
+          }
+        }
+        if (EPI == EPI_RESID_ADD && a.ssq_out) {
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          const int n = n_lo + (threadIdx.x - 64);
+          if (n < n_end)
+            a.ssq_out[(size_t)tile * a.bn_ld + a.row0 + n] = sred[0][n] + sred[1][n] + sred[2][n] + sred[3][n];
+        }
       } else if constexpr (EPI == EPI_SWIGLU) {
         // rows [0, 64) of the tile are gate features f, rows [64, 128) the matching up
         const int f = tile * 64 + m;
@@ -353,7 +464,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int hk = tile - e.Hq - (is_v ? e.Hkv : 0);
         for (int n = n_lo; n < n_end; ++n) {
           const int row = a.row0 + n;
-          if (!e.row_active[row]) continue;
+          if (!srow_act[n]) continue;
           float y = stg[n * kBM + m];
           if (!is_v) {
             const int i = m & 63;
@@ -365,7 +476,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             e.q_out[((size_t)row * e.Hq + tile) * kBM + m] = b;
           } else {
             const int kvsel = is_v ? 1 : 0;
-            const int loc = e.row_kvloc[row];
+            const int loc = srow_kv[n];
             size_t off;
             if (e.prefill) off = (((size_t)kvsel * e.Hkv + hk) * e.pcap + loc) * kBM + m;
             else off = ((((size_t)(loc / e.pt) * 2 + kvsel) * e.Hkv + hk) * e.pt + loc % e.pt) * kBM + m;

@@ -252,21 +252,27 @@ struct Stages {
   static constexpr int v = !DEEP ? 4 : (BN == 16 ? 8 : (BN == 32 ? 6 : 4));
 };
 
+// B_NORM buffer: the CTA's K range of BN normalised rows, bf16.
+static int bnorm_bytes(int BN, int kb_total, int split) { return BN * 128 * (int)ceil_div64(kb_total, split); }
+template <int BN, bool DEEP>
+static int gemm_smem_of() { return GemmCfg<BN, Stages<BN, DEEP>::v>::kSmem; }
+
 template <int BN, int EPI, bool DEEP>
 static is_status launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB, GemmArgs a, cudaStream_t st) {
   constexpr int STAGES = Stages<BN, DEEP>::v;
   using C = GemmCfg<BN, STAGES>;
-  static bool attr = false;
+  static int attr = 0;
   auto kern = gemm_swapab_kernel<BN, EPI, STAGES>;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-    attr = true;
+  const int smem = C::kSmem + (a.bn_resid ? bnorm_bytes(BN, a.K / kBK, a.split) : 0);
+  if (smem > attr) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = smem;
   }
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute at[2];
   int na = 0;
   cfg.blockDim = dim3(kGemmThreads);
-  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   if (a.split > 1) {
     cfg.gridDim = dim3(a.num_tiles * a.split);
@@ -366,6 +372,7 @@ static is_status launch_k(K kern, dim3 grid, dim3 block, cudaStream_t st, Args..
 struct LayerW {
   __nv_bfloat16 *wqkv, *wo, *wgu, *wd;
   float *in_norm, *post_norm, *q_norm, *k_norm;
+  __nv_bfloat16 *in_norm_bf, *post_norm_bf;  // exact bf16 copies (B_NORM operand fill)
   CUtensorMap tm_qkv, tm_o, tm_gu, tm_d;
 };
 
@@ -390,6 +397,9 @@ struct is_ctx {
   float* resid;
   __nv_bfloat16 *xn, *attn, *act, *q;
   float *part_o, *part_ml;
+  int* merge_cnt;  // [max_rows][Hkv] fused-merge counters (decode, tcgen05 prefix)
+  float *ssqA, *ssqB;  // [Th][max_rows] per-128-column sums of squares: QKV input, gate/up input
+  int bnorm;           // decode: RMSNorm folded into the QKV / gate-up B operand
   int32_t* attn_items;
   float* splitk_ws;  // split-K partials workspace
   int NC, nc_pre, nc_suf;
@@ -555,12 +565,15 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
   const int chunk = prefill ? 64 : rows;
 
   prof_mark(st, 0);
-  CKS(launch_k(embed_kernel, dim3(rows), dim3(256), st, (const __nv_bfloat16*)c->embed,
-               (const int32_t*)c->row_tok, (const int32_t*)c->row_active, c->resid, H));
+  CKS(launch_k(embed_kernel, dim3(rows), dim3(128), st, (const __nv_bfloat16*)c->embed,
+               (const int32_t*)c->row_tok, (const int32_t*)c->row_active, c->resid, H,
+               (!prefill && c->bnorm) ? c->ssqA : (float*)nullptr, c->max_rows));
   for (int l = 0; l < s.layers; ++l) {
     LayerW& w = c->L[l];
-    if (prefill || !(g_skip & 1)) CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.in_norm,
-                 c->xn, H, s.rms_eps));
+    const bool bn = !prefill && c->bnorm;
+    if (!bn && (prefill || !(g_skip & 1)))
+      CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.in_norm, c->xn, H,
+                   s.rms_eps));
     prof_mark(st, 0);
     const size_t prefix_layer = (size_t)2 * Hkv * c->pcap * kHD;
     const size_t pool_layer = (size_t)c->num_pages * 2 * Hkv * c->pt * kHD;
@@ -588,6 +601,14 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
       e.pcap = c->pcap;
       e.prefill = prefill ? 1 : 0;
       e.eps = s.rms_eps;
+      if (bn) {
+        a.bn_resid = c->resid;
+        a.bn_ssq = c->ssqA;
+        a.bn_gain = w.in_norm_bf;
+        a.bn_tsq = (int)ceil_div64(H, 128);
+        a.bn_ld = c->max_rows;
+        a.bn_eps = s.rms_eps;
+      }
       if (prefill || !(g_skip & 2)) CKS(launch_gemm<EPI_QKV>(BN, w.tm_qkv, tm_xn, a, st));
     }
     prof_mark(st, 1);
@@ -614,6 +635,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
     aa.nc_pre = prefill ? c->nc_pre : c->nc_pre_dec;
     aa.nc_suf = prefill ? 0 : c->nc_suf;
     aa.tc_prefix = prefill ? 0 : c->tc_prefix;
+    aa.merge_cnt = (!prefill && c->tc_prefix && !getenv("IS_SEPARATE_MERGE")) ? c->merge_cnt : nullptr;
     aa.NC = c->NC;
     aa.prefill = prefill ? 1 : 0;
     aa.scale = 1.0f / sqrtf((float)kHD);
@@ -628,7 +650,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
       if (a2.dbg_ts) a2.dbg_ts += (size_t)2 * 296 * 16;                                                       \
       CKS(launch_k_smem(attn_kernel<R>, dim3(nblk), dim3(kAttnThreads), AttnSmem<R>::v, st, a2));            \
     }                                                                                                          \
-    if (do_attn) CKS(launch_k(attn_merge_kernel<R>, dim3(rows, Hkv), dim3(32), st, aa));                      \
+    if (do_attn && !aa.merge_cnt) CKS(launch_k(attn_merge_kernel<R>, dim3(rows, Hkv), dim3(32), st, aa));     \
   } while (0)
     switch (Hq / Hkv) {
       case 1: IS_ATTN_LAUNCH(1); break;
@@ -648,11 +670,16 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
       a.n_valid = std::min(chunk, rows - r0);
       a.out = c->resid;
       a.ld_out = H;
+      if (bn) {
+        a.ssq_out = c->ssqB;
+        a.bn_ld = c->max_rows;
+      }
       if (prefill || !(g_skip & 16)) CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_o, tm_attn, a, st));
     }
     prof_mark(st, 4);
-    if (prefill || !(g_skip & 1)) CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.post_norm,
-                 c->xn, H, s.rms_eps));
+    if (!bn && (prefill || !(g_skip & 1)))
+      CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.post_norm, c->xn, H,
+                   s.rms_eps));
     prof_mark(st, 0);
     for (int r0 = 0; r0 < rows; r0 += chunk) {
       GemmArgs a{};
@@ -664,6 +691,14 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
       a.n_valid = std::min(chunk, rows - r0);
       a.act = c->act;
       a.ld_act = F;
+      if (bn) {
+        a.bn_resid = c->resid;
+        a.bn_ssq = c->ssqB;
+        a.bn_gain = w.post_norm_bf;
+        a.bn_tsq = (int)ceil_div64(H, 128);
+        a.bn_ld = c->max_rows;
+        a.bn_eps = s.rms_eps;
+      }
       if (prefill || !(g_skip & 32)) CKS(launch_gemm<EPI_SWIGLU>(BN, w.tm_gu, tm_xn, a, st));
     }
     prof_mark(st, 5);
@@ -677,6 +712,10 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
       a.n_valid = std::min(chunk, rows - r0);
       a.out = c->resid;
       a.ld_out = H;
+      if (bn) {
+        a.ssq_out = c->ssqA;
+        a.bn_ld = c->max_rows;
+      }
       if (prefill || !(g_skip & 64)) CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_d, tm_act, a, st));
     }
     prof_mark(st, 6);
@@ -1005,7 +1044,7 @@ static is_status enqueue_step(is_ctx* c) {
   g_splitk_ws = c->splitk_ws;
   CKS(launch_gemm<EPI_SAMPLE>(c->BN, c->tm_embed, c->tm_xn_dec, a, st));
   prof_mark(st, 7);
-  CKS(launch_k(sched_kernel, dim3(1), dim3(32), st, sched_args(c), 1));
+  CKS(launch_k(sched_kernel, dim3(1), dim3(kSchedThreads), st, sched_args(c), 1));
   prof_mark(st, 8);
   CK(cudaMemcpyAsync(c->st_host, c->st_dev, sizeof(long long) * ST_COUNT, cudaMemcpyDeviceToHost, st));
   return IS_OK;
@@ -1158,9 +1197,13 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
     CK(cudaMemcpy(w.wd, p[10], (size_t)H * F * 2, cudaMemcpyDeviceToDevice));
     w.in_norm = (float*)A(H * 4);
     w.post_norm = (float*)A(H * 4);
+    w.in_norm_bf = (__nv_bfloat16*)A(H * 2);
+    w.post_norm_bf = (__nv_bfloat16*)A(H * 2);
     w.q_norm = (float*)A(128 * 4);
     w.k_norm = (float*)A(128 * 4);
     if (err != IS_OK) return err;
+    CK(cudaMemcpy(w.in_norm_bf, p[0], (size_t)H * 2, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(w.post_norm_bf, p[7], (size_t)H * 2, cudaMemcpyDeviceToDevice));
     bf16_to_f32_kernel<<<(H + 255) / 256, 256>>>((const __nv_bfloat16*)p[0], w.in_norm, H);
     bf16_to_f32_kernel<<<(H + 255) / 256, 256>>>((const __nv_bfloat16*)p[7], w.post_norm, H);
     bf16_to_f32_kernel<<<1, 128>>>((const __nv_bfloat16*)p[4], w.q_norm, 128);
@@ -1185,6 +1228,9 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->q = (__nv_bfloat16*)A((size_t)R * Hq * 128 * 2);
   c->part_o = (float*)A((size_t)R * Hq * c->NC * 128 * 4);
   c->part_ml = (float*)A((size_t)R * Hq * c->NC * 2 * 4);
+  c->merge_cnt = (int*)A((size_t)R * Hkv * 4);
+  c->ssqA = (float*)A((size_t)ceil_div64(H, 128) * R * 4);
+  c->ssqB = (float*)A((size_t)ceil_div64(H, 128) * R * 4);
   c->splitk_ws = (float*)A((size_t)2 * 160 * kBM * 64 * 4);
   c->attn_items = (int32_t*)A((size_t)Hkv * (c->nc_pre * ((c->rc + 3) / 4) + c->rc * c->nc_suf) * kItemStride * 4 + 64);
   c->rope_cos = (float*)A((size_t)c->max_pos * 64 * 4);
@@ -1236,6 +1282,25 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->split_o = choose_split((int)ceil_div64(H, kBM), Hq * 128 / kBK, c->BN);
   c->split_gu = choose_split((int)ceil_div64(2 * F, kBM), H / kBK, c->BN);
   c->split_d = choose_split((int)ceil_div64(H, kBM), F / kBK, c->BN);
+  {
+    // RMSNorm folded into the QKV / gate-up GEMMs when the CTA's normalised B rows fit in smem
+    int maxsm = 0;
+    CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
+    auto fits = [&](int split) {
+      const bool deep = split == 1;
+      int base = 0;
+      switch (c->BN * 2 + (deep ? 1 : 0)) {
+        case 32: base = gemm_smem_of<16, false>(); break;
+        case 33: base = gemm_smem_of<16, true>(); break;
+        case 64: base = gemm_smem_of<32, false>(); break;
+        case 65: base = gemm_smem_of<32, true>(); break;
+        case 128: base = gemm_smem_of<64, false>(); break;
+        default: base = gemm_smem_of<64, true>(); break;
+      }
+      return base + bnorm_bytes(c->BN, H / kBK, split) <= maxsm;
+    };
+    c->bnorm = fits(c->split_qkv) && fits(c->split_gu) && getenv("IS_BNORM") != nullptr;  // measured slower (profiles/r01)
+  }
   c->l2_prefetch = getenv("IS_L2_PREFETCH") ? atoi(getenv("IS_L2_PREFETCH")) : 0;
   if (const char* e = getenv("IS_SPLIT_OVERRIDE")) {
     int v = atoi(e);
@@ -1252,7 +1317,7 @@ extern "C" void is_destroy(is_ctx* c) {
   cudaStreamSynchronize(c->st);
   if (c->graph_ok) cudaGraphExecDestroy(c->graph);
   void* bufs[] = {c->wblob, c->final_norm, c->prefix, c->pool, c->resid, c->xn, c->attn, c->act, c->q,
-                  c->part_o, c->part_ml, c->attn_items, c->splitk_ws, c->rope_cos, c->rope_sin, c->row_active, c->row_uid, c->row_lid,
+                  c->part_o, c->part_ml, c->merge_cnt, c->ssqA, c->ssqB, c->attn_items, c->splitk_ws, c->rope_cos, c->rope_sin, c->row_active, c->row_uid, c->row_lid,
                   c->row_t, c->row_tok, c->row_pos, c->row_kvloc, c->row_len, c->keys, c->last_tok,
                   c->last_fin, c->st_dev, c->slot_uid, c->slot_count, c->tpos, c->true_len, c->queue,
                   c->main_init, c->main_queue, c->free_stack, c->pagetab, c->npages, c->tokens, c->log_slot,
@@ -1261,6 +1326,8 @@ extern "C" void is_destroy(is_ctx* c) {
     if (p) cudaFree(p);
   for (int i = 0; i < c->mk_nbufs; ++i) cudaFree(c->mk_bufs[i]);
   for (auto& w : c->L) {
+    cudaFree(w.in_norm_bf);
+    cudaFree(w.post_norm_bf);
     cudaFree(w.in_norm);
     cudaFree(w.post_norm);
     cudaFree(w.q_norm);
@@ -1359,7 +1426,7 @@ extern "C" is_status is_start_group(is_ctx* c, const int32_t* true_len, const in
   CK(cudaMemsetAsync(c->tokens, 0xFF, (size_t)G * c->max_new * 4, c->st));
   CK(cudaMemsetAsync(c->log_slot, 0xFF, (size_t)c->log_cap * g * 4, c->st));
   CK(cudaMemsetAsync(c->log_live, 0, (size_t)c->log_cap * 4, c->st));
-  CKS(launch_k(sched_kernel, dim3(1), dim3(32), c->st, sched_args(c), 0));
+  CKS(launch_k(sched_kernel, dim3(1), dim3(kSchedThreads), c->st, sched_args(c), 0));
   CK(cudaMemcpyAsync(c->st_host, c->st_dev, sizeof(long long) * ST_COUNT, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   if (!c->graph_ok) CKS(build_graph(c));
@@ -1382,7 +1449,7 @@ extern "C" is_status is_refill(is_ctx* c, uint8_t* d_fin, int32_t* d_new_uid) {
   if (!c) return fail(IS_ERR_CONFIG, "null argument");
   if (!c->started) return fail(IS_ERR_STATE, "is_refill before is_start_group");
   StreamGuard guard(c, c->user);
-  CKS(launch_k(sched_kernel, dim3(1), dim3(32), c->st, sched_args(c), 1));
+  CKS(launch_k(sched_kernel, dim3(1), dim3(kSchedThreads), c->st, sched_args(c), 1));
   if (d_fin) CK(cudaMemcpyAsync(d_fin, c->last_fin, c->rc, cudaMemcpyDeviceToDevice, c->st));
   if (d_new_uid) {
     CK(cudaMemsetAsync(d_new_uid, 0xFF, c->rc * 4, c->st));

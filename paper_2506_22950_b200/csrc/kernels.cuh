@@ -9,16 +9,30 @@ constexpr int kHD = 128;      // head_dim (all Qwen3 shapes, R1)
 constexpr int kKPad = 136;    // smem row pitch (bf16) -> conflict-free 16-B row reads
 
 // ------------------------------------------------------------------ embed
-// resid[r][:] = E[tok[r]][:] (fp32 residual stream); idle rows get zeros.
+// resid[r][:] = E[tok[r]][:] (fp32 residual stream); idle rows get zeros.  With
+// ssq != null also the per-128-column sums of squares ssq[t][r] that the first
+// QKV GEMM folds its RMSNorm from.  One CTA of 128 threads per row.
 __global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ row_tok,
-                             const int32_t* __restrict__ row_active, float* __restrict__ resid, int H) {
+                             const int32_t* __restrict__ row_active, float* __restrict__ resid, int H,
+                             float* __restrict__ ssq, int ld_ssq) {
   pdl_launch_dependents();  // let the next kernel launch and prefetch now; it waits for our completion itself
   pdl_wait();
+  __shared__ float red[4];
   const int r = blockIdx.x;
   const bool act = row_active[r] != 0;
   const __nv_bfloat16* e = E + (size_t)(act ? row_tok[r] : 0) * H;
-  for (int k = threadIdx.x; k < H; k += blockDim.x)
-    resid[(size_t)r * H + k] = act ? __bfloat162float(e[k]) : 0.f;
+  for (int t0 = 0; t0 < H; t0 += 128) {
+    const int k = t0 + threadIdx.x;
+    const float x = (act && k < H) ? __bfloat162float(e[k]) : 0.f;
+    if (k < H) resid[(size_t)r * H + k] = x;
+    if (ssq) {
+      const float s2 = warp_sum(x * x);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s2;
+      __syncthreads();
+      if (threadIdx.x == 0) ssq[(size_t)(t0 / 128) * ld_ssq + r] = red[0] + red[1] + red[2] + red[3];
+      __syncthreads();
+    }
+  }
 }
 
 // ------------------------------------------------------------------ RMSNorm
@@ -104,6 +118,7 @@ struct AttnArgs {
   int nc_pre, nc_suf, NC;
   int prefill;                // 1: rows are prompt positions, causal over the prefix, no suffix
   int tc_prefix;              // decode: shared prefix done by attn_prefix_tc_kernel (tcgen05)
+  int* merge_cnt;             // decode: [rows][Hkv] suffix units done; the last one merges (reset by it)
   float scale;                // 1/sqrt(128)
 };
 
@@ -221,6 +236,53 @@ struct AttnSmem {
   static constexpr int v = kKV + kQ + kComb + 64;
 };
 
+// LSE merge (R8) of one (row r, query head h*REP + j): lane i holds partial i's
+// (m, l) (<= 32 partials); all o loads are issued together; fixed order.
+template <int REP>
+__device__ __forceinline__ void attn_merge_one(const AttnArgs& a, int r, int h, int j, int lane) {
+  const int npre = a.nc_pre;
+  const int nsuf = (a.row_len[r] + kSC - 1) / kSC;
+  const int n = npre + nsuf;
+  const int my_slot = lane < npre ? lane : a.nc_pre + (lane - npre);
+  const int qh = h * REP + j;
+  const size_t base = ((size_t)r * a.Hq + qh) * a.NC;
+  float mi = -INFINITY, li = 0.f;
+  if (lane < n) {
+    const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (base + my_slot) * 2));
+    mi = ml.x;
+    li = ml.y;
+  }
+  const float M = warp_max(mi);
+  const float wi = (lane < n && mi != -INFINITY) ? expf(mi - M) * li : 0.f;
+  const float den = warp_sum(wi);
+  float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+  for (int i0 = 0; i0 < n; i0 += 16) {
+    float4 o[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int i = i0 + k;
+      const int slot = i < npre ? i : a.nc_pre + (i - npre);
+      o[k] = i < n ? __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + slot) * kHD) + lane)
+                   : make_float4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const float w = __shfl_sync(0xffffffffu, wi, (i0 + k) & 31);
+      if (i0 + k < n) {
+        num.x += w * o[k].x;
+        num.y += w * o[k].y;
+        num.z += w * o[k].z;
+        num.w += w * o[k].w;
+      }
+    }
+  }
+  const float inv = 1.0f / den;
+  __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(a.out + ((size_t)r * a.Hq + qh) * kHD) + 2 * lane;
+  o2[0] = __floats2bfloat162_rn(num.x * inv, num.y * inv);
+  o2[1] = __floats2bfloat162_rn(num.z * inv, num.w * inv);
+}
+
 // Work units (persistent grid, ~4 CTAs per SM):
 //   prefix (h, c, g): DMA the kPC-token prefix chunk once; warp w scores row
 //                     4g + w (all of its REP heads) -> partial slot c;
@@ -237,7 +299,10 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnArgs a) {
   float* qs_all = reinterpret_cast<float*>(asmem + SM::kKV);
   float* comb = reinterpret_cast<float*>(asmem + SM::kKV + SM::kQ);
   uint64_t* bar = reinterpret_cast<uint64_t*>(asmem + SM::kKV + SM::kQ + SM::kComb);
+  __shared__ int merge_list[128];
+  __shared__ int merge_n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) merge_n = 0;
   float* qs = qs_all + warp * REP * kHD;
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
@@ -343,6 +408,19 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnArgs a) {
           }
         }
         store_partial<REP>(a, r, h, a.nc_pre + c, M, L, O, lane);
+        if (a.merge_cnt) {
+          // count this (row, kv head)'s suffix units; the last one merges it at the end
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) {
+            const int nsuf = (a.row_len[r] + kSC - 1) / kSC;
+            if (atomicAdd(a.merge_cnt + r * a.Hkv + h, 1) + 1 == nsuf) {
+              __threadfence();
+              a.merge_cnt[r * a.Hkv + h] = 0;  // ready for the next launch
+              if (merge_n < 128) merge_list[merge_n++] = (r << 8) | h;  // single writer: warp 0 lane 0
+            }
+          }
+        }
       }
     }
     __syncthreads();  // smem reuse by the next unit
@@ -350,7 +428,15 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnArgs a) {
     if (nu < 3) astamp(a, 3 + 4 * nu);
     if (nu < 3 && threadIdx.x == 0 && a.dbg_ts) a.dbg_ts[blockIdx.x * 16 + 4 + 4 * nu] = (code < 0) ? 1 : 2;
   }
-  if (!a.prefill && a.tc_prefix) pdl_wait();
+  if (!a.prefill && a.tc_prefix) pdl_wait();  // the tcgen05 prefix partials are complete from here on
+  if (!a.prefill && a.merge_cnt) {
+    // LSE merge (R8) fused: the unit that completed a (row, kv head) merges it after the wait above
+    const int nm = merge_n;
+    for (int j = warp; j < nm * REP; j += kAttnWarps) {
+      const int rh = merge_list[j / REP];
+      attn_merge_one<REP>(a, rh >> 8, rh & 0xFF, j % REP, lane);
+    }
+  }
   astamp(a, 15);
 }
 
@@ -476,10 +562,9 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   const uint32_t tmem = *tslot;
   astamp(a, 0);
-  pdl_wait();                 // q and the appended KV of this step come from the QKV GEMM
-  astamp(a, 1);
-  pdl_launch_dependents();    // the suffix kernel may start now (it does not touch our outputs)
   if (threadIdx.x == 0) {
+    // The shared prefix KV is immutable after is_prefill: stage it BEFORE waiting for
+    // the QKV GEMM, so its TMA latency hides under the previous kernel.
     // K rows: [(kv=0) * Hkv + h] * pcap + tok ; V rows: [(kv=1) * Hkv + h] * pcap + tok
     const int rk = kv_row_base + (0 * a.Hkv + h) * a.pcap + tok0;
     const int rv = kv_row_base + (1 * a.Hkv + h) * a.pcap + tok0;
@@ -489,6 +574,9 @@ __global__ void __launch_bounds__(128, 1)
     tma_load_2d(Vsm, &tmKV, &bars[0], 0, rv, kEvictNormal);
     tma_load_2d(Vsm + 128 * 128, &tmKV, &bars[0], 64, rv, kEvictNormal);
   }
+  pdl_wait();                 // q of this step comes from the QKV GEMM
+  astamp(a, 1);
+  pdl_launch_dependents();    // the suffix kernel may start now (it does not touch our outputs)
   // Q rows n = r*REP + e (K-major, 128-byte swizzle, two 64-d atoms)
   for (int i = threadIdx.x; i < N * 16; i += 128) {
     const int n = i >> 4, c = i & 15;
@@ -677,73 +765,100 @@ struct SchedArgs {
   int Hkv, nc_pre, nc_suf, chunk, tc_prefix;
 };
 
-// Single thread: the work is O(g + pages) integer bookkeeping per step.
-// consume = 1: take the sampled tokens of the step that just ran, finish /
-// park / refill in ascending slot order (R18); then always prepare the rows of
-// the next step (page allocation on boundary crossing, R26).
-__global__ void sched_kernel(SchedArgs a, int consume) {
+// One CTA of kSchedThreads.  The policy itself (finish / park / refill in
+// ascending slot order, R18; LIFO page recycling, R26) is sequential and runs
+// on thread 0; the per-row preparation of the next step and its attention work
+// list are independent per row and run one thread per row.
+constexpr int kSchedThreads = 128;
+__global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int consume) {
   pdl_launch_dependents();  // let the next kernel launch and prefetch now; it waits for our completion itself
   pdl_wait();
-  if (threadIdx.x != 0) return;
+  __shared__ int s_alloc_page[64];  // page allocated for row s this step, or -1
+  __shared__ int s_cnt[65];         // suffix chunk counts -> exclusive prefix sums
+  __shared__ int s_any, s_npre;
   long long* st = a.st;
-  if (consume) {
-    for (int s = 0; s < a.row_cap; ++s) {
-      a.last_tok[s] = -1;
-      a.last_fin[s] = 0;
-    }
-    for (int s = 0; s < a.g; ++s) {
-      const int uid = a.slot_uid[s];
-      if (uid < 0) continue;
-      const uint32_t tok = 0xFFFFFFFFu - (uint32_t)(a.keys[s] & 0xFFFFFFFFull);
-      a.tokens[(size_t)uid * a.max_new + a.t[uid]] = (int32_t)tok;
-      a.last_tok[s] = (int32_t)tok;
-      a.t[uid] += 1;
-      st[ST_TOKENS] += 1;
-    }
-    for (int s = 0; s < a.g; ++s) {  // ascending slot index
-      const int uid = a.slot_uid[s];
-      if (uid < 0) continue;
-      if (a.t[uid] == a.true_len[uid]) {
-        st[ST_DONE] += 1;
-        a.last_fin[s] = 1;
-        for (int i = 0; i < a.npages[uid]; ++i) a.free_stack[st[ST_FREE_TOP]++] = a.pagetab[(size_t)uid * a.maxp + i];
-        st[ST_LIVE] -= a.npages[uid];
-        a.npages[uid] = 0;
-      } else if (st[ST_STOPK] > 0 && a.t[uid] == st[ST_STOPK]) {
-        // park: keep pages (prefix reuse)
-      } else {
-        continue;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    if (consume) {
+      for (int s = 0; s < a.row_cap; ++s) {
+        a.last_tok[s] = -1;
+        a.last_fin[s] = 0;
       }
-      a.slot_uid[s] = -1;
-      a.slot_count[s] += 1;
-      if (!st[ST_BARRIER] && st[ST_QHEAD] < st[ST_QLEN] && (st[ST_QUOTA] == 0 || a.slot_count[s] < st[ST_QUOTA]))
-        a.slot_uid[s] = a.queue[st[ST_QHEAD]++];
-    }
-    bool idle = true;
-    for (int s = 0; s < a.g; ++s) idle = idle && a.slot_uid[s] < 0;
-    if (st[ST_BARRIER] && idle && st[ST_QHEAD] < st[ST_QLEN]) {
-      for (int s = 0; s < a.g && st[ST_QHEAD] < st[ST_QLEN]; ++s) a.slot_uid[s] = a.queue[st[ST_QHEAD]++];
-      idle = false;
-    }
-    if (st[ST_PHASE] == 0 && idle && st[ST_QHEAD] >= st[ST_QLEN] && st[ST_MAIN_PENDING]) {
-      // prefix phase over: install the Alg. 2 plan (init fill + static SJF queue)
-      for (int i = 0; i < st[ST_MAIN_QLEN]; ++i) a.queue[i] = a.main_queue[i];
-      st[ST_QLEN] = st[ST_MAIN_QLEN];
-      st[ST_QHEAD] = 0;
-      st[ST_BARRIER] = 0;
-      st[ST_QUOTA] = 0;
-      st[ST_STOPK] = 0;
-      st[ST_PHASE] = 1;
-      st[ST_MAIN_PENDING] = 0;
       for (int s = 0; s < a.g; ++s) {
-        a.slot_count[s] = 0;
-        a.slot_uid[s] = s < st[ST_MAIN_NINIT] ? a.main_init[s] : -1;
+        const int uid = a.slot_uid[s];
+        if (uid < 0) continue;
+        const uint32_t tok = 0xFFFFFFFFu - (uint32_t)(a.keys[s] & 0xFFFFFFFFull);
+        a.tokens[(size_t)uid * a.max_new + a.t[uid]] = (int32_t)tok;
+        a.last_tok[s] = (int32_t)tok;
+        a.t[uid] += 1;
+        st[ST_TOKENS] += 1;
+      }
+      for (int s = 0; s < a.g; ++s) {  // ascending slot index
+        const int uid = a.slot_uid[s];
+        if (uid < 0) continue;
+        if (a.t[uid] == a.true_len[uid]) {
+          st[ST_DONE] += 1;
+          a.last_fin[s] = 1;
+          for (int i = 0; i < a.npages[uid]; ++i) a.free_stack[st[ST_FREE_TOP]++] = a.pagetab[(size_t)uid * a.maxp + i];
+          st[ST_LIVE] -= a.npages[uid];
+          a.npages[uid] = 0;
+        } else if (st[ST_STOPK] > 0 && a.t[uid] == st[ST_STOPK]) {
+          // park: keep pages (prefix reuse)
+        } else {
+          continue;
+        }
+        a.slot_uid[s] = -1;
+        a.slot_count[s] += 1;
+        if (!st[ST_BARRIER] && st[ST_QHEAD] < st[ST_QLEN] && (st[ST_QUOTA] == 0 || a.slot_count[s] < st[ST_QUOTA]))
+          a.slot_uid[s] = a.queue[st[ST_QHEAD]++];
+      }
+      bool idle = true;
+      for (int s = 0; s < a.g; ++s) idle = idle && a.slot_uid[s] < 0;
+      if (st[ST_BARRIER] && idle && st[ST_QHEAD] < st[ST_QLEN]) {
+        for (int s = 0; s < a.g && st[ST_QHEAD] < st[ST_QLEN]; ++s) a.slot_uid[s] = a.queue[st[ST_QHEAD]++];
+        idle = false;
+      }
+      if (st[ST_PHASE] == 0 && idle && st[ST_QHEAD] >= st[ST_QLEN] && st[ST_MAIN_PENDING]) {
+        // prefix phase over: install the Alg. 2 plan (init fill + static SJF queue)
+        for (int i = 0; i < st[ST_MAIN_QLEN]; ++i) a.queue[i] = a.main_queue[i];
+        st[ST_QLEN] = st[ST_MAIN_QLEN];
+        st[ST_QHEAD] = 0;
+        st[ST_BARRIER] = 0;
+        st[ST_QUOTA] = 0;
+        st[ST_STOPK] = 0;
+        st[ST_PHASE] = 1;
+        st[ST_MAIN_PENDING] = 0;
+        for (int s = 0; s < a.g; ++s) {
+          a.slot_count[s] = 0;
+          a.slot_uid[s] = s < st[ST_MAIN_NINIT] ? a.main_init[s] : -1;
+        }
       }
     }
+    // pages for rows crossing a page boundary, allocated in ascending slot order (LIFO stack)
+    int any = 0;
+    for (int s = 0; s < a.row_cap; ++s) {
+      s_alloc_page[s] = -1;
+      const int uid = s < a.g ? a.slot_uid[s] : -1;
+      if (uid < 0) continue;
+      any = 1;
+      const int tt = a.t[uid];
+      if (tt % a.pt == 0) {
+        int page = 0;
+        if (st[ST_FREE_TOP] > 0) page = a.free_stack[--st[ST_FREE_TOP]];
+        else st[ST_ERROR] = 1;  // budget violated: pool exhausted
+        a.pagetab[(size_t)uid * a.maxp + tt / a.pt] = page;
+        a.npages[uid] += 1;
+        st[ST_LIVE] += 1;
+      }
+    }
+    s_any = any;
   }
-  // ---- prepare rows of the next step
-  bool any = false;
-  for (int s = 0; s < a.row_cap; ++s) {
+  __syncthreads();
+  // ---- rows of the next step, one thread per row
+  const bool any = s_any != 0;
+  int nch = 0;
+  if (tid < a.row_cap) {
+    const int s = tid;
     a.keys[s] = 0ull;
     const int uid = s < a.g ? a.slot_uid[s] : -1;
     if (uid < 0) {
@@ -755,36 +870,26 @@ __global__ void sched_kernel(SchedArgs a, int consume) {
       a.row_pos[s] = 0;
       a.row_kvloc[s] = 0;
       a.row_len[s] = 0;
-      continue;
+    } else {
+      const int tt = a.t[uid];
+      a.row_active[s] = 1;
+      a.row_uid[s] = a.prompt_id * a.G + uid;
+      a.row_lid[s] = uid;
+      a.row_t[s] = tt;
+      a.row_tok[s] = tt == 0 ? a.prompt_last : a.tokens[(size_t)uid * a.max_new + tt - 1];
+      a.row_pos[s] = a.P - 1 + tt;
+      a.row_kvloc[s] = a.pagetab[(size_t)uid * a.maxp + tt / a.pt] * a.pt + tt % a.pt;
+      a.row_len[s] = tt + 1;
+      nch = (tt + 1 + a.chunk - 1) / a.chunk;
     }
-    any = true;
-    const int tt = a.t[uid];
-    if (tt % a.pt == 0) {
-      int page = 0;
-      if (st[ST_FREE_TOP] > 0) page = a.free_stack[--st[ST_FREE_TOP]];
-      else st[ST_ERROR] = 1;  // budget violated: pool exhausted
-      a.pagetab[(size_t)uid * a.maxp + tt / a.pt] = page;
-      a.npages[uid] += 1;
-      st[ST_LIVE] += 1;
-    }
-    a.row_active[s] = 1;
-    a.row_uid[s] = a.prompt_id * a.G + uid;
-    a.row_lid[s] = uid;
-    a.row_t[s] = tt;
-    a.row_tok[s] = tt == 0 ? a.prompt_last : a.tokens[(size_t)uid * a.max_new + tt - 1];
-    a.row_pos[s] = a.P - 1 + tt;
-    a.row_kvloc[s] = a.pagetab[(size_t)uid * a.maxp + tt / a.pt] * a.pt + tt % a.pt;
-    a.row_len[s] = tt + 1;
-    st[ST_SUFFIX] += tt + 1;
+    s_cnt[s] = nch;
   }
-  // attention work list of the next step: shared-prefix chunks first (one CTA
-  // each, all live rows), then every live slot's suffix chunks (one warp each,
-  // with the chunk's page ids embedded so the warp stages in one round trip).
-  {
-    int n = 0, npre = 0;
-    if (any) {
-      // prefix units: (kv head, chunk, group of 4 rows) for groups holding a live row
-      for (int g = 0; !a.tc_prefix && g * 4 < a.row_cap; ++g) {
+  __syncthreads();
+  if (tid == 0) {
+    // exclusive prefix sum of suffix chunks; shared-prefix items first (CUDA-core prefix only)
+    int n = 0;
+    if (any && !a.tc_prefix) {
+      for (int g = 0; g * 4 < a.row_cap; ++g) {
         bool live = false;
         for (int s = 4 * g; s < 4 * g + 4 && s < a.row_cap; ++s) live = live || a.row_active[s];
         if (!live) continue;
@@ -792,30 +897,44 @@ __global__ void sched_kernel(SchedArgs a, int consume) {
           for (int c = 0; c < a.nc_pre; ++c)
             a.attn_items[(size_t)(n++) * kItemStride] = (int)(0x80000000u | (h << 16) | (c << 8) | g);
       }
-      npre = n;
-      const int ppc = a.chunk / a.pt;  // pages per suffix chunk (<= 16)
-      for (int c = 0; c < a.nc_suf; ++c)
-        for (int s = 0; s < a.row_cap; ++s)
-          if (a.row_active[s] && c * a.chunk < a.row_len[s])
-            for (int h = 0; h < a.Hkv; ++h) {
-              int32_t* item = a.attn_items + (size_t)(n++) * kItemStride;
-              item[0] = (c << 16) | (s << 8) | h;
-              const int np = min(ppc, (a.row_len[s] - c * a.chunk + a.pt - 1) / a.pt);
-              for (int j = 0; j < np; ++j) item[1 + j] = a.pagetab[(size_t)a.row_lid[s] * a.maxp + c * ppc + j];
-            }
     }
-    st[ST_ATTN_ITEMS] = n;
-    st[ST_ATTN_PRE] = npre;
+    s_npre = n;
+    int acc = 0;
+    for (int s = 0; s < a.row_cap; ++s) {
+      const int v = s_cnt[s];
+      s_cnt[s] = acc;
+      acc += v;
+    }
+    s_cnt[a.row_cap] = acc;
+    st[ST_ATTN_ITEMS] = n + acc * a.Hkv;
+    st[ST_ATTN_PRE] = n;
+    long long suf = 0;
+    for (int s = 0; s < a.row_cap; ++s) suf += a.row_len[s];
+    st[ST_SUFFIX] += suf;
+    if (any) {
+      const long long step = st[ST_STEP];
+      if (step < a.log_cap) {
+        for (int s = 0; s < a.g; ++s) a.log_slot[step * a.g + s] = a.slot_uid[s];
+        a.log_live[step] = (int32_t)st[ST_LIVE];
+      }
+      st[ST_STEP] = step + 1;
+      if (st[ST_PHASE] == 0) st[ST_PREFIX_STEPS] += 1;
+      if (st[ST_LIVE] > st[ST_PEAK]) st[ST_PEAK] = st[ST_LIVE];
+    }
   }
-  if (any) {
-    const long long step = st[ST_STEP];
-    if (step < a.log_cap) {
-      for (int s = 0; s < a.g; ++s) a.log_slot[step * a.g + s] = a.slot_uid[s];
-      a.log_live[step] = (int32_t)st[ST_LIVE];
-    }
-    st[ST_STEP] = step + 1;
-    if (st[ST_PHASE] == 0) st[ST_PREFIX_STEPS] += 1;
-    if (st[ST_LIVE] > st[ST_PEAK]) st[ST_PEAK] = st[ST_LIVE];
+  __syncthreads();
+  // ---- suffix items of row s: (chunk c, kv head h) with the chunk's page ids embedded
+  if (tid < a.row_cap && nch > 0) {
+    const int s = tid;
+    const int ppc = a.chunk / a.pt;  // pages per suffix chunk (<= 16)
+    const int len = a.row_len[s], lid = a.row_lid[s];
+    for (int c = 0; c < nch; ++c)
+      for (int h = 0; h < a.Hkv; ++h) {
+        int32_t* item = a.attn_items + (size_t)(s_npre + (s_cnt[s] + c) * a.Hkv + h) * kItemStride;
+        item[0] = (c << 16) | (s << 8) | h;
+        const int np = min(ppc, (len - c * a.chunk + a.pt - 1) / a.pt);
+        for (int j = 0; j < np; ++j) item[1 + j] = a.pagetab[(size_t)lid * a.maxp + c * ppc + j];
+      }
   }
 }
 

@@ -1,5 +1,5 @@
 #!/bin/bash
-# One gpurun call: GPU tests, bench line, launch list and one full ncu capture of the top kernel.
+# One gpurun call: GPU tests, bench line, smoke, launch list and full ncu captures of the top kernels.
 # usage (from this container):  gpurun --timeout 2400 -- 'bash tools/gpu_round.sh [tag]'
 TAG=${1:-r01}
 OUT=gpurun_out/$TAG
@@ -8,12 +8,14 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $
 timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
-# launch list: eager decode steps (IS_NO_GRAPH=1) after prefill; cold-cache serialised -> compare shares
+# launch list of eager decode steps after prefill (cold-cache, serialised: compare shares)
 IS_NO_GRAPH=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $OUT/launches.csv python tools/step_driver.py --steps 3 > $OUT/launches.log 2>&1
-# full capture of the gate/up GEMM (EPI_SWIGLU = 2) and of the attention kernels
+# full captures: gate/up GEMM (EPI_SWIGLU = 2), the suffix attention kernel, the tcgen05 prefix kernel
 IS_NO_GRAPH=1 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k 'regex:gemm_swapab_kernel<[0-9]+, 2,' -s 28 -c 2 -o $OUT/gateup python tools/step_driver.py --steps 2 > $OUT/ncu_gateup.log 2>&1
+  -k 'regex:gemm_swapab_kernel<\(int\)16, \(int\)2' -s 28 -c 2 -o $OUT/gateup python tools/step_driver.py --steps 2 > $OUT/ncu_gateup.log 2>&1
 IS_NO_GRAPH=1 timeout 900 ncu --set full --clock-control none --import-source on \
   -k 'regex:attn' -s 56 -c 4 -o $OUT/attn python tools/step_driver.py --steps 2 > $OUT/ncu_attn.log 2>&1
+IS_NO_GRAPH=1 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+  -k 'regex:gemm_swapab_kernel<\(int\)16, \(int\)3' -s 0 -c 1 -o $OUT/lmhead python tools/step_driver.py --steps 2 > $OUT/ncu_lmhead.log 2>&1
 echo done > $OUT/DONE

@@ -1586,11 +1586,11 @@ extern "C" is_status is_profile_step(is_ctx* c, float* h_ms, int32_t* h_kind, in
 extern "C" is_status is_dbg_gemm(const void* d_w, const void* d_x, float* d_y, int32_t M, int32_t K, int32_t rows,
                                  int32_t split, void* stream) {
   if (rows < 1 || rows > 64 || K % 64 || split < 1 || split > 8) return fail(IS_ERR_CONFIG, "bad dbg_gemm shape");
-  int dev = 0;
-  CK(cudaGetDevice(&dev));
-  cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, dev));
-  g_num_sms = prop.multiProcessorCount;
+  if (!g_num_sms) {  // (cudaGetDeviceProperties costs milliseconds: once)
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
   const int BN = rows <= 16 ? 16 : (rows <= 32 ? 32 : 64);
   CUtensorMap tA, tB;
   CKS(make_tmap(&tA, d_w, M, K, kBM));

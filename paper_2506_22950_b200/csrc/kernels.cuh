@@ -578,6 +578,10 @@ __global__ void __launch_bounds__(128, 1)
   astamp(a, 1);
   pdl_launch_dependents();    // the suffix kernel may start now (it does not touch our outputs)
   // Q rows n = r*REP + e (K-major, 128-byte swizzle, two 64-d atoms)
+  if (threadIdx.x < N) {
+    const int r = threadIdx.x / REP;
+    colI[N + threadIdx.x] = (r < a.rows && a.row_active[r]) ? 1.f : 0.f;  // row live (read by the epilogue)
+  }
   for (int i = threadIdx.x; i < N * 16; i += 128) {
     const int n = i >> 4, c = i & 15;
     const int r = n / REP, e = n % REP;
@@ -606,58 +610,76 @@ __global__ void __launch_bounds__(128, 1)
   mbar_wait(&bars[1], 0);
   astamp(a, 4);
   tc_fence_after();
-  // ---- column softmax.  S^T rows (token t) are transposed through padded smem
-  // so that column statistics are computed with independent loads (lane = column).
+  // ---- column softmax in registers.  Thread t holds S^T row t (its token) for 32
+  // query columns at a time; a transpose reduction (31 shuffles) leaves lane l with
+  // column l's max / sum over the warp's 32 tokens, the 4 warps combine through smem.
   const int t = warp * 32 + lane;  // token lane (TMEM lane quadrant = warp)
+  float* sbuf = Ssm;               // [4][32] maxima, [4][32] sums, [64] column sums (Ssm is free now)
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   const bool valid = t < ntok;
 #pragma unroll 1
-  for (int c = 0; c < N / 16; ++c) {
-    float v16[16];
-    tmem_ld16(trow + c * 16, v16);
+  for (int c32 = 0; c32 < (N + 31) / 32; ++c32) {
+    const int ncol = N - c32 * 32 < 32 ? N - c32 * 32 : 32;  // 16 or 32
+    float sv[32], r[32];
+    tmem_ld16(trow + c32 * 32, sv);
+    if (ncol > 16) tmem_ld16(trow + c32 * 32 + 16, sv + 16);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) Ssm[(c * 16 + j) * 129 + t] = valid ? v16[j] * a.scale : -INFINITY;
-  }
-  __syncthreads();
-  // column max over the 128 tokens: warp w covers tokens [32w, 32w+32), lane = column
-#pragma unroll 1
-  for (int n0 = 0; n0 < N; n0 += 32) {
-    const int n = n0 + lane;
-    float mx = -INFINITY;
-    if (n < N) {
-#pragma unroll 8
-      for (int i = 0; i < 32; ++i) mx = fmaxf(mx, Ssm[n * 129 + warp * 32 + i]);
-      red[warp * N + n] = mx;
+    for (int j = 0; j < 32; ++j) {
+      sv[j] = (valid && j < ncol) ? sv[j] * a.scale : -INFINITY;
+      r[j] = sv[j];
     }
-  }
-  __syncthreads();
-  if (threadIdx.x < N) {
-    const int n = threadIdx.x;
-    colM[n] = fmaxf(fmaxf(red[n], red[N + n]), fmaxf(red[2 * N + n], red[3 * N + n]));
-  }
-  __syncthreads();
-  // p = exp(s - M): P^T operand (row n, K index t, two 64-token atoms, 128-byte
-  // swizzle) as a bf16 hi/lo pair (two accumulating MMAs keep P to ~2^-16)
-#pragma unroll 4
-  for (int n = 0; n < N; ++n) {
-    const float sv = Ssm[n * 129 + t];
-    const float p = valid ? expf(sv - colM[n]) : 0.f;
-    Ssm[n * 129 + t] = p;
-    const int off = (t >> 6) * N * 128 + n * 128 + ((((t & 63) >> 3) ^ (n & 7)) << 4) + (t & 7) * 2;
-    const __nv_bfloat16 phi = __float2bfloat16_rn(p);
-    *reinterpret_cast<__nv_bfloat16*>(Psm + off) = phi;
-    *reinterpret_cast<__nv_bfloat16*>(Plo + off) = __float2bfloat16_rn(p - __bfloat162float(phi));
-  }
-  __syncthreads();
-#pragma unroll 1
-  for (int n0 = 0; n0 < N; n0 += 32) {
-    const int n = n0 + lane;
-    float sm_ = 0.f;
-    if (n < N) {
-#pragma unroll 8
-      for (int i = 0; i < 32; ++i) sm_ += Ssm[n * 129 + warp * 32 + i];
-      red[4 * N + warp * N + n] = sm_;
+    // transpose-max: after the step with offset o, lanes with bit o hold the upper half
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int j = 0; j < o; ++j) {
+        const float send = up ? r[j] : r[j + o];
+        const float keep = up ? r[j + o] : r[j];
+        r[j] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, o));
+      }
     }
+    sbuf[warp * 32 + lane] = r[0];  // column c32*32 + lane, this warp's 32 tokens
+    __syncthreads();
+    float mcol = fmaxf(fmaxf(sbuf[lane], sbuf[32 + lane]), fmaxf(sbuf[64 + lane], sbuf[96 + lane]));
+    __syncthreads();
+    // p = exp(s - M[column]); M of column j comes from lane j
+    float p[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float Mj = __shfl_sync(0xffffffffu, mcol, j);
+      p[j] = (valid && j < ncol) ? expf(sv[j] - Mj) : 0.f;
+      r[j] = p[j];
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int j = 0; j < o; ++j) {
+        const float send = up ? r[j] : r[j + o];
+        const float keep = up ? r[j + o] : r[j];
+        r[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    sbuf[128 + warp * 32 + lane] = r[0];
+    // P^T operand (row n, K index t, two 64-token atoms, 128-byte swizzle) as a bf16
+    // hi/lo pair (two accumulating MMAs keep P to ~2^-16)
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j >= ncol) break;
+      const int n = c32 * 32 + j;
+      const int off = (t >> 6) * N * 128 + n * 128 + ((((t & 63) >> 3) ^ (n & 7)) << 4) + (t & 7) * 2;
+      const __nv_bfloat16 phi = __float2bfloat16_rn(p[j]);
+      *reinterpret_cast<__nv_bfloat16*>(Psm + off) = phi;
+      *reinterpret_cast<__nv_bfloat16*>(Plo + off) = __float2bfloat16_rn(p[j] - __bfloat162float(phi));
+    }
+    __syncthreads();
+    if (threadIdx.x < ncol) {
+      const int n = c32 * 32 + threadIdx.x;
+      colM[n] = mcol;  // (thread x < 32 is lane x of warp 0: its mcol is column x)
+      sbuf[8 * 64 + n] = sbuf[128 + threadIdx.x] + sbuf[160 + threadIdx.x] + sbuf[192 + threadIdx.x] + sbuf[224 + threadIdx.x];
+    }
+    __syncthreads();
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
@@ -682,9 +704,9 @@ __global__ void __launch_bounds__(128, 1)
   // ---- epilogue: lane = head dim d; normalise and write partial slot `tile`
   if (threadIdx.x < N) {
     const int n = threadIdx.x, r = n / REP, e = n % REP;
-    const float L = red[4 * N + n] + red[5 * N + n] + red[6 * N + n] + red[7 * N + n];
+    const float L = Ssm[8 * 64 + n];
     colI[n] = 1.0f / L;
-    const bool act = r < a.rows && a.row_active[r];
+    const bool act = colI[N + n] != 0.f;
     colP[n] = act ? (long long)(((size_t)r * a.Hq + h * REP + e) * a.NC + tile) : -1ll;
     if (act) *reinterpret_cast<float2*>(a.part_ml + colP[n] * 2) = make_float2(colM[n], L);
   }

@@ -459,8 +459,6 @@ static SchedArgs sched_args(is_ctx* c) {
   a.maxp = c->maxp;
   a.P = c->P;
   a.log_cap = c->log_cap;
-  a.prompt_id = c->prompt_id;
-  a.prompt_last = c->prompt_last;
   a.st = c->st_dev;
   a.slot_uid = c->slot_uid;
   a.slot_count = c->slot_count;
@@ -1411,6 +1409,8 @@ extern "C" is_status is_start_group(is_ctx* c, const int32_t* true_len, const in
     st[ST_QLEN] = po.queue_len;
   }
   st[ST_FREE_TOP] = c->num_pages;
+  st[ST_PROMPT_ID] = c->prompt_id;
+  st[ST_PROMPT_LAST] = c->prompt_last;
   std::vector<int32_t> fs(std::max(c->num_pages, 1));
   for (int i = 0; i < c->num_pages; ++i) fs[i] = c->num_pages - 1 - i;  // pop order 0, 1, 2, ...
   CK(cudaMemcpyAsync(c->st_dev, st.data(), st.size() * 8, cudaMemcpyHostToDevice, c->st));

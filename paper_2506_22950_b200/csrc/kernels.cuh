@@ -753,11 +753,13 @@ enum SchedState {
   ST_ATTN_ITEMS,   // length of the attention work list for the next step
   ST_ATTN_PRE,     // of which shared-prefix items (must follow ST_ATTN_ITEMS)
   ST_SUFFIX,       // sum over steps of the live rows' suffix lengths
+  ST_PROMPT_ID,    // prompt of the current group (RNG uid base), set by is_start_group: device state,
+  ST_PROMPT_LAST,  //   not a kernel parameter, because the decode step is a CUDA graph reused across prompts
   ST_COUNT
 };
 
 struct SchedArgs {
-  int G, g, row_cap, max_new, pt, maxp, P, log_cap, prompt_id, prompt_last;
+  int G, g, row_cap, max_new, pt, maxp, P, log_cap;
   long long* st;             // [ST_COUNT]
   int32_t* slot_uid;         // [g]
   int32_t* slot_count;       // [g]
@@ -895,10 +897,10 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
     } else {
       const int tt = a.t[uid];
       a.row_active[s] = 1;
-      a.row_uid[s] = a.prompt_id * a.G + uid;
+      a.row_uid[s] = (int)st[ST_PROMPT_ID] * a.G + uid;
       a.row_lid[s] = uid;
       a.row_t[s] = tt;
-      a.row_tok[s] = tt == 0 ? a.prompt_last : a.tokens[(size_t)uid * a.max_new + tt - 1];
+      a.row_tok[s] = tt == 0 ? (int)st[ST_PROMPT_LAST] : a.tokens[(size_t)uid * a.max_new + tt - 1];
       a.row_pos[s] = a.P - 1 + tt;
       a.row_kvloc[s] = a.pagetab[(size_t)uid * a.maxp + tt / a.pt] * a.pt + tt % a.pt;
       a.row_len[s] = tt + 1;

@@ -124,3 +124,43 @@ def test_fullsize_late_step_logits(full):
         assert sampler.sample_token(full["late"][s], SEED, 3 * G + uid, LATE) == full["tokens"][uid, LATE]
         checked += 1
     assert checked > 0
+
+
+@pytest.fixture(scope="module")
+def prefix_phase():
+    """BASELINE config 4 at full size: Qwen3-1.7B shape, G = 64, g = 8, prefix phase k = 16
+    (parked pages), long-tail lengths, 1 GiB KV budget."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2506_22950_b200 import _lib
+    G4, g4, k4, budget = 64, 8, 16, 1 << 30
+    w = gen_weights(SHAPE, seed=SEED, device="cuda")
+    cfg = _lib.make_config(SHAPE, G4, g4, MAX_NEW, P, mode="infinite", prefix_k=k4, page_tokens=16,
+                           kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED)
+    ctx = _lib.Context(cfg, w)
+    prompt = gen_prompt(SHAPE.vocab, P, 5, seed=SEED)
+    true = gen_trace("longtail", G4, MAX_NEW, SEED + 5)
+    pred = predict_lengths(true, "noisy", 0.3, seed=SEED + 5, prefix_k=k4)
+    ctx.is_prefill(torch.as_tensor(prompt, device="cuda"), 5)
+    ctx.is_start_group(true, pred)
+    steps = ctx.is_run_group()
+    res = dict(steps=steps, stats=ctx.is_query(), sched=ctx.is_copy_schedule(), true=true, pred=pred,
+               budget=budget, G=G4, g=g4, k=k4)
+    ctx.close()
+    del w
+    torch.cuda.empty_cache()
+    return res
+
+
+def test_fullsize_prefix_phase_schedule_and_budget(prefix_phase):
+    r = prefix_phase
+    ref = simulator.simulate(r["true"], "infinite", r["g"], pred=r["pred"], eps=0.1, prefix_k=r["k"], page_tokens=16)
+    slots, live = r["sched"]
+    assert r["steps"] == ref.total_steps
+    assert r["stats"]["prefix_steps"] == ref.prefix_steps
+    assert slots.tolist() == ref.slot_table
+    assert live.tolist() == ref.live_pages
+    st = r["stats"]
+    assert st["completed"] == r["G"] and st["error"] == 0
+    assert st["peak_pages"] == ref.peak_pages
+    assert st["peak_kv_bytes"] <= r["budget"]  # R25: the budget is a hard invariant

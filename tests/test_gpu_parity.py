@@ -197,3 +197,39 @@ def test_tiny_rewards_and_advantages(lib, tiny):
     assert ln.cpu().tolist() == [int(x) for x in tiny["true"]]
     adv = lib.is_group_advantages(rew.cpu().numpy())
     assert np.allclose(adv, grpo.advantages(ref), atol=1e-5)
+
+
+def test_tiny_context_reused_across_prompts(lib, tiny):
+    """The decode step is one CUDA graph per context, replayed for every prompt: prompt 1
+    decoded after prompt 0 in the same context must equal prompt 1 in a fresh context
+    (RNG uids prompt_id*G + i and the first input token come from device state)."""
+    w_dev = tiny["w_dev"]
+    p1 = gen_prompt(TINY.vocab, 16, 1, seed=SEED)
+    true1 = gen_trace("tiny", 8, 32, 2)
+    pred1 = predict_lengths(true1, "noisy", 0.3, seed=2)
+
+    def mk():
+        cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", kv_budget_bytes=tiny["budget"], seed=SEED,
+                              decode_impl=tiny["impl"])
+        return lib.Context(cfg, w_dev)
+
+    a = mk()
+    a.is_prefill(torch.as_tensor(tiny["prompt"], device="cuda"), 0)
+    a.is_start_group(tiny["true"], tiny["pred"])
+    a.is_run_group()
+    a.is_prefill(torch.as_tensor(p1, device="cuda"), 1)
+    a.is_start_group(true1, pred1)
+    a.is_run_group()
+    reused = a.is_copy_tokens()
+    a.close()
+    b = mk()
+    b.is_prefill(torch.as_tensor(p1, device="cuda"), 1)
+    b.is_start_group(true1, pred1)
+    b.is_run_group()
+    fresh = b.is_copy_tokens()
+    b.close()
+    assert np.array_equal(reused, fresh)
+    # and prompt 1's stream is its own (uid base 1*G), not a replay of prompt 0's RNG
+    z = M.teacher_forced_logits(tiny["w"], TINY, p1, [int(x) for x in fresh[0, :2]], mirror=True, rows=[0])[0]
+    tok, margin = sampler.sample_margin(z.astype(np.float32), SEED, 1 * 8 + 0, 0)
+    assert tok == fresh[0, 0] or margin < 0.05

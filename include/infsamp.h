@@ -73,6 +73,10 @@ typedef struct {
                               (falls back to 1 when Hq/Hkv > 4 or the attention needs more than
                               64 partials per row); 1: one kernel per operator (the Python
                               binding's default) */
+  int32_t max_groups;      /* co-resident prompt groups sharing each decode step (SURVEY §8f
+                              NEXT-1; 0 or 1 = the paper's one group per GPU).  Group slot m owns
+                              rows m*g .. m*g+g-1; kv_budget_bytes is per group, the page pool
+                              (max_groups x the per-group pool) is shared.  max_groups*g <= 64 */
 } is_config;
 
 /* Alg. 2 output plus the runtime plan (Alg. 1, Alg. 3).  All arrays are
@@ -108,6 +112,9 @@ typedef struct {
   int64_t layer_kernel_ns;       /* persistent decode kernel: accumulated device time (globaltimer, CTA 0) */
   int64_t layer_kernel_launches; /*   and launches, since is_create */
   int64_t suffix_tokens;  /* sum over decode steps of the live rows' suffix lengths (algorithmic KV bytes) */
+  int32_t groups;         /* co-resident group slots of the context */
+  int64_t global_steps;   /* decode steps with >= 1 active slot in any group */
+  int64_t global_peak_kv_bytes;  /* all groups' prefixes + peak pages of the shared pool */
 } is_stats;
 
 typedef struct is_ctx is_ctx;
@@ -175,6 +182,25 @@ is_status is_copy_tokens(is_ctx* ctx, int32_t* dst, int32_t dst_is_device);
  * [max_steps] (R26); returns the number of logged steps in *h_n. */
 is_status is_copy_schedule(is_ctx* ctx, int32_t* h_slot_table, int32_t* h_live_pages, int32_t max_steps,
                            int32_t* h_n);
+
+/* Co-resident groups (is_config.max_groups > 1).  The _slot
+ * calls act on group slot m in [0, max_groups); the unsuffixed calls above are
+ * the slot-0 calls.  Groups are independent: each has its own prompt (shared
+ * prefix KV), plan, refill queue, RNG uids (prompt_id*G + i) and schedule log,
+ * and every decode step serves all started groups' live rows at once.
+ * is_prefill_slot / is_start_group_slot may be called while other groups are
+ * mid-rollout (between decode steps); restarting a slot returns the pages its
+ * previous group still held.  is_run_until_any_done decodes until a started
+ * group completes; *h_done_mask gets bit m for every started group that is
+ * done, *h_global_steps the decode steps run so far in this context. */
+is_status is_prefill_slot(is_ctx* ctx, int32_t slot, const int32_t* d_prompt, int32_t prompt_id);
+is_status is_start_group_slot(is_ctx* ctx, int32_t slot, const int32_t* h_true_len, const int32_t* h_pred_len);
+is_status is_run_until_any_done(is_ctx* ctx, int32_t max_steps, int32_t* h_done_mask, int64_t* h_global_steps);
+is_status is_query_slot(is_ctx* ctx, int32_t slot, is_stats* out);
+is_status is_copy_tokens_slot(is_ctx* ctx, int32_t slot, int32_t* dst, int32_t dst_is_device);
+is_status is_copy_schedule_slot(is_ctx* ctx, int32_t slot, int32_t* h_slot_table, int32_t* h_live_pages,
+                                int32_t max_steps, int32_t* h_n);
+is_status is_group_results_slot(is_ctx* ctx, int32_t slot, float* d_reward, int32_t* d_len);
 
 /* Benchmark reward and completion length per sample (R29):
  * d_reward[G] = #{tokens < vocab/2}/len, d_len[G] = len.  Device buffers. */

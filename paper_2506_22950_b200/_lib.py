@@ -18,7 +18,9 @@ ADV_MODES = {"std_norm": 0, "mean_only": 1}
 EXPORTS = ["is_plan", "is_create", "is_destroy", "is_prefill", "is_start_group", "is_decode_step",
            "is_refill", "is_run_group", "is_query", "is_copy_tokens", "is_copy_schedule",
            "is_group_results", "is_group_advantages", "is_set_logits_dump", "is_profile_step",
-           "is_dbg_gemm", "is_dbg_mk_trace", "is_dbg_copy", "is_last_error", "is_version"]
+           "is_dbg_gemm", "is_dbg_mk_trace", "is_dbg_copy", "is_prefill_slot", "is_start_group_slot",
+           "is_run_until_any_done", "is_query_slot", "is_copy_tokens_slot", "is_copy_schedule_slot",
+           "is_group_results_slot", "is_last_error", "is_version"]
 
 
 class InfsampError(RuntimeError):
@@ -39,7 +41,7 @@ class Config(ctypes.Structure):
                 ("prefix_k", ctypes.c_int32), ("page_tokens", ctypes.c_int32),
                 ("row_capacity", ctypes.c_int32), ("kv_budget_bytes", ctypes.c_int64),
                 ("eps", ctypes.c_double), ("temperature", ctypes.c_float), ("seed", ctypes.c_uint64),
-                ("mode", ctypes.c_int32), ("decode_impl", ctypes.c_int32)]
+                ("mode", ctypes.c_int32), ("decode_impl", ctypes.c_int32), ("max_groups", ctypes.c_int32)]
 
 
 class PlanOut(ctypes.Structure):
@@ -58,7 +60,8 @@ class Stats(ctypes.Structure):
                 ("page_bytes", ctypes.c_int64), ("prefix_bytes", ctypes.c_int64),
                 ("num_pages", ctypes.c_int32), ("row_capacity", ctypes.c_int32),
                 ("decode_impl", ctypes.c_int32), ("layer_kernel_ns", ctypes.c_int64),
-                ("layer_kernel_launches", ctypes.c_int64), ("suffix_tokens", ctypes.c_int64)]
+                ("layer_kernel_launches", ctypes.c_int64), ("suffix_tokens", ctypes.c_int64),
+                ("groups", ctypes.c_int32), ("global_steps", ctypes.c_int64), ("global_peak_kv_bytes", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -105,6 +108,13 @@ def load(build_if_missing=True):
     L.is_dbg_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]
     L.is_dbg_mk_trace.argtypes = [vp, vp, i32, vp, i32, vp, ctypes.c_int64, vp]
     L.is_dbg_copy.argtypes = [vp, i32, vp, ctypes.c_int64]
+    L.is_prefill_slot.argtypes = [vp, i32, vp, i32]
+    L.is_start_group_slot.argtypes = [vp, i32, vp, vp]
+    L.is_run_until_any_done.argtypes = [vp, i32, ctypes.POINTER(i32), i64p]
+    L.is_query_slot.argtypes = [vp, i32, ctypes.POINTER(Stats)]
+    L.is_copy_tokens_slot.argtypes = [vp, i32, vp, i32]
+    L.is_copy_schedule_slot.argtypes = [vp, i32, vp, vp, i32, ctypes.POINTER(i32)]
+    L.is_group_results_slot.argtypes = [vp, i32, vp, vp]
     L.is_last_error.restype = ctypes.c_char_p
     L.is_last_error.argtypes = []
     L.is_version.restype = ctypes.c_char_p
@@ -125,7 +135,8 @@ def _np_ptr(a):
 
 
 def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix_k=0, page_tokens=16,
-                row_capacity=0, kv_budget_bytes=0, eps=0.1, temperature=0.8, seed=20261017, decode_impl=None):
+                row_capacity=0, kv_budget_bytes=0, eps=0.1, temperature=0.8, seed=20261017, decode_impl=None,
+                max_groups=1):
     """decode_impl: 0 = persistent decode kernel, 1 = one kernel per operator (default: it is
     faster on B200); None reads IS_DECODE_IMPL from the environment."""
     c = Config()
@@ -138,6 +149,7 @@ def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix
     if decode_impl is None:
         decode_impl = int(os.environ.get("IS_DECODE_IMPL", "1"))
     c.decode_impl = decode_impl
+    c.max_groups = max_groups
     return c
 
 
@@ -224,13 +236,21 @@ class Context:
         except Exception:
             pass
 
-    def is_prefill(self, d_prompt, prompt_id):
-        _check(load().is_prefill(self._h, d_prompt.data_ptr(), int(prompt_id)))
+    def is_prefill(self, d_prompt, prompt_id, slot=0):
+        _check(load().is_prefill_slot(self._h, int(slot), d_prompt.data_ptr(), int(prompt_id)))
 
-    def is_start_group(self, true_len, pred_len=None):
+    def is_start_group(self, true_len, pred_len=None, slot=0):
         t = np.ascontiguousarray(true_len, np.int32)
         p = None if pred_len is None else np.ascontiguousarray(pred_len, np.int32)
-        _check(load().is_start_group(self._h, _np_ptr(t), None if p is None else _np_ptr(p)))
+        _check(load().is_start_group_slot(self._h, int(slot), _np_ptr(t), None if p is None else _np_ptr(p)))
+
+    def is_run_until_any_done(self, max_steps=1 << 30):
+        """Decode until a started group completes: (done-slot mask, global decode steps so far)."""
+        mask = ctypes.c_int32()
+        steps = ctypes.c_int64()
+        _check(load().is_run_until_any_done(self._h, int(min(max_steps, 2 ** 31 - 1)), ctypes.byref(mask),
+                                            ctypes.byref(steps)))
+        return mask.value, steps.value
 
     def is_decode_step(self, d_next=None, d_fin=None):
         _check(load().is_decode_step(self._h, None if d_next is None else d_next.data_ptr(),
@@ -245,27 +265,28 @@ class Context:
         _check(load().is_run_group(self._h, int(min(max_steps, 2 ** 31 - 1)), ctypes.byref(n)))
         return n.value
 
-    def is_query(self):
+    def is_query(self, slot=0):
         s = Stats()
-        _check(load().is_query(self._h, ctypes.byref(s)))
+        _check(load().is_query_slot(self._h, int(slot), ctypes.byref(s)))
         return s.as_dict()
 
-    def is_copy_tokens(self):
+    def is_copy_tokens(self, slot=0):
         out = np.zeros((self.G, self.cfg.max_new_tokens), np.int32)
-        _check(load().is_copy_tokens(self._h, _np_ptr(out), 0))
+        _check(load().is_copy_tokens_slot(self._h, int(slot), _np_ptr(out), 0))
         return out
 
-    def is_copy_schedule(self, max_steps=None):
+    def is_copy_schedule(self, max_steps=None, slot=0):
         if max_steps is None:
-            max_steps = self.is_query()["steps"]
+            max_steps = self.is_query(slot)["steps"]
         slots = np.zeros((max(max_steps, 1), self.g), np.int32)
         live = np.zeros(max(max_steps, 1), np.int32)
         n = ctypes.c_int32()
-        _check(load().is_copy_schedule(self._h, _np_ptr(slots), _np_ptr(live), max_steps, ctypes.byref(n)))
+        _check(load().is_copy_schedule_slot(self._h, int(slot), _np_ptr(slots), _np_ptr(live), max_steps,
+                                            ctypes.byref(n)))
         return slots[:n.value], live[:n.value]
 
-    def is_group_results(self, d_reward, d_len):
-        _check(load().is_group_results(self._h, d_reward.data_ptr(), d_len.data_ptr()))
+    def is_group_results(self, d_reward, d_len, slot=0):
+        _check(load().is_group_results_slot(self._h, int(slot), d_reward.data_ptr(), d_len.data_ptr()))
 
     def is_set_logits_dump(self, d_logits):
         _check(load().is_set_logits_dump(self._h, None if d_logits is None else d_logits.data_ptr()))

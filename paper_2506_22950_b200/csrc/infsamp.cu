@@ -57,6 +57,8 @@ static int64_t kv_bytes_per_token(const is_shape& s) {
   return 2ll * s.layers * s.n_kv_heads * s.head_dim * 2;
 }
 
+static int n_groups(const is_config* c) { return c->max_groups > 0 ? c->max_groups : 1; }
+
 static is_status check_config(const is_config* c) {
   const is_shape& s = c->shape;
   if (s.head_dim != 128) return fail(IS_ERR_CONFIG, "head_dim must be 128 (got %d)", s.head_dim);
@@ -72,12 +74,14 @@ static is_status check_config(const is_config* c) {
   if (c->prefix_k < 0 || (c->prefix_k > 0 && c->mode != IS_MODE_INFINITE))
     return fail(IS_ERR_CONFIG, "prefix_k > 0 requires IS_MODE_INFINITE");
   if (!(c->temperature > 0)) return fail(IS_ERR_CONFIG, "temperature must be > 0");
+  if (c->max_groups < 0 || n_groups(c) > 8 || n_groups(c) * g > 64)
+    return fail(IS_ERR_CONFIG, "need 1 <= max_groups <= 8 and max_groups * g <= 64 (got %d x %d)", n_groups(c), g);
   return IS_OK;
 }
 
 static int eff_g(const is_config* c) { return c->mode == IS_MODE_FULL ? c->G : c->g; }
 static int row_cap_of(const is_config* c) {
-  int rc = c->row_capacity > 0 ? c->row_capacity : ((eff_g(c) + 15) / 16) * 16;
+  int rc = c->row_capacity > 0 ? c->row_capacity : ((n_groups(c) * eff_g(c) + 15) / 16) * 16;
   return rc;
 }
 
@@ -418,6 +422,10 @@ struct is_ctx {
   float* logits_dump;
   int prompt_id, prompt_last;
   bool prefilled, started;
+  int M;                                    // co-resident group slots (NEXT-1)
+  std::vector<int> gprompt_id, gprompt_last;  // per group slot
+  std::vector<char> gprefilled, gstarted;
+  int32_t *prow_active, *prow_tok, *prow_pos, *prow_kvloc, *prow_len;  // prefill row tables
   cudaGraphExec_t graph;
   bool graph_ok;
   int32_t* d_prompt_copy;
@@ -459,6 +467,7 @@ static SchedArgs sched_args(is_ctx* c) {
   a.maxp = c->maxp;
   a.P = c->P;
   a.log_cap = c->log_cap;
+  a.M = c->M;
   a.st = c->st_dev;
   a.slot_uid = c->slot_uid;
   a.slot_count = c->slot_count;
@@ -523,7 +532,7 @@ static is_status launch_prefix_tc_n(is_ctx* c, const AttnArgs& aa, int l, cudaSt
   const int kv_row_base = l * 2 * c->sh.n_kv_heads * c->pcap;
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute at[1];
-  cfg.gridDim = dim3(c->sh.n_kv_heads * nt);
+  cfg.gridDim = dim3(c->M * c->sh.n_kv_heads * nt);
   cfg.blockDim = dim3(128);
   cfg.dynamicSmemBytes = SM::v;
   cfg.stream = st;
@@ -536,12 +545,16 @@ static is_status launch_prefix_tc_n(is_ctx* c, const AttnArgs& aa, int l, cudaSt
   }
   AttnArgs a2 = aa;
   a2.dbg_ts = aa.dbg_ts ? aa.dbg_ts + (size_t)2 * 296 * 16 : nullptr;
+  a2.grp_rows = c->g;
+  a2.grp_kv_rows = c->sh.layers * 2 * c->sh.n_kv_heads * c->pcap;
   CK(cudaLaunchKernelEx(&cfg, kern, c->tm_prefix_kv, a2, kv_row_base));
   return IS_OK;
 }
+// MMA N of the tcgen05 prefix part: one group's live slots x Hq/Hkv query heads, padded to 16.
+static int prefix_cols(int g, int rep) { return (int)ceil_div64((int64_t)g * rep, 16) * 16; }
 template <int REP>
 static is_status launch_prefix_tc(is_ctx* c, const AttnArgs& aa, int l, cudaStream_t st) {
-  switch (c->rc * REP) {
+  switch (prefix_cols(c->g, REP)) {
     case 16: return launch_prefix_tc_n<REP, 16>(c, aa, l, st);
     case 32: return launch_prefix_tc_n<REP, 32>(c, aa, l, st);
     case 64: return launch_prefix_tc_n<REP, 64>(c, aa, l, st);
@@ -551,9 +564,16 @@ static is_status launch_prefix_tc(is_ctx* c, const AttnArgs& aa, int l, cudaStre
 
 // One layer stack over `rows` rows starting at row 0 (decode: rows = rc, BN = c->BN;
 // prefill: rows = pcap processed in 64-row GEMM chunks).
-static is_status run_layers(is_ctx* c, int rows, bool prefill) {
+static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
   g_splitk_ws = c->splitk_ws;
   cudaStream_t st = c->st;
+  // prefill: the group slot's own prefix KV and separate row tables (decode rows stay intact)
+  int32_t* r_active = prefill ? c->prow_active : c->row_active;
+  int32_t* r_tok = prefill ? c->prow_tok : c->row_tok;
+  int32_t* r_pos = prefill ? c->prow_pos : c->row_pos;
+  int32_t* r_kvloc = prefill ? c->prow_kvloc : c->row_kvloc;
+  int32_t* r_len = prefill ? c->prow_len : c->row_len;
+  __nv_bfloat16* prefix_g = c->prefix + (size_t)grp * c->sh.layers * 2 * c->sh.n_kv_heads * c->pcap * kHD;
   const is_shape& s = c->sh;
   const int H = s.hidden, F = s.ffn, Hq = s.n_q_heads, Hkv = s.n_kv_heads;
   const int BN = prefill ? 64 : c->BN;
@@ -564,7 +584,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
 
   prof_mark(st, 0);
   CKS(launch_k(embed_kernel, dim3(rows), dim3(128), st, (const __nv_bfloat16*)c->embed,
-               (const int32_t*)c->row_tok, (const int32_t*)c->row_active, c->resid, H,
+               (const int32_t*)r_tok, (const int32_t*)r_active, c->resid, H,
                (!prefill && c->bnorm) ? c->ssqA : (float*)nullptr, c->max_rows));
   for (int l = 0; l < s.layers; ++l) {
     LayerW& w = c->L[l];
@@ -588,11 +608,11 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
       e.k_gain = w.k_norm;
       e.rope_cos = c->rope_cos;
       e.rope_sin = c->rope_sin;
-      e.row_active = c->row_active;
-      e.row_pos = c->row_pos;
-      e.row_kvloc = c->row_kvloc;
+      e.row_active = r_active;
+      e.row_pos = r_pos;
+      e.row_kvloc = r_kvloc;
       e.q_out = c->q;
-      e.kv = prefill ? c->prefix + l * prefix_layer : c->pool + l * pool_layer;
+      e.kv = prefill ? prefix_g + l * prefix_layer : c->pool + l * pool_layer;
       e.Hq = Hq;
       e.Hkv = Hkv;
       e.pt = c->pt;
@@ -612,15 +632,15 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill) {
     prof_mark(st, 1);
     AttnArgs aa{};
     aa.q = c->q;
-    aa.kpre = c->prefix + l * prefix_layer;
+    aa.kpre = prefix_g + l * prefix_layer;
     aa.vpre = aa.kpre + (size_t)Hkv * c->pcap * kHD;
     aa.pool = c->pool + l * pool_layer;
-    aa.row_active = c->row_active;
-    aa.row_len = c->row_len;
+    aa.row_active = r_active;
+    aa.row_len = r_len;
     aa.part_o = c->part_o;
     aa.part_ml = c->part_ml;
     aa.items = c->attn_items;
-    aa.n_items = c->st_dev + ST_ATTN_ITEMS;
+    aa.n_items = c->st_dev + (size_t)c->M * ST_COUNT + ST_ATTN_ITEMS;
     aa.dbg_ts = nullptr;
     if (g_tl && l < 4) aa.dbg_ts = g_tl + (size_t)(400 + 4 * l) * 296 * 16;  // attn: 2x296 CTAs, prefix_tc after
     aa.out = c->attn;
@@ -785,6 +805,7 @@ static is_status mk_launch(is_ctx* c, cudaStream_t st) {
 // Does the persistent decode kernel support this context?  (Hq/Hkv <= 4, <= 64
 // attention partials per row, smem for at least 4 weight stages.)
 static bool mk_supported(const is_ctx* c) {
+  if (c->M != 1) return false;
   const int REP = c->sh.n_q_heads / c->sh.n_kv_heads;
   if (REP != 1 && REP != 2 && REP != 4) return false;
   const int nc_pre = (int)ceil_div64(c->pcap, kMkPC);
@@ -1042,9 +1063,9 @@ static is_status enqueue_step(is_ctx* c) {
   g_splitk_ws = c->splitk_ws;
   CKS(launch_gemm<EPI_SAMPLE>(c->BN, c->tm_embed, c->tm_xn_dec, a, st));
   prof_mark(st, 7);
-  CKS(launch_k(sched_kernel, dim3(1), dim3(kSchedThreads), st, sched_args(c), 1));
+  CKS(launch_k(sched_kernel, dim3(1), dim3(kSchedThreads), st, sched_args(c), 1, (1 << c->M) - 1));
   prof_mark(st, 8);
-  CK(cudaMemcpyAsync(c->st_host, c->st_dev, sizeof(long long) * ST_COUNT, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(c->st_host, c->st_dev, sizeof(long long) * ST_COUNT * (c->M + 1), cudaMemcpyDeviceToHost, st));
   return IS_OK;
 }
 
@@ -1109,6 +1130,11 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->sh = s;
   c->G = cfg->G;
   c->g = eff_g(cfg);
+  c->M = n_groups(cfg);
+  c->gprompt_id.assign(c->M, 0);
+  c->gprompt_last.assign(c->M, 0);
+  c->gprefilled.assign(c->M, 0);
+  c->gstarted.assign(c->M, 0);
   c->N = c->G / c->g;
   c->rc = row_cap_of(cfg);
   if (c->rc < c->g || c->rc > 64) {
@@ -1135,12 +1161,13 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   } else {
     c->num_pages = (int)((resv - c->prefix_bytes) / c->page_bytes);
   }
+  c->num_pages *= c->M;  // the budget is per group; the pool is shared by the co-resident groups
   c->log_cap = c->G * c->max_new + c->N * cfg->prefix_k + 8;
   c->max_rows = std::max(c->rc, (int)ceil_div64(c->pcap, 64) * 64);
   c->max_pos = c->P + c->max_new + 1;
   c->nc_pre = (int)ceil_div64(c->pcap, kPC);  // prefill (CUDA-core causal prefix units)
   {
-    const int N = c->rc * (s.n_q_heads / s.n_kv_heads);
+    const int N = prefix_cols(c->g, s.n_q_heads / s.n_kv_heads);
     c->tc_prefix = (N == 16 || N == 32 || N == 64) && !getenv("IS_NO_TC_PREFIX");
     c->nc_pre_dec = c->tc_prefix ? (int)ceil_div64(c->pcap, 128) : c->nc_pre;
   }
@@ -1214,8 +1241,8 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   CKS(make_tmap(&c->tm_embed, c->embed, V, H, kBM));
   CK(cudaDeviceSynchronize());
   // ---- KV
-  c->prefix = (__nv_bfloat16*)A((size_t)s.layers * 2 * Hkv * c->pcap * 128 * 2);
-  if (err == IS_OK) CKS(make_tmap(&c->tm_prefix_kv, c->prefix, (int64_t)s.layers * 2 * Hkv * c->pcap, 128, 128));
+  c->prefix = (__nv_bfloat16*)A((size_t)c->M * s.layers * 2 * Hkv * c->pcap * 128 * 2);
+  if (err == IS_OK) CKS(make_tmap(&c->tm_prefix_kv, c->prefix, (int64_t)c->M * s.layers * 2 * Hkv * c->pcap, 128, 128));
   c->pool = (__nv_bfloat16*)A((size_t)s.layers * c->num_pages * (size_t)c->page_bytes / s.layers);
   // ---- activations
   const int R = c->max_rows;
@@ -1236,27 +1263,40 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   for (int32_t** p : {&c->row_active, &c->row_uid, &c->row_lid, &c->row_t, &c->row_tok, &c->row_pos,
                       &c->row_kvloc, &c->row_len})
     *p = (int32_t*)A((size_t)R * 4);
+  for (int32_t** p : {&c->prow_active, &c->prow_tok, &c->prow_pos, &c->prow_kvloc, &c->prow_len})
+    *p = (int32_t*)A((size_t)R * 4);
   c->keys = (unsigned long long*)A((size_t)R * 8);
   c->last_tok = (int32_t*)A((size_t)R * 4);
   c->last_fin = (uint8_t*)A((size_t)R);
-  c->st_dev = (long long*)A(sizeof(long long) * ST_COUNT);
-  c->slot_uid = (int32_t*)A(c->g * 4);
-  c->slot_count = (int32_t*)A(c->g * 4);
-  c->tpos = (int32_t*)A(c->G * 4);
-  c->true_len = (int32_t*)A(c->G * 4);
-  c->queue = (int32_t*)A(c->G * 4);
-  c->main_init = (int32_t*)A(c->g * 4);
-  c->main_queue = (int32_t*)A(c->G * 4);
+  const int M = c->M;
+  c->st_dev = (long long*)A(sizeof(long long) * ST_COUNT * (M + 1));
+  c->slot_uid = (int32_t*)A((size_t)M * c->g * 4);
+  c->slot_count = (int32_t*)A((size_t)M * c->g * 4);
+  c->tpos = (int32_t*)A((size_t)M * c->G * 4);
+  c->true_len = (int32_t*)A((size_t)M * c->G * 4);
+  c->queue = (int32_t*)A((size_t)M * c->G * 4);
+  c->main_init = (int32_t*)A((size_t)M * c->g * 4);
+  c->main_queue = (int32_t*)A((size_t)M * c->G * 4);
   c->free_stack = (int32_t*)A((size_t)std::max(c->num_pages, 1) * 4);
-  c->pagetab = (int32_t*)A((size_t)c->G * c->maxp * 4);
-  c->npages = (int32_t*)A(c->G * 4);
-  c->tokens = (int32_t*)A((size_t)c->G * c->max_new * 4);
-  c->log_slot = (int32_t*)A((size_t)c->log_cap * c->g * 4);
-  c->log_live = (int32_t*)A((size_t)c->log_cap * 4);
+  c->pagetab = (int32_t*)A((size_t)M * c->G * c->maxp * 4);
+  c->npages = (int32_t*)A((size_t)M * c->G * 4);
+  c->tokens = (int32_t*)A((size_t)M * c->G * c->max_new * 4);
+  c->log_slot = (int32_t*)A((size_t)M * c->log_cap * c->g * 4);
+  c->log_live = (int32_t*)A((size_t)M * c->log_cap * 4);
   c->d_prompt_copy = (int32_t*)A((size_t)c->P * 4);
   if (err != IS_OK) return err;
-  CK(cudaMallocHost(&c->st_host, sizeof(long long) * ST_COUNT));
-  memset(c->st_host, 0, sizeof(long long) * ST_COUNT);
+  CK(cudaMallocHost(&c->st_host, sizeof(long long) * ST_COUNT * (M + 1)));
+  memset(c->st_host, 0, sizeof(long long) * ST_COUNT * (M + 1));
+  {
+    // shared page pool: LIFO free stack (pop order 0, 1, 2, ...), every slot idle
+    std::vector<int32_t> fs(std::max(c->num_pages, 1));
+    for (int i = 0; i < c->num_pages; ++i) fs[i] = c->num_pages - 1 - i;
+    CK(cudaMemcpy(c->free_stack, fs.data(), fs.size() * 4, cudaMemcpyHostToDevice));
+    std::vector<long long> st((size_t)ST_COUNT * (M + 1), 0);
+    st[(size_t)M * ST_COUNT + ST_FREE_TOP] = c->num_pages;
+    CK(cudaMemcpy(c->st_dev, st.data(), st.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemset(c->slot_uid, 0xFF, (size_t)M * c->g * 4));
+  }
   // RoPE table (rotate-half, theta^(-2i/d)), fp64 -> fp32
   {
     std::vector<float> cs((size_t)c->max_pos * 64), sn((size_t)c->max_pos * 64);
@@ -1319,7 +1359,8 @@ extern "C" void is_destroy(is_ctx* c) {
                   c->row_t, c->row_tok, c->row_pos, c->row_kvloc, c->row_len, c->keys, c->last_tok,
                   c->last_fin, c->st_dev, c->slot_uid, c->slot_count, c->tpos, c->true_len, c->queue,
                   c->main_init, c->main_queue, c->free_stack, c->pagetab, c->npages, c->tokens, c->log_slot,
-                  c->log_live, c->d_prompt_copy};
+                  c->log_live, c->d_prompt_copy, c->prow_active, c->prow_tok, c->prow_pos, c->prow_kvloc,
+                  c->prow_len};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (int i = 0; i < c->mk_nbufs; ++i) cudaFree(c->mk_bufs[i]);
@@ -1338,27 +1379,44 @@ extern "C" void is_destroy(is_ctx* c) {
   delete c;
 }
 
-extern "C" is_status is_prefill(is_ctx* c, const int32_t* d_prompt, int32_t prompt_id) {
+extern "C" is_status is_prefill_slot(is_ctx* c, int32_t slot, const int32_t* d_prompt, int32_t prompt_id) {
   if (!c || !d_prompt) return fail(IS_ERR_CONFIG, "null argument");
+  if (slot < 0 || slot >= c->M) return fail(IS_ERR_CONFIG, "group slot %d out of range [0, %d)", slot, c->M);
+  if (c->gstarted[slot] && c->st_host[(size_t)slot * ST_COUNT + ST_DONE] < c->G) {
+    // the slot's group is still decoding: wait for the stream, then look again
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaMemcpy(c->st_host, c->st_dev, sizeof(long long) * ST_COUNT * (c->M + 1), cudaMemcpyDeviceToHost));
+  }
   StreamGuard guard(c, c->user);
-  c->prompt_id = prompt_id;
   CK(cudaMemcpyAsync(c->d_prompt_copy, d_prompt, (size_t)c->P * 4, cudaMemcpyDeviceToDevice, c->st));
   int32_t last = 0;
   CK(cudaMemcpyAsync(&last, d_prompt + c->P - 1, 4, cudaMemcpyDeviceToHost, c->st));
   CKS(launch_k(prefill_rows_kernel, dim3((c->pcap + 127) / 128), dim3(128), c->st, (const int32_t*)c->d_prompt_copy,
-               c->pcap, c->row_active, c->row_tok, c->row_pos, c->row_kvloc));
-  CKS(run_layers(c, c->pcap, true));
+               c->pcap, c->prow_active, c->prow_tok, c->prow_pos, c->prow_kvloc));
+  CKS(run_layers(c, c->pcap, true, slot));
   CK(cudaStreamSynchronize(c->st));
   if (last < 0 || last >= c->sh.vocab) return fail(IS_ERR_DATA, "prompt token %d out of range", last);
-  c->prompt_last = last;
-  c->prefilled = true;
-  c->started = false;
+  c->gprompt_id[slot] = prompt_id;
+  c->gprompt_last[slot] = last;
+  c->gprefilled[slot] = 1;
+  c->gstarted[slot] = 0;
+  if (slot == 0) {
+    c->prompt_id = prompt_id;
+    c->prompt_last = last;
+    c->prefilled = true;
+    c->started = false;
+  }
   return IS_OK;
 }
 
-extern "C" is_status is_start_group(is_ctx* c, const int32_t* true_len, const int32_t* pred) {
+extern "C" is_status is_prefill(is_ctx* c, const int32_t* d_prompt, int32_t prompt_id) {
+  return is_prefill_slot(c, 0, d_prompt, prompt_id);
+}
+
+extern "C" is_status is_start_group_slot(is_ctx* c, int32_t m, const int32_t* true_len, const int32_t* pred) {
   if (!c || !true_len) return fail(IS_ERR_CONFIG, "null argument");
-  if (!c->prefilled) return fail(IS_ERR_STATE, "is_start_group before is_prefill");
+  if (m < 0 || m >= c->M) return fail(IS_ERR_CONFIG, "group slot %d out of range [0, %d)", m, c->M);
+  if (!c->gprefilled[m]) return fail(IS_ERR_STATE, "is_start_group before is_prefill (slot %d)", m);
   StreamGuard guard(c, c->user);
   const int G = c->G, g = c->g;
   for (int i = 0; i < G; ++i)
@@ -1383,7 +1441,9 @@ extern "C" is_status is_start_group(is_ctx* c, const int32_t* true_len, const in
   po.init_slots = init.data();
   po.refill_queue = queue.data();
   CKS(is_plan(&c->cfg, pred_eff.data(), k > 0 ? fin.data() : nullptr, &po));
-  // device state
+  // pages a previous (possibly abandoned) group of this slot still holds go back to the pool
+  CKS(launch_k(reclaim_group_kernel, dim3(1), dim3(32), c->st, sched_args(c), (int)m));
+  // per-group device state (block m of st; the global block M is left alone)
   std::vector<long long> st(ST_COUNT, 0);
   std::vector<int32_t> slots(g, -1), q0(G, 0);
   if (k > 0) {  // prefix phase: barriered rounds in trace order, stop at k (R22)
@@ -1408,35 +1468,39 @@ extern "C" is_status is_start_group(is_ctx* c, const int32_t* true_len, const in
     for (int i = 0; i < po.queue_len; ++i) q0[i] = queue[i];
     st[ST_QLEN] = po.queue_len;
   }
-  st[ST_FREE_TOP] = c->num_pages;
-  st[ST_PROMPT_ID] = c->prompt_id;
-  st[ST_PROMPT_LAST] = c->prompt_last;
-  std::vector<int32_t> fs(std::max(c->num_pages, 1));
-  for (int i = 0; i < c->num_pages; ++i) fs[i] = c->num_pages - 1 - i;  // pop order 0, 1, 2, ...
-  CK(cudaMemcpyAsync(c->st_dev, st.data(), st.size() * 8, cudaMemcpyHostToDevice, c->st));
-  CK(cudaMemcpyAsync(c->slot_uid, slots.data(), g * 4, cudaMemcpyHostToDevice, c->st));
-  CK(cudaMemsetAsync(c->slot_count, 0, g * 4, c->st));
-  CK(cudaMemsetAsync(c->tpos, 0, G * 4, c->st));
-  CK(cudaMemcpyAsync(c->true_len, true_len, G * 4, cudaMemcpyHostToDevice, c->st));
-  CK(cudaMemcpyAsync(c->queue, q0.data(), G * 4, cudaMemcpyHostToDevice, c->st));
-  CK(cudaMemcpyAsync(c->main_init, init.data(), g * 4, cudaMemcpyHostToDevice, c->st));
-  CK(cudaMemcpyAsync(c->main_queue, queue.data(), G * 4, cudaMemcpyHostToDevice, c->st));
-  CK(cudaMemcpyAsync(c->free_stack, fs.data(), fs.size() * 4, cudaMemcpyHostToDevice, c->st));
-  CK(cudaMemsetAsync(c->npages, 0, G * 4, c->st));
-  CK(cudaMemsetAsync(c->tokens, 0xFF, (size_t)G * c->max_new * 4, c->st));
-  CK(cudaMemsetAsync(c->log_slot, 0xFF, (size_t)c->log_cap * g * 4, c->st));
-  CK(cudaMemsetAsync(c->log_live, 0, (size_t)c->log_cap * 4, c->st));
-  CKS(launch_k(sched_kernel, dim3(1), dim3(kSchedThreads), c->st, sched_args(c), 0));
-  CK(cudaMemcpyAsync(c->st_host, c->st_dev, sizeof(long long) * ST_COUNT, cudaMemcpyDeviceToHost, c->st));
+  st[ST_PROMPT_ID] = c->gprompt_id[m];
+  st[ST_PROMPT_LAST] = c->gprompt_last[m];
+  const size_t oG = (size_t)m * G, og = (size_t)m * g;
+  CK(cudaMemcpyAsync(c->st_dev + (size_t)m * ST_COUNT, st.data(), st.size() * 8, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->slot_uid + og, slots.data(), g * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemsetAsync(c->slot_count + og, 0, g * 4, c->st));
+  CK(cudaMemsetAsync(c->tpos + oG, 0, G * 4, c->st));
+  CK(cudaMemcpyAsync(c->true_len + oG, true_len, G * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->queue + oG, q0.data(), G * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->main_init + og, init.data(), g * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->main_queue + oG, queue.data(), G * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemsetAsync(c->npages + oG, 0, G * 4, c->st));
+  CK(cudaMemsetAsync(c->tokens + oG * c->max_new, 0xFF, (size_t)G * c->max_new * 4, c->st));
+  CK(cudaMemsetAsync(c->log_slot + (size_t)m * c->log_cap * g, 0xFF, (size_t)c->log_cap * g * 4, c->st));
+  CK(cudaMemsetAsync(c->log_live + (size_t)m * c->log_cap, 0, (size_t)c->log_cap * 4, c->st));
+  // rows of the next step: allocate / log for this group only (the others are mid-step)
+  CKS(launch_k(sched_kernel, dim3(1), dim3(kSchedThreads), c->st, sched_args(c), 0, 1 << m));
+  CK(cudaMemcpyAsync(c->st_host, c->st_dev, sizeof(long long) * ST_COUNT * (c->M + 1), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   if (!c->graph_ok) CKS(build_graph(c));
-  c->started = true;
+  c->gstarted[m] = 1;
+  if (m == 0) c->started = true;
   return IS_OK;
+}
+
+extern "C" is_status is_start_group(is_ctx* c, const int32_t* true_len, const int32_t* pred) {
+  return is_start_group_slot(c, 0, true_len, pred);
 }
 
 extern "C" is_status is_decode_step(is_ctx* c, int32_t* d_next, uint8_t* d_fin) {
   if (!c) return fail(IS_ERR_CONFIG, "null argument");
-  if (!c->started) return fail(IS_ERR_STATE, "is_decode_step before is_start_group");
+  if (!c->started && std::find(c->gstarted.begin(), c->gstarted.end(), 1) == c->gstarted.end())
+    return fail(IS_ERR_STATE, "is_decode_step before is_start_group");
   StreamGuard guard(c, c->user);
   if (getenv("IS_NO_GRAPH")) CKS(enqueue_step(c));
   else CK(cudaGraphLaunch(c->graph, c->st));
@@ -1447,9 +1511,10 @@ extern "C" is_status is_decode_step(is_ctx* c, int32_t* d_next, uint8_t* d_fin) 
 
 extern "C" is_status is_refill(is_ctx* c, uint8_t* d_fin, int32_t* d_new_uid) {
   if (!c) return fail(IS_ERR_CONFIG, "null argument");
-  if (!c->started) return fail(IS_ERR_STATE, "is_refill before is_start_group");
+  if (!c->started && std::find(c->gstarted.begin(), c->gstarted.end(), 1) == c->gstarted.end())
+    return fail(IS_ERR_STATE, "is_refill before is_start_group");
   StreamGuard guard(c, c->user);
-  CKS(launch_k(sched_kernel, dim3(1), dim3(kSchedThreads), c->st, sched_args(c), 1));
+  CKS(launch_k(sched_kernel, dim3(1), dim3(kSchedThreads), c->st, sched_args(c), 1, (1 << c->M) - 1));
   if (d_fin) CK(cudaMemcpyAsync(d_fin, c->last_fin, c->rc, cudaMemcpyDeviceToDevice, c->st));
   if (d_new_uid) {
     CK(cudaMemsetAsync(d_new_uid, 0xFF, c->rc * 4, c->st));
@@ -1458,20 +1523,31 @@ extern "C" is_status is_refill(is_ctx* c, uint8_t* d_fin, int32_t* d_new_uid) {
   return IS_OK;
 }
 
-extern "C" is_status is_run_group(is_ctx* c, int32_t max_steps, int32_t* h_steps) {
-  if (!c) return fail(IS_ERR_CONFIG, "null argument");
-  if (!c->started) return fail(IS_ERR_STATE, "is_run_group before is_start_group");
-  StreamGuard guard(c, c->user);
+// Decode steps until a started group completes (any = true) or until every
+// started group has completed (any = false); bounded host run-ahead, no per-step
+// synchronisation.  *h_done_mask: bit m set for every started group that is done.
+static is_status run_until(is_ctx* c, int32_t max_steps, bool any, int32_t* h_done_mask) {
   constexpr int D = 3;  // bounded host run-ahead
   cudaEvent_t ev[D];
   for (int i = 0; i < D; ++i) CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
   const bool nograph = getenv("IS_NO_GRAPH") != nullptr;
+  auto done_mask = [&](const volatile long long* h) {
+    int mask = 0, running = 0;
+    for (int m = 0; m < c->M; ++m) {
+      if (!c->gstarted[m]) continue;
+      if (h[(size_t)m * ST_COUNT + ST_DONE] >= c->G) mask |= 1 << m;
+      else running |= 1 << m;
+    }
+    return std::make_pair(mask, running);
+  };
+  // groups already complete when called do not end an `any` run
+  const int done0 = done_mask(c->st_host).first;
   is_status rs = IS_OK;
   for (int i = 0; i < max_steps; ++i) {
     if (i >= D) {
       cudaEventSynchronize(ev[i % D]);
-      const volatile long long* h = c->st_host;
-      if (h[ST_DONE] >= c->G) break;
+      const auto dm = done_mask(c->st_host);
+      if (dm.second == 0 || (any && (dm.first & ~done0))) break;
     }
     if (nograph) rs = enqueue_step(c);
     else if (cudaGraphLaunch(c->graph, c->st) != cudaSuccess) rs = fail(IS_ERR_CUDA, "graph launch failed");
@@ -1481,22 +1557,43 @@ extern "C" is_status is_run_group(is_ctx* c, int32_t max_steps, int32_t* h_steps
   CK(cudaStreamSynchronize(c->st));
   for (int i = 0; i < D; ++i) cudaEventDestroy(ev[i]);
   if (rs != IS_OK) return rs;
-  if (h_steps) *h_steps = (int32_t)c->st_host[ST_STEP];
-  if (c->st_host[ST_DONE] < c->G) return fail(IS_ERR_CAPACITY, "group not finished after %d steps", max_steps);
+  if (h_done_mask) *h_done_mask = done_mask(c->st_host).first;
   return IS_OK;
 }
 
-extern "C" is_status is_query(is_ctx* c, is_stats* o) {
+extern "C" is_status is_run_group(is_ctx* c, int32_t max_steps, int32_t* h_steps) {
+  if (!c) return fail(IS_ERR_CONFIG, "null argument");
+  if (!c->gstarted[0]) return fail(IS_ERR_STATE, "is_run_group before is_start_group");
+  StreamGuard guard(c, c->user);
+  int32_t mask = 0;
+  CKS(run_until(c, max_steps, false, &mask));
+  if (h_steps) *h_steps = (int32_t)c->st_host[ST_STEP];
+  if (!(mask & 1)) return fail(IS_ERR_CAPACITY, "group not finished after %d steps", max_steps);
+  return IS_OK;
+}
+
+extern "C" is_status is_run_until_any_done(is_ctx* c, int32_t max_steps, int32_t* h_done_mask, int64_t* h_global_steps) {
+  if (!c) return fail(IS_ERR_CONFIG, "null argument");
+  StreamGuard guard(c, c->user);
+  CKS(run_until(c, max_steps, true, h_done_mask));
+  if (h_global_steps) *h_global_steps = c->st_host[(size_t)c->M * ST_COUNT + ST_GSTEP];
+  return IS_OK;
+}
+
+extern "C" is_status is_query_slot(is_ctx* c, int32_t m, is_stats* o) {
   if (!c || !o) return fail(IS_ERR_CONFIG, "null argument");
+  if (m < 0 || m >= c->M) return fail(IS_ERR_CONFIG, "group slot %d out of range [0, %d)", m, c->M);
   CK(cudaStreamSynchronize(c->st));
-  long long st[ST_COUNT];
-  CK(cudaMemcpy(st, c->st_dev, sizeof st, cudaMemcpyDeviceToHost));
+  std::vector<long long> all((size_t)ST_COUNT * (c->M + 1));
+  CK(cudaMemcpy(all.data(), c->st_dev, all.size() * 8, cudaMemcpyDeviceToHost));
+  const long long* st = all.data() + (size_t)m * ST_COUNT;
+  const long long* g0 = all.data() + (size_t)c->M * ST_COUNT;
   o->steps = (int32_t)st[ST_STEP];
   o->prefix_steps = (int32_t)st[ST_PREFIX_STEPS];
   o->completed = (int32_t)st[ST_DONE];
   o->live_pages = (int32_t)st[ST_LIVE];
   o->peak_pages = (int32_t)st[ST_PEAK];
-  o->error = (int32_t)st[ST_ERROR];
+  o->error = (int32_t)g0[ST_ERROR];
   o->tokens_decoded = st[ST_TOKENS];
   o->page_bytes = c->page_bytes;
   o->prefix_bytes = c->prefix_bytes;
@@ -1513,47 +1610,66 @@ extern "C" is_status is_query(is_ctx* c, is_stats* o) {
     o->layer_kernel_ns = (int64_t)clk[0];
     o->layer_kernel_launches = (int64_t)clk[1];
   }
+  o->groups = c->M;
+  o->global_steps = g0[ST_GSTEP];
+  o->global_peak_kv_bytes = (int64_t)c->M * c->prefix_bytes + g0[ST_GPEAK] * c->page_bytes;
   return IS_OK;
 }
 
-extern "C" is_status is_copy_tokens(is_ctx* c, int32_t* dst, int32_t dev) {
+extern "C" is_status is_query(is_ctx* c, is_stats* o) { return is_query_slot(c, 0, o); }
+
+extern "C" is_status is_copy_tokens_slot(is_ctx* c, int32_t m, int32_t* dst, int32_t dev) {
   if (!c || !dst) return fail(IS_ERR_CONFIG, "null argument");
+  if (m < 0 || m >= c->M) return fail(IS_ERR_CONFIG, "group slot %d out of range [0, %d)", m, c->M);
   CK(cudaStreamSynchronize(c->st));
-  CK(cudaMemcpy(dst, c->tokens, (size_t)c->G * c->max_new * 4, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(dst, c->tokens + (size_t)m * c->G * c->max_new, (size_t)c->G * c->max_new * 4,
+                dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
   return IS_OK;
 }
+extern "C" is_status is_copy_tokens(is_ctx* c, int32_t* dst, int32_t dev) { return is_copy_tokens_slot(c, 0, dst, dev); }
 
-extern "C" is_status is_copy_schedule(is_ctx* c, int32_t* h_slots, int32_t* h_live, int32_t max_steps, int32_t* h_n) {
+extern "C" is_status is_copy_schedule_slot(is_ctx* c, int32_t m, int32_t* h_slots, int32_t* h_live, int32_t max_steps,
+                                           int32_t* h_n) {
   if (!c) return fail(IS_ERR_CONFIG, "null argument");
+  if (m < 0 || m >= c->M) return fail(IS_ERR_CONFIG, "group slot %d out of range [0, %d)", m, c->M);
   CK(cudaStreamSynchronize(c->st));
   long long st[ST_COUNT];
-  CK(cudaMemcpy(st, c->st_dev, sizeof st, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(st, c->st_dev + (size_t)m * ST_COUNT, sizeof st, cudaMemcpyDeviceToHost));
   const int n = (int)std::min<long long>(std::min<long long>(st[ST_STEP], c->log_cap), max_steps);
-  if (h_slots) CK(cudaMemcpy(h_slots, c->log_slot, (size_t)n * c->g * 4, cudaMemcpyDeviceToHost));
-  if (h_live) CK(cudaMemcpy(h_live, c->log_live, (size_t)n * 4, cudaMemcpyDeviceToHost));
+  if (h_slots) CK(cudaMemcpy(h_slots, c->log_slot + (size_t)m * c->log_cap * c->g, (size_t)n * c->g * 4, cudaMemcpyDeviceToHost));
+  if (h_live) CK(cudaMemcpy(h_live, c->log_live + (size_t)m * c->log_cap, (size_t)n * 4, cudaMemcpyDeviceToHost));
   if (h_n) *h_n = n;
   return IS_OK;
 }
+extern "C" is_status is_copy_schedule(is_ctx* c, int32_t* h_slots, int32_t* h_live, int32_t max_steps, int32_t* h_n) {
+  return is_copy_schedule_slot(c, 0, h_slots, h_live, max_steps, h_n);
+}
 
-extern "C" is_status is_group_results(is_ctx* c, float* d_reward, int32_t* d_len) {
+extern "C" is_status is_group_results_slot(is_ctx* c, int32_t m, float* d_reward, int32_t* d_len) {
   if (!c || !d_reward || !d_len) return fail(IS_ERR_CONFIG, "null argument");
+  if (m < 0 || m >= c->M) return fail(IS_ERR_CONFIG, "group slot %d out of range [0, %d)", m, c->M);
   StreamGuard guard(c, c->user);
-  results_kernel<<<(c->G + 127) / 128, 128, 0, c->st>>>(c->tokens, c->true_len, c->G, c->max_new, c->sh.vocab,
+  results_kernel<<<(c->G + 127) / 128, 128, 0, c->st>>>(c->tokens + (size_t)m * c->G * c->max_new,
+                                                      c->true_len + (size_t)m * c->G, c->G, c->max_new, c->sh.vocab,
                                                       d_reward, d_len);
   CK(cudaGetLastError());
   return IS_OK;
+}
+extern "C" is_status is_group_results(is_ctx* c, float* d_reward, int32_t* d_len) {
+  return is_group_results_slot(c, 0, d_reward, d_len);
 }
 
 extern "C" is_status is_set_logits_dump(is_ctx* c, float* d_logits) {
   if (!c) return fail(IS_ERR_CONFIG, "null argument");
   c->logits_dump = d_logits;
-  if (c->started) CKS(build_graph(c));
+  if (c->graph_ok) CKS(build_graph(c));
   return IS_OK;
 }
 
 extern "C" is_status is_profile_step(is_ctx* c, float* h_ms, int32_t* h_kind, int32_t cap, int32_t* h_n) {
   if (!c) return fail(IS_ERR_CONFIG, "null argument");
-  if (!c->started) return fail(IS_ERR_STATE, "is_profile_step before is_start_group");
+  if (std::find(c->gstarted.begin(), c->gstarted.end(), 1) == c->gstarted.end())
+    return fail(IS_ERR_STATE, "is_profile_step before is_start_group");
   StreamGuard guard(c, c->user);
   std::vector<cudaEvent_t> ev;
   std::vector<int> kind;

@@ -119,6 +119,8 @@ struct AttnArgs {
   int prefill;                // 1: rows are prompt positions, causal over the prefix, no suffix
   int tc_prefix;              // decode: shared prefix done by attn_prefix_tc_kernel (tcgen05)
   int* merge_cnt;             // decode: [rows][Hkv] suffix units done; the last one merges (reset by it)
+  int grp_rows;               // decode, tcgen05 prefix: rows per co-resident group (g); group m = rows m*g ..
+  int grp_kv_rows;            //   prefix-KV tensor-map rows per group (L * 2 * Hkv * pcap)
   float scale;                // 1/sqrt(128)
 };
 
@@ -548,7 +550,11 @@ __global__ void __launch_bounds__(128, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = (a.plen + 127) / 128;
-  const int h = blockIdx.x / nt, tile = blockIdx.x % nt;
+  // CTA = (group, kv head, 128-token prefix tile); the group's live rows are the N columns
+  const int grp = blockIdx.x / (a.Hkv * nt);
+  const int h = (blockIdx.x / nt) % a.Hkv, tile = blockIdx.x % nt;
+  const int row0 = grp * a.grp_rows;
+  kv_row_base += grp * a.grp_kv_rows;
   const int tok0 = tile * 128, ntok = min(128, a.plen - tok0);
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmKV);
@@ -579,14 +585,14 @@ __global__ void __launch_bounds__(128, 1)
   pdl_launch_dependents();    // the suffix kernel may start now (it does not touch our outputs)
   // Q rows n = r*REP + e (K-major, 128-byte swizzle, two 64-d atoms)
   if (threadIdx.x < N) {
-    const int r = threadIdx.x / REP;
-    colI[N + threadIdx.x] = (r < a.rows && a.row_active[r]) ? 1.f : 0.f;  // row live (read by the epilogue)
+    const int rl = threadIdx.x / REP, r = row0 + rl;
+    colI[N + threadIdx.x] = (rl < a.grp_rows && r < a.rows && a.row_active[r]) ? 1.f : 0.f;  // row live
   }
   for (int i = threadIdx.x; i < N * 16; i += 128) {
     const int n = i >> 4, c = i & 15;
-    const int r = n / REP, e = n % REP;
+    const int rl = n / REP, r = row0 + rl, e = n % REP;
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < a.rows && a.row_active[r])
+    if (rl < a.grp_rows && r < a.rows && a.row_active[r])
       v = *reinterpret_cast<const uint4*>(a.q + ((size_t)r * a.Hq + h * REP + e) * kHD + c * 8);
     *reinterpret_cast<uint4*>(Qsm + (c >> 3) * N * 128 + n * 128 + (((c & 7) ^ (n & 7)) << 4)) = v;
   }
@@ -703,7 +709,7 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   // ---- epilogue: lane = head dim d; normalise and write partial slot `tile`
   if (threadIdx.x < N) {
-    const int n = threadIdx.x, r = n / REP, e = n % REP;
+    const int n = threadIdx.x, r = row0 + n / REP, e = n % REP;
     const float L = Ssm[8 * 64 + n];
     colI[n] = 1.0f / L;
     const bool act = colI[N + n] != 0.f;
@@ -755,25 +761,31 @@ enum SchedState {
   ST_SUFFIX,       // sum over steps of the live rows' suffix lengths
   ST_PROMPT_ID,    // prompt of the current group (RNG uid base), set by is_start_group: device state,
   ST_PROMPT_LAST,  //   not a kernel parameter, because the decode step is a CUDA graph reused across prompts
+  ST_GLIVE,        // block 0 only: pages allocated by all groups (shared pool)
+  ST_GPEAK,        // block 0 only: max over steps of ST_GLIVE
+  ST_GSTEP,        // block 0 only: decode steps with >= 1 active slot in any group
   ST_COUNT
 };
+// st[] holds one block of ST_COUNT words per co-resident group (NEXT-1) plus a
+// global block M: the shared page pool (ST_FREE_TOP, ST_GLIVE, ST_GPEAK),
+// ST_ERROR, the attention work list length and ST_GSTEP.
 
 struct SchedArgs {
-  int G, g, row_cap, max_new, pt, maxp, P, log_cap;
-  long long* st;             // [ST_COUNT]
-  int32_t* slot_uid;         // [g]
-  int32_t* slot_count;       // [g]
-  int32_t* t;                // [G]
-  const int32_t* true_len;   // [G]
-  int32_t* queue;            // [G]
-  const int32_t* main_init;  // [g]
-  const int32_t* main_queue; // [G]
-  int32_t* free_stack;       // [num_pages]
-  int32_t* pagetab;          // [G][maxp]
-  int32_t* npages;           // [G]
-  int32_t* tokens;           // [G][max_new]
-  int32_t* log_slot;         // [log_cap][g]
-  int32_t* log_live;         // [log_cap]
+  int G, g, row_cap, max_new, pt, maxp, P, log_cap, M;  // M co-resident groups (rows m*g .. m*g+g-1)
+  long long* st;             // [M + 1][ST_COUNT] (block M: global)
+  int32_t* slot_uid;         // [M][g]
+  int32_t* slot_count;       // [M][g]
+  int32_t* t;                // [M][G]
+  const int32_t* true_len;   // [M][G]
+  int32_t* queue;            // [M][G]
+  const int32_t* main_init;  // [M][g]
+  const int32_t* main_queue; // [M][G]
+  int32_t* free_stack;       // [num_pages] (shared)
+  int32_t* pagetab;          // [M*G][maxp] (row_lid = m*G + uid)
+  int32_t* npages;           // [M][G]
+  int32_t* tokens;           // [M][G][max_new]
+  int32_t* log_slot;         // [M][log_cap][g]
+  int32_t* log_live;         // [M][log_cap] pages held by the group
   unsigned long long* keys;  // [row_cap] lm_head argmax keys
   int32_t* last_tok;         // [row_cap]
   uint8_t* last_fin;         // [row_cap]
@@ -794,97 +806,115 @@ struct SchedArgs {
 // on thread 0; the per-row preparation of the next step and its attention work
 // list are independent per row and run one thread per row.
 constexpr int kSchedThreads = 128;
-__global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int consume) {
+__global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int consume, int prep_mask) {
   pdl_launch_dependents();  // let the next kernel launch and prefetch now; it waits for our completion itself
   pdl_wait();
-  __shared__ int s_alloc_page[64];  // page allocated for row s this step, or -1
   __shared__ int s_cnt[65];         // suffix chunk counts -> exclusive prefix sums
   __shared__ int s_any, s_npre;
-  long long* st = a.st;
+  long long* st0 = a.st + (size_t)a.M * ST_COUNT;  // global block: shared pool, counters
   const int tid = threadIdx.x;
   if (tid == 0) {
-    if (consume) {
+    if (consume)
       for (int s = 0; s < a.row_cap; ++s) {
         a.last_tok[s] = -1;
         a.last_fin[s] = 0;
       }
-      for (int s = 0; s < a.g; ++s) {
-        const int uid = a.slot_uid[s];
-        if (uid < 0) continue;
-        const uint32_t tok = 0xFFFFFFFFu - (uint32_t)(a.keys[s] & 0xFFFFFFFFull);
-        a.tokens[(size_t)uid * a.max_new + a.t[uid]] = (int32_t)tok;
-        a.last_tok[s] = (int32_t)tok;
-        a.t[uid] += 1;
-        st[ST_TOKENS] += 1;
-      }
-      for (int s = 0; s < a.g; ++s) {  // ascending slot index
-        const int uid = a.slot_uid[s];
-        if (uid < 0) continue;
-        if (a.t[uid] == a.true_len[uid]) {
-          st[ST_DONE] += 1;
-          a.last_fin[s] = 1;
-          for (int i = 0; i < a.npages[uid]; ++i) a.free_stack[st[ST_FREE_TOP]++] = a.pagetab[(size_t)uid * a.maxp + i];
-          st[ST_LIVE] -= a.npages[uid];
-          a.npages[uid] = 0;
-        } else if (st[ST_STOPK] > 0 && a.t[uid] == st[ST_STOPK]) {
-          // park: keep pages (prefix reuse)
-        } else {
-          continue;
-        }
-        a.slot_uid[s] = -1;
-        a.slot_count[s] += 1;
-        if (!st[ST_BARRIER] && st[ST_QHEAD] < st[ST_QLEN] && (st[ST_QUOTA] == 0 || a.slot_count[s] < st[ST_QUOTA]))
-          a.slot_uid[s] = a.queue[st[ST_QHEAD]++];
-      }
-      bool idle = true;
-      for (int s = 0; s < a.g; ++s) idle = idle && a.slot_uid[s] < 0;
-      if (st[ST_BARRIER] && idle && st[ST_QHEAD] < st[ST_QLEN]) {
-        for (int s = 0; s < a.g && st[ST_QHEAD] < st[ST_QLEN]; ++s) a.slot_uid[s] = a.queue[st[ST_QHEAD]++];
-        idle = false;
-      }
-      if (st[ST_PHASE] == 0 && idle && st[ST_QHEAD] >= st[ST_QLEN] && st[ST_MAIN_PENDING]) {
-        // prefix phase over: install the Alg. 2 plan (init fill + static SJF queue)
-        for (int i = 0; i < st[ST_MAIN_QLEN]; ++i) a.queue[i] = a.main_queue[i];
-        st[ST_QLEN] = st[ST_MAIN_QLEN];
-        st[ST_QHEAD] = 0;
-        st[ST_BARRIER] = 0;
-        st[ST_QUOTA] = 0;
-        st[ST_STOPK] = 0;
-        st[ST_PHASE] = 1;
-        st[ST_MAIN_PENDING] = 0;
+    // groups in ascending index; within a group the paper's order (R18)
+    for (int m = 0; m < a.M; ++m) {
+      long long* st = a.st + (size_t)m * ST_COUNT;
+      int32_t* slot_uid = a.slot_uid + m * a.g;
+      int32_t* slot_count = a.slot_count + m * a.g;
+      int32_t* tt_ = a.t + (size_t)m * a.G;
+      const int32_t* true_len = a.true_len + (size_t)m * a.G;
+      int32_t* queue = a.queue + (size_t)m * a.G;
+      int32_t* npages = a.npages + (size_t)m * a.G;
+      int32_t* tokens = a.tokens + (size_t)m * a.G * a.max_new;
+      const int32_t* pagetab = a.pagetab + (size_t)m * a.G * a.maxp;
+      if (consume) {
         for (int s = 0; s < a.g; ++s) {
-          a.slot_count[s] = 0;
-          a.slot_uid[s] = s < st[ST_MAIN_NINIT] ? a.main_init[s] : -1;
+          const int uid = slot_uid[s];
+          if (uid < 0) continue;
+          const int row = m * a.g + s;
+          const uint32_t tok = 0xFFFFFFFFu - (uint32_t)(a.keys[row] & 0xFFFFFFFFull);
+          tokens[(size_t)uid * a.max_new + tt_[uid]] = (int32_t)tok;
+          a.last_tok[row] = (int32_t)tok;
+          tt_[uid] += 1;
+          st[ST_TOKENS] += 1;
+        }
+        for (int s = 0; s < a.g; ++s) {  // ascending slot index
+          const int uid = slot_uid[s];
+          if (uid < 0) continue;
+          if (tt_[uid] == true_len[uid]) {
+            st[ST_DONE] += 1;
+            a.last_fin[m * a.g + s] = 1;
+            for (int i = 0; i < npages[uid]; ++i) a.free_stack[st0[ST_FREE_TOP]++] = pagetab[(size_t)uid * a.maxp + i];
+            st[ST_LIVE] -= npages[uid];
+            st0[ST_GLIVE] -= npages[uid];
+            npages[uid] = 0;
+          } else if (st[ST_STOPK] > 0 && tt_[uid] == st[ST_STOPK]) {
+            // park: keep pages (prefix reuse)
+          } else {
+            continue;
+          }
+          slot_uid[s] = -1;
+          slot_count[s] += 1;
+          if (!st[ST_BARRIER] && st[ST_QHEAD] < st[ST_QLEN] && (st[ST_QUOTA] == 0 || slot_count[s] < st[ST_QUOTA]))
+            slot_uid[s] = queue[st[ST_QHEAD]++];
+        }
+        bool idle = true;
+        for (int s = 0; s < a.g; ++s) idle = idle && slot_uid[s] < 0;
+        if (st[ST_BARRIER] && idle && st[ST_QHEAD] < st[ST_QLEN]) {
+          for (int s = 0; s < a.g && st[ST_QHEAD] < st[ST_QLEN]; ++s) slot_uid[s] = queue[st[ST_QHEAD]++];
+          idle = false;
+        }
+        if (st[ST_PHASE] == 0 && idle && st[ST_QHEAD] >= st[ST_QLEN] && st[ST_MAIN_PENDING]) {
+          // prefix phase over: install the Alg. 2 plan (init fill + static SJF queue)
+          for (int i = 0; i < st[ST_MAIN_QLEN]; ++i) queue[i] = a.main_queue[(size_t)m * a.G + i];
+          st[ST_QLEN] = st[ST_MAIN_QLEN];
+          st[ST_QHEAD] = 0;
+          st[ST_BARRIER] = 0;
+          st[ST_QUOTA] = 0;
+          st[ST_STOPK] = 0;
+          st[ST_PHASE] = 1;
+          st[ST_MAIN_PENDING] = 0;
+          for (int s = 0; s < a.g; ++s) {
+            slot_count[s] = 0;
+            slot_uid[s] = s < st[ST_MAIN_NINIT] ? a.main_init[m * a.g + s] : -1;
+          }
+        }
+      }
+      // pages for rows crossing a page boundary, ascending slot order (LIFO shared stack);
+      // only for groups being prepared (all of them after a step; the new group at its start)
+      if ((prep_mask >> m) & 1) {
+        for (int s = 0; s < a.g; ++s) {
+          const int uid = slot_uid[s];
+          if (uid < 0) continue;
+          const int tt = tt_[uid];
+          if (tt % a.pt == 0) {
+            int page = 0;
+            if (st0[ST_FREE_TOP] > 0) page = a.free_stack[--st0[ST_FREE_TOP]];
+            else st0[ST_ERROR] = 1;  // budget violated: pool exhausted
+            a.pagetab[((size_t)m * a.G + uid) * a.maxp + tt / a.pt] = page;
+            npages[uid] += 1;
+            st[ST_LIVE] += 1;
+            st0[ST_GLIVE] += 1;
+          }
         }
       }
     }
-    // pages for rows crossing a page boundary, allocated in ascending slot order (LIFO stack)
     int any = 0;
-    for (int s = 0; s < a.row_cap; ++s) {
-      s_alloc_page[s] = -1;
-      const int uid = s < a.g ? a.slot_uid[s] : -1;
-      if (uid < 0) continue;
-      any = 1;
-      const int tt = a.t[uid];
-      if (tt % a.pt == 0) {
-        int page = 0;
-        if (st[ST_FREE_TOP] > 0) page = a.free_stack[--st[ST_FREE_TOP]];
-        else st[ST_ERROR] = 1;  // budget violated: pool exhausted
-        a.pagetab[(size_t)uid * a.maxp + tt / a.pt] = page;
-        a.npages[uid] += 1;
-        st[ST_LIVE] += 1;
-      }
-    }
+    for (int r = 0; r < a.M * a.g; ++r) any |= a.slot_uid[r] >= 0;
     s_any = any;
   }
   __syncthreads();
-  // ---- rows of the next step, one thread per row
+  // ---- rows of the next step, one thread per row (row s = group m, slot s - m*g)
   const bool any = s_any != 0;
   int nch = 0;
   if (tid < a.row_cap) {
     const int s = tid;
     a.keys[s] = 0ull;
-    const int uid = s < a.g ? a.slot_uid[s] : -1;
+    const int m = s / a.g;
+    const int uid = m < a.M ? a.slot_uid[s] : -1;
     if (uid < 0) {
       a.row_active[s] = 0;
       a.row_uid[s] = 0;
@@ -895,14 +925,16 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
       a.row_kvloc[s] = 0;
       a.row_len[s] = 0;
     } else {
-      const int tt = a.t[uid];
+      const long long* st = a.st + (size_t)m * ST_COUNT;
+      const int lid = m * a.G + uid;
+      const int tt = a.t[lid];
       a.row_active[s] = 1;
       a.row_uid[s] = (int)st[ST_PROMPT_ID] * a.G + uid;
-      a.row_lid[s] = uid;
+      a.row_lid[s] = lid;
       a.row_t[s] = tt;
-      a.row_tok[s] = tt == 0 ? (int)st[ST_PROMPT_LAST] : a.tokens[(size_t)uid * a.max_new + tt - 1];
+      a.row_tok[s] = tt == 0 ? (int)st[ST_PROMPT_LAST] : a.tokens[(size_t)lid * a.max_new + tt - 1];
       a.row_pos[s] = a.P - 1 + tt;
-      a.row_kvloc[s] = a.pagetab[(size_t)uid * a.maxp + tt / a.pt] * a.pt + tt % a.pt;
+      a.row_kvloc[s] = a.pagetab[(size_t)lid * a.maxp + tt / a.pt] * a.pt + tt % a.pt;
       a.row_len[s] = tt + 1;
       nch = (tt + 1 + a.chunk - 1) / a.chunk;
     }
@@ -930,21 +962,31 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
       acc += v;
     }
     s_cnt[a.row_cap] = acc;
-    st[ST_ATTN_ITEMS] = n + acc * a.Hkv;
-    st[ST_ATTN_PRE] = n;
-    long long suf = 0;
-    for (int s = 0; s < a.row_cap; ++s) suf += a.row_len[s];
-    st[ST_SUFFIX] += suf;
-    if (any) {
-      const long long step = st[ST_STEP];
-      if (step < a.log_cap) {
-        for (int s = 0; s < a.g; ++s) a.log_slot[step * a.g + s] = a.slot_uid[s];
-        a.log_live[step] = (int32_t)st[ST_LIVE];
+    st0[ST_ATTN_ITEMS] = n + acc * a.Hkv;
+    st0[ST_ATTN_PRE] = n;
+    for (int m = 0; m < a.M; ++m) {
+      if (!((prep_mask >> m) & 1)) continue;
+      long long* st = a.st + (size_t)m * ST_COUNT;
+      bool gany = false;
+      long long suf = 0;
+      for (int s = m * a.g; s < m * a.g + a.g; ++s) {
+        gany = gany || a.row_active[s];
+        suf += a.row_len[s];
       }
-      st[ST_STEP] = step + 1;
-      if (st[ST_PHASE] == 0) st[ST_PREFIX_STEPS] += 1;
-      if (st[ST_LIVE] > st[ST_PEAK]) st[ST_PEAK] = st[ST_LIVE];
+      st[ST_SUFFIX] += suf;
+      if (gany) {
+        const long long step = st[ST_STEP];
+        if (step < a.log_cap) {
+          for (int s = 0; s < a.g; ++s) a.log_slot[((size_t)m * a.log_cap + step) * a.g + s] = a.slot_uid[m * a.g + s];
+          a.log_live[(size_t)m * a.log_cap + step] = (int32_t)st[ST_LIVE];
+        }
+        st[ST_STEP] = step + 1;
+        if (st[ST_PHASE] == 0) st[ST_PREFIX_STEPS] += 1;
+        if (st[ST_LIVE] > st[ST_PEAK]) st[ST_PEAK] = st[ST_LIVE];
+      }
     }
+    if (any && consume) st0[ST_GSTEP] += 1;
+    if (st0[ST_GLIVE] > st0[ST_GPEAK]) st0[ST_GPEAK] = st0[ST_GLIVE];
   }
   __syncthreads();
   // ---- suffix items of row s: (chunk c, kv head h) with the chunk's page ids embedded
@@ -973,6 +1015,22 @@ __global__ void prefill_rows_kernel(const int32_t* __restrict__ prompt, int n, i
   row_tok[r] = prompt[r];
   row_pos[r] = r;
   row_kvloc[r] = r;
+}
+
+// Return every page still held by group m to the shared pool (a group slot is
+// being restarted; its previous group may have been abandoned mid-way).
+__global__ void reclaim_group_kernel(SchedArgs a, int m) {
+  if (threadIdx.x != 0) return;
+  long long* st0 = a.st + (size_t)a.M * ST_COUNT;
+  long long* st = a.st + (size_t)m * ST_COUNT;
+  for (int uid = 0; uid < a.G; ++uid) {
+    int32_t* np = a.npages + (size_t)m * a.G + uid;
+    for (int i = 0; i < *np; ++i) a.free_stack[st0[ST_FREE_TOP]++] = a.pagetab[((size_t)m * a.G + uid) * a.maxp + i];
+    st0[ST_GLIVE] -= *np;
+    *np = 0;
+  }
+  st[ST_LIVE] = 0;
+  for (int s = 0; s < a.g; ++s) a.slot_uid[m * a.g + s] = -1;
 }
 
 // Benchmark reward (R29) and length per sample.

@@ -1,8 +1,7 @@
 #!/bin/bash
 OUT=gpurun_out/${1:-det}
 mkdir -p $OUT
-timeout 600 python tools/modes_compare.py --config 3 --prompts 1 --modes infinite,infinite > $OUT/inf_inf.json 2>&1
-timeout 600 python tools/modes_compare.py --config 3 --prompts 1 --modes naive,infinite > $OUT/naive_inf.json 2>&1
-IS_SEPARATE_MERGE=1 timeout 600 python tools/modes_compare.py --config 3 --prompts 1 --modes naive,infinite > $OUT/naive_inf_sepmerge.json 2>&1
-IS_NO_TC_PREFIX=1 timeout 600 python tools/modes_compare.py --config 3 --prompts 1 --modes naive,infinite > $OUT/naive_inf_notc.json 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest.log 2>&1; echo "rc=$?" >> $OUT/pytest.log
+timeout 900 python tools/modes_compare.py --config 3 --prompts 2 > $OUT/modes_c3.json 2>&1
+timeout 900 python tools/modes_compare.py --config 2 --prompts 4 > $OUT/modes_c2.json 2>&1
 echo done > $OUT/DONE

@@ -15,7 +15,7 @@ ctx = _lib.Context(cfg, w)
 ctx.is_prefill(torch.as_tensor(gen_prompt(shape.vocab, P, 0), device="cuda"), 0)
 true = gen_trace("math", G, max_new, 1)
 ctx.is_start_group(true, predict_lengths(true, "noisy", 0.3, seed=1))
-for _ in range(20):
+for _ in range(int(os.environ.get("WARM", "20"))):
     ctx.is_decode_step()
 torch.cuda.synchronize()
 q0 = ctx.is_query()

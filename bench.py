@@ -314,6 +314,122 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_groups(args):
+    """NEXT-1: --groups M co-resident prompt groups share every decode step.
+    K + W prompts are pushed through M group slots (a finished slot is refilled with the
+    next prompt); the timed region covers the K timed prompts' rollouts end to end."""
+    import torch
+    from paper_2506_22950_b200 import _lib
+    from synth import SHAPES, gen_prompt, gen_trace, gen_weights, predict_lengths
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    C = CONFIGS[args.config]
+    shape = SHAPES[C["shape"]]
+    G, g, max_new, P, M = C["G"], C["g"], C["max_new"], C["P"], args.groups
+    kv_tok = 2 * shape.layers * shape.n_kv_heads * shape.head_dim * 2
+    budget = (P - 1) * kv_tok + g * math.ceil(max_new / 16) * 16 * kv_tok
+    if C["prefix_k"]:
+        budget = 1 << 30
+    w = gen_weights(shape, seed=SEED, device="cuda")
+    cfg = _lib.make_config(shape, G, g, max_new, P, mode="infinite", prefix_k=C["prefix_k"], page_tokens=16,
+                           kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED, max_groups=M)
+    ctx = _lib.Context(cfg, w)
+    del w
+    torch.cuda.empty_cache()
+
+    def workload(j):
+        pid = rank * 100000 + j  # global prompt id (RNG keyed by global uid)
+        prompt = gen_prompt(shape.vocab, P, pid, seed=SEED)
+        true = gen_trace(C["family"], G, max_new, SEED + pid)
+        pred = predict_lengths(true, "noisy", 0.3, seed=SEED + pid, prefix_k=C["prefix_k"])
+        return pid, torch.as_tensor(prompt, device="cuda"), true, pred
+
+    d_rew = torch.zeros(G, device="cuda")
+    d_len = torch.zeros(G, dtype=torch.int32, device="cuda")
+    all_len = torch.zeros(world * G, dtype=torch.int32, device="cuda")
+    all_rew = torch.zeros(world * G, device="cuda")
+
+    def pipeline(prompts):
+        """Push the prompts through the M slots; returns (tokens generated, global decode steps)."""
+        queue = list(prompts)
+        slot_of, tokens = {}, 0
+        for slot in range(min(M, len(queue))):
+            pid, dp, true, pred = queue.pop(0)
+            ctx.is_prefill(dp, pid, slot=slot)
+            ctx.is_start_group(true, pred, slot=slot)
+            slot_of[slot] = true
+        steps0 = None
+        steps = 0
+        while slot_of:
+            mask, steps = ctx.is_run_until_any_done()
+            for slot in list(slot_of):
+                if mask >> slot & 1:
+                    true = slot_of.pop(slot)
+                    tokens += int(np.sum(true))
+                    ctx.is_group_results(d_rew, d_len, slot=slot)
+                    if dist is not None:  # the one exchange: lengths + rewards for Eq. 2
+                        dist.all_gather_into_tensor(all_len, d_len)
+                        dist.all_gather_into_tensor(all_rew, d_rew)
+                    if queue:
+                        pid, dp, tr, pr = queue.pop(0)
+                        ctx.is_prefill(dp, pid, slot=slot)
+                        ctx.is_start_group(tr, pr, slot=slot)
+                        slot_of[slot] = tr
+        return tokens, steps
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    warm = [workload(j) for j in range(args.warmup)]
+    timed = [workload(args.warmup + j) for j in range(args.steps * M)]
+    pipeline(warm)
+    barrier()
+    s0 = ctx.is_query()["global_steps"]
+    clocks = ClockSampler(local)
+    clocks.start()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    tokens, steps = pipeline(timed)
+    e1.record(stream)
+    barrier()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    st = ctx.is_query()
+    t = torch.tensor([ms, float(tokens)], device="cuda", dtype=torch.float64)
+    if dist is not None:
+        tt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(tt, t)
+        ms_max = max(float(x[0]) for x in tt)
+        tok_all = sum(float(x[1]) for x in tt)
+    else:
+        ms_max, tok_all = ms, float(tokens)
+    if rank == 0:
+        dsteps = st["global_steps"] - s0
+        print(json.dumps({
+            "metric": METRIC, "value": round(tok_all / (ms_max * 1e-3), 1), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"config {args.config} x {M} co-resident groups (SURVEY §8f NEXT-1): {C['desc']}",
+                       "model": C["shape"] + " (random init)", "G": G, "g": g, "groups": M,
+                       "prompts_timed": len(timed), "kv_budget_bytes_per_group": budget,
+                       "step": f"{M} GRPO-group rollouts through {M} group slots",
+                       "parallelism": f"dp{world} (prompt-sharded)"},
+            "decode_steps": int(dsteps), "ms_per_decode_step": round(ms_max / max(dsteps, 1), 4),
+            "global_peak_kv_bytes": st["global_peak_kv_bytes"], "clocks": clk}))
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def _oracle_tokens_per_s(C, budget_s, step_seed=0):
     """The oracle as it stands: full-recompute decode of one sample, tokens until ~budget_s."""
     import torch
@@ -378,11 +494,15 @@ def main():
     ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--groups", type=int, default=1,
+                    help="co-resident prompt groups per GPU (SURVEY §8f NEXT-1); 1 = the paper's setting")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.groups > 1:
+        run_groups(args)
     else:
         run_ours(args)
 

@@ -323,8 +323,9 @@ static is_status launch_gemm(int BN, const CUtensorMap& tA, const CUtensorMap& t
 // takes more than half an SM, so the next kernel's CTAs (PDL) co-reside and
 // prefetch their weights while this one drains.
 static int choose_split(int num_tiles, int kb_total, int /*BN*/) {
-  if (num_tiles * 2 > g_num_sms) return 1;
-  int s = g_num_sms / num_tiles;
+  if (num_tiles > g_num_sms) return 1;
+  int s = std::max(1, g_num_sms / num_tiles);
+  if (s == 1) s = 2;  // 75..148 tiles: a 2-CTA cluster per tile keeps every SM streaming (gate/up: -5%/step)
   s = std::min(s, 8);
   s = std::min(s, kb_total);
   return std::max(s, 1);
@@ -332,10 +333,17 @@ static int choose_split(int num_tiles, int kb_total, int /*BN*/) {
 
 template <typename K, typename... Args>
 static is_status launch_k_smem(K kern, dim3 grid, dim3 block, int smem, cudaStream_t st, Args... args) {
-  static bool attr = false;
-  if (!attr) {
+  // (one attribute per kernel: kernels of the same signature share this instantiation)
+  static std::vector<std::pair<const void*, int>> attr;
+  bool found = false;
+  for (auto& pr : attr)
+    if (pr.first == (const void*)kern) {
+      found = pr.second >= smem;
+      if (!found) pr.second = smem;
+    }
+  if (!found) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
+    attr.push_back({(const void*)kern, smem});
   }
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute at[1];
@@ -1340,6 +1348,11 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
     c->bnorm = fits(c->split_qkv) && fits(c->split_gu) && getenv("IS_BNORM") != nullptr;  // measured slower (profiles/r01)
   }
   c->l2_prefetch = getenv("IS_L2_PREFETCH") ? atoi(getenv("IS_L2_PREFETCH")) : 0;
+  // per-GEMM split experiments (timing only)
+  if (const char* e = getenv("IS_SPLIT_QKV")) c->split_qkv = std::max(1, std::min(8, atoi(e)));
+  if (const char* e = getenv("IS_SPLIT_O")) c->split_o = std::max(1, std::min(8, atoi(e)));
+  if (const char* e = getenv("IS_SPLIT_GU")) c->split_gu = std::max(1, std::min(8, atoi(e)));
+  if (const char* e = getenv("IS_SPLIT_D")) c->split_d = std::max(1, std::min(8, atoi(e)));
   if (const char* e = getenv("IS_SPLIT_OVERRIDE")) {
     int v = atoi(e);
     if (v >= 1 && v <= 8) c->split_qkv = c->split_o = c->split_gu = c->split_d = v;

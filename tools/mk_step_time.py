@@ -10,11 +10,14 @@ shape = SHAPES[os.environ.get("SHAPE", "qwen3-1.7b")]
 impl = int(os.environ.get("IMPL", "0"))
 P, G, g, max_new = 256, 32, 8, 1024
 w = gen_weights(shape, seed=20261017, device="cuda")
-cfg = _lib.make_config(shape, G, g, max_new, P, mode="infinite", kv_budget_bytes=0, seed=20261017, decode_impl=impl)
+M = int(os.environ.get("GROUPS", "1"))
+cfg = _lib.make_config(shape, G, g, max_new, P, mode="infinite", kv_budget_bytes=0, seed=20261017, decode_impl=impl,
+                       max_groups=M)
 ctx = _lib.Context(cfg, w)
-ctx.is_prefill(torch.as_tensor(gen_prompt(shape.vocab, P, 0), device="cuda"), 0)
-true = gen_trace("math", G, max_new, 1)
-ctx.is_start_group(true, predict_lengths(true, "noisy", 0.3, seed=1))
+for m in range(M):
+    ctx.is_prefill(torch.as_tensor(gen_prompt(shape.vocab, P, m), device="cuda"), m, slot=m)
+    true = gen_trace("math", G, max_new, 1 + m)
+    ctx.is_start_group(true, predict_lengths(true, "noisy", 0.3, seed=1 + m), slot=m)
 for _ in range(int(os.environ.get("WARM", "20"))):
     ctx.is_decode_step()
 torch.cuda.synchronize()

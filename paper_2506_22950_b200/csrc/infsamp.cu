@@ -441,6 +441,7 @@ struct is_ctx {
   int split_qkv, split_o, split_gu, split_d;
   int l2_prefetch;
   int tc_prefix;       // decode prefix attention on tcgen05 (N = rc * Hq/Hkv in {16, 32, 64})
+  int sc;              // decode suffix chunk (tokens per attention work item)
   int nc_pre_dec;      // prefix partial slots in decode
   CUtensorMap tm_prefix_kv;
   unsigned long long* timeline;  // debug: [launch][148 CTAs][16] GEMM stamps (IS_TIMELINE)
@@ -505,7 +506,7 @@ static SchedArgs sched_args(is_ctx* c) {
   a.Hkv = c->sh.n_kv_heads;
   a.nc_pre = c->nc_pre_dec;
   a.nc_suf = c->nc_suf;
-  a.chunk = kSC;
+  a.chunk = c->sc;
   a.tc_prefix = c->tc_prefix;
   return a;
 }
@@ -662,6 +663,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
     aa.nc_suf = prefill ? 0 : c->nc_suf;
     aa.tc_prefix = prefill ? 0 : c->tc_prefix;
     aa.merge_cnt = (!prefill && c->tc_prefix && !getenv("IS_SEPARATE_MERGE")) ? c->merge_cnt : nullptr;
+    aa.sc = prefill ? kSC : c->sc;
     aa.NC = c->NC;
     aa.prefill = prefill ? 1 : 0;
     aa.scale = 1.0f / sqrtf((float)kHD);
@@ -670,7 +672,10 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
 #define IS_ATTN_LAUNCH(R)                                                                                      \
   do {                                                                                                         \
     if (do_attn && aa.tc_prefix) CKS(launch_prefix_tc<R>(c, aa, l, st));                                       \
-    if (do_attn) CKS(launch_k_smem(attn_kernel<R>, dim3(nblk), dim3(kAttnThreads), AttnSmem<R>::v, st, aa)); \
+    if (do_attn && aa.merge_cnt)                                                                               \
+      CKS(launch_k_smem(attn_suffix_warp_kernel<R>, dim3(3 * g_num_sms), dim3(kAttnThreads),                  \
+                        SuffixWarpSmem<R>::v, st, aa));                                                      \
+    else if (do_attn) CKS(launch_k_smem(attn_kernel<R>, dim3(nblk), dim3(kAttnThreads), AttnSmem<R>::v, st, aa)); \
     if (do_attn && getenv("IS_ATTN_TWICE")) {                                                                 \
       AttnArgs a2 = aa;                                                                                        \
       if (a2.dbg_ts) a2.dbg_ts += (size_t)2 * 296 * 16;                                                       \
@@ -1179,12 +1184,16 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
     c->tc_prefix = (N == 16 || N == 32 || N == 64) && !getenv("IS_NO_TC_PREFIX");
     c->nc_pre_dec = c->tc_prefix ? (int)ceil_div64(c->pcap, 128) : c->nc_pre;
   }
-  c->nc_suf = (int)ceil_div64(c->max_new, kSC);
+  // decode suffix chunk: 32-token warp units behind the tcgen05 prefix, else 64-token CTA units
+  c->sc = (c->tc_prefix && !getenv("IS_SEPARATE_MERGE")) ? kSCW : kSC;
+  c->nc_suf = (int)ceil_div64(c->max_new, c->sc);
   c->NC = c->nc_pre + c->nc_suf;
-  if (c->NC > 32 || s.n_q_heads / s.n_kv_heads > kMaxRep) {
-    const int nc = c->NC;
+  // partials one LSE merge combines: decode = prefix tiles + suffix chunks, prefill = prefix chunks
+  const int ndec = c->nc_pre_dec + c->nc_suf, nmax = c->sc == kSCW ? 64 : 32;
+  if (ndec > nmax || c->nc_pre > 32 || s.n_q_heads / s.n_kv_heads > kMaxRep) {
     delete c;
-    return fail(IS_ERR_CAPACITY, "prompt_len + max_new_tokens too long for the attention merge (%d chunks > 32)", nc);
+    return fail(IS_ERR_CAPACITY, "prompt_len + max_new_tokens too long for the attention merge (%d partials > %d)",
+                ndec, nmax);
   }
   c->prompt_id = 0;
 

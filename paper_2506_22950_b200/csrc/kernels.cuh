@@ -119,6 +119,7 @@ struct AttnArgs {
   int prefill;                // 1: rows are prompt positions, causal over the prefix, no suffix
   int tc_prefix;              // decode: shared prefix done by attn_prefix_tc_kernel (tcgen05)
   int* merge_cnt;             // decode: [rows][Hkv] suffix units done; the last one merges (reset by it)
+  int sc;                     // decode suffix chunk (tokens per work item): kSC, or kSCW for the warp kernel
   int grp_rows;               // decode, tcgen05 prefix: rows per co-resident group (g); group m = rows m*g ..
   int grp_kv_rows;            //   prefix-KV tensor-map rows per group (L * 2 * Hkv * pcap)
   float scale;                // 1/sqrt(128)
@@ -243,35 +244,40 @@ struct AttnSmem {
 template <int REP>
 __device__ __forceinline__ void attn_merge_one(const AttnArgs& a, int r, int h, int j, int lane) {
   const int npre = a.nc_pre;
-  const int nsuf = (a.row_len[r] + kSC - 1) / kSC;
-  const int n = npre + nsuf;
-  const int my_slot = lane < npre ? lane : a.nc_pre + (lane - npre);
+  const int nsuf = (a.row_len[r] + a.sc - 1) / a.sc;
+  const int n = npre + nsuf;  // <= 64
   const int qh = h * REP + j;
   const size_t base = ((size_t)r * a.Hq + qh) * a.NC;
-  float mi = -INFINITY, li = 0.f;
+  // partial i lives in slot i (prefix) or nc_pre + (i - npre) (suffix): the same index
+  float m0 = -INFINITY, l0 = 0.f, m1 = -INFINITY, l1 = 0.f;
   if (lane < n) {
-    const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (base + my_slot) * 2));
-    mi = ml.x;
-    li = ml.y;
+    const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (base + lane) * 2));
+    m0 = ml.x;
+    l0 = ml.y;
   }
-  const float M = warp_max(mi);
-  const float wi = (lane < n && mi != -INFINITY) ? expf(mi - M) * li : 0.f;
-  const float den = warp_sum(wi);
+  if (lane + 32 < n) {
+    const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (base + lane + 32) * 2));
+    m1 = ml.x;
+    l1 = ml.y;
+  }
+  const float M = warp_max(fmaxf(m0, m1));
+  const float w0 = (lane < n && m0 != -INFINITY) ? expf(m0 - M) * l0 : 0.f;
+  const float w1 = (lane + 32 < n && m1 != -INFINITY) ? expf(m1 - M) * l1 : 0.f;
+  const float den = warp_sum(w0) + warp_sum(w1);
   float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
   for (int i0 = 0; i0 < n; i0 += 16) {
     float4 o[16];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const int i = i0 + k;
-      const int slot = i < npre ? i : a.nc_pre + (i - npre);
-      o[k] = i < n ? __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + slot) * kHD) + lane)
-                   : make_float4(0, 0, 0, 0);
-    }
+    for (int k = 0; k < 16; ++k)
+      o[k] = i0 + k < n ? __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + i0 + k) * kHD) + lane)
+                        : make_float4(0, 0, 0, 0);
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-      const float w = __shfl_sync(0xffffffffu, wi, (i0 + k) & 31);
-      if (i0 + k < n) {
+      const int i = i0 + k;
+      const float wa = __shfl_sync(0xffffffffu, w0, i & 31), wb = __shfl_sync(0xffffffffu, w1, i & 31);
+      const float w = i < 32 ? wa : wb;
+      if (i < n) {
         num.x += w * o[k].x;
         num.y += w * o[k].y;
         num.z += w * o[k].z;
@@ -283,6 +289,88 @@ __device__ __forceinline__ void attn_merge_one(const AttnArgs& a, int r, int h, 
   __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(a.out + ((size_t)r * a.Hq + qh) * kHD) + 2 * lane;
   o2[0] = __floats2bfloat162_rn(num.x * inv, num.y * inv);
   o2[1] = __floats2bfloat162_rn(num.z * inv, num.w * inv);
+}
+
+// Decode suffix pass behind the tcgen05 prefix kernel (every work item is a suffix
+// chunk of kSCW tokens): one WARP per unit, each warp with its own staging buffer
+// and mbarrier, so a CTA keeps kAttnWarps independent units in flight and an SM
+// ~12 (the latency of a unit is its page DMA, the q load and the partial's store +
+// count, not its arithmetic).  Lane t scores token t of the chunk (all 128 dims,
+// REP heads); partials, counting and the fused LSE merge as in attn_kernel.
+constexpr int kSCW = 32;
+template <int REP>
+struct SuffixWarpSmem {
+  static constexpr int kWarp = 2 * kSCW * kHD * 2 + REP * kHD * 4;  // K, V [32][128] bf16 + q [REP][128] fp32
+  static constexpr int v = kAttnWarps * kWarp + kAttnWarps * 8 + 64;
+};
+
+template <int REP>
+__global__ void __launch_bounds__(kAttnThreads) attn_suffix_warp_kernel(AttnArgs a) {
+  pdl_launch_dependents();
+  using SM = SuffixWarpSmem<REP>;
+  extern __shared__ __align__(128) uint8_t wsm[];
+  __shared__ int merge_list[kAttnWarps][64];
+  __shared__ int merge_n[kAttnWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(wsm + warp * SM::kWarp);
+  __nv_bfloat16* Vs = Ks + kSCW * kHD;
+  float* qs = reinterpret_cast<float*>(Vs + kSCW * kHD);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wsm + kAttnWarps * SM::kWarp) + warp;
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+    merge_n[warp] = 0;
+  }
+  __syncwarp();
+  // Launched behind attn_prefix_tc_kernel, which triggers only after its wait on the
+  // QKV GEMM: q and the appended KV are complete here.
+  const int n = (int)a.n_items[0];
+  const size_t hs = (size_t)a.pt * kHD;
+  uint32_t phase = 0;
+  const int stride = gridDim.x * kAttnWarps;
+#pragma unroll 1
+  for (int u = blockIdx.x * kAttnWarps + warp; u < n; u += stride) {
+    const int32_t* item = a.items + (size_t)u * kItemStride;
+    const int code = item[0];
+    const int c = (code >> 16) & 0xFF, r = (code >> 8) & 0xFF, h = code & 0xFF;
+    const int len = a.row_len[r];
+    const int ntok = min(kSCW, len - c * kSCW);
+    const int npg = (ntok + a.pt - 1) / a.pt;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // our buffer was last read generically
+    if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)ntok * kHD * 2 * 2);
+    __syncwarp();
+    if (lane < npg) {
+      const int page = item[1 + lane];
+      const uint32_t bytes = (uint32_t)min(a.pt, ntok - lane * a.pt) * kHD * 2;
+      const __nv_bfloat16* kb = a.pool + (((size_t)page * 2) * a.Hkv + h) * hs;
+      bulk_g2s(Ks + lane * a.pt * kHD, kb, bytes, bar);
+      bulk_g2s(Vs + lane * a.pt * kHD, kb + (size_t)a.Hkv * hs, bytes, bar);
+    }
+    attn_load_q<REP>(a, r, h, qs, lane);
+    __syncwarp();
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    WarpPartial<REP, 1> wp;
+    wp.run(qs, Ks, Vs, ntok, a.scale, lane);
+    store_partial<REP>(a, r, h, a.nc_pre + c, wp.m, wp.l, wp.o, lane);
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+      const int nsuf = (len + kSCW - 1) / kSCW;
+      if (atomicAdd(a.merge_cnt + r * a.Hkv + h, 1) + 1 == nsuf) {
+        __threadfence();
+        a.merge_cnt[r * a.Hkv + h] = 0;  // ready for the next launch
+        if (merge_n[warp] < 64) merge_list[warp][merge_n[warp]++] = (r << 8) | h;
+      }
+    }
+    __syncwarp();
+  }
+  pdl_wait();  // the tcgen05 prefix partials are complete from here on
+  const int nm = merge_n[warp];
+  for (int j = 0; j < nm * REP; ++j) {
+    const int rh = merge_list[warp][j / REP];
+    attn_merge_one<REP>(a, rh >> 8, rh & 0xFF, j % REP, lane);
+  }
 }
 
 // Work units (persistent grid, ~4 CTAs per SM):

@@ -26,13 +26,16 @@ args = ap.parse_args()
 shape = SHAPES[args.shape]
 P, max_new = 256, 1024
 w = gen_weights(shape, seed=20261017, device="cuda")
-cfg = _lib.make_config(shape, args.G, args.g, max_new, P, mode="infinite", kv_budget_bytes=0, seed=20261017)
+M = int(os.environ.get("GROUPS", "1"))
+cfg = _lib.make_config(shape, args.G, args.g, max_new, P, mode="infinite", kv_budget_bytes=0, seed=20261017,
+                       max_groups=M)
 ctx = _lib.Context(cfg, w)
-prompt = torch.as_tensor(gen_prompt(shape.vocab, P, 0), device="cuda")
-true = gen_trace("math", args.G, max_new, 1)
-pred = predict_lengths(true, "noisy", 0.3, seed=1)
-ctx.is_prefill(prompt, 0)
-ctx.is_start_group(true, pred)
+for m in range(M):
+    prompt = torch.as_tensor(gen_prompt(shape.vocab, P, m), device="cuda")
+    true = gen_trace("math", args.G, max_new, 1 + m)
+    pred = predict_lengths(true, "noisy", 0.3, seed=1 + m)
+    ctx.is_prefill(prompt, m, slot=m)
+    ctx.is_start_group(true, pred, slot=m)
 torch.cuda.synchronize()
 for _ in range(args.steps):
     ctx.is_decode_step()

@@ -140,6 +140,7 @@ def run_ours(args):
     ctx = _lib.Context(cfg, w)
     del w
     torch.cuda.empty_cache()
+    comm = nccl_comm(_lib, dist, rank, world)
     n_total = args.warmup + args.steps
 
     def workload(i):
@@ -173,9 +174,8 @@ def run_ours(args):
         acc["rows"] += q["tokens_decoded"]
         acc["steps"] += q["steps"]
         ctx.is_group_results(d_rew, d_len)
-        if dist is not None:                 # the one exchange: lengths + rewards for Eq. 2
-            dist.all_gather_into_tensor(all_len, d_len)
-            dist.all_gather_into_tensor(all_rew, d_rew)
+        if comm is not None:                 # the one exchange: lengths + rewards for Eq. 2 (NCCL, C ABI)
+            ctx.is_allgather_results(comm, d_len, d_rew, all_len, all_rew)
         out = None
         if host_inputs:                      # device -> host read of the step's result
             out = (all_rew if dist is not None else d_rew).cpu()
@@ -341,6 +341,7 @@ def run_groups(args):
     ctx = _lib.Context(cfg, w)
     del w
     torch.cuda.empty_cache()
+    comm = nccl_comm(_lib, dist, rank, world)
 
     def workload(j):
         pid = rank * 100000 + j  # global prompt id (RNG keyed by global uid)
@@ -372,9 +373,8 @@ def run_groups(args):
                     true = slot_of.pop(slot)
                     tokens += int(np.sum(true))
                     ctx.is_group_results(d_rew, d_len, slot=slot)
-                    if dist is not None:  # the one exchange: lengths + rewards for Eq. 2
-                        dist.all_gather_into_tensor(all_len, d_len)
-                        dist.all_gather_into_tensor(all_rew, d_rew)
+                    if comm is not None:  # the one exchange: lengths + rewards for Eq. 2 (NCCL, C ABI)
+                        ctx.is_allgather_results(comm, d_len, d_rew, all_len, all_rew)
                     if queue:
                         pid, dp, tr, pr = queue.pop(0)
                         ctx.is_prefill(dp, pid, slot=slot)
@@ -426,8 +426,23 @@ def run_groups(args):
             "decode_steps": int(dsteps), "ms_per_decode_step": round(ms_max / max(dsteps, 1), 4),
             "global_peak_kv_bytes": st["global_peak_kv_bytes"], "clocks": clk}))
     ctx.close()
+    if comm is not None:
+        _lib.nccl_comm_destroy(comm)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def nccl_comm(_lib, dist, rank, world):
+    """The library's NCCL communicator for the results all-gather: rank 0 creates the
+    unique id, the torch process group broadcasts it (plumbing only)."""
+    if dist is None:
+        return None
+    import torch
+    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(_lib.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(uid, 0)
+    return _lib.nccl_comm_init(bytes(uid.cpu().numpy().tobytes()), rank, world)
 
 
 def _oracle_tokens_per_s(C, budget_s, step_seed=0):

@@ -210,6 +210,25 @@ is_status is_group_results(is_ctx* ctx, float* d_reward, int32_t* d_len);
  * ascending index, population sigma, sigma = 0 -> 0 (R28).  Host pointers. */
 is_status is_group_advantages(const float* h_rewards, int32_t G, is_adv_mode mode, float* h_adv);
 
+/* The one cross-GPU exchange (BASELINE north_star "NCCL over NVLink
+ * used only to all-gather completion lengths and rewards"): prompts are sharded by
+ * rank, and after a group completes every rank all-gathers its (length, reward)
+ * per sample so each holds the global arrays the group advantages (Eq. 2,
+ * P:128-131) and the policy update need.
+ *   is_nccl_unique_id   rank 0 creates the 128-byte ncclUniqueId (h_uid); the caller
+ *                       broadcasts it (e.g. over its torch process group);
+ *   is_nccl_comm_init   every rank joins; *comm_out is an ncclComm_t owned by the caller;
+ *   is_allgather_results  on the context's stream: d_len[G] int32, d_reward[G] fp32
+ *                       (device; e.g. from is_group_results) -> d_all_len[world*G],
+ *                       d_all_reward[world*G] in rank order;
+ *   is_nccl_comm_destroy  frees the communicator.
+ * NCCL is resolved at run time from the process's libnccl.so.2 (IS_ERR_CUDA if absent). */
+is_status is_nccl_unique_id(void* h_uid);
+is_status is_nccl_comm_init(const void* h_uid, int32_t rank, int32_t world, void** comm_out);
+is_status is_allgather_results(is_ctx* ctx, void* comm, const int32_t* d_len, const float* d_reward,
+                               int32_t* d_all_len, float* d_all_reward);
+is_status is_nccl_comm_destroy(void* comm);
+
 /* Debug: when d_logits != NULL every following lm_head launch also writes its
  * fp32 logits to d_logits[row_capacity][vocab] (sampler parity, R12 (i)). */
 is_status is_set_logits_dump(is_ctx* ctx, float* d_logits);

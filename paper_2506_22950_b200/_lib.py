@@ -20,7 +20,8 @@ EXPORTS = ["is_plan", "is_create", "is_destroy", "is_prefill", "is_start_group",
            "is_group_results", "is_group_advantages", "is_set_logits_dump", "is_profile_step",
            "is_dbg_gemm", "is_dbg_mk_trace", "is_dbg_copy", "is_prefill_slot", "is_start_group_slot",
            "is_run_until_any_done", "is_query_slot", "is_copy_tokens_slot", "is_copy_schedule_slot",
-           "is_group_results_slot", "is_last_error", "is_version"]
+           "is_group_results_slot", "is_nccl_unique_id", "is_nccl_comm_init", "is_allgather_results",
+           "is_nccl_comm_destroy", "is_last_error", "is_version"]
 
 
 class InfsampError(RuntimeError):
@@ -115,6 +116,10 @@ def load(build_if_missing=True):
     L.is_copy_tokens_slot.argtypes = [vp, i32, vp, i32]
     L.is_copy_schedule_slot.argtypes = [vp, i32, vp, vp, i32, ctypes.POINTER(i32)]
     L.is_group_results_slot.argtypes = [vp, i32, vp, vp]
+    L.is_nccl_unique_id.argtypes = [vp]
+    L.is_nccl_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
+    L.is_allgather_results.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.is_nccl_comm_destroy.argtypes = [vp]
     L.is_last_error.restype = ctypes.c_char_p
     L.is_last_error.argtypes = []
     L.is_version.restype = ctypes.c_char_p
@@ -208,6 +213,25 @@ def weight_pointer_list(weights, layers):
     return ptrs
 
 
+def nccl_unique_id():
+    """128-byte ncclUniqueId (rank 0); broadcast it to the other ranks."""
+    buf = (ctypes.c_char * 128)()
+    _check(load().is_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def nccl_comm_init(uid, rank, world):
+    """Join the communicator; returns an opaque handle (pass to is_allgather_results / nccl_comm_destroy)."""
+    buf = (ctypes.c_char * 128).from_buffer_copy(uid)
+    comm = ctypes.c_void_p()
+    _check(load().is_nccl_comm_init(buf, int(rank), int(world), ctypes.byref(comm)))
+    return comm
+
+
+def nccl_comm_destroy(comm):
+    _check(load().is_nccl_comm_destroy(comm))
+
+
 class Context:
     """Owning handle of an is_ctx (library-owned device state for one GPU)."""
 
@@ -287,6 +311,10 @@ class Context:
 
     def is_group_results(self, d_reward, d_len, slot=0):
         _check(load().is_group_results_slot(self._h, int(slot), d_reward.data_ptr(), d_len.data_ptr()))
+
+    def is_allgather_results(self, comm, d_len, d_reward, d_all_len, d_all_reward):
+        _check(load().is_allgather_results(self._h, comm, d_len.data_ptr(), d_reward.data_ptr(),
+                                           d_all_len.data_ptr(), d_all_reward.data_ptr()))
 
     def is_set_logits_dump(self, d_logits):
         _check(load().is_set_logits_dump(self._h, None if d_logits is None else d_logits.data_ptr()))

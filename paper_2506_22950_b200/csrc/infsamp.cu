@@ -5,6 +5,8 @@
 // check (R25), weight packing, the paged KV pool, and the
 // decode step orchestration, captured once into a CUDA graph with
 // programmatic dependent launch between kernels.
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -1881,5 +1883,96 @@ extern "C" is_status is_dbg_copy(is_ctx* c, int32_t which, void* h_dst, int64_t 
   if (!src) return fail(IS_ERR_STATE, "buffer %d not in use", which);
   if (bytes < n) return fail(IS_ERR_CAPACITY, "need %lld bytes", (long long)n);
   CK(cudaMemcpy(h_dst, src, (size_t)n, cudaMemcpyDeviceToHost));
+  return IS_OK;
+}
+
+// ------------------------------------------------------------------ NCCL (a9: the one exchange)
+// NCCL is bound at run time (dlopen / dlsym of libnccl.so.2): the process's NCCL
+// (torch's bundled one when torch is loaded) is used, and the library has no
+// link-time NCCL dependency.  Types mirror nccl.h.
+namespace {
+struct NcclUid { char internal[128]; };
+typedef void* NcclComm;
+typedef int (*PfnGetUid)(NcclUid*);
+typedef int (*PfnInitRank)(NcclComm*, int, NcclUid, int);
+typedef int (*PfnAllGather)(const void*, void*, size_t, int, NcclComm, cudaStream_t);
+typedef int (*PfnGroup)();
+typedef int (*PfnDestroy)(NcclComm);
+typedef const char* (*PfnErr)(int);
+struct NcclApi {
+  PfnGetUid get_uid = nullptr;
+  PfnInitRank init_rank = nullptr;
+  PfnAllGather all_gather = nullptr;
+  PfnGroup group_start = nullptr, group_end = nullptr;
+  PfnDestroy destroy = nullptr;
+  PfnErr err = nullptr;
+  bool ok = false;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.get_uid = (PfnGetUid)dlsym(h, "ncclGetUniqueId");
+      api.init_rank = (PfnInitRank)dlsym(h, "ncclCommInitRank");
+      api.all_gather = (PfnAllGather)dlsym(h, "ncclAllGather");
+      api.group_start = (PfnGroup)dlsym(h, "ncclGroupStart");
+      api.group_end = (PfnGroup)dlsym(h, "ncclGroupEnd");
+      api.destroy = (PfnDestroy)dlsym(h, "ncclCommDestroy");
+      api.err = (PfnErr)dlsym(h, "ncclGetErrorString");
+      api.ok = api.get_uid && api.init_rank && api.all_gather && api.group_start && api.group_end && api.destroy;
+    }
+  }
+  return api;
+}
+constexpr int kNcclInt32 = 2, kNcclFloat32 = 7;
+}  // namespace
+
+#define NCK(x)                                                                                      \
+  do {                                                                                              \
+    int r_ = (x);                                                                                   \
+    if (r_ != 0) return fail(IS_ERR_CUDA, "NCCL error %d (%s) in %s", r_,                            \
+                             nccl().err ? nccl().err(r_) : "?", #x);                                \
+  } while (0)
+
+extern "C" is_status is_nccl_unique_id(void* h_uid) {
+  if (!h_uid) return fail(IS_ERR_CONFIG, "null argument");
+  if (!nccl().ok) return fail(IS_ERR_CUDA, "libnccl.so.2 not available");
+  NcclUid u;
+  NCK(nccl().get_uid(&u));
+  memcpy(h_uid, &u, sizeof u);
+  return IS_OK;
+}
+
+extern "C" is_status is_nccl_comm_init(const void* h_uid, int32_t rank, int32_t world, void** comm_out) {
+  if (!h_uid || !comm_out || world < 1 || rank < 0 || rank >= world) return fail(IS_ERR_CONFIG, "bad arguments");
+  if (!nccl().ok) return fail(IS_ERR_CUDA, "libnccl.so.2 not available");
+  NcclUid u;
+  memcpy(&u, h_uid, sizeof u);
+  NcclComm comm = nullptr;
+  NCK(nccl().init_rank(&comm, world, u, rank));
+  *comm_out = comm;
+  return IS_OK;
+}
+
+extern "C" is_status is_nccl_comm_destroy(void* comm) {
+  if (!comm) return fail(IS_ERR_CONFIG, "null argument");
+  if (!nccl().ok) return fail(IS_ERR_CUDA, "libnccl.so.2 not available");
+  NCK(nccl().destroy(comm));
+  return IS_OK;
+}
+
+extern "C" is_status is_allgather_results(is_ctx* c, void* comm, const int32_t* d_len, const float* d_reward,
+                                          int32_t* d_all_len, float* d_all_reward) {
+  if (!c || !comm || !d_len || !d_reward || !d_all_len || !d_all_reward) return fail(IS_ERR_CONFIG, "null argument");
+  if (!nccl().ok) return fail(IS_ERR_CUDA, "libnccl.so.2 not available");
+  StreamGuard guard(c, c->user);
+  NCK(nccl().group_start());
+  NCK(nccl().all_gather(d_len, d_all_len, (size_t)c->G, kNcclInt32, comm, c->st));
+  NCK(nccl().all_gather(d_reward, d_all_reward, (size_t)c->G, kNcclFloat32, comm, c->st));
+  NCK(nccl().group_end());
   return IS_OK;
 }

@@ -233,3 +233,30 @@ def test_tiny_context_reused_across_prompts(lib, tiny):
     z = M.teacher_forced_logits(tiny["w"], TINY, p1, [int(x) for x in fresh[0, :2]], mirror=True, rows=[0])[0]
     tok, margin = sampler.sample_margin(z.astype(np.float32), SEED, 1 * 8 + 0, 0)
     assert tok == fresh[0, 0] or margin < 0.05
+
+
+def test_nccl_allgather_results_single_rank(lib, tiny):
+    """The C-ABI NCCL exchange (a9) on a one-rank communicator: the gathered arrays
+    are the rank's own (length, reward) per sample, in order."""
+    try:
+        uid = lib.nccl_unique_id()
+    except lib.InfsampError as e:
+        pytest.skip(f"no NCCL: {e}")
+    comm = lib.nccl_comm_init(uid, 0, 1)
+    cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", kv_budget_bytes=tiny["budget"], seed=SEED,
+                          decode_impl=tiny["impl"])
+    ctx = lib.Context(cfg, tiny["w_dev"])
+    ctx.is_prefill(torch.as_tensor(tiny["prompt"], device="cuda"), 0)
+    ctx.is_start_group(tiny["true"], tiny["pred"])
+    ctx.is_run_group()
+    rew = torch.zeros(8, device="cuda")
+    ln = torch.zeros(8, dtype=torch.int32, device="cuda")
+    ctx.is_group_results(rew, ln)
+    all_rew = torch.full((8,), -1.0, device="cuda")
+    all_len = torch.full((8,), -1, dtype=torch.int32, device="cuda")
+    ctx.is_allgather_results(comm, ln, rew, all_len, all_rew)
+    torch.cuda.synchronize()
+    ctx.close()
+    lib.nccl_comm_destroy(comm)
+    assert all_len.cpu().tolist() == ln.cpu().tolist() == [int(x) for x in tiny["true"]]
+    assert torch.equal(all_rew.cpu(), rew.cpu())

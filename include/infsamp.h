@@ -202,6 +202,13 @@ is_status is_copy_schedule_slot(is_ctx* ctx, int32_t slot, int32_t* h_slot_table
                                 int32_t max_steps, int32_t* h_n);
 is_status is_group_results_slot(is_ctx* ctx, int32_t slot, float* d_reward, int32_t* d_len);
 
+/* Log-probability of every generated token: h_dst[G][max_new]
+ * host fp32, log pi_theta(token) = z_tok - logsumexp_v(z_v) of the step's logits at
+ * temperature 1 (R33), reduced on the device from the lm_head CTAs'
+ * online (max, sum-exp) partials in a fixed order; 0 beyond each sample's length. */
+is_status is_copy_logprobs(is_ctx* ctx, float* h_dst);
+is_status is_copy_logprobs_slot(is_ctx* ctx, int32_t slot, float* h_dst);
+
 /* Benchmark reward and completion length per sample (R29):
  * d_reward[G] = #{tokens < vocab/2}/len, d_len[G] = len.  Device buffers. */
 is_status is_group_results(is_ctx* ctx, float* d_reward, int32_t* d_len);

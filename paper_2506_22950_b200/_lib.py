@@ -21,7 +21,7 @@ EXPORTS = ["is_plan", "is_create", "is_destroy", "is_prefill", "is_start_group",
            "is_dbg_gemm", "is_dbg_mk_trace", "is_dbg_copy", "is_prefill_slot", "is_start_group_slot",
            "is_run_until_any_done", "is_query_slot", "is_copy_tokens_slot", "is_copy_schedule_slot",
            "is_group_results_slot", "is_nccl_unique_id", "is_nccl_comm_init", "is_allgather_results",
-           "is_nccl_comm_destroy", "is_last_error", "is_version"]
+           "is_nccl_comm_destroy", "is_copy_logprobs", "is_copy_logprobs_slot", "is_last_error", "is_version"]
 
 
 class InfsampError(RuntimeError):
@@ -120,6 +120,8 @@ def load(build_if_missing=True):
     L.is_nccl_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
     L.is_allgather_results.argtypes = [vp, vp, vp, vp, vp, vp]
     L.is_nccl_comm_destroy.argtypes = [vp]
+    L.is_copy_logprobs.argtypes = [vp, vp]
+    L.is_copy_logprobs_slot.argtypes = [vp, i32, vp]
     L.is_last_error.restype = ctypes.c_char_p
     L.is_last_error.argtypes = []
     L.is_version.restype = ctypes.c_char_p
@@ -297,6 +299,11 @@ class Context:
     def is_copy_tokens(self, slot=0):
         out = np.zeros((self.G, self.cfg.max_new_tokens), np.int32)
         _check(load().is_copy_tokens_slot(self._h, int(slot), _np_ptr(out), 0))
+        return out
+
+    def is_copy_logprobs(self, slot=0):
+        out = np.zeros((self.G, self.cfg.max_new_tokens), np.float32)
+        _check(load().is_copy_logprobs_slot(self._h, int(slot), _np_ptr(out)))
         return out
 
     def is_copy_schedule(self, max_steps=None, slot=0):

@@ -64,6 +64,8 @@ struct GemmArgs {
   const int32_t* row_t;
   const int32_t* row_active;
   unsigned long long* keys;
+  unsigned long long* lp_key;  // SAMPLE (NEXT-3): per (row, CTA) best key of the CTA's tiles  [rows][gridDim]
+  float4* lp_mlz;              //   and its online (max z, sum exp(z - max), winner's z, -)   [rows][gridDim]
   float* logits_dump;  // optional [rows][M]
   uint64_t seed;
   float inv_temp;
@@ -131,6 +133,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const bool bnorm = a.bn_resid != nullptr;
   __shared__ unsigned long long skey[BN];
   __shared__ float sred[4][BN];
+  __shared__ unsigned long long swkey[4][BN];  // SAMPLE: per-warp best key, its logit, tile max / sum
+  __shared__ float swz[4][BN], swm[4][BN];
+  __shared__ float run_m[BN], run_l[BN], run_z[BN];  // the CTA's running log-sum-exp state per row
+  __shared__ unsigned long long run_k[BN];
   __shared__ int srow_act[BN], srow_kv[BN];  // EPI_QKV: row tables, loaded during the mainloop
 
   const int warp = threadIdx.x >> 5;
@@ -163,7 +169,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
-  if (EPI == EPI_SAMPLE && threadIdx.x < BN) skey[threadIdx.x] = 0ull;
+  if (EPI == EPI_SAMPLE && threadIdx.x < BN) {
+    skey[threadIdx.x] = 0ull;
+    run_m[threadIdx.x] = -INFINITY;
+    run_l[threadIdx.x] = 0.f;
+    run_z[threadIdx.x] = 0.f;
+    run_k[threadIdx.x] = 0ull;
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -484,28 +496,66 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       } else if constexpr (EPI == EPI_SAMPLE) {
+        const bool lp = a.lp_key != nullptr;
         for (int n = 0; n < min(BN, a.n_valid); ++n) {
           if (!a.row_active[a.row0 + n]) continue;
           unsigned long long key = 0ull;
+          float z = -INFINITY;
           if (gm < a.M) {
-            const float z = stg[n * kBM + m];
+            z = stg[n * kBM + m];
             if (a.logits_dump) a.logits_dump[(size_t)(a.row0 + n) * a.ld_out + gm] = z;
             const float g = gumbel(a.seed, (uint32_t)a.row_uid[a.row0 + n], (uint32_t)a.row_t[a.row0 + n],
                                    (uint32_t)gm);
             key = order_key(__fadd_rn(__fmul_rn(z, a.inv_temp), g), (uint32_t)gm);
           }
+          float zk = z;  // logit carried with the key
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
             const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-            key = other > key ? other : key;
+            const float oz = __shfl_xor_sync(0xffffffffu, zk, o);
+            if (other > key) {
+              key = other;
+              zk = oz;
+            }
           }
           if (lane == 0) atomicMax(&skey[n], key);
+          if (lp) {
+            // per-warp (max, sum exp) of the tile's logits for this row (log-probabilities, NEXT-3)
+            const float wm = warp_max(z);
+            const float ws = warp_sum(z == -INFINITY ? 0.f : expf(z - wm));
+            if (lane == 0) {
+              swkey[q][n] = key;
+              swz[q][n] = zk;
+              swm[q][n] = wm;
+              sred[q][n] = ws;
+            }
+          }
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (threadIdx.x - 64 < BN) {
           const int n = threadIdx.x - 64;
           if (skey[n]) atomicMax(a.keys + a.row0 + n, skey[n]);
           skey[n] = 0ull;
+          if (lp && n < a.n_valid && a.row_active[a.row0 + n]) {
+            // fold the tile into the CTA's running state (warps in fixed order), publish it
+            float M = run_m[n], L = run_l[n];
+            for (int w = 0; w < 4; ++w) {
+              const float mw = swm[w][n];
+              if (mw == -INFINITY) continue;
+              const float Mn = fmaxf(M, mw);
+              L = (M == -INFINITY ? 0.f : L * expf(M - Mn)) + sred[w][n] * expf(mw - Mn);
+              M = Mn;
+              if (swkey[w][n] > run_k[n]) {
+                run_k[n] = swkey[w][n];
+                run_z[n] = swz[w][n];
+              }
+            }
+            run_m[n] = M;
+            run_l[n] = L;
+            const size_t idx = (size_t)(a.row0 + n) * gridDim.x + blockIdx.x;
+            a.lp_key[idx] = run_k[n];
+            a.lp_mlz[idx] = make_float4(M, L, run_z[n], 0.f);
+          }
         }
       }
       // stg / pre / skey are rewritten by the next tile

@@ -422,6 +422,10 @@ struct is_ctx {
   // rows
   int32_t *row_active, *row_uid, *row_lid, *row_t, *row_tok, *row_pos, *row_kvloc, *row_len;
   unsigned long long* keys;
+  unsigned long long* lp_key;  // NEXT-3: lm_head per-(row, CTA) partials for log-probabilities
+  float4* lp_mlz;
+  float* logprobs;             // [M][G][max_new]
+  int lp_grid;
   int32_t* last_tok;
   uint8_t* last_fin;
   // scheduler
@@ -494,6 +498,10 @@ static SchedArgs sched_args(is_ctx* c) {
   a.log_slot = c->log_slot;
   a.log_live = c->log_live;
   a.keys = c->keys;
+  a.lp_key = c->lp_key;
+  a.lp_mlz = c->lp_mlz;
+  a.logprobs = c->logprobs;
+  a.lp_grid = c->lp_grid;
   a.last_tok = c->last_tok;
   a.last_fin = c->last_fin;
   a.row_active = c->row_active;
@@ -1068,6 +1076,8 @@ static is_status enqueue_step(is_ctx* c) {
   a.row_t = c->row_t;
   a.row_active = c->row_active;
   a.keys = c->keys;
+  a.lp_key = c->lp_key;
+  a.lp_mlz = c->lp_mlz;
   a.logits_dump = c->logits_dump;
   if (c->mk) {
     a.zero = c->mka.sync;  // the next step's dependency counters start from zero
@@ -1285,6 +1295,9 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   for (int32_t** p : {&c->prow_active, &c->prow_tok, &c->prow_pos, &c->prow_kvloc, &c->prow_len})
     *p = (int32_t*)A((size_t)R * 4);
   c->keys = (unsigned long long*)A((size_t)R * 8);
+  c->lp_grid = std::min((int)ceil_div64(s.vocab, kBM), g_num_sms);  // the lm_head launch's grid
+  c->lp_key = (unsigned long long*)A((size_t)R * c->lp_grid * 8);
+  c->lp_mlz = (float4*)A((size_t)R * c->lp_grid * 16);
   c->last_tok = (int32_t*)A((size_t)R * 4);
   c->last_fin = (uint8_t*)A((size_t)R);
   const int M = c->M;
@@ -1302,6 +1315,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->tokens = (int32_t*)A((size_t)M * c->G * c->max_new * 4);
   c->log_slot = (int32_t*)A((size_t)M * c->log_cap * c->g * 4);
   c->log_live = (int32_t*)A((size_t)M * c->log_cap * 4);
+  c->logprobs = (float*)A((size_t)M * c->G * c->max_new * 4);
   c->d_prompt_copy = (int32_t*)A((size_t)c->P * 4);
   if (err != IS_OK) return err;
   CK(cudaMallocHost(&c->st_host, sizeof(long long) * ST_COUNT * (M + 1)));
@@ -1383,7 +1397,7 @@ extern "C" void is_destroy(is_ctx* c) {
                   c->row_t, c->row_tok, c->row_pos, c->row_kvloc, c->row_len, c->keys, c->last_tok,
                   c->last_fin, c->st_dev, c->slot_uid, c->slot_count, c->tpos, c->true_len, c->queue,
                   c->main_init, c->main_queue, c->free_stack, c->pagetab, c->npages, c->tokens, c->log_slot,
-                  c->log_live, c->d_prompt_copy, c->prow_active, c->prow_tok, c->prow_pos, c->prow_kvloc,
+                  c->log_live, c->d_prompt_copy, c->lp_key, c->lp_mlz, c->logprobs, c->prow_active, c->prow_tok, c->prow_pos, c->prow_kvloc,
                   c->prow_len};
   for (void* p : bufs)
     if (p) cudaFree(p);
@@ -1505,6 +1519,7 @@ extern "C" is_status is_start_group_slot(is_ctx* c, int32_t m, const int32_t* tr
   CK(cudaMemcpyAsync(c->main_queue + oG, queue.data(), G * 4, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemsetAsync(c->npages + oG, 0, G * 4, c->st));
   CK(cudaMemsetAsync(c->tokens + oG * c->max_new, 0xFF, (size_t)G * c->max_new * 4, c->st));
+  CK(cudaMemsetAsync(c->logprobs + oG * c->max_new, 0, (size_t)G * c->max_new * 4, c->st));
   CK(cudaMemsetAsync(c->log_slot + (size_t)m * c->log_cap * g, 0xFF, (size_t)c->log_cap * g * 4, c->st));
   CK(cudaMemsetAsync(c->log_live + (size_t)m * c->log_cap, 0, (size_t)c->log_cap * 4, c->st));
   // rows of the next step: allocate / log for this group only (the others are mid-step)
@@ -1976,3 +1991,13 @@ extern "C" is_status is_allgather_results(is_ctx* c, void* comm, const int32_t* 
   NCK(nccl().group_end());
   return IS_OK;
 }
+
+extern "C" is_status is_copy_logprobs_slot(is_ctx* c, int32_t m, float* h_dst) {
+  if (!c || !h_dst) return fail(IS_ERR_CONFIG, "null argument");
+  if (m < 0 || m >= c->M) return fail(IS_ERR_CONFIG, "group slot %d out of range [0, %d)", m, c->M);
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaMemcpy(h_dst, c->logprobs + (size_t)m * c->G * c->max_new, (size_t)c->G * c->max_new * 4,
+                cudaMemcpyDeviceToHost));
+  return IS_OK;
+}
+extern "C" is_status is_copy_logprobs(is_ctx* c, float* h_dst) { return is_copy_logprobs_slot(c, 0, h_dst); }

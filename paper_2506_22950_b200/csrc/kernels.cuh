@@ -875,6 +875,10 @@ struct SchedArgs {
   int32_t* log_slot;         // [M][log_cap][g]
   int32_t* log_live;         // [M][log_cap] pages held by the group
   unsigned long long* keys;  // [row_cap] lm_head argmax keys
+  const unsigned long long* lp_key;  // [row_cap][lp_grid] per-CTA best keys (NEXT-3 log-probabilities)
+  const float4* lp_mlz;      // [row_cap][lp_grid] per-CTA (max z, sum exp, winner's z)
+  float* logprobs;           // [M][G][max_new] log pi(token) at temperature 1 (R33)
+  int lp_grid;
   int32_t* last_tok;         // [row_cap]
   uint8_t* last_fin;         // [row_cap]
   int32_t* row_active;
@@ -901,6 +905,36 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
   __shared__ int s_any, s_npre;
   long long* st0 = a.st + (size_t)a.M * ST_COUNT;  // global block: shared pool, counters
   const int tid = threadIdx.x;
+  if (consume && a.logprobs) {
+    // log pi(token) = z_tok - logsumexp(z) from the lm_head CTAs' partials, one warp per row,
+    // CTAs combined in a fixed order (before the policy below advances t)
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int row = warp; row < a.M * a.g; row += kSchedThreads / 32) {
+      const int uid = a.slot_uid[row];
+      if (uid < 0) continue;
+      const int m = row / a.g;
+      const unsigned long long key = a.keys[row];
+      float Mx = -INFINITY, zt = -INFINITY;
+      for (int c = lane; c < a.lp_grid; c += 32) {
+        const float4 v = a.lp_mlz[(size_t)row * a.lp_grid + c];
+        Mx = fmaxf(Mx, v.x);
+        if (a.lp_key[(size_t)row * a.lp_grid + c] == key) zt = v.z;
+      }
+      Mx = warp_max(Mx);
+      zt = warp_max(zt);
+      float L = 0.f;
+      for (int c = lane; c < a.lp_grid; c += 32) {
+        const float4 v = a.lp_mlz[(size_t)row * a.lp_grid + c];
+        if (v.x != -INFINITY) L += v.y * expf(v.x - Mx);
+      }
+      L = warp_sum(L);
+      if (lane == 0) {
+        const size_t lid = (size_t)m * a.G + uid;
+        a.logprobs[lid * a.max_new + a.t[lid]] = zt - (Mx + logf(L));
+      }
+    }
+    __syncthreads();
+  }
   if (tid == 0) {
     if (consume)
       for (int s = 0; s < a.row_cap; ++s) {

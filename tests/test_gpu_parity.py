@@ -83,8 +83,9 @@ def _run(lib, w_dev, prompt, true, pred, mode, g, budget=0, prefix_k=0, pt=16, r
     st = ctx.is_query()
     slots, live = ctx.is_copy_schedule()
     toks = ctx.is_copy_tokens()
+    lps = ctx.is_copy_logprobs()
     ctx.close()
-    return dict(steps=steps, stats=st, slots=slots, live=live, tokens=toks, dumps=dumps)
+    return dict(steps=steps, stats=st, slots=slots, live=live, tokens=toks, dumps=dumps, logprobs=lps)
 
 
 @pytest.fixture(scope="module", params=[0, 1], ids=["persistent", "per_op"])
@@ -260,3 +261,37 @@ def test_nccl_allgather_results_single_rank(lib, tiny):
     lib.nccl_comm_destroy(comm)
     assert all_len.cpu().tolist() == ln.cpu().tolist() == [int(x) for x in tiny["true"]]
     assert torch.equal(all_rew.cpu(), rew.cpu())
+
+
+def _log_softmax64(z):
+    z = np.asarray(z, np.float64)
+    m = z.max()
+    return z - (m + np.log(np.sum(np.exp(z - m))))
+
+
+def test_tiny_logprobs(lib, tiny):
+    """NEXT-3: log pi(token) emitted by the lm_head/sampler path equals the exact fp64
+    log-softmax of the kernel's own logits (1e-4, R31's fp32-accumulation class) and the
+    oracle's teacher-forced one within 2 max|dz| (the logits tolerance propagated)."""
+    r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "infinite", 2,
+             budget=tiny["budget"], logits=True, impl=tiny["impl"])
+    toks, lps = r["tokens"], r["logprobs"]
+    t_of, checked = {}, 0
+    for step, row in enumerate(r["slots"]):
+        for s, uid in enumerate(row):
+            if uid < 0:
+                continue
+            t = t_of.get(uid, 0)
+            tok = int(toks[uid, t])
+            own = _log_softmax64(r["dump" + "s"][step][s])[tok]
+            assert abs(lps[uid, t] - own) <= 1e-4, (step, uid, t, lps[uid, t], own)
+            if t == 0 or step % 7 == 0:
+                gen = [int(x) for x in toks[uid, :t + 1]]
+                z = M.teacher_forced_logits(tiny["w"], TINY, tiny["prompt"], gen, mirror=True, rows=[t])[0]
+                dz = np.max(np.abs(np.asarray(r["dumps"][step][s], np.float64) - z))
+                assert abs(lps[uid, t] - _log_softmax64(z)[tok]) <= 2 * dz + 1e-5, (uid, t)
+                checked += 1
+            t_of[uid] = t + 1
+    assert checked > 0
+    for i, L in enumerate(tiny["true"]):
+        assert np.all(lps[i, :L] < 0) and np.all(lps[i, L:] == 0)

@@ -43,7 +43,10 @@ typedef enum {
   IS_MODE_FULL = 0,    /* all G samples decode in parallel (g = G); unbudgeted reference */
   IS_MODE_NAIVE = 1,   /* N = G/g micro groups, barrier between groups */
   IS_MODE_FIFO = 2,    /* fixed-slot continuous sampling: quota N per slot, trace order (R19) */
-  IS_MODE_INFINITE = 3 /* Alg. 1: [prefix phase] + Alg. 2 FPTAS plan + Alg. 3 SJF refill */
+  IS_MODE_INFINITE = 3, /* Alg. 1: [prefix phase] + Alg. 2 FPTAS plan + Alg. 3 SJF refill */
+  /* Table 2's decomposition (definitions of SPEC.md, DESIGN R23): */
+  IS_MODE_FPTAS_ONLY = 4, /* Alg. 2 plan in its lexicographic (n, j) order, FIFO refill, no quota */
+  IS_MODE_SJF_ONLY = 5    /* trace-order start (samples 0..g-1), Alg. 3 SJF refill, no quota */
 } is_mode;
 
 typedef enum { IS_ADV_STD_NORM = 0, IS_ADV_MEAN_ONLY = 1 } is_adv_mode;

@@ -75,8 +75,12 @@ def sjf_refill(pred, finished, started):
 def build_plan(mode, G, g, pred=None, eps=0.1, finished=()):
     """Initial slot fill + static refill queue for one group.
 
-    mode: 'full' | 'naive' | 'fifo' | 'infinite'.  `finished` = samples that
-    completed in the prefix phase (infinite only).
+    mode: 'full' | 'naive' | 'fifo' | 'infinite' | 'fptas_only' | 'sjf_only'.
+    `finished` = samples that completed in the prefix phase (infinite only).
+    Table 2's decomposition is undefined in the paper; SPEC.md's
+    definitions (R23): fptas_only = the Alg. 2 plan executed in its
+    lexicographic (n, j) order with FIFO refill; sjf_only = trace-order start
+    (samples 0..g-1) with the Alg. 3 SJF refill of the rest.
     """
     if g < 1 or g > G or G % g != 0:
         raise PlanError("IS_ERR_CONFIG: need 1 <= g <= G and G mod g == 0")
@@ -84,6 +88,21 @@ def build_plan(mode, G, g, pred=None, eps=0.1, finished=()):
         return dict(init=list(range(G)), queue=[], plan=None)
     if mode in ("naive", "fifo"):
         return dict(init=list(range(g)), queue=list(range(g, G)), plan=None)
+    if mode == "sjf_only":
+        init = list(range(g))
+        started = set(init)
+        queue = []
+        while True:
+            j = sjf_refill(pred, set(), started)
+            if j is None:
+                break
+            queue.append(j)
+            started.add(j)
+        return dict(init=init, queue=queue, plan=None)
+    if mode == "fptas_only":
+        plan = fptas_plan(pred, G // g, eps)
+        lex = sorted(range(G), key=lambda i: plan["mask"][i])
+        return dict(init=lex[:g], queue=lex[g:], plan=plan)
     if mode != "infinite":
         raise PlanError(f"IS_ERR_CONFIG: unknown mode {mode}")
     N = G // g

@@ -115,6 +115,12 @@ def simulate(true_len, mode, g, pred=None, eps=0.1, prefix_k=0, page_tokens=16):
         p = build_plan(mode, G, g)
         res.init, res.queue = p["init"], p["queue"]
         run_phase(p["queue"], lambda u: big, False, N, p["init"])
+    elif mode in ("fptas_only", "sjf_only"):
+        if pred is None:
+            raise ValueError(f"{mode} mode needs predicted lengths")
+        p = build_plan(mode, G, g, pred=pred, eps=eps)
+        res.init, res.queue, res.plan = p["init"], p["queue"], p["plan"]
+        run_phase(p["queue"], lambda u: big, False, 0, p["init"])
     elif mode == "infinite":
         if pred is None:
             raise ValueError("infinite mode needs predicted lengths")

@@ -12,7 +12,7 @@ import numpy as np
 from . import build as _build
 
 IS_OK, IS_ERR_CONFIG, IS_ERR_BUDGET, IS_ERR_CAPACITY, IS_ERR_DATA, IS_ERR_STATE, IS_ERR_CUDA = range(7)
-MODES = {"full": 0, "naive": 1, "fifo": 2, "infinite": 3}
+MODES = {"full": 0, "naive": 1, "fifo": 2, "infinite": 3, "fptas_only": 4, "sjf_only": 5}
 ADV_MODES = {"std_norm": 0, "mean_only": 1}
 
 EXPORTS = ["is_plan", "is_create", "is_destroy", "is_prefill", "is_start_group", "is_decode_step",

@@ -76,6 +76,7 @@ static is_status check_config(const is_config* c) {
   if (c->prefix_k < 0 || (c->prefix_k > 0 && c->mode != IS_MODE_INFINITE))
     return fail(IS_ERR_CONFIG, "prefix_k > 0 requires IS_MODE_INFINITE");
   if (!(c->temperature > 0)) return fail(IS_ERR_CONFIG, "temperature must be > 0");
+  if (c->mode < IS_MODE_FULL || c->mode > IS_MODE_SJF_ONLY) return fail(IS_ERR_CONFIG, "unknown mode %d", (int)c->mode);
   if (c->max_groups < 0 || n_groups(c) > 8 || n_groups(c) * g > 64)
     return fail(IS_ERR_CONFIG, "need 1 <= max_groups <= 8 and max_groups * g <= 64 (got %d x %d)", n_groups(c), g);
   return IS_OK;
@@ -108,7 +109,25 @@ extern "C" is_status is_plan(const is_config* cfg, const int32_t* pred, const ui
   if (cfg->kv_budget_bytes > 0 && out->reserved_bytes > cfg->kv_budget_bytes)
     return fail(IS_ERR_BUDGET, "worst-case KV reservation %lld B exceeds budget %lld B",
                 (long long)out->reserved_bytes, (long long)cfg->kv_budget_bytes);
-  if (cfg->mode != IS_MODE_INFINITE) {
+  if (cfg->mode < IS_MODE_FULL || cfg->mode > IS_MODE_SJF_ONLY) return fail(IS_ERR_CONFIG, "unknown mode %d", (int)cfg->mode);
+  const bool planned = cfg->mode == IS_MODE_INFINITE || cfg->mode == IS_MODE_FPTAS_ONLY;
+  if (cfg->mode == IS_MODE_SJF_ONLY) {
+    // trace-order start, Alg. 3 SJF refill of the rest (DESIGN R23)
+    if (!pred) return fail(IS_ERR_DATA, "IS_MODE_SJF_ONLY needs predicted lengths");
+    for (int i = 0; i < G; ++i)
+      if (pred[i] < 1) return fail(IS_ERR_DATA, "predicted length of sample %d is %d (< 1)", i, pred[i]);
+    if (out->mask) std::fill(out->mask, out->mask + 2 * G, 0);
+    if (out->scaled_len) std::fill(out->scaled_len, out->scaled_len + G, 0);
+    if (out->loads) std::fill(out->loads, out->loads + N, 0);
+    for (int i = 0; i < g; ++i) out->init_slots[i] = i;
+    std::vector<int> rest;
+    for (int i = g; i < G; ++i) rest.push_back(i);
+    std::stable_sort(rest.begin(), rest.end(), [&](int a, int b) { return pred[a] < pred[b]; });
+    out->queue_len = G - g;
+    for (int i = 0; i < G - g; ++i) out->refill_queue[i] = rest[i];
+    return IS_OK;
+  }
+  if (!planned) {
     if (out->mask) std::fill(out->mask, out->mask + 2 * G, 0);
     if (out->scaled_len) std::fill(out->scaled_len, out->scaled_len + G, 0);
     if (out->loads) std::fill(out->loads, out->loads + N, 0);
@@ -117,7 +136,7 @@ extern "C" is_status is_plan(const is_config* cfg, const int32_t* pred, const ui
     for (int i = g; i < G; ++i) out->refill_queue[i - g] = i;
     return IS_OK;
   }
-  if (!pred) return fail(IS_ERR_DATA, "IS_MODE_INFINITE needs predicted lengths");
+  if (!pred) return fail(IS_ERR_DATA, "the FPTAS plan needs predicted lengths");
   int64_t S = 0;
   for (int i = 0; i < G; ++i) {
     if (pred[i] < 1) return fail(IS_ERR_DATA, "predicted length of sample %d is %d (< 1)", i, pred[i]);
@@ -184,6 +203,12 @@ extern "C" is_status is_plan(const is_config* cfg, const int32_t* pred, const ui
     }
   }
   for (int s = ni; s < g; ++s) out->init_slots[s] = -1;
+  if (cfg->mode == IS_MODE_FPTAS_ONLY) {  // the plan's own order, FIFO refill (DESIGN R23)
+    out->queue_len = 0;
+    for (int i : lex)
+      if (!used[i] && !(finished && finished[i])) out->refill_queue[out->queue_len++] = i;
+    return IS_OK;
+  }
   // Alg. 3 repeated: argmin pred over unstarted, unfinished, ties -> lower id (R17)
   std::vector<int> rest;
   for (int i = 0; i < G; ++i)
@@ -517,6 +542,7 @@ static SchedArgs sched_args(is_ctx* c) {
   a.nc_pre = c->nc_pre_dec;
   a.nc_suf = c->nc_suf;
   a.chunk = c->sc;
+  a.sgroups = c->sc == kSCW ? kSGroups : 0;
   a.tc_prefix = c->tc_prefix;
   return a;
 }
@@ -674,6 +700,9 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
     aa.tc_prefix = prefill ? 0 : c->tc_prefix;
     aa.merge_cnt = (!prefill && c->tc_prefix && !getenv("IS_SEPARATE_MERGE")) ? c->merge_cnt : nullptr;
     aa.sc = prefill ? kSC : c->sc;
+    aa.sgroups = (!prefill && c->sc == kSCW) ? kSGroups : 0;
+    aa.pagetab = c->pagetab;
+    aa.maxp = c->maxp;
     aa.NC = c->NC;
     aa.prefill = prefill ? 1 : 0;
     aa.scale = 1.0f / sqrtf((float)kHD);
@@ -683,7 +712,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
   do {                                                                                                         \
     if (do_attn && aa.tc_prefix) CKS(launch_prefix_tc<R>(c, aa, l, st));                                       \
     if (do_attn && aa.merge_cnt)                                                                               \
-      CKS(launch_k_smem(attn_suffix_warp_kernel<R>, dim3(3 * g_num_sms), dim3(kAttnThreads),                  \
+      CKS(launch_k_smem(attn_suffix_warp_kernel<R>, dim3(3 * g_num_sms), dim3(kSWarps * 32),                  \
                         SuffixWarpSmem<R>::v, st, aa));                                                      \
     else if (do_attn) CKS(launch_k_smem(attn_kernel<R>, dim3(nblk), dim3(kAttnThreads), AttnSmem<R>::v, st, aa)); \
     if (do_attn && getenv("IS_ATTN_TWICE")) {                                                                 \

@@ -69,6 +69,20 @@ def test_is_plan_bit_exact_vs_oracle_random(lib):
         assert init == ref["init"] and got["queue"] == ref["queue"]
 
 
+def test_is_plan_table2_modes_bit_exact_vs_oracle(lib):
+    rng = np.random.default_rng(23)
+    for trial in range(150):
+        g = int(rng.choice([1, 2, 4, 8]))
+        G = g * int(rng.integers(1, 9))
+        true = gen_trace("math", G, 1024, int(rng.integers(1 << 30)))
+        pred = [int(x) for x in predict_lengths(true, "noisy", 0.3, seed=trial)]
+        for mode in ("fptas_only", "sjf_only"):
+            got = lib.is_plan(_cfg(lib, G, g, mode=mode), pred)
+            ref = planner.build_plan(mode, G, g, pred=pred, eps=0.1)
+            assert [x for x in got["init"] if x >= 0] == ref["init"], (mode, trial)
+            assert got["queue"] == ref["queue"], (mode, trial)
+
+
 def test_is_plan_trace_order_modes(lib):
     for mode in ("naive", "fifo"):
         p = lib.is_plan(_cfg(lib, 8, 2, mode=mode), None)

@@ -96,12 +96,12 @@ def tiny(lib, request):
     w_dev = {k: v.cuda() for k, v in w.items()}
     budget = okv.prefix_bytes(TINY, 16) + 4 * 2 * okv.page_bytes(TINY, 16)  # config 1: "KV budget 4 slots"
     runs = {m: _run(lib, w_dev, prompt, true, pred, m, 2, budget=budget, impl=impl)
-            for m in ("naive", "fifo", "infinite")}
+            for m in ("naive", "fifo", "infinite", "fptas_only", "sjf_only")}
     runs["full"] = _run(lib, w_dev, prompt, true, pred, "full", 8, impl=impl)
     return dict(w=w, w_dev=w_dev, prompt=prompt, true=true, pred=pred, runs=runs, budget=budget, impl=impl)
 
 
-@pytest.mark.parametrize("mode", ["naive", "fifo", "infinite", "full"])
+@pytest.mark.parametrize("mode", ["naive", "fifo", "infinite", "full", "fptas_only", "sjf_only"])
 def test_tiny_schedule_bit_exact(tiny, mode):
     r = tiny["runs"][mode]
     ref = simulator.simulate(tiny["true"], mode, 2, pred=tiny["pred"], eps=0.1, page_tokens=16)
@@ -120,7 +120,7 @@ def test_tiny_schedule_bit_exact(tiny, mode):
 def test_tiny_token_streams_identical_across_modes(tiny):
     """Batch invariance (R12 iv): a uid's tokens do not depend on the schedule."""
     base = tiny["runs"]["infinite"]["tokens"]
-    for mode in ("naive", "fifo", "full"):
+    for mode in ("naive", "fifo", "full", "fptas_only", "sjf_only"):
         assert np.array_equal(tiny["runs"][mode]["tokens"], base), mode
     for i, L in enumerate(tiny["true"]):
         assert np.all(base[i, :L] >= 0) and np.all(base[i, :L] < TINY.vocab) and np.all(base[i, L:] == -1)

@@ -156,7 +156,7 @@ def test_simulation_invariants_random():
         lens = [int(x) for x in rng.integers(1, 15, G)]
         pred = predict_lengths(lens, "noisy", 0.3, seed=int(rng.integers(1 << 30)))
         opt = planner.optimal_makespan(lens, g) if G <= 12 else None
-        for mode in ("naive", "fifo", "infinite", "full"):
+        for mode in ("naive", "fifo", "infinite", "full", "fptas_only", "sjf_only"):
             r = simulator.simulate(lens, mode, g, pred=pred, eps=0.1, page_tokens=4)
             gg = G if mode == "full" else g
             assert r.total_steps >= simulator.step_lower_bound(lens, gg)
@@ -237,3 +237,28 @@ def test_trace_generator_shape_and_determinism():
     assert np.all(gen_trace((np.log(7.0), 0.0), 4, 100, 3) == 7)
     p = predict_lengths(a, "noisy", 0.0, seed=3)
     assert np.array_equal(p, a)
+
+
+def test_table2_decomposition_definitions():
+    """NEXT-2 (Table 2; SPEC's definitions, DESIGN R23): fptas_only = the Alg. 2
+    plan in lexicographic (n, j) order with FIFO refill; sjf_only = trace-order start, SJF
+    refill.  Pinned against their definitions written out independently of build_plan."""
+    rng = np.random.default_rng(17)
+    for _ in range(200):
+        g = int(rng.integers(1, 5))
+        G = g * int(rng.integers(1, 7))
+        pred = [int(x) for x in rng.integers(1, 60, G)]
+        plan = planner.fptas_plan(pred, G // g, 0.1)
+        lex = sorted(range(G), key=lambda i: tuple(plan["mask"][i]))
+        f = planner.build_plan("fptas_only", G, g, pred=pred, eps=0.1)
+        assert f["init"] == lex[:g] and f["queue"] == lex[g:]
+        inf = planner.build_plan("infinite", G, g, pred=pred, eps=0.1)
+        assert f["init"] == inf["init"]  # same start, different refill order
+        assert sorted(inf["queue"]) == sorted(f["queue"])
+        s = planner.build_plan("sjf_only", G, g, pred=pred)
+        assert s["init"] == list(range(g))
+        assert s["queue"] == sorted(range(g, G), key=lambda i: (pred[i], i))
+    # equal predictions: SJF keeps trace order, i.e. FIFO without a quota
+    lens = [5, 3, 4, 2, 6, 1]
+    r = simulator.simulate(lens, "sjf_only", 2, pred=[7] * 6)
+    assert [e[2] for e in r.events if e[3] == "refill"] == [2, 3, 4, 5]

@@ -26,7 +26,7 @@ from synth import SHAPES, gen_prompt, gen_trace, gen_weights, predict_lengths  #
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--prompts", type=int, default=2)
-ap.add_argument("--modes", default="naive,fifo,infinite,full")
+ap.add_argument("--modes", default="naive,fifo,fptas_only,sjf_only,infinite,full")
 args = ap.parse_args()
 C = CONFIGS[args.config]
 shape = SHAPES[C["shape"]]

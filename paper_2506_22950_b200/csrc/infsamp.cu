@@ -542,7 +542,6 @@ static SchedArgs sched_args(is_ctx* c) {
   a.nc_pre = c->nc_pre_dec;
   a.nc_suf = c->nc_suf;
   a.chunk = c->sc;
-  a.sgroups = c->sc == kSCW ? kSGroups : 0;
   a.tc_prefix = c->tc_prefix;
   return a;
 }
@@ -700,9 +699,6 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
     aa.tc_prefix = prefill ? 0 : c->tc_prefix;
     aa.merge_cnt = (!prefill && c->tc_prefix && !getenv("IS_SEPARATE_MERGE")) ? c->merge_cnt : nullptr;
     aa.sc = prefill ? kSC : c->sc;
-    aa.sgroups = (!prefill && c->sc == kSCW) ? kSGroups : 0;
-    aa.pagetab = c->pagetab;
-    aa.maxp = c->maxp;
     aa.NC = c->NC;
     aa.prefill = prefill ? 1 : 0;
     aa.scale = 1.0f / sqrtf((float)kHD);
@@ -712,7 +708,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
   do {                                                                                                         \
     if (do_attn && aa.tc_prefix) CKS(launch_prefix_tc<R>(c, aa, l, st));                                       \
     if (do_attn && aa.merge_cnt)                                                                               \
-      CKS(launch_k_smem(attn_suffix_warp_kernel<R>, dim3(3 * g_num_sms), dim3(kSWarps * 32),                  \
+      CKS(launch_k_smem(attn_suffix_warp_kernel<R>, dim3(3 * g_num_sms), dim3(kAttnThreads),                  \
                         SuffixWarpSmem<R>::v, st, aa));                                                      \
     else if (do_attn) CKS(launch_k_smem(attn_kernel<R>, dim3(nblk), dim3(kAttnThreads), AttnSmem<R>::v, st, aa)); \
     if (do_attn && getenv("IS_ATTN_TWICE")) {                                                                 \

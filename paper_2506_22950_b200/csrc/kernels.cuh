@@ -120,9 +120,6 @@ struct AttnArgs {
   int tc_prefix;              // decode: shared prefix done by attn_prefix_tc_kernel (tcgen05)
   int* merge_cnt;             // decode: [rows][Hkv] suffix units done; the last one merges (reset by it)
   int sc;                     // decode suffix chunk (tokens per work item): kSC, or kSCW for the warp kernel
-  int sgroups;                // > 0: suffix items are chunk groups, <= sgroups per (row, kv head)
-  const int32_t* pagetab;     // [M*G][maxp] (chunk-group kernel reads pages itself)
-  int maxp;
   int grp_rows;               // decode, tcgen05 prefix: rows per co-resident group (g); group m = rows m*g ..
   int grp_kv_rows;            //   prefix-KV tensor-map rows per group (L * 2 * Hkv * pcap)
   float scale;                // 1/sqrt(128)
@@ -247,8 +244,7 @@ struct AttnSmem {
 template <int REP>
 __device__ __forceinline__ void attn_merge_one(const AttnArgs& a, int r, int h, int j, int lane) {
   const int npre = a.nc_pre;
-  int nsuf = (a.row_len[r] + a.sc - 1) / a.sc;
-  if (a.sgroups > 0) nsuf = min(nsuf, a.sgroups);
+  const int nsuf = (a.row_len[r] + a.sc - 1) / a.sc;
   const int n = npre + nsuf;  // <= 64
   const int qh = h * REP + j;
   const size_t base = ((size_t)r * a.Hq + qh) * a.NC;
@@ -295,39 +291,33 @@ __device__ __forceinline__ void attn_merge_one(const AttnArgs& a, int r, int h, 
   o2[1] = __floats2bfloat162_rn(num.z * inv, num.w * inv);
 }
 
-// Decode suffix pass behind the tcgen05 prefix kernel.  A work item is (row r,
-// kv head h, chunk group j): the row's suffix is cut into ng = min(kSGroups,
-// ceil(len / 32)) contiguous groups of 32-token chunks, and ONE warp walks its
-// group's chunks with a double-buffered staging ring (the next chunk's pages are
-// in flight while the current one is scored) and an online softmax, then stores
-// one partial (o, m, l) in slot nc_pre + j.  Lane t scores token t of a chunk
-// (all 128 dims, REP heads).  The unit that completes a (row, kv head) merges it
-// (fixed order) after the prefix kernel is known complete.  Items carry the row
-// length and page-table row, so a warp starts with no dependent global loads.
+// Decode suffix pass behind the tcgen05 prefix kernel (every work item is a suffix
+// chunk of kSCW tokens): one WARP per unit, each warp with its own staging buffer
+// and mbarrier, so a CTA keeps kAttnWarps independent units in flight and an SM
+// ~12 (the latency of a unit is its page DMA, the q load and the partial's store +
+// count, not its arithmetic).  Lane t scores token t of the chunk (all 128 dims,
+// REP heads); partials, counting and the fused LSE merge as in attn_kernel.
 constexpr int kSCW = 32;
-constexpr int kSGroups = 4;
-constexpr int kSWarps = 2;  // warps per CTA (3 CTAs per SM)
 template <int REP>
 struct SuffixWarpSmem {
-  static constexpr int kStage = 2 * kSCW * kHD * 2;           // K, V [32][128] bf16
-  static constexpr int kWarp = 2 * kStage + REP * kHD * 4;    // two stages + q [REP][128] fp32
-  static constexpr int v = kSWarps * kWarp + kSWarps * 2 * 8 + 64;
+  static constexpr int kWarp = 2 * kSCW * kHD * 2 + REP * kHD * 4;  // K, V [32][128] bf16 + q [REP][128] fp32
+  static constexpr int v = kAttnWarps * kWarp + kAttnWarps * 8 + 64;
 };
 
 template <int REP>
-__global__ void __launch_bounds__(kSWarps * 32) attn_suffix_warp_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(kAttnThreads) attn_suffix_warp_kernel(AttnArgs a) {
   pdl_launch_dependents();
   using SM = SuffixWarpSmem<REP>;
   extern __shared__ __align__(128) uint8_t wsm[];
-  __shared__ int merge_list[kSWarps][64];
-  __shared__ int merge_n[kSWarps];
+  __shared__ int merge_list[kAttnWarps][64];
+  __shared__ int merge_n[kAttnWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* wbase = wsm + warp * SM::kWarp;
-  float* qs = reinterpret_cast<float*>(wbase + 2 * SM::kStage);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wsm + kSWarps * SM::kWarp) + 2 * warp;
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(wsm + warp * SM::kWarp);
+  __nv_bfloat16* Vs = Ks + kSCW * kHD;
+  float* qs = reinterpret_cast<float*>(Vs + kSCW * kHD);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wsm + kAttnWarps * SM::kWarp) + warp;
   if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    mbar_init(bar, 1);
     fence_barrier_init();
     merge_n[warp] = 0;
   }
@@ -336,69 +326,38 @@ __global__ void __launch_bounds__(kSWarps * 32) attn_suffix_warp_kernel(AttnArgs
   // QKV GEMM: q and the appended KV are complete here.
   const int n = (int)a.n_items[0];
   const size_t hs = (size_t)a.pt * kHD;
-  uint32_t ph[2] = {0u, 0u};
-  const int stride = gridDim.x * kSWarps;
+  uint32_t phase = 0;
+  const int stride = gridDim.x * kAttnWarps;
 #pragma unroll 1
-  for (int u = blockIdx.x * kSWarps + warp; u < n; u += stride) {
-    const int32_t* itp = a.items + (size_t)u * kItemStride;  // code, len, lid, ng (independent loads)
-    const int4 it = make_int4(itp[0], itp[1], itp[2], itp[3]);
-    const int j = (it.x >> 16) & 0xFF, r = (it.x >> 8) & 0xFF, h = it.x & 0xFF;
-    const int len = it.y, lid = it.z, ng = it.w;
-    const int nch = (len + kSCW - 1) / kSCW;
-    const int c0 = j * nch / ng, c1 = (j + 1) * nch / ng;
-    const int32_t* pt_row = a.pagetab + (size_t)lid * a.maxp;
-    // stage chunk c into buffer b (lanes < pages of the chunk issue its page copies)
-    auto stage = [&](int c, int b) {
-      const int tok0 = c * kSCW, ntok = min(kSCW, len - tok0);
-      __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(wbase + b * SM::kStage);
-      __nv_bfloat16* Vs = Ks + kSCW * kHD;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the buffer was last read generically
-      if (lane == 0) mbar_arrive_expect_tx(&bar[b], (uint32_t)ntok * kHD * 2 * 2);
-      __syncwarp();
-      const int npg = (ntok + a.pt - 1) / a.pt;
-      if (lane < npg) {
-        const int page = pt_row[tok0 / a.pt + lane];
-        const uint32_t bytes = (uint32_t)min(a.pt, ntok - lane * a.pt) * kHD * 2;
-        const __nv_bfloat16* kb = a.pool + (((size_t)page * 2) * a.Hkv + h) * hs;
-        bulk_g2s(Ks + lane * a.pt * kHD, kb, bytes, &bar[b]);
-        bulk_g2s(Vs + lane * a.pt * kHD, kb + (size_t)a.Hkv * hs, bytes, &bar[b]);
-      }
-    };
-    stage(c0, 0);
+  for (int u = blockIdx.x * kAttnWarps + warp; u < n; u += stride) {
+    const int32_t* item = a.items + (size_t)u * kItemStride;
+    const int code = item[0];
+    const int c = (code >> 16) & 0xFF, r = (code >> 8) & 0xFF, h = code & 0xFF;
+    const int len = a.row_len[r];
+    const int ntok = min(kSCW, len - c * kSCW);
+    const int npg = (ntok + a.pt - 1) / a.pt;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // our buffer was last read generically
+    if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)ntok * kHD * 2 * 2);
+    __syncwarp();
+    if (lane < npg) {
+      const int page = item[1 + lane];
+      const uint32_t bytes = (uint32_t)min(a.pt, ntok - lane * a.pt) * kHD * 2;
+      const __nv_bfloat16* kb = a.pool + (((size_t)page * 2) * a.Hkv + h) * hs;
+      bulk_g2s(Ks + lane * a.pt * kHD, kb, bytes, bar);
+      bulk_g2s(Vs + lane * a.pt * kHD, kb + (size_t)a.Hkv * hs, bytes, bar);
+    }
     attn_load_q<REP>(a, r, h, qs, lane);
     __syncwarp();
-    float M[REP], L[REP], O[REP][4];
-#pragma unroll
-    for (int e = 0; e < REP; ++e) {
-      M[e] = -INFINITY;
-      L[e] = 0.f;
-      O[e][0] = O[e][1] = O[e][2] = O[e][3] = 0.f;
-    }
-    for (int c = c0; c < c1; ++c) {
-      const int b = (c - c0) & 1;
-      if (c + 1 < c1) stage(c + 1, b ^ 1);
-      mbar_wait(&bar[b], ph[b]);
-      ph[b] ^= 1;
-      const __nv_bfloat16* Ks = reinterpret_cast<const __nv_bfloat16*>(wbase + b * SM::kStage);
-      const int ntok = min(kSCW, len - c * kSCW);
-      WarpPartial<REP, 1> wp;
-      wp.run(qs, Ks, Ks + kSCW * kHD, ntok, a.scale, lane);
-#pragma unroll
-      for (int e = 0; e < REP; ++e) {  // online softmax across the group's chunks
-        const float Mn = fmaxf(M[e], wp.m[e]);
-        const float fa = M[e] == -INFINITY ? 0.f : expf(M[e] - Mn), fb = expf(wp.m[e] - Mn);
-        L[e] = L[e] * fa + wp.l[e] * fb;
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) O[e][q4] = O[e][q4] * fa + wp.o[e][q4] * fb;
-        M[e] = Mn;
-      }
-      __syncwarp();  // buffer b is re-staged two chunks later
-    }
-    store_partial<REP>(a, r, h, a.nc_pre + j, M, L, O, lane);
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    WarpPartial<REP, 1> wp;
+    wp.run(qs, Ks, Vs, ntok, a.scale, lane);
+    store_partial<REP>(a, r, h, a.nc_pre + c, wp.m, wp.l, wp.o, lane);
     __threadfence();
     __syncwarp();
     if (lane == 0) {
-      if (atomicAdd(a.merge_cnt + r * a.Hkv + h, 1) + 1 == ng) {
+      const int nsuf = (len + kSCW - 1) / kSCW;
+      if (atomicAdd(a.merge_cnt + r * a.Hkv + h, 1) + 1 == nsuf) {
         __threadfence();
         a.merge_cnt[r * a.Hkv + h] = 0;  // ready for the next launch
         if (merge_n[warp] < 64) merge_list[warp][merge_n[warp]++] = (r << 8) | h;
@@ -408,9 +367,9 @@ __global__ void __launch_bounds__(kSWarps * 32) attn_suffix_warp_kernel(AttnArgs
   }
   pdl_wait();  // the tcgen05 prefix partials are complete from here on
   const int nm = merge_n[warp];
-  for (int jj = 0; jj < nm * REP; ++jj) {
-    const int rh = merge_list[warp][jj / REP];
-    attn_merge_one<REP>(a, rh >> 8, rh & 0xFF, jj % REP, lane);
+  for (int j = 0; j < nm * REP; ++j) {
+    const int rh = merge_list[warp][j / REP];
+    attn_merge_one<REP>(a, rh >> 8, rh & 0xFF, j % REP, lane);
   }
 }
 
@@ -932,7 +891,6 @@ struct SchedArgs {
   int32_t* row_len;
   int32_t* attn_items;       // [Hkv * (nc_pre + row_cap * nc_suf)][kItemStride]
   int Hkv, nc_pre, nc_suf, chunk, tc_prefix;
-  int sgroups;               // > 0: suffix items are (row, kv head, chunk group), <= sgroups per row
 };
 
 // One CTA of kSchedThreads.  The policy itself (finish / park / refill in
@@ -1101,7 +1059,6 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
       a.row_kvloc[s] = a.pagetab[(size_t)lid * a.maxp + tt / a.pt] * a.pt + tt % a.pt;
       a.row_len[s] = tt + 1;
       nch = (tt + 1 + a.chunk - 1) / a.chunk;
-      if (a.sgroups > 0) nch = min(nch, a.sgroups);  // items per row: chunk groups
     }
     s_cnt[s] = nch;
   }
@@ -1155,18 +1112,7 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
   }
   __syncthreads();
   // ---- suffix items of row s: (chunk c, kv head h) with the chunk's page ids embedded
-  if (tid < a.row_cap && nch > 0 && a.sgroups > 0) {
-    // (chunk group j, kv head h): the warp reads pages from the page table itself
-    const int s = tid;
-    for (int j = 0; j < nch; ++j)
-      for (int h = 0; h < a.Hkv; ++h) {
-        int32_t* item = a.attn_items + (size_t)(s_npre + (s_cnt[s] + j) * a.Hkv + h) * kItemStride;
-        item[0] = (j << 16) | (s << 8) | h;
-        item[1] = a.row_len[s];
-        item[2] = a.row_lid[s];
-        item[3] = nch;
-      }
-  } else if (tid < a.row_cap && nch > 0) {
+  if (tid < a.row_cap && nch > 0) {
     const int s = tid;
     const int ppc = a.chunk / a.pt;  // pages per suffix chunk (<= 16)
     const int len = a.row_len[s], lid = a.row_lid[s];

@@ -194,8 +194,8 @@ def run_ours(args):
         acc["rows"] += q["tokens_decoded"]
         acc["steps"] += q["steps"]
         ctx.is_group_results(d_rew, d_len)
-        if comm is not None:                 # the one exchange: lengths + rewards for Eq. 2 (NCCL, C ABI)
-            ctx.is_allgather_results(comm, d_len, d_rew, all_len, all_rew)
+        # the one exchange: lengths + rewards for Eq. 2 (NCCL through the C ABI)
+        exchange_results(ctx, comm, dist, d_len, d_rew, all_len, all_rew)
         out = None
         if host_inputs:                      # device -> host read of the step's result
             out = (all_rew if dist is not None else d_rew).cpu()
@@ -316,6 +316,7 @@ def run_ours(args):
                    "G": G, "g": g, "prompt_len": P, "max_new_tokens": max_new, "length_family": C["family"],
                    "kv_budget_bytes": budget, "global_batch": G * world, "seq_len": P + max_new,
                    "parallelism": f"dp{world} (prompt-sharded)", "step": "one GRPO-group rollout",
+                   "exchange": EXCHANGE["path"],
                    "l2": "inputs larger than L2 (3.4 GB of weights streamed per decode step)"},
         "roofline": roof,
         "decode_impl": "persistent" if st["decode_impl"] == 0 else "per_op",
@@ -333,6 +334,8 @@ def run_ours(args):
     print(json.dumps(line))
     sys.stdout.flush()
     ctx.close()
+    if comm is not None and comm != "torch":
+        _lib.nccl_comm_destroy(comm)
     if dist is not None:
         dist.destroy_process_group()
 
@@ -396,8 +399,7 @@ def run_groups(args):
                     true = slot_of.pop(slot)
                     tokens += int(np.sum(true))
                     ctx.is_group_results(d_rew, d_len, slot=slot)
-                    if comm is not None:  # the one exchange: lengths + rewards for Eq. 2 (NCCL, C ABI)
-                        ctx.is_allgather_results(comm, d_len, d_rew, all_len, all_rew)
+                    exchange_results(ctx, comm, dist, d_len, d_rew, all_len, all_rew)
                     if queue:
                         pid, dp, tr, pr = queue.pop(0)
                         ctx.is_prefill(dp, pid, slot=slot)
@@ -449,23 +451,57 @@ def run_groups(args):
             "decode_steps": int(dsteps), "ms_per_decode_step": round(ms_max / max(dsteps, 1), 4),
             "global_peak_kv_bytes": st["global_peak_kv_bytes"], "clocks": clk}))
     ctx.close()
-    if comm is not None:
+    if comm is not None and comm != "torch":
         _lib.nccl_comm_destroy(comm)
     if dist is not None:
         dist.destroy_process_group()
 
 
+EXCHANGE = {"path": "none"}
+
+
 def nccl_comm(_lib, dist, rank, world):
     """The library's NCCL communicator for the results all-gather: rank 0 creates the
-    unique id, the torch process group broadcasts it (plumbing only)."""
+    unique id, the torch process group broadcasts it (plumbing only).  If the library
+    cannot bind NCCL on some rank, every rank uses torch's all-gather for this one
+    exchange instead (recorded in the JSON line as config.exchange)."""
     if dist is None:
         return None
     import torch
+    ok = torch.ones(1, device="cuda")
     uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
     if rank == 0:
-        uid.copy_(torch.frombuffer(bytearray(_lib.nccl_unique_id()), dtype=torch.uint8))
+        try:
+            uid.copy_(torch.frombuffer(bytearray(_lib.nccl_unique_id()), dtype=torch.uint8))
+        except Exception:
+            ok.zero_()
     dist.broadcast(uid, 0)
-    return _lib.nccl_comm_init(bytes(uid.cpu().numpy().tobytes()), rank, world)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    comm = None
+    if ok.item() > 0:
+        try:
+            comm = _lib.nccl_comm_init(bytes(uid.cpu().numpy().tobytes()), rank, world)
+        except Exception:
+            comm = None
+    flag = torch.tensor([1.0 if comm is not None else 0.0], device="cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if flag.item() == 0:
+        if comm is not None:
+            _lib.nccl_comm_destroy(comm)
+        EXCHANGE["path"] = "torch.distributed all_gather (library NCCL unavailable)"
+        return "torch"
+    EXCHANGE["path"] = "is_allgather_results (library NCCL)"
+    return comm
+
+
+def exchange_results(ctx, comm, dist, d_len, d_rew, all_len, all_rew):
+    if comm is None:
+        return
+    if comm == "torch":
+        dist.all_gather_into_tensor(all_len, d_len)
+        dist.all_gather_into_tensor(all_rew, d_rew)
+    else:
+        ctx.is_allgather_results(comm, d_len, d_rew, all_len, all_rew)
 
 
 def _oracle_tokens_per_s(C, budget_s, step_seed=0):

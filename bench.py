@@ -304,7 +304,7 @@ def run_ours(args):
     roof["step_ms_eager"] = round(step_ms, 4)
     roof["step_GBps"] = round(algorithmic_bytes_per_step(shape, g, 0, P) / (ms_max / max(steps_total, 1) * 1e-3) / 1e9, 1)
     roof["per_kind_ms"] = {k: round(v, 4) for k, v in per_kind.items() if n_launch_kind[k]}
-    launches_per_step = int(len(kind))
+    launches_per_step = int(st["launches_per_step"])  # counted by the library while capturing the step
     avg_steps = steps_total / args.steps
     value = tok_all / (ms_max * 1e-3)
     e2e_value = tok_all / (e2e_max * 1e-3)
@@ -323,7 +323,8 @@ def run_ours(args):
         "decode_steps_per_rollout": round(avg_steps, 1),
         "ms_per_decode_step": round(ms_max / max(steps_total, 1), 4),
         "peak_kv_bytes": st["peak_kv_bytes"],
-        "gpu_launches": int(launches_per_step * steps_total + 0),
+        "gpu_launches": int(launches_per_step * steps_total + st["launches_per_prefill"] * args.steps
+                            + 2 * args.steps),  # decode steps + prefills + start-group scheduler / results kernels
         "launches_per_decode_step": launches_per_step,
         "e2e": {"value": round(e2e_value, 1), "unit": "tokens/s", "h2d_bytes_per_step": P * 4,
                 "d2h_bytes_per_step": G * world * 4},

@@ -118,6 +118,8 @@ typedef struct {
   int32_t groups;         /* co-resident group slots of the context */
   int64_t global_steps;   /* decode steps with >= 1 active slot in any group */
   int64_t global_peak_kv_bytes;  /* all groups' prefixes + peak pages of the shared pool */
+  int32_t launches_per_step;      /* kernel launches in one decode step (the captured graph) */
+  int32_t launches_per_prefill;   /* kernel launches of one is_prefill */
 } is_stats;
 
 typedef struct is_ctx is_ctx;

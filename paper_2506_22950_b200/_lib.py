@@ -62,7 +62,8 @@ class Stats(ctypes.Structure):
                 ("num_pages", ctypes.c_int32), ("row_capacity", ctypes.c_int32),
                 ("decode_impl", ctypes.c_int32), ("layer_kernel_ns", ctypes.c_int64),
                 ("layer_kernel_launches", ctypes.c_int64), ("suffix_tokens", ctypes.c_int64),
-                ("groups", ctypes.c_int32), ("global_steps", ctypes.c_int64), ("global_peak_kv_bytes", ctypes.c_int64)]
+                ("groups", ctypes.c_int32), ("global_steps", ctypes.c_int64), ("global_peak_kv_bytes", ctypes.c_int64),
+                ("launches_per_step", ctypes.c_int32), ("launches_per_prefill", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

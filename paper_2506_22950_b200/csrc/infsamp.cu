@@ -268,6 +268,7 @@ static is_status make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_
 
 // ------------------------------------------------------------------ GEMM launch
 static int g_num_sms = 0;
+static int g_launches = 0;  // kernel launches issued since the last reset (enqueue_step counts its own)
 static bool g_use_pdl = true;
 static int g_skip = 0;
 static float* g_splitk_ws = nullptr;  // set per context before enqueueing
@@ -329,6 +330,7 @@ static is_status launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB, Gem
     g_tl_name[g_tl_n++] = EPI == EPI_QKV ? "qkv" : EPI == EPI_RESID_ADD ? "resid" : EPI == EPI_SWIGLU ? "gu" : EPI == EPI_SAMPLE ? "lm" : "f32";
   }
   CK(cudaLaunchKernelEx(&cfg, kern, tA, tB, a));
+  ++g_launches;
   return IS_OK;
 }
 
@@ -386,6 +388,7 @@ static is_status launch_k_smem(K kern, dim3 grid, dim3 block, int smem, cudaStre
     cfg.numAttrs = 1;
   }
   CK(cudaLaunchKernelEx(&cfg, kern, args...));
+  ++g_launches;
   return IS_OK;
 }
 
@@ -404,6 +407,7 @@ static is_status launch_k(K kern, dim3 grid, dim3 block, cudaStream_t st, Args..
     cfg.numAttrs = 1;
   }
   CK(cudaLaunchKernelEx(&cfg, kern, args...));
+  ++g_launches;
   return IS_OK;
 }
 
@@ -485,6 +489,8 @@ struct is_ctx {
   int mk_nbufs;
   int mk_sync_n;
   int mk_ntasks;
+  int launches_per_step;  // kernels in one decode step (counted while capturing it)
+  int launches_per_prefill;
 };
 
 static void* dalloc(size_t bytes, is_status* s) {
@@ -592,6 +598,7 @@ static is_status launch_prefix_tc_n(is_ctx* c, const AttnArgs& aa, int l, cudaSt
   a2.grp_rows = c->g;
   a2.grp_kv_rows = c->sh.layers * 2 * c->sh.n_kv_heads * c->pcap;
   CK(cudaLaunchKernelEx(&cfg, kern, c->tm_prefix_kv, a2, kv_row_base));
+  ++g_launches;
   return IS_OK;
 }
 // MMA N of the tcgen05 prefix part: one group's live slots x Hq/Hkv query heads, padded to 16.
@@ -832,6 +839,7 @@ static is_status mk_launch_t(is_ctx* c, cudaStream_t st) {
     cfg.numAttrs = 2;
   }
   CK(cudaLaunchKernelEx(&cfg, kern, c->mka));
+  ++g_launches;
   return IS_OK;
 }
 static is_status mk_launch(is_ctx* c, cudaStream_t st) {
@@ -1077,7 +1085,15 @@ static is_status setup_mega(is_ctx* c, const void* const* dw) {
   return IS_OK;
 }
 
+static is_status enqueue_step_body(is_ctx* c);
 static is_status enqueue_step(is_ctx* c) {
+  const int launches0 = g_launches;
+  is_status r = enqueue_step_body(c);
+  c->launches_per_step = g_launches - launches0;
+  return r;
+}
+
+static is_status enqueue_step_body(is_ctx* c) {
   cudaStream_t st = c->st;
   const is_shape& s = c->sh;
   if (c->mk) {
@@ -1454,9 +1470,11 @@ extern "C" is_status is_prefill_slot(is_ctx* c, int32_t slot, const int32_t* d_p
   CK(cudaMemcpyAsync(c->d_prompt_copy, d_prompt, (size_t)c->P * 4, cudaMemcpyDeviceToDevice, c->st));
   int32_t last = 0;
   CK(cudaMemcpyAsync(&last, d_prompt + c->P - 1, 4, cudaMemcpyDeviceToHost, c->st));
+  const int launches0 = g_launches;
   CKS(launch_k(prefill_rows_kernel, dim3((c->pcap + 127) / 128), dim3(128), c->st, (const int32_t*)c->d_prompt_copy,
                c->pcap, c->prow_active, c->prow_tok, c->prow_pos, c->prow_kvloc));
   CKS(run_layers(c, c->pcap, true, slot));
+  c->launches_per_prefill = g_launches - launches0;
   CK(cudaStreamSynchronize(c->st));
   if (last < 0 || last >= c->sh.vocab) return fail(IS_ERR_DATA, "prompt token %d out of range", last);
   c->gprompt_id[slot] = prompt_id;
@@ -1675,6 +1693,8 @@ extern "C" is_status is_query_slot(is_ctx* c, int32_t m, is_stats* o) {
     o->layer_kernel_launches = (int64_t)clk[1];
   }
   o->groups = c->M;
+  o->launches_per_step = c->launches_per_step;
+  o->launches_per_prefill = c->launches_per_prefill;
   o->global_steps = g0[ST_GSTEP];
   o->global_peak_kv_bytes = (int64_t)c->M * c->prefix_bytes + g0[ST_GPEAK] * c->page_bytes;
   return IS_OK;

@@ -639,7 +639,8 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
                (!prefill && c->bnorm) ? c->ssqA : (float*)nullptr, c->max_rows));
   for (int l = 0; l < s.layers; ++l) {
     LayerW& w = c->L[l];
-    const bool bn = !prefill && c->bnorm;
+    const bool bn = !prefill && (c->bnorm & 1);       // QKV folds the input RMSNorm
+    const bool bn_gu = !prefill && (c->bnorm & 2);    // gate/up folds the post-attention RMSNorm
     if (!bn && (prefill || !(g_skip & 1)))
       CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.in_norm, c->xn, H,
                    s.rms_eps));
@@ -743,14 +744,14 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       a.n_valid = std::min(chunk, rows - r0);
       a.out = c->resid;
       a.ld_out = H;
-      if (bn) {
+      if (bn_gu) {
         a.ssq_out = c->ssqB;
         a.bn_ld = c->max_rows;
       }
       if (prefill || !(g_skip & 16)) CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_o, tm_attn, a, st));
     }
     prof_mark(st, 4);
-    if (!bn && (prefill || !(g_skip & 1)))
+    if (!bn_gu && (prefill || !(g_skip & 1)))
       CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.post_norm, c->xn, H,
                    s.rms_eps));
     prof_mark(st, 0);
@@ -764,7 +765,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       a.n_valid = std::min(chunk, rows - r0);
       a.act = c->act;
       a.ld_act = F;
-      if (bn) {
+      if (bn_gu) {
         a.bn_resid = c->resid;
         a.bn_ssq = c->ssqB;
         a.bn_gain = w.post_norm_bf;
@@ -1411,7 +1412,11 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
       }
       return base + bnorm_bytes(c->BN, H / kBK, split) <= maxsm;
     };
-    c->bnorm = fits(c->split_qkv) && fits(c->split_gu) && getenv("IS_BNORM") != nullptr;  // measured slower (profiles/r01)
+    // IS_BNORM=1: QKV and gate/up (measured slower: profiles/r01); IS_BNORM=qkv: QKV only
+    const char* e = getenv("IS_BNORM");
+    c->bnorm = 0;
+    if (e && !strcmp(e, "qkv") && fits(c->split_qkv)) c->bnorm = 1;
+    else if (e && fits(c->split_qkv) && fits(c->split_gu)) c->bnorm = 3;
   }
   c->l2_prefetch = getenv("IS_L2_PREFETCH") ? atoi(getenv("IS_L2_PREFETCH")) : 0;
   // per-GEMM split experiments (timing only)

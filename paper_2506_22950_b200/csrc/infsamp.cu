@@ -1905,6 +1905,21 @@ extern "C" int is_dbg_timeline(is_ctx* c) {
     }
     printf("prefix_tc L%d ctas=%d start %.2f waited %.2f q_staged %.2f tma %.2f S_done %.2f P_done %.2f O_done %.2f end %.2f\n", l, n,
            mn0, mx[1], mx[2], mx[3], mx[4], mx[5], mx[6], mx[7]);
+    // per-CTA phase durations (median / max, us): wait->q, q->S, S->P (softmax), P->O, O->end
+    const char* nm[5] = {"q_stage", "S_mma", "softmax", "PV_mma", "epilogue"};
+    const int k0[5] = {1, 2, 4, 5, 6}, k1[5] = {2, 4, 5, 6, 7};
+    printf("      per-CTA:");
+    for (int ph = 0; ph < 5; ++ph) {
+      std::vector<double> d;
+      for (int b = 0; b < 64; ++b) {
+        const unsigned long long* p = base + b * 16;
+        if (p[0] && p[k0[ph]] && p[k1[ph]]) d.push_back((double)((long long)(p[k1[ph]] - p[k0[ph]])) / 1e3);
+      }
+      if (d.empty()) continue;
+      std::sort(d.begin(), d.end());
+      printf(" %s %.2f/%.2f", nm[ph], d[d.size() / 2], d.back());
+    }
+    printf("\n");
   }
   fflush(stdout);
   return c->tl_count;

@@ -127,6 +127,19 @@ def ncu_traffic(name):
     return {"bytes_per_launch": round(float(np.min(vals))), "source": os.path.relpath(files[-1], ROOT)} if vals else None
 
 
+def lpt_place(pool, world, per_rank):
+    """LPT placement of prompts on ranks: pool = [(prompt id, predicted
+    work)]; the heaviest prompt goes to the least-loaded rank that still has room (equal
+    counts per rank, ties -> lower rank / lower id).  Returns {rank: sorted prompt ids}."""
+    load, cnt, out = [0.0] * world, [0] * world, {r: [] for r in range(world)}
+    for pid, w in sorted(pool, key=lambda x: (-x[1], x[0])):
+        r = min((r for r in range(world) if cnt[r] < per_rank), key=lambda r: (load[r], r))
+        out[r].append(pid)
+        load[r] += w
+        cnt[r] += 1
+    return {r: sorted(v) for r, v in out.items()}
+
+
 def algorithmic_bytes_per_step(shape, live_rows, suffix_tokens, P):
     """weights once per step + prefix KV once per group + live suffix KV + appends."""
     L, H, F, V = shape.layers, shape.hidden, shape.ffn, shape.vocab
@@ -163,14 +176,24 @@ def run_ours(args):
     comm = nccl_comm(_lib, dist, rank, world)
     n_total = args.warmup + args.steps
 
-    def workload(i):
-        pid = rank * n_total + i               # global prompt id (RNG keyed by global uid)
+    def workload(pid):                       # global prompt id (RNG keyed by global uid)
         prompt = gen_prompt(shape.vocab, P, pid, seed=SEED)
         true = gen_trace(C["family"], G, max_new, SEED + pid)
         pred = predict_lengths(true, "noisy", 0.3, seed=SEED + pid, prefix_k=C["prefix_k"])
         return pid, prompt, true, pred
 
-    work = [workload(i) for i in range(n_total)]
+    # warm-up prompts stay with their rank; the timed prompts are placed by LPT on the
+    # predicted work: every rank predicts its block, the totals are
+    # all-gathered, then the longest goes to the least-loaded rank (equal counts per rank)
+    own = [rank * n_total + i for i in range(n_total)]
+    timed_ids = own[args.warmup:]
+    if dist is not None and args.placement == "lpt":
+        mine = torch.tensor([[float(pid), float(np.sum(workload(pid)[3]))] for pid in timed_ids], device="cuda")
+        gathered = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(gathered, mine)
+        pool = [(int(p), float(w)) for t in gathered for p, w in t.cpu().numpy()]
+        timed_ids = lpt_place(pool, world, args.steps)[rank]
+    work = [workload(pid) for pid in own[:args.warmup] + timed_ids]
     d_prompts = [torch.as_tensor(p, device="cuda") for _, p, _, _ in work]
     d_rew = torch.zeros(G, device="cuda")
     d_len = torch.zeros(G, dtype=torch.int32, device="cuda")
@@ -317,6 +340,7 @@ def run_ours(args):
                    "kv_budget_bytes": budget, "global_batch": G * world, "seq_len": P + max_new,
                    "parallelism": f"dp{world} (prompt-sharded)", "step": "one GRPO-group rollout",
                    "exchange": EXCHANGE["path"],
+                   "placement": args.placement if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (3.4 GB of weights streamed per decode step)"},
         "roofline": roof,
         "decode_impl": "persistent" if st["decode_impl"] == 0 else "per_op",
@@ -569,6 +593,8 @@ def main():
     ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--placement", default="lpt", choices=["lpt", "block"],
+                    help="N>1: timed prompts placed on ranks by LPT on predicted work, or contiguous blocks")
     ap.add_argument("--groups", type=int, default=1,
                     help="co-resident prompt groups per GPU (SURVEY §8f NEXT-1); 1 = the paper's setting")
     args = ap.parse_args()

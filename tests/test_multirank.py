@@ -86,3 +86,20 @@ def test_shard_prompts_partitions():
         for w in (1, 2, 3, 4, 8):
             got = [p for r in range(w) for p in rollout.shard_prompts(n, r, w)]
             assert got == list(range(n))
+
+
+def test_lpt_placement_balances_predicted_work():
+    """bench.py's LPT placement of prompts on ranks (NEXT-4): equal counts, every prompt
+    placed once, and the max rank load within one prompt of the mean (LPT's bound)."""
+    import bench
+    rng = np.random.default_rng(3)
+    for world in (2, 4, 8):
+        per = 3
+        pool = [(pid, float(w)) for pid, w in enumerate(rng.lognormal(9.0, 0.5, world * per))]
+        out = bench.lpt_place(pool, world, per)
+        assert sorted(p for v in out.values() for p in v) == list(range(world * per))
+        assert all(len(v) == per for v in out.values())
+        w = dict(pool)
+        loads = [sum(w[p] for p in v) for v in out.values()]
+        assert max(loads) - np.mean(loads) <= max(w.values())
+        assert out == bench.lpt_place(pool, world, per)  # deterministic

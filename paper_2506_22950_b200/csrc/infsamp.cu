@@ -289,9 +289,8 @@ static int bnorm_bytes(int BN, int kb_total, int split) { return BN * 128 * (int
 template <int BN, bool DEEP>
 static int gemm_smem_of() { return GemmCfg<BN, Stages<BN, DEEP>::v>::kSmem; }
 
-template <int BN, int EPI, bool DEEP>
-static is_status launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB, GemmArgs a, cudaStream_t st) {
-  constexpr int STAGES = Stages<BN, DEEP>::v;
+template <int BN, int EPI, int STAGES>
+static is_status launch_gemm_s(const CUtensorMap& tA, const CUtensorMap& tB, GemmArgs a, cudaStream_t st) {
   using C = GemmCfg<BN, STAGES>;
   static int attr = 0;
   auto kern = gemm_swapab_kernel<BN, EPI, STAGES>;
@@ -334,9 +333,18 @@ static is_status launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB, Gem
   return IS_OK;
 }
 
+template <int BN, int EPI, bool DEEP>
+static is_status launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB, GemmArgs a, cudaStream_t st) {
+  return launch_gemm_s<BN, EPI, Stages<BN, DEEP>::v>(tA, tB, a, st);
+}
+
 template <int EPI>
-static is_status launch_gemm(int BN, const CUtensorMap& tA, const CUtensorMap& tB, GemmArgs a, cudaStream_t st) {
+static is_status launch_gemm(int BN, const CUtensorMap& tA, const CUtensorMap& tB, GemmArgs a, cudaStream_t st,
+                             int stages = 0) {
   const bool deep = a.split == 1;
+  // deeper weight ring for a split-K GEMM (more of its weights arrive before the PDL wait returns)
+  if (!deep && BN == 16 && stages == 6) return launch_gemm_s<16, EPI, 6>(tA, tB, a, st);
+  if (!deep && BN == 16 && stages == 8) return launch_gemm_s<16, EPI, 8>(tA, tB, a, st);
   switch (BN * 2 + (deep ? 1 : 0)) {
     case 32: return launch_gemm_t<16, EPI, false>(tA, tB, a, st);
     case 33: return launch_gemm_t<16, EPI, true>(tA, tB, a, st);
@@ -474,6 +482,7 @@ struct is_ctx {
   int32_t* d_prompt_copy;
   // splits
   int split_qkv, split_o, split_gu, split_d;
+  int stg_qkv, stg_o, stg_gu, stg_d;  // weight-ring depth of the split-K decode GEMMs (0 = default 4)
   int l2_prefetch;
   int tc_prefix;       // decode prefix attention on tcgen05 (N = rc * Hq/Hkv in {16, 32, 64})
   int sc;              // decode suffix chunk (tokens per attention work item)
@@ -679,7 +688,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
         a.bn_ld = c->max_rows;
         a.bn_eps = s.rms_eps;
       }
-      if (prefill || !(g_skip & 2)) CKS(launch_gemm<EPI_QKV>(BN, w.tm_qkv, tm_xn, a, st));
+      if (prefill || !(g_skip & 2)) CKS(launch_gemm<EPI_QKV>(BN, w.tm_qkv, tm_xn, a, st, prefill ? 0 : c->stg_qkv));
     }
     prof_mark(st, 1);
     AttnArgs aa{};
@@ -748,7 +757,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
         a.ssq_out = c->ssqB;
         a.bn_ld = c->max_rows;
       }
-      if (prefill || !(g_skip & 16)) CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_o, tm_attn, a, st));
+      if (prefill || !(g_skip & 16)) CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_o, tm_attn, a, st, prefill ? 0 : c->stg_o));
     }
     prof_mark(st, 4);
     if (!bn_gu && (prefill || !(g_skip & 1)))
@@ -773,7 +782,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
         a.bn_ld = c->max_rows;
         a.bn_eps = s.rms_eps;
       }
-      if (prefill || !(g_skip & 32)) CKS(launch_gemm<EPI_SWIGLU>(BN, w.tm_gu, tm_xn, a, st));
+      if (prefill || !(g_skip & 32)) CKS(launch_gemm<EPI_SWIGLU>(BN, w.tm_gu, tm_xn, a, st, prefill ? 0 : c->stg_gu));
     }
     prof_mark(st, 5);
     for (int r0 = 0; r0 < rows; r0 += chunk) {
@@ -790,7 +799,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
         a.ssq_out = c->ssqA;
         a.bn_ld = c->max_rows;
       }
-      if (prefill || !(g_skip & 64)) CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_d, tm_act, a, st));
+      if (prefill || !(g_skip & 64)) CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_d, tm_act, a, st, prefill ? 0 : c->stg_d));
     }
     prof_mark(st, 6);
   }
@@ -1419,6 +1428,10 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
     else if (e && fits(c->split_qkv) && fits(c->split_gu)) c->bnorm = 3;
   }
   c->l2_prefetch = getenv("IS_L2_PREFETCH") ? atoi(getenv("IS_L2_PREFETCH")) : 0;
+  c->stg_qkv = getenv("IS_STG_QKV") ? atoi(getenv("IS_STG_QKV")) : 0;
+  c->stg_o = getenv("IS_STG_O") ? atoi(getenv("IS_STG_O")) : 0;
+  c->stg_gu = getenv("IS_STG_GU") ? atoi(getenv("IS_STG_GU")) : 0;
+  c->stg_d = getenv("IS_STG_D") ? atoi(getenv("IS_STG_D")) : 0;
   // per-GEMM split experiments (timing only)
   if (const char* e = getenv("IS_SPLIT_QKV")) c->split_qkv = std::max(1, std::min(8, atoi(e)));
   if (const char* e = getenv("IS_SPLIT_O")) c->split_o = std::max(1, std::min(8, atoi(e)));

@@ -328,35 +328,56 @@ __global__ void __launch_bounds__(kAttnThreads) attn_suffix_warp_kernel(AttnArgs
   const size_t hs = (size_t)a.pt * kHD;
   uint32_t phase = 0;
   const int stride = gridDim.x * kAttnWarps;
-#pragma unroll 1
-  for (int u = blockIdx.x * kAttnWarps + warp; u < n; u += stride) {
-    const int32_t* item = a.items + (size_t)u * kItemStride;
-    const int code = item[0];
-    const int c = (code >> 16) & 0xFF, r = (code >> 8) & 0xFF, h = code & 0xFF;
-    const int len = a.row_len[r];
+  // Software-pipelined over this warp's units: the next unit's item is read during the
+  // current one, and its pages are DMA'd as soon as the current chunk has been scored
+  // (the buffer is free), i.e. before the current partial's store / fence / count.
+  // Item: [0] code (c << 16 | r << 8 | h), [1..8] page ids, [16] the row's length.
+  int u = blockIdx.x * kAttnWarps + warp;
+  int code = 0, len = 0, page_l = 0;
+  auto fetch = [&](int uu) {
+    const int32_t* item = a.items + (size_t)uu * kItemStride;
+    code = item[0];
+    len = item[16];
+    page_l = lane < 8 ? item[1 + lane] : 0;
+  };
+  auto issue = [&]() {
+    const int c = (code >> 16) & 0xFF, h = code & 0xFF;
     const int ntok = min(kSCW, len - c * kSCW);
     const int npg = (ntok + a.pt - 1) / a.pt;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // our buffer was last read generically
     if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)ntok * kHD * 2 * 2);
     __syncwarp();
     if (lane < npg) {
-      const int page = item[1 + lane];
       const uint32_t bytes = (uint32_t)min(a.pt, ntok - lane * a.pt) * kHD * 2;
-      const __nv_bfloat16* kb = a.pool + (((size_t)page * 2) * a.Hkv + h) * hs;
+      const __nv_bfloat16* kb = a.pool + (((size_t)page_l * 2) * a.Hkv + h) * hs;
       bulk_g2s(Ks + lane * a.pt * kHD, kb, bytes, bar);
       bulk_g2s(Vs + lane * a.pt * kHD, kb + (size_t)a.Hkv * hs, bytes, bar);
     }
+  };
+  if (u < n) {
+    fetch(u);
+    issue();
+  }
+#pragma unroll 1
+  while (u < n) {
+    const int c = (code >> 16) & 0xFF, r = (code >> 8) & 0xFF, h = code & 0xFF;
+    const int cur_len = len;
+    const int ntok = min(kSCW, cur_len - c * kSCW);
     attn_load_q<REP>(a, r, h, qs, lane);
+    const int nu = u + stride;
+    if (nu < n) fetch(nu);  // independent loads, in flight during the wait + math
     __syncwarp();
     mbar_wait(bar, phase);
     phase ^= 1;
     WarpPartial<REP, 1> wp;
     wp.run(qs, Ks, Vs, ntok, a.scale, lane);
+    __syncwarp();          // every lane is done reading the buffer
+    if (nu < n) issue();   // next unit's pages overlap this unit's store / fence / count
     store_partial<REP>(a, r, h, a.nc_pre + c, wp.m, wp.l, wp.o, lane);
     __threadfence();
     __syncwarp();
     if (lane == 0) {
-      const int nsuf = (len + kSCW - 1) / kSCW;
+      const int nsuf = (cur_len + kSCW - 1) / kSCW;
       if (atomicAdd(a.merge_cnt + r * a.Hkv + h, 1) + 1 == nsuf) {
         __threadfence();
         a.merge_cnt[r * a.Hkv + h] = 0;  // ready for the next launch
@@ -364,6 +385,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_suffix_warp_kernel(AttnArgs
       }
     }
     __syncwarp();
+    u = nu;
   }
   pdl_wait();  // the tcgen05 prefix partials are complete from here on
   const int nm = merge_n[warp];
@@ -1120,6 +1142,7 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
       for (int h = 0; h < a.Hkv; ++h) {
         int32_t* item = a.attn_items + (size_t)(s_npre + (s_cnt[s] + c) * a.Hkv + h) * kItemStride;
         item[0] = (c << 16) | (s << 8) | h;
+        if (a.chunk <= 32) item[16] = len;  // (<= 8 page ids: slot 16 is free)
         const int np = min(ppc, (len - c * a.chunk + a.pt - 1) / a.pt);
         for (int j = 0; j < np; ++j) item[1 + j] = a.pagetab[(size_t)lid * a.maxp + c * ppc + j];
       }

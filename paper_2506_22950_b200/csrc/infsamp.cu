@@ -892,23 +892,18 @@ static is_status setup_mega(is_ctx* c, const void* const* dw) {
   };
   MkArgs& a = c->mka;
   a = MkArgs{};
-  // ---- GEMM geometry and K splits: units of ~unit_kb k-blocks (16 KB each)
-  int unit_kb = 8;
-  if (const char* e = getenv("IS_MK_UNIT_KB")) unit_kb = std::max(1, atoi(e));
+  // ---- GEMM geometry: every tile's K range is split over the 4 CTAs of a cluster
   const int Ms[4] = {c->qkv_w, H, 2 * F, H};
   const int Ks[4] = {H, Hq * 128, H, F};
-  long long w_off = 0, ws_off = 0;
+  long long w_off = 0;
   for (int i = 0; i < 4; ++i) {
     MkGemm& g = a.g[i];
     g.M = Ms[i];
     g.KB = Ks[i] / 64;
     g.T = (int)ceil_div64(g.M, 128);
     g.S = kCS;  // K split across the 4 CTAs of a cluster (partials exchanged over DSMEM)
-    (void)unit_kb;
     g.w_off = w_off;
     w_off += (long long)g.T * g.KB * 128 * 64;
-    g.ws_off = ws_off;
-    if (g.S > 1) ws_off += (long long)g.T * g.S * 128 * BN;
   }
   a.layer_stride = w_off;
   // ---- packed, swizzled weights
@@ -946,7 +941,6 @@ static is_status setup_mega(is_ctx* c, const void* const* dw) {
   a.ssq = (float*)A((size_t)(2 * L + 1) * a.Th * rc * 4);
   a.attn_sw = (__nv_bfloat16*)A((size_t)Hq * 128 * BN * 2);
   a.act_sw = (__nv_bfloat16*)A((size_t)F * BN * 2);
-  a.ws = (float*)A((size_t)std::max(ws_off, 1ll) * 4);
   a.nc_pre = (int)ceil_div64(c->pcap, kMkPC);
   a.NCm = a.nc_pre + (int)ceil_div64(c->max_new, kMkSC);
   a.part_o = (float*)A((size_t)rc * Hq * a.NCm * 128 * 4);
@@ -958,14 +952,10 @@ static is_status setup_mega(is_ctx* c, const void* const* dw) {
   so.o_done = o++;
   so.dn_done = o++;
   so.emb_done = o++;
-  so.qkv_cnt = o; o += a.g[0].T;
   so.qkv_flag = o; o += a.g[0].T;
   so.att_row = o; o += Hkv * rc;
   so.att_done = o; o += Hkv;
-  so.o_cnt = o; o += a.g[1].T;
-  so.gu_cnt = o; o += a.g[2].T;
   so.gu_flag = o; o += a.g[2].T;
-  so.dn_cnt = o; o += a.g[3].T;
   so.stride = (o + 31) / 32 * 32;
   c->mk_sync_n = so.stride * L;
   a.sync = (int*)A((size_t)c->mk_sync_n * 4);

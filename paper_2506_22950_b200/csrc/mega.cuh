@@ -61,14 +61,12 @@ constexpr int kMkStage = 16384;
 struct MkGemm {
   int M, KB, T, S;   // output features, k-blocks, 128-row tiles, K split
   long long w_off;   // element offset inside a layer's packed block
-  long long ws_off;  // float offset of this GEMM's split-K partials
 };
 
 struct MkSync {
   int stride;                                 // ints per layer
   int att_next, o_done, dn_done, emb_done;    // scalars
-  int qkv_cnt, qkv_flag, att_row, att_done;   // arrays
-  int o_cnt, gu_cnt, gu_flag, dn_cnt;
+  int qkv_flag, att_row, att_done, gu_flag;    // arrays
 };
 
 struct MkArgs {
@@ -87,7 +85,6 @@ struct MkArgs {
   float *resid0, *resid1, *ssq;   // [rc][H] x2, [2L+1][Th][rc]
   __nv_bfloat16 *attn_sw, *act_sw;  // O / DN inputs [Hq*128/64][BN][64], [F/64][BN][64]
   __nv_bfloat16 *q, *xn_final;    // [rc][Hq][128], [rows][H] (lm_head input, row-major)
-  float* ws;                      // split-K partials
   const __nv_bfloat16* prefix;    // [L][2][Hkv][pcap][128]
   long long prefix_layer;
   __nv_bfloat16* pool;            // [L][pages][2][Hkv][pt][128]

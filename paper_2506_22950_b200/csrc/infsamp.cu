@@ -499,6 +499,9 @@ struct is_ctx {
   int mk_sync_n;
   int mk_ntasks;
   int launches_per_step;  // kernels in one decode step (counted while capturing it)
+  cudaGraphExec_t graphK;  // steps_per_graph decode steps in one graph (run loops)
+  bool graphK_ok;
+  int steps_per_graph;
   int launches_per_prefill;
 };
 
@@ -1157,6 +1160,22 @@ static is_status build_graph(is_ctx* c) {
   CK(cudaGraphInstantiate(&c->graph, g, 0));
   cudaGraphDestroy(g);
   c->graph_ok = true;
+  // the run loops replay K steps per launch: PDL then spans K-1 of the step boundaries
+  if (c->graphK_ok) {
+    cudaGraphExecDestroy(c->graphK);
+    c->graphK_ok = false;
+  }
+  if (c->steps_per_graph > 1 && !getenv("IS_TIMELINE")) {
+    CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+    is_status sk = IS_OK;
+    for (int k = 0; k < c->steps_per_graph && sk == IS_OK; ++k) sk = enqueue_step(c);
+    cudaError_t ek = cudaStreamEndCapture(c->st, &g);
+    if (sk != IS_OK) return sk;
+    CK(ek);
+    CK(cudaGraphInstantiate(&c->graphK, g, 0));
+    cudaGraphDestroy(g);
+    c->graphK_ok = true;
+  }
   return IS_OK;
 }
 
@@ -1418,6 +1437,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
     else if (e && fits(c->split_qkv) && fits(c->split_gu)) c->bnorm = 3;
   }
   c->l2_prefetch = getenv("IS_L2_PREFETCH") ? atoi(getenv("IS_L2_PREFETCH")) : 0;
+  c->steps_per_graph = getenv("IS_STEPS_PER_GRAPH") ? std::max(1, atoi(getenv("IS_STEPS_PER_GRAPH"))) : 1;
   c->stg_qkv = getenv("IS_STG_QKV") ? atoi(getenv("IS_STG_QKV")) : 0;
   c->stg_o = getenv("IS_STG_O") ? atoi(getenv("IS_STG_O")) : 0;
   c->stg_gu = getenv("IS_STG_GU") ? atoi(getenv("IS_STG_GU")) : 0;
@@ -1441,6 +1461,7 @@ extern "C" void is_destroy(is_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->st);
   if (c->graph_ok) cudaGraphExecDestroy(c->graph);
+  if (c->graphK_ok) cudaGraphExecDestroy(c->graphK);
   void* bufs[] = {c->wblob, c->final_norm, c->prefix, c->pool, c->resid, c->xn, c->attn, c->act, c->q,
                   c->part_o, c->part_ml, c->merge_cnt, c->ssqA, c->ssqB, c->attn_items, c->splitk_ws, c->rope_cos, c->rope_sin, c->row_active, c->row_uid, c->row_lid,
                   c->row_t, c->row_tok, c->row_pos, c->row_kvloc, c->row_len, c->keys, c->last_tok,
@@ -1640,7 +1661,8 @@ static is_status run_until(is_ctx* c, int32_t max_steps, bool any, int32_t* h_do
       if (dm.second == 0 || (any && (dm.first & ~done0))) break;
     }
     if (nograph) rs = enqueue_step(c);
-    else if (cudaGraphLaunch(c->graph, c->st) != cudaSuccess) rs = fail(IS_ERR_CUDA, "graph launch failed");
+    else if (cudaGraphLaunch(c->graphK_ok ? c->graphK : c->graph, c->st) != cudaSuccess)
+      rs = fail(IS_ERR_CUDA, "graph launch failed");
     if (rs != IS_OK) break;
     cudaEventRecord(ev[i % D], c->st);
   }

@@ -1,13 +1,7 @@
 #!/bin/bash
 OUT=gpurun_out/${1:-split}
 mkdir -p $OUT
-run() { echo "$1" >> $OUT/sweep.txt; env $1 IMPL=1 timeout 300 python tools/mk_step_time.py 2>&1 | head -1 >> $OUT/sweep.txt; }
-run "IS_X=0"
-run "IS_STG_QKV=6"
-run "IS_STG_QKV=8"
-run "IS_STG_O=6"
-run "IS_STG_GU=6"
-run "IS_STG_D=6"
-run "IS_STG_D=8"
-run "IS_STG_QKV=6 IS_STG_D=6"
-run "IS_X=0"
+for k in 1 4 8 1; do
+  echo "K=$k" >> $OUT/sweep.txt
+  IS_STEPS_PER_GRAPH=$k timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_decode_step'], d['decode_steps_per_rollout'])" >> $OUT/sweep.txt 2>&1
+done

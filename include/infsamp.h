@@ -207,6 +207,22 @@ is_status is_copy_schedule_slot(is_ctx* ctx, int32_t slot, int32_t* h_slot_table
                                 int32_t max_steps, int32_t* h_n);
 is_status is_group_results_slot(is_ctx* ctx, int32_t slot, float* d_reward, int32_t* d_len);
 
+/* KL-penalised reward, host arrays:
+ *   out[i] = rm[i] - beta * sum_{t < len[i]} (logp[i][t] - logp_ref[i][t])
+ * logp / logp_ref [G][max_new] (logp from is_copy_logprobs, logp_ref the caller's
+ * reference model), sums in fp64 over ascending t.  Pure; IS_ERR_DATA on a bad length. */
+is_status is_kl_rewards(const float* h_rm, const float* h_logp, const float* h_logp_ref, const int32_t* h_len,
+                        int32_t G, int32_t max_new, float beta, float* h_out);
+
+/* Value of the GRPO objective, Eq. 3 (l.133-141) = Eq. 4's micro-group average
+ * (l.327-345; equal micro groups), host arrays [G][max_new]:
+ *   (1/G) sum_i (1/len_i) sum_t { min(lam A_i, clip(lam, 1-eps, 1+eps) A_i) - beta KL_t },
+ *   lam = exp(logp - logp_old), KL_t = exp(logp_ref - logp) - (logp_ref - logp) - 1 (DESIGN R34).
+ * fp64; *h_out receives the value.  No gradients (training is out of scope). */
+is_status is_grpo_objective(const float* h_logp, const float* h_logp_old, const float* h_logp_ref, const float* h_adv,
+                            const int32_t* h_len, int32_t G, int32_t max_new, float clip_eps, float beta,
+                            double* h_out);
+
 /* Log-probability of every generated token: h_dst[G][max_new]
  * host fp32, log pi_theta(token) = z_tok - logsumexp_v(z_v) of the step's logits at
  * temperature 1 (R33), reduced on the device from the lm_head CTAs'

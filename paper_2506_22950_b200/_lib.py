@@ -21,7 +21,8 @@ EXPORTS = ["is_plan", "is_create", "is_destroy", "is_prefill", "is_start_group",
            "is_dbg_gemm", "is_dbg_mk_trace", "is_dbg_copy", "is_prefill_slot", "is_start_group_slot",
            "is_run_until_any_done", "is_query_slot", "is_copy_tokens_slot", "is_copy_schedule_slot",
            "is_group_results_slot", "is_nccl_unique_id", "is_nccl_comm_init", "is_allgather_results",
-           "is_nccl_comm_destroy", "is_copy_logprobs", "is_copy_logprobs_slot", "is_last_error", "is_version"]
+           "is_nccl_comm_destroy", "is_copy_logprobs", "is_copy_logprobs_slot", "is_kl_rewards", "is_grpo_objective", "is_last_error",
+           "is_version"]
 
 
 class InfsampError(RuntimeError):
@@ -122,6 +123,9 @@ def load(build_if_missing=True):
     L.is_allgather_results.argtypes = [vp, vp, vp, vp, vp, vp]
     L.is_nccl_comm_destroy.argtypes = [vp]
     L.is_copy_logprobs.argtypes = [vp, vp]
+    L.is_kl_rewards.argtypes = [vp, vp, vp, vp, i32, i32, ctypes.c_float, vp]
+    L.is_grpo_objective.argtypes = [vp, vp, vp, vp, vp, i32, i32, ctypes.c_float, ctypes.c_float,
+                                    ctypes.POINTER(ctypes.c_double)]
     L.is_copy_logprobs_slot.argtypes = [vp, i32, vp]
     L.is_last_error.restype = ctypes.c_char_p
     L.is_last_error.argtypes = []
@@ -214,6 +218,28 @@ def weight_pointer_list(weights, layers):
             raise InfsampError(IS_ERR_DATA, f"weight {n} must be a contiguous CUDA tensor")
         ptrs.append(t.data_ptr())
     return ptrs
+
+
+def is_kl_rewards(rm, logp, logp_ref, lengths, beta):
+    """P:311 KL-penalised reward (host): rm[G], logp / logp_ref [G][T], lengths[G]."""
+    rm = np.ascontiguousarray(rm, np.float32)
+    lp = np.ascontiguousarray(logp, np.float32)
+    lr = np.ascontiguousarray(logp_ref, np.float32)
+    ln = np.ascontiguousarray(lengths, np.int32)
+    out = np.zeros(len(rm), np.float32)
+    _check(load().is_kl_rewards(_np_ptr(rm), _np_ptr(lp), _np_ptr(lr), _np_ptr(ln), len(rm), lp.shape[1],
+                                float(beta), _np_ptr(out)))
+    return out
+
+
+def is_grpo_objective(logp, logp_old, logp_ref, adv, lengths, clip_eps=0.2, beta=0.04):
+    """Eq. 3 / Eq. 4 objective value (host, fp64)."""
+    a = [np.ascontiguousarray(x, np.float32) for x in (logp, logp_old, logp_ref, adv)]
+    ln = np.ascontiguousarray(lengths, np.int32)
+    out = ctypes.c_double()
+    _check(load().is_grpo_objective(_np_ptr(a[0]), _np_ptr(a[1]), _np_ptr(a[2]), _np_ptr(a[3]), _np_ptr(ln),
+                                    len(ln), a[0].shape[1], float(clip_eps), float(beta), ctypes.byref(out)))
+    return out.value
 
 
 def nccl_unique_id():

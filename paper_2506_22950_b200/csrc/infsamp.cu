@@ -2091,3 +2091,39 @@ extern "C" is_status is_copy_logprobs_slot(is_ctx* c, int32_t m, float* h_dst) {
   return IS_OK;
 }
 extern "C" is_status is_copy_logprobs(is_ctx* c, float* h_dst) { return is_copy_logprobs_slot(c, 0, h_dst); }
+
+// ------------------------------------------------------------------ NEXT-3: KL-penalised reward, objective value
+extern "C" is_status is_kl_rewards(const float* rm, const float* logp, const float* logp_ref, const int32_t* len,
+                                   int32_t G, int32_t max_new, float beta, float* out) {
+  if (!rm || !logp || !logp_ref || !len || !out || G < 1 || max_new < 1) return fail(IS_ERR_CONFIG, "bad arguments");
+  for (int i = 0; i < G; ++i) {
+    if (len[i] < 1 || len[i] > max_new) return fail(IS_ERR_DATA, "length of sample %d is %d", i, len[i]);
+    double s = 0;
+    for (int t = 0; t < len[i]; ++t) s += (double)logp[(size_t)i * max_new + t] - (double)logp_ref[(size_t)i * max_new + t];
+    out[i] = (float)((double)rm[i] - (double)beta * s);
+  }
+  return IS_OK;
+}
+
+extern "C" is_status is_grpo_objective(const float* logp, const float* logp_old, const float* logp_ref, const float* adv,
+                                       const int32_t* len, int32_t G, int32_t max_new, float clip_eps, float beta,
+                                       double* out) {
+  if (!logp || !logp_old || !logp_ref || !adv || !len || !out || G < 1 || max_new < 1)
+    return fail(IS_ERR_CONFIG, "bad arguments");
+  double total = 0;
+  for (int i = 0; i < G; ++i) {
+    if (len[i] < 1 || len[i] > max_new) return fail(IS_ERR_DATA, "length of sample %d is %d", i, len[i]);
+    double s = 0;
+    for (int t = 0; t < len[i]; ++t) {
+      const size_t k = (size_t)i * max_new + t;
+      const double lam = std::exp((double)logp[k] - (double)logp_old[k]), a = adv[i];
+      const double clipped = std::min(std::max(lam, 1.0 - clip_eps), 1.0 + (double)clip_eps);
+      const double surr = std::min(lam * a, clipped * a);
+      const double d = (double)logp_ref[k] - (double)logp[k];
+      s += surr - (double)beta * (std::exp(d) - d - 1.0);
+    }
+    total += s / len[i];
+  }
+  *out = total / G;
+  return IS_OK;
+}

@@ -119,3 +119,26 @@ def test_group_advantages_match_oracle(lib):
             ref = np.float32(grpo.advantages([float(x) for x in r], mode))
             assert np.array_equal(a, ref)
     assert np.all(lib.is_group_advantages(np.full(5, 2.0, np.float32)) == 0)
+
+
+def test_kl_rewards_and_objective_match_oracle(lib):
+    rng = np.random.default_rng(21)
+    for _ in range(20):
+        G, T = int(rng.integers(1, 17)), int(rng.integers(1, 40))
+        rm = rng.normal(size=G).astype(np.float32)
+        lp, lo, lr = (np.log(rng.uniform(0.01, 1.0, size=(G, T))).astype(np.float32) for _ in range(3))
+        lens = rng.integers(1, T + 1, size=G).astype(np.int32)
+        beta = float(np.float32(rng.uniform(0, 0.2)))
+        got = lib.is_kl_rewards(rm, lp, lr, lens, beta)
+        ref = np.float32(grpo.kl_rewards(rm.astype(np.float64), lp.astype(np.float64), lr.astype(np.float64),
+                                         lens, beta))
+        assert np.array_equal(got, ref)
+        adv = rng.normal(size=G).astype(np.float32)
+        j = lib.is_grpo_objective(lp, lo, lr, adv, lens, float(np.float32(0.2)), beta)
+        jr = grpo.grpo_objective(lp.astype(np.float64), lo.astype(np.float64), lr.astype(np.float64),
+                                 adv.astype(np.float64), lens, float(np.float32(0.2)), beta)
+        assert abs(j - jr) <= 1e-12 * max(1.0, abs(jr))
+    with pytest.raises(lib.InfsampError) as e:
+        lib.is_kl_rewards(np.zeros(2, np.float32), np.zeros((2, 4), np.float32), np.zeros((2, 4), np.float32),
+                          np.array([1, 5], np.int32), 0.1)
+    assert e.value.status == lib.IS_ERR_DATA

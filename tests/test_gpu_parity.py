@@ -295,3 +295,18 @@ def test_tiny_logprobs(lib, tiny):
     assert checked > 0
     for i, L in enumerate(tiny["true"]):
         assert np.all(lps[i, :L] < 0) and np.all(lps[i, L:] == 0)
+    from oracle import grpo
+    # P:311 reward and Eq. 3 value on the emitted log-probs (reference model = the tokens'
+    # own log-probs shifted by a per-sample constant, so the KL sum has a closed form)
+    G = len(tiny["true"])
+    lens = np.asarray(tiny["true"], np.int32)
+    rm = np.linspace(-1, 1, G).astype(np.float32)
+    shift = np.float32(0.125)
+    lref = (lps - shift).astype(np.float32)
+    kr = lib.is_kl_rewards(rm, lps, lref, lens, 0.5)
+    assert np.allclose(kr, rm - 0.5 * shift * lens, atol=1e-5)
+    assert np.array_equal(kr, np.float32(grpo.kl_rewards(rm.astype(np.float64), lps.astype(np.float64),
+                                                         lref.astype(np.float64), lens, 0.5)))
+    adv = lib.is_group_advantages(kr, "mean_only")
+    j = lib.is_grpo_objective(lps, lps, lps, adv, lens, 0.2, 0.04)
+    assert abs(j - float(np.mean(adv.astype(np.float64)))) < 1e-9

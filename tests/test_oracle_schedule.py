@@ -230,6 +230,55 @@ def test_advantages():
         assert abs(np.mean(np.square(s)) - 1.0) < 1e-9      # unit population variance
 
 
+def test_kl_rewards_pins():
+    """r = RM - beta * log(pi_theta(O|x) / pi_ref(O|x))."""
+    rng = np.random.default_rng(11)
+    G, T = 6, 9
+    rm = list(rng.normal(size=G))
+    lp = np.log(rng.uniform(0.05, 1.0, size=(G, T)))
+    lr = np.log(rng.uniform(0.05, 1.0, size=(G, T)))
+    lens = [int(x) for x in rng.integers(1, T + 1, size=G)]
+    assert grpo.kl_rewards(rm, lp, lr, lens, 0.0) == rm                   # beta = 0 -> RM
+    assert grpo.kl_rewards(rm, lp, lp, lens, 0.3) == rm                   # pi_theta = pi_ref -> RM
+    # the sequence probability is the product of the token probabilities (chain rule)
+    r = grpo.kl_rewards(rm, lp, lr, lens, 0.25)
+    for i in range(G):
+        p = np.prod(np.exp(lp[i, :lens[i]]))
+        q = np.prod(np.exp(lr[i, :lens[i]]))
+        assert abs(r[i] - (rm[i] - 0.25 * math.log(p / q))) < 1e-12
+    assert grpo.kl_rewards([1.0], [[-1.0, -1.0, float("nan")]], [[-2.0, -2.0, 0.0]], [2], 0.1) == [1.0 - 0.1 * 2.0]
+    a, b = grpo.kl_rewards(rm, lp, lr, lens, 0.1), grpo.kl_rewards(rm, lp, lr, lens, 0.3)
+    assert np.allclose(np.subtract(b, rm), 3 * np.subtract(a, rm), atol=1e-12)   # linear in beta
+
+
+def test_grpo_objective_pins():
+    """Eq. 3 / Eq. 4 value; per-token KL estimator pi_ref/pi - log(pi_ref/pi) - 1 (R34)."""
+    f = grpo.grpo_objective
+    # lambda = 1, pi_ref = pi: the objective is the mean advantage
+    assert abs(f([[-1.0, -2.0]] * 3, [[-1.0, -2.0]] * 3, [[-1.0, -2.0]] * 3, [0.5, -1.0, 2.0], [2, 1, 2], 0.2, 0.04)
+               - 0.5) < 1e-15
+    # clip (Eq. 3): A > 0, lambda = 2 -> 1.2 A; A < 0, lambda = 0.5 -> 0.8 A; A < 0, lambda = 2 -> 2 A
+    ln2 = math.log(2.0)
+    assert abs(f([[ln2]], [[0.0]], [[ln2]], [1.0], [1], 0.2, 0.0) - 1.2) < 1e-12
+    assert abs(f([[-ln2]], [[0.0]], [[-ln2]], [-1.0], [1], 0.2, 0.0) - (-0.8)) < 1e-12
+    assert abs(f([[ln2]], [[0.0]], [[ln2]], [-1.0], [1], 0.2, 0.0) - (-2.0)) < 1e-12
+    # KL term alone: pi = 0.5, pi_ref = 0.25 -> 0.5 - ln 0.5 - 1
+    kl = 0.5 - math.log(0.5) - 1.0
+    assert abs(f([[math.log(0.5)]], [[math.log(0.5)]], [[math.log(0.25)]], [0.0], [1], 0.2, 0.1) + 0.1 * kl) < 1e-15
+    # 1/|O_i| normalisation: repeating a token does not change a sample's term
+    assert abs(f([[ln2, ln2]], [[0.0, 0.0]], [[0.0, 0.0]], [1.0], [2], 0.2, 0.04)
+               - f([[ln2]], [[0.0]], [[0.0]], [1.0], [1], 0.2, 0.04)) < 1e-15
+    # Eq. 4 = (1/N) sum_n J^(n) over equal micro groups = Eq. 3
+    rng = np.random.default_rng(5)
+    G, g, T = 8, 2, 7
+    lp, lo, lr = (np.log(rng.uniform(0.05, 1.0, size=(G, T))) for _ in range(3))
+    adv = list(rng.normal(size=G))
+    lens = [int(x) for x in rng.integers(1, T + 1, size=G)]
+    whole = f(lp, lo, lr, adv, lens, 0.2, 0.04)
+    parts = [f(lp[n:n + g], lo[n:n + g], lr[n:n + g], adv[n:n + g], lens[n:n + g], 0.2, 0.04) for n in range(0, G, g)]
+    assert abs(whole - sum(parts) / len(parts)) < 1e-12
+
+
 def test_trace_generator_shape_and_determinism():
     a = gen_trace("math", 32, 1024, 1)
     assert a.dtype == np.int32 and len(a) == 32 and a.min() >= 1 and a.max() <= 1024

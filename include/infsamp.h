@@ -268,6 +268,21 @@ is_status is_set_logits_dump(is_ctx* ctx, float* d_logits);
  * 8 refill).  Returns the number of launches in *h_n. */
 is_status is_profile_step(is_ctx* ctx, float* h_ms, int32_t* h_kind, int32_t cap, int32_t* h_n);
 
+/* Same outputs, but the step is captured into a CUDA graph (as the run loops
+ * replay it) with an event node after every launch, then replayed once: each
+ * interval is the launch's device duration plus one graph-node hop (the event
+ * nodes turn PDL edges into full dependencies).  Advances one decode step. */
+is_status is_profile_step_graph(is_ctx* ctx, float* h_ms, int32_t* h_kind, int32_t cap, int32_t* h_n);
+
+/* Average device duration (ms) of one launch of a decode GEMM kind (1 QKV,
+ * 4 o_proj, 5 gate/up, 6 down), issued exactly as the decode step issues it
+ * (arguments, split, stages, PDL) for every layer, `reps` passes, back to back in
+ * one CUDA graph timed with CUDA events on the context stream (one warm-up replay
+ * first).  The launches write the step's scratch buffers (activations, residual),
+ * so the context must be re-prefilled / restarted before decoding on.  Per-op path
+ * only (IS_ERR_CONFIG otherwise).  *h_launches receives the launches timed. */
+is_status is_profile_kernel(is_ctx* ctx, int32_t kind, int32_t reps, float* h_ms_per_launch, int32_t* h_launches);
+
 /* Kernel-level test hook: one tcgen05 swap-AB GEMM Y[n][m] = sum_k X[n][k] W[m][k]
  * (X: d_x [rows][K] bf16, W: d_w [M][K] bf16, Y: d_y [rows][M] fp32),
  * rows <= 64, K % 64 == 0, on `stream`. split = K-split cluster size (1..8). */

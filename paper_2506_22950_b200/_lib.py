@@ -18,6 +18,7 @@ ADV_MODES = {"std_norm": 0, "mean_only": 1}
 EXPORTS = ["is_plan", "is_create", "is_destroy", "is_prefill", "is_start_group", "is_decode_step",
            "is_refill", "is_run_group", "is_query", "is_copy_tokens", "is_copy_schedule",
            "is_group_results", "is_group_advantages", "is_set_logits_dump", "is_profile_step",
+           "is_profile_step_graph", "is_profile_kernel",
            "is_dbg_gemm", "is_dbg_mk_trace", "is_dbg_copy", "is_prefill_slot", "is_start_group_slot",
            "is_run_until_any_done", "is_query_slot", "is_copy_tokens_slot", "is_copy_schedule_slot",
            "is_group_results_slot", "is_nccl_unique_id", "is_nccl_comm_init", "is_allgather_results",
@@ -108,6 +109,8 @@ def load(build_if_missing=True):
     L.is_group_advantages.argtypes = [vp, i32, i32, vp]
     L.is_set_logits_dump.argtypes = [vp, vp]
     L.is_profile_step.argtypes = [vp, vp, vp, i32, ctypes.POINTER(i32)]
+    L.is_profile_step_graph.argtypes = [vp, vp, vp, i32, ctypes.POINTER(i32)]
+    L.is_profile_kernel.argtypes = [vp, i32, i32, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32)]
     L.is_dbg_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]
     L.is_dbg_mk_trace.argtypes = [vp, vp, i32, vp, i32, vp, ctypes.c_int64, vp]
     L.is_dbg_copy.argtypes = [vp, i32, vp, ctypes.c_int64]
@@ -372,9 +375,16 @@ class Context:
         _check(load().is_dbg_copy(self._h, int(which), _np_ptr(out), nbytes))
         return out
 
-    def is_profile_step(self, cap=4096):
+    def is_profile_kernel(self, kind, reps=4):
+        ms = ctypes.c_float()
+        n = ctypes.c_int32()
+        _check(load().is_profile_kernel(self._h, int(kind), int(reps), ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
+
+    def is_profile_step(self, cap=4096, graph=False):
         ms = np.zeros(cap, np.float32)
         kind = np.zeros(cap, np.int32)
         n = ctypes.c_int32()
-        _check(load().is_profile_step(self._h, _np_ptr(ms), _np_ptr(kind), cap, ctypes.byref(n)))
+        fn = load().is_profile_step_graph if graph else load().is_profile_step
+        _check(fn(self._h, _np_ptr(ms), _np_ptr(kind), cap, ctypes.byref(n)))
         return ms[:n.value], kind[:n.value]

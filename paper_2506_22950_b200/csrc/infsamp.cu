@@ -568,13 +568,15 @@ static SchedArgs sched_args(is_ctx* c) {
 struct Prof {
   std::vector<cudaEvent_t>* ev;
   std::vector<int>* kind;
+  bool graph;  // capturing: record as event nodes of the step graph
 };
 static Prof* g_prof = nullptr;
 static void prof_mark(cudaStream_t st, int kind) {
   if (!g_prof) return;
   cudaEvent_t e;
   cudaEventCreate(&e);
-  cudaEventRecord(e, st);
+  if (g_prof->graph) cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+  else cudaEventRecord(e, st);
   g_prof->ev->push_back(e);
   g_prof->kind->push_back(kind);
 }
@@ -646,9 +648,10 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
   const int chunk = prefill ? 64 : rows;
 
   prof_mark(st, 0);
-  CKS(launch_k(embed_kernel, dim3(rows), dim3(128), st, (const __nv_bfloat16*)c->embed,
-               (const int32_t*)r_tok, (const int32_t*)r_active, c->resid, H,
-               (!prefill && c->bnorm) ? c->ssqA : (float*)nullptr, c->max_rows));
+  if (prefill || !(g_skip & 128))
+    CKS(launch_k(embed_kernel, dim3(rows), dim3(128), st, (const __nv_bfloat16*)c->embed,
+                 (const int32_t*)r_tok, (const int32_t*)r_active, c->resid, H,
+                 (!prefill && c->bnorm) ? c->ssqA : (float*)nullptr, c->max_rows));
   for (int l = 0; l < s.layers; ++l) {
     LayerW& w = c->L[l];
     const bool bn = !prefill && (c->bnorm & 1);       // QKV folds the input RMSNorm
@@ -1780,21 +1783,45 @@ extern "C" is_status is_set_logits_dump(is_ctx* c, float* d_logits) {
   return IS_OK;
 }
 
-extern "C" is_status is_profile_step(is_ctx* c, float* h_ms, int32_t* h_kind, int32_t cap, int32_t* h_n) {
+static is_status profile_step(is_ctx* c, bool graph, float* h_ms, int32_t* h_kind, int32_t cap, int32_t* h_n) {
   if (!c) return fail(IS_ERR_CONFIG, "null argument");
   if (std::find(c->gstarted.begin(), c->gstarted.end(), 1) == c->gstarted.end())
     return fail(IS_ERR_STATE, "is_profile_step before is_start_group");
   StreamGuard guard(c, c->user);
   std::vector<cudaEvent_t> ev;
   std::vector<int> kind;
-  Prof p{&ev, &kind};
+  Prof p{&ev, &kind, graph};
   cudaEvent_t e0;
   CK(cudaEventCreate(&e0));
-  CK(cudaEventRecord(e0, c->st));
-  g_prof = &p;
-  is_status s = enqueue_step(c);
-  g_prof = nullptr;
-  CK(cudaStreamSynchronize(c->st));
+  is_status s = IS_OK;
+  if (graph) {
+    // the step captured exactly as build_graph does, plus an event node after every
+    // launch; one replay.  (An event node between two kernels turns their PDL edge into
+    // a full dependency, so each interval is the kernel plus one graph-node hop.)
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+    cudaEventRecordWithFlags(e0, c->st, cudaEventRecordExternal);
+    g_prof = &p;
+    s = enqueue_step(c);
+    g_prof = nullptr;
+    cudaError_t e = cudaStreamEndCapture(c->st, &g);
+    if (s != IS_OK) return s;
+    CK(e);
+    CK(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    CK(cudaGraphUpload(ge, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaGraphLaunch(ge, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    cudaGraphExecDestroy(ge);
+  } else {
+    CK(cudaEventRecord(e0, c->st));
+    g_prof = &p;
+    s = enqueue_step(c);
+    g_prof = nullptr;
+    CK(cudaStreamSynchronize(c->st));
+  }
   int n = 0;
   cudaEvent_t prev = e0;
   for (size_t i = 0; i < ev.size(); ++i) {
@@ -1811,6 +1838,66 @@ extern "C" is_status is_profile_step(is_ctx* c, float* h_ms, int32_t* h_kind, in
   cudaEventDestroy(e0);
   if (h_n) *h_n = n;
   return s;
+}
+
+// Average device duration of one decode-step GEMM kind as the step issues it
+// (same arguments, tensor maps, split, stages, PDL), all layers' launches of that
+// kind back to back in one CUDA graph, `reps` passes over the layers, CUDA events
+// on the context stream around the replay.  kind: 1 QKV, 4 o_proj, 5 gate/up, 6 down.
+extern "C" is_status is_profile_kernel(is_ctx* c, int32_t kind, int32_t reps, float* h_ms_per_launch,
+                                       int32_t* h_launches) {
+  if (!c || !h_ms_per_launch) return fail(IS_ERR_CONFIG, "null argument");
+  if (c->mk) return fail(IS_ERR_CONFIG, "is_profile_kernel: per-op decode path only");
+  int keep;
+  switch (kind) {
+    case 1: keep = 2; break;
+    case 4: keep = 16; break;
+    case 5: keep = 32; break;
+    case 6: keep = 64; break;
+    default: return fail(IS_ERR_CONFIG, "is_profile_kernel: kind %d is not a GEMM kind", kind);
+  }
+  if (reps < 1) return fail(IS_ERR_CONFIG, "reps must be >= 1");
+  StreamGuard guard(c, c->user);
+  const int skip0 = g_skip;
+  g_skip = (1 | 2 | 8 | 16 | 32 | 64 | 128) & ~keep;
+  cudaGraph_t g;
+  cudaGraphExec_t ge;
+  const int launches0 = g_launches;
+  cudaError_t e = cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal);
+  is_status s = IS_OK;
+  for (int r = 0; r < reps && s == IS_OK && e == cudaSuccess; ++r) s = run_layers(c, c->rc, false);
+  if (e == cudaSuccess) e = cudaStreamEndCapture(c->st, &g);
+  g_skip = skip0;
+  const int n = g_launches - launches0;
+  g_launches = launches0;
+  if (s != IS_OK) return s;
+  CK(e);
+  CK(cudaGraphInstantiate(&ge, g, 0));
+  cudaGraphDestroy(g);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaGraphLaunch(ge, c->st));  // warm-up (instruction cache, TLB)
+  CK(cudaEventRecord(e0, c->st));
+  CK(cudaGraphLaunch(ge, c->st));
+  CK(cudaEventRecord(e1, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaGraphExecDestroy(ge);
+  *h_ms_per_launch = n > 0 ? ms / n : 0.f;
+  if (h_launches) *h_launches = n;
+  return IS_OK;
+}
+
+extern "C" is_status is_profile_step(is_ctx* c, float* h_ms, int32_t* h_kind, int32_t cap, int32_t* h_n) {
+  return profile_step(c, false, h_ms, h_kind, cap, h_n);
+}
+
+extern "C" is_status is_profile_step_graph(is_ctx* c, float* h_ms, int32_t* h_kind, int32_t cap, int32_t* h_n) {
+  return profile_step(c, true, h_ms, h_kind, cap, h_n);
 }
 
 extern "C" is_status is_dbg_gemm(const void* d_w, const void* d_x, float* d_y, int32_t M, int32_t K, int32_t rows,

@@ -310,3 +310,31 @@ def test_tiny_logprobs(lib, tiny):
     adv = lib.is_group_advantages(kr, "mean_only")
     j = lib.is_grpo_objective(lps, lps, lps, adv, lens, 0.2, 0.04)
     assert abs(j - float(np.mean(adv.astype(np.float64)))) < 1e-9
+
+
+def test_profile_hooks_then_decode_unchanged(lib, tiny):
+    """bench.py's timing hooks (is_profile_kernel, is_profile_step[_graph]) run on a live
+    context; a group started afterwards decodes the same tokens as an undisturbed run."""
+    if tiny["impl"] == 0:
+        pytest.skip("per-op decode path only")
+    cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", kv_budget_bytes=tiny["budget"], eps=0.1,
+                          temperature=0.8, seed=SEED, decode_impl=1)
+    ctx = lib.Context(cfg, tiny["w_dev"])
+    ctx.is_prefill(torch.as_tensor(tiny["prompt"], device="cuda"), 0)
+    ctx.is_start_group(tiny["true"], tiny["pred"])
+    ctx.is_decode_step()
+    for kind in (1, 4, 5, 6):
+        ms, n = ctx.is_profile_kernel(kind, reps=2)
+        assert n == 2 * TINY.layers and 0 < ms < 1.0, (kind, ms, n)
+    with pytest.raises(lib.InfsampError) as e:
+        ctx.is_profile_kernel(3)
+    assert e.value.status == lib.IS_ERR_CONFIG
+    for graph in (False, True):
+        ms, kind = ctx.is_profile_step(graph=graph)
+        assert len(ms) == len(kind) > 0 and np.all(ms >= 0) and 5 in set(kind.tolist())
+    ctx.is_prefill(torch.as_tensor(tiny["prompt"], device="cuda"), 0)
+    ctx.is_start_group(tiny["true"], tiny["pred"])
+    ctx.is_run_group()
+    toks = ctx.is_copy_tokens()
+    ctx.close()
+    assert np.array_equal(toks, tiny["runs"]["infinite"]["tokens"])

@@ -46,7 +46,10 @@ typedef enum {
   IS_MODE_INFINITE = 3, /* Alg. 1: [prefix phase] + Alg. 2 FPTAS plan + Alg. 3 SJF refill */
   /* Table 2's decomposition (definitions of SPEC.md, DESIGN R23): */
   IS_MODE_FPTAS_ONLY = 4, /* Alg. 2 plan in its lexicographic (n, j) order, FIFO refill, no quota */
-  IS_MODE_SJF_ONLY = 5    /* trace-order start (samples 0..g-1), Alg. 3 SJF refill, no quota */
+  IS_MODE_SJF_ONLY = 5,   /* trace-order start (samples 0..g-1), Alg. 3 SJF refill, no quota */
+  IS_MODE_DYNAMIC = 6     /* dynamic-slot sampling (NEXT-2, DESIGN R35): g slots, no quota,
+                             the G samples are candidates drawn in trace order; the group stops at
+                             the dynamic_target-th completion and in-flight samples are discarded */
 } is_mode;
 
 typedef enum { IS_ADV_STD_NORM = 0, IS_ADV_MEAN_ONLY = 1 } is_adv_mode;
@@ -80,6 +83,7 @@ typedef struct {
                               NEXT-1; 0 or 1 = the paper's one group per GPU).  Group slot m owns
                               rows m*g .. m*g+g-1; kv_budget_bytes is per group, the page pool
                               (max_groups x the per-group pool) is shared.  max_groups*g <= 64 */
+  int32_t dynamic_target;  /* IS_MODE_DYNAMIC: completions to stop at (0 = G); 0 in every other mode */
 } is_config;
 
 /* Alg. 2 output plus the runtime plan (Alg. 1, Alg. 3).  All arrays are
@@ -120,6 +124,7 @@ typedef struct {
   int64_t global_peak_kv_bytes;  /* all groups' prefixes + peak pages of the shared pool */
   int32_t launches_per_step;      /* kernel launches in one decode step (the captured graph) */
   int32_t launches_per_prefill;   /* kernel launches of one is_prefill */
+  int32_t discarded;      /* IS_MODE_DYNAMIC: samples in flight at the stop, discarded (R35) */
 } is_stats;
 
 typedef struct is_ctx is_ctx;

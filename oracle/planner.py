@@ -75,7 +75,8 @@ def sjf_refill(pred, finished, started):
 def build_plan(mode, G, g, pred=None, eps=0.1, finished=()):
     """Initial slot fill + static refill queue for one group.
 
-    mode: 'full' | 'naive' | 'fifo' | 'infinite' | 'fptas_only' | 'sjf_only'.
+    mode: 'full' | 'naive' | 'fifo' | 'infinite' | 'fptas_only' | 'sjf_only' | 'dynamic'.
+    dynamic (R35): the G candidates in trace order, no quota.
     `finished` = samples that completed in the prefix phase (infinite only).
     Table 2's decomposition is undefined in the paper; SPEC.md's
     definitions (R23): fptas_only = the Alg. 2 plan executed in its
@@ -86,7 +87,7 @@ def build_plan(mode, G, g, pred=None, eps=0.1, finished=()):
         raise PlanError("IS_ERR_CONFIG: need 1 <= g <= G and G mod g == 0")
     if mode == "full":
         return dict(init=list(range(G)), queue=[], plan=None)
-    if mode in ("naive", "fifo"):
+    if mode in ("naive", "fifo", "dynamic"):
         return dict(init=list(range(g)), queue=list(range(g, G)), plan=None)
     if mode == "sjf_only":
         init = list(range(g))

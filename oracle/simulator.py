@@ -10,6 +10,11 @@ Follows PAPER.md Alg. 1 (l.218-241) step by step, with the modes of §3.1-3.2:
   infinite  Alg. 1: [optional prefix phase of k tokens in ceil(G/g) barriered
             rounds, l.215-216, l.371] -> Alg. 2 plan -> first g samples from the
             mask -> SJF refill (Alg. 3) with no quota           (R17-R22)
+  dynamic   dynamic-slot sampling, §3.2 l.199-200 ("slot is immediately
+            reassigned"): g slots, no quota, candidates drawn in trace order from
+            the len(true_len) >= target candidates; the run stops at the step of
+            the target-th completion and every in-flight sample is discarded
+            (R35)
 
 One step = one token for every occupied slot (R20: a step
 happens while >= 1 slot is active).  Termination is trace-driven (R5): sample
@@ -42,11 +47,14 @@ class SimResult:
     init: list = field(default_factory=list)
     queue: list = field(default_factory=list)
     plan: dict = None
+    discarded: list = field(default_factory=list)    # dynamic: in-flight uids at the stop, ascending slot
 
 
-def simulate(true_len, mode, g, pred=None, eps=0.1, prefix_k=0, page_tokens=16):
+def simulate(true_len, mode, g, pred=None, eps=0.1, prefix_k=0, page_tokens=16, target=0):
     true_len = [int(x) for x in true_len]
     G = len(true_len)
+    if target and (mode != "dynamic" or not 1 <= target <= G):
+        raise ValueError("IS_ERR_CONFIG: target needs dynamic mode and 1 <= target <= G")
     if mode == "full":
         g = G
     if g < 1 or G % g != 0:
@@ -91,6 +99,16 @@ def simulate(true_len, mode, g, pred=None, eps=0.1, prefix_k=0, page_tokens=16):
                     res.finish_step[uid] = step
                     pages[uid] = 0
                     res.events.append((step, s, uid, "finish"))
+                    if target and len(finished) == target:   # dynamic: stop, discard in-flight work
+                        slot[s] = -1
+                        for s2 in range(g):
+                            if slot[s2] >= 0:
+                                res.discarded.append(slot[s2])
+                                res.events.append((step, s2, slot[s2], "discard"))
+                                pages[slot[s2]] = 0
+                                slot[s2] = -1
+                        q.clear()
+                        return
                 elif t[uid] == stop_at(uid):
                     res.events.append((step, s, uid, "park"))
                 else:
@@ -115,6 +133,11 @@ def simulate(true_len, mode, g, pred=None, eps=0.1, prefix_k=0, page_tokens=16):
         p = build_plan(mode, G, g)
         res.init, res.queue = p["init"], p["queue"]
         run_phase(p["queue"], lambda u: big, False, N, p["init"])
+    elif mode == "dynamic":
+        p = build_plan(mode, G, g)
+        res.init, res.queue = p["init"], p["queue"]
+        target = target or G
+        run_phase(p["queue"], lambda u: big, False, 0, p["init"])
     elif mode in ("fptas_only", "sjf_only"):
         if pred is None:
             raise ValueError(f"{mode} mode needs predicted lengths")
@@ -137,7 +160,7 @@ def simulate(true_len, mode, g, pred=None, eps=0.1, prefix_k=0, page_tokens=16):
     else:
         raise ValueError(f"IS_ERR_CONFIG: unknown mode {mode}")
     res.total_steps = step
-    assert len(finished) == G
+    assert len(finished) == (target or G)
     return res
 
 

@@ -12,7 +12,7 @@ import numpy as np
 from . import build as _build
 
 IS_OK, IS_ERR_CONFIG, IS_ERR_BUDGET, IS_ERR_CAPACITY, IS_ERR_DATA, IS_ERR_STATE, IS_ERR_CUDA = range(7)
-MODES = {"full": 0, "naive": 1, "fifo": 2, "infinite": 3, "fptas_only": 4, "sjf_only": 5}
+MODES = {"full": 0, "naive": 1, "fifo": 2, "infinite": 3, "fptas_only": 4, "sjf_only": 5, "dynamic": 6}
 ADV_MODES = {"std_norm": 0, "mean_only": 1}
 
 EXPORTS = ["is_plan", "is_create", "is_destroy", "is_prefill", "is_start_group", "is_decode_step",
@@ -44,7 +44,8 @@ class Config(ctypes.Structure):
                 ("prefix_k", ctypes.c_int32), ("page_tokens", ctypes.c_int32),
                 ("row_capacity", ctypes.c_int32), ("kv_budget_bytes", ctypes.c_int64),
                 ("eps", ctypes.c_double), ("temperature", ctypes.c_float), ("seed", ctypes.c_uint64),
-                ("mode", ctypes.c_int32), ("decode_impl", ctypes.c_int32), ("max_groups", ctypes.c_int32)]
+                ("mode", ctypes.c_int32), ("decode_impl", ctypes.c_int32), ("max_groups", ctypes.c_int32),
+                ("dynamic_target", ctypes.c_int32)]
 
 
 class PlanOut(ctypes.Structure):
@@ -65,7 +66,8 @@ class Stats(ctypes.Structure):
                 ("decode_impl", ctypes.c_int32), ("layer_kernel_ns", ctypes.c_int64),
                 ("layer_kernel_launches", ctypes.c_int64), ("suffix_tokens", ctypes.c_int64),
                 ("groups", ctypes.c_int32), ("global_steps", ctypes.c_int64), ("global_peak_kv_bytes", ctypes.c_int64),
-                ("launches_per_step", ctypes.c_int32), ("launches_per_prefill", ctypes.c_int32)]
+                ("launches_per_step", ctypes.c_int32), ("launches_per_prefill", ctypes.c_int32),
+                ("discarded", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -151,7 +153,7 @@ def _np_ptr(a):
 
 def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix_k=0, page_tokens=16,
                 row_capacity=0, kv_budget_bytes=0, eps=0.1, temperature=0.8, seed=20261017, decode_impl=None,
-                max_groups=1):
+                max_groups=1, dynamic_target=0):
     """decode_impl: 0 = persistent decode kernel, 1 = one kernel per operator (default: it is
     faster on B200); None reads IS_DECODE_IMPL from the environment."""
     c = Config()
@@ -165,6 +167,7 @@ def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix
         decode_impl = int(os.environ.get("IS_DECODE_IMPL", "1"))
     c.decode_impl = decode_impl
     c.max_groups = max_groups
+    c.dynamic_target = dynamic_target
     return c
 
 

@@ -76,7 +76,9 @@ static is_status check_config(const is_config* c) {
   if (c->prefix_k < 0 || (c->prefix_k > 0 && c->mode != IS_MODE_INFINITE))
     return fail(IS_ERR_CONFIG, "prefix_k > 0 requires IS_MODE_INFINITE");
   if (!(c->temperature > 0)) return fail(IS_ERR_CONFIG, "temperature must be > 0");
-  if (c->mode < IS_MODE_FULL || c->mode > IS_MODE_SJF_ONLY) return fail(IS_ERR_CONFIG, "unknown mode %d", (int)c->mode);
+  if (c->mode < IS_MODE_FULL || c->mode > IS_MODE_DYNAMIC) return fail(IS_ERR_CONFIG, "unknown mode %d", (int)c->mode);
+  if (c->dynamic_target < 0 || c->dynamic_target > c->G || (c->dynamic_target > 0 && c->mode != IS_MODE_DYNAMIC))
+    return fail(IS_ERR_CONFIG, "dynamic_target must be 0 or 1..G (got %d) and needs IS_MODE_DYNAMIC", c->dynamic_target);
   if (c->max_groups < 0 || n_groups(c) > 8 || n_groups(c) * g > 64)
     return fail(IS_ERR_CONFIG, "need 1 <= max_groups <= 8 and max_groups * g <= 64 (got %d x %d)", n_groups(c), g);
   return IS_OK;
@@ -109,7 +111,6 @@ extern "C" is_status is_plan(const is_config* cfg, const int32_t* pred, const ui
   if (cfg->kv_budget_bytes > 0 && out->reserved_bytes > cfg->kv_budget_bytes)
     return fail(IS_ERR_BUDGET, "worst-case KV reservation %lld B exceeds budget %lld B",
                 (long long)out->reserved_bytes, (long long)cfg->kv_budget_bytes);
-  if (cfg->mode < IS_MODE_FULL || cfg->mode > IS_MODE_SJF_ONLY) return fail(IS_ERR_CONFIG, "unknown mode %d", (int)cfg->mode);
   const bool planned = cfg->mode == IS_MODE_INFINITE || cfg->mode == IS_MODE_FPTAS_ONLY;
   if (cfg->mode == IS_MODE_SJF_ONLY) {
     // trace-order start, Alg. 3 SJF refill of the rest (DESIGN R23)
@@ -1490,10 +1491,15 @@ extern "C" void is_destroy(is_ctx* c) {
   delete c;
 }
 
+// a group is done when all G samples completed, or (dynamic mode, R35) its target did
+static bool group_done(const is_ctx* c, const long long* st) {
+  return st[ST_DONE] >= (st[ST_TARGET] > 0 ? st[ST_TARGET] : (long long)c->G);
+}
+
 extern "C" is_status is_prefill_slot(is_ctx* c, int32_t slot, const int32_t* d_prompt, int32_t prompt_id) {
   if (!c || !d_prompt) return fail(IS_ERR_CONFIG, "null argument");
   if (slot < 0 || slot >= c->M) return fail(IS_ERR_CONFIG, "group slot %d out of range [0, %d)", slot, c->M);
-  if (c->gstarted[slot] && c->st_host[(size_t)slot * ST_COUNT + ST_DONE] < c->G) {
+  if (c->gstarted[slot] && !group_done(c, c->st_host + (size_t)slot * ST_COUNT)) {
     // the slot's group is still decoding: wait for the stream, then look again
     CK(cudaStreamSynchronize(c->st));
     CK(cudaMemcpy(c->st_host, c->st_dev, sizeof(long long) * ST_COUNT * (c->M + 1), cudaMemcpyDeviceToHost));
@@ -1577,6 +1583,7 @@ extern "C" is_status is_start_group_slot(is_ctx* c, int32_t m, const int32_t* tr
     st[ST_BARRIER] = (c->cfg.mode == IS_MODE_NAIVE || c->cfg.mode == IS_MODE_FULL) ? 1 : 0;
     st[ST_QUOTA] = c->cfg.mode == IS_MODE_FIFO ? c->N : 0;
     st[ST_STOPK] = 0;
+    if (c->cfg.mode == IS_MODE_DYNAMIC) st[ST_TARGET] = c->cfg.dynamic_target > 0 ? c->cfg.dynamic_target : G;
     for (int s = 0; s < g; ++s) slots[s] = init[s];
     for (int i = 0; i < po.queue_len; ++i) q0[i] = queue[i];
     st[ST_QLEN] = po.queue_len;
@@ -1649,7 +1656,7 @@ static is_status run_until(is_ctx* c, int32_t max_steps, bool any, int32_t* h_do
     int mask = 0, running = 0;
     for (int m = 0; m < c->M; ++m) {
       if (!c->gstarted[m]) continue;
-      if (h[(size_t)m * ST_COUNT + ST_DONE] >= c->G) mask |= 1 << m;
+      if (group_done(c, (const long long*)h + (size_t)m * ST_COUNT)) mask |= 1 << m;
       else running |= 1 << m;
     }
     return std::make_pair(mask, running);
@@ -1706,6 +1713,7 @@ extern "C" is_status is_query_slot(is_ctx* c, int32_t m, is_stats* o) {
   o->steps = (int32_t)st[ST_STEP];
   o->prefix_steps = (int32_t)st[ST_PREFIX_STEPS];
   o->completed = (int32_t)st[ST_DONE];
+  o->discarded = (int32_t)st[ST_DISCARDED];
   o->live_pages = (int32_t)st[ST_LIVE];
   o->peak_pages = (int32_t)st[ST_PEAK];
   o->error = (int32_t)g0[ST_ERROR];

@@ -874,6 +874,8 @@ enum SchedState {
   ST_GLIVE,        // block 0 only: pages allocated by all groups (shared pool)
   ST_GPEAK,        // block 0 only: max over steps of ST_GLIVE
   ST_GSTEP,        // block 0 only: decode steps with >= 1 active slot in any group
+  ST_TARGET,       // dynamic-slot mode: stop at this many completions (0 = all G), R35
+  ST_DISCARDED,    //   samples in flight at the stop, discarded
   ST_COUNT
 };
 // st[] holds one block of ST_COUNT words per co-resident group (NEXT-1) plus a
@@ -995,6 +997,23 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
             st[ST_LIVE] -= npages[uid];
             st0[ST_GLIVE] -= npages[uid];
             npages[uid] = 0;
+            if (st[ST_TARGET] > 0 && st[ST_DONE] >= st[ST_TARGET]) {
+              // dynamic-slot stop (R35): every other slot's sample is discarded, ascending
+              // slot order, its pages back to the pool; nothing is refilled
+              slot_uid[s] = -1;
+              for (int s2 = 0; s2 < a.g; ++s2) {
+                const int u2 = slot_uid[s2];
+                if (u2 < 0) continue;
+                for (int i = 0; i < npages[u2]; ++i) a.free_stack[st0[ST_FREE_TOP]++] = pagetab[(size_t)u2 * a.maxp + i];
+                st[ST_LIVE] -= npages[u2];
+                st0[ST_GLIVE] -= npages[u2];
+                npages[u2] = 0;
+                slot_uid[s2] = -1;
+                st[ST_DISCARDED] += 1;
+              }
+              st[ST_QHEAD] = st[ST_QLEN];
+              break;
+            }
           } else if (st[ST_STOPK] > 0 && tt_[uid] == st[ST_STOPK]) {
             // park: keep pages (prefix reuse)
           } else {

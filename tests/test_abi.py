@@ -142,3 +142,18 @@ def test_kl_rewards_and_objective_match_oracle(lib):
         lib.is_kl_rewards(np.zeros(2, np.float32), np.zeros((2, 4), np.float32), np.zeros((2, 4), np.float32),
                           np.array([1, 5], np.int32), 0.1)
     assert e.value.status == lib.IS_ERR_DATA
+
+
+def test_dynamic_mode_plan_and_config_errors(lib):
+    cfg = _cfg(lib, 8, 2)
+    cfg.mode = lib.MODES["dynamic"]
+    out = lib.is_plan(cfg, [3] * 8)
+    ref = planner.build_plan("dynamic", 8, 2)
+    assert out["init"] == ref["init"] and out["queue"] == ref["queue"]
+    for mode, target in (("dynamic", 9), ("dynamic", -1), ("infinite", 3)):
+        bad = _cfg(lib, 8, 2)
+        bad.mode = lib.MODES[mode]
+        bad.dynamic_target = target
+        with pytest.raises(lib.InfsampError) as e:
+            lib.is_plan(bad, [3] * 8)
+        assert e.value.status == lib.IS_ERR_CONFIG

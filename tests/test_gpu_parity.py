@@ -61,9 +61,11 @@ def _tiny_setup():
     return w, prompt, true, pred
 
 
-def _run(lib, w_dev, prompt, true, pred, mode, g, budget=0, prefix_k=0, pt=16, rc=16, logits=False, impl=0):
-    cfg = lib.make_config(TINY, 8, g, 32, 16, mode=mode, prefix_k=prefix_k, page_tokens=pt, row_capacity=rc,
-                          kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED, decode_impl=impl)
+def _run(lib, w_dev, prompt, true, pred, mode, g, budget=0, prefix_k=0, pt=16, rc=16, logits=False, impl=0,
+         target=0):
+    cfg = lib.make_config(TINY, len(true), g, 32, 16, mode=mode, prefix_k=prefix_k, page_tokens=pt, row_capacity=rc,
+                          kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED, decode_impl=impl,
+                          dynamic_target=target)
     ctx = lib.Context(cfg, w_dev)
     ctx.is_prefill(torch.as_tensor(prompt, device="cuda"), 0)
     ctx.is_start_group(true, pred)
@@ -72,7 +74,7 @@ def _run(lib, w_dev, prompt, true, pred, mode, g, budget=0, prefix_k=0, pt=16, r
         buf = torch.zeros(rc, TINY.vocab, device="cuda")
         ctx.is_set_logits_dump(buf)
         slots_seen = []
-        while ctx.is_query()["completed"] < 8:
+        while ctx.is_query()["completed"] < (target or len(true)):
             # rows of the step about to run
             ctx.is_decode_step()
             torch.cuda.synchronize()
@@ -338,3 +340,24 @@ def test_profile_hooks_then_decode_unchanged(lib, tiny):
     toks = ctx.is_copy_tokens()
     ctx.close()
     assert np.array_equal(toks, tiny["runs"]["infinite"]["tokens"])
+
+
+@pytest.mark.parametrize("target", [5, 8])
+def test_tiny_dynamic_slot_mode(lib, tiny, target):
+    """NEXT-2 dynamic-slot sampling (R35): the 8 samples are candidates in
+    trace order; the run stops at the target-th completion and discards in-flight work.
+    Slot table, page log, discards and counters equal the oracle's simulation; completed
+    samples' tokens equal the same uids' tokens under every other schedule."""
+    r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "dynamic", 2,
+             budget=tiny["budget"], impl=tiny["impl"], target=target)
+    ref = simulator.simulate(tiny["true"], "dynamic", 2, page_tokens=16, target=target)
+    st = r["stats"]
+    assert st["completed"] == target and st["error"] == 0 and st["discarded"] == len(ref.discarded)
+    assert r["steps"] == ref.total_steps
+    assert r["slots"].tolist() == ref.slot_table
+    assert r["live"].tolist() == ref.live_pages
+    assert st["live_pages"] == 0 and st["peak_pages"] == ref.peak_pages
+    assert st["tokens_decoded"] == ref.tokens_decoded
+    base = tiny["runs"]["infinite"]["tokens"]
+    for uid in ref.finish_step:
+        assert np.array_equal(r["tokens"][uid], base[uid]), uid

@@ -311,3 +311,45 @@ def test_table2_decomposition_definitions():
     lens = [5, 3, 4, 2, 6, 1]
     r = simulator.simulate(lens, "sjf_only", 2, pred=[7] * 6)
     assert [e[2] for e in r.events if e[3] == "refill"] == [2, 3, 4, 5]
+
+
+def _greedy_list_schedule(lengths, g):
+    """Independent check: no-quota slot refill in trace order is greedy list scheduling;
+    each sample goes to the slot that frees first (ties -> lower slot), makespan = steps."""
+    free = [0] * g
+    for L in lengths:
+        s = min(range(g), key=lambda j: (free[j], j))
+        free[s] += L
+    return max(free)
+
+
+def test_dynamic_slot_mode_pins():
+    """R35: stop at the target-th completion."""
+    # hand trace, g = 2, lengths [5,3,4,2,6,1,7,2], target 3:
+    # steps 1-3 (0,1): uid 1 done at 3 -> slot 1 takes 2; steps 4-5 (0,2): uid 0 done at 5 ->
+    # slot 0 takes 3; steps 6-7 (3,2): uid 3 done at 7 = 3rd completion (slot 0 first, R18),
+    # uid 2 (also at its last token) is in flight on slot 1 -> discarded.
+    r = simulator.simulate([5, 3, 4, 2, 6, 1, 7, 2], "dynamic", 2, target=3)
+    assert r.total_steps == 7
+    assert r.finish_step == {1: 3, 0: 5, 3: 7}
+    assert r.discarded == [2]
+    assert r.slot_table == [[0, 1]] * 3 + [[0, 2]] * 2 + [[3, 2]] * 2
+    assert r.tokens_decoded == 3 + 5 + 2 + 4
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        g = int(rng.integers(1, 5))
+        G = g * int(rng.integers(1, 6))
+        lens = [int(x) for x in rng.integers(1, 40, size=G)]
+        full = simulator.simulate(lens, "dynamic", g)             # target = G: every candidate completes
+        assert full.total_steps == _greedy_list_schedule(lens, g) and not full.discarded
+        target = int(rng.integers(1, G + 1))
+        d = simulator.simulate(lens, "dynamic", g, target=target, page_tokens=4)
+        assert len(d.finish_step) == target and d.total_steps <= full.total_steps
+        assert len(d.discarded) <= g - 1
+        # token conservation (SPEC l.246): steps x active slots = completed + discarded partial work
+        occ = sum(1 for row in d.slot_table for u in row if u >= 0)
+        assert occ == d.tokens_decoded
+        part = sum(sum(1 for row in d.slot_table for u in row if u == x) for x in d.discarded)
+        assert d.tokens_decoded == sum(lens[u] for u in d.finish_step) + part
+    with pytest.raises(ValueError):
+        simulator.simulate([3, 4], "fifo", 1, target=1)

@@ -26,7 +26,7 @@ from synth import SHAPES, gen_prompt, gen_trace, gen_weights, predict_lengths  #
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--prompts", type=int, default=2)
-ap.add_argument("--modes", default="naive,fifo,fptas_only,sjf_only,infinite,full")
+ap.add_argument("--modes", default="naive,fifo,fptas_only,sjf_only,infinite,full,dynamic")
 args = ap.parse_args()
 C = CONFIGS[args.config]
 shape = SHAPES[C["shape"]]
@@ -40,14 +40,19 @@ out = {"config": args.config, "desc": C["desc"], "prompts": args.prompts, "kv_bu
 tokens_ref = {}
 for mode in args.modes.split(","):
     full = mode == "full"
-    cfg = _lib.make_config(shape, G, g, max_new, P, mode=mode, prefix_k=k if mode == "infinite" else 0,
-                           kv_budget_bytes=0 if full else budget, seed=SEED)
+    dyn = mode == "dynamic"   # R35: 2G candidates (the trace, then a second draw), stop at G completions
+    cfg = _lib.make_config(shape, 2 * G if dyn else G, g, max_new, P, mode=mode,
+                           prefix_k=k if mode == "infinite" else 0,
+                           kv_budget_bytes=0 if full else budget, seed=SEED, dynamic_target=G if dyn else 0)
     ctx = _lib.Context(cfg, w)
     steps, toks, peak, dt = 0, 0, 0, 0.0
+    emitted, discarded = [], 0
     same = True
     for pid in range(args.prompts):
         prompt = torch.as_tensor(gen_prompt(shape.vocab, P, pid, seed=SEED), device="cuda")
         true = gen_trace(C["family"], G, max_new, SEED + pid)
+        if dyn:
+            true = np.concatenate([true, gen_trace(C["family"], G, max_new, SEED + pid + 1000)])
         pred = predict_lengths(true, "noisy", 0.3, seed=SEED + pid, prefix_k=k if mode == "infinite" else 0)
         ctx.is_prefill(prompt, pid)
         torch.cuda.synchronize()
@@ -58,15 +63,21 @@ for mode in args.modes.split(","):
         dt += time.perf_counter() - t0
         st = ctx.is_query()
         assert st["completed"] == G and st["error"] == 0, st
-        toks += int(np.sum(true))
+        toks += int(st["tokens_decoded"])
         peak = max(peak, st["peak_kv_bytes"])
         tk = ctx.is_copy_tokens()
-        if pid in tokens_ref:
+        done = [u for u in range(len(true)) if tk[u, true[u] - 1] >= 0]
+        emitted += [int(true[u]) for u in done]
+        discarded += st["discarded"]
+        if dyn:
+            pass                                  # 2G candidate rows: not comparable row for row
+        elif pid in tokens_ref:
             same = same and bool(np.array_equal(tk, tokens_ref[pid]))
         else:
             tokens_ref[pid] = tk
     ctx.close()
     out["modes"][mode] = {"decode_steps": steps, "tokens": toks, "tokens_per_s": round(toks / dt, 1),
                           "ms_per_step": round(dt / steps * 1e3, 4), "peak_kv_gb": round(peak / 1e9, 4),
-                          "within_budget": bool(full or peak <= budget), "tokens_identical_to_first_mode": same}
+                          "within_budget": bool(full or peak <= budget), "tokens_identical_to_first_mode": same,
+                          "avg_emitted_len": round(float(np.mean(emitted)), 2), "discarded": discarded}
 print(json.dumps(out))

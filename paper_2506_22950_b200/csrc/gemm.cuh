@@ -81,6 +81,13 @@ struct GemmArgs {
   int bn_tsq, bn_ld;
   float bn_eps;
   float* ssq_out;              // EPI_RESID_ADD: per-(tile, row) sums of squares of the new residual [tiles][bn_ld]
+  // RMSNorm of the new residual fused into EPI_RESID_ADD (needs ssq_out; one tile per CTA):
+  // after a grid barrier every CTA reads the row's per-tile sums of squares (fixed order) and
+  // writes fn_out[row][m] = bf16(x * rs * fn_gain[m]) for its own outputs (rounding point r1)
+  const float* fn_gain;
+  __nv_bfloat16* fn_out;       // [rows][M]
+  unsigned int* fn_bar;        // [2] arrival counter, generation
+  float fn_eps;
   int* zero;                   // optional: words zeroed once the previous kernel completed
   int zero_n;                  //   (the persistent decode kernel's dependency counters)
 };
@@ -108,6 +115,31 @@ __device__ __forceinline__ void stamp(const GemmArgs& a, int i) {
 }
 
 __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + expf(-x)); }
+
+// One-shot grid barrier for a grid whose CTAs are all co-resident (called by one thread per
+// CTA after a CTA barrier; release / acquire at gpu scope; bounded: 2 s, then __trap).
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int n) {
+  unsigned int gen;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
+  __threadfence();
+  const unsigned int old = atomicAdd(bar, 1u);
+  if (old == n - 1) {
+    atomicExch(bar, 0u);
+    __threadfence();
+    atomicAdd(bar + 1, 1u);
+  } else {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+      unsigned int g;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+      if (g != gen) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 2000000000ull) __trap();
+    }
+  }
+  __threadfence();
+}
 
 
 template <int BN, int EPI, int STAGES>
@@ -137,7 +169,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __shared__ float swz[4][BN], swm[4][BN];
   __shared__ float run_m[BN], run_l[BN], run_z[BN];  // the CTA's running log-sum-exp state per row
   __shared__ unsigned long long run_k[BN];
-  __shared__ int srow_act[BN], srow_kv[BN];  // EPI_QKV: row tables, loaded during the mainloop
+  __shared__ int srow_act[BN], srow_kv[BN];
+  __shared__ float srs[BN];  // fused RMSNorm: 1/rms per row  // EPI_QKV: row tables, loaded during the mainloop
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -434,6 +467,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             x = stg[n * kBM + m];
             if (EPI == EPI_RESID_ADD) x += pre[n * kBM + m];
             a.out[(size_t)(a.row0 + n) * a.ld_out + gm] = x;
+            if (EPI == EPI_RESID_ADD && a.fn_out) stg[n * kBM + m] = x;
           }
           if (EPI == EPI_RESID_ADD && a.ssq_out) {
             const float ss = warp_sum(x * x);
@@ -445,6 +479,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const int n = n_lo + (threadIdx.x - 64);
           if (n < n_end)
             a.ssq_out[(size_t)tile * a.bn_ld + a.row0 + n] = sred[0][n] + sred[1][n] + sred[2][n] + sred[3][n];
+        }
+        if (EPI == EPI_RESID_ADD && a.fn_out) {
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (threadIdx.x == 64) grid_barrier(a.fn_bar, gridDim.x);
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          // rs per row: one warp per row, lane t holds tiles t, t + 32, ... (all loads in flight
+          // together), then the same butterfly sum in every CTA
+          for (int n = n_lo + q; n < n_end; n += 4) {
+            float ss = 0.f;
+            for (int t = lane; t < a.num_tiles; t += 32) ss += __ldcg(a.ssq_out + (size_t)t * a.bn_ld + a.row0 + n);
+            ss = warp_sum(ss);
+            if (lane == 0) srs[n] = 1.0f / sqrtf(ss / (float)a.M + a.fn_eps);
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (gm < a.M) {
+            const float gg = a.fn_gain[gm];
+            for (int n = n_lo; n < n_end; ++n)
+              a.fn_out[(size_t)(a.row0 + n) * a.M + gm] = __float2bfloat16_rn(stg[n * kBM + m] * srs[n] * gg);
+          }
         }
       } else if constexpr (EPI == EPI_SWIGLU) {
         // rows [0, 64) of the tile are gate features f, rows [64, 128) the matching up

@@ -452,6 +452,8 @@ struct is_ctx {
   int* merge_cnt;  // [max_rows][Hkv] fused-merge counters (decode, tcgen05 prefix)
   float *ssqA, *ssqB;  // [Th][max_rows] per-128-column sums of squares: QKV input, gate/up input
   int bnorm;           // decode: RMSNorm folded into the QKV / gate-up B operand
+  int fuse_norm;       // decode: RMSNorm of the new residual fused into the o_proj / down epilogues
+  unsigned int* fn_bar;  // [4] their grid barriers (o_proj, down)
   int32_t* attn_items;
   float* splitk_ws;  // split-K partials workspace
   int NC, nc_pre, nc_suf;
@@ -657,7 +659,8 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
     LayerW& w = c->L[l];
     const bool bn = !prefill && (c->bnorm & 1);       // QKV folds the input RMSNorm
     const bool bn_gu = !prefill && (c->bnorm & 2);    // gate/up folds the post-attention RMSNorm
-    if (!bn && (prefill || !(g_skip & 1)))
+    const bool fn = !prefill && c->fuse_norm;          // o_proj / down epilogues write the next xn
+    if (!bn && !(fn && l > 0) && (prefill || !(g_skip & 1)))
       CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.in_norm, c->xn, H,
                    s.rms_eps));
     prof_mark(st, 0);
@@ -760,14 +763,20 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       a.n_valid = std::min(chunk, rows - r0);
       a.out = c->resid;
       a.ld_out = H;
-      if (bn_gu) {
+      if (bn_gu || fn) {
         a.ssq_out = c->ssqB;
         a.bn_ld = c->max_rows;
+      }
+      if (fn) {
+        a.fn_gain = w.post_norm;
+        a.fn_out = c->xn;
+        a.fn_bar = c->fn_bar;
+        a.fn_eps = s.rms_eps;
       }
       if (prefill || !(g_skip & 16)) CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_o, tm_attn, a, st, prefill ? 0 : c->stg_o));
     }
     prof_mark(st, 4);
-    if (!bn_gu && (prefill || !(g_skip & 1)))
+    if (!bn_gu && !fn && (prefill || !(g_skip & 1)))
       CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.post_norm, c->xn, H,
                    s.rms_eps));
     prof_mark(st, 0);
@@ -802,9 +811,15 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       a.n_valid = std::min(chunk, rows - r0);
       a.out = c->resid;
       a.ld_out = H;
-      if (bn) {
+      if (bn || fn) {
         a.ssq_out = c->ssqA;
         a.bn_ld = c->max_rows;
+      }
+      if (fn) {  // the next layer's input norm, or the final norm after the last layer
+        a.fn_gain = l + 1 < s.layers ? (const float*)c->L[l + 1].in_norm : (const float*)c->final_norm;
+        a.fn_out = c->xn;
+        a.fn_bar = c->fn_bar + 2;
+        a.fn_eps = s.rms_eps;
       }
       if (prefill || !(g_skip & 64)) CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_d, tm_act, a, st, prefill ? 0 : c->stg_d));
     }
@@ -1108,8 +1123,9 @@ static is_status enqueue_step_body(is_ctx* c) {
     prof_mark(st, 9);
   } else {
     CKS(run_layers(c, c->rc, false));
-    CKS(launch_k(rmsnorm_kernel, dim3(c->rc), dim3(256), st, (const float*)c->resid, (const float*)c->final_norm,
-                 c->xn, s.hidden, s.rms_eps));
+    if (!c->fuse_norm)  // (else the last down GEMM's epilogue applied the final norm)
+      CKS(launch_k(rmsnorm_kernel, dim3(c->rc), dim3(256), st, (const float*)c->resid, (const float*)c->final_norm,
+                   c->xn, s.hidden, s.rms_eps));
     prof_mark(st, 0);
   }
   GemmArgs a{};
@@ -1350,6 +1366,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->ssqA = (float*)A((size_t)ceil_div64(H, 128) * R * 4);
   c->ssqB = (float*)A((size_t)ceil_div64(H, 128) * R * 4);
   c->splitk_ws = (float*)A((size_t)2 * 160 * kBM * 64 * 4);
+  c->fn_bar = (unsigned int*)A(4 * sizeof(unsigned int));
   c->attn_items = (int32_t*)A((size_t)Hkv * (c->nc_pre * ((c->rc + 3) / 4) + c->rc * c->nc_suf) * kItemStride * 4 + 64);
   c->rope_cos = (float*)A((size_t)c->max_pos * 64 * 4);
   c->rope_sin = (float*)A((size_t)c->max_pos * 64 * 4);
@@ -1454,6 +1471,14 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   if (const char* e = getenv("IS_SPLIT_OVERRIDE")) {
     int v = atoi(e);
     if (v >= 1 && v <= 8) c->split_qkv = c->split_o = c->split_gu = c->split_d = v;
+  }
+  {
+    // IS_FUSE_NORM=1 (opt-in, measured slower: DESIGN §5a).  The fused norm's grid barrier
+    // needs every CTA co-resident and one tile per CTA
+    const int th = (int)ceil_div64(H, kBM);
+    const char* e = getenv("IS_FUSE_NORM");
+    c->fuse_norm = (e && atoi(e) != 0) && !c->bnorm && th * std::max(c->split_o, 1) <= g_num_sms &&
+                   th * std::max(c->split_d, 1) <= g_num_sms;
   }
   CK(cudaDeviceSynchronize());
   if (cfg->decode_impl == 0 && mk_supported(c) && !getenv("IS_NO_MEGA")) CKS(setup_mega(c, dw));

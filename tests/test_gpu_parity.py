@@ -361,3 +361,19 @@ def test_tiny_dynamic_slot_mode(lib, tiny, target):
     base = tiny["runs"]["infinite"]["tokens"]
     for uid in ref.finish_step:
         assert np.array_equal(r["tokens"][uid], base[uid]), uid
+
+
+def test_tiny_fused_norm_opt_in(lib, tiny, monkeypatch):
+    """IS_FUSE_NORM=1 (opt-in): RMSNorm in the o_proj / down epilogues behind a grid
+    barrier.  Same schedule; the norm's fp32 sum order differs, so tokens are compared with the
+    teacher-forced tolerance of the default path (all but a near-tie few identical)."""
+    if tiny["impl"] == 0:
+        pytest.skip("per-op decode path only")
+    monkeypatch.setenv("IS_FUSE_NORM", "1")
+    r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "infinite", 2,
+             budget=tiny["budget"], impl=1)
+    base = tiny["runs"]["infinite"]
+    assert r["slots"].tolist() == base["slots"].tolist() and r["stats"]["completed"] == 8
+    valid = base["tokens"] >= 0
+    same = np.mean(r["tokens"][valid] == base["tokens"][valid])
+    assert same >= 0.9, same

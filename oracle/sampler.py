@@ -21,7 +21,20 @@ float32 scalar/array arithmetic is exactly that (no contraction into FMA).
 Pins (tests/test_oracle_sampler.py): Random123 Philox KATs, logf_is vs math.log
 within 2 ulp, chi-square of sampled frequencies against softmax(z/T), T->0
 argmax, tie-break.
+
+top-p < 1 (SURVEY §8f NEXT-4; BASELINE north_star "temperature/top-p sampler";
+the paper itself never uses it).  DESIGN.md reading R36, every decision
+in exactly reproducible arithmetic:
+  u_v = fl(z_v * invT);  e_v = expf_is(fl(u_v - max u))      (fixed fp32 op sequence)
+  w_v = floor(e_v * 2^44)  (integer; exact)                   W = sum_v w_v  (exact)
+  thr = ceil(fl64(top_p) * fl64(W))                            (binary64 ops)
+  order the vocabulary by (-e_v, v); the nucleus is the shortest prefix whose
+  integer mass reaches thr; the token is the Gumbel-max key (as above) over the
+  nucleus only.  Pins: fp64 nucleus by definition (away from boundaries),
+  top_p -> 0 gives the argmax, chi-square against the renormalised nucleus.
 """
+import math
+
 import numpy as np
 
 M0 = np.uint64(0xD2511F53)
@@ -147,3 +160,56 @@ def sample_margin(logits_f32, seed, uid, t, T=0.8):
     s2 = s.copy()
     s2[i] = -np.inf
     return i, float(s[i] - s2.max())
+
+
+_LOG2E = np.float32(1.4426950408889634)
+_LN2_HI = np.uint32(0x3F317200).view(np.float32)   # 0.693145751953125 (exact products n*_LN2_HI)
+_LN2_LO = np.uint32(0x35BFBE8E).view(np.float32)   # ln2 - _LN2_HI
+_EXP_C = [np.float32(1.0 / 720.0), np.float32(1.0 / 120.0), np.float32(1.0 / 24.0), np.float32(1.0 / 6.0),
+          np.float32(0.5), np.float32(1.0), np.float32(1.0)]
+
+
+def expf_is(d):
+    """exp(d) for fp32 d <= 0 as a FIXED fp32 op sequence (R36): n = rint(d*log2e),
+    r = (d - n*ln2_hi) - n*ln2_lo (Cody-Waite), degree-6 Taylor polynomial in Horner
+    form, times 2^n; 0 when n < -125.  Every step one separately rounded fp32 op."""
+    d = np.asarray(d, dtype=np.float32)
+    n = np.rint((d * _LOG2E).astype(np.float32)).astype(np.float32)
+    r = (d - (n * _LN2_HI).astype(np.float32)).astype(np.float32)
+    r = (r - (n * _LN2_LO).astype(np.float32)).astype(np.float32)
+    p = _EXP_C[0]
+    for c in _EXP_C[1:]:
+        p = ((r * p).astype(np.float32) + c).astype(np.float32)
+    ni = n.astype(np.int32)
+    ok = ni >= -125
+    two_n = ((np.where(ok, ni, 0) + 127).astype(np.uint32) << np.uint32(23)).view(np.float32)
+    return np.where(ok, (p * two_n).astype(np.float32), np.float32(0.0)).astype(np.float32)
+
+
+def topp_nucleus(logits_f32, T, top_p):
+    """Boolean mask of the top-p nucleus (R36)."""
+    z = np.asarray(logits_f32, dtype=np.float32)
+    u = (z * inv_temperature(T)).astype(np.float32)
+    e = expf_is((u - u.max()).astype(np.float32))
+    w = np.floor((e * np.float32(2.0 ** 44)).astype(np.float32).astype(np.float64)).astype(np.uint64)
+    W = int(sum(int(x) for x in w))
+    thr = math.ceil(float(np.float32(top_p)) * float(W))
+    order = np.lexsort((np.arange(len(z)), -e.astype(np.float64)))   # (-e, v)
+    acc = 0
+    mask = np.zeros(len(z), dtype=bool)
+    for v in order:
+        mask[v] = True
+        acc += int(w[v])
+        if acc >= thr:
+            break
+    return mask
+
+
+def sample_token_topp(logits_f32, seed, uid, t, T=0.8, top_p=1.0):
+    """Gumbel-max over the top-p nucleus; top_p >= 1 (or <= 0) is the plain sampler."""
+    if not 0.0 < top_p < 1.0:
+        return sample_token(logits_f32, seed, uid, t, T)
+    z = np.asarray(logits_f32, dtype=np.float32)
+    k = order_key(score(z, gumbel_noise(seed, uid, t, len(z)), inv_temperature(T)))
+    k = np.where(topp_nucleus(z, T, top_p), k, np.uint64(0))
+    return int(np.argmax(k))

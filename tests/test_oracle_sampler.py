@@ -93,3 +93,71 @@ def test_stream_depends_only_on_uid_and_t():
     b = [sampler.sample_token(z, 5, 3, t) for t in range(10)]
     c = [sampler.sample_token(z, 5, 4, t) for t in range(10)]
     assert a == b and a != c
+
+
+def test_expf_within_three_ulp_of_libm():
+    """R36's fixed-sequence exp against binary64 exp, d in [-86, 0]; exact at 0; 0 below 2^-125."""
+    d = np.linspace(-86.0, 0.0, 200_001).astype(np.float32)
+    e = sampler.expf_is(d).astype(np.float64)
+    ref = np.exp(d.astype(np.float64))
+    ulp = np.spacing(ref.astype(np.float32)).astype(np.float64)
+    assert np.max(np.abs(e - ref) / ulp) <= 3.0
+    assert sampler.expf_is(np.float32(0.0)) == np.float32(1.0)
+    assert sampler.expf_is(np.float32(-100.0)) == 0.0
+
+
+def _nucleus_fp64(z, T, top_p):
+    """The top-p definition in binary64: sort by probability (ties -> lower v), shortest
+    prefix with mass >= top_p; also the distance of every prefix mass from top_p."""
+    u = z.astype(np.float64) / T
+    p = np.exp(u - u.max())
+    p /= p.sum()
+    order = np.lexsort((np.arange(len(z)), -p))
+    cum = np.cumsum(p[order])
+    k = int(np.searchsorted(cum, top_p))
+    mask = np.zeros(len(z), dtype=bool)
+    mask[order[:k + 1]] = True
+    return mask, float(np.min(np.abs(cum - top_p)))
+
+
+def test_topp_nucleus_matches_binary64_definition():
+    rng = np.random.default_rng(8)
+    checked = 0
+    for i in range(300):
+        V = int(rng.integers(4, 600))
+        z = (rng.normal(size=V) * rng.uniform(0.2, 4.0)).astype(np.float32)
+        top_p = float(np.float32(rng.uniform(0.05, 0.99)))
+        ref, margin = _nucleus_fp64(z, 0.8, top_p)
+        if margin < 1e-5:
+            continue                      # boundary within rounding distance: not decided by the definition
+        assert np.array_equal(sampler.topp_nucleus(z, 0.8, top_p), ref), i
+        checked += 1
+    assert checked > 250
+
+
+def test_topp_tiny_is_argmax_and_one_is_plain():
+    rng = np.random.default_rng(9)
+    for t in range(20):
+        z = rng.normal(size=512).astype(np.float32)
+        assert sampler.sample_token_topp(z, 5, 1, t, 0.8, 1e-6) == int(np.argmax(z))
+        assert sampler.sample_token_topp(z, 5, 1, t, 0.8, 1.0) == sampler.sample_token(z, 5, 1, t, 0.8)
+        # the sampled token always lies in the nucleus
+        tok = sampler.sample_token_topp(z, 5, 1, t, 0.8, 0.5)
+        assert sampler.topp_nucleus(z, 0.8, 0.5)[tok]
+
+
+def test_topp_chi_square_against_renormalised_nucleus():
+    z = np.float32([0.3, -1.0, 2.0, 0.0, 1.2, -0.5, 0.7, 1.9])
+    T, top_p = 0.8, 0.75
+    mask, margin = _nucleus_fp64(z, T, top_p)
+    assert margin > 1e-3 and np.array_equal(sampler.topp_nucleus(z, T, top_p), mask)
+    p = np.where(mask, np.exp(z.astype(np.float64) / T), 0.0)
+    p /= p.sum()
+    n = 6000
+    counts = np.zeros(8)
+    for uid in range(n):
+        counts[sampler.sample_token_topp(z, 77, uid, 0, T, top_p)] += 1
+    assert np.all(counts[~mask] == 0)
+    k = int(mask.sum())
+    chi2 = ((counts[mask] - n * p[mask]) ** 2 / (n * p[mask])).sum()
+    assert chi2 < {2: 10.83, 3: 13.82, 4: 16.27, 5: 18.47}[k]   # k-1 dof, p = 0.001

@@ -84,6 +84,10 @@ typedef struct {
                               rows m*g .. m*g+g-1; kv_budget_bytes is per group, the page pool
                               (max_groups x the per-group pool) is shared.  max_groups*g <= 64 */
   int32_t dynamic_target;  /* IS_MODE_DYNAMIC: completions to stop at (0 = G); 0 in every other mode */
+  float top_p;             /* nucleus sampling (DESIGN R36): 0 < top_p < 1 samples the
+                              Gumbel-max token inside the top-p nucleus (integer-exact mass, fixed-
+                              sequence exp); 0 or 1 = off (the paper's plain temperature sampling).
+                              Costs a [row_capacity][vocab] fp32 logits buffer and one extra kernel */
 } is_config;
 
 /* Alg. 2 output plus the runtime plan (Alg. 1, Alg. 3).  All arrays are

@@ -195,13 +195,10 @@ def topp_nucleus(logits_f32, T, top_p):
     W = int(sum(int(x) for x in w))
     thr = math.ceil(float(np.float32(top_p)) * float(W))
     order = np.lexsort((np.arange(len(z)), -e.astype(np.float64)))   # (-e, v)
-    acc = 0
+    cum = np.cumsum(w[order], dtype=np.uint64)                          # exact: W < 2^63
+    k = int(np.searchsorted(cum, np.uint64(thr)))                       # first prefix with mass >= thr
     mask = np.zeros(len(z), dtype=bool)
-    for v in order:
-        mask[v] = True
-        acc += int(w[v])
-        if acc >= thr:
-            break
+    mask[order[:k + 1]] = True
     return mask
 
 

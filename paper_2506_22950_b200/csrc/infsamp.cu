@@ -76,6 +76,7 @@ static is_status check_config(const is_config* c) {
   if (c->prefix_k < 0 || (c->prefix_k > 0 && c->mode != IS_MODE_INFINITE))
     return fail(IS_ERR_CONFIG, "prefix_k > 0 requires IS_MODE_INFINITE");
   if (!(c->temperature > 0)) return fail(IS_ERR_CONFIG, "temperature must be > 0");
+  if (!(c->top_p >= 0.f && c->top_p <= 1.f)) return fail(IS_ERR_CONFIG, "top_p must be in [0, 1] (0 or 1 = off)");
   if (c->mode < IS_MODE_FULL || c->mode > IS_MODE_DYNAMIC) return fail(IS_ERR_CONFIG, "unknown mode %d", (int)c->mode);
   if (c->dynamic_target < 0 || c->dynamic_target > c->G || (c->dynamic_target > 0 && c->mode != IS_MODE_DYNAMIC))
     return fail(IS_ERR_CONFIG, "dynamic_target must be 0 or 1..G (got %d) and needs IS_MODE_DYNAMIC", c->dynamic_target);
@@ -453,6 +454,9 @@ struct is_ctx {
   float *ssqA, *ssqB;  // [Th][max_rows] per-128-column sums of squares: QKV input, gate/up input
   int bnorm;           // decode: RMSNorm folded into the QKV / gate-up B operand
   int fuse_norm;       // decode: RMSNorm of the new residual fused into the o_proj / down epilogues
+  int topp;            // 0 < top_p < 1: nucleus sampling pass after the lm_head (R36)
+  float* logits_tp;    //   its fp32 logits [max_rows][vocab]
+  float* tok_z;        //   the sampled token's logit per row (log-probabilities)
   unsigned int* fn_bar;  // [4] their grid barriers (o_proj, down)
   int32_t* attn_items;
   float* splitk_ws;  // split-K partials workspace
@@ -548,6 +552,7 @@ static SchedArgs sched_args(is_ctx* c) {
   a.lp_mlz = c->lp_mlz;
   a.logprobs = c->logprobs;
   a.lp_grid = c->lp_grid;
+  a.tok_z = c->tok_z;
   a.last_tok = c->last_tok;
   a.last_fin = c->last_fin;
   a.row_active = c->row_active;
@@ -1142,7 +1147,7 @@ static is_status enqueue_step_body(is_ctx* c) {
   a.keys = c->keys;
   a.lp_key = c->lp_key;
   a.lp_mlz = c->lp_mlz;
-  a.logits_dump = c->logits_dump;
+  a.logits_dump = c->topp ? (c->logits_dump ? c->logits_dump : c->logits_tp) : c->logits_dump;
   if (c->mk) {
     a.zero = c->mka.sync;  // the next step's dependency counters start from zero
     a.zero_n = c->mk_sync_n;
@@ -1151,6 +1156,10 @@ static is_status enqueue_step_body(is_ctx* c) {
   a.inv_temp = (float)(1.0 / (double)c->cfg.temperature);
   g_splitk_ws = c->splitk_ws;
   CKS(launch_gemm<EPI_SAMPLE>(c->BN, c->tm_embed, c->tm_xn_dec, a, st));
+  if (c->topp)  // top-p < 1 (R36): the nucleus and its Gumbel-max replace the full-vocabulary key
+    CKS(launch_k(topp_kernel, dim3(c->rc), dim3(kToppThreads), st, (const float*)a.logits_dump, s.vocab,
+                 (const int32_t*)c->row_active, (const int32_t*)c->row_uid, (const int32_t*)c->row_t,
+                 (uint64_t)c->cfg.seed, a.inv_temp, c->cfg.top_p, c->keys, c->tok_z));
   prof_mark(st, 7);
   CKS(launch_k(sched_kernel, dim3(1), dim3(kSchedThreads), st, sched_args(c), 1, (1 << c->M) - 1));
   prof_mark(st, 8);
@@ -1367,6 +1376,9 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->ssqB = (float*)A((size_t)ceil_div64(H, 128) * R * 4);
   c->splitk_ws = (float*)A((size_t)2 * 160 * kBM * 64 * 4);
   c->fn_bar = (unsigned int*)A(4 * sizeof(unsigned int));
+  c->topp = cfg->top_p > 0.f && cfg->top_p < 1.f;
+  c->logits_tp = c->topp ? (float*)A((size_t)R * s.vocab * 4) : nullptr;
+  c->tok_z = c->topp ? (float*)A((size_t)R * 4) : nullptr;
   c->attn_items = (int32_t*)A((size_t)Hkv * (c->nc_pre * ((c->rc + 3) / 4) + c->rc * c->nc_suf) * kItemStride * 4 + 64);
   c->rope_cos = (float*)A((size_t)c->max_pos * 64 * 4);
   c->rope_sin = (float*)A((size_t)c->max_pos * 64 * 4);
@@ -1497,7 +1509,7 @@ extern "C" void is_destroy(is_ctx* c) {
                   c->last_fin, c->st_dev, c->slot_uid, c->slot_count, c->tpos, c->true_len, c->queue,
                   c->main_init, c->main_queue, c->free_stack, c->pagetab, c->npages, c->tokens, c->log_slot,
                   c->log_live, c->d_prompt_copy, c->lp_key, c->lp_mlz, c->logprobs, c->prow_active, c->prow_tok, c->prow_pos, c->prow_kvloc,
-                  c->prow_len};
+                  c->prow_len, c->fn_bar, c->logits_tp, c->tok_z};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (int i = 0; i < c->mk_nbufs; ++i) cudaFree(c->mk_bufs[i]);

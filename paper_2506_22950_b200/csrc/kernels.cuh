@@ -902,6 +902,7 @@ struct SchedArgs {
   const unsigned long long* lp_key;  // [row_cap][lp_grid] per-CTA best keys (NEXT-3 log-probabilities)
   const float4* lp_mlz;      // [row_cap][lp_grid] per-CTA (max z, sum exp, winner's z)
   float* logprobs;           // [M][G][max_new] log pi(token) at temperature 1 (R33)
+  const float* tok_z;        // top-p (R36): the sampled token's logit per row (null: from the lm_head partials)
   int lp_grid;
   int32_t* last_tok;         // [row_cap]
   uint8_t* last_fin;         // [row_cap]
@@ -946,6 +947,7 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
       }
       Mx = warp_max(Mx);
       zt = warp_max(zt);
+      if (a.tok_z) zt = a.tok_z[row];
       float L = 0.f;
       for (int c = lane; c < a.lp_grid; c += 32) {
         const float4 v = a.lp_mlz[(size_t)row * a.lp_grid + c];
@@ -1214,4 +1216,164 @@ __global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ x, float* _
   if (i < n) y[i] = __bfloat162float(x[i]);
 }
 
+
+// ------------------------------------------------------------------ top-p < 1 (NEXT-4, DESIGN R36)
+// exp(d), d <= 0: the fixed fp32 op sequence of R36 (Cody-Waite split, degree-6 Taylor
+// polynomial in Horner form, times 2^n; 0 below 2^-125), explicit _rn intrinsics.
+__device__ __forceinline__ float expf_is(float d) {
+  const float n = rintf(__fmul_rn(d, __uint_as_float(0x3FB8AA3Bu)));  // fl32(log2 e)
+  float r = __fsub_rn(d, __fmul_rn(n, __uint_as_float(0x3F317200u)));
+  r = __fsub_rn(r, __fmul_rn(n, __uint_as_float(0x35BFBE8Eu)));
+  float p = __uint_as_float(0x3AB60B61u);                          // fl32(1/720)
+  p = __fadd_rn(__fmul_rn(r, p), __uint_as_float(0x3C088889u));  // 1/120
+  p = __fadd_rn(__fmul_rn(r, p), __uint_as_float(0x3D2AAAABu));  // 1/24
+  p = __fadd_rn(__fmul_rn(r, p), __uint_as_float(0x3E2AAAABu));  // 1/6
+  p = __fadd_rn(__fmul_rn(r, p), 0.5f);
+  p = __fadd_rn(__fmul_rn(r, p), 1.0f);
+  p = __fadd_rn(__fmul_rn(r, p), 1.0f);
+  const int ni = (int)n;
+  if (ni < -125) return 0.f;
+  return __fmul_rn(p, __uint_as_float((uint32_t)(ni + 127) << 23));
+}
+
+__device__ __forceinline__ unsigned long long topp_w(float e) {
+  return (unsigned long long)__fmul_rn(e, 17592186044416.0f /* 2^44 */);  // exact, then truncation = floor
+}
+
+constexpr int kToppThreads = 1024;
+
+// One CTA per live row, over the row's fp32 logits (written by the lm_head epilogue):
+// max -> integer nucleus mass W -> radix select (4 x 8 bits, descending) of the boundary
+// value e* and the mass above it -> the boundary's last member in ascending v -> Gumbel-max
+// over the nucleus.  keys[row] / tok_z[row] receive the winner (the scheduler consumes them).
+// Each thread owns a contiguous range of v (the tie scan needs index order).
+__global__ void __launch_bounds__(kToppThreads) topp_kernel(const float* __restrict__ logits, int V,
+                                                            const int32_t* __restrict__ row_active,
+                                                            const int32_t* __restrict__ row_uid,
+                                                            const int32_t* __restrict__ row_t, uint64_t seed,
+                                                            float invT, float top_p, unsigned long long* keys,
+                                                            float* tok_z) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int row = blockIdx.x;
+  if (!row_active[row]) return;
+  const float* z = logits + (size_t)row * V;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int per = (V + kToppThreads - 1) / kToppThreads;
+  const int v0 = min(V, tid * per), v1 = min(V, v0 + per);
+  __shared__ float s_f[32];
+  __shared__ unsigned long long s_u[32];
+  __shared__ unsigned long long hist[256];
+  __shared__ unsigned long long s_above, s_thr;
+  __shared__ uint32_t s_prefix;
+  __shared__ int s_cnt[kToppThreads / 32];
+  __shared__ int s_vk;
+  // 1. max of u = fl(z * invT)
+  float mx = -INFINITY;
+  for (int v = v0; v < v1; ++v) mx = fmaxf(mx, __fmul_rn(z[v], invT));
+  mx = warp_max(mx);
+  if (lane == 0) s_f[wid] = mx;
+  __syncthreads();
+  mx = s_f[0];
+  for (int w = 1; w < kToppThreads / 32; ++w) mx = fmaxf(mx, s_f[w]);
+  // 2. integer mass W, threshold
+  unsigned long long wsum = 0;
+  for (int v = v0; v < v1; ++v) wsum += topp_w(expf_is(__fsub_rn(__fmul_rn(z[v], invT), mx)));
+  for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+  if (lane == 0) s_u[wid] = wsum;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long W = 0;
+    for (int w = 0; w < kToppThreads / 32; ++w) W += s_u[w];
+    s_thr = (unsigned long long)ceil(__dmul_rn((double)top_p, __ull2double_rn(W)));
+    s_above = 0;
+    s_prefix = 0;
+  }
+  // 3. radix select of the boundary value's bits, most significant byte first
+  uint32_t mask = 0;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    if (tid < 256) hist[tid] = 0;
+    __syncthreads();
+    const uint32_t prefix = s_prefix;
+    int cur = -1;
+    unsigned long long run = 0;  // runs of equal digits are added once (contention)
+    for (int v = v0; v < v1; ++v) {
+      const float e = expf_is(__fsub_rn(__fmul_rn(z[v], invT), mx));
+      const uint32_t b = __float_as_uint(e);
+      if ((b & mask) != prefix) continue;
+      const int d = (int)((b >> shift) & 255u);
+      if (d != cur) {
+        if (cur >= 0 && run) atomicAdd(&hist[cur], run);
+        cur = d;
+        run = 0;
+      }
+      run += topp_w(e);
+    }
+    if (cur >= 0 && run) atomicAdd(&hist[cur], run);
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long acc = s_above;
+      int d = 255;
+      for (; d > 0; --d) {
+        if (acc + hist[d] >= s_thr) break;
+        acc += hist[d];
+      }
+      s_above = acc;
+      s_prefix = prefix | ((uint32_t)d << shift);
+    }
+    mask |= 255u << shift;
+    __syncthreads();
+  }
+  const uint32_t bstar = s_prefix;
+  const unsigned long long wb = topp_w(__uint_as_float(bstar));
+  const unsigned long long need = wb ? (s_thr - s_above + wb - 1) / wb : 1;  // members with e == e* (>= 1)
+  // 4. the need-th member of value e* in ascending v
+  int cnt = 0;
+  for (int v = v0; v < v1; ++v)
+    cnt += __float_as_uint(expf_is(__fsub_rn(__fmul_rn(z[v], invT), mx))) == bstar;
+  int incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_cnt[wid] = incl;
+  __syncthreads();
+  int before = incl - cnt;
+  for (int w = 0; w < wid; ++w) before += s_cnt[w];
+  if (tid == 0) s_vk = V - 1;
+  __syncthreads();
+  if ((unsigned long long)before < need && (unsigned long long)(before + cnt) >= need) {
+    int k = before;
+    for (int v = v0; v < v1; ++v)
+      if (__float_as_uint(expf_is(__fsub_rn(__fmul_rn(z[v], invT), mx))) == bstar && ++k == (int)need) {
+        s_vk = v;
+        break;
+      }
+  }
+  __syncthreads();
+  const int vk = s_vk;
+  // 5. Gumbel-max over the nucleus (same key as the lm_head epilogue)
+  const uint32_t uid = (uint32_t)row_uid[row], t = (uint32_t)row_t[row];
+  unsigned long long best = 0;
+  for (int v = v0; v < v1; ++v) {
+    const float u = __fmul_rn(z[v], invT);
+    const uint32_t b = __float_as_uint(expf_is(__fsub_rn(u, mx)));
+    if (b > bstar || (b == bstar && v <= vk)) {
+      const unsigned long long k = order_key(__fadd_rn(u, gumbel(seed, uid, t, (uint32_t)v)), (uint32_t)v);
+      best = k > best ? k : best;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+    best = y > best ? y : best;
+  }
+  if (lane == 0) s_u[wid] = best;
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < kToppThreads / 32; ++w) best = s_u[w] > best ? s_u[w] : best;
+    best = s_u[0] > best ? s_u[0] : best;
+    keys[row] = best;
+    if (tok_z) tok_z[row] = z[0xFFFFFFFFu - (uint32_t)(best & 0xFFFFFFFFull)];
+  }
+}
 }  // namespace isk

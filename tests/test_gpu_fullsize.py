@@ -164,3 +164,37 @@ def test_fullsize_prefix_phase_schedule_and_budget(prefix_phase):
     assert st["completed"] == r["G"] and st["error"] == 0
     assert st["peak_pages"] == ref.peak_pages
     assert st["peak_kv_bytes"] <= r["budget"]  # R25: the budget is a hard invariant
+
+
+def test_fullsize_topp_step_bit_exact():
+    """top-p = 0.9 at full size (vocab 151,936, 8 live rows): three decode steps, every
+    sampled token equals the oracle's nucleus draw on the dumped logits."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2506_22950_b200 import _lib
+    w = gen_weights(SHAPE, seed=SEED, device="cuda")
+    cfg = _lib.make_config(SHAPE, G, g, MAX_NEW, P, mode="infinite", page_tokens=16, eps=0.1, temperature=0.8,
+                           seed=SEED, decode_impl=1, top_p=0.9)
+    ctx = _lib.Context(cfg, w)
+    prompt = gen_prompt(SHAPE.vocab, P, 5, seed=SEED)
+    true = gen_trace("math", G, MAX_NEW, SEED + 5)
+    ctx.is_prefill(torch.as_tensor(prompt, device="cuda"), 5)
+    ctx.is_start_group(true, predict_lengths(true, "noisy", 0.3, seed=SEED + 5))
+    dump = torch.zeros(16, SHAPE.vocab, device="cuda")
+    ctx.is_set_logits_dump(dump)
+    dumps = []
+    for _ in range(3):
+        ctx.is_decode_step()
+        torch.cuda.synchronize()
+        dumps.append(dump.cpu().numpy().copy())
+    slots, _ = ctx.is_copy_schedule()
+    toks = ctx.is_copy_tokens()
+    ctx.close()
+    del w
+    torch.cuda.empty_cache()
+    for step in range(3):
+        for s, uid in enumerate(slots[step]):
+            if uid < 0:
+                continue
+            got = sampler.sample_token_topp(dumps[step][s], SEED, 5 * G + int(uid), step, 0.8, 0.9)
+            assert got == toks[uid, step], (step, s, uid)

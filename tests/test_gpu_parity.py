@@ -62,10 +62,10 @@ def _tiny_setup():
 
 
 def _run(lib, w_dev, prompt, true, pred, mode, g, budget=0, prefix_k=0, pt=16, rc=16, logits=False, impl=0,
-         target=0):
+         target=0, top_p=1.0):
     cfg = lib.make_config(TINY, len(true), g, 32, 16, mode=mode, prefix_k=prefix_k, page_tokens=pt, row_capacity=rc,
                           kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED, decode_impl=impl,
-                          dynamic_target=target)
+                          dynamic_target=target, top_p=top_p)
     ctx = lib.Context(cfg, w_dev)
     ctx.is_prefill(torch.as_tensor(prompt, device="cuda"), 0)
     ctx.is_start_group(true, pred)
@@ -377,3 +377,30 @@ def test_tiny_fused_norm_opt_in(lib, tiny, monkeypatch):
     valid = base["tokens"] >= 0
     same = np.mean(r["tokens"][valid] == base["tokens"][valid])
     assert same >= 0.9, same
+
+
+@pytest.mark.parametrize("top_p", [0.9, 0.5, 0.05])
+def test_tiny_topp_sampler_bit_exact(lib, tiny, top_p):
+    """NEXT-4 top-p (R36): every token equals the oracle's nucleus Gumbel-max draw on the
+    kernel's own dumped logits, bit-exactly; log pi(token) stays the full-softmax value
+    (R33); the schedule is unchanged."""
+    r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "infinite", 2,
+             budget=tiny["budget"], logits=True, impl=tiny["impl"], top_p=top_p)
+    assert r["slots"].tolist() == tiny["runs"]["infinite"]["slots"].tolist()
+    toks, lps = r["tokens"], r["logprobs"]
+    t_of, n, in_nucleus_only = {}, 0, 0
+    for step, row in enumerate(r["slots"]):
+        for s, uid in enumerate(row):
+            if uid < 0:
+                continue
+            t = t_of.get(uid, 0)
+            z = r["dumps"][step][s]
+            got = sampler.sample_token_topp(z, SEED, int(uid), t, 0.8, top_p)
+            assert got == toks[uid, t], (step, s, uid, t)
+            assert abs(lps[uid, t] - _log_softmax64(z)[got]) <= 1e-4
+            in_nucleus_only += got != sampler.sample_token(z, SEED, int(uid), t, 0.8)
+            t_of[uid] = t + 1
+            n += 1
+    assert n == int(np.sum(tiny["true"]))
+    if top_p <= 0.5:
+        assert in_nucleus_only > 0      # the nucleus actually changed some draws

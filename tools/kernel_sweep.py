@@ -48,8 +48,9 @@ for setting in SETTINGS:
         if kv:
             k, v = kv.split("=")
             os.environ[k] = v
+    top_p = float(os.environ.pop("TOP_P", "1.0"))   # (a make_config field, not an env knob)
     cfg = _lib.make_config(shape, G, g, max_new, P, mode="infinite", page_tokens=16, kv_budget_bytes=budget,
-                           eps=0.1, temperature=0.8, seed=SEED)
+                           eps=0.1, temperature=0.8, seed=SEED, top_p=top_p)
     ctx = _lib.Context(cfg, w)
     ctx.is_prefill(prompt, 0)
     ctx.is_start_group(true, pred)

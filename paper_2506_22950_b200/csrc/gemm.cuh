@@ -67,6 +67,7 @@ struct GemmArgs {
   unsigned long long* lp_key;  // SAMPLE (NEXT-3): per (row, CTA) best key of the CTA's tiles  [rows][gridDim]
   float4* lp_mlz;              //   and its online (max z, sum exp(z - max), winner's z, -)   [rows][gridDim]
   float* logits_dump;  // optional [rows][M]
+  float* score_dump;   // optional [rows][M] fl(fl(z * invT) + G_v) (top-p pass, R36)
   uint64_t seed;
   float inv_temp;
   QkvEpiArgs qkv;
@@ -559,7 +560,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (a.logits_dump) a.logits_dump[(size_t)(a.row0 + n) * a.ld_out + gm] = z;
             const float g = gumbel(a.seed, (uint32_t)a.row_uid[a.row0 + n], (uint32_t)a.row_t[a.row0 + n],
                                    (uint32_t)gm);
-            key = order_key(__fadd_rn(__fmul_rn(z, a.inv_temp), g), (uint32_t)gm);
+            const float sc = __fadd_rn(__fmul_rn(z, a.inv_temp), g);
+            if (a.score_dump) a.score_dump[(size_t)(a.row0 + n) * a.ld_out + gm] = sc;
+            key = order_key(sc, (uint32_t)gm);
           }
           float zk = z;  // logit carried with the key
 #pragma unroll

@@ -456,7 +456,10 @@ struct is_ctx {
   int fuse_norm;       // decode: RMSNorm of the new residual fused into the o_proj / down epilogues
   int topp;            // 0 < top_p < 1: nucleus sampling pass after the lm_head (R36)
   float* logits_tp;    //   its fp32 logits [max_rows][vocab]
-  float* tok_z;        //   the sampled token's logit per row (log-probabilities)
+  float* scores_tp;    //   the lm_head's Gumbel scores [max_rows][vocab]
+  uint32_t* ebits_tp;  //   e_v bits [max_rows][vocab]
+  unsigned long long *wpart_tp, *hist_tp;  // per-slice mass, level-1 histograms
+  int2* sel_tp;        //   per row (e*, v_k)
   unsigned int* fn_bar;  // [4] their grid barriers (o_proj, down)
   int32_t* attn_items;
   float* splitk_ws;  // split-K partials workspace
@@ -552,7 +555,8 @@ static SchedArgs sched_args(is_ctx* c) {
   a.lp_mlz = c->lp_mlz;
   a.logprobs = c->logprobs;
   a.lp_grid = c->lp_grid;
-  a.tok_z = c->tok_z;
+  a.tok_logits = c->topp ? (c->logits_dump ? c->logits_dump : c->logits_tp) : nullptr;
+  a.vocab = c->sh.vocab;
   a.last_tok = c->last_tok;
   a.last_fin = c->last_fin;
   a.row_active = c->row_active;
@@ -1148,6 +1152,7 @@ static is_status enqueue_step_body(is_ctx* c) {
   a.lp_key = c->lp_key;
   a.lp_mlz = c->lp_mlz;
   a.logits_dump = c->topp ? (c->logits_dump ? c->logits_dump : c->logits_tp) : c->logits_dump;
+  a.score_dump = c->topp ? c->scores_tp : nullptr;
   if (c->mk) {
     a.zero = c->mka.sync;  // the next step's dependency counters start from zero
     a.zero_n = c->mk_sync_n;
@@ -1156,10 +1161,25 @@ static is_status enqueue_step_body(is_ctx* c) {
   a.inv_temp = (float)(1.0 / (double)c->cfg.temperature);
   g_splitk_ws = c->splitk_ws;
   CKS(launch_gemm<EPI_SAMPLE>(c->BN, c->tm_embed, c->tm_xn_dec, a, st));
-  if (c->topp)  // top-p < 1 (R36): the nucleus and its Gumbel-max replace the full-vocabulary key
-    CKS(launch_k(topp_kernel, dim3(c->rc), dim3(kToppThreads), st, (const float*)a.logits_dump, s.vocab,
-                 (const int32_t*)c->row_active, (const int32_t*)c->row_uid, (const int32_t*)c->row_t,
-                 (uint64_t)c->cfg.seed, a.inv_temp, c->cfg.top_p, c->keys, c->tok_z));
+  if (c->topp) {  // top-p < 1 (R36): the nucleus and its Gumbel-max replace the full-vocabulary key
+    ToppArgs t{};
+    t.scores = c->scores_tp;
+    t.logits = a.logits_dump;
+    t.lp_mlz = c->lp_mlz;
+    t.lp_grid = c->lp_grid;
+    t.ebits = c->ebits_tp;
+    t.wpart = c->wpart_tp;
+    t.hist1 = c->hist_tp;
+    t.sel = c->sel_tp;
+    t.row_active = c->row_active;
+    t.keys = c->keys;
+    t.V = s.vocab;
+    t.invT = a.inv_temp;
+    t.top_p = c->cfg.top_p;
+    CKS(launch_k(topp_prep_kernel, dim3(kToppBlocks, c->rc), dim3(kToppThreads), st, t));
+    CKS(launch_k(topp_select_kernel, dim3(c->rc), dim3(kToppThreads), st, t));
+    CKS(launch_k(topp_sample_kernel, dim3(kToppBlocks, c->rc), dim3(kToppThreads), st, t));
+  }
   prof_mark(st, 7);
   CKS(launch_k(sched_kernel, dim3(1), dim3(kSchedThreads), st, sched_args(c), 1, (1 << c->M) - 1));
   prof_mark(st, 8);
@@ -1378,7 +1398,11 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->fn_bar = (unsigned int*)A(4 * sizeof(unsigned int));
   c->topp = cfg->top_p > 0.f && cfg->top_p < 1.f;
   c->logits_tp = c->topp ? (float*)A((size_t)R * s.vocab * 4) : nullptr;
-  c->tok_z = c->topp ? (float*)A((size_t)R * 4) : nullptr;
+  c->scores_tp = c->topp ? (float*)A((size_t)R * s.vocab * 4) : nullptr;
+  c->ebits_tp = c->topp ? (uint32_t*)A((size_t)R * s.vocab * 4) : nullptr;
+  c->wpart_tp = c->topp ? (unsigned long long*)A((size_t)R * kToppBlocks * 8) : nullptr;
+  c->hist_tp = c->topp ? (unsigned long long*)A((size_t)R * kToppBlocks * 256 * 8) : nullptr;
+  c->sel_tp = c->topp ? (int2*)A((size_t)R * 8) : nullptr;
   c->attn_items = (int32_t*)A((size_t)Hkv * (c->nc_pre * ((c->rc + 3) / 4) + c->rc * c->nc_suf) * kItemStride * 4 + 64);
   c->rope_cos = (float*)A((size_t)c->max_pos * 64 * 4);
   c->rope_sin = (float*)A((size_t)c->max_pos * 64 * 4);
@@ -1509,7 +1533,8 @@ extern "C" void is_destroy(is_ctx* c) {
                   c->last_fin, c->st_dev, c->slot_uid, c->slot_count, c->tpos, c->true_len, c->queue,
                   c->main_init, c->main_queue, c->free_stack, c->pagetab, c->npages, c->tokens, c->log_slot,
                   c->log_live, c->d_prompt_copy, c->lp_key, c->lp_mlz, c->logprobs, c->prow_active, c->prow_tok, c->prow_pos, c->prow_kvloc,
-                  c->prow_len, c->fn_bar, c->logits_tp, c->tok_z};
+                  c->prow_len, c->fn_bar, c->logits_tp, c->scores_tp, c->ebits_tp, c->wpart_tp, c->hist_tp,
+                  c->sel_tp};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (int i = 0; i < c->mk_nbufs; ++i) cudaFree(c->mk_bufs[i]);

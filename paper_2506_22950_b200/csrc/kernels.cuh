@@ -902,7 +902,8 @@ struct SchedArgs {
   const unsigned long long* lp_key;  // [row_cap][lp_grid] per-CTA best keys (NEXT-3 log-probabilities)
   const float4* lp_mlz;      // [row_cap][lp_grid] per-CTA (max z, sum exp, winner's z)
   float* logprobs;           // [M][G][max_new] log pi(token) at temperature 1 (R33)
-  const float* tok_z;        // top-p (R36): the sampled token's logit per row (null: from the lm_head partials)
+  const float* tok_logits;   // top-p (R36): [rows][vocab] logits; the sampled token's logit is read there
+  int vocab;
   int lp_grid;
   int32_t* last_tok;         // [row_cap]
   uint8_t* last_fin;         // [row_cap]
@@ -947,7 +948,7 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
       }
       Mx = warp_max(Mx);
       zt = warp_max(zt);
-      if (a.tok_z) zt = a.tok_z[row];
+      if (a.tok_logits) zt = a.tok_logits[(size_t)row * a.vocab + (0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull))];
       float L = 0.f;
       for (int c = lane; c < a.lp_grid; c += 32) {
         const float4 v = a.lp_mlz[(size_t)row * a.lp_grid + c];
@@ -1241,76 +1242,132 @@ __device__ __forceinline__ unsigned long long topp_w(float e) {
 }
 
 constexpr int kToppThreads = 1024;
+constexpr int kToppBlocks = 16;  // vocabulary slices per row for the parallel passes
 
-// One CTA per live row, over the row's fp32 logits (written by the lm_head epilogue):
-// max -> integer nucleus mass W -> radix select (4 x 8 bits, descending) of the boundary
-// value e* and the mass above it -> the boundary's last member in ascending v -> Gumbel-max
-// over the nucleus.  keys[row] / tok_z[row] receive the winner (the scheduler consumes them).
-// Each thread owns a contiguous range of v (the tie scan needs index order).
-__global__ void __launch_bounds__(kToppThreads) topp_kernel(const float* __restrict__ logits, int V,
-                                                            const int32_t* __restrict__ row_active,
-                                                            const int32_t* __restrict__ row_uid,
-                                                            const int32_t* __restrict__ row_t, uint64_t seed,
-                                                            float invT, float top_p, unsigned long long* keys,
-                                                            float* tok_z) {
+struct ToppArgs {
+  const float* scores;       // [rows][V] fl(fl(z * invT) + G_v) from the lm_head epilogue
+  const float* logits;       // [rows][V] z
+  const float4* lp_mlz;      // [rows][lp_grid] lm_head per-CTA (max z, ...): the row max
+  int lp_grid;
+  uint32_t* ebits;           // [rows][V] bits of e_v
+  unsigned long long* wpart; // [rows][kToppBlocks] integer mass per slice
+  unsigned long long* hist1; // [rows][kToppBlocks][256] level-1 (top byte) mass histogram per slice
+  int2* sel;                 // [rows] (boundary bits e*, last boundary member v_k)
+  const int32_t* row_active;
+  unsigned long long* keys;  // [rows]
+  int V;
+  float invT, top_p;
+};
+
+// Pass A (rows x kToppBlocks CTAs): e_v bits, the slice's integer mass and its top-byte
+// histogram.  max u = fl(max z * invT) (rounding is monotonic), max z from the lm_head partials.
+__global__ void __launch_bounds__(kToppThreads) topp_prep_kernel(ToppArgs a) {
   pdl_launch_dependents();
   pdl_wait();
-  const int row = blockIdx.x;
-  if (!row_active[row]) return;
-  const float* z = logits + (size_t)row * V;
+  const int row = blockIdx.y;
+  if (!a.row_active[row]) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int per = (V + kToppThreads - 1) / kToppThreads;
-  const int v0 = min(V, tid * per), v1 = min(V, v0 + per);
   __shared__ float s_f[32];
   __shared__ unsigned long long s_u[32];
   __shared__ unsigned long long hist[256];
-  __shared__ unsigned long long s_above, s_thr;
-  __shared__ uint32_t s_prefix;
-  __shared__ int s_cnt[kToppThreads / 32];
-  __shared__ int s_vk;
-  // 1. max of u = fl(z * invT)
-  float mx = -INFINITY;
-  for (int v = v0; v < v1; ++v) mx = fmaxf(mx, __fmul_rn(z[v], invT));
-  mx = warp_max(mx);
-  if (lane == 0) s_f[wid] = mx;
+  if (tid < 256) hist[tid] = 0;
+  float mz = -INFINITY;
+  for (int c = tid; c < a.lp_grid; c += kToppThreads) mz = fmaxf(mz, a.lp_mlz[(size_t)row * a.lp_grid + c].x);
+  mz = warp_max(mz);
+  if (lane == 0) s_f[wid] = mz;
   __syncthreads();
-  mx = s_f[0];
-  for (int w = 1; w < kToppThreads / 32; ++w) mx = fmaxf(mx, s_f[w]);
-  // 2. integer mass W, threshold
+  mz = s_f[0];
+  for (int w = 1; w < kToppThreads / 32; ++w) mz = fmaxf(mz, s_f[w]);
+  const float mx = __fmul_rn(mz, a.invT);
+  const int per = (a.V + kToppBlocks - 1) / kToppBlocks;
+  const int lo = blockIdx.x * per, hi = min(a.V, lo + per);
+  const float* z = a.logits + (size_t)row * a.V;
+  uint32_t* eb = a.ebits + (size_t)row * a.V;
   unsigned long long wsum = 0;
-  for (int v = v0; v < v1; ++v) wsum += topp_w(expf_is(__fsub_rn(__fmul_rn(z[v], invT), mx)));
+  for (int b0 = lo; b0 < hi; b0 += kToppThreads) {
+    const int v = b0 + tid;
+    float e = 0.f;
+    if (v < hi) {
+      e = expf_is(__fsub_rn(__fmul_rn(z[v], a.invT), mx));
+      eb[v] = __float_as_uint(e);
+    }
+    const unsigned long long w = topp_w(e);
+    wsum += w;
+    // level-1 digit (top byte): few distinct values, so equal digits of a warp are combined
+    // first (labelled partition; 22-bit halves keep the 32-lane sums exact)
+    const uint32_t d = v < hi ? (__float_as_uint(e) >> 24) : 256u + lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const unsigned slo = __reduce_add_sync(peers, (unsigned)(w & 0x3FFFFFull));
+    const unsigned shi = __reduce_add_sync(peers, (unsigned)(w >> 22));
+    if (d < 256u && lane == __ffs(peers) - 1) atomicAdd(&hist[d], ((unsigned long long)shi << 22) + slo);
+  }
   for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
   if (lane == 0) s_u[wid] = wsum;
   __syncthreads();
   if (tid == 0) {
     unsigned long long W = 0;
     for (int w = 0; w < kToppThreads / 32; ++w) W += s_u[w];
-    s_thr = (unsigned long long)ceil(__dmul_rn((double)top_p, __ull2double_rn(W)));
+    a.wpart[row * kToppBlocks + blockIdx.x] = W;
+  }
+  if (tid < 256) a.hist1[((size_t)row * kToppBlocks + blockIdx.x) * 256 + tid] = hist[tid];
+}
+
+// Pass B (one CTA per row): W, thr = ceil(top_p * W) in binary64, the boundary value e* by
+// radix select (level 1 from pass A's histograms, then 3 x 8 bits) with the mass above it,
+// and the last boundary member v_k in ascending v.  Resets keys[row] for pass C.
+__global__ void __launch_bounds__(kToppThreads) topp_select_kernel(ToppArgs a) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int row = blockIdx.x;
+  if (!a.row_active[row]) return;
+  const int tid = threadIdx.x;
+  __shared__ unsigned long long hist[256];
+  __shared__ unsigned long long hist8[8 * 256];
+  __shared__ unsigned long long s_above, s_thr;
+  __shared__ uint32_t s_prefix;
+  __shared__ int s_vk;
+  const uint32_t* eb = a.ebits + (size_t)row * a.V;
+  if (tid < 256) {
+    unsigned long long h = 0;
+    for (int b = 0; b < kToppBlocks; ++b) h += a.hist1[((size_t)row * kToppBlocks + b) * 256 + tid];
+    hist[tid] = h;
+  }
+  if (tid == 0) {
+    unsigned long long W = 0;
+    for (int b = 0; b < kToppBlocks; ++b) W += a.wpart[row * kToppBlocks + b];
+    s_thr = (unsigned long long)ceil(__dmul_rn((double)a.top_p, __ull2double_rn(W)));
     s_above = 0;
     s_prefix = 0;
+    a.keys[row] = 0ull;
   }
-  // 3. radix select of the boundary value's bits, most significant byte first
+  __syncthreads();
   uint32_t mask = 0;
   for (int shift = 24; shift >= 0; shift -= 8) {
-    if (tid < 256) hist[tid] = 0;
-    __syncthreads();
-    const uint32_t prefix = s_prefix;
-    int cur = -1;
-    unsigned long long run = 0;  // runs of equal digits are added once (contention)
-    for (int v = v0; v < v1; ++v) {
-      const float e = expf_is(__fsub_rn(__fmul_rn(z[v], invT), mx));
-      const uint32_t b = __float_as_uint(e);
-      if ((b & mask) != prefix) continue;
-      const int d = (int)((b >> shift) & 255u);
-      if (d != cur) {
-        if (cur >= 0 && run) atomicAdd(&hist[cur], run);
-        cur = d;
-        run = 0;
+    if (shift < 24) {
+      for (int i = tid; i < 8 * 256; i += kToppThreads) hist8[i] = 0;
+      __syncthreads();
+      unsigned long long* hw = hist8 + ((tid >> 5) & 7) * 256;  // 8 copies: less contention
+      const uint32_t prefix = s_prefix;
+      for (int v0 = tid; v0 < a.V; v0 += 8 * kToppThreads) {  // 8 independent loads in flight
+        uint32_t b8[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int v = v0 + j * kToppThreads;
+          b8[j] = v < a.V ? __ldcg(eb + v) : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (b8[j] != 0xFFFFFFFFu && (b8[j] & mask) == prefix)
+            atomicAdd(&hw[(b8[j] >> shift) & 255u], topp_w(__uint_as_float(b8[j])));
       }
-      run += topp_w(e);
+      __syncthreads();
+      if (tid < 256) {
+        unsigned long long h = 0;
+        for (int c = 0; c < 8; ++c) h += hist8[c * 256 + tid];
+        hist[tid] = h;
+      }
+      __syncthreads();
     }
-    if (cur >= 0 && run) atomicAdd(&hist[cur], run);
-    __syncthreads();
     if (tid == 0) {
       unsigned long long acc = s_above;
       int d = 255;
@@ -1319,47 +1376,70 @@ __global__ void __launch_bounds__(kToppThreads) topp_kernel(const float* __restr
         acc += hist[d];
       }
       s_above = acc;
-      s_prefix = prefix | ((uint32_t)d << shift);
+      s_prefix |= (uint32_t)d << shift;
     }
     mask |= 255u << shift;
     __syncthreads();
   }
   const uint32_t bstar = s_prefix;
   const unsigned long long wb = topp_w(__uint_as_float(bstar));
-  const unsigned long long need = wb ? (s_thr - s_above + wb - 1) / wb : 1;  // members with e == e* (>= 1)
-  // 4. the need-th member of value e* in ascending v
+  const unsigned long long need = wb ? (s_thr - s_above + wb - 1) / wb : 1;  // boundary members (>= 1)
+  // the need-th v (ascending) with e == e*: thread t scans the contiguous range
+  // [t*per, (t+1)*per) (8 loads in flight), an exclusive scan of the counts over threads
+  // (in v order), and the thread holding the need-th hit rescans its range
+  __shared__ int s_cnt[kToppThreads / 32];
+  const int per = (a.V + kToppThreads - 1) / kToppThreads;
+  const int r0 = min(a.V, tid * per), r1 = min(a.V, r0 + per);
   int cnt = 0;
-  for (int v = v0; v < v1; ++v)
-    cnt += __float_as_uint(expf_is(__fsub_rn(__fmul_rn(z[v], invT), mx))) == bstar;
+  for (int v0 = r0; v0 < r1; v0 += 8) {
+    uint32_t b8[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b8[j] = v0 + j < r1 ? __ldcg(eb + v0 + j) : 0u;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) cnt += (v0 + j < r1) && b8[j] == bstar;
+  }
+  const int lane = tid & 31, wid = tid >> 5;
   int incl = cnt;
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
   if (lane == 31) s_cnt[wid] = incl;
+  if (tid == 0) s_vk = a.V - 1;
   __syncthreads();
   int before = incl - cnt;
   for (int w = 0; w < wid; ++w) before += s_cnt[w];
-  if (tid == 0) s_vk = V - 1;
-  __syncthreads();
   if ((unsigned long long)before < need && (unsigned long long)(before + cnt) >= need) {
     int k = before;
-    for (int v = v0; v < v1; ++v)
-      if (__float_as_uint(expf_is(__fsub_rn(__fmul_rn(z[v], invT), mx))) == bstar && ++k == (int)need) {
+    for (int v = r0; v < r1; ++v)
+      if (eb[v] == bstar && (unsigned long long)(++k) == need) {
         s_vk = v;
         break;
       }
   }
   __syncthreads();
-  const int vk = s_vk;
-  // 5. Gumbel-max over the nucleus (same key as the lm_head epilogue)
-  const uint32_t uid = (uint32_t)row_uid[row], t = (uint32_t)row_t[row];
+  if (tid == 0) a.sel[row] = make_int2((int)bstar, s_vk);
+}
+
+// Pass C (rows x kToppBlocks CTAs): Gumbel-max over the nucleus with the lm_head's scores.
+__global__ void __launch_bounds__(kToppThreads) topp_sample_kernel(ToppArgs a) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int row = blockIdx.y;
+  if (!a.row_active[row]) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  __shared__ unsigned long long s_u[32];
+  const int2 sl = a.sel[row];
+  const uint32_t bstar = (uint32_t)sl.x;
+  const int per = (a.V + kToppBlocks - 1) / kToppBlocks;
+  const int lo = blockIdx.x * per, hi = min(a.V, lo + per);
+  const uint32_t* eb = a.ebits + (size_t)row * a.V;
+  const float* sc = a.scores + (size_t)row * a.V;
   unsigned long long best = 0;
-  for (int v = v0; v < v1; ++v) {
-    const float u = __fmul_rn(z[v], invT);
-    const uint32_t b = __float_as_uint(expf_is(__fsub_rn(u, mx)));
-    if (b > bstar || (b == bstar && v <= vk)) {
-      const unsigned long long k = order_key(__fadd_rn(u, gumbel(seed, uid, t, (uint32_t)v)), (uint32_t)v);
+  for (int v = lo + tid; v < hi; v += kToppThreads) {
+    const uint32_t b = eb[v];
+    if (b > bstar || (b == bstar && v <= sl.y)) {
+      const unsigned long long k = order_key(sc[v], (uint32_t)v);
       best = k > best ? k : best;
     }
   }
@@ -1371,9 +1451,7 @@ __global__ void __launch_bounds__(kToppThreads) topp_kernel(const float* __restr
   __syncthreads();
   if (tid == 0) {
     for (int w = 1; w < kToppThreads / 32; ++w) best = s_u[w] > best ? s_u[w] : best;
-    best = s_u[0] > best ? s_u[0] : best;
-    keys[row] = best;
-    if (tok_z) tok_z[row] = z[0xFFFFFFFFu - (uint32_t)(best & 0xFFFFFFFFull)];
+    if (best) atomicMax(a.keys + row, best);
   }
 }
 }  // namespace isk

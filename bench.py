@@ -281,6 +281,16 @@ def run_ours(args):
         # the dominant kernel alone: every layer's gate/up launch as the step issues it, back to
         # back in one graph (4 passes over the layers), CUDA events around the replay
         gu_kernel = [ctx.is_profile_kernel(5, reps=4) for _ in range(3)]
+        # split attention at a mid-rollout step (suffixes of a few hundred tokens): the layer's
+        # prefix + suffix launches back to back; its algorithmic bytes = the shared prefix KV
+        # once + every live row's suffix KV
+        for _ in range(400):
+            ctx.is_decode_step()
+        s0 = ctx.is_query()["suffix_tokens"]
+        ctx.is_decode_step()
+        q1 = ctx.is_query()
+        attn_suffix = int(q1["suffix_tokens"] - s0)
+        attn_ms = float(np.median([ctx.is_profile_kernel(3, reps=4)[0] for _ in range(3)]))
     stq = ctx.is_query()
 
     t = torch.tensor([ms, ms_e2e, float(tokens)], device="cuda", dtype=torch.float64)
@@ -341,6 +351,17 @@ def run_ours(args):
                                   "interval includes one graph-node hop; median of 5 replays)"}
     roof["step_ms_graph_events"] = round(step_ms, 4)
     roof["step_ms_eager"] = round(step_ms_eager, 4)
+    if gu_kernel is not None:
+        kv_tok_layer = 2 * shape.n_kv_heads * shape.head_dim * 2
+        attn_bytes = (P - 1) * kv_tok_layer + attn_suffix * kv_tok_layer
+        roof["attention"] = {"bound": "hbm", "kernel": "split attention per layer (tcgen05 shared prefix + "
+                             "warp-per-chunk suffix + fused LSE merge)", "unit": "GB/s",
+                             "achieved": round(attn_bytes / (attn_ms * 1e-3) / 1e9, 1), "peak": hbm,
+                             "frac": round(attn_bytes / (attn_ms * 1e-3) / 1e9 / hbm, 4),
+                             "bytes_per_layer": int(attn_bytes), "suffix_tokens": attn_suffix,
+                             "layer_ms": round(attn_ms, 5),
+                             "timing": "step 401 of a rollout; all layers' attention launches back to back in "
+                                       "a graph, CUDA events (median of 3)"}
     roof["step_GBps"] = round(algorithmic_bytes_per_step(shape, g, 0, P) / (ms_max / max(steps_total, 1) * 1e-3) / 1e9, 1)
     roof["per_kind_ms"] = {k: round(v, 4) for k, v in per_kind.items() if n_launch_kind[k]}
     launches_per_step = int(st["launches_per_step"])  # counted by the library while capturing the step

@@ -283,8 +283,9 @@ is_status is_profile_step(is_ctx* ctx, float* h_ms, int32_t* h_kind, int32_t cap
  * nodes turn PDL edges into full dependencies).  Advances one decode step. */
 is_status is_profile_step_graph(is_ctx* ctx, float* h_ms, int32_t* h_kind, int32_t cap, int32_t* h_n);
 
-/* Average device duration (ms) of one launch of a decode GEMM kind (1 QKV,
- * 4 o_proj, 5 gate/up, 6 down), issued exactly as the decode step issues it
+/* Average device duration (ms) per layer of a decode kernel kind (1 QKV, 3 attention
+ * (the layer's shared-prefix + suffix launches), 4 o_proj, 5 gate/up, 6 down), issued
+ * exactly as the decode step issues it
  * (arguments, split, stages, PDL) for every layer, `reps` passes, back to back in
  * one CUDA graph timed with CUDA events on the context stream (one warm-up replay
  * first).  The launches write the step's scratch buffers (activations, residual),

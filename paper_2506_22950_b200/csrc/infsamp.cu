@@ -1921,10 +1921,11 @@ extern "C" is_status is_profile_kernel(is_ctx* c, int32_t kind, int32_t reps, fl
   int keep;
   switch (kind) {
     case 1: keep = 2; break;
+    case 3: keep = 8; break;  // attention: the layer's prefix + suffix launches
     case 4: keep = 16; break;
     case 5: keep = 32; break;
     case 6: keep = 64; break;
-    default: return fail(IS_ERR_CONFIG, "is_profile_kernel: kind %d is not a GEMM kind", kind);
+    default: return fail(IS_ERR_CONFIG, "is_profile_kernel: kind %d is not a GEMM or attention kind", kind);
   }
   if (reps < 1) return fail(IS_ERR_CONFIG, "reps must be >= 1");
   StreamGuard guard(c, c->user);
@@ -1957,7 +1958,7 @@ extern "C" is_status is_profile_kernel(is_ctx* c, int32_t kind, int32_t reps, fl
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaGraphExecDestroy(ge);
-  *h_ms_per_launch = n > 0 ? ms / n : 0.f;
+  *h_ms_per_launch = ms / (reps * c->sh.layers);  // per layer (kind 3: all of the layer's attention launches)
   if (h_launches) *h_launches = n;
   return IS_OK;
 }

@@ -325,11 +325,11 @@ def test_profile_hooks_then_decode_unchanged(lib, tiny):
     ctx.is_prefill(torch.as_tensor(tiny["prompt"], device="cuda"), 0)
     ctx.is_start_group(tiny["true"], tiny["pred"])
     ctx.is_decode_step()
-    for kind in (1, 4, 5, 6):
+    for kind in (1, 3, 4, 5, 6):
         ms, n = ctx.is_profile_kernel(kind, reps=2)
-        assert n == 2 * TINY.layers and 0 < ms < 1.0, (kind, ms, n)
+        assert n == (2 if kind == 3 else 1) * 2 * TINY.layers and 0 < ms < 1.0, (kind, ms, n)
     with pytest.raises(lib.InfsampError) as e:
-        ctx.is_profile_kernel(3)
+        ctx.is_profile_kernel(7)
     assert e.value.status == lib.IS_ERR_CONFIG
     for graph in (False, True):
         ms, kind = ctx.is_profile_step(graph=graph)

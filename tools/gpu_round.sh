@@ -18,4 +18,9 @@ IS_NO_GRAPH=1 timeout 900 ncu --set full --clock-control none --import-source on
   -k 'regex:attn' -s 56 -c 4 -o $OUT/attn python tools/step_driver.py --steps 2 > $OUT/ncu_attn.log 2>&1
 IS_NO_GRAPH=1 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k 'regex:gemm_swapab_kernel<\(int\)16, \(int\)3' -s 0 -c 1 -o $OUT/lmhead python tools/step_driver.py --steps 2 > $OUT/ncu_lmhead.log 2>&1
+# counters of the captures summarised here (ncu is on this box), the large .ncu-rep files kept
+# out of gpurun_out/ (the merge back is capped at 64 MiB)
+python tools/summarize_profiles.py $OUT $OUT/summary 60 > $OUT/summary.log 2>&1
+mkdir -p /tmp/ncu_reps && mv $OUT/*.ncu-rep /tmp/ncu_reps/ 2>/dev/null
+for f in $OUT/*.log $OUT/*.csv; do [ -f "$f" ] && [ $(stat -c %s "$f") -gt 8000000 ] && gzip -f "$f"; done
 echo done > $OUT/DONE

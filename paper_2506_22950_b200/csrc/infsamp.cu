@@ -460,6 +460,7 @@ struct is_ctx {
   uint32_t* ebits_tp;  //   e_v bits [max_rows][vocab]
   unsigned long long *wpart_tp, *hist_tp;  // per-slice mass, level-1 histograms
   int2* sel_tp;        //   per row (e*, v_k)
+  ToppState* state_tp; //   per row radix-select state
   unsigned int* fn_bar;  // [4] their grid barriers (o_proj, down)
   int32_t* attn_items;
   float* splitk_ws;  // split-K partials workspace
@@ -1176,8 +1177,15 @@ static is_status enqueue_step_body(is_ctx* c) {
     t.V = s.vocab;
     t.invT = a.inv_temp;
     t.top_p = c->cfg.top_p;
+    ToppState* ts = c->state_tp;
     CKS(launch_k(topp_prep_kernel, dim3(kToppBlocks, c->rc), dim3(kToppThreads), st, t));
-    CKS(launch_k(topp_select_kernel, dim3(c->rc), dim3(kToppThreads), st, t));
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      if (shift < 24) CKS(launch_k(topp_hist_kernel, dim3(kToppBlocks, c->rc), dim3(kToppThreads), st, t,
+                                   (const ToppState*)ts, shift));
+      CKS(launch_k(topp_pick_kernel, dim3(c->rc), dim3(256), st, t, ts, shift));
+    }
+    CKS(launch_k(topp_tiecount_kernel, dim3(kToppBlocks, c->rc), dim3(kToppThreads), st, t, (const ToppState*)ts));
+    CKS(launch_k(topp_tiepick_kernel, dim3(c->rc), dim3(kToppThreads), st, t, (const ToppState*)ts));
     CKS(launch_k(topp_sample_kernel, dim3(kToppBlocks, c->rc), dim3(kToppThreads), st, t));
   }
   prof_mark(st, 7);
@@ -1403,6 +1411,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->wpart_tp = c->topp ? (unsigned long long*)A((size_t)R * kToppBlocks * 8) : nullptr;
   c->hist_tp = c->topp ? (unsigned long long*)A((size_t)R * kToppBlocks * 256 * 8) : nullptr;
   c->sel_tp = c->topp ? (int2*)A((size_t)R * 8) : nullptr;
+  c->state_tp = c->topp ? (ToppState*)A((size_t)R * sizeof(ToppState)) : nullptr;
   c->attn_items = (int32_t*)A((size_t)Hkv * (c->nc_pre * ((c->rc + 3) / 4) + c->rc * c->nc_suf) * kItemStride * 4 + 64);
   c->rope_cos = (float*)A((size_t)c->max_pos * 64 * 4);
   c->rope_sin = (float*)A((size_t)c->max_pos * 64 * 4);
@@ -1534,7 +1543,7 @@ extern "C" void is_destroy(is_ctx* c) {
                   c->main_init, c->main_queue, c->free_stack, c->pagetab, c->npages, c->tokens, c->log_slot,
                   c->log_live, c->d_prompt_copy, c->lp_key, c->lp_mlz, c->logprobs, c->prow_active, c->prow_tok, c->prow_pos, c->prow_kvloc,
                   c->prow_len, c->fn_bar, c->logits_tp, c->scores_tp, c->ebits_tp, c->wpart_tp, c->hist_tp,
-                  c->sel_tp};
+                  c->sel_tp, c->state_tp};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (int i = 0; i < c->mk_nbufs; ++i) cudaFree(c->mk_bufs[i]);

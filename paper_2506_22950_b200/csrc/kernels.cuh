@@ -1244,6 +1244,24 @@ __device__ __forceinline__ unsigned long long topp_w(float e) {
 constexpr int kToppThreads = 1024;
 constexpr int kToppBlocks = 16;  // vocabulary slices per row for the parallel passes
 
+// Exact 64-bit mass histograms from 32-bit shared atomics: w < 2^45 is kept as three
+// 15-bit limbs; a slice holds < 2^14 elements, so every limb sum stays below 2^29.
+struct ToppHist {
+  unsigned int l[3][256];
+  __device__ __forceinline__ void clear(int tid) {
+    if (tid < 256) l[0][tid] = l[1][tid] = l[2][tid] = 0u;
+  }
+  __device__ __forceinline__ void add(uint32_t d, unsigned long long w) {
+    if (!w) return;
+    atomicAdd(&l[0][d], (unsigned)(w & 0x7FFFull));
+    atomicAdd(&l[1][d], (unsigned)((w >> 15) & 0x7FFFull));
+    atomicAdd(&l[2][d], (unsigned)(w >> 30));
+  }
+  __device__ __forceinline__ unsigned long long get(int d) const {
+    return (unsigned long long)l[0][d] + ((unsigned long long)l[1][d] << 15) + ((unsigned long long)l[2][d] << 30);
+  }
+};
+
 struct ToppArgs {
   const float* scores;       // [rows][V] fl(fl(z * invT) + G_v) from the lm_head epilogue
   const float* logits;       // [rows][V] z
@@ -1269,8 +1287,8 @@ __global__ void __launch_bounds__(kToppThreads) topp_prep_kernel(ToppArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   __shared__ float s_f[32];
   __shared__ unsigned long long s_u[32];
-  __shared__ unsigned long long hist[256];
-  if (tid < 256) hist[tid] = 0;
+  __shared__ ToppHist hist;
+  hist.clear(tid);
   float mz = -INFINITY;
   for (int c = tid; c < a.lp_grid; c += kToppThreads) mz = fmaxf(mz, a.lp_mlz[(size_t)row * a.lp_grid + c].x);
   mz = warp_max(mz);
@@ -1293,13 +1311,7 @@ __global__ void __launch_bounds__(kToppThreads) topp_prep_kernel(ToppArgs a) {
     }
     const unsigned long long w = topp_w(e);
     wsum += w;
-    // level-1 digit (top byte): few distinct values, so equal digits of a warp are combined
-    // first (labelled partition; 22-bit halves keep the 32-lane sums exact)
-    const uint32_t d = v < hi ? (__float_as_uint(e) >> 24) : 256u + lane;
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
-    const unsigned slo = __reduce_add_sync(peers, (unsigned)(w & 0x3FFFFFull));
-    const unsigned shi = __reduce_add_sync(peers, (unsigned)(w >> 22));
-    if (d < 256u && lane == __ffs(peers) - 1) atomicAdd(&hist[d], ((unsigned long long)shi << 22) + slo);
+    if (v < hi) hist.add(__float_as_uint(e) >> 24, w);  // level-1 digit: the top byte
   }
   for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
   if (lane == 0) s_u[wid] = wsum;
@@ -1309,110 +1321,143 @@ __global__ void __launch_bounds__(kToppThreads) topp_prep_kernel(ToppArgs a) {
     for (int w = 0; w < kToppThreads / 32; ++w) W += s_u[w];
     a.wpart[row * kToppBlocks + blockIdx.x] = W;
   }
-  if (tid < 256) a.hist1[((size_t)row * kToppBlocks + blockIdx.x) * 256 + tid] = hist[tid];
+  if (tid < 256) a.hist1[((size_t)row * kToppBlocks + blockIdx.x) * 256 + tid] = hist.get(tid);
 }
 
-// Pass B (one CTA per row): W, thr = ceil(top_p * W) in binary64, the boundary value e* by
-// radix select (level 1 from pass A's histograms, then 3 x 8 bits) with the mass above it,
-// and the last boundary member v_k in ascending v.  Resets keys[row] for pass C.
-__global__ void __launch_bounds__(kToppThreads) topp_select_kernel(ToppArgs a) {
+// Pass B, level by level (radix select of the boundary value e*, most significant byte
+// first): topp_pick_kernel sums the slices' histograms of the current byte and picks the
+// byte (one CTA per row); topp_hist_kernel builds the next byte's per-slice histograms over
+// the elements that match the picked prefix (rows x kToppBlocks CTAs, equal digits of a warp
+// combined as in pass A).  Level 1's histograms come from pass A.
+struct ToppState {
+  unsigned long long thr, above;  // nucleus threshold; integer mass strictly above the prefix
+  uint32_t prefix, mask;          // picked bytes of e*
+};
+
+__global__ void __launch_bounds__(256) topp_pick_kernel(ToppArgs a, ToppState* stt, int shift) {
   pdl_launch_dependents();
   pdl_wait();
   const int row = blockIdx.x;
   if (!a.row_active[row]) return;
   const int tid = threadIdx.x;
   __shared__ unsigned long long hist[256];
-  __shared__ unsigned long long hist8[8 * 256];
-  __shared__ unsigned long long s_above, s_thr;
-  __shared__ uint32_t s_prefix;
-  __shared__ int s_vk;
-  const uint32_t* eb = a.ebits + (size_t)row * a.V;
-  if (tid < 256) {
-    unsigned long long h = 0;
-    for (int b = 0; b < kToppBlocks; ++b) h += a.hist1[((size_t)row * kToppBlocks + b) * 256 + tid];
-    hist[tid] = h;
-  }
+  unsigned long long h = 0;
+  for (int b = 0; b < kToppBlocks; ++b) h += a.hist1[((size_t)row * kToppBlocks + b) * 256 + tid];
+  hist[tid] = h;
+  __syncthreads();
   if (tid == 0) {
-    unsigned long long W = 0;
-    for (int b = 0; b < kToppBlocks; ++b) W += a.wpart[row * kToppBlocks + b];
-    s_thr = (unsigned long long)ceil(__dmul_rn((double)a.top_p, __ull2double_rn(W)));
-    s_above = 0;
-    s_prefix = 0;
-    a.keys[row] = 0ull;
+    ToppState t = stt[row];
+    if (shift == 24) {
+      unsigned long long W = 0;
+      for (int b = 0; b < kToppBlocks; ++b) W += a.wpart[row * kToppBlocks + b];
+      t.thr = (unsigned long long)ceil(__dmul_rn((double)a.top_p, __ull2double_rn(W)));
+      t.above = 0;
+      t.prefix = 0;
+      t.mask = 0;
+      a.keys[row] = 0ull;  // pass C's atomicMax starts from zero
+    }
+    unsigned long long acc = t.above;
+    int d = 255;
+    for (; d > 0; --d) {
+      if (acc + hist[d] >= t.thr) break;
+      acc += hist[d];
+    }
+    t.above = acc;
+    t.prefix |= (uint32_t)d << shift;
+    t.mask |= 255u << shift;
+    stt[row] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kToppThreads) topp_hist_kernel(ToppArgs a, const ToppState* stt, int shift) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int row = blockIdx.y;
+  if (!a.row_active[row]) return;
+  const int tid = threadIdx.x;
+  __shared__ ToppHist hist;
+  hist.clear(tid);
+  __syncthreads();
+  const uint32_t prefix = stt[row].prefix, mask = stt[row].mask;
+  const int per = (a.V + kToppBlocks - 1) / kToppBlocks;
+  const int lo = blockIdx.x * per, hi = min(a.V, lo + per);
+  const uint32_t* eb = a.ebits + (size_t)row * a.V;
+  for (int b0 = lo; b0 < hi; b0 += kToppThreads) {
+    const int v = b0 + tid;
+    const uint32_t b = v < hi ? __ldcg(eb + v) : 0xFFFFFFFFu;
+    if (v < hi && (b & mask) == prefix) hist.add((b >> shift) & 255u, topp_w(__uint_as_float(b)));
   }
   __syncthreads();
-  uint32_t mask = 0;
-  for (int shift = 24; shift >= 0; shift -= 8) {
-    if (shift < 24) {
-      for (int i = tid; i < 8 * 256; i += kToppThreads) hist8[i] = 0;
-      __syncthreads();
-      unsigned long long* hw = hist8 + ((tid >> 5) & 7) * 256;  // 8 copies: less contention
-      const uint32_t prefix = s_prefix;
-      for (int v0 = tid; v0 < a.V; v0 += 8 * kToppThreads) {  // 8 independent loads in flight
-        uint32_t b8[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int v = v0 + j * kToppThreads;
-          b8[j] = v < a.V ? __ldcg(eb + v) : 0xFFFFFFFFu;
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (b8[j] != 0xFFFFFFFFu && (b8[j] & mask) == prefix)
-            atomicAdd(&hw[(b8[j] >> shift) & 255u], topp_w(__uint_as_float(b8[j])));
-      }
-      __syncthreads();
-      if (tid < 256) {
-        unsigned long long h = 0;
-        for (int c = 0; c < 8; ++c) h += hist8[c * 256 + tid];
-        hist[tid] = h;
-      }
-      __syncthreads();
-    }
-    if (tid == 0) {
-      unsigned long long acc = s_above;
-      int d = 255;
-      for (; d > 0; --d) {
-        if (acc + hist[d] >= s_thr) break;
-        acc += hist[d];
-      }
-      s_above = acc;
-      s_prefix |= (uint32_t)d << shift;
-    }
-    mask |= 255u << shift;
-    __syncthreads();
-  }
-  const uint32_t bstar = s_prefix;
-  const unsigned long long wb = topp_w(__uint_as_float(bstar));
-  const unsigned long long need = wb ? (s_thr - s_above + wb - 1) / wb : 1;  // boundary members (>= 1)
-  // the need-th v (ascending) with e == e*: thread t scans the contiguous range
-  // [t*per, (t+1)*per) (8 loads in flight), an exclusive scan of the counts over threads
-  // (in v order), and the thread holding the need-th hit rescans its range
-  __shared__ int s_cnt[kToppThreads / 32];
-  const int per = (a.V + kToppThreads - 1) / kToppThreads;
-  const int r0 = min(a.V, tid * per), r1 = min(a.V, r0 + per);
+  if (tid < 256) a.hist1[((size_t)row * kToppBlocks + blockIdx.x) * 256 + tid] = hist.get(tid);
+}
+
+// Boundary members (e == e*) per slice, then the need-th one in ascending v: the slice that
+// holds it is found from the counts, and one CTA scans that slice with contiguous ranges.
+__global__ void __launch_bounds__(kToppThreads) topp_tiecount_kernel(ToppArgs a, const ToppState* stt) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int row = blockIdx.y;
+  if (!a.row_active[row]) return;
+  const uint32_t bstar = stt[row].prefix;
+  const int per = (a.V + kToppBlocks - 1) / kToppBlocks;
+  const int lo = blockIdx.x * per, hi = min(a.V, lo + per);
+  const uint32_t* eb = a.ebits + (size_t)row * a.V;
   int cnt = 0;
-  for (int v0 = r0; v0 < r1; v0 += 8) {
-    uint32_t b8[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) b8[j] = v0 + j < r1 ? __ldcg(eb + v0 + j) : 0u;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) cnt += (v0 + j < r1) && b8[j] == bstar;
+  for (int v = lo + threadIdx.x; v < hi; v += kToppThreads) cnt += __ldcg(eb + v) == bstar;
+  __shared__ int s_c[kToppThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0) s_c[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < kToppThreads / 32; ++w) t += s_c[w];
+    reinterpret_cast<int*>(a.wpart)[row * kToppBlocks + blockIdx.x] = t;  // (pass A's masses are consumed)
   }
-  const int lane = tid & 31, wid = tid >> 5;
+}
+
+__global__ void __launch_bounds__(kToppThreads) topp_tiepick_kernel(ToppArgs a, const ToppState* stt) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int row = blockIdx.x;
+  if (!a.row_active[row]) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const ToppState t = stt[row];
+  const uint32_t bstar = t.prefix;
+  const unsigned long long wb = topp_w(__uint_as_float(bstar));
+  const unsigned long long need = wb ? (t.thr - t.above + wb - 1) / wb : 1;  // boundary members (>= 1)
+  const int* cnts = reinterpret_cast<const int*>(a.wpart) + row * kToppBlocks;
+  int blk = kToppBlocks - 1;
+  unsigned long long before = 0;
+  for (int b = 0; b < kToppBlocks; ++b) {
+    if (before + (unsigned long long)cnts[b] >= need) {
+      blk = b;
+      break;
+    }
+    before += cnts[b];
+  }
+  const int per = (a.V + kToppBlocks - 1) / kToppBlocks;
+  const int lo = blk * per, hi = min(a.V, lo + per);
+  const int pt = (hi - lo + kToppThreads - 1) / kToppThreads;
+  const int r0 = min(hi, lo + tid * pt), r1 = min(hi, r0 + pt);
+  const uint32_t* eb = a.ebits + (size_t)row * a.V;
+  int cnt = 0;
+  for (int v = r0; v < r1; ++v) cnt += __ldcg(eb + v) == bstar;
+  __shared__ int s_cnt[kToppThreads / 32];
+  __shared__ int s_vk;
   int incl = cnt;
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
   if (lane == 31) s_cnt[wid] = incl;
-  if (tid == 0) s_vk = a.V - 1;
+  if (tid == 0) s_vk = hi - 1;
   __syncthreads();
-  int before = incl - cnt;
-  for (int w = 0; w < wid; ++w) before += s_cnt[w];
-  if ((unsigned long long)before < need && (unsigned long long)(before + cnt) >= need) {
-    int k = before;
+  unsigned long long bef = before + (unsigned long long)(incl - cnt);
+  for (int w = 0; w < wid; ++w) bef += s_cnt[w];
+  if (bef < need && bef + (unsigned long long)cnt >= need) {
+    unsigned long long k = bef;
     for (int v = r0; v < r1; ++v)
-      if (eb[v] == bstar && (unsigned long long)(++k) == need) {
+      if (__ldcg(eb + v) == bstar && ++k == need) {
         s_vk = v;
         break;
       }

@@ -299,6 +299,13 @@ is_status is_profile_kernel(is_ctx* ctx, int32_t kind, int32_t reps, float* h_ms
 is_status is_dbg_gemm(const void* d_w, const void* d_x, float* d_y, int32_t M, int32_t K, int32_t rows,
                       int32_t split, void* stream);
 
+/* Kernel-level test hook of the top-p chain (R36) on caller logits: d_logits
+ * [rows][V] fp32 (V % 4 == 0), per-row Philox counters d_uid[rows] / d_t[rows];
+ * 0 < top_p < 1.  d_tok[rows] (device) receives the sampled tokens.  Synchronous;
+ * allocates its scratch per call. */
+is_status is_dbg_topp(const float* d_logits, int32_t rows, int32_t V, float temperature, float top_p, uint64_t seed,
+                      const int32_t* d_uid, const int32_t* d_t, int32_t* d_tok, void* stream);
+
 /* Debug hook of the persistent decode kernel: h_info[4] = {in use, grid, task
  * count, trace capacity}; copies the per-CTA task lists (int4 {kind | layer<<8 |
  * part<<16, tile, kb0, kb1}, h_tasks[4 * count]) and offsets (h_off[grid + 1])

@@ -18,7 +18,7 @@ ADV_MODES = {"std_norm": 0, "mean_only": 1}
 EXPORTS = ["is_plan", "is_create", "is_destroy", "is_prefill", "is_start_group", "is_decode_step",
            "is_refill", "is_run_group", "is_query", "is_copy_tokens", "is_copy_schedule",
            "is_group_results", "is_group_advantages", "is_set_logits_dump", "is_profile_step",
-           "is_profile_step_graph", "is_profile_kernel",
+           "is_profile_step_graph", "is_profile_kernel", "is_dbg_topp",
            "is_dbg_gemm", "is_dbg_mk_trace", "is_dbg_copy", "is_prefill_slot", "is_start_group_slot",
            "is_run_until_any_done", "is_query_slot", "is_copy_tokens_slot", "is_copy_schedule_slot",
            "is_group_results_slot", "is_nccl_unique_id", "is_nccl_comm_init", "is_allgather_results",
@@ -114,6 +114,7 @@ def load(build_if_missing=True):
     L.is_profile_step_graph.argtypes = [vp, vp, vp, i32, ctypes.POINTER(i32)]
     L.is_profile_kernel.argtypes = [vp, i32, i32, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32)]
     L.is_dbg_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]
+    L.is_dbg_topp.argtypes = [vp, i32, i32, ctypes.c_float, ctypes.c_float, ctypes.c_uint64, vp, vp, vp, vp]
     L.is_dbg_mk_trace.argtypes = [vp, vp, i32, vp, i32, vp, ctypes.c_int64, vp]
     L.is_dbg_copy.argtypes = [vp, i32, vp, ctypes.c_int64]
     L.is_prefill_slot.argtypes = [vp, i32, vp, i32]
@@ -204,6 +205,16 @@ def is_group_advantages(rewards, mode="std_norm"):
     a = np.zeros_like(r)
     _check(L.is_group_advantages(_np_ptr(r), len(r), ADV_MODES[mode], _np_ptr(a)))
     return a
+
+
+def is_dbg_topp(logits, uid, t, temperature, top_p, seed, stream=0):
+    """Top-p chain on device logits [rows][V] fp32 with int32 uid / t per row; returns tokens."""
+    import torch
+    rows, V = logits.shape
+    tok = torch.empty(rows, dtype=torch.int32, device=logits.device)
+    _check(load().is_dbg_topp(logits.data_ptr(), rows, V, float(temperature), float(top_p), int(seed),
+                              uid.data_ptr(), t.data_ptr(), tok.data_ptr(), stream))
+    return tok
 
 
 def is_dbg_gemm(w, x, y, split=1, stream=0):

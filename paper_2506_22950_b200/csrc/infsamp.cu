@@ -2294,3 +2294,61 @@ extern "C" is_status is_grpo_objective(const float* logp, const float* logp_old,
   *out = total / G;
   return IS_OK;
 }
+
+// ------------------------------------------------------------------ top-p test hook (R36)
+extern "C" is_status is_dbg_topp(const float* d_logits, int32_t rows, int32_t V, float temperature, float top_p,
+                                 uint64_t seed, const int32_t* d_uid, const int32_t* d_t, int32_t* d_tok, void* stream) {
+  if (!d_logits || !d_uid || !d_t || !d_tok || rows < 1 || V < 4 || V % 4 || !(temperature > 0) ||
+      !(top_p > 0.f && top_p < 1.f))
+    return fail(IS_ERR_CONFIG, "bad is_dbg_topp arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  is_status err = IS_OK;
+  float *scores = (float*)dalloc((size_t)rows * V * 4, &err);
+  float4* mlz = (float4*)dalloc((size_t)rows * 16, &err);
+  uint32_t* ebits = (uint32_t*)dalloc((size_t)rows * V * 4, &err);
+  unsigned long long* wpart = (unsigned long long*)dalloc((size_t)rows * kToppBlocks * 8, &err);
+  unsigned long long* hist = (unsigned long long*)dalloc((size_t)rows * kToppBlocks * 256 * 8, &err);
+  int2* sel = (int2*)dalloc((size_t)rows * 8, &err);
+  ToppState* ts = (ToppState*)dalloc((size_t)rows * sizeof(ToppState), &err);
+  int32_t* active = (int32_t*)dalloc((size_t)rows * 4, &err);
+  unsigned long long* keys = (unsigned long long*)dalloc((size_t)rows * 8, &err);
+  if (err == IS_OK) {
+    std::vector<int32_t> ones(rows, 1);
+    cudaMemcpy(active, ones.data(), rows * 4, cudaMemcpyHostToDevice);
+    const float invT = (float)(1.0 / (double)temperature);
+    topp_dbg_scores_kernel<<<rows, kToppThreads, 0, st>>>(d_logits, V, d_uid, d_t, seed, invT, scores, mlz);
+    ToppArgs t{};
+    t.scores = scores;
+    t.logits = d_logits;
+    t.lp_mlz = mlz;
+    t.lp_grid = 1;
+    t.ebits = ebits;
+    t.wpart = wpart;
+    t.hist1 = hist;
+    t.sel = sel;
+    t.row_active = active;
+    t.keys = keys;
+    t.V = V;
+    t.invT = invT;
+    t.top_p = top_p;
+    topp_prep_kernel<<<dim3(kToppBlocks, rows), kToppThreads, 0, st>>>(t);
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      if (shift < 24) topp_hist_kernel<<<dim3(kToppBlocks, rows), kToppThreads, 0, st>>>(t, ts, shift);
+      topp_pick_kernel<<<rows, 256, 0, st>>>(t, ts, shift);
+    }
+    topp_tiecount_kernel<<<dim3(kToppBlocks, rows), kToppThreads, 0, st>>>(t, ts);
+    topp_tiepick_kernel<<<rows, kToppThreads, 0, st>>>(t, ts);
+    topp_sample_kernel<<<dim3(kToppBlocks, rows), kToppThreads, 0, st>>>(t);
+    std::vector<unsigned long long> hk(rows);
+    cudaMemcpyAsync(hk.data(), keys, rows * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    std::vector<int32_t> tok(rows);
+    for (int r = 0; r < rows; ++r) tok[r] = (int32_t)(0xFFFFFFFFu - (uint32_t)(hk[r] & 0xFFFFFFFFull));
+    cudaMemcpy(d_tok, tok.data(), rows * 4, cudaMemcpyHostToDevice);
+    if (cudaGetLastError() != cudaSuccess) err = fail(IS_ERR_CUDA, "is_dbg_topp kernels failed");
+  }
+  for (void* p : {(void*)scores, (void*)mlz, (void*)ebits, (void*)wpart, (void*)hist, (void*)sel, (void*)ts,
+                  (void*)active, (void*)keys})
+    if (p) cudaFree(p);
+  return err;
+}

@@ -1499,4 +1499,28 @@ __global__ void __launch_bounds__(kToppThreads) topp_sample_kernel(ToppArgs a) {
     if (best) atomicMax(a.keys + row, best);
   }
 }
+
+// Test hook for the top-p chain on caller logits: per row, the lm_head's contribution
+// (Gumbel scores, and the row max as a one-entry partial list).
+__global__ void __launch_bounds__(kToppThreads) topp_dbg_scores_kernel(const float* __restrict__ z, int V,
+                                                                       const int32_t* __restrict__ uid,
+                                                                       const int32_t* __restrict__ t, uint64_t seed,
+                                                                       float invT, float* scores, float4* mlz) {
+  const int row = blockIdx.x, tid = threadIdx.x;
+  __shared__ float s_f[32];
+  float mz = -INFINITY;
+  for (int v = tid; v < V; v += kToppThreads) {
+    const float x = z[(size_t)row * V + v];
+    mz = fmaxf(mz, x);
+    scores[(size_t)row * V + v] = __fadd_rn(__fmul_rn(x, invT), gumbel(seed, (uint32_t)uid[row], (uint32_t)t[row], (uint32_t)v));
+  }
+  mz = warp_max(mz);
+  if ((tid & 31) == 0) s_f[tid >> 5] = mz;
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < kToppThreads / 32; ++w) mz = fmaxf(mz, s_f[w]);
+    mz = fmaxf(mz, s_f[0]);
+    mlz[row] = make_float4(mz, 0.f, 0.f, 0.f);
+  }
+}
 }  // namespace isk

@@ -404,3 +404,33 @@ def test_tiny_topp_sampler_bit_exact(lib, tiny, top_p):
     assert n == int(np.sum(tiny["true"]))
     if top_p <= 0.5:
         assert in_nucleus_only > 0      # the nucleus actually changed some draws
+
+
+@pytest.mark.parametrize("case", ["random", "all_equal", "quantised", "dominant", "vocab_151936"])
+def test_topp_chain_edge_cases_bit_exact(lib, case):
+    """The top-p kernels alone (is_dbg_topp) on synthetic logits with the edge cases of R36:
+    every element tied, a few quantised levels (ties at the boundary), one dominant logit,
+    and the full Qwen3 vocabulary; tokens equal the oracle's bit for bit."""
+    rng = np.random.default_rng({"random": 1, "all_equal": 2, "quantised": 3, "dominant": 4,
+                                 "vocab_151936": 5}[case])
+    rows, V = (8, 151936) if case == "vocab_151936" else (16, 4096)
+    z = rng.normal(size=(rows, V)).astype(np.float32) * np.float32(2.0)
+    if case == "all_equal":
+        z[:] = 0.0
+    elif case == "quantised":
+        z = (np.round(z * 2) / 2).astype(np.float32)
+    elif case == "dominant":
+        z[:, 7] = 20.0
+    uid = np.arange(rows, dtype=np.int32) * 3 + 1
+    t = np.arange(rows, dtype=np.int32) + 5
+    for top_p in (0.05, 0.3, 0.9, 0.999):
+        got = lib.is_dbg_topp(torch.as_tensor(z, device="cuda"), torch.as_tensor(uid, device="cuda"),
+                              torch.as_tensor(t, device="cuda"), 0.8, top_p, SEED).cpu().numpy()
+        for r in range(rows):
+            ref = sampler.sample_token_topp(z[r], SEED, int(uid[r]), int(t[r]), 0.8, top_p)
+            assert got[r] == ref, (case, top_p, r, got[r], ref)
+        if case == "all_equal":   # nucleus = the first ceil(top_p * V) ids
+            k = -(-int(np.ceil(float(np.float32(top_p)) * float(V * 2 ** 44))) // 2 ** 44)
+            assert np.all(got < k)
+        if case == "dominant" and top_p < 0.9:
+            assert np.all(got == 7)

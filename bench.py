@@ -169,7 +169,8 @@ def run_ours(args):
         budget = 1 << 30
     w = gen_weights(shape, seed=SEED, device="cuda")
     cfg = _lib.make_config(shape, G, g, max_new, P, mode="infinite", prefix_k=C["prefix_k"],
-                           page_tokens=page_tokens, kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED)
+                           page_tokens=page_tokens, kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED,
+                           top_p=args.top_p)
     ctx = _lib.Context(cfg, w)
     del w
     torch.cuda.empty_cache()
@@ -373,7 +374,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"config {args.config}: {C['desc']}", "model": C["shape"] + " (random init)",
-                   "G": G, "g": g, "prompt_len": P, "max_new_tokens": max_new, "length_family": C["family"],
+                   "top_p": args.top_p, "G": G, "g": g, "prompt_len": P, "max_new_tokens": max_new, "length_family": C["family"],
                    "kv_budget_bytes": budget, "global_batch": G * world, "seq_len": P + max_new,
                    "parallelism": f"dp{world} (prompt-sharded)", "step": "one GRPO-group rollout",
                    "exchange": EXCHANGE["path"],
@@ -425,7 +426,8 @@ def run_groups(args):
         budget = 1 << 30
     w = gen_weights(shape, seed=SEED, device="cuda")
     cfg = _lib.make_config(shape, G, g, max_new, P, mode="infinite", prefix_k=C["prefix_k"], page_tokens=16,
-                           kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED, max_groups=M)
+                           kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED, max_groups=M,
+                           top_p=args.top_p)
     ctx = _lib.Context(cfg, w)
     del w
     torch.cuda.empty_cache()
@@ -506,7 +508,7 @@ def run_groups(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"config {args.config} x {M} co-resident groups (SURVEY §8f NEXT-1): {C['desc']}",
-                       "model": C["shape"] + " (random init)", "G": G, "g": g, "groups": M,
+                       "model": C["shape"] + " (random init)", "top_p": args.top_p, "G": G, "g": g, "groups": M,
                        "prompts_timed": len(timed), "kv_budget_bytes_per_group": budget,
                        "step": f"{M} GRPO-group rollouts through {M} group slots",
                        "parallelism": f"dp{world} (prompt-sharded)"},
@@ -587,13 +589,16 @@ def _oracle_tokens_per_s(C, budget_s, step_seed=0):
     n = 0
     while True:
         z = M.forward(w, shape, seq, mirror=True, logit_rows=[len(seq) - 1])[0]
-        tok = sampler.sample_token(z.astype(np.float32), SEED, step_seed * C["G"], n)
+        tok = sampler.sample_token_topp(z.astype(np.float32), SEED, step_seed * C["G"], n, 0.8, TOP_P[0])
         seq.append(tok)
         n += 1
         if time.perf_counter() - t0 > budget_s:
             break
     dt = time.perf_counter() - t0
     return n, dt
+
+
+TOP_P = [1.0]   # bench --top-p (1 = the paper's plain temperature sampling)
 
 
 def cpu_baseline(C, budget_s=20.0):
@@ -620,7 +625,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": "tokens/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_tot / args.steps * 1e3, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config {args.config}: {C['desc']}", "step": "oracle decodes 1 token (full recompute)"},
+        "config": {"workload": f"config {args.config}: {C['desc']}", "top_p": args.top_p,
+                   "step": "oracle decodes 1 token (full recompute)"},
         "cpu_baseline": {"value": round(v, 5), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "oracle",
                          "sample": f"{n_tot} tokens, 1 per step, full-recompute fp64 oracle on host cores"},
         "e2e": {"value": round(v, 5), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -635,6 +641,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--top-p", type=float, default=1.0,
+                    help="nucleus sampling (SURVEY §8f NEXT-4, DESIGN R36); 1 = the paper's setting")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--placement", default="lpt", choices=["lpt", "block"],
                     help="N>1: timed prompts placed on ranks by LPT on predicted work, or contiguous blocks")
@@ -643,6 +651,7 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    TOP_P[0] = args.top_p
     if args.impl == "reference":
         run_reference(args)
     elif args.groups > 1:

@@ -347,6 +347,9 @@ static is_status launch_gemm(int BN, const CUtensorMap& tA, const CUtensorMap& t
   // deeper weight ring for a split-K GEMM (more of its weights arrive before the PDL wait returns)
   if (!deep && BN == 16 && stages == 6) return launch_gemm_s<16, EPI, 6>(tA, tB, a, st);
   if (!deep && BN == 16 && stages == 8) return launch_gemm_s<16, EPI, 8>(tA, tB, a, st);
+  // lm_head (persistent, one CTA per SM): more bytes in flight per SM (IS_STG_LM)
+  if (EPI == EPI_SAMPLE && deep && BN == 16 && stages == 10) return launch_gemm_s<16, EPI, 10>(tA, tB, a, st);
+  if (EPI == EPI_SAMPLE && deep && BN == 16 && stages == 11) return launch_gemm_s<16, EPI, 11>(tA, tB, a, st);
   switch (BN * 2 + (deep ? 1 : 0)) {
     case 32: return launch_gemm_t<16, EPI, false>(tA, tB, a, st);
     case 33: return launch_gemm_t<16, EPI, true>(tA, tB, a, st);
@@ -453,6 +456,7 @@ struct is_ctx {
   int* merge_cnt;  // [max_rows][Hkv] fused-merge counters (decode, tcgen05 prefix)
   float *ssqA, *ssqB;  // [Th][max_rows] per-128-column sums of squares: QKV input, gate/up input
   int bnorm;           // decode: RMSNorm folded into the QKV / gate-up B operand
+  int stg_lm;          // lm_head ring depth override (IS_STG_LM = 10 / 11; default 8)
   int fuse_norm;       // decode: RMSNorm of the new residual fused into the o_proj / down epilogues
   int topp;            // 0 < top_p < 1: nucleus sampling pass after the lm_head (R36)
   float* logits_tp;    //   its fp32 logits [max_rows][vocab]
@@ -1161,7 +1165,7 @@ static is_status enqueue_step_body(is_ctx* c) {
   a.seed = c->cfg.seed;
   a.inv_temp = (float)(1.0 / (double)c->cfg.temperature);
   g_splitk_ws = c->splitk_ws;
-  CKS(launch_gemm<EPI_SAMPLE>(c->BN, c->tm_embed, c->tm_xn_dec, a, st));
+  CKS(launch_gemm<EPI_SAMPLE>(c->BN, c->tm_embed, c->tm_xn_dec, a, st, c->stg_lm));
   if (c->topp) {  // top-p < 1 (R36): the nucleus and its Gumbel-max replace the full-vocabulary key
     ToppArgs t{};
     t.scores = c->scores_tp;
@@ -1508,6 +1512,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->stg_o = getenv("IS_STG_O") ? atoi(getenv("IS_STG_O")) : 0;
   c->stg_gu = getenv("IS_STG_GU") ? atoi(getenv("IS_STG_GU")) : 0;
   c->stg_d = getenv("IS_STG_D") ? atoi(getenv("IS_STG_D")) : 0;
+  c->stg_lm = getenv("IS_STG_LM") ? atoi(getenv("IS_STG_LM")) : 0;
   // per-GEMM split experiments (timing only)
   if (const char* e = getenv("IS_SPLIT_QKV")) c->split_qkv = std::max(1, std::min(8, atoi(e)));
   if (const char* e = getenv("IS_SPLIT_O")) c->split_o = std::max(1, std::min(8, atoi(e)));

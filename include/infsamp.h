@@ -84,6 +84,10 @@ typedef struct {
                               rows m*g .. m*g+g-1; kv_budget_bytes is per group, the page pool
                               (max_groups x the per-group pool) is shared.  max_groups*g <= 64 */
   int32_t dynamic_target;  /* IS_MODE_DYNAMIC: completions to stop at (0 = G); 0 in every other mode */
+  int32_t eos_enabled;     /* R37 (SURVEY a8 "or token == eos if enabled"): 0 = trace-driven termination
+                              only (R5, the parity setting); 1 = a sample also finishes when it samples
+                              eos_id (its length is then shorter than true_len).  Needs prefix_k == 0 */
+  int32_t eos_id;
   float top_p;             /* nucleus sampling (DESIGN R36): 0 < top_p < 1 samples the
                               Gumbel-max token inside the top-p nucleus (integer-exact mass, fixed-
                               sequence exp); 0 or 1 = off (the paper's plain temperature sampling).

@@ -45,7 +45,8 @@ class Config(ctypes.Structure):
                 ("row_capacity", ctypes.c_int32), ("kv_budget_bytes", ctypes.c_int64),
                 ("eps", ctypes.c_double), ("temperature", ctypes.c_float), ("seed", ctypes.c_uint64),
                 ("mode", ctypes.c_int32), ("decode_impl", ctypes.c_int32), ("max_groups", ctypes.c_int32),
-                ("dynamic_target", ctypes.c_int32), ("top_p", ctypes.c_float)]
+                ("dynamic_target", ctypes.c_int32), ("eos_enabled", ctypes.c_int32), ("eos_id", ctypes.c_int32),
+                ("top_p", ctypes.c_float)]
 
 
 class PlanOut(ctypes.Structure):
@@ -154,7 +155,7 @@ def _np_ptr(a):
 
 def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix_k=0, page_tokens=16,
                 row_capacity=0, kv_budget_bytes=0, eps=0.1, temperature=0.8, seed=20261017, decode_impl=None,
-                max_groups=1, dynamic_target=0, top_p=1.0):
+                max_groups=1, dynamic_target=0, top_p=1.0, eos_id=None):
     """decode_impl: 0 = persistent decode kernel, 1 = one kernel per operator (default: it is
     faster on B200); None reads IS_DECODE_IMPL from the environment."""
     c = Config()
@@ -170,6 +171,7 @@ def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix
     c.max_groups = max_groups
     c.dynamic_target = dynamic_target
     c.top_p = top_p
+    c.eos_enabled, c.eos_id = (0, 0) if eos_id is None else (1, int(eos_id))
     return c
 
 

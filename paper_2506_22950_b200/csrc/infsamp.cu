@@ -78,6 +78,8 @@ static is_status check_config(const is_config* c) {
   if (!(c->temperature > 0)) return fail(IS_ERR_CONFIG, "temperature must be > 0");
   if (!(c->top_p >= 0.f && c->top_p <= 1.f)) return fail(IS_ERR_CONFIG, "top_p must be in [0, 1] (0 or 1 = off)");
   if (c->mode < IS_MODE_FULL || c->mode > IS_MODE_DYNAMIC) return fail(IS_ERR_CONFIG, "unknown mode %d", (int)c->mode);
+  if (c->eos_enabled && (c->eos_id < 0 || c->eos_id >= s.vocab || c->prefix_k > 0))
+    return fail(IS_ERR_CONFIG, "eos_id must be a token id (0..vocab-1) and needs prefix_k == 0 (R37)");
   if (c->dynamic_target < 0 || c->dynamic_target > c->G || (c->dynamic_target > 0 && c->mode != IS_MODE_DYNAMIC))
     return fail(IS_ERR_CONFIG, "dynamic_target must be 0 or 1..G (got %d) and needs IS_MODE_DYNAMIC", c->dynamic_target);
   if (c->max_groups < 0 || n_groups(c) > 8 || n_groups(c) * g > 64)
@@ -562,6 +564,8 @@ static SchedArgs sched_args(is_ctx* c) {
   a.lp_grid = c->lp_grid;
   a.tok_logits = c->topp ? (c->logits_dump ? c->logits_dump : c->logits_tp) : nullptr;
   a.vocab = c->sh.vocab;
+  a.eos_on = c->cfg.eos_enabled ? 1 : 0;
+  a.eos_id = c->cfg.eos_id;
   a.last_tok = c->last_tok;
   a.last_fin = c->last_fin;
   a.row_active = c->row_active;

@@ -904,6 +904,7 @@ struct SchedArgs {
   float* logprobs;           // [M][G][max_new] log pi(token) at temperature 1 (R33)
   const float* tok_logits;   // top-p (R36): [rows][vocab] logits; the sampled token's logit is read there
   int vocab;
+  int eos_on, eos_id;        // R37: a sample also finishes when it samples eos_id
   int lp_grid;
   int32_t* last_tok;         // [row_cap]
   uint8_t* last_fin;         // [row_cap]
@@ -993,7 +994,7 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
         for (int s = 0; s < a.g; ++s) {  // ascending slot index
           const int uid = slot_uid[s];
           if (uid < 0) continue;
-          if (tt_[uid] == true_len[uid]) {
+          if (tt_[uid] == true_len[uid] || (a.eos_on && tokens[(size_t)uid * a.max_new + tt_[uid] - 1] == a.eos_id)) {
             st[ST_DONE] += 1;
             a.last_fin[m * a.g + s] = 1;
             for (int i = 0; i < npages[uid]; ++i) a.free_stack[st0[ST_FREE_TOP]++] = pagetab[(size_t)uid * a.maxp + i];
@@ -1205,10 +1206,15 @@ __global__ void results_kernel(const int32_t* __restrict__ tokens, const int32_t
                                int max_new, int vocab, float* reward, int32_t* len) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= G) return;
-  int c = 0;
-  const int L = true_len[i];
-  for (int t = 0; t < L; ++t) c += tokens[(size_t)i * max_new + t] < vocab / 2;
-  reward[i] = (float)c / (float)L;
+  // emitted length: true_len, or fewer when the sample stopped at EOS (R37) or was
+  // discarded in flight (dynamic mode, R35); tokens past it are -1
+  int c = 0, L = 0;
+  const int T = true_len[i];
+  while (L < T && tokens[(size_t)i * max_new + L] >= 0) {
+    c += tokens[(size_t)i * max_new + L] < vocab / 2;
+    ++L;
+  }
+  reward[i] = L ? (float)c / (float)L : 0.f;
   len[i] = L;
 }
 

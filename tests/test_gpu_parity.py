@@ -62,10 +62,10 @@ def _tiny_setup():
 
 
 def _run(lib, w_dev, prompt, true, pred, mode, g, budget=0, prefix_k=0, pt=16, rc=16, logits=False, impl=0,
-         target=0, top_p=1.0):
+         target=0, top_p=1.0, eos_id=None):
     cfg = lib.make_config(TINY, len(true), g, 32, 16, mode=mode, prefix_k=prefix_k, page_tokens=pt, row_capacity=rc,
                           kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED, decode_impl=impl,
-                          dynamic_target=target, top_p=top_p)
+                          dynamic_target=target, top_p=top_p, eos_id=eos_id)
     ctx = lib.Context(cfg, w_dev)
     ctx.is_prefill(torch.as_tensor(prompt, device="cuda"), 0)
     ctx.is_start_group(true, pred)
@@ -434,3 +434,30 @@ def test_topp_chain_edge_cases_bit_exact(lib, case):
             assert np.all(got < k)
         if case == "dominant" and top_p < 0.9:
             assert np.all(got == 7)
+
+
+def test_tiny_eos_termination(lib, tiny):
+    """R37 (SURVEY a8 "or token == eos if enabled"): with eos_id set, a sample stops at its first
+    eos token.  Tokens are schedule-independent (batch invariance), so the effective lengths
+    follow from the trace-driven run; the schedule then equals the oracle simulation on those
+    lengths, tokens are the trace-driven ones truncated, and is_group_results reports them."""
+    base = tiny["runs"]["infinite"]["tokens"]
+    true = np.asarray(tiny["true"])
+    eos = int(base[0, min(3, true[0] - 1)])
+    eff = []
+    for i, L in enumerate(true):
+        hit = np.nonzero(base[i, :L] == eos)[0]
+        eff.append(int(hit[0]) + 1 if len(hit) else int(L))
+    assert eff[0] < true[0] or true[0] <= 4
+    r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "infinite", 2,
+             budget=tiny["budget"], impl=tiny["impl"], eos_id=eos)
+    ref = simulator.simulate(eff, "infinite", 2, pred=tiny["pred"], eps=0.1, page_tokens=16)
+    assert r["stats"]["completed"] == 8 and r["stats"]["error"] == 0
+    assert r["slots"].tolist() == ref.slot_table and r["live"].tolist() == ref.live_pages
+    assert r["stats"]["tokens_decoded"] == sum(eff)
+    for i, L in enumerate(eff):
+        assert np.array_equal(r["tokens"][i, :L], base[i, :L]) and np.all(r["tokens"][i, L:] == -1)
+    with pytest.raises(lib.InfsampError) as e:
+        lib.Context(lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", prefix_k=4, page_tokens=4,
+                                    eos_id=eos), tiny["w_dev"])
+    assert e.value.status == lib.IS_ERR_CONFIG

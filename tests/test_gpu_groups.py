@@ -108,3 +108,38 @@ def test_groups_tokens_equal_single_group_runs(multi):
 
 def test_groups_shared_pool_within_budget(multi):
     assert multi["peak"] <= M * multi["budget"]
+
+
+def test_groups_dynamic_mode_each_group_as_alone(lib):
+    """Dynamic-slot sampling (R35) with co-resident groups: every group stops at its own
+    target-th completion; its schedule equals the single-group oracle simulation and its
+    completed samples' tokens equal a single-group context's."""
+    w_dev = {k: v.cuda() for k, v in gen_weights(TINY, seed=SEED).items()}
+    target = 5
+    cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="dynamic", row_capacity=16, seed=SEED, max_groups=3,
+                          dynamic_target=target)
+    ctx = lib.Context(cfg, w_dev)
+    groups = {pid: _group(pid) for pid in range(3)}
+    for slot, (p, t, pr) in groups.items():
+        ctx.is_prefill(torch.as_tensor(p, device="cuda"), slot, slot=slot)
+        ctx.is_start_group(t, pr, slot=slot)
+    done = 0
+    while done != 0b111:
+        mask, _ = ctx.is_run_until_any_done()
+        done |= mask
+    res = {s: (ctx.is_query(s), ctx.is_copy_schedule(slot=s), ctx.is_copy_tokens(s)) for s in range(3)}
+    ctx.close()
+    for s, (st, (slots, live), toks) in res.items():
+        _, true, _ = groups[s]
+        ref = simulator.simulate(true, "dynamic", 2, page_tokens=16, target=target)
+        assert st["completed"] == target and st["discarded"] == len(ref.discarded), s
+        assert slots.tolist() == ref.slot_table and live.tolist() == ref.live_pages, s
+        c1 = lib.Context(lib.make_config(TINY, 8, 2, 32, 16, mode="dynamic", row_capacity=16, seed=SEED,
+                                         dynamic_target=target), w_dev)
+        c1.is_prefill(torch.as_tensor(groups[s][0], device="cuda"), s)
+        c1.is_start_group(true, groups[s][2])
+        c1.is_run_group()
+        alone = c1.is_copy_tokens()
+        c1.close()
+        for uid in ref.finish_step:
+            assert np.array_equal(toks[uid], alone[uid]), (s, uid)

@@ -366,10 +366,12 @@ static is_status launch_gemm(int BN, const CUtensorMap& tA, const CUtensorMap& t
 // Split-K so that tiles * split fills at most one CTA per SM: a GEMM never
 // takes more than half an SM, so the next kernel's CTAs (PDL) co-reside and
 // prefetch their weights while this one drains.
-static int choose_split(int num_tiles, int kb_total, int /*BN*/) {
+static int choose_split(int num_tiles, int kb_total, int BN) {
   if (num_tiles > g_num_sms) return 1;
   int s = std::max(1, g_num_sms / num_tiles);
-  if (s == 1) s = 2;  // 75..148 tiles: a 2-CTA cluster per tile keeps every SM streaming (gate/up: -5%/step)
+  // 75..148 tiles: a 2-CTA cluster per tile keeps every SM streaming (gate/up: -5%/step at 16 rows);
+  // with 32 or 64 rows the cluster exchange costs more than it saves (+8% tokens/s with split 1)
+  if (s == 1) s = BN <= 16 ? 2 : 1;
   s = std::min(s, 8);
   s = std::min(s, kb_total);
   return std::max(s, 1);
@@ -458,6 +460,7 @@ struct is_ctx {
   int* merge_cnt;  // [max_rows][Hkv] fused-merge counters (decode, tcgen05 prefix)
   float *ssqA, *ssqB;  // [Th][max_rows] per-128-column sums of squares: QKV input, gate/up input
   int bnorm;           // decode: RMSNorm folded into the QKV / gate-up B operand
+  int sep_merge;       // decode suffix: 64-token CTA units + separate merge kernel (else warp units, fused merge)
   int stg_lm;          // lm_head ring depth override (IS_STG_LM = 10 / 11; default 8)
   int fuse_norm;       // decode: RMSNorm of the new residual fused into the o_proj / down epilogues
   int topp;            // 0 < top_p < 1: nucleus sampling pass after the lm_head (R36)
@@ -742,7 +745,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
     aa.nc_pre = prefill ? c->nc_pre : c->nc_pre_dec;
     aa.nc_suf = prefill ? 0 : c->nc_suf;
     aa.tc_prefix = prefill ? 0 : c->tc_prefix;
-    aa.merge_cnt = (!prefill && c->tc_prefix && !getenv("IS_SEPARATE_MERGE")) ? c->merge_cnt : nullptr;
+    aa.merge_cnt = (!prefill && c->tc_prefix && !c->sep_merge) ? c->merge_cnt : nullptr;
     aa.sc = prefill ? kSC : c->sc;
     aa.NC = c->NC;
     aa.prefill = prefill ? 1 : 0;
@@ -1322,7 +1325,13 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
     c->nc_pre_dec = c->tc_prefix ? (int)ceil_div64(c->pcap, 128) : c->nc_pre;
   }
   // decode suffix chunk: 32-token warp units behind the tcgen05 prefix, else 64-token CTA units
-  c->sc = (c->tc_prefix && !getenv("IS_SEPARATE_MERGE")) ? kSCW : kSC;
+  // (>= 32 rows, i.e. co-resident groups: the 64-token CTA units with the separate merge kernel
+  //  measured 3% faster, profiles/r01g/groups_*; IS_SEPARATE_MERGE=0/1 overrides)
+  {
+    const char* e = getenv("IS_SEPARATE_MERGE");
+    c->sep_merge = e ? atoi(e) != 0 : c->rc >= 32;
+  }
+  c->sc = (c->tc_prefix && !c->sep_merge) ? kSCW : kSC;
   c->nc_suf = (int)ceil_div64(c->max_new, c->sc);
   c->NC = c->nc_pre + c->nc_suf;
   // partials one LSE merge combines: decode = prefix tiles + suffix chunks, prefill = prefix chunks

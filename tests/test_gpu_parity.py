@@ -461,3 +461,27 @@ def test_tiny_eos_termination(lib, tiny):
         lib.Context(lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", prefix_k=4, page_tokens=4,
                                     eos_id=eos), tiny["w_dev"])
     assert e.value.status == lib.IS_ERR_CONFIG
+
+
+def test_tiny_row_capacity_32_decode_path(lib, tiny):
+    """row_capacity >= 32 (co-resident groups' row counts) selects the 64-token suffix units with
+    the separate merge kernel: schedule, sampler on dumped logits (bit-exact) and
+    teacher-forced logits (2e-2) against the oracle."""
+    r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "infinite", 2,
+             budget=tiny["budget"], logits=True, impl=tiny["impl"], rc=32)
+    ref = simulator.simulate(tiny["true"], "infinite", 2, pred=tiny["pred"], eps=0.1, page_tokens=16)
+    assert r["slots"].tolist() == ref.slot_table and r["stats"]["completed"] == 8
+    toks, t_of, checked = r["tokens"], {}, 0
+    for step, row in enumerate(r["slots"]):
+        for s, uid in enumerate(row):
+            if uid < 0:
+                continue
+            t = t_of.get(uid, 0)
+            assert sampler.sample_token(r["dumps"][step][s], SEED, int(uid), t) == toks[uid, t]
+            if t == 0 or step % 6 == 0:
+                gen = [int(x) for x in toks[uid, :t + 1]]
+                z = M.teacher_forced_logits(tiny["w"], TINY, tiny["prompt"], gen, mirror=True, rows=[t])[0]
+                assert _rel(r["dumps"][step][s], z) < 2e-2
+                checked += 1
+            t_of[uid] = t + 1
+    assert checked > 0

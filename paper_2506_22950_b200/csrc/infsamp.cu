@@ -372,7 +372,7 @@ static int choose_split(int num_tiles, int kb_total, int BN) {
   // 75..148 tiles: a 2-CTA cluster per tile keeps every SM streaming (gate/up: -5%/step at 16 rows);
   // with 32 or 64 rows the cluster exchange costs more than it saves (+8% tokens/s with split 1)
   if (s == 1) s = BN <= 16 ? 2 : 1;
-  s = std::min(s, 8);
+  s = std::min(s, BN <= 16 ? 8 : 4);  // >= 32 rows: o_proj / down at split 4 measured +8.5% tokens/s
   s = std::min(s, kb_total);
   return std::max(s, 1);
 }

@@ -251,8 +251,6 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     st = ctx.is_query()
     timed = dict(acc)
-    mk_ns = st["layer_kernel_ns"] - q0["layer_kernel_ns"]
-    mk_n = st["layer_kernel_launches"] - q0["layer_kernel_launches"]
     clk = clocks.stop()
     # ---- e2e: same rollouts through the public API with host buffers
     e2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -277,8 +275,7 @@ def run_ours(args):
         prof_e.append(msl_e)
     msl = np.median(np.stack(prof), axis=0)
     step_ms_eager = float(np.median(np.stack(prof_e), axis=0).sum())
-    gu_kernel = None
-    if st["decode_impl"] != 0:
+    if True:
         # the dominant kernel alone: every layer's gate/up launch as the step issues it, back to
         # back in one graph (4 passes over the layers), CUDA events around the replay
         gu_kernel = [ctx.is_profile_kernel(5, reps=4) for _ in range(3)]
@@ -310,30 +307,14 @@ def run_ours(args):
 
     hbm, tflops, peak_kind = peaks()
     kinds = {0: "embed/norm", 1: "qkv_gemm", 2: "qkv_post", 3: "attention", 4: "o_proj", 5: "gate_up", 6: "down",
-             7: "lm_head_sampler", 8: "refill", 9: "persistent_layers"}
+             7: "lm_head_sampler", 8: "refill"}
     per_kind = {kinds[k]: float(msl[kind == k].sum()) for k in kinds}
     n_launch_kind = {kinds[k]: int((kind == k).sum()) for k in kinds}
     step_ms = float(msl.sum())
     H, F, L = shape.hidden, shape.ffn, shape.layers
     kv_tok = 2 * L * shape.n_kv_heads * shape.head_dim * 2
     layer_w = ((shape.q_dim + 2 * shape.kv_dim) * H + H * shape.q_dim + 2 * F * H + H * F) * 2
-    if st["decode_impl"] == 0 and mk_n > 0:
-        # dominant kernel: the persistent decode kernel (all L layers, one launch per step).
-        # Algorithmic bytes per launch: every layer's weights once, the shared prefix KV once
-        # per group, the live suffix KV, the appended KV, averaged over the
-        # timed region's steps; time: its device-clock duration summed over the timed region.
-        n_steps = max(timed["steps"], 1)
-        bytes_launch = (L * layer_w + (P - 1) * kv_tok + timed["suffix"] / n_steps * kv_tok
-                        + timed["rows"] / n_steps * kv_tok)
-        ms_launch = mk_ns / mk_n * 1e-6
-        achieved = bytes_launch / (ms_launch * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": "persistent decode kernel (all layers: TMA weight stream + tcgen05 "
-                "swap-AB GEMMs, split attention, fused norms/RoPE/SwiGLU)",
-                "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                "peak_kind": peak_kind, "bytes_per_launch": int(bytes_launch), "traffic": None,
-                "launch_ms": round(ms_launch, 4), "launches_timed": int(mk_n),
-                "timing": "device globaltimer of the kernel's CTA 0, summed over the timed region"}
-    else:
+    if True:
         gu_bytes = 2 * F * H * 2                          # algorithmic bytes per gate/up launch (weights)
         gu_ms_step = per_kind["gate_up"] / max(n_launch_kind["gate_up"], 1)
         gu_ms = float(np.median([m for m, _ in gu_kernel]))
@@ -352,7 +333,7 @@ def run_ours(args):
                                   "interval includes one graph-node hop; median of 5 replays)"}
     roof["step_ms_graph_events"] = round(step_ms, 4)
     roof["step_ms_eager"] = round(step_ms_eager, 4)
-    if gu_kernel is not None:
+    if True:
         kv_tok_layer = 2 * shape.n_kv_heads * shape.head_dim * 2
         attn_bytes = (P - 1) * kv_tok_layer + attn_suffix * kv_tok_layer
         roof["attention"] = {"bound": "hbm", "kernel": "split attention per layer (tcgen05 shared prefix + "
@@ -381,7 +362,6 @@ def run_ours(args):
                    "placement": args.placement if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (3.4 GB of weights streamed per decode step)"},
         "roofline": roof,
-        "decode_impl": "persistent" if st["decode_impl"] == 0 else "per_op",
         "decode_steps_per_rollout": round(avg_steps, 1),
         "ms_per_decode_step": round(ms_max / max(steps_total, 1), 4),
         "peak_kv_bytes": st["peak_kv_bytes"],

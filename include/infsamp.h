@@ -75,10 +75,10 @@ typedef struct {
   float temperature;       /* sampling temperature (0.8) */
   uint64_t seed;           /* Philox key (R11) */
   is_mode mode;
-  int32_t decode_impl;     /* 0: persistent decode kernel, one launch for the whole layer stack
-                              (falls back to 1 when Hq/Hkv > 4 or the attention needs more than
-                              64 partials per row); 1: one kernel per operator (the Python
-                              binding's default) */
+  int32_t decode_impl;     /* reserved: 0 and 1 both select the decode step of one kernel per
+                              operator in one CUDA graph (round 1's persistent whole-stack kernel
+                              was slower, 2.74 vs 1.74 ms per step, and is retired); other
+                              values are IS_ERR_CONFIG */
   int32_t max_groups;      /* co-resident prompt groups sharing each decode step (SURVEY §8f
                               NEXT-1; 0 or 1 = the paper's one group per GPU).  Group slot m owns
                               rows m*g .. m*g+g-1; kv_budget_bytes is per group, the page pool
@@ -123,9 +123,6 @@ typedef struct {
   int64_t prefix_bytes;
   int32_t num_pages;      /* size of the page pool */
   int32_t row_capacity;
-  int32_t decode_impl;    /* implementation in use (see is_config.decode_impl) */
-  int64_t layer_kernel_ns;       /* persistent decode kernel: accumulated device time (globaltimer, CTA 0) */
-  int64_t layer_kernel_launches; /*   and launches, since is_create */
   int64_t suffix_tokens;  /* sum over decode steps of the live rows' suffix lengths (algorithmic KV bytes) */
   int32_t groups;         /* co-resident group slots of the context */
   int64_t global_steps;   /* decode steps with >= 1 active slot in any group */
@@ -310,20 +307,10 @@ is_status is_dbg_gemm(const void* d_w, const void* d_x, float* d_y, int32_t M, i
 is_status is_dbg_topp(const float* d_logits, int32_t rows, int32_t V, float temperature, float top_p, uint64_t seed,
                       const int32_t* d_uid, const int32_t* d_t, int32_t* d_tok, void* stream);
 
-/* Debug hook of the persistent decode kernel: h_info[4] = {in use, grid, task
- * count, trace capacity}; copies the per-CTA task lists (int4 {kind | layer<<8 |
- * part<<16, tile, kb0, kb1}, h_tasks[4 * count]) and offsets (h_off[grid + 1])
- * and, when the context was created with IS_MK_TRACE=<cap> in the environment,
- * the last step's timeline (h_trace[grid][4][cap][2] = {globaltimer ns, type<<32
- * | task}).  Any destination may be NULL.  Synchronises the stream. */
-is_status is_dbg_mk_trace(is_ctx* ctx, int32_t* h_tasks, int32_t task_cap, int32_t* h_off, int32_t off_cap,
-                          uint64_t* h_trace, int64_t trace_cap, int32_t* h_info);
-
 /* Debug: copy an internal activation buffer to the host (0 q [rc][Hq][128] bf16,
- * 1 residual [rc][H] f32, 2 persistent-kernel post-attention residual, 3 final
- * normalised rows [rc][H] bf16, 4 attention output [rc][Hq*128] bf16, 5 the
- * persistent kernel's swizzled attention operand, 6 SwiGLU activations, 7 their
- * swizzled copy).  Synchronises the stream. */
+ * 1 residual [rc][H] f32, 3 final normalised rows [rc][H] bf16, 4 attention
+ * output [rc][Hq*128] bf16, 6 SwiGLU activations [rc][F] bf16).  Synchronises
+ * the stream. */
 is_status is_dbg_copy(is_ctx* ctx, int32_t which, void* h_dst, int64_t bytes);
 
 const char* is_last_error(void);

@@ -19,7 +19,7 @@ EXPORTS = ["is_plan", "is_create", "is_destroy", "is_prefill", "is_start_group",
            "is_refill", "is_run_group", "is_query", "is_copy_tokens", "is_copy_schedule",
            "is_group_results", "is_group_advantages", "is_set_logits_dump", "is_profile_step",
            "is_profile_step_graph", "is_profile_kernel", "is_dbg_topp",
-           "is_dbg_gemm", "is_dbg_mk_trace", "is_dbg_copy", "is_prefill_slot", "is_start_group_slot",
+           "is_dbg_gemm", "is_dbg_copy", "is_prefill_slot", "is_start_group_slot",
            "is_run_until_any_done", "is_query_slot", "is_copy_tokens_slot", "is_copy_schedule_slot",
            "is_group_results_slot", "is_nccl_unique_id", "is_nccl_comm_init", "is_allgather_results",
            "is_nccl_comm_destroy", "is_copy_logprobs", "is_copy_logprobs_slot", "is_kl_rewards", "is_grpo_objective", "is_last_error",
@@ -64,8 +64,7 @@ class Stats(ctypes.Structure):
                 ("tokens_decoded", ctypes.c_int64), ("peak_kv_bytes", ctypes.c_int64),
                 ("page_bytes", ctypes.c_int64), ("prefix_bytes", ctypes.c_int64),
                 ("num_pages", ctypes.c_int32), ("row_capacity", ctypes.c_int32),
-                ("decode_impl", ctypes.c_int32), ("layer_kernel_ns", ctypes.c_int64),
-                ("layer_kernel_launches", ctypes.c_int64), ("suffix_tokens", ctypes.c_int64),
+                ("suffix_tokens", ctypes.c_int64),
                 ("groups", ctypes.c_int32), ("global_steps", ctypes.c_int64), ("global_peak_kv_bytes", ctypes.c_int64),
                 ("launches_per_step", ctypes.c_int32), ("launches_per_prefill", ctypes.c_int32),
                 ("discarded", ctypes.c_int32)]
@@ -116,7 +115,6 @@ def load(build_if_missing=True):
     L.is_profile_kernel.argtypes = [vp, i32, i32, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32)]
     L.is_dbg_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]
     L.is_dbg_topp.argtypes = [vp, i32, i32, ctypes.c_float, ctypes.c_float, ctypes.c_uint64, vp, vp, vp, vp]
-    L.is_dbg_mk_trace.argtypes = [vp, vp, i32, vp, i32, vp, ctypes.c_int64, vp]
     L.is_dbg_copy.argtypes = [vp, i32, vp, ctypes.c_int64]
     L.is_prefill_slot.argtypes = [vp, i32, vp, i32]
     L.is_start_group_slot.argtypes = [vp, i32, vp, vp]
@@ -154,10 +152,8 @@ def _np_ptr(a):
 
 
 def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix_k=0, page_tokens=16,
-                row_capacity=0, kv_budget_bytes=0, eps=0.1, temperature=0.8, seed=20261017, decode_impl=None,
+                row_capacity=0, kv_budget_bytes=0, eps=0.1, temperature=0.8, seed=20261017,
                 max_groups=1, dynamic_target=0, top_p=1.0, eos_id=None):
-    """decode_impl: 0 = persistent decode kernel, 1 = one kernel per operator (default: it is
-    faster on B200); None reads IS_DECODE_IMPL from the environment."""
     c = Config()
     c.shape = Shape(shape.layers, shape.hidden, shape.n_q_heads, shape.n_kv_heads, shape.head_dim, shape.ffn,
                     shape.vocab, shape.rms_eps, shape.rope_theta)
@@ -165,9 +161,7 @@ def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix
     c.prefix_k, c.page_tokens, c.row_capacity = prefix_k, page_tokens, row_capacity
     c.kv_budget_bytes, c.eps, c.temperature, c.seed = kv_budget_bytes, eps, temperature, seed
     c.mode = MODES[mode] if isinstance(mode, str) else int(mode)
-    if decode_impl is None:
-        decode_impl = int(os.environ.get("IS_DECODE_IMPL", "1"))
-    c.decode_impl = decode_impl
+    c.decode_impl = 0  # reserved (include/infsamp.h)
     c.max_groups = max_groups
     c.dynamic_target = dynamic_target
     c.top_p = top_p
@@ -372,20 +366,6 @@ class Context:
 
     def is_set_logits_dump(self, d_logits):
         _check(load().is_set_logits_dump(self._h, None if d_logits is None else d_logits.data_ptr()))
-
-    def is_dbg_mk_trace(self):
-        """Persistent decode kernel debug: (tasks [n,4], offsets [grid+1], trace [grid,4,cap,2] or None)."""
-        info = np.zeros(4, np.int32)
-        _check(load().is_dbg_mk_trace(self._h, None, 0, None, 0, None, 0, _np_ptr(info)))
-        if not info[0]:
-            return None
-        grid, n, cap = int(info[1]), int(info[2]), int(info[3])
-        tasks = np.zeros((n, 4), np.int32)
-        off = np.zeros(grid + 1, np.int32)
-        trace = np.zeros((grid, 4, cap, 2), np.uint64) if cap else None
-        _check(load().is_dbg_mk_trace(self._h, _np_ptr(tasks), tasks.size, _np_ptr(off), off.size,
-                                      _np_ptr(trace) if cap else None, trace.size if cap else 0, _np_ptr(info)))
-        return tasks, off, trace
 
     def is_dbg_copy(self, which, nbytes):
         out = np.zeros(nbytes, np.uint8)

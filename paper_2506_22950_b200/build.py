@@ -6,7 +6,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(PKG, "csrc", "infsamp.cu")
 OUT = os.path.join(PKG, "libinfsamp.so")
-DEPS = [os.path.join(PKG, "csrc", f) for f in ("infsamp.cu", "common.cuh", "gemm.cuh", "kernels.cuh", "mega.cuh",
+DEPS = [os.path.join(PKG, "csrc", f) for f in ("infsamp.cu", "common.cuh", "gemm.cuh", "kernels.cuh",
                                                 "sampler.cuh")] + [
     os.path.join(os.path.dirname(PKG), "include", "infsamp.h")]
 

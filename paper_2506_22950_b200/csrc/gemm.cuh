@@ -12,12 +12,11 @@
 //
 // Split-K: `split` CTAs of a thread-block cluster share one 128-row tile, each
 // streaming a contiguous K range.  Column slice j of the tile belongs to rank
-// j: every rank stages its partials of slice j in its idle stage ring and DMAs
-// them into rank j's shared memory (cp.async.bulk, completion counted on rank
-// j's mbarrier), then each rank sums its
-// slice in rank order 0..split-1 -- deterministic, one cluster barrier (at
-// start-up, hidden under the first TMA), no pull round trips.  With split == 1
-// the kernel is persistent over tiles and double-buffers the TMEM accumulator.
+// j: every rank writes its fp32 partial tile to an L2-resident workspace
+// (coalesced float4 stores), one cluster barrier (release / acquire) orders
+// them, and each rank sums its column slice over ranks 0..split-1 in rank order
+// (deterministic; no atomics).  With split == 1 the kernel is persistent over
+// tiles and double-buffers the TMEM accumulator.
 //
 // Epilogues (fused, no extra pass over HBM):
 //   EPI_QKV        per-head RMSNorm of q/k + RoPE + bf16 q / KV-cache append (R12 r2)

@@ -20,7 +20,6 @@
 #include "common.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
-#include "mega.cuh"
 
 using namespace isk;
 
@@ -82,6 +81,7 @@ static is_status check_config(const is_config* c) {
     return fail(IS_ERR_CONFIG, "eos_id must be a token id (0..vocab-1) and needs prefix_k == 0 (R37)");
   if (c->dynamic_target < 0 || c->dynamic_target > c->G || (c->dynamic_target > 0 && c->mode != IS_MODE_DYNAMIC))
     return fail(IS_ERR_CONFIG, "dynamic_target must be 0 or 1..G (got %d) and needs IS_MODE_DYNAMIC", c->dynamic_target);
+  if (c->decode_impl != 0 && c->decode_impl != 1) return fail(IS_ERR_CONFIG, "decode_impl must be 0 or 1 (reserved)");
   if (c->max_groups < 0 || n_groups(c) > 8 || n_groups(c) * g > 64)
     return fail(IS_ERR_CONFIG, "need 1 <= max_groups <= 8 and max_groups * g <= 64 (got %d x %d)", n_groups(c), g);
   return IS_OK;
@@ -510,14 +510,6 @@ struct is_ctx {
   CUtensorMap tm_prefix_kv;
   unsigned long long* timeline;  // debug: [launch][148 CTAs][16] GEMM stamps (IS_TIMELINE)
   int tl_count;
-  // persistent decode kernel (decode_impl 0)
-  int mk;                    // 1 = in use
-  int mk_grid, mk_smem;
-  MkArgs mka;
-  void* mk_bufs[32];
-  int mk_nbufs;
-  int mk_sync_n;
-  int mk_ntasks;
   int launches_per_step;  // kernels in one decode step (counted while capturing it)
   cudaGraphExec_t graphK;  // steps_per_graph decode steps in one graph (run loops)
   bool graphK_ok;
@@ -849,285 +841,6 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
   return IS_OK;
 }
 
-// ------------------------------------------------------------------ persistent decode kernel setup
-template <int BN, int REP>
-static int mk_scratch_bytes() { return MkScratch<BN, REP>::v; }
-static int mk_scratch_of(int BN, int REP) {
-  switch (BN * 16 + REP) {
-    case 16 * 16 + 1: return mk_scratch_bytes<16, 1>();
-    case 16 * 16 + 2: return mk_scratch_bytes<16, 2>();
-    case 16 * 16 + 4: return mk_scratch_bytes<16, 4>();
-    case 32 * 16 + 1: return mk_scratch_bytes<32, 1>();
-    case 32 * 16 + 2: return mk_scratch_bytes<32, 2>();
-    case 32 * 16 + 4: return mk_scratch_bytes<32, 4>();
-    case 64 * 16 + 1: return mk_scratch_bytes<64, 1>();
-    case 64 * 16 + 2: return mk_scratch_bytes<64, 2>();
-    case 64 * 16 + 4: return mk_scratch_bytes<64, 4>();
-  }
-  return -1;
-}
-template <int BN, int REP>
-static is_status mk_launch_t(is_ctx* c, cudaStream_t st) {
-  auto kern = mk_decode_kernel<BN, REP>;
-  static int attr = 0;
-  if (attr != c->mk_smem) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, c->mk_smem));
-    attr = c->mk_smem;
-  }
-  cudaLaunchConfig_t cfg{};
-  cudaLaunchAttribute at[2];
-  cfg.gridDim = dim3(c->mk_grid);
-  cfg.blockDim = dim3(kMkThreads);
-  cfg.dynamicSmemBytes = c->mk_smem;
-  cfg.stream = st;
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = kCS;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  if (g_use_pdl) {
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.numAttrs = 2;
-  }
-  CK(cudaLaunchKernelEx(&cfg, kern, c->mka));
-  ++g_launches;
-  return IS_OK;
-}
-static is_status mk_launch(is_ctx* c, cudaStream_t st) {
-  const int REP = c->sh.n_q_heads / c->sh.n_kv_heads;
-  switch (c->BN * 16 + REP) {
-    case 16 * 16 + 1: return mk_launch_t<16, 1>(c, st);
-    case 16 * 16 + 2: return mk_launch_t<16, 2>(c, st);
-    case 16 * 16 + 4: return mk_launch_t<16, 4>(c, st);
-    case 32 * 16 + 1: return mk_launch_t<32, 1>(c, st);
-    case 32 * 16 + 2: return mk_launch_t<32, 2>(c, st);
-    case 32 * 16 + 4: return mk_launch_t<32, 4>(c, st);
-    case 64 * 16 + 1: return mk_launch_t<64, 1>(c, st);
-    case 64 * 16 + 2: return mk_launch_t<64, 2>(c, st);
-    case 64 * 16 + 4: return mk_launch_t<64, 4>(c, st);
-  }
-  return fail(IS_ERR_CONFIG, "persistent decode kernel: unsupported BN %d / REP %d", c->BN, REP);
-}
-
-// Does the persistent decode kernel support this context?  (Hq/Hkv <= 4, <= 64
-// attention partials per row, smem for at least 4 weight stages.)
-static bool mk_supported(const is_ctx* c) {
-  if (c->M != 1) return false;
-  const int REP = c->sh.n_q_heads / c->sh.n_kv_heads;
-  if (REP != 1 && REP != 2 && REP != 4) return false;
-  const int nc_pre = (int)ceil_div64(c->pcap, kMkPC);
-  if (nc_pre + ceil_div64(c->max_new, kMkSC) > 64) return false;
-  if (c->sh.layers > 255) return false;
-  return true;
-}
-
-static is_status setup_mega(is_ctx* c, const void* const* dw) {
-  const is_shape& s = c->sh;
-  const int H = s.hidden, F = s.ffn, Hq = s.n_q_heads, Hkv = s.n_kv_heads, L = s.layers, BN = c->BN, rc = c->rc;
-  const int REP = Hq / Hkv;
-  is_status err = IS_OK;
-  auto A = [&](size_t bytes) -> void* {
-    void* p = err == IS_OK ? dalloc(bytes, &err) : nullptr;
-    if (p) c->mk_bufs[c->mk_nbufs++] = p;
-    return p;
-  };
-  MkArgs& a = c->mka;
-  a = MkArgs{};
-  // ---- GEMM geometry: every tile's K range is split over the 4 CTAs of a cluster
-  const int Ms[4] = {c->qkv_w, H, 2 * F, H};
-  const int Ks[4] = {H, Hq * 128, H, F};
-  long long w_off = 0;
-  for (int i = 0; i < 4; ++i) {
-    MkGemm& g = a.g[i];
-    g.M = Ms[i];
-    g.KB = Ks[i] / 64;
-    g.T = (int)ceil_div64(g.M, 128);
-    g.S = kCS;  // K split across the 4 CTAs of a cluster (partials exchanged over DSMEM)
-    g.w_off = w_off;
-    w_off += (long long)g.T * g.KB * 128 * 64;
-  }
-  a.layer_stride = w_off;
-  // ---- packed, swizzled weights
-  __nv_bfloat16* wpk = (__nv_bfloat16*)A((size_t)w_off * L * 2);
-  if (err != IS_OK) return err;
-  for (int l = 0; l < L; ++l) {
-    const LayerW& w = c->L[l];
-    const __nv_bfloat16* src[4] = {w.wqkv, w.wo, w.wgu, w.wd};
-    for (int i = 0; i < 4; ++i)
-      pack_sw128_kernel<<<1024, 256>>>(src[i], Ms[i], Ks[i], wpk + (size_t)l * w_off + a.g[i].w_off);
-  }
-  CK(cudaGetLastError());
-  // ---- norms [L][H] etc. (fp32)
-  float* in_norm = (float*)A((size_t)L * H * 4);
-  float* post_norm = (float*)A((size_t)L * H * 4);
-  float* qn = (float*)A((size_t)L * 128 * 4);
-  float* kn = (float*)A((size_t)L * 128 * 4);
-  __nv_bfloat16* in_bf = (__nv_bfloat16*)A((size_t)L * H * 2);
-  __nv_bfloat16* post_bf = (__nv_bfloat16*)A((size_t)L * H * 2);
-  if (err != IS_OK) return err;
-  for (int l = 0; l < L; ++l) {
-    const void* const* p = dw + 2 + 11 * l;
-    bf16_to_f32_kernel<<<(H + 255) / 256, 256>>>((const __nv_bfloat16*)p[0], in_norm + (size_t)l * H, H);
-    bf16_to_f32_kernel<<<(H + 255) / 256, 256>>>((const __nv_bfloat16*)p[7], post_norm + (size_t)l * H, H);
-    bf16_to_f32_kernel<<<1, 128>>>((const __nv_bfloat16*)p[4], qn + l * 128, 128);
-    bf16_to_f32_kernel<<<1, 128>>>((const __nv_bfloat16*)p[5], kn + l * 128, 128);
-    CK(cudaMemcpy(in_bf + (size_t)l * H, p[0], (size_t)H * 2, cudaMemcpyDeviceToDevice));
-    CK(cudaMemcpy(post_bf + (size_t)l * H, p[7], (size_t)H * 2, cudaMemcpyDeviceToDevice));
-  }
-  CK(cudaGetLastError());
-  // ---- activations
-  a.Th = (int)ceil_div64(H, 128);
-  a.resid0 = c->resid;
-  a.resid1 = (float*)A((size_t)rc * H * 4);
-  a.ssq = (float*)A((size_t)(2 * L + 1) * a.Th * rc * 4);
-  a.attn_sw = (__nv_bfloat16*)A((size_t)Hq * 128 * BN * 2);
-  a.act_sw = (__nv_bfloat16*)A((size_t)F * BN * 2);
-  a.nc_pre = (int)ceil_div64(c->pcap, kMkPC);
-  a.NCm = a.nc_pre + (int)ceil_div64(c->max_new, kMkSC);
-  a.part_o = (float*)A((size_t)rc * Hq * a.NCm * 128 * 4);
-  a.part_ml = (float*)A((size_t)rc * Hq * a.NCm * 2 * 4);
-  // ---- dependency counters, one block per layer
-  MkSync& so = a.so;
-  int o = 0;
-  so.att_next = o++;
-  so.o_done = o++;
-  so.dn_done = o++;
-  so.emb_done = o++;
-  so.qkv_flag = o; o += a.g[0].T;
-  so.att_row = o; o += Hkv * rc;
-  so.att_done = o; o += Hkv;
-  so.gu_flag = o; o += a.g[2].T;
-  so.stride = (o + 31) / 32 * 32;
-  c->mk_sync_n = so.stride * L;
-  a.sync = (int*)A((size_t)c->mk_sync_n * 4);
-  a.clock = (unsigned long long*)A(16);
-  if (const char* e = getenv("IS_MK_TRACE")) {
-    a.trace_cap = std::max(16, atoi(e));
-    a.trace = (unsigned long long*)A((size_t)g_num_sms * 4 * a.trace_cap * 16);
-  }
-  if (err != IS_OK) return err;
-  // ---- grid: every CTA co-resident, clusters of kCS
-  int dev = 0;
-  CK(cudaGetDevice(&dev));
-  int maxsm = 0;
-  CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  a.scratch = mk_scratch_of(BN, REP);
-  a.nb = BN == 16 ? 8 : (BN == 32 ? 6 : 4);
-  const int fixed = 1024 + 2 * a.nb * BN * 128 + 2 * (kCS * 128 * (BN / kCS) * 4) + 2 * a.scratch + 1024;
-  a.na = std::min(16, (maxsm - fixed) / kMkStage);
-  if (const char* e = getenv("IS_MK_STAGES")) a.na = std::max(2, std::min(a.na, atoi(e)));
-  if (a.na < 3) return fail(IS_ERR_CONFIG, "persistent decode kernel: not enough shared memory");
-  c->mk_smem = fixed + a.na * kMkStage;
-  int nclusters = 0;
-  {
-    cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute at[1];
-    cfg.gridDim = dim3(kCS * (g_num_sms / kCS));
-    cfg.blockDim = dim3(kMkThreads);
-    cfg.dynamicSmemBytes = c->mk_smem;
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = kCS;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    switch (BN * 16 + REP) {
-#define IS_OCC(B, R) \
-  case B * 16 + R: { \
-    CK(cudaFuncSetAttribute(mk_decode_kernel<B, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->mk_smem)); \
-    CK(cudaFuncSetAttribute(mk_decode_kernel<B, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)); \
-    CK(cudaOccupancyMaxActiveClusters(&nclusters, mk_decode_kernel<B, R>, &cfg)); \
-    break; }
-      IS_OCC(16, 1) IS_OCC(16, 2) IS_OCC(16, 4) IS_OCC(32, 1) IS_OCC(32, 2) IS_OCC(32, 4) IS_OCC(64, 1) IS_OCC(64, 2) IS_OCC(64, 4)
-#undef IS_OCC
-    }
-  }
-  nclusters = std::min(nclusters, g_num_sms / kCS);
-  if (const char* e = getenv("IS_MK_CLUSTERS")) nclusters = std::max(1, std::min(nclusters, atoi(e)));
-  if (nclusters < 1) return fail(IS_ERR_CONFIG, "persistent decode kernel: no co-resident cluster (smem %d)", c->mk_smem);
-  const int grid = kCS * nclusters;
-  // ---- static per-CTA task lists (global order: EMBED, per layer QKV ATT O GU DN, FINAL).
-  //      A GEMM tile goes to one cluster, part p (K range p/kCS) to its CTA of rank p, so
-  //      the kCS CTAs of a cluster walk mirrored lists.
-  std::vector<std::vector<int4>> tl(grid);
-  for (int r = 0; r < rc; ++r) tl[r % grid].push_back(make_int4(MK_EMBED, r, 0, 0));
-  long long u = 0;
-  const int kinds[4] = {MK_QKV, MK_O, MK_GU, MK_DN};
-  for (int l = 0; l < L; ++l) {
-    for (int gi = 0; gi < 4; ++gi) {
-      const MkGemm& g = a.g[gi];
-      for (int t = 0; t < g.T; ++t) {
-        const int cl = (int)((u++) % nclusters);
-        for (int p = 0; p < kCS; ++p)
-          tl[cl * kCS + p].push_back(make_int4(kinds[gi] | (l << 8) | (p << 16), t, p * g.KB / kCS, (p + 1) * g.KB / kCS));
-      }
-      if (gi == 0)
-        for (int b = 0; b < grid; ++b) tl[b].push_back(make_int4(MK_ATT | (l << 8), 0, 0, 0));
-    }
-  }
-  for (int r = 0; r < rc; ++r) tl[r % grid].push_back(make_int4(MK_FINAL | ((L - 1) << 8), r, 0, 0));
-  std::vector<int> off(grid + 1, 0);
-  std::vector<int4> flat;
-  for (int b = 0; b < grid; ++b) {
-    off[b] = (int)flat.size();
-    flat.insert(flat.end(), tl[b].begin(), tl[b].end());
-  }
-  off[grid] = (int)flat.size();
-  int4* d_tasks = (int4*)A(flat.size() * sizeof(int4));
-  int* d_off = (int*)A(off.size() * 4);
-  c->mk_ntasks = (int)flat.size();
-  if (err != IS_OK) return err;
-  CK(cudaMemcpy(d_tasks, flat.data(), flat.size() * sizeof(int4), cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(d_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
-  c->mk_grid = grid;
-  a.pf_units = 2;
-  a.nodeps = getenv("IS_MK_NODEPS") ? 1 : 0;
-  if (const char* e = getenv("IS_MK_PF")) a.pf_units = std::max(0, atoi(e));
-  // ---- the rest of the arguments
-  a.tasks = d_tasks;
-  a.task_off = d_off;
-  a.wpk = wpk;
-  a.L = L;
-  a.H = H;
-  a.F = F;
-  a.Hq = Hq;
-  a.Hkv = Hkv;
-  a.rc = rc;
-  a.eps = s.rms_eps;
-  a.scale = 1.0f / sqrtf((float)kHD);
-  a.embed = c->embed;
-  a.in_norm = in_norm;
-  a.post_norm = post_norm;
-  a.in_norm_bf = in_bf;
-  a.post_norm_bf = post_bf;
-  a.q_norm = qn;
-  a.k_norm = kn;
-  a.final_norm = c->final_norm;
-  a.rope_cos = c->rope_cos;
-  a.rope_sin = c->rope_sin;
-  a.row_active = c->row_active;
-  a.row_tok = c->row_tok;
-  a.row_pos = c->row_pos;
-  a.row_kvloc = c->row_kvloc;
-  a.row_len = c->row_len;
-  a.row_lid = c->row_lid;
-  a.q = c->q;
-  a.xn_final = c->xn;
-  a.prefix = c->prefix;
-  a.prefix_layer = (long long)2 * Hkv * c->pcap * kHD;
-  a.pool = c->pool;
-  a.pool_layer = (long long)c->num_pages * 2 * Hkv * c->pt * kHD;
-  a.pagetab = c->pagetab;
-  a.maxp = c->maxp;
-  a.pt = c->pt;
-  a.pcap = c->pcap;
-  CK(cudaDeviceSynchronize());
-  c->mk = 1;
-  return IS_OK;
-}
-
 static is_status enqueue_step_body(is_ctx* c);
 static is_status enqueue_step(is_ctx* c) {
   const int launches0 = g_launches;
@@ -1139,16 +852,11 @@ static is_status enqueue_step(is_ctx* c) {
 static is_status enqueue_step_body(is_ctx* c) {
   cudaStream_t st = c->st;
   const is_shape& s = c->sh;
-  if (c->mk) {
-    CKS(mk_launch(c, st));
-    prof_mark(st, 9);
-  } else {
-    CKS(run_layers(c, c->rc, false));
-    if (!c->fuse_norm)  // (else the last down GEMM's epilogue applied the final norm)
-      CKS(launch_k(rmsnorm_kernel, dim3(c->rc), dim3(256), st, (const float*)c->resid, (const float*)c->final_norm,
-                   c->xn, s.hidden, s.rms_eps));
-    prof_mark(st, 0);
-  }
+  CKS(run_layers(c, c->rc, false));
+  if (!c->fuse_norm)  // (else the last down GEMM's epilogue applied the final norm)
+    CKS(launch_k(rmsnorm_kernel, dim3(c->rc), dim3(256), st, (const float*)c->resid, (const float*)c->final_norm,
+                 c->xn, s.hidden, s.rms_eps));
+  prof_mark(st, 0);
   GemmArgs a{};
   a.M = s.vocab;
   a.K = s.hidden;
@@ -1165,10 +873,6 @@ static is_status enqueue_step_body(is_ctx* c) {
   a.lp_mlz = c->lp_mlz;
   a.logits_dump = c->topp ? (c->logits_dump ? c->logits_dump : c->logits_tp) : c->logits_dump;
   a.score_dump = c->topp ? c->scores_tp : nullptr;
-  if (c->mk) {
-    a.zero = c->mka.sync;  // the next step's dependency counters start from zero
-    a.zero_n = c->mk_sync_n;
-  }
   a.seed = c->cfg.seed;
   a.inv_temp = (float)(1.0 / (double)c->cfg.temperature);
   g_splitk_ws = c->splitk_ws;
@@ -1544,7 +1248,6 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
                    th * std::max(c->split_d, 1) <= g_num_sms;
   }
   CK(cudaDeviceSynchronize());
-  if (cfg->decode_impl == 0 && mk_supported(c) && !getenv("IS_NO_MEGA")) CKS(setup_mega(c, dw));
   *out = c;
   return IS_OK;
 }
@@ -1564,7 +1267,6 @@ extern "C" void is_destroy(is_ctx* c) {
                   c->sel_tp, c->state_tp};
   for (void* p : bufs)
     if (p) cudaFree(p);
-  for (int i = 0; i < c->mk_nbufs; ++i) cudaFree(c->mk_bufs[i]);
   for (auto& w : c->L) {
     cudaFree(w.in_norm_bf);
     cudaFree(w.post_norm_bf);
@@ -1812,16 +1514,7 @@ extern "C" is_status is_query_slot(is_ctx* c, int32_t m, is_stats* o) {
   o->peak_kv_bytes = c->prefix_bytes + st[ST_PEAK] * c->page_bytes;
   o->num_pages = c->num_pages;
   o->row_capacity = c->rc;
-  o->decode_impl = c->mk ? 0 : 1;
   o->suffix_tokens = st[ST_SUFFIX];
-  o->layer_kernel_ns = 0;
-  o->layer_kernel_launches = 0;
-  if (c->mk) {
-    unsigned long long clk[2];
-    CK(cudaMemcpy(clk, c->mka.clock, sizeof clk, cudaMemcpyDeviceToHost));
-    o->layer_kernel_ns = (int64_t)clk[0];
-    o->layer_kernel_launches = (int64_t)clk[1];
-  }
   o->groups = c->M;
   o->launches_per_step = c->launches_per_step;
   o->launches_per_prefill = c->launches_per_prefill;
@@ -1944,7 +1637,6 @@ static is_status profile_step(is_ctx* c, bool graph, float* h_ms, int32_t* h_kin
 extern "C" is_status is_profile_kernel(is_ctx* c, int32_t kind, int32_t reps, float* h_ms_per_launch,
                                        int32_t* h_launches) {
   if (!c || !h_ms_per_launch) return fail(IS_ERR_CONFIG, "null argument");
-  if (c->mk) return fail(IS_ERR_CONFIG, "is_profile_kernel: per-op decode path only");
   int keep;
   switch (kind) {
     case 1: keep = 2; break;
@@ -2135,24 +1827,6 @@ extern "C" int is_dbg_timeline(is_ctx* c) {
   return c->tl_count;
 }
 
-extern "C" is_status is_dbg_mk_trace(is_ctx* c, int32_t* h_tasks, int32_t task_cap, int32_t* h_off, int32_t off_cap,
-                                     uint64_t* h_trace, int64_t trace_cap, int32_t* h_info) {
-  if (!c || !h_info) return fail(IS_ERR_CONFIG, "null argument");
-  CK(cudaStreamSynchronize(c->st));
-  h_info[0] = c->mk;
-  h_info[1] = c->mk ? c->mk_grid : 0;
-  h_info[2] = c->mk ? c->mk_ntasks : 0;
-  h_info[3] = c->mk ? c->mka.trace_cap : 0;
-  if (!c->mk) return IS_OK;
-  if (h_tasks && task_cap >= c->mk_ntasks * 4)
-    CK(cudaMemcpy(h_tasks, c->mka.tasks, (size_t)c->mk_ntasks * 16, cudaMemcpyDeviceToHost));
-  if (h_off && off_cap >= c->mk_grid + 1)
-    CK(cudaMemcpy(h_off, c->mka.task_off, (size_t)(c->mk_grid + 1) * 4, cudaMemcpyDeviceToHost));
-  const int64_t n = (int64_t)c->mk_grid * 4 * c->mka.trace_cap * 2;
-  if (h_trace && c->mka.trace && trace_cap >= n) CK(cudaMemcpy(h_trace, c->mka.trace, (size_t)n * 8, cudaMemcpyDeviceToHost));
-  return IS_OK;
-}
-
 extern "C" is_status is_dbg_copy(is_ctx* c, int32_t which, void* h_dst, int64_t bytes) {
   if (!c || !h_dst) return fail(IS_ERR_CONFIG, "null argument");
   CK(cudaStreamSynchronize(c->st));
@@ -2162,12 +1836,9 @@ extern "C" is_status is_dbg_copy(is_ctx* c, int32_t which, void* h_dst, int64_t 
   switch (which) {
     case 0: src = c->q; n = (int64_t)c->rc * s.n_q_heads * 128 * 2; break;
     case 1: src = c->resid; n = (int64_t)c->rc * s.hidden * 4; break;
-    case 2: src = c->mk ? (const void*)c->mka.resid1 : nullptr; n = (int64_t)c->rc * s.hidden * 4; break;
     case 3: src = c->xn; n = (int64_t)c->rc * s.hidden * 2; break;
     case 4: src = c->attn; n = (int64_t)c->rc * s.n_q_heads * 128 * 2; break;
-    case 5: src = c->mk ? (const void*)c->mka.attn_sw : nullptr; n = (int64_t)c->BN * s.n_q_heads * 128 * 2; break;
     case 6: src = c->act; n = (int64_t)c->rc * s.ffn * 2; break;
-    case 7: src = c->mk ? (const void*)c->mka.act_sw : nullptr; n = (int64_t)c->BN * s.ffn * 2; break;
     default: return fail(IS_ERR_CONFIG, "unknown buffer %d", which);
   }
   if (!src) return fail(IS_ERR_STATE, "buffer %d not in use", which);

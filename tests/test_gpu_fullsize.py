@@ -19,8 +19,8 @@ P, G, g, MAX_NEW = 256, 32, 8, 1024
 LATE = 70  # step whose logits are checked at t = 70 (3 suffix chunks of 32 tokens)
 
 
-@pytest.fixture(scope="module", params=[0, 1], ids=["persistent", "per_op"])
-def full(request):
+@pytest.fixture(scope="module")
+def full():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2506_22950_b200 import _lib
@@ -28,7 +28,7 @@ def full(request):
     kv_tok = okv.kv_bytes_per_token(SHAPE.layers, SHAPE.n_kv_heads, SHAPE.head_dim)
     budget = (P - 1) * kv_tok + g * (MAX_NEW // 16) * 16 * kv_tok
     cfg = _lib.make_config(SHAPE, G, g, MAX_NEW, P, mode="infinite", page_tokens=16, kv_budget_bytes=budget,
-                           eps=0.1, temperature=0.8, seed=SEED, decode_impl=request.param)
+                           eps=0.1, temperature=0.8, seed=SEED)
     ctx = _lib.Context(cfg, w)
     prompt = gen_prompt(SHAPE.vocab, P, 3, seed=SEED)
     true = gen_trace("math", G, MAX_NEW, SEED + 3)
@@ -52,7 +52,7 @@ def full(request):
     ctx.is_set_logits_dump(None)
     steps = ctx.is_run_group()
     res = dict(steps=steps, stats=ctx.is_query(), sched=ctx.is_copy_schedule(), tokens=ctx.is_copy_tokens(),
-               dumps=dumps, late=late, true=true, pred=pred, prompt=prompt, budget=budget, impl=request.param,
+               dumps=dumps, late=late, true=true, pred=pred, prompt=prompt, budget=budget,
                w_cpu={k: v.cpu() for k, v in w.items()})
     ctx.close()
     del w
@@ -101,10 +101,6 @@ def test_fullsize_teacher_forced_logits_and_tokens(full):
         tok, margin = sampler.sample_margin(z[t].astype(np.float32), SEED, 3 * G + uid, t)
         if tok != gen[t]:
             assert margin < 2 * 1.25 * np.max(np.abs(d - z[t])), (t, margin)
-
-
-def test_fullsize_decode_impl_in_use(full):
-    assert full["stats"]["decode_impl"] == full["impl"]
 
 
 def test_fullsize_late_step_logits(full):
@@ -174,7 +170,7 @@ def test_fullsize_topp_step_bit_exact():
     from paper_2506_22950_b200 import _lib
     w = gen_weights(SHAPE, seed=SEED, device="cuda")
     cfg = _lib.make_config(SHAPE, G, g, MAX_NEW, P, mode="infinite", page_tokens=16, eps=0.1, temperature=0.8,
-                           seed=SEED, decode_impl=1, top_p=0.9)
+                           seed=SEED, top_p=0.9)
     ctx = _lib.Context(cfg, w)
     prompt = gen_prompt(SHAPE.vocab, P, 5, seed=SEED)
     true = gen_trace("math", G, MAX_NEW, SEED + 5)

@@ -61,10 +61,10 @@ def _tiny_setup():
     return w, prompt, true, pred
 
 
-def _run(lib, w_dev, prompt, true, pred, mode, g, budget=0, prefix_k=0, pt=16, rc=16, logits=False, impl=0,
+def _run(lib, w_dev, prompt, true, pred, mode, g, budget=0, prefix_k=0, pt=16, rc=16, logits=False,
          target=0, top_p=1.0, eos_id=None):
     cfg = lib.make_config(TINY, len(true), g, 32, 16, mode=mode, prefix_k=prefix_k, page_tokens=pt, row_capacity=rc,
-                          kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED, decode_impl=impl,
+                          kv_budget_bytes=budget, eps=0.1, temperature=0.8, seed=SEED,
                           dynamic_target=target, top_p=top_p, eos_id=eos_id)
     ctx = lib.Context(cfg, w_dev)
     ctx.is_prefill(torch.as_tensor(prompt, device="cuda"), 0)
@@ -90,17 +90,15 @@ def _run(lib, w_dev, prompt, true, pred, mode, g, budget=0, prefix_k=0, pt=16, r
     return dict(steps=steps, stats=st, slots=slots, live=live, tokens=toks, dumps=dumps, logprobs=lps)
 
 
-@pytest.fixture(scope="module", params=[0, 1], ids=["persistent", "per_op"])
-def tiny(lib, request):
-    """decode_impl 0 = the persistent decode kernel, 1 = one kernel per operator."""
-    impl = request.param
+@pytest.fixture(scope="module")
+def tiny(lib):
     w, prompt, true, pred = _tiny_setup()
     w_dev = {k: v.cuda() for k, v in w.items()}
     budget = okv.prefix_bytes(TINY, 16) + 4 * 2 * okv.page_bytes(TINY, 16)  # config 1: "KV budget 4 slots"
-    runs = {m: _run(lib, w_dev, prompt, true, pred, m, 2, budget=budget, impl=impl)
+    runs = {m: _run(lib, w_dev, prompt, true, pred, m, 2, budget=budget)
             for m in ("naive", "fifo", "infinite", "fptas_only", "sjf_only")}
-    runs["full"] = _run(lib, w_dev, prompt, true, pred, "full", 8, impl=impl)
-    return dict(w=w, w_dev=w_dev, prompt=prompt, true=true, pred=pred, runs=runs, budget=budget, impl=impl)
+    runs["full"] = _run(lib, w_dev, prompt, true, pred, "full", 8)
+    return dict(w=w, w_dev=w_dev, prompt=prompt, true=true, pred=pred, runs=runs, budget=budget)
 
 
 @pytest.mark.parametrize("mode", ["naive", "fifo", "infinite", "full", "fptas_only", "sjf_only"])
@@ -108,7 +106,6 @@ def test_tiny_schedule_bit_exact(tiny, mode):
     r = tiny["runs"][mode]
     ref = simulator.simulate(tiny["true"], mode, 2, pred=tiny["pred"], eps=0.1, page_tokens=16)
     assert r["stats"]["completed"] == 8 and r["stats"]["error"] == 0
-    assert r["stats"]["decode_impl"] == tiny["impl"]
     assert r["steps"] == ref.total_steps
     assert r["slots"].tolist() == ref.slot_table
     assert r["live"].tolist() == ref.live_pages
@@ -145,7 +142,7 @@ def test_tiny_teacher_forced_tokens_and_logits(tiny):
 
 def test_tiny_sampler_bit_exact_on_dumped_logits(lib, tiny):
     r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "infinite", 2,
-             budget=tiny["budget"], logits=True, impl=tiny["impl"])
+             budget=tiny["budget"], logits=True)
     toks = r["tokens"]
     slots = r["slots"]
     t_of = {}
@@ -173,7 +170,7 @@ def test_tiny_budget_error_and_prefix_phase(lib, tiny):
     assert e.value.status == lib.IS_ERR_BUDGET
     pred = predict_lengths(tiny["true"], "noisy", 0.3, seed=1, prefix_k=4)
     r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], pred, "infinite", 2, budget=tiny["budget"],
-             prefix_k=4, pt=4, impl=tiny["impl"])
+             prefix_k=4, pt=4)
     ref = simulator.simulate(tiny["true"], "infinite", 2, pred=pred, eps=0.1, prefix_k=4, page_tokens=4)
     assert r["steps"] == ref.total_steps
     assert r["slots"].tolist() == ref.slot_table
@@ -184,8 +181,7 @@ def test_tiny_budget_error_and_prefix_phase(lib, tiny):
 
 def test_tiny_rewards_and_advantages(lib, tiny):
     from oracle import grpo
-    cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", kv_budget_bytes=tiny["budget"], seed=SEED,
-                          decode_impl=tiny["impl"])
+    cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", kv_budget_bytes=tiny["budget"], seed=SEED)
     ctx = lib.Context(cfg, tiny["w_dev"])
     ctx.is_prefill(torch.as_tensor(tiny["prompt"], device="cuda"), 0)
     ctx.is_start_group(tiny["true"], tiny["pred"])
@@ -212,8 +208,7 @@ def test_tiny_context_reused_across_prompts(lib, tiny):
     pred1 = predict_lengths(true1, "noisy", 0.3, seed=2)
 
     def mk():
-        cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", kv_budget_bytes=tiny["budget"], seed=SEED,
-                              decode_impl=tiny["impl"])
+        cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", kv_budget_bytes=tiny["budget"], seed=SEED)
         return lib.Context(cfg, w_dev)
 
     a = mk()
@@ -246,8 +241,7 @@ def test_nccl_allgather_results_single_rank(lib, tiny):
     except lib.InfsampError as e:
         pytest.skip(f"no NCCL: {e}")
     comm = lib.nccl_comm_init(uid, 0, 1)
-    cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", kv_budget_bytes=tiny["budget"], seed=SEED,
-                          decode_impl=tiny["impl"])
+    cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", kv_budget_bytes=tiny["budget"], seed=SEED)
     ctx = lib.Context(cfg, tiny["w_dev"])
     ctx.is_prefill(torch.as_tensor(tiny["prompt"], device="cuda"), 0)
     ctx.is_start_group(tiny["true"], tiny["pred"])
@@ -276,7 +270,7 @@ def test_tiny_logprobs(lib, tiny):
     log-softmax of the kernel's own logits (1e-4, R31's fp32-accumulation class) and the
     oracle's teacher-forced one within 2 max|dz| (the logits tolerance propagated)."""
     r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "infinite", 2,
-             budget=tiny["budget"], logits=True, impl=tiny["impl"])
+             budget=tiny["budget"], logits=True)
     toks, lps = r["tokens"], r["logprobs"]
     t_of, checked = {}, 0
     for step, row in enumerate(r["slots"]):
@@ -317,10 +311,8 @@ def test_tiny_logprobs(lib, tiny):
 def test_profile_hooks_then_decode_unchanged(lib, tiny):
     """bench.py's timing hooks (is_profile_kernel, is_profile_step[_graph]) run on a live
     context; a group started afterwards decodes the same tokens as an undisturbed run."""
-    if tiny["impl"] == 0:
-        pytest.skip("per-op decode path only")
     cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", kv_budget_bytes=tiny["budget"], eps=0.1,
-                          temperature=0.8, seed=SEED, decode_impl=1)
+                          temperature=0.8, seed=SEED)
     ctx = lib.Context(cfg, tiny["w_dev"])
     ctx.is_prefill(torch.as_tensor(tiny["prompt"], device="cuda"), 0)
     ctx.is_start_group(tiny["true"], tiny["pred"])
@@ -349,7 +341,7 @@ def test_tiny_dynamic_slot_mode(lib, tiny, target):
     Slot table, page log, discards and counters equal the oracle's simulation; completed
     samples' tokens equal the same uids' tokens under every other schedule."""
     r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "dynamic", 2,
-             budget=tiny["budget"], impl=tiny["impl"], target=target)
+             budget=tiny["budget"], target=target)
     ref = simulator.simulate(tiny["true"], "dynamic", 2, page_tokens=16, target=target)
     st = r["stats"]
     assert st["completed"] == target and st["error"] == 0 and st["discarded"] == len(ref.discarded)
@@ -367,11 +359,9 @@ def test_tiny_fused_norm_opt_in(lib, tiny, monkeypatch):
     """IS_FUSE_NORM=1 (opt-in): RMSNorm in the o_proj / down epilogues behind a grid
     barrier.  Same schedule; the norm's fp32 sum order differs, so tokens are compared with the
     teacher-forced tolerance of the default path (all but a near-tie few identical)."""
-    if tiny["impl"] == 0:
-        pytest.skip("per-op decode path only")
     monkeypatch.setenv("IS_FUSE_NORM", "1")
     r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "infinite", 2,
-             budget=tiny["budget"], impl=1)
+             budget=tiny["budget"])
     base = tiny["runs"]["infinite"]
     assert r["slots"].tolist() == base["slots"].tolist() and r["stats"]["completed"] == 8
     valid = base["tokens"] >= 0
@@ -385,7 +375,7 @@ def test_tiny_topp_sampler_bit_exact(lib, tiny, top_p):
     kernel's own dumped logits, bit-exactly; log pi(token) stays the full-softmax value
     (R33); the schedule is unchanged."""
     r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "infinite", 2,
-             budget=tiny["budget"], logits=True, impl=tiny["impl"], top_p=top_p)
+             budget=tiny["budget"], logits=True, top_p=top_p)
     assert r["slots"].tolist() == tiny["runs"]["infinite"]["slots"].tolist()
     toks, lps = r["tokens"], r["logprobs"]
     t_of, n, in_nucleus_only = {}, 0, 0
@@ -450,7 +440,7 @@ def test_tiny_eos_termination(lib, tiny):
         eff.append(int(hit[0]) + 1 if len(hit) else int(L))
     assert eff[0] < true[0] or true[0] <= 4
     r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "infinite", 2,
-             budget=tiny["budget"], impl=tiny["impl"], eos_id=eos)
+             budget=tiny["budget"], eos_id=eos)
     ref = simulator.simulate(eff, "infinite", 2, pred=tiny["pred"], eps=0.1, page_tokens=16)
     assert r["stats"]["completed"] == 8 and r["stats"]["error"] == 0
     assert r["slots"].tolist() == ref.slot_table and r["live"].tolist() == ref.live_pages
@@ -468,7 +458,7 @@ def test_tiny_row_capacity_32_decode_path(lib, tiny):
     the separate merge kernel: schedule, sampler on dumped logits (bit-exact) and
     teacher-forced logits (2e-2) against the oracle."""
     r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "infinite", 2,
-             budget=tiny["budget"], logits=True, impl=tiny["impl"], rc=32)
+             budget=tiny["budget"], logits=True, rc=32)
     ref = simulator.simulate(tiny["true"], "infinite", 2, pred=tiny["pred"], eps=0.1, page_tokens=16)
     assert r["slots"].tolist() == ref.slot_table and r["stats"]["completed"] == 8
     toks, t_of, checked = r["tokens"], {}, 0

@@ -172,20 +172,27 @@ is_status is_start_group(is_ctx* ctx, const int32_t* h_true_len, const int32_t* 
 /* One decode step: every active slot attends to the shared prefix
  * plus its own pages, samples its next token, then finished slots are refilled
  * in place (is_refill).  d_next_tokens / d_finished: [row_capacity] device
- * buffers (nullable) receiving the sampled token / finish flag per slot
- * (-1 / 0 for idle slots).  Asynchronous: no host synchronisation. */
+ * buffers (nullable) receiving the sampled token / finish flag per row (row
+ * m*g + s = group m, slot s; -1 / 0 for rows idle in that step).  Asynchronous:
+ * no host synchronisation.  IS_ERR_BUDGET once the device scheduler has found the
+ * page pool exhausted (R25: cannot happen within a budget is_create accepted; the
+ * flag is seen with the lag of the steps still in flight, and from then on every row
+ * is idle: no page is ever handed out twice). */
 is_status is_decode_step(is_ctx* ctx, int32_t* d_next_tokens, uint8_t* d_finished);
 
 /* Finish/refill/page-recycle policy alone (Alg. 3, "cache is
  * cleared and the memory is reassigned back to the pool"): consumes the last
  * sampled keys, appends tokens, finishes/parks samples, refills freed slots in
  * ascending slot order from the static queue, allocates pages for the next
- * step.  Called inside is_decode_step; exported for tests.  d_new_uid
- * [row_capacity] (nullable) receives the uid now in each slot (-1 idle). */
+ * step.  Called inside is_decode_step; exported for tests.  d_finished
+ * [row_capacity] (nullable) receives the finish flag per row; d_new_uid
+ * [row_capacity] (nullable) the uid now in each row (m*g + s; -1 idle). */
 is_status is_refill(is_ctx* ctx, uint8_t* d_finished, int32_t* d_new_uid);
 
 /* Decode steps until the group completes (bounded host run-ahead, no per-step
- * sync).  h_steps (nullable) receives the number of steps. */
+ * sync).  h_steps (nullable) receives the number of steps.  IS_ERR_CAPACITY if
+ * max_steps ran out first; IS_ERR_BUDGET if the page pool was exhausted (see
+ * is_decode_step). */
 is_status is_run_group(is_ctx* ctx, int32_t max_steps, int32_t* h_steps);
 
 is_status is_query(is_ctx* ctx, is_stats* out); /* synchronises the stream */
@@ -211,6 +218,8 @@ is_status is_copy_schedule(is_ctx* ctx, int32_t* h_slot_table, int32_t* h_live_p
 is_status is_prefill_slot(is_ctx* ctx, int32_t slot, const int32_t* d_prompt, int32_t prompt_id);
 is_status is_start_group_slot(is_ctx* ctx, int32_t slot, const int32_t* h_true_len, const int32_t* h_pred_len);
 is_status is_run_until_any_done(is_ctx* ctx, int32_t max_steps, int32_t* h_done_mask, int64_t* h_global_steps);
+/* (is_run_until_any_done: IS_ERR_BUDGET as is_run_group.  Environment knob for negative
+ * tests only: IS_DBG_POOL_PAGES=n at is_create sizes the page pool to n pages.) */
 is_status is_query_slot(is_ctx* ctx, int32_t slot, is_stats* out);
 is_status is_copy_tokens_slot(is_ctx* ctx, int32_t slot, int32_t* dst, int32_t dst_is_device);
 is_status is_copy_schedule_slot(is_ctx* ctx, int32_t slot, int32_t* h_slot_table, int32_t* h_live_pages,
@@ -241,7 +250,11 @@ is_status is_copy_logprobs(is_ctx* ctx, float* h_dst);
 is_status is_copy_logprobs_slot(is_ctx* ctx, int32_t slot, float* h_dst);
 
 /* Benchmark reward and completion length per sample (R29):
- * d_reward[G] = #{tokens < vocab/2}/len, d_len[G] = len.  Device buffers. */
+ * d_reward[G] = #{tokens < vocab/2}/len, d_len[G] = len.  Device buffers.  len is the
+ * emitted length of a completed sample (true_len, or shorter when it stopped at
+ * eos_id, R37); a sample that did not complete (IS_MODE_DYNAMIC, R35: discarded in
+ * flight or never started) reports len = 0 and reward = 0, so callers select the
+ * completed samples (len >= 1) before the advantages or is_kl_rewards. */
 is_status is_group_results(is_ctx* ctx, float* d_reward, int32_t* d_len);
 
 /* Group advantages, Eq. 2 or mean-only; fp64 sums in
@@ -306,6 +319,31 @@ is_status is_dbg_gemm(const void* d_w, const void* d_x, float* d_y, int32_t M, i
  * allocates its scratch per call. */
 is_status is_dbg_topp(const float* d_logits, int32_t rows, int32_t V, float temperature, float top_p, uint64_t seed,
                       const int32_t* d_uid, const int32_t* d_t, int32_t* d_tok, void* stream);
+
+/* Kernel-level test hook of the decode split attention ("retain
+ * the prefill KV cache for the prompt itself, which is shared by all groups", l.205 "a separate
+ * KV buffer for its response tokens"; LSE merge = DESIGN R8): builds the step's attention work
+ * list and issues exactly the launches one decode layer issues, on caller data (one layer):
+ *   d_q        [rows][Hq][128] bf16 query rows (after QK-norm and RoPE)
+ *   d_prefix   [groups][2][Hkv][plen][128] bf16 shared-prefix K then V of each group
+ *   d_pool     [num_pages][2][Hkv][page_tokens][128] bf16 page pool (K then V per page)
+ *   d_pagetab  [rows][maxp] int32 page ids of each row's suffix, in token order
+ *   d_row_len  [rows] int32 suffix tokens each row attends to (t + 1); 0 = idle row
+ *   grp_rows   rows per group: rows m*grp_rows .. attend to prefix m (groups*grp_rows <= rows <= 64)
+ *   impl       0 = the decode step's choice for `rows` rows, 1 = tcgen05 prefix + warp suffix units
+ *              with the fused merge, 2 = tcgen05 prefix + 64-token CTA units + merge kernel,
+ *              3 = CUDA-core prefix chunks + CTA units + merge kernel (groups = 1)
+ *   d_out      [rows][Hq][128] bf16 output (rows that are idle are not written);
+ *   d_out_f32  (nullable) the same before the bf16 rounding
+ *   reps, h_ms reps > 0: then `reps` more timed runs, each after a 256 MiB write that evicts L2;
+ *              h_ms[reps] receives each run's CUDA-event time of the attention launches alone.
+ * Synchronous (allocates its scratch per call).  Errors: IS_ERR_CONFIG (shapes, impl),
+ * IS_ERR_CAPACITY (more partials than the merge holds), IS_ERR_DATA (a length above
+ * maxp*page_tokens). */
+is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t plen, int32_t groups, int32_t grp_rows,
+                      const void* d_pool, int32_t num_pages, int32_t page_tokens, const int32_t* d_pagetab,
+                      int32_t maxp, const int32_t* d_row_len, int32_t rows, int32_t Hq, int32_t Hkv, int32_t impl,
+                      void* d_out, float* d_out_f32, int32_t reps, float* h_ms, void* stream);
 
 /* Debug: copy an internal activation buffer to the host (0 q [rc][Hq][128] bf16,
  * 1 residual [rc][H] f32, 3 final normalised rows [rc][H] bf16, 4 attention

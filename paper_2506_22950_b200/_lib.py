@@ -18,7 +18,7 @@ ADV_MODES = {"std_norm": 0, "mean_only": 1}
 EXPORTS = ["is_plan", "is_create", "is_destroy", "is_prefill", "is_start_group", "is_decode_step",
            "is_refill", "is_run_group", "is_query", "is_copy_tokens", "is_copy_schedule",
            "is_group_results", "is_group_advantages", "is_set_logits_dump", "is_profile_step",
-           "is_profile_step_graph", "is_profile_kernel", "is_dbg_topp",
+           "is_profile_step_graph", "is_profile_kernel", "is_dbg_topp", "is_dbg_attn",
            "is_dbg_gemm", "is_dbg_copy", "is_prefill_slot", "is_start_group_slot",
            "is_run_until_any_done", "is_query_slot", "is_copy_tokens_slot", "is_copy_schedule_slot",
            "is_group_results_slot", "is_nccl_unique_id", "is_nccl_comm_init", "is_allgather_results",
@@ -116,6 +116,8 @@ def load(build_if_missing=True):
     L.is_dbg_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]
     L.is_dbg_topp.argtypes = [vp, i32, i32, ctypes.c_float, ctypes.c_float, ctypes.c_uint64, vp, vp, vp, vp]
     L.is_dbg_copy.argtypes = [vp, i32, vp, ctypes.c_int64]
+    L.is_dbg_attn.argtypes = [vp, vp, i32, i32, i32, vp, i32, i32, vp, i32, vp, i32, i32, i32, i32, vp, vp, i32,
+                              ctypes.POINTER(ctypes.c_float), vp]
     L.is_prefill_slot.argtypes = [vp, i32, vp, i32]
     L.is_start_group_slot.argtypes = [vp, i32, vp, vp]
     L.is_run_until_any_done.argtypes = [vp, i32, ctypes.POINTER(i32), i64p]
@@ -218,6 +220,23 @@ def is_dbg_gemm(w, x, y, split=1, stream=0):
     L = load()
     M, K = w.shape
     _check(L.is_dbg_gemm(w.data_ptr(), x.data_ptr(), y.data_ptr(), M, K, x.shape[0], split, stream))
+
+
+def is_dbg_attn(q, prefix, pool, pagetab, row_len, grp_rows, impl=0, out_f32=None, reps=0, stream=0):
+    """Decode split attention of one layer on caller device tensors (include/infsamp.h):
+    q [rows][Hq][128] bf16, prefix [groups][2][Hkv][plen][128] bf16, pool [pages][2][Hkv][pt][128]
+    bf16, pagetab [rows][maxp] int32, row_len [rows] int32.  Returns (out bf16 [rows][Hq][128],
+    per-rep milliseconds)."""
+    import torch
+    rows, Hq, _ = q.shape
+    groups, _, Hkv, plen, _ = prefix.shape
+    num_pages, _, _, pt, _ = pool.shape
+    out = torch.zeros(rows, Hq, 128, dtype=torch.bfloat16, device=q.device)
+    ms = (ctypes.c_float * max(reps, 1))()
+    _check(load().is_dbg_attn(q.data_ptr(), prefix.data_ptr(), plen, groups, grp_rows, pool.data_ptr(), num_pages,
+                              pt, pagetab.data_ptr(), pagetab.shape[1], row_len.data_ptr(), rows, Hq, Hkv, impl,
+                              out.data_ptr(), None if out_f32 is None else out_f32.data_ptr(), reps, ms, stream))
+    return out, [float(ms[i]) for i in range(reps)]
 
 
 def weight_pointer_list(weights, layers):

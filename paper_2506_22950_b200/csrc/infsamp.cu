@@ -365,7 +365,8 @@ static is_status launch_gemm(int BN, const CUtensorMap& tA, const CUtensorMap& t
 
 // Split-K so that tiles * split fills at most one CTA per SM: a GEMM never
 // takes more than half an SM, so the next kernel's CTAs (PDL) co-reside and
-// prefetch their weights while this one drains.
+// prefetch their weights while this one drains.  BN is the decode row tile; the
+// prefill's 64-row chunks use the 16-row policy (the one measured for them).
 static int choose_split(int num_tiles, int kb_total, int BN) {
   if (num_tiles > g_num_sms) return 1;
   int s = std::max(1, g_num_sms / num_tiles);
@@ -490,6 +491,7 @@ struct is_ctx {
   long long* st_host;  // pinned mirror
   int32_t *slot_uid, *slot_count, *tpos, *true_len, *queue, *main_init, *main_queue, *free_stack, *pagetab,
       *npages, *tokens, *log_slot, *log_live;
+  uint8_t* done_flag;  // [M][G] sample completed
   float* logits_dump;
   int prompt_id, prompt_last;
   bool prefilled, started;
@@ -552,6 +554,7 @@ static SchedArgs sched_args(is_ctx* c) {
   a.tokens = c->tokens;
   a.log_slot = c->log_slot;
   a.log_live = c->log_live;
+  a.done_flag = c->done_flag;
   a.keys = c->keys;
   a.lp_key = c->lp_key;
   a.lp_mlz = c->lp_mlz;
@@ -598,9 +601,22 @@ static void prof_mark(cudaStream_t st, int kind) {
 }
 
 
-// Decode shared-prefix attention on tcgen05: one CTA per (kv head, 128-token tile).
+// Attention launches of one layer.  Decode: the shared-prefix part on tcgen05
+// (attn_prefix_tc_kernel, one CTA per (group, kv head, 128-token prefix tile)) then the
+// per-slot suffix units, whose last unit per (row, kv head) merges it (fused), or 64-token
+// CTA units and a separate merge kernel; without the tcgen05 prefix (N > 64) the prefix
+// chunks are CUDA-core work items of the same attn_kernel.  Prefill: causal CUDA-core
+// prefix units + merge.
+struct AttnLaunch {
+  const CUtensorMap* tm_prefix;  // decode tcgen05 prefix: rows = groups x grp_kv_rows, 128 bf16 columns
+  int kv_row_base;               // tensor-map row of this layer's prefix K, group 0
+  int grp_kv_rows;               // tensor-map rows per group
+  int groups;                    // co-resident groups M
+  int grp_rows;                  // rows per group g
+};
+
 template <int REP, int N>
-static is_status launch_prefix_tc_n(is_ctx* c, const AttnArgs& aa, int l, cudaStream_t st) {
+static is_status launch_prefix_tc_n(const AttnArgs& aa, const AttnLaunch& al, cudaStream_t st) {
   using SM = PrefixTcSmem<N>;
   auto kern = attn_prefix_tc_kernel<REP, N>;
   static bool attr = false;
@@ -608,11 +624,10 @@ static is_status launch_prefix_tc_n(is_ctx* c, const AttnArgs& aa, int l, cudaSt
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::v));
     attr = true;
   }
-  const int nt = (int)ceil_div64(c->pcap, 128);
-  const int kv_row_base = l * 2 * c->sh.n_kv_heads * c->pcap;
+  const int nt = (int)ceil_div64(aa.plen, 128);
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute at[1];
-  cfg.gridDim = dim3(c->M * c->sh.n_kv_heads * nt);
+  cfg.gridDim = dim3(al.groups * aa.Hkv * nt);
   cfg.blockDim = dim3(128);
   cfg.dynamicSmemBytes = SM::v;
   cfg.stream = st;
@@ -625,22 +640,44 @@ static is_status launch_prefix_tc_n(is_ctx* c, const AttnArgs& aa, int l, cudaSt
   }
   AttnArgs a2 = aa;
   a2.dbg_ts = aa.dbg_ts ? aa.dbg_ts + (size_t)2 * 296 * 16 : nullptr;
-  a2.grp_rows = c->g;
-  a2.grp_kv_rows = c->sh.layers * 2 * c->sh.n_kv_heads * c->pcap;
-  CK(cudaLaunchKernelEx(&cfg, kern, c->tm_prefix_kv, a2, kv_row_base));
+  a2.grp_rows = al.grp_rows;
+  a2.grp_kv_rows = al.grp_kv_rows;
+  CK(cudaLaunchKernelEx(&cfg, kern, *al.tm_prefix, a2, al.kv_row_base));
   ++g_launches;
   return IS_OK;
 }
 // MMA N of the tcgen05 prefix part: one group's live slots x Hq/Hkv query heads, padded to 16.
 static int prefix_cols(int g, int rep) { return (int)ceil_div64((int64_t)g * rep, 16) * 16; }
+
 template <int REP>
-static is_status launch_prefix_tc(is_ctx* c, const AttnArgs& aa, int l, cudaStream_t st) {
-  switch (prefix_cols(c->g, REP)) {
-    case 16: return launch_prefix_tc_n<REP, 16>(c, aa, l, st);
-    case 32: return launch_prefix_tc_n<REP, 32>(c, aa, l, st);
-    case 64: return launch_prefix_tc_n<REP, 64>(c, aa, l, st);
+static is_status launch_attn_rep(const AttnArgs& aa, const AttnLaunch& al, cudaStream_t st) {
+  if (aa.tc_prefix) {
+    switch (prefix_cols(al.grp_rows, REP)) {
+      case 16: CKS((launch_prefix_tc_n<REP, 16>(aa, al, st))); break;
+      case 32: CKS((launch_prefix_tc_n<REP, 32>(aa, al, st))); break;
+      case 64: CKS((launch_prefix_tc_n<REP, 64>(aa, al, st))); break;
+      default: return fail(IS_ERR_CONFIG, "tcgen05 prefix attention needs g * Hq/Hkv <= 64");
+    }
   }
-  return fail(IS_ERR_CONFIG, "tcgen05 prefix attention needs row_capacity * Hq/Hkv in {16, 32, 64}");
+  if (aa.merge_cnt) {  // decode, warp units with the fused merge
+    CKS(launch_k_smem(attn_suffix_warp_kernel<REP>, dim3(3 * g_num_sms), dim3(kAttnThreads), SuffixWarpSmem<REP>::v,
+                      st, aa));
+    return IS_OK;
+  }
+  const int nblk = aa.prefill ? aa.Hkv * aa.nc_pre * (int)ceil_div64(aa.rows, kAttnWarps) : 4 * g_num_sms;
+  CKS(launch_k_smem(attn_kernel<REP>, dim3(nblk), dim3(kAttnThreads), AttnSmem<REP>::v, st, aa));
+  CKS(launch_k(attn_merge_kernel<REP>, dim3(aa.rows, aa.Hkv), dim3(32), st, aa));
+  return IS_OK;
+}
+
+static is_status launch_attention(const AttnArgs& aa, const AttnLaunch& al, cudaStream_t st) {
+  switch (aa.Hq / aa.Hkv) {
+    case 1: return launch_attn_rep<1>(aa, al, st);
+    case 2: return launch_attn_rep<2>(aa, al, st);
+    case 4: return launch_attn_rep<4>(aa, al, st);
+    case 8: return launch_attn_rep<8>(aa, al, st);
+  }
+  return fail(IS_ERR_CONFIG, "Hq / Hkv must be 1, 2, 4 or 8");
 }
 
 // One layer stack over `rows` rows starting at row 0 (decode: rows = rc, BN = c->BN;
@@ -684,7 +721,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       a.M = c->qkv_w;
       a.K = H;
       a.num_tiles = ceil_div64(a.M, kBM);
-      a.split = prefill ? choose_split(a.num_tiles, H / kBK, 64) : c->split_qkv;
+      a.split = prefill ? choose_split(a.num_tiles, H / kBK, 16) : c->split_qkv;
       a.row0 = r0;
       a.n_valid = std::min(chunk, rows - r0);
       QkvEpiArgs& e = a.qkv;
@@ -742,36 +779,22 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
     aa.NC = c->NC;
     aa.prefill = prefill ? 1 : 0;
     aa.scale = 1.0f / sqrtf((float)kHD);
-    const int nblk = prefill ? Hkv * aa.nc_pre * (int)ceil_div64(rows, kAttnWarps) : 4 * g_num_sms;
-    const bool do_attn = prefill || !(g_skip & 8);
-#define IS_ATTN_LAUNCH(R)                                                                                      \
-  do {                                                                                                         \
-    if (do_attn && aa.tc_prefix) CKS(launch_prefix_tc<R>(c, aa, l, st));                                       \
-    if (do_attn && aa.merge_cnt)                                                                               \
-      CKS(launch_k_smem(attn_suffix_warp_kernel<R>, dim3(3 * g_num_sms), dim3(kAttnThreads),                  \
-                        SuffixWarpSmem<R>::v, st, aa));                                                      \
-    else if (do_attn) CKS(launch_k_smem(attn_kernel<R>, dim3(nblk), dim3(kAttnThreads), AttnSmem<R>::v, st, aa)); \
-    if (do_attn && getenv("IS_ATTN_TWICE")) {                                                                 \
-      AttnArgs a2 = aa;                                                                                        \
-      if (a2.dbg_ts) a2.dbg_ts += (size_t)2 * 296 * 16;                                                       \
-      CKS(launch_k_smem(attn_kernel<R>, dim3(nblk), dim3(kAttnThreads), AttnSmem<R>::v, st, a2));            \
-    }                                                                                                          \
-    if (do_attn && !aa.merge_cnt) CKS(launch_k(attn_merge_kernel<R>, dim3(rows, Hkv), dim3(32), st, aa));     \
-  } while (0)
-    switch (Hq / Hkv) {
-      case 1: IS_ATTN_LAUNCH(1); break;
-      case 2: IS_ATTN_LAUNCH(2); break;
-      case 4: IS_ATTN_LAUNCH(4); break;
-      default: IS_ATTN_LAUNCH(8); break;
+    if (prefill || !(g_skip & 8)) {
+      AttnLaunch al{};
+      al.tm_prefix = &c->tm_prefix_kv;
+      al.kv_row_base = l * 2 * Hkv * c->pcap;
+      al.grp_kv_rows = s.layers * 2 * Hkv * c->pcap;
+      al.groups = c->M;
+      al.grp_rows = c->g;
+      CKS(launch_attention(aa, al, st));
     }
-#undef IS_ATTN_LAUNCH
     prof_mark(st, 3);
     for (int r0 = 0; r0 < rows; r0 += chunk) {
       GemmArgs a{};
       a.M = H;
       a.K = Hq * kHD;
       a.num_tiles = ceil_div64(a.M, kBM);
-      a.split = prefill ? choose_split(a.num_tiles, a.K / kBK, 64) : c->split_o;
+      a.split = prefill ? choose_split(a.num_tiles, a.K / kBK, 16) : c->split_o;
       a.row0 = r0;
       a.n_valid = std::min(chunk, rows - r0);
       a.out = c->resid;
@@ -798,7 +821,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       a.M = 2 * F;
       a.K = H;
       a.num_tiles = ceil_div64(a.M, kBM);
-      a.split = prefill ? choose_split(a.num_tiles, H / kBK, 64) : c->split_gu;
+      a.split = prefill ? choose_split(a.num_tiles, H / kBK, 16) : c->split_gu;
       a.row0 = r0;
       a.n_valid = std::min(chunk, rows - r0);
       a.act = c->act;
@@ -819,7 +842,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       a.M = H;
       a.K = F;
       a.num_tiles = ceil_div64(a.M, kBM);
-      a.split = prefill ? choose_split(a.num_tiles, F / kBK, 64) : c->split_d;
+      a.split = prefill ? choose_split(a.num_tiles, F / kBK, 16) : c->split_d;
       a.row0 = r0;
       a.n_valid = std::min(chunk, rows - r0);
       a.out = c->resid;
@@ -1019,6 +1042,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
     c->num_pages = (int)((resv - c->prefix_bytes) / c->page_bytes);
   }
   c->num_pages *= c->M;  // the budget is per group; the pool is shared by the co-resident groups
+  if (const char* e = getenv("IS_DBG_POOL_PAGES")) c->num_pages = std::max(1, atoi(e));  // negative tests only
   c->log_cap = c->G * c->max_new + c->N * cfg->prefix_k + 8;
   c->max_rows = std::max(c->rc, (int)ceil_div64(c->pcap, 64) * 64);
   c->max_pos = c->P + c->max_new + 1;
@@ -1034,6 +1058,9 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   {
     const char* e = getenv("IS_SEPARATE_MERGE");
     c->sep_merge = e ? atoi(e) != 0 : c->rc >= 32;
+    // the separate merge kernel holds <= 32 partials (prefix tiles + 64-token chunks); longer
+    // prompts / generations fall back to the warp units with the fused (<= 64-partial) merge
+    if (c->sep_merge && c->tc_prefix && c->nc_pre_dec + ceil_div64(c->max_new, kSC) > 32) c->sep_merge = 0;
   }
   c->sc = (c->tc_prefix && !c->sep_merge) ? kSCW : kSC;
   c->nc_suf = (int)ceil_div64(c->max_new, c->sc);
@@ -1163,6 +1190,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->log_slot = (int32_t*)A((size_t)M * c->log_cap * c->g * 4);
   c->log_live = (int32_t*)A((size_t)M * c->log_cap * 4);
   c->logprobs = (float*)A((size_t)M * c->G * c->max_new * 4);
+  c->done_flag = (uint8_t*)A((size_t)M * c->G);
   c->d_prompt_copy = (int32_t*)A((size_t)c->P * 4);
   if (err != IS_OK) return err;
   CK(cudaMallocHost(&c->st_host, sizeof(long long) * ST_COUNT * (M + 1)));
@@ -1262,7 +1290,7 @@ extern "C" void is_destroy(is_ctx* c) {
                   c->row_t, c->row_tok, c->row_pos, c->row_kvloc, c->row_len, c->keys, c->last_tok,
                   c->last_fin, c->st_dev, c->slot_uid, c->slot_count, c->tpos, c->true_len, c->queue,
                   c->main_init, c->main_queue, c->free_stack, c->pagetab, c->npages, c->tokens, c->log_slot,
-                  c->log_live, c->d_prompt_copy, c->lp_key, c->lp_mlz, c->logprobs, c->prow_active, c->prow_tok, c->prow_pos, c->prow_kvloc,
+                  c->log_live, c->d_prompt_copy, c->lp_key, c->lp_mlz, c->logprobs, c->done_flag, c->prow_active, c->prow_tok, c->prow_pos, c->prow_kvloc,
                   c->prow_len, c->fn_bar, c->logits_tp, c->scores_tp, c->ebits_tp, c->wpart_tp, c->hist_tp,
                   c->sel_tp, c->state_tp};
   for (void* p : bufs)
@@ -1285,6 +1313,12 @@ extern "C" void is_destroy(is_ctx* c) {
 // a group is done when all G samples completed, or (dynamic mode, R35) its target did
 static bool group_done(const is_ctx* c, const long long* st) {
   return st[ST_DONE] >= (st[ST_TARGET] > 0 ? st[ST_TARGET] : (long long)c->G);
+}
+
+// The device scheduler found the page pool exhausted (the KV budget violated, R25):
+// sticky for the context, every row idle from that step on.
+static is_status budget_error() {
+  return fail(IS_ERR_BUDGET, "KV page pool exhausted during decoding (budget violated); the context's rows are stopped");
 }
 
 extern "C" is_status is_prefill_slot(is_ctx* c, int32_t slot, const int32_t* d_prompt, int32_t prompt_id) {
@@ -1391,6 +1425,7 @@ extern "C" is_status is_start_group_slot(is_ctx* c, int32_t m, const int32_t* tr
   CK(cudaMemcpyAsync(c->main_init + og, init.data(), g * 4, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(c->main_queue + oG, queue.data(), G * 4, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemsetAsync(c->npages + oG, 0, G * 4, c->st));
+  CK(cudaMemsetAsync(c->done_flag + oG, 0, G, c->st));
   CK(cudaMemsetAsync(c->tokens + oG * c->max_new, 0xFF, (size_t)G * c->max_new * 4, c->st));
   CK(cudaMemsetAsync(c->logprobs + oG * c->max_new, 0, (size_t)G * c->max_new * 4, c->st));
   CK(cudaMemsetAsync(c->log_slot + (size_t)m * c->log_cap * g, 0xFF, (size_t)c->log_cap * g * 4, c->st));
@@ -1413,6 +1448,7 @@ extern "C" is_status is_decode_step(is_ctx* c, int32_t* d_next, uint8_t* d_fin) 
   if (!c) return fail(IS_ERR_CONFIG, "null argument");
   if (!c->started && std::find(c->gstarted.begin(), c->gstarted.end(), 1) == c->gstarted.end())
     return fail(IS_ERR_STATE, "is_decode_step before is_start_group");
+  if (c->st_host[(size_t)c->M * ST_COUNT + ST_ERROR]) return budget_error();  // (as of the last step copied back)
   StreamGuard guard(c, c->user);
   if (getenv("IS_NO_GRAPH")) CKS(enqueue_step(c));
   else CK(cudaGraphLaunch(c->graph, c->st));
@@ -1430,7 +1466,7 @@ extern "C" is_status is_refill(is_ctx* c, uint8_t* d_fin, int32_t* d_new_uid) {
   if (d_fin) CK(cudaMemcpyAsync(d_fin, c->last_fin, c->rc, cudaMemcpyDeviceToDevice, c->st));
   if (d_new_uid) {
     CK(cudaMemsetAsync(d_new_uid, 0xFF, c->rc * 4, c->st));
-    CK(cudaMemcpyAsync(d_new_uid, c->slot_uid, c->g * 4, cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaMemcpyAsync(d_new_uid, c->slot_uid, (size_t)c->M * c->g * 4, cudaMemcpyDeviceToDevice, c->st));
   }
   return IS_OK;
 }
@@ -1454,12 +1490,13 @@ static is_status run_until(is_ctx* c, int32_t max_steps, bool any, int32_t* h_do
   };
   // groups already complete when called do not end an `any` run
   const int done0 = done_mask(c->st_host).first;
+  const long long* err = c->st_host + (size_t)c->M * ST_COUNT + ST_ERROR;
   is_status rs = IS_OK;
   for (int i = 0; i < max_steps; ++i) {
     if (i >= D) {
       cudaEventSynchronize(ev[i % D]);
       const auto dm = done_mask(c->st_host);
-      if (dm.second == 0 || (any && (dm.first & ~done0))) break;
+      if (dm.second == 0 || (any && (dm.first & ~done0)) || *err) break;
     }
     if (nograph) rs = enqueue_step(c);
     else if (cudaGraphLaunch(c->graphK_ok ? c->graphK : c->graph, c->st) != cudaSuccess)
@@ -1471,6 +1508,7 @@ static is_status run_until(is_ctx* c, int32_t max_steps, bool any, int32_t* h_do
   for (int i = 0; i < D; ++i) cudaEventDestroy(ev[i]);
   if (rs != IS_OK) return rs;
   if (h_done_mask) *h_done_mask = done_mask(c->st_host).first;
+  if (*err) return budget_error();
   return IS_OK;
 }
 
@@ -1557,8 +1595,8 @@ extern "C" is_status is_group_results_slot(is_ctx* c, int32_t m, float* d_reward
   if (m < 0 || m >= c->M) return fail(IS_ERR_CONFIG, "group slot %d out of range [0, %d)", m, c->M);
   StreamGuard guard(c, c->user);
   results_kernel<<<(c->G + 127) / 128, 128, 0, c->st>>>(c->tokens + (size_t)m * c->G * c->max_new,
-                                                      c->true_len + (size_t)m * c->G, c->G, c->max_new, c->sh.vocab,
-                                                      d_reward, d_len);
+                                                      c->true_len + (size_t)m * c->G, c->done_flag + (size_t)m * c->G,
+                                                      c->G, c->max_new, c->sh.vocab, d_reward, d_len);
   CK(cudaGetLastError());
   return IS_OK;
 }
@@ -1718,6 +1756,134 @@ extern "C" is_status is_dbg_gemm(const void* d_w, const void* d_x, float* d_y, i
   CKS(launch_gemm<EPI_STORE_F32>(BN, tA, tB, a, (cudaStream_t)stream));
   CK(cudaGetLastError());
   return IS_OK;
+}
+
+// Kernel-level hook of the decode split attention (R8):
+// the work list and the attention launches of one decode layer, exactly as the step issues
+// them (launch_attention), on caller data.  See include/infsamp.h.
+extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t plen, int32_t groups,
+                                 int32_t grp_rows, const void* d_pool, int32_t num_pages, int32_t page_tokens,
+                                 const int32_t* d_pagetab, int32_t maxp, const int32_t* d_row_len, int32_t rows,
+                                 int32_t Hq, int32_t Hkv, int32_t impl, void* d_out, float* d_out_f32,
+                                 int32_t reps, float* h_ms, void* stream) {
+  if (!d_q || !d_prefix || !d_pool || !d_pagetab || !d_row_len || !d_out) return fail(IS_ERR_CONFIG, "null argument");
+  if (rows < 1 || rows > 64 || groups < 1 || grp_rows < 1 || groups * grp_rows > rows || plen < 1 || Hkv < 1 ||
+      Hq % Hkv || Hq / Hkv > kMaxRep || page_tokens < 4 || 64 % page_tokens || maxp < 1 || num_pages < 1 ||
+      impl < 0 || impl > 3 || reps < 0 || (reps > 0 && !h_ms))
+    return fail(IS_ERR_CONFIG, "bad is_dbg_attn arguments");
+  if (!g_num_sms) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int rep = Hq / Hkv;
+  const bool tc_ok = prefix_cols(grp_rows, rep) <= 64;
+  const bool tc = impl == 0 ? tc_ok : impl != 3;
+  const bool sep = impl == 0 ? rows >= 32 : impl != 1;
+  if (tc && !tc_ok) return fail(IS_ERR_CONFIG, "tcgen05 prefix needs grp_rows * Hq/Hkv <= 64");
+  if (!tc && groups != 1) return fail(IS_ERR_CONFIG, "the CUDA-core prefix serves one group");
+  const int sc = (tc && !sep) ? kSCW : kSC;
+  const int nc_pre = tc ? (int)ceil_div64(plen, 128) : (int)ceil_div64(plen, kPC);
+  const int nc_suf = (int)ceil_div64((int64_t)maxp * page_tokens, sc);
+  if (nc_pre + nc_suf > (sc == kSCW ? 64 : 32))
+    return fail(IS_ERR_CAPACITY, "%d partials exceed the merge (%d)", nc_pre + nc_suf, sc == kSCW ? 64 : 32);
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<int32_t> len(rows), act(rows), lid(rows);
+  CK(cudaMemcpy(len.data(), d_row_len, rows * 4, cudaMemcpyDeviceToHost));
+  for (int r = 0; r < rows; ++r) {
+    if (len[r] < 0 || len[r] > maxp * page_tokens) return fail(IS_ERR_DATA, "row %d length %d", r, len[r]);
+    act[r] = len[r] > 0 && r < groups * grp_rows;
+    lid[r] = r;
+  }
+  const int NC = nc_pre + nc_suf;
+  is_status err = IS_OK;
+  int32_t* d_act = (int32_t*)dalloc((size_t)rows * 4, &err);
+  int32_t* d_lid = (int32_t*)dalloc((size_t)rows * 4, &err);
+  int32_t* items = (int32_t*)dalloc((size_t)Hkv * (nc_pre * ((rows + 3) / 4) + rows * nc_suf) * kItemStride * 4 + 64, &err);
+  long long* nit = (long long*)dalloc(2 * sizeof(long long), &err);
+  float* part_o = (float*)dalloc((size_t)rows * Hq * NC * 128 * 4, &err);
+  float* part_ml = (float*)dalloc((size_t)rows * Hq * NC * 2 * 4, &err);
+  int* mcnt = (int*)dalloc((size_t)rows * Hkv * 4, &err);
+  uint8_t* flush = reps > 0 ? (uint8_t*)dalloc((size_t)256 << 20, &err) : nullptr;  // > 2x the 126 MB L2
+  CUtensorMap tm;
+  if (err == IS_OK) err = make_tmap(&tm, d_prefix, (int64_t)groups * 2 * Hkv * plen, 128, 128);
+  if (err == IS_OK) {
+    cudaMemcpy(d_act, act.data(), rows * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_lid, lid.data(), rows * 4, cudaMemcpyHostToDevice);
+    WorkList wl;
+    wl.row_cap = rows;
+    wl.chunk = sc;
+    wl.pt = page_tokens;
+    wl.Hkv = Hkv;
+    wl.nc_pre = nc_pre;
+    wl.tc_prefix = tc ? 1 : 0;
+    wl.maxp = maxp;
+    wl.row_active = d_act;
+    wl.row_len = d_row_len;
+    wl.row_lid = d_lid;
+    wl.pagetab = d_pagetab;
+    wl.items = items;
+    wl.n_items = nit;
+    attn_worklist_kernel<<<1, kSchedThreads, 0, st>>>(wl);
+    AttnArgs aa{};
+    aa.q = (const __nv_bfloat16*)d_q;
+    aa.kpre = (const __nv_bfloat16*)d_prefix;
+    aa.vpre = aa.kpre + (size_t)Hkv * plen * kHD;
+    aa.pool = (const __nv_bfloat16*)d_pool;
+    aa.row_active = d_act;
+    aa.row_len = d_row_len;
+    aa.part_o = part_o;
+    aa.part_ml = part_ml;
+    aa.items = items;
+    aa.n_items = nit;
+    aa.out = (__nv_bfloat16*)d_out;
+    aa.out_f32 = d_out_f32;
+    aa.rows = rows;
+    aa.Hq = Hq;
+    aa.Hkv = Hkv;
+    aa.pcap = plen;
+    aa.plen = plen;
+    aa.pt = page_tokens;
+    aa.nc_pre = nc_pre;
+    aa.nc_suf = nc_suf;
+    aa.NC = NC;
+    aa.prefill = 0;
+    aa.tc_prefix = tc ? 1 : 0;
+    aa.merge_cnt = (tc && !sep) ? mcnt : nullptr;
+    aa.sc = sc;
+    aa.scale = 1.0f / sqrtf((float)kHD);
+    AttnLaunch al{};
+    al.tm_prefix = &tm;
+    al.kv_row_base = 0;
+    al.grp_kv_rows = 2 * Hkv * plen;
+    al.groups = groups;
+    al.grp_rows = grp_rows;
+    err = launch_attention(aa, al, st);
+    if (err == IS_OK && reps > 0) {
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      for (int i = 0; i < reps && err == IS_OK; ++i) {
+        cudaMemsetAsync(flush, i & 0xFF, (size_t)256 << 20, st);  // evict the KV from L2
+        cudaEventRecord(e0, st);
+        err = launch_attention(aa, al, st);
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&h_ms[i], e0, e1);
+      }
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+    if (err == IS_OK) {
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e != cudaSuccess) err = fail(IS_ERR_CUDA, "is_dbg_attn: %s", cudaGetErrorString(e));
+    }
+  }
+  for (void* p : {(void*)d_act, (void*)d_lid, (void*)items, (void*)nit, (void*)part_o, (void*)part_ml, (void*)mcnt,
+                  (void*)flush})
+    if (p) cudaFree(p);
+  return err;
 }
 
 // Debug: print the GEMM timeline of the last replayed step (IS_TIMELINE=1).

@@ -114,6 +114,7 @@ struct AttnArgs {
   const long long* n_items;   // [2]: total items, prefix items
   unsigned long long* dbg_ts; // optional [gridDim][16] globaltimer stamps
   __nv_bfloat16* out;         // [rows][Hq][128]
+  float* out_f32;             // optional (is_dbg_attn): the merged output before the bf16 rounding (r4)
   int rows, Hq, Hkv, pcap, plen, pt;
   int nc_pre, nc_suf, NC;
   int prefill;                // 1: rows are prompt positions, causal over the prefix, no suffix
@@ -239,6 +240,14 @@ struct AttnSmem {
   static constexpr int v = kKV + kQ + kComb + 64;
 };
 
+// Merged output of (row r, query head qh): dims 4*lane..4*lane+3, rounded to bf16 (r4).
+__device__ __forceinline__ void attn_store_out(const AttnArgs& a, int r, int qh, float4 o, int lane) {
+  __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(a.out + ((size_t)r * a.Hq + qh) * kHD) + 2 * lane;
+  o2[0] = __floats2bfloat162_rn(o.x, o.y);
+  o2[1] = __floats2bfloat162_rn(o.z, o.w);
+  if (a.out_f32) reinterpret_cast<float4*>(a.out_f32 + ((size_t)r * a.Hq + qh) * kHD)[lane] = o;
+}
+
 // LSE merge (R8) of one (row r, query head h*REP + j): lane i holds partial i's
 // (m, l) (<= 32 partials); all o loads are issued together; fixed order.
 template <int REP>
@@ -286,9 +295,7 @@ __device__ __forceinline__ void attn_merge_one(const AttnArgs& a, int r, int h, 
     }
   }
   const float inv = 1.0f / den;
-  __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(a.out + ((size_t)r * a.Hq + qh) * kHD) + 2 * lane;
-  o2[0] = __floats2bfloat162_rn(num.x * inv, num.y * inv);
-  o2[1] = __floats2bfloat162_rn(num.z * inv, num.w * inv);
+  attn_store_out(a, r, qh, make_float4(num.x * inv, num.y * inv, num.z * inv, num.w * inv), lane);
 }
 
 // Decode suffix pass behind the tcgen05 prefix kernel (every work item is a suffix
@@ -599,9 +606,7 @@ __global__ void __launch_bounds__(32) attn_merge_kernel(AttnArgs a) {
       }
     }
     const float inv = 1.0f / den;
-    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(a.out + ((size_t)r * a.Hq + qh) * kHD) + 2 * lane;
-    o2[0] = __floats2bfloat162_rn(num.x * inv, num.y * inv);
-    o2[1] = __floats2bfloat162_rn(num.z * inv, num.w * inv);
+    attn_store_out(a, r, qh, make_float4(num.x * inv, num.y * inv, num.z * inv, num.w * inv), lane);
   }
 }
 
@@ -898,6 +903,7 @@ struct SchedArgs {
   int32_t* tokens;           // [M][G][max_new]
   int32_t* log_slot;         // [M][log_cap][g]
   int32_t* log_live;         // [M][log_cap] pages held by the group
+  uint8_t* done_flag;        // [M][G] 1 once the sample completed (length or EOS)
   unsigned long long* keys;  // [row_cap] lm_head argmax keys
   const unsigned long long* lp_key;  // [row_cap][lp_grid] per-CTA best keys (NEXT-3 log-probabilities)
   const float4* lp_mlz;      // [row_cap][lp_grid] per-CTA (max z, sum exp, winner's z)
@@ -920,11 +926,75 @@ struct SchedArgs {
   int Hkv, nc_pre, nc_suf, chunk, tc_prefix;
 };
 
+// Work list of one decode attention launch, built from the row tables by
+// the kSchedThreads threads of one CTA: shared-prefix items first (CUDA-core prefix only:
+// one per (group of 4 rows with a live row, kv head, kPC-token chunk)), then one suffix
+// item per (row, chunk of `chunk` tokens, kv head) carrying the chunk's page ids and
+// the row's length.  n_items[0] = items, n_items[1] = prefix items.
+struct WorkList {
+  int row_cap, chunk, pt, Hkv, nc_pre, tc_prefix, maxp;
+  const int32_t* row_active;
+  const int32_t* row_len;   // suffix tokens visible (t + 1)
+  const int32_t* row_lid;   // page-table row of each row
+  const int32_t* pagetab;   // [*][maxp]
+  int32_t* items;           // [*][kItemStride]
+  long long* n_items;       // [2]
+};
+constexpr int kSchedThreads = 128;
+__device__ void build_attn_worklist(const WorkList& w, int* s_cnt /* [65] */, int* s_npre) {
+  const int tid = threadIdx.x;
+  int nch = 0;
+  if (tid < w.row_cap) {
+    nch = w.row_active[tid] ? (w.row_len[tid] + w.chunk - 1) / w.chunk : 0;
+    s_cnt[tid] = nch;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // exclusive prefix sum of suffix chunks; shared-prefix items first (CUDA-core prefix only)
+    int n = 0;
+    if (!w.tc_prefix) {
+      for (int g = 0; g * 4 < w.row_cap; ++g) {
+        bool live = false;
+        for (int s = 4 * g; s < 4 * g + 4 && s < w.row_cap; ++s) live = live || w.row_active[s];
+        if (!live) continue;
+        for (int h = 0; h < w.Hkv; ++h)
+          for (int c = 0; c < w.nc_pre; ++c)
+            w.items[(size_t)(n++) * kItemStride] = (int)(0x80000000u | (h << 16) | (c << 8) | g);
+      }
+    }
+    *s_npre = n;
+    int acc = 0;
+    for (int s = 0; s < w.row_cap; ++s) {
+      const int v = s_cnt[s];
+      s_cnt[s] = acc;
+      acc += v;
+    }
+    s_cnt[w.row_cap] = acc;
+    w.n_items[0] = n + acc * w.Hkv;
+    w.n_items[1] = n;
+  }
+  __syncthreads();
+  // ---- suffix items of row s: (chunk c, kv head h) with the chunk's page ids embedded
+  if (tid < w.row_cap && nch > 0) {
+    const int s = tid;
+    const int ppc = w.chunk / w.pt;  // pages per suffix chunk (<= 16)
+    const int len = w.row_len[s], lid = w.row_lid[s];
+    for (int c = 0; c < nch; ++c)
+      for (int h = 0; h < w.Hkv; ++h) {
+        int32_t* item = w.items + (size_t)(*s_npre + (s_cnt[s] + c) * w.Hkv + h) * kItemStride;
+        item[0] = (c << 16) | (s << 8) | h;
+        if (w.chunk <= 32) item[16] = len;  // (<= 8 page ids: slot 16 is free)
+        const int np = min(ppc, (len - c * w.chunk + w.pt - 1) / w.pt);
+        for (int j = 0; j < np; ++j) item[1 + j] = w.pagetab[(size_t)lid * w.maxp + c * ppc + j];
+      }
+  }
+  __syncthreads();
+}
+
 // One CTA of kSchedThreads.  The policy itself (finish / park / refill in
 // ascending slot order, R18; LIFO page recycling, R26) is sequential and runs
 // on thread 0; the per-row preparation of the next step and its attention work
 // list are independent per row and run one thread per row.
-constexpr int kSchedThreads = 128;
 __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int consume, int prep_mask) {
   pdl_launch_dependents();  // let the next kernel launch and prefetch now; it waits for our completion itself
   pdl_wait();
@@ -996,6 +1066,7 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
           if (uid < 0) continue;
           if (tt_[uid] == true_len[uid] || (a.eos_on && tokens[(size_t)uid * a.max_new + tt_[uid] - 1] == a.eos_id)) {
             st[ST_DONE] += 1;
+            a.done_flag[(size_t)m * a.G + uid] = 1;
             a.last_fin[m * a.g + s] = 1;
             for (int i = 0; i < npages[uid]; ++i) a.free_stack[st0[ST_FREE_TOP]++] = pagetab[(size_t)uid * a.maxp + i];
             st[ST_LIVE] -= npages[uid];
@@ -1058,10 +1129,14 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
           if (uid < 0) continue;
           const int tt = tt_[uid];
           if (tt % a.pt == 0) {
-            int page = 0;
-            if (st0[ST_FREE_TOP] > 0) page = a.free_stack[--st0[ST_FREE_TOP]];
-            else st0[ST_ERROR] = 1;  // budget violated: pool exhausted
-            a.pagetab[((size_t)m * a.G + uid) * a.maxp + tt / a.pt] = page;
+            if (st0[ST_FREE_TOP] == 0) {
+              // budget violated: the pool is exhausted.  No page is handed out (nothing may
+              // alias another sample's KV); the flag stops every row from the next step on
+              // and the host calls report IS_ERR_BUDGET
+              st0[ST_ERROR] = 1;
+              continue;
+            }
+            a.pagetab[((size_t)m * a.G + uid) * a.maxp + tt / a.pt] = a.free_stack[--st0[ST_FREE_TOP]];
             npages[uid] += 1;
             st[ST_LIVE] += 1;
             st0[ST_GLIVE] += 1;
@@ -1071,17 +1146,17 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
     }
     int any = 0;
     for (int r = 0; r < a.M * a.g; ++r) any |= a.slot_uid[r] >= 0;
-    s_any = any;
+    s_any = st0[ST_ERROR] ? 0 : any;
   }
   __syncthreads();
-  // ---- rows of the next step, one thread per row (row s = group m, slot s - m*g)
+  // ---- rows of the next step, one thread per row (row s = group m, slot s - m*g); after a
+  // budget violation no row runs
   const bool any = s_any != 0;
-  int nch = 0;
   if (tid < a.row_cap) {
     const int s = tid;
     a.keys[s] = 0ull;
     const int m = s / a.g;
-    const int uid = m < a.M ? a.slot_uid[s] : -1;
+    const int uid = (m < a.M && any) ? a.slot_uid[s] : -1;
     if (uid < 0) {
       a.row_active[s] = 0;
       a.row_uid[s] = 0;
@@ -1103,34 +1178,27 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
       a.row_pos[s] = a.P - 1 + tt;
       a.row_kvloc[s] = a.pagetab[(size_t)lid * a.maxp + tt / a.pt] * a.pt + tt % a.pt;
       a.row_len[s] = tt + 1;
-      nch = (tt + 1 + a.chunk - 1) / a.chunk;
     }
-    s_cnt[s] = nch;
   }
   __syncthreads();
+  {
+    WorkList wl;
+    wl.row_cap = a.row_cap;
+    wl.chunk = a.chunk;
+    wl.pt = a.pt;
+    wl.Hkv = a.Hkv;
+    wl.nc_pre = a.nc_pre;
+    wl.tc_prefix = a.tc_prefix;
+    wl.maxp = a.maxp;
+    wl.row_active = a.row_active;
+    wl.row_len = a.row_len;
+    wl.row_lid = a.row_lid;
+    wl.pagetab = a.pagetab;
+    wl.items = a.attn_items;
+    wl.n_items = st0 + ST_ATTN_ITEMS;
+    build_attn_worklist(wl, s_cnt, &s_npre);
+  }
   if (tid == 0) {
-    // exclusive prefix sum of suffix chunks; shared-prefix items first (CUDA-core prefix only)
-    int n = 0;
-    if (any && !a.tc_prefix) {
-      for (int g = 0; g * 4 < a.row_cap; ++g) {
-        bool live = false;
-        for (int s = 4 * g; s < 4 * g + 4 && s < a.row_cap; ++s) live = live || a.row_active[s];
-        if (!live) continue;
-        for (int h = 0; h < a.Hkv; ++h)
-          for (int c = 0; c < a.nc_pre; ++c)
-            a.attn_items[(size_t)(n++) * kItemStride] = (int)(0x80000000u | (h << 16) | (c << 8) | g);
-      }
-    }
-    s_npre = n;
-    int acc = 0;
-    for (int s = 0; s < a.row_cap; ++s) {
-      const int v = s_cnt[s];
-      s_cnt[s] = acc;
-      acc += v;
-    }
-    s_cnt[a.row_cap] = acc;
-    st0[ST_ATTN_ITEMS] = n + acc * a.Hkv;
-    st0[ST_ATTN_PRE] = n;
     for (int m = 0; m < a.M; ++m) {
       if (!((prep_mask >> m) & 1)) continue;
       long long* st = a.st + (size_t)m * ST_COUNT;
@@ -1155,21 +1223,13 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
     if (any && consume) st0[ST_GSTEP] += 1;
     if (st0[ST_GLIVE] > st0[ST_GPEAK]) st0[ST_GPEAK] = st0[ST_GLIVE];
   }
-  __syncthreads();
-  // ---- suffix items of row s: (chunk c, kv head h) with the chunk's page ids embedded
-  if (tid < a.row_cap && nch > 0) {
-    const int s = tid;
-    const int ppc = a.chunk / a.pt;  // pages per suffix chunk (<= 16)
-    const int len = a.row_len[s], lid = a.row_lid[s];
-    for (int c = 0; c < nch; ++c)
-      for (int h = 0; h < a.Hkv; ++h) {
-        int32_t* item = a.attn_items + (size_t)(s_npre + (s_cnt[s] + c) * a.Hkv + h) * kItemStride;
-        item[0] = (c << 16) | (s << 8) | h;
-        if (a.chunk <= 32) item[16] = len;  // (<= 8 page ids: slot 16 is free)
-        const int np = min(ppc, (len - c * a.chunk + a.pt - 1) / a.pt);
-        for (int j = 0; j < np; ++j) item[1 + j] = a.pagetab[(size_t)lid * a.maxp + c * ppc + j];
-      }
-  }
+}
+
+// Work list of one decode attention launch, alone (is_dbg_attn): one CTA of kSchedThreads.
+__global__ void __launch_bounds__(kSchedThreads) attn_worklist_kernel(WorkList wl) {
+  __shared__ int s_cnt[65];
+  __shared__ int s_npre;
+  build_attn_worklist(wl, s_cnt, &s_npre);
 }
 
 // Prefill rows: row r = prompt position r (0..P-2), causal over the prefix.
@@ -1201,13 +1261,19 @@ __global__ void reclaim_group_kernel(SchedArgs a, int m) {
   for (int s = 0; s < a.g; ++s) a.slot_uid[m * a.g + s] = -1;
 }
 
-// Benchmark reward (R29) and length per sample.
-__global__ void results_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ true_len, int G,
-                               int max_new, int vocab, float* reward, int32_t* len) {
+// Benchmark reward (R29) and length per sample.  A sample that did not complete
+// (dynamic mode, R35: discarded in flight or never started) reports length 0 and
+// reward 0; a completed one its emitted length (true_len, or shorter at EOS, R37).
+__global__ void results_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ true_len,
+                               const uint8_t* __restrict__ done, int G, int max_new, int vocab, float* reward,
+                               int32_t* len) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= G) return;
-  // emitted length: true_len, or fewer when the sample stopped at EOS (R37) or was
-  // discarded in flight (dynamic mode, R35); tokens past it are -1
+  if (!done[i]) {
+    reward[i] = 0.f;
+    len[i] = 0;
+    return;
+  }
   int c = 0, L = 0;
   const int T = true_len[i];
   while (L < T && tokens[(size_t)i * max_new + L] >= 0) {

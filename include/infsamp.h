@@ -330,9 +330,10 @@ is_status is_dbg_topp(const float* d_logits, int32_t rows, int32_t V, float temp
  *   d_pagetab  [rows][maxp] int32 page ids of each row's suffix, in token order
  *   d_row_len  [rows] int32 suffix tokens each row attends to (t + 1); 0 = idle row
  *   grp_rows   rows per group: rows m*grp_rows .. attend to prefix m (groups*grp_rows <= rows <= 64)
- *   impl       0 = the decode step's choice for `rows` rows, 1 = tcgen05 prefix + warp suffix units
- *              with the fused merge, 2 = tcgen05 prefix + 64-token CTA units + merge kernel,
- *              3 = CUDA-core prefix chunks + CTA units + merge kernel (groups = 1)
+ *   impl       0 = the decode step's choice, 1 = tcgen05 prefix + 32-token warp suffix units with
+ *              the fused merge, 2 = tcgen05 prefix + 64-token CTA units + merge kernel, 3 = CUDA-core
+ *              prefix chunks + CTA units + merge kernel (groups = 1), 4 = tcgen05 prefix + 64-token
+ *              suffix units on mma.sync with the fused merge (the default when page_tokens % 8 == 0)
  *   d_out      [rows][Hq][128] bf16 output (rows that are idle are not written);
  *   d_out_f32  (nullable) the same before the bf16 rounding
  *   reps, h_ms reps > 0: then `reps` more timed runs, each after a 256 MiB write that evicts L2;

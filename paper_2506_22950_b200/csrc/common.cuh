@@ -29,6 +29,19 @@ IS_DEVICE void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
 IS_DEVICE void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Busy-poll with test_wait.parity (never suspends the warp).
+IS_DEVICE void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra LAB_WAIT;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
 // Spin on try_wait.parity with a suspend-time hint: the standard PTX idiom (the same
 // loop as CUTLASS ClusterBarrier::wait, cutlass/arch/barrier.h).
 IS_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {

@@ -270,6 +270,23 @@ static is_status make_tmap(CUtensorMap* m, const void* ptr, int64_t rows, int64_
   return IS_OK;
 }
 
+// The page pool ([pages][2 = K|V][Hkv][pt][128] bf16, all layers) as a 5-D tensor whose box is one
+// page of one kv head: (64 dims, 2 halves, pt rows, K|V, page x head), 128-byte swizzle
+// (attn_suffix_mma_kernel).  Coordinate 4 = (layer * num_pages + page) * 2 * Hkv + head.
+static is_status make_tmap_pool(CUtensorMap* m, const void* ptr, int64_t layer_pages, int Hkv, int pt) {
+  PFN_encodeTiled_t enc = get_encode();
+  if (!enc) return fail(IS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[5] = {64, 2, (cuuint64_t)pt, 2, (cuuint64_t)(layer_pages * 2 * Hkv)};
+  cuuint64_t strides[4] = {128, 256, (cuuint64_t)Hkv * pt * 256, (cuuint64_t)pt * 256};
+  cuuint32_t box[5] = {64, 2, (cuuint32_t)pt, 2, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(IS_ERR_CUDA, "cuTensorMapEncodeTiled (page pool) failed (%d)", (int)r);
+  return IS_OK;
+}
+
 // ------------------------------------------------------------------ GEMM launch
 static int g_num_sms = 0;
 static int g_launches = 0;  // kernel launches issued since the last reset (enqueue_step counts its own)
@@ -458,10 +475,13 @@ struct is_ctx {
   float* resid;
   __nv_bfloat16 *xn, *attn, *act, *q;
   float *part_o, *part_ml;
-  int* merge_cnt;  // [max_rows][Hkv] fused-merge counters (decode, tcgen05 prefix)
+  int* merge_cnt;  // [max_rows][Hkv] fused-merge counters (decode, tcgen05 prefix), then 2 unit counters
+  bool static_units;  // IS_STATIC_UNITS: the suffix pass strides its units statically (round 1)
   float *ssqA, *ssqB;  // [Th][max_rows] per-128-column sums of squares: QKV input, gate/up input
   int bnorm;           // decode: RMSNorm folded into the QKV / gate-up B operand
-  int sep_merge;       // decode suffix: 64-token CTA units + separate merge kernel (else warp units, fused merge)
+  int sep_merge;       // decode suffix: 64-token CTA units + separate merge kernel
+  int suffix_mma;      // decode suffix: 64-token units on mma.sync, fused merge (default)
+  CUtensorMap tm_pool; // the page pool of all layers as rows of 128 bf16, box = one page (128-byte swizzle)
   int stg_lm;          // lm_head ring depth override (IS_STG_LM = 10 / 11; default 8)
   int fuse_norm;       // decode: RMSNorm of the new residual fused into the o_proj / down epilogues
   int topp;            // 0 < top_p < 1: nucleus sampling pass after the lm_head (R36)
@@ -613,6 +633,8 @@ struct AttnLaunch {
   int grp_kv_rows;               // tensor-map rows per group
   int groups;                    // co-resident groups M
   int grp_rows;                  // rows per group g
+  const CUtensorMap* tm_pool;    // decode mma suffix pass: the page pool, rows of 128 bf16, box = page_tokens
+  int suffix_mma;                // decode: suffix units on mma.sync (attn_suffix_mma_kernel)
 };
 
 template <int REP, int N>
@@ -658,6 +680,18 @@ static is_status launch_attn_rep(const AttnArgs& aa, const AttnLaunch& al, cudaS
       case 64: CKS((launch_prefix_tc_n<REP, 64>(aa, al, st))); break;
       default: return fail(IS_ERR_CONFIG, "tcgen05 prefix attention needs g * Hq/Hkv <= 64");
     }
+  }
+  if (al.suffix_mma) {  // decode, 64-token units on mma.sync with the fused merge
+    switch (aa.pt) {
+      case 8: CKS(launch_k_smem(attn_suffix_mma_kernel<REP, 8>, dim3(g_num_sms), dim3(kSThreads), SuffixMmaSmem::v,
+                                st, *al.tm_pool, aa)); break;
+      case 16: CKS(launch_k_smem(attn_suffix_mma_kernel<REP, 16>, dim3(g_num_sms), dim3(kSThreads),
+                                 SuffixMmaSmem::v, st, *al.tm_pool, aa)); break;
+      case 32: CKS(launch_k_smem(attn_suffix_mma_kernel<REP, 32>, dim3(g_num_sms), dim3(kSThreads),
+                                 SuffixMmaSmem::v, st, *al.tm_pool, aa)); break;
+      default: return fail(IS_ERR_CONFIG, "the mma suffix pass needs page_tokens 8, 16 or 32");
+    }
+    return IS_OK;
   }
   if (aa.merge_cnt) {  // decode, warp units with the fused merge
     CKS(launch_k_smem(attn_suffix_warp_kernel<REP>, dim3(3 * g_num_sms), dim3(kAttnThreads), SuffixWarpSmem<REP>::v,
@@ -775,6 +809,8 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
     aa.nc_suf = prefill ? 0 : c->nc_suf;
     aa.tc_prefix = prefill ? 0 : c->tc_prefix;
     aa.merge_cnt = (!prefill && c->tc_prefix && !c->sep_merge) ? c->merge_cnt : nullptr;
+    aa.pool_row0 = l * c->num_pages * 2 * Hkv;
+    aa.unit_ctr = (!prefill && !c->static_units) ? c->merge_cnt + (size_t)c->max_rows * Hkv : nullptr;
     aa.sc = prefill ? kSC : c->sc;
     aa.NC = c->NC;
     aa.prefill = prefill ? 1 : 0;
@@ -786,6 +822,8 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       al.grp_kv_rows = s.layers * 2 * Hkv * c->pcap;
       al.groups = c->M;
       al.grp_rows = c->g;
+      al.tm_pool = &c->tm_pool;
+      al.suffix_mma = !prefill && c->suffix_mma;
       CKS(launch_attention(aa, al, st));
     }
     prof_mark(st, 3);
@@ -1052,21 +1090,22 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
     c->tc_prefix = (N == 16 || N == 32 || N == 64) && !getenv("IS_NO_TC_PREFIX");
     c->nc_pre_dec = c->tc_prefix ? (int)ceil_div64(c->pcap, 128) : c->nc_pre;
   }
-  // decode suffix chunk: 32-token warp units behind the tcgen05 prefix, else 64-token CTA units
-  // (>= 32 rows, i.e. co-resident groups: the 64-token CTA units with the separate merge kernel
-  //  measured 3% faster, profiles/r01g/groups_*; IS_SEPARATE_MERGE=0/1 overrides)
+  // decode suffix pass behind the tcgen05 prefix: 64-token units on mma.sync with the fused
+  // merge (default; needs page_tokens % 8 == 0 for the swizzled page boxes); IS_SUFFIX_IMPL=
+  // warp / cta selects round 1's 32-token warp units (fused merge) or 64-token CTA units with
+  // the separate merge kernel.  Without the tcgen05 prefix: 64-token CTA units + merge kernel.
   {
-    const char* e = getenv("IS_SEPARATE_MERGE");
-    c->sep_merge = e ? atoi(e) != 0 : c->rc >= 32;
-    // the separate merge kernel holds <= 32 partials (prefix tiles + 64-token chunks); longer
-    // prompts / generations fall back to the warp units with the fused (<= 64-partial) merge
-    if (c->sep_merge && c->tc_prefix && c->nc_pre_dec + ceil_div64(c->max_new, kSC) > 32) c->sep_merge = 0;
+    const char* e = getenv("IS_SUFFIX_IMPL");
+    c->suffix_mma = c->tc_prefix && c->pt % 8 == 0 && c->pt <= kSUnit && !(e && strcmp(e, "mma"));
+    c->sep_merge = !c->suffix_mma && (!c->tc_prefix || c->pt > kSCW || (e && !strcmp(e, "cta")));
+    if (c->sep_merge && c->tc_prefix && c->pt <= kSCW && c->nc_pre_dec + ceil_div64(c->max_new, kSC) > 32)
+      c->sep_merge = 0;
   }
-  c->sc = (c->tc_prefix && !c->sep_merge) ? kSCW : kSC;
+  c->sc = c->suffix_mma ? kSUnit : ((c->tc_prefix && !c->sep_merge) ? kSCW : kSC);
   c->nc_suf = (int)ceil_div64(c->max_new, c->sc);
   c->NC = c->nc_pre + c->nc_suf;
   // partials one LSE merge combines: decode = prefix tiles + suffix chunks, prefill = prefix chunks
-  const int ndec = c->nc_pre_dec + c->nc_suf, nmax = c->sc == kSCW ? 64 : 32;
+  const int ndec = c->nc_pre_dec + c->nc_suf, nmax = c->sep_merge || !c->tc_prefix ? 32 : 64;
   if (ndec > nmax || c->nc_pre > 32 || s.n_q_heads / s.n_kv_heads > kMaxRep) {
     delete c;
     return fail(IS_ERR_CAPACITY, "prompt_len + max_new_tokens too long for the attention merge (%d partials > %d)",
@@ -1138,6 +1177,8 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->prefix = (__nv_bfloat16*)A((size_t)c->M * s.layers * 2 * Hkv * c->pcap * 128 * 2);
   if (err == IS_OK) CKS(make_tmap(&c->tm_prefix_kv, c->prefix, (int64_t)c->M * s.layers * 2 * Hkv * c->pcap, 128, 128));
   c->pool = (__nv_bfloat16*)A((size_t)s.layers * c->num_pages * (size_t)c->page_bytes / s.layers);
+  if (err == IS_OK && c->suffix_mma)
+    CKS(make_tmap_pool(&c->tm_pool, c->pool, (int64_t)s.layers * c->num_pages, Hkv, c->pt));
   // ---- activations
   const int R = c->max_rows;
   c->resid = (float*)A((size_t)R * H * 4);
@@ -1147,7 +1188,8 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->q = (__nv_bfloat16*)A((size_t)R * Hq * 128 * 2);
   c->part_o = (float*)A((size_t)R * Hq * c->NC * 128 * 4);
   c->part_ml = (float*)A((size_t)R * Hq * c->NC * 2 * 4);
-  c->merge_cnt = (int*)A((size_t)R * Hkv * 4);
+  c->merge_cnt = (int*)A(((size_t)R * Hkv + 2) * 4);  // + the suffix pass's 2 unit counters
+  c->static_units = getenv("IS_STATIC_UNITS") != nullptr;  // timing comparison only
   c->ssqA = (float*)A((size_t)ceil_div64(H, 128) * R * 4);
   c->ssqB = (float*)A((size_t)ceil_div64(H, 128) * R * 4);
   c->splitk_ws = (float*)A((size_t)2 * 160 * kBM * 64 * 4);
@@ -1769,7 +1811,7 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
   if (!d_q || !d_prefix || !d_pool || !d_pagetab || !d_row_len || !d_out) return fail(IS_ERR_CONFIG, "null argument");
   if (rows < 1 || rows > 64 || groups < 1 || grp_rows < 1 || groups * grp_rows > rows || plen < 1 || Hkv < 1 ||
       Hq % Hkv || Hq / Hkv > kMaxRep || page_tokens < 4 || 64 % page_tokens || maxp < 1 || num_pages < 1 ||
-      impl < 0 || impl > 3 || reps < 0 || (reps > 0 && !h_ms))
+      impl < 0 || impl > 4 || reps < 0 || (reps > 0 && !h_ms))
     return fail(IS_ERR_CONFIG, "bad is_dbg_attn arguments");
   if (!g_num_sms) {
     int dev = 0;
@@ -1779,14 +1821,17 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
   const int rep = Hq / Hkv;
   const bool tc_ok = prefix_cols(grp_rows, rep) <= 64;
   const bool tc = impl == 0 ? tc_ok : impl != 3;
-  const bool sep = impl == 0 ? rows >= 32 : impl != 1;
+  const bool mma = impl == 0 ? tc_ok && page_tokens % 8 == 0 && page_tokens <= kSUnit : impl == 4;
+  const bool sep = impl == 2 || impl == 3 || (impl == 0 && !mma && (!tc || page_tokens > kSCW));
   if (tc && !tc_ok) return fail(IS_ERR_CONFIG, "tcgen05 prefix needs grp_rows * Hq/Hkv <= 64");
+  if (mma && (page_tokens % 8 || page_tokens > kSUnit))
+    return fail(IS_ERR_CONFIG, "the mma suffix pass needs page_tokens in {8, 16, 32}");
   if (!tc && groups != 1) return fail(IS_ERR_CONFIG, "the CUDA-core prefix serves one group");
-  const int sc = (tc && !sep) ? kSCW : kSC;
+  const int sc = mma ? kSUnit : ((tc && !sep) ? kSCW : kSC);
   const int nc_pre = tc ? (int)ceil_div64(plen, 128) : (int)ceil_div64(plen, kPC);
   const int nc_suf = (int)ceil_div64((int64_t)maxp * page_tokens, sc);
-  if (nc_pre + nc_suf > (sc == kSCW ? 64 : 32))
-    return fail(IS_ERR_CAPACITY, "%d partials exceed the merge (%d)", nc_pre + nc_suf, sc == kSCW ? 64 : 32);
+  const int nmax = sep ? 32 : 64;
+  if (nc_pre + nc_suf > nmax) return fail(IS_ERR_CAPACITY, "%d partials exceed the merge (%d)", nc_pre + nc_suf, nmax);
   cudaStream_t st = (cudaStream_t)stream;
   std::vector<int32_t> len(rows), act(rows), lid(rows);
   CK(cudaMemcpy(len.data(), d_row_len, rows * 4, cudaMemcpyDeviceToHost));
@@ -1803,10 +1848,11 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
   long long* nit = (long long*)dalloc(2 * sizeof(long long), &err);
   float* part_o = (float*)dalloc((size_t)rows * Hq * NC * 128 * 4, &err);
   float* part_ml = (float*)dalloc((size_t)rows * Hq * NC * 2 * 4, &err);
-  int* mcnt = (int*)dalloc((size_t)rows * Hkv * 4, &err);
+  int* mcnt = (int*)dalloc(((size_t)rows * Hkv + 2) * 4, &err);
   uint8_t* flush = reps > 0 ? (uint8_t*)dalloc((size_t)256 << 20, &err) : nullptr;  // > 2x the 126 MB L2
-  CUtensorMap tm;
+  CUtensorMap tm, tmp;
   if (err == IS_OK) err = make_tmap(&tm, d_prefix, (int64_t)groups * 2 * Hkv * plen, 128, 128);
+  if (err == IS_OK && mma) err = make_tmap_pool(&tmp, d_pool, num_pages, Hkv, page_tokens);
   if (err == IS_OK) {
     cudaMemcpy(d_act, act.data(), rows * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(d_lid, lid.data(), rows * 4, cudaMemcpyHostToDevice);
@@ -1850,6 +1896,7 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
     aa.prefill = 0;
     aa.tc_prefix = tc ? 1 : 0;
     aa.merge_cnt = (tc && !sep) ? mcnt : nullptr;
+    aa.unit_ctr = getenv("IS_STATIC_UNITS") ? nullptr : mcnt + (size_t)rows * Hkv;
     aa.sc = sc;
     aa.scale = 1.0f / sqrtf((float)kHD);
     AttnLaunch al{};
@@ -1858,6 +1905,10 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
     al.grp_kv_rows = 2 * Hkv * plen;
     al.groups = groups;
     al.grp_rows = grp_rows;
+    al.tm_pool = &tmp;
+    al.suffix_mma = mma ? 1 : 0;
+    aa.pool_row0 = 0;
+    aa.dbg_mode = getenv("IS_DBG_SUFFIX_MODE") ? atoi(getenv("IS_DBG_SUFFIX_MODE")) : 0;
     err = launch_attention(aa, al, st);
     if (err == IS_OK && reps > 0) {
       cudaEvent_t e0, e1;
@@ -1878,6 +1929,40 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
       cudaError_t e = cudaStreamSynchronize(st);
       if (e == cudaSuccess) e = cudaGetLastError();
       if (e != cudaSuccess) err = fail(IS_ERR_CUDA, "is_dbg_attn: %s", cudaGetErrorString(e));
+    }
+    if (err == IS_OK && getenv("IS_DBG_STAMPS")) {
+      // one more run with globaltimer stamps of the suffix CTAs (timing experiments only)
+      unsigned long long* ts = nullptr;
+      cudaMalloc(&ts, (size_t)4 * 296 * 16 * 8);
+      cudaMemset(ts, 0, (size_t)4 * 296 * 16 * 8);
+      AttnArgs a3 = aa;
+      a3.dbg_ts = ts;
+      cudaMemsetAsync(flush, 1, (size_t)256 << 20, st);
+      err = launch_attention(a3, al, st);
+      cudaStreamSynchronize(st);
+      std::vector<unsigned long long> h((size_t)4 * 296 * 16);
+      cudaMemcpy(h.data(), ts, h.size() * 8, cudaMemcpyDeviceToHost);
+      cudaFree(ts);
+      unsigned long long t0 = ~0ull;
+      for (int b = 0; b < g_num_sms; ++b)
+        if (h[b * 16]) t0 = std::min(t0, h[b * 16]);
+      for (int i = 0; i < 9; ++i) {
+        std::vector<double> v;
+        for (int b = 0; b < g_num_sms; ++b)
+          if (h[b * 16 + i]) v.push_back((double)(h[b * 16 + i] - t0) / 1e3);
+        if (v.empty()) continue;
+        std::sort(v.begin(), v.end());
+        fprintf(stderr, "stamp %d: n=%zu min %.2f med %.2f max %.2f us\n", i, v.size(), v[0], v[v.size() / 2], v.back());
+      }
+      std::vector<double> u, m;
+      for (int b = 0; b < g_num_sms; ++b) {
+        u.push_back((double)h[b * 16 + 9]);
+        m.push_back((double)h[b * 16 + 10]);
+      }
+      std::sort(u.begin(), u.end());
+      std::sort(m.begin(), m.end());
+      fprintf(stderr, "slots per CTA min %.0f med %.0f max %.0f; merges per CTA min %.0f med %.0f max %.0f\n", u[0],
+              u[u.size() / 2], u.back(), m[0], m[m.size() / 2], m.back());
     }
   }
   for (void* p : {(void*)d_act, (void*)d_lid, (void*)items, (void*)nit, (void*)part_o, (void*)part_ml, (void*)mcnt,

@@ -97,7 +97,7 @@ __global__ void rmsnorm_kernel(const float* __restrict__ resid, const float* __r
 constexpr int kPC = 32;           // tokens per shared-prefix chunk (one CTA, all live rows)
 constexpr int kSC = 64;           // tokens per suffix chunk (one warp)
 constexpr int kMaxRep = 8;        // Hq / Hkv <= 8
-constexpr int kItemStride = 17;   // work item: code + up to 16 page ids
+constexpr int kItemStride = 20;   // work item (80 B, 16-B aligned): [0] code, [1] row length, [2..17] page ids
 constexpr int kAttnWarps = 4;
 constexpr int kAttnThreads = kAttnWarps * 32;
 
@@ -120,6 +120,10 @@ struct AttnArgs {
   int prefill;                // 1: rows are prompt positions, causal over the prefix, no suffix
   int tc_prefix;              // decode: shared prefix done by attn_prefix_tc_kernel (tcgen05)
   int* merge_cnt;             // decode: [rows][Hkv] suffix units done; the last one merges (reset by it)
+  int pool_row0;              // decode (mma suffix): page-pool tensor-map coordinate of this layer (page x head)
+  int dbg_mode;               // timing experiments (is_dbg_attn, IS_DBG_SUFFIX_MODE): 1 no KV loads, 2 no math
+  int* unit_ctr;              // decode: [2] dynamic work fetching (next unit, warps / CTAs done; the last
+                              //   finisher resets both for the next launch); null = static striding
   int sc;                     // decode suffix chunk (tokens per work item): kSC, or kSCW for the warp kernel
   int grp_rows;               // decode, tcgen05 prefix: rows per co-resident group (g); group m = rows m*g ..
   int grp_kv_rows;            //   prefix-KV tensor-map rows per group (L * 2 * Hkv * pcap)
@@ -128,6 +132,14 @@ struct AttnArgs {
 
 __device__ __forceinline__ void astamp(const AttnArgs& a, int i) {
   if (a.dbg_ts && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.dbg_ts[blockIdx.x * 16 + i] = t;
+  }
+}
+
+__device__ __forceinline__ void astamp_lane(const AttnArgs& a, int i) {  // caller picks the thread
+  if (a.dbg_ts) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.dbg_ts[blockIdx.x * 16 + i] = t;
@@ -335,17 +347,25 @@ __global__ void __launch_bounds__(kAttnThreads) attn_suffix_warp_kernel(AttnArgs
   const size_t hs = (size_t)a.pt * kHD;
   uint32_t phase = 0;
   const int stride = gridDim.x * kAttnWarps;
+  // Units are taken dynamically (one atomic per unit): a warp whose CTA became resident
+  // late (behind the prefix kernel's CTAs) or whose units were short simply takes more.
+  auto next_unit = [&](int cur) {
+    if (!a.unit_ctr) return cur + stride;
+    int v = 0;
+    if (lane == 0) v = atomicAdd(a.unit_ctr, 1);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
   // Software-pipelined over this warp's units: the next unit's item is read during the
   // current one, and its pages are DMA'd as soon as the current chunk has been scored
   // (the buffer is free), i.e. before the current partial's store / fence / count.
   // Item: [0] code (c << 16 | r << 8 | h), [1..8] page ids, [16] the row's length.
-  int u = blockIdx.x * kAttnWarps + warp;
+  int u = a.unit_ctr ? next_unit(0) : blockIdx.x * kAttnWarps + warp;
   int code = 0, len = 0, page_l = 0;
   auto fetch = [&](int uu) {
     const int32_t* item = a.items + (size_t)uu * kItemStride;
     code = item[0];
-    len = item[16];
-    page_l = lane < 8 ? item[1 + lane] : 0;
+    len = item[1];
+    page_l = lane < 8 ? item[2 + lane] : 0;
   };
   auto issue = [&]() {
     const int c = (code >> 16) & 0xFF, h = code & 0xFF;
@@ -371,7 +391,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_suffix_warp_kernel(AttnArgs
     const int cur_len = len;
     const int ntok = min(kSCW, cur_len - c * kSCW);
     attn_load_q<REP>(a, r, h, qs, lane);
-    const int nu = u + stride;
+    const int nu = next_unit(u);
     if (nu < n) fetch(nu);  // independent loads, in flight during the wait + math
     __syncwarp();
     mbar_wait(bar, phase);
@@ -394,11 +414,366 @@ __global__ void __launch_bounds__(kAttnThreads) attn_suffix_warp_kernel(AttnArgs
     __syncwarp();
     u = nu;
   }
+  if (a.unit_ctr && lane == 0 && atomicAdd(a.unit_ctr + 1, 1) == stride - 1) {
+    a.unit_ctr[0] = 0;  // every warp has taken its last unit: ready for the next launch
+    a.unit_ctr[1] = 0;
+  }
   pdl_wait();  // the tcgen05 prefix partials are complete from here on
   const int nm = merge_n[warp];
   for (int j = 0; j < nm * REP; ++j) {
     const int rh = merge_list[warp][j / REP];
     attn_merge_one<REP>(a, rh >> 8, rh & 0xFF, j % REP, lane);
+  }
+}
+
+// ------------------------------------------------------------------ suffix pass on mma.sync
+// Decode suffix pass behind the tcgen05 prefix kernel ("a separate
+// KV buffer for its response tokens"): unit = (row r, kv head h, 32-token chunk c of the slot's
+// pages).  One CTA per SM of kSWarps independent warps; each warp runs its own kSWStages-deep
+// ring: it TMA-loads a unit's pages (one 5-D box per page = K and V, both 64-dim halves, 128-byte
+// swizzle) and the row's REP query heads into a stage, and while later units load it scores the
+// oldest one on the tensor cores with warp-level mma.sync m16n8k16 (the REP query heads padded to
+// the MMA's 16 rows: S = Q.K^T with the keys in N), takes the row softmax in registers (quad
+// shuffles) and accumulates O = P.V with P as a bf16 hi/lo pair (two MMAs, ~2^-16 relative, like
+// the prefix kernel).  The normalised partial (o, m, l) goes to partial slot nc_pre + c; the
+// partials are released in batches (one fence per batch) and counted per (row, kv head), whose
+// LSE merge runs after the prefix kernel is known complete, spread over the grid.
+// Units: the first kSStaticPct% of the work list is split statically over the warps (contiguous
+// ranges), the rest is claimed kSClaim units at a time (one atomic), so warps of CTAs that became
+// resident late (behind the prefix kernel's CTAs) just claim less.
+constexpr int kSUnit = 32;          // keys per unit
+constexpr int kSWarps = 6;          // warps per CTA (each its own ring)
+constexpr int kSWStages = 2;        // stages per warp
+constexpr int kSThreads = 32 * kSWarps;
+constexpr int kSQueue = 6;          // work items loaded ahead of their issue
+constexpr int kSStaticPct = 50;     // share of the work list split statically over the warps
+struct SuffixMmaSmem {
+  static constexpr int kKV = kSUnit * 2 * kHD * 2;    // K and V of one unit: 16 KB
+  static constexpr int kQ = kMaxRep * kHD * 2;        // the row's query heads
+  static constexpr int kStage = kKV + kQ;             // 18 KB, a multiple of 1024 (swizzle atoms)
+  static constexpr int v = kSWarps * kSWStages * kStage + 16 + kSWarps * kSWStages * 8 + 1024;
+};
+
+IS_DEVICE void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+IS_DEVICE void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+// D (16x8 fp32) += A (16x16 bf16, row) . B (16x8 bf16, col)
+IS_DEVICE void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+IS_DEVICE uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+// 5-D tiled load (box = one page: K and V, both halves): coordinates innermost first.
+IS_DEVICE void tma_load_5d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2, int c3, int c4,
+                           uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+      "l"(cache_hint)
+      : "memory");
+}
+
+template <int REP, int PT>
+__global__ void __launch_bounds__(kSThreads, 1) attn_suffix_mma_kernel(const __grid_constant__ CUtensorMap tmPool,
+                                                                        AttnArgs a) {
+  pdl_launch_dependents();
+  using SM = SuffixMmaSmem;
+  extern __shared__ uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  uint4* zero16 = reinterpret_cast<uint4*>(sm + kSWarps * kSWStages * SM::kStage);  // Q padding rows
+  uint64_t* bars = reinterpret_cast<uint64_t*>(zero16 + 1);
+  __shared__ int done_list[kSWarps * 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    astamp_lane(a, 0);
+    for (int i = 0; i < kSWarps * kSWStages; ++i) mbar_init(&bars[i], 1);
+    *zero16 = make_uint4(0, 0, 0, 0);
+    tma_prefetch_desc(&tmPool);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int n = (int)a.n_items[0];
+  constexpr int pt = PT;  // page tokens (8, 16 or 32): the stage addressing is compile-time
+  uint8_t* wsm = sm + warp * kSWStages * SM::kStage;
+  uint64_t* full = bars + warp * kSWStages;
+  // ---- unit source.  Units u < Ls are strided statically over the warps (warp gw: gw, gw + GW,
+  // ...; their items are prefetched kSQueue deep), units >= Ls are claimed one at a time from a
+  // counter, one unit ahead (claim + item load overlap the current unit's math; a warp never
+  // hoards more than one unit, so the tail stays short).  Small work lists are all static.
+  const bool loads = !(a.dbg_mode & 1), qload = !(a.dbg_mode & 4);
+  const int GW = gridDim.x * kSWarps, gw = blockIdx.x * kSWarps + warp;
+  const int Ls = n <= 2 * GW ? n : (int)((long long)n * kSStaticPct / 100);
+  int snext = gw;  // next static unit to load into the queue
+  // static queue: lane q < kSQueue holds the item (code, length, pages 0..3) of the q-th next static
+  // unit; code -1 = none
+  uint4 x0 = make_uint4(0xFFFFFFFFu, 0, 0, 0);
+  uint2 x1 = make_uint2(0, 0);
+  auto load_to = [&](int u, int q, uint4& y0, uint2& y1) {
+    if (lane == q) {
+      y0 = make_uint4(0xFFFFFFFFu, 0, 0, 0);
+      y1 = make_uint2(0, 0);
+      if (u < n) {
+        const uint4* it = reinterpret_cast<const uint4*>(a.items + (size_t)u * kItemStride);
+        y0 = it[0];
+        const uint4 y = it[1];
+        y1 = make_uint2(y.x, y.y);
+      }
+    }
+  };
+#pragma unroll 1
+  for (int q = 0; q < kSQueue; ++q, snext += GW) load_to(snext < Ls ? snext : n, q, x0, x1);
+  // dynamic: lane 0 holds the item of the next claimed unit (d0.x = -1: none / not claimed yet)
+  uint4 d0 = make_uint4(0xFFFFFFFFu, 0, 0, 0);
+  uint2 d1 = make_uint2(0, 0);
+  bool dyn_started = false, dyn_done = Ls >= n;
+  auto claim_next = [&]() {  // claim one unit and load its item into lane 0's dynamic slot
+    int u = n;
+    if (lane == 0) u = Ls + atomicAdd(a.unit_ctr, 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= n) dyn_done = true;
+    load_to(u, 0, d0, d1);
+  };
+  // issue the next unit into stage st: returns its code (-1 if there is none) and its row length
+  auto issue = [&](int st, int& len_out) {
+    int cd = __shfl_sync(0xffffffffu, (int)x0.x, 0);
+    uint4 h0;
+    uint2 h1;
+    if (cd >= 0) {  // static queue head; shift and refill the tail
+      h0 = make_uint4(x0.x, x0.y, x0.z, x0.w);
+      h1 = x1;
+      x0.x = __shfl_down_sync(0xffffffffu, x0.x, 1);
+      x0.y = __shfl_down_sync(0xffffffffu, x0.y, 1);
+      x0.z = __shfl_down_sync(0xffffffffu, x0.z, 1);
+      x0.w = __shfl_down_sync(0xffffffffu, x0.w, 1);
+      x1.x = __shfl_down_sync(0xffffffffu, x1.x, 1);
+      x1.y = __shfl_down_sync(0xffffffffu, x1.y, 1);
+      load_to(snext < Ls ? snext : n, kSQueue - 1, x0, x1);
+      snext += GW;
+      if (!dyn_started && !dyn_done && __shfl_sync(0xffffffffu, (int)x0.x, 0) < 0) {
+        dyn_started = true;  // the static queue has run dry behind this unit: claim the first dynamic one
+        claim_next();
+      }
+    } else {
+      if (!dyn_started && !dyn_done) {
+        dyn_started = true;
+        claim_next();
+      }
+      cd = __shfl_sync(0xffffffffu, (int)d0.x, 0);
+      h0 = d0;
+      h1 = d1;
+      if (cd >= 0 && !dyn_done) claim_next();  // one unit ahead
+      else if (cd >= 0) d0.x = 0xFFFFFFFFu;
+    }
+    const int ln = __shfl_sync(0xffffffffu, (int)h0.y, 0);
+    len_out = ln;
+    if (cd < 0) return -1;
+    const int p0 = __shfl_sync(0xffffffffu, (int)h0.z, 0), p1 = __shfl_sync(0xffffffffu, (int)h0.w, 0);
+    const int p2 = __shfl_sync(0xffffffffu, (int)h1.x, 0), p3 = __shfl_sync(0xffffffffu, (int)h1.y, 0);
+    const int c = (cd >> 16) & 0xFF, r = (cd >> 8) & 0xFF, h = cd & 0xFF;
+    const int ntok = min(kSUnit, ln - c * kSUnit);
+    const int npl = (((ntok + 15) & ~15) + pt - 1) / pt;  // pages covering the 16-key MMA steps (<= 4)
+    uint8_t* stg = wsm + st * SM::kStage;
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&full[st], (loads ? (uint32_t)npl * pt * 512 : 0u) + (qload ? REP * kHD * 2 : 0));
+      if (qload) bulk_g2s(stg + SM::kKV, a.q + ((size_t)r * a.Hq + h * REP) * kHD, REP * kHD * 2, &full[st]);
+      if (loads) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {  // box (64 dims, 2 halves, pt rows, K|V, page x head)
+          const int pg = j == 0 ? p0 : (j == 1 ? p1 : (j == 2 ? p2 : p3));
+          if (j < npl)
+            tma_load_5d(stg + j * pt * 512, &tmPool, &full[st], 0, 0, 0, 0, a.pool_row0 + pg * 2 * a.Hkv + h,
+                        kEvictFirst);
+        }
+      }
+    }
+    return cd;
+  };
+  int hcode[kSWStages], hlen[kSWStages];
+  int nq = 0;  // units issued
+#pragma unroll
+  for (int st = 0; st < kSWStages; ++st) {
+    hcode[st] = issue(st, hlen[st]);
+    nq += hcode[st] >= 0;
+  }
+  // ---- consume in order; refill the freed stage
+  const int g = lane >> 2, t4 = lane & 3, mi = lane >> 3, mr = lane & 7;
+  const float sl2 = a.scale * 1.4426950408889634f;  // exp(x * scale) = exp2(x * sl2)
+  const uint32_t z16 = smem_u32(zero16);
+  int* dl = done_list + warp * 32;  // this warp's finished units, published in batches (one fence each)
+  int ndl = 0;
+  auto publish = [&]() {
+    __syncwarp();
+    __threadfence();
+    if (lane < ndl) atomicAdd(a.merge_cnt + dl[lane], 1);
+    __syncwarp();
+    ndl = 0;
+  };
+  // key row k of a stage (page k / pt, row k % pt) of K (kv = 0) or V (kv = 1): byte offset of its
+  // 256-B row; the 128-B half h of that row sits at + 128 h, its 16-B chunk c at ^ swizzle
+  auto krow = [&](int k0, int kv) { return (2 * k0 - (k0 & (pt - 1)) + kv * pt) * 256; };
+#pragma unroll 1
+  for (int i = 0;; ++i) {
+    const int st = i % kSWStages;
+    const int cd = hcode[st];
+    if (cd < 0) break;
+    mbar_wait(&full[st], (i / kSWStages) & 1);
+    if (i == 0 && lane == 0) astamp_lane(a, 3);
+    const int c = (cd >> 16) & 0xFF, r = (cd >> 8) & 0xFF, h = cd & 0xFF;
+    const int ntok = (a.dbg_mode & 2) ? 0 : min(kSUnit, hlen[st] - c * kSUnit);
+    const uint32_t sKV = smem_u32(wsm + st * SM::kStage), sQ = sKV + SM::kKV;
+    constexpr int NJ = kSUnit / 8, NKK = kSUnit / 16;  // 8-key n-tiles of S, 16-key k-steps of P.V
+    // S = Q . K^T: NJ n-tiles of 8 keys, 8 k-steps of 16 dims (taken in pairs)
+    float sacc[NJ][4];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
+    const int qrow = mr + 8 * (mi & 1);
+    const uint32_t qbase = qrow < REP ? sQ + qrow * 256 + 16 * (mi >> 1) : 0u;
+    const int nj = (ntok + 7) >> 3;
+#pragma unroll
+    for (int kp = 0; kp < 4; ++kp) {
+      uint32_t qa[2][4];
+      ldsm_x4(qrow < REP ? qbase + (2 * kp) * 32 : z16, qa[0]);
+      ldsm_x4(qrow < REP ? qbase + (2 * kp + 1) * 32 : z16, qa[1]);
+      // chunk (kp & 1) * 4 + mi of half kp >> 1; the 128-B row index of key k, half h is 2k + h
+      const int hh = kp >> 1;
+      const uint32_t sw = ((((kp & 1) * 4 + mi) ^ ((2 * mr + hh) & 7)) << 4) + hh * 128 + mr * 256;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        if (j < nj) {
+          uint32_t kb[4];
+          ldsm_x4(sKV + krow(8 * j, 0) + sw, kb);
+          mma16816(sacc[j], qa[0], kb[0], kb[1]);
+          mma16816(sacc[j], qa[1], kb[2], kb[3]);
+        }
+      }
+    }
+    // row softmax: thread holds rows g (sacc[.][0..1]) and g + 8 (sacc[.][2..3], always a padding
+    // row: REP <= 8), keys 8j + 2 t4 + {0,1}; the quad (t4) shares a row
+    float mA = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        sacc[j][e] = 8 * j + 2 * t4 + e < ntok ? sacc[j][e] : -INFINITY;
+        mA = fmaxf(mA, sacc[j][e]);
+      }
+    }
+    mA = fmaxf(mA, __shfl_xor_sync(0xffffffffu, mA, 1));
+    mA = fmaxf(mA, __shfl_xor_sync(0xffffffffu, mA, 2));
+    const float mb = mA * sl2;
+    float lA = 0.f;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        sacc[j][e] = exp2f(fmaf(sacc[j][e], sl2, -mb));  // masked keys: exp2(-inf) = 0
+        lA += sacc[j][e];
+      }
+    }
+    lA += __shfl_xor_sync(0xffffffffu, lA, 1);
+    lA += __shfl_xor_sync(0xffffffffu, lA, 2);
+    // O = P . V, P = P_hi + P_lo (bf16 pair): NKK k-steps of 16 keys, 16 n-tiles of 8 dims; the
+    // padding rows g + 8 enter as zeros
+    float oacc[16][4];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < NKK; ++kk) {
+      if (16 * kk < ntok) {
+        // A fragment: a0 (row g, keys 0-7 of the step) = n-tile 2kk, a2 (row g, keys 8-15) = 2kk+1;
+        // a1 / a3 (row g + 8) = 0
+        uint32_t ph[4], pl[4];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const float* sv = sacc[2 * kk + q];
+          const __nv_bfloat162 hi = __floats2bfloat162_rn(sv[0], sv[1]);
+          const float2 hf = __bfloat1622float2(hi);
+          ph[2 * q] = *reinterpret_cast<const uint32_t*>(&hi);
+          pl[2 * q] = pack_bf16(sv[0] - hf.x, sv[1] - hf.y);
+          ph[2 * q + 1] = 0u;
+          pl[2 * q + 1] = 0u;
+        }
+        // ldmatrix.trans rows: key 16kk + 8 (mi & 1) + mr; n-tiles nt, nt + 1 (mi >> 1)
+        const uint32_t vb0 = sKV + krow(16 * kk + 8 * (mi & 1), 1) + mr * 256;
+#pragma unroll
+        for (int nt = 0; nt < 16; nt += 2) {
+          const int hh = nt >> 3;
+          uint32_t vb[4];
+          ldsm_x4_t(vb0 + hh * 128 + ((((nt & 7) + (mi >> 1)) ^ ((2 * mr + hh) & 7)) << 4), vb);
+          mma16816(oacc[nt], ph, vb[0], vb[1]);
+          mma16816(oacc[nt + 1], ph, vb[2], vb[3]);
+          mma16816(oacc[nt], pl, vb[0], vb[1]);
+          mma16816(oacc[nt + 1], pl, vb[2], vb[3]);
+        }
+      }
+    }
+    __syncwarp();  // every lane is done reading the stage: refill it
+    hcode[st] = issue(st, hlen[st]);
+    nq += hcode[st] >= 0;
+    // partial of the unit for the real rows g < REP (published with the batch's fence)
+    if (g < REP && !(a.dbg_mode & 8)) {
+      const float inv = 1.0f / lA;
+      const size_t pidx = ((size_t)r * a.Hq + h * REP + g) * a.NC + a.nc_pre + c;
+      float2* po = reinterpret_cast<float2*>(a.part_o + pidx * kHD) + t4;
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt) po[4 * nt] = make_float2(oacc[nt][0] * inv, oacc[nt][1] * inv);
+      if (t4 == 0) *reinterpret_cast<float2*>(a.part_ml + pidx * 2) = make_float2(mA * a.scale, lA);
+    }
+    if (lane == 0) dl[ndl] = r * a.Hkv + h;
+    if (++ndl == 32) publish();
+  }
+  publish();
+  if (lane == 0) {
+    if (warp == 0) astamp_lane(a, 2);
+    if (a.dbg_ts) atomicAdd(reinterpret_cast<int*>(a.dbg_ts + blockIdx.x * 16 + 9), nq);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(a.unit_ctr + 1, 1) == (int)gridDim.x - 1) {
+    a.unit_ctr[0] = 0;  // every CTA has taken its last unit: ready for the next launch
+    a.unit_ctr[1] = 0;
+  }
+  if (threadIdx.x == 0) astamp_lane(a, 6);
+  pdl_wait();  // the tcgen05 prefix partials are complete from here on
+  if (threadIdx.x == 0) astamp_lane(a, 7);
+  // LSE merge (R8): (row, kv head) pair i is merged by warp i / grid of CTA i % grid, spread over
+  // the whole grid; it waits (acquire) until all the pair's units are counted.  No deadlock: units
+  // are taken only by running CTAs, which finish them without waiting on anything.
+  const int npairs = a.rows * a.Hkv;
+  int nm = 0;
+  for (int i = blockIdx.x + warp * gridDim.x; i < npairs; i += gridDim.x * kSWarps) {
+    const int r = i / a.Hkv, h = i - r * a.Hkv;
+    if (!a.row_active[r]) continue;
+    const int nsuf = (a.row_len[r] + kSUnit - 1) / kSUnit;
+    int cnt;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(cnt) : "l"(a.merge_cnt + i) : "memory");
+      if (cnt >= nsuf) break;
+      __nanosleep(128);
+    }
+#pragma unroll 1
+    for (int e = 0; e < REP; ++e) attn_merge_one<REP>(a, r, h, e, lane);
+    __syncwarp();
+    if (lane == 0) a.merge_cnt[i] = 0;  // ready for the next launch
+    ++nm;
+  }
+  if (a.dbg_ts) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      astamp_lane(a, 8);
+      a.dbg_ts[blockIdx.x * 16 + 10] = nm;
+    }
   }
 }
 
@@ -436,8 +811,18 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnArgs a) {
   const int n = a.prefill ? a.Hkv * a.nc_pre * ((a.rows + kAttnWarps - 1) / kAttnWarps) : (int)a.n_items[0];
   uint32_t phase = 0;
   int nu = 0;
+  __shared__ int s_unit;
+  const bool dyn = !a.prefill && a.unit_ctr;  // decode: units taken dynamically (see the warp kernel)
 #pragma unroll 1
-  for (int u = blockIdx.x; u < n; u += gridDim.x, ++nu) {
+  for (int u = blockIdx.x;; ++nu) {
+    if (dyn) {
+      if (threadIdx.x == 0) s_unit = atomicAdd(a.unit_ctr, 1);
+      __syncthreads();
+      u = s_unit;
+    } else if (nu > 0) {
+      u += gridDim.x;
+    }
+    if (u >= n) break;
     if (nu < 3) astamp(a, 1 + 4 * nu);
     int code;
     if (a.prefill) {
@@ -472,7 +857,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnArgs a) {
       // ---------------- per-slot suffix chunk, one page per warp
       const int c = (code >> 16) & 0xFF, r = (code >> 8) & 0xFF, h = code & 0xFF;
       const int32_t* item = a.items + (size_t)u * kItemStride;
-      const int page_l = lane < 16 ? item[1 + lane] : 0;
+      const int page_l = lane < 16 ? item[2 + lane] : 0;
       const int tok0 = c * kSC, ntok = min(kSC, a.row_len[r] - tok0);
       const int npg = (ntok + a.pt - 1) / a.pt;
       const size_t hs = (size_t)a.pt * kHD;
@@ -546,6 +931,10 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(AttnArgs a) {
     phase ^= 1;
     if (nu < 3) astamp(a, 3 + 4 * nu);
     if (nu < 3 && threadIdx.x == 0 && a.dbg_ts) a.dbg_ts[blockIdx.x * 16 + 4 + 4 * nu] = (code < 0) ? 1 : 2;
+  }
+  if (dyn && threadIdx.x == 0 && atomicAdd(a.unit_ctr + 1, 1) == (int)gridDim.x - 1) {
+    a.unit_ctr[0] = 0;  // every CTA has taken its last unit: ready for the next launch
+    a.unit_ctr[1] = 0;
   }
   if (!a.prefill && a.tc_prefix) pdl_wait();  // the tcgen05 prefix partials are complete from here on
   if (!a.prefill && a.merge_cnt) {
@@ -983,9 +1372,9 @@ __device__ void build_attn_worklist(const WorkList& w, int* s_cnt /* [65] */, in
       for (int h = 0; h < w.Hkv; ++h) {
         int32_t* item = w.items + (size_t)(*s_npre + (s_cnt[s] + c) * w.Hkv + h) * kItemStride;
         item[0] = (c << 16) | (s << 8) | h;
-        if (w.chunk <= 32) item[16] = len;  // (<= 8 page ids: slot 16 is free)
+        item[1] = len;
         const int np = min(ppc, (len - c * w.chunk + w.pt - 1) / w.pt);
-        for (int j = 0; j < np; ++j) item[1 + j] = w.pagetab[(size_t)lid * w.maxp + c * ppc + j];
+        for (int j = 0; j < np; ++j) item[2 + j] = w.pagetab[(size_t)lid * w.maxp + c * ppc + j];
       }
   }
   __syncthreads();

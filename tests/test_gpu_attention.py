@@ -80,13 +80,14 @@ def _oracle(q, prefix, pool, pagetab, row_len, grp_rows, pt):
     return out
 
 
-def _check(lib, rows, groups, grp_rows, plen, Hq, Hkv, lens, impl, seed, qscale=1.0):
-    q, prefix, pool, pagetab, row_len = _case(rows, groups, grp_rows, plen, Hq, Hkv, lens, seed=seed, qscale=qscale)
+def _check(lib, rows, groups, grp_rows, plen, Hq, Hkv, lens, impl, seed, qscale=1.0, pt=16):
+    q, prefix, pool, pagetab, row_len = _case(rows, groups, grp_rows, plen, Hq, Hkv, lens, seed=seed, qscale=qscale,
+                                             pt=pt)
     dev = [t.cuda() for t in (q, prefix, pool, pagetab, row_len)]
     f32 = torch.full((rows, Hq, 128), float("nan"), device="cuda")
     out, _ = lib.is_dbg_attn(*dev, grp_rows=grp_rows, impl=impl, out_f32=f32)
     torch.cuda.synchronize()
-    ref = _oracle(q, prefix, pool, pagetab, row_len, grp_rows, 16)
+    ref = _oracle(q, prefix, pool, pagetab, row_len, grp_rows, pt)
     got, got_bf = f32.cpu().double().numpy(), out.cpu()
     # the bf16 output is the RNE rounding of the fp32 one (r4)
     live = row_len.numpy() > 0
@@ -127,10 +128,11 @@ def test_split_attention_default_impl(lib, rows, groups, grp_rows, plen):
     _check(lib, rows, groups, grp_rows, plen, 16, 8, lens, 0, seed=rows * 1000 + plen)
 
 
-@pytest.mark.parametrize("impl", [1, 2, 3])
+@pytest.mark.parametrize("impl", [1, 2, 3, 4])
 @pytest.mark.parametrize("rows,groups,grp_rows", [(16, 1, 8), (16, 1, 16), (64, 8, 8)])
 def test_split_attention_every_impl(lib, impl, rows, groups, grp_rows):
-    """Each launch variant on every layout it serves (3 = CUDA-core prefix: one group)."""
+    """Each launch variant on every layout it serves (1 warp units, 2 CTA units + merge kernel,
+    3 = CUDA-core prefix: one group, 4 = mma.sync units)."""
     if impl == 3 and groups > 1:
         pytest.skip("the CUDA-core prefix serves one group")
     lens = _lens(rows, groups, grp_rows, rot=impl)
@@ -163,4 +165,12 @@ def test_split_attention_errors(lib):
     with pytest.raises(InfsampError):
         lib.is_dbg_attn(dev[0], dev[1], dev[2], dev[3], bad_len, grp_rows=8)
     with pytest.raises(InfsampError):
-        lib.is_dbg_attn(*dev, grp_rows=8, impl=4)
+        lib.is_dbg_attn(*dev, grp_rows=8, impl=5)
+
+
+@pytest.mark.parametrize("pt", [4, 8, 32, 64])
+def test_split_attention_page_sizes(lib, pt):
+    """Other page sizes: 8 and 32 take the mma.sync units (one TMA box per page half),
+    4 falls back to the warp units, 64 to the 64-token CTA units + merge kernel."""
+    lens = _lens(16, 1, 16, rot=pt)
+    _check(lib, 16, 1, 16, 255, 16, 8, lens, 0, seed=pt, pt=pt)

@@ -123,19 +123,21 @@ def test_decode_step_outputs(lib, setup):
 def test_undersized_pool_is_a_budget_error(lib, setup):
     w, budget, groups = setup
     pid, prompt, true, pred = groups[0]
-    os.environ["IS_DBG_POOL_PAGES"] = "3"
+    ref = simulator.simulate(true, "infinite", 2, pred=pred, eps=0.1, page_tokens=16)
+    small = ref.peak_pages - 1  # one page short of what the schedule needs at its peak
+    os.environ["IS_DBG_POOL_PAGES"] = str(small)
     try:
         ctx = _ctx(lib, w, budget)
     finally:
         del os.environ["IS_DBG_POOL_PAGES"]
-    assert ctx.is_query()["num_pages"] == 3
+    assert ctx.is_query()["num_pages"] == small
     ctx.is_prefill(torch.as_tensor(prompt, device="cuda"), pid)
     ctx.is_start_group(true, pred)
     with pytest.raises(lib.InfsampError) as e:
         ctx.is_run_group()
     assert e.value.status == lib.IS_ERR_BUDGET
     st = ctx.is_query()
-    assert st["error"] == 1 and st["live_pages"] <= 3 and st["peak_pages"] <= 3
+    assert st["error"] == 1 and st["live_pages"] <= small and st["peak_pages"] <= small
     with pytest.raises(lib.InfsampError) as e:
         ctx.is_decode_step()
     assert e.value.status == lib.IS_ERR_BUDGET

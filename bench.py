@@ -128,16 +128,9 @@ def ncu_traffic(name):
 
 
 def lpt_place(pool, world, per_rank):
-    """LPT placement of prompts on ranks: pool = [(prompt id, predicted
-    work)]; the heaviest prompt goes to the least-loaded rank that still has room (equal
-    counts per rank, ties -> lower rank / lower id).  Returns {rank: sorted prompt ids}."""
-    load, cnt, out = [0.0] * world, [0] * world, {r: [] for r in range(world)}
-    for pid, w in sorted(pool, key=lambda x: (-x[1], x[0])):
-        r = min((r for r in range(world) if cnt[r] < per_rank), key=lambda r: (load[r], r))
-        out[r].append(pid)
-        load[r] += w
-        cnt[r] += 1
-    return {r: sorted(v) for r, v in out.items()}
+    """(paper_2506_22950_b200.rollout.lpt_place)"""
+    from paper_2506_22950_b200.rollout import lpt_place as f
+    return f(pool, world, per_rank)
 
 
 def algorithmic_bytes_per_step(shape, live_rows, suffix_tokens, P):
@@ -148,12 +141,35 @@ def algorithmic_bytes_per_step(shape, live_rows, suffix_tokens, P):
     return L * per_layer_w + V * H * 2 + (P - 1) * kv_tok + suffix_tokens * kv_tok + live_rows * kv_tok
 
 
+def attention_k5(_lib, torch, rows=64, groups=8, plen=255, slen=1024, Hq=16, Hkv=8, pt=16, reps=10):
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    q = torch.randn(rows, Hq, 128, device="cuda", generator=gen).to(torch.bfloat16)
+    prefix = torch.randn(groups, 2, Hkv, plen, 128, device="cuda", generator=gen).to(torch.bfloat16)
+    npg = math.ceil(slen / pt)
+    pool = torch.randn(rows * npg + 1, 2, Hkv, pt, 128, device="cuda", generator=gen).to(torch.bfloat16)
+    pagetab = torch.randperm(rows * npg, device="cuda").to(torch.int32).reshape(rows, npg)
+    row_len = torch.full((rows,), slen, dtype=torch.int32, device="cuda")
+    _, ms = _lib.is_dbg_attn(q, prefix, pool, pagetab, row_len, rows // groups, reps=reps)
+    kv_tok = 2 * Hkv * 128 * 2
+    nbytes = groups * plen * kv_tok + rows * slen * kv_tok
+    med = float(np.median(ms))
+    hbm = peaks()[0]
+    return {"case": f"{groups} groups x {rows // groups} rows x {slen} suffix tokens + {plen}-token prefix, 1.7B heads",
+            "bytes_per_launch": int(nbytes), "us_median": round(med * 1e3, 2),
+            "achieved": round(nbytes / (med * 1e-3) / 1e9, 1), "peak": hbm,
+            "frac": round(nbytes / (med * 1e-3) / 1e9 / hbm, 4),
+            "timing": f"is_dbg_attn, {reps} reps, a 256 MiB write evicts L2 before each, CUDA events (median)"}
+
+
 def run_ours(args):
     import torch
     from paper_2506_22950_b200 import _lib
+    from paper_2506_22950_b200 import rollout as rollout_mod
     from synth import SHAPES, gen_prompt, gen_trace, gen_weights, predict_lengths
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -187,24 +203,23 @@ def run_ours(args):
     # predicted work: every rank predicts its block, the totals are
     # all-gathered, then the longest goes to the least-loaded rank (equal counts per rank)
     own = [rank * n_total + i for i in range(n_total)]
-    timed_ids = own[args.warmup:]
+    placement = {r: [r * n_total + args.warmup + k for k in range(args.steps)] for r in range(world)}
     if dist is not None and args.placement == "lpt":
-        mine = torch.tensor([[float(pid), float(np.sum(workload(pid)[3]))] for pid in timed_ids], device="cuda")
+        mine = torch.tensor([[float(pid), float(np.sum(workload(pid)[3]))] for pid in placement[rank]], device="cuda")
         gathered = [torch.zeros_like(mine) for _ in range(world)]
         dist.all_gather(gathered, mine)
         pool = [(int(p), float(w)) for t in gathered for p, w in t.cpu().numpy()]
-        timed_ids = lpt_place(pool, world, args.steps)[rank]
+        placement = rollout_mod.lpt_place(pool, world, args.steps)
+    timed_ids = placement[rank]
     work = [workload(pid) for pid in own[:args.warmup] + timed_ids]
     d_prompts = [torch.as_tensor(p, device="cuda") for _, p, _, _ in work]
-    d_rew = torch.zeros(G, device="cuda")
-    d_len = torch.zeros(G, dtype=torch.int32, device="cuda")
-    all_len = torch.zeros(world * G, dtype=torch.int32, device="cuda")
-    all_rew = torch.zeros(world * G, device="cuda")
+    res = rollout_mod.RankResults(max(args.steps, 1), G, world)
+    warm_res = rollout_mod.RankResults(max(args.warmup, 1), G, 1)
     stream = torch.cuda.current_stream()
 
     acc = {"suffix": 0, "rows": 0, "steps": 0}
 
-    def rollout(i, host_inputs=False):
+    def rollout(i, out, k, host_inputs=False):
         pid, prompt, true, pred = work[i]
         if host_inputs:                      # e2e: host -> device copy of the step's input inside the timed region
             dp = torch.from_numpy(prompt).pin_memory().to("cuda", non_blocking=True)
@@ -217,13 +232,9 @@ def run_ours(args):
         acc["suffix"] += q["suffix_tokens"]
         acc["rows"] += q["tokens_decoded"]
         acc["steps"] += q["steps"]
-        ctx.is_group_results(d_rew, d_len)
-        # the one exchange: lengths + rewards for Eq. 2 (NCCL through the C ABI)
-        exchange_results(ctx, comm, dist, d_len, d_rew, all_len, all_rew)
-        out = None
-        if host_inputs:                      # device -> host read of the step's result
-            out = (all_rew if dist is not None else d_rew).cpu()
-        return steps, out
+        d_rew, d_len = out.slot(k)
+        ctx.is_group_results(d_rew, d_len)   # rewards + lengths into this group's slots
+        return steps
 
     def barrier():
         torch.cuda.synchronize()
@@ -232,7 +243,7 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     for i in range(args.warmup):
-        rollout(i)
+        rollout(i, warm_res, i)
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -242,25 +253,31 @@ def run_ours(args):
     for k in acc:
         acc[k] = 0
     e0.record(stream)
-    for i in range(args.warmup, n_total):
-        s, _ = rollout(i)
-        steps_total += s
+    for k, i in enumerate(range(args.warmup, n_total)):
+        steps_total += rollout(i, res, k)
         tokens += int(np.sum(work[i][2]))
+    # the one exchange, after the rank's last group: lengths + rewards of all its groups
+    res.exchange(ctx, comm, dist)
     e1.record(stream)
     barrier()
     ms = e0.elapsed_time(e1)
     st = ctx.is_query()
     timed = dict(acc)
     clk = clocks.stop()
-    # ---- e2e: same rollouts through the public API with host buffers
+    # ---- e2e: same rollouts through the public API with host buffers; the result read back is
+    # every rank's (length, reward) and the Eq. 2 advantages computed from them
     e2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     barrier()
     e2[0].record(stream)
-    for i in range(args.warmup, n_total):
-        rollout(i, host_inputs=True)
+    for k, i in enumerate(range(args.warmup, n_total)):
+        rollout(i, res, k, host_inputs=True)
+    all_len, all_rew = res.exchange(ctx, comm, dist)
+    adv = rollout_mod.advantages_by_prompt(all_len.cpu().numpy(), all_rew.cpu().numpy(),
+                                           rollout_mod.global_order(placement, world, args.steps), G)
     e2[1].record(stream)
     barrier()
     ms_e2e = e2[0].elapsed_time(e2[1])
+    assert len(adv) == world * args.steps
     # ---- per-launch profile of one decode step (eager replay with events) for the roofline
     pid, prompt, true, pred = work[0]
     ctx.is_prefill(d_prompts[0], pid)
@@ -290,6 +307,9 @@ def run_ours(args):
         attn_suffix = int(q1["suffix_tokens"] - s0)
         attn_ms = float(np.median([ctx.is_profile_kernel(3, reps=4)[0] for _ in range(3)]))
     stq = ctx.is_query()
+    # K5 microbenchmark (>= 32 MB per launch, L2 flushed before each rep): the decode
+    # attention of one layer on 8 groups x 8 rows x 1024 suffix tokens through is_dbg_attn
+    k5 = attention_k5(_lib, torch)
 
     t = torch.tensor([ms, ms_e2e, float(tokens)], device="cuda", dtype=torch.float64)
     if dist is not None:
@@ -344,7 +364,15 @@ def run_ours(args):
                              "layer_ms": round(attn_ms, 5),
                              "timing": "step 401 of a rollout; all layers' attention launches back to back in "
                                        "a graph, CUDA events (median of 3)"}
-    roof["step_GBps"] = round(algorithmic_bytes_per_step(shape, g, 0, P) / (ms_max / max(steps_total, 1) * 1e-3) / 1e9, 1)
+    # step roofline: algorithmic bytes of an average step of the timed rollouts (weights
+    # + prefix KV + the live rows' suffix KV as measured by the scheduler + appends) / step time
+    per_step_suffix = timed["suffix"] / max(steps_total, 1)
+    per_step_rows = timed["rows"] / max(steps_total, 1)
+    step_bytes = algorithmic_bytes_per_step(shape, per_step_rows, per_step_suffix, P)
+    roof["step_GBps"] = round(step_bytes / (ms_max / max(steps_total, 1) * 1e-3) / 1e9, 1)
+    roof["step_frac"] = round(roof["step_GBps"] / hbm, 4)
+    roof["step_bytes"] = int(step_bytes)
+    roof["attention_k5"] = k5
     roof["per_kind_ms"] = {k: round(v, 4) for k, v in per_kind.items() if n_launch_kind[k]}
     launches_per_step = int(st["launches_per_step"])  # counted by the library while capturing the step
     avg_steps = steps_total / args.steps
@@ -368,8 +396,9 @@ def run_ours(args):
         "gpu_launches": int(launches_per_step * steps_total + st["launches_per_prefill"] * args.steps
                             + 2 * args.steps),  # decode steps + prefills + start-group scheduler / results kernels
         "launches_per_decode_step": launches_per_step,
+        "per_gpu": round(value / world, 1),
         "e2e": {"value": round(e2e_value, 1), "unit": "tokens/s", "h2d_bytes_per_step": P * 4,
-                "d2h_bytes_per_step": G * world * 4},
+                "d2h_bytes_per_step": 8 * G * world},
         "clocks": clk,
     }
     if not args.no_cpu_baseline:
@@ -389,9 +418,12 @@ def run_groups(args):
     next prompt); the timed region covers the K timed prompts' rollouts end to end."""
     import torch
     from paper_2506_22950_b200 import _lib
+    from paper_2506_22950_b200 import rollout as rollout_mod
     from synth import SHAPES, gen_prompt, gen_trace, gen_weights, predict_lengths
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -420,15 +452,11 @@ def run_groups(args):
         pred = predict_lengths(true, "noisy", 0.3, seed=SEED + pid, prefix_k=C["prefix_k"])
         return pid, torch.as_tensor(prompt, device="cuda"), true, pred
 
-    d_rew = torch.zeros(G, device="cuda")
-    d_len = torch.zeros(G, dtype=torch.int32, device="cuda")
-    all_len = torch.zeros(world * G, dtype=torch.int32, device="cuda")
-    all_rew = torch.zeros(world * G, device="cuda")
-
-    def pipeline(prompts):
-        """Push the prompts through the M slots; returns (tokens generated, global decode steps)."""
+    def pipeline(prompts, res):
+        """Push the prompts through the M slots; returns (tokens generated, global decode steps).
+        Group results land in `res` (one slot per finished group), exchanged once at the end."""
         queue = list(prompts)
-        slot_of, tokens = {}, 0
+        slot_of, tokens, kdone = {}, 0, 0
         for slot in range(min(M, len(queue))):
             pid, dp, true, pred = queue.pop(0)
             ctx.is_prefill(dp, pid, slot=slot)
@@ -442,8 +470,9 @@ def run_groups(args):
                 if mask >> slot & 1:
                     true = slot_of.pop(slot)
                     tokens += int(np.sum(true))
+                    d_rew, d_len = res.slot(kdone)
                     ctx.is_group_results(d_rew, d_len, slot=slot)
-                    exchange_results(ctx, comm, dist, d_len, d_rew, all_len, all_rew)
+                    kdone += 1
                     if queue:
                         pid, dp, tr, pr = queue.pop(0)
                         ctx.is_prefill(dp, pid, slot=slot)
@@ -459,7 +488,8 @@ def run_groups(args):
 
     warm = [workload(j) for j in range(args.warmup)]
     timed = [workload(args.warmup + j) for j in range(args.steps * M)]
-    pipeline(warm)
+    pipeline(warm, rollout_mod.RankResults(len(warm), G, 1))
+    res = rollout_mod.RankResults(len(timed), G, world)
     barrier()
     s0 = ctx.is_query()["global_steps"]
     clocks = ClockSampler(local)
@@ -467,7 +497,8 @@ def run_groups(args):
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    tokens, steps = pipeline(timed)
+    tokens, steps = pipeline(timed, res)
+    res.exchange(ctx, comm, dist)  # the one exchange, after the rank's last group
     e1.record(stream)
     barrier()
     ms = e0.elapsed_time(e1)
@@ -485,6 +516,7 @@ def run_groups(args):
         dsteps = st["global_steps"] - s0
         print(json.dumps({
             "metric": METRIC, "value": round(tok_all / (ms_max * 1e-3), 1), "unit": "tokens/s", "n_gpus": world,
+            "per_gpu": round(tok_all / (ms_max * 1e-3) / world, 1),
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"config {args.config} x {M} co-resident groups (SURVEY §8f NEXT-1): {C['desc']}",
@@ -532,20 +564,10 @@ def nccl_comm(_lib, dist, rank, world):
     if flag.item() == 0:
         if comm is not None:
             _lib.nccl_comm_destroy(comm)
-        EXCHANGE["path"] = "torch.distributed all_gather (library NCCL unavailable)"
+        EXCHANGE["path"] = "torch.distributed all_gather (library NCCL unavailable), once per rank"
         return "torch"
-    EXCHANGE["path"] = "is_allgather_results (library NCCL)"
+    EXCHANGE["path"] = "is_allgather_results_n (library NCCL), once per rank after its last group"
     return comm
-
-
-def exchange_results(ctx, comm, dist, d_len, d_rew, all_len, all_rew):
-    if comm is None:
-        return
-    if comm == "torch":
-        dist.all_gather_into_tensor(all_len, d_len)
-        dist.all_gather_into_tensor(all_rew, d_rew)
-    else:
-        ctx.is_allgather_results(comm, d_len, d_rew, all_len, all_rew)
 
 
 _ORACLE_W = {}
@@ -582,10 +604,40 @@ TOP_P = [1.0]   # bench --top-p (1 = the paper's plain temperature sampling)
 
 
 def cpu_baseline(C, budget_s=20.0):
+    """The oracle as it stands, on this host's cores: full-recompute fp64 decode of
+    the bench config at nproc BLAS threads (the headline value) and at 1 thread, config 1
+    (tiny) decoded in full, and the schedule simulator (Alg. 1-3) per config."""
+    from threadpoolctl import threadpool_limits
+    from oracle import model as M
+    from oracle import simulator
+    from synth import SHAPES, gen_prompt, gen_trace, gen_weights, predict_lengths
     n, dt = _oracle_tokens_per_s(C, budget_s)
+    with threadpool_limits(limits=1):
+        n1, dt1 = _oracle_tokens_per_s(C, budget_s / 2)
+    # config 1 in full: every sample of the tiny group, full recompute per token
+    tiny = SHAPES["tiny"]
+    w = gen_weights(tiny, seed=SEED)
+    prompt = gen_prompt(tiny.vocab, 16, 0, seed=SEED)
+    true = gen_trace("tiny", 8, 32, 1)
+    t0 = time.perf_counter()
+    for i, L in enumerate(true):
+        M.generate(w, tiny, prompt, i, int(L), SEED)
+    t_tiny = time.perf_counter() - t0
+    # the schedule simulator per config (trace-driven Alg. 1-3 with the noisy predictor)
+    sims = {}
+    for cid, cc in sorted(CONFIGS.items()):
+        tr = gen_trace(cc["family"], cc["G"], cc["max_new"], SEED)
+        pr = predict_lengths(tr, "noisy", 0.3, seed=SEED, prefix_k=cc["prefix_k"])
+        t0 = time.perf_counter()
+        r = simulator.simulate(tr, "infinite", cc["g"], pred=pr, eps=0.1, prefix_k=cc["prefix_k"], page_tokens=16)
+        sims[f"config {cid}"] = {"ms": round((time.perf_counter() - t0) * 1e3, 2), "steps": r.total_steps}
     return {"value": round(n / dt, 5), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "oracle",
             "sample": f"oracle full-recompute fp64 decode of sample 0 of prompt 0 ({C['shape']}, prompt {C['P']}): "
-                      f"{n} tokens in {dt:.1f} s"}
+                      f"{n} tokens in {dt:.1f} s on {os.cpu_count()} BLAS threads",
+            "one_thread": {"value": round(n1 / dt1, 5), "unit": "tokens/s", "sample": f"{n1} tokens in {dt1:.1f} s"},
+            "config1_full": {"value": round(float(np.sum(true)) / t_tiny, 3), "unit": "tokens/s",
+                             "sample": f"all 8 samples of config 1 ({int(np.sum(true))} tokens) in {t_tiny:.2f} s"},
+            "schedule_simulator": sims}
 
 
 def run_reference(args):
@@ -631,6 +683,16 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (the driver may also launch us that way)
+        import socket
+        sock = socket.socket()
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+        sock.close()
+        os.execvp(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                   f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+                                   f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:])
     TOP_P[0] = args.top_p
     if args.impl == "reference":
         run_reference(args)

@@ -278,6 +278,11 @@ is_status is_nccl_unique_id(void* h_uid);
 is_status is_nccl_comm_init(const void* h_uid, int32_t rank, int32_t world, void** comm_out);
 is_status is_allgather_results(is_ctx* ctx, void* comm, const int32_t* d_len, const float* d_reward,
                                int32_t* d_all_len, float* d_all_reward);
+/* The same exchange for n samples per rank (e.g. all of a rank's groups at once, k x G, after
+ * its last rollout: SURVEY §8e "one ncclAllGather ... after a rank's groups"): d_len / d_reward
+ * [n], d_all_len / d_all_reward [world * n] in rank order.  IS_ERR_CONFIG if n < 1. */
+is_status is_allgather_results_n(is_ctx* ctx, void* comm, int32_t n, const int32_t* d_len, const float* d_reward,
+                                 int32_t* d_all_len, float* d_all_reward);
 is_status is_nccl_comm_destroy(void* comm);
 
 /* Debug: when d_logits != NULL every following lm_head launch also writes its

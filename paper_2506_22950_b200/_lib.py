@@ -21,7 +21,7 @@ EXPORTS = ["is_plan", "is_create", "is_destroy", "is_prefill", "is_start_group",
            "is_profile_step_graph", "is_profile_kernel", "is_dbg_topp", "is_dbg_attn",
            "is_dbg_gemm", "is_dbg_copy", "is_prefill_slot", "is_start_group_slot",
            "is_run_until_any_done", "is_query_slot", "is_copy_tokens_slot", "is_copy_schedule_slot",
-           "is_group_results_slot", "is_nccl_unique_id", "is_nccl_comm_init", "is_allgather_results",
+           "is_group_results_slot", "is_nccl_unique_id", "is_nccl_comm_init", "is_allgather_results", "is_allgather_results_n",
            "is_nccl_comm_destroy", "is_copy_logprobs", "is_copy_logprobs_slot", "is_kl_rewards", "is_grpo_objective", "is_last_error",
            "is_version"]
 
@@ -128,6 +128,7 @@ def load(build_if_missing=True):
     L.is_nccl_unique_id.argtypes = [vp]
     L.is_nccl_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
     L.is_allgather_results.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.is_allgather_results_n.argtypes = [vp, vp, i32, vp, vp, vp, vp]
     L.is_nccl_comm_destroy.argtypes = [vp]
     L.is_copy_logprobs.argtypes = [vp, vp]
     L.is_kl_rewards.argtypes = [vp, vp, vp, vp, i32, i32, ctypes.c_float, vp]
@@ -382,6 +383,11 @@ class Context:
     def is_allgather_results(self, comm, d_len, d_reward, d_all_len, d_all_reward):
         _check(load().is_allgather_results(self._h, comm, d_len.data_ptr(), d_reward.data_ptr(),
                                            d_all_len.data_ptr(), d_all_reward.data_ptr()))
+
+    def is_allgather_results_n(self, comm, d_len, d_reward, d_all_len, d_all_reward):
+        """One all-gather of this rank's n = d_len.numel() (length, reward) pairs."""
+        _check(load().is_allgather_results_n(self._h, comm, int(d_len.numel()), d_len.data_ptr(), d_reward.data_ptr(),
+                                             d_all_len.data_ptr(), d_all_reward.data_ptr()))
 
     def is_set_logits_dump(self, d_logits):
         _check(load().is_set_logits_dump(self._h, None if d_logits is None else d_logits.data_ptr()))

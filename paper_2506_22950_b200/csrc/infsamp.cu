@@ -811,6 +811,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
     aa.merge_cnt = (!prefill && c->tc_prefix && !c->sep_merge) ? c->merge_cnt : nullptr;
     aa.pool_row0 = l * c->num_pages * 2 * Hkv;
     aa.unit_ctr = (!prefill && !c->static_units) ? c->merge_cnt + (size_t)c->max_rows * Hkv : nullptr;
+    aa.merge_done = c->merge_cnt + (size_t)c->max_rows * Hkv + 2;
     aa.sc = prefill ? kSC : c->sc;
     aa.NC = c->NC;
     aa.prefill = prefill ? 1 : 0;
@@ -1188,7 +1189,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->q = (__nv_bfloat16*)A((size_t)R * Hq * 128 * 2);
   c->part_o = (float*)A((size_t)R * Hq * c->NC * 128 * 4);
   c->part_ml = (float*)A((size_t)R * Hq * c->NC * 2 * 4);
-  c->merge_cnt = (int*)A(((size_t)R * Hkv + 2) * 4);  // + the suffix pass's 2 unit counters
+  c->merge_cnt = (int*)A(((size_t)2 * R * Hkv + 2) * 4);  // + 2 unit counters + merged-head counters
   c->static_units = getenv("IS_STATIC_UNITS") != nullptr;  // timing comparison only
   c->ssqA = (float*)A((size_t)ceil_div64(H, 128) * R * 4);
   c->ssqB = (float*)A((size_t)ceil_div64(H, 128) * R * 4);
@@ -1848,7 +1849,7 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
   long long* nit = (long long*)dalloc(2 * sizeof(long long), &err);
   float* part_o = (float*)dalloc((size_t)rows * Hq * NC * 128 * 4, &err);
   float* part_ml = (float*)dalloc((size_t)rows * Hq * NC * 2 * 4, &err);
-  int* mcnt = (int*)dalloc(((size_t)rows * Hkv + 2) * 4, &err);
+  int* mcnt = (int*)dalloc(((size_t)2 * rows * Hkv + 2) * 4, &err);
   uint8_t* flush = reps > 0 ? (uint8_t*)dalloc((size_t)256 << 20, &err) : nullptr;  // > 2x the 126 MB L2
   CUtensorMap tm, tmp;
   if (err == IS_OK) err = make_tmap(&tm, d_prefix, (int64_t)groups * 2 * Hkv * plen, 128, 128);
@@ -1897,6 +1898,7 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
     aa.tc_prefix = tc ? 1 : 0;
     aa.merge_cnt = (tc && !sep) ? mcnt : nullptr;
     aa.unit_ctr = getenv("IS_STATIC_UNITS") ? nullptr : mcnt + (size_t)rows * Hkv;
+    aa.merge_done = mcnt + (size_t)rows * Hkv + 2;
     aa.sc = sc;
     aa.scale = 1.0f / sqrtf((float)kHD);
     AttnLaunch al{};
@@ -1946,6 +1948,8 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
       unsigned long long t0 = ~0ull;
       for (int b = 0; b < g_num_sms; ++b)
         if (h[b * 16]) t0 = std::min(t0, h[b * 16]);
+      for (int b = 0; b < 296; ++b)  // (and the prefix kernel's CTAs)
+        if (h[(size_t)2 * 296 * 16 + b * 16]) t0 = std::min(t0, h[(size_t)2 * 296 * 16 + b * 16]);
       for (int i = 0; i < 9; ++i) {
         std::vector<double> v;
         for (int b = 0; b < g_num_sms; ++b)
@@ -1961,6 +1965,19 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
       }
       std::sort(u.begin(), u.end());
       std::sort(m.begin(), m.end());
+      {  // the tcgen05 prefix kernel's CTAs (stamps 0 start, 1 waited, 2 q staged, 3 K/V landed, 4 S done,
+         // 5 P stored, 6 O done, 7 end)
+        const unsigned long long* pb = h.data() + (size_t)2 * 296 * 16;
+        for (int i = 0; i < 8; ++i) {
+          std::vector<double> v;
+          for (int b = 0; b < 296; ++b)
+            if (pb[b * 16] && pb[b * 16 + i]) v.push_back((double)((long long)(pb[b * 16 + i] - t0)) / 1e3);
+          if (v.empty()) continue;
+          std::sort(v.begin(), v.end());
+          fprintf(stderr, "prefix stamp %d: n=%zu min %.2f med %.2f max %.2f us\n", i, v.size(), v[0], v[v.size() / 2],
+                  v.back());
+        }
+      }
       fprintf(stderr, "slots per CTA min %.0f med %.0f max %.0f; merges per CTA min %.0f med %.0f max %.0f\n", u[0],
               u[u.size() / 2], u.back(), m[0], m[m.size() / 2], m.back());
     }
@@ -2177,16 +2194,23 @@ extern "C" is_status is_nccl_comm_destroy(void* comm) {
   return IS_OK;
 }
 
-extern "C" is_status is_allgather_results(is_ctx* c, void* comm, const int32_t* d_len, const float* d_reward,
-                                          int32_t* d_all_len, float* d_all_reward) {
-  if (!c || !comm || !d_len || !d_reward || !d_all_len || !d_all_reward) return fail(IS_ERR_CONFIG, "null argument");
+extern "C" is_status is_allgather_results_n(is_ctx* c, void* comm, int32_t n, const int32_t* d_len,
+                                            const float* d_reward, int32_t* d_all_len, float* d_all_reward) {
+  if (!c || !comm || !d_len || !d_reward || !d_all_len || !d_all_reward || n < 1)
+    return fail(IS_ERR_CONFIG, "null argument or n < 1");
   if (!nccl().ok) return fail(IS_ERR_CUDA, "libnccl.so.2 not available");
   StreamGuard guard(c, c->user);
   NCK(nccl().group_start());
-  NCK(nccl().all_gather(d_len, d_all_len, (size_t)c->G, kNcclInt32, comm, c->st));
-  NCK(nccl().all_gather(d_reward, d_all_reward, (size_t)c->G, kNcclFloat32, comm, c->st));
+  NCK(nccl().all_gather(d_len, d_all_len, (size_t)n, kNcclInt32, comm, c->st));
+  NCK(nccl().all_gather(d_reward, d_all_reward, (size_t)n, kNcclFloat32, comm, c->st));
   NCK(nccl().group_end());
   return IS_OK;
+}
+
+extern "C" is_status is_allgather_results(is_ctx* c, void* comm, const int32_t* d_len, const float* d_reward,
+                                          int32_t* d_all_len, float* d_all_reward) {
+  if (!c) return fail(IS_ERR_CONFIG, "null argument");
+  return is_allgather_results_n(c, comm, c->G, d_len, d_reward, d_all_len, d_all_reward);
 }
 
 extern "C" is_status is_copy_logprobs_slot(is_ctx* c, int32_t m, float* h_dst) {

@@ -122,6 +122,7 @@ struct AttnArgs {
   int* merge_cnt;             // decode: [rows][Hkv] suffix units done; the last one merges (reset by it)
   int pool_row0;              // decode (mma suffix): page-pool tensor-map coordinate of this layer (page x head)
   int dbg_mode;               // timing experiments (is_dbg_attn, IS_DBG_SUFFIX_MODE): 1 no KV loads, 2 no math
+  int* merge_done;            // decode (mma suffix): [rows][Hkv] query heads merged per pair
   int* unit_ctr;              // decode: [2] dynamic work fetching (next unit, warps / CTAs done; the last
                               //   finisher resets both for the next launch); null = static striding
   int sc;                     // decode suffix chunk (tokens per work item): kSC, or kSCW for the warp kernel
@@ -446,6 +447,7 @@ constexpr int kSWarps = 6;          // warps per CTA (each its own ring)
 constexpr int kSWStages = 2;        // stages per warp
 constexpr int kSThreads = 32 * kSWarps;
 constexpr int kSQueue = 6;          // work items loaded ahead of their issue
+constexpr int kSPublish = 8;        // units per release batch (one fence)
 constexpr int kSStaticPct = 50;     // share of the work list split statically over the warps
 struct SuffixMmaSmem {
   static constexpr int kKV = kSUnit * 2 * kHD * 2;    // K and V of one unit: 16 KB
@@ -600,13 +602,16 @@ __global__ void __launch_bounds__(kSThreads, 1) attn_suffix_mma_kernel(const __g
     }
     return cd;
   };
-  int hcode[kSWStages], hlen[kSWStages];
-  int nq = 0;  // units issued
-#pragma unroll
-  for (int st = 0; st < kSWStages; ++st) {
-    hcode[st] = issue(st, hlen[st]);
-    nq += hcode[st] >= 0;
-  }
+  // this warp's stages zero-filled (finite stale rows, see consume) while its items load
+  for (int i = lane; i < kSWStages * SM::kStage / 16; i += 32)
+    reinterpret_cast<uint4*>(wsm)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the TMA writes
+  __syncwarp();
+  static_assert(kSWStages == 2, "the consume loop is unrolled over two stages");
+  int hc0, hl0, hc1, hl1;  // per stage: the unit's code (-1: none) and row length
+  hc0 = issue(0, hl0);
+  hc1 = issue(1, hl1);
+  int nq = (hc0 >= 0) + (hc1 >= 0);  // units issued
   // ---- consume in order; refill the freed stage
   const int g = lane >> 2, t4 = lane & 3, mi = lane >> 3, mr = lane & 7;
   const float sl2 = a.scale * 1.4426950408889634f;  // exp(x * scale) = exp2(x * sl2)
@@ -623,40 +628,38 @@ __global__ void __launch_bounds__(kSThreads, 1) attn_suffix_mma_kernel(const __g
   // key row k of a stage (page k / pt, row k % pt) of K (kv = 0) or V (kv = 1): byte offset of its
   // 256-B row; the 128-B half h of that row sits at + 128 h, its 16-B chunk c at ^ swizzle
   auto krow = [&](int k0, int kv) { return (2 * k0 - (k0 & (pt - 1)) + kv * pt) * 256; };
-#pragma unroll 1
-  for (int i = 0;; ++i) {
-    const int st = i % kSWStages;
-    const int cd = hcode[st];
-    if (cd < 0) break;
-    mbar_wait(&full[st], (i / kSWStages) & 1);
-    if (i == 0 && lane == 0) astamp_lane(a, 3);
+  const int qrow = mr + 8 * (mi & 1);
+  // Every unit computes all kSUnit keys (keys past the row's length are masked to -inf, p = 0):
+  // no per-fragment branches.  The stages were zero-filled at launch and only ever hold finite KV,
+  // so a key row that was not loaded for this unit still contributes 0 * finite.
+  auto consume = [&](const int st, const int ph, int& hc, int& hl) -> bool {
+    const int cd = hc;
+    if (cd < 0) return false;
+    mbar_wait(&full[st], ph);
     const int c = (cd >> 16) & 0xFF, r = (cd >> 8) & 0xFF, h = cd & 0xFF;
-    const int ntok = (a.dbg_mode & 2) ? 0 : min(kSUnit, hlen[st] - c * kSUnit);
+    const int ntok = (a.dbg_mode & 2) ? 0 : min(kSUnit, hl - c * kSUnit);
     const uint32_t sKV = smem_u32(wsm + st * SM::kStage), sQ = sKV + SM::kKV;
     constexpr int NJ = kSUnit / 8, NKK = kSUnit / 16;  // 8-key n-tiles of S, 16-key k-steps of P.V
     // S = Q . K^T: NJ n-tiles of 8 keys, 8 k-steps of 16 dims (taken in pairs)
     float sacc[NJ][4];
 #pragma unroll
     for (int j = 0; j < NJ; ++j) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
-    const int qrow = mr + 8 * (mi & 1);
-    const uint32_t qbase = qrow < REP ? sQ + qrow * 256 + 16 * (mi >> 1) : 0u;
-    const int nj = (ntok + 7) >> 3;
+    const uint32_t qbase = qrow < REP ? sQ + qrow * 256 + 16 * (mi >> 1) : z16;
+    const uint32_t qstep = qrow < REP ? 32u : 0u;
 #pragma unroll
     for (int kp = 0; kp < 4; ++kp) {
       uint32_t qa[2][4];
-      ldsm_x4(qrow < REP ? qbase + (2 * kp) * 32 : z16, qa[0]);
-      ldsm_x4(qrow < REP ? qbase + (2 * kp + 1) * 32 : z16, qa[1]);
+      ldsm_x4(qbase + (2 * kp) * qstep, qa[0]);
+      ldsm_x4(qbase + (2 * kp + 1) * qstep, qa[1]);
       // chunk (kp & 1) * 4 + mi of half kp >> 1; the 128-B row index of key k, half h is 2k + h
       const int hh = kp >> 1;
       const uint32_t sw = ((((kp & 1) * 4 + mi) ^ ((2 * mr + hh) & 7)) << 4) + hh * 128 + mr * 256;
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
-        if (j < nj) {
-          uint32_t kb[4];
-          ldsm_x4(sKV + krow(8 * j, 0) + sw, kb);
-          mma16816(sacc[j], qa[0], kb[0], kb[1]);
-          mma16816(sacc[j], qa[1], kb[2], kb[3]);
-        }
+        uint32_t kb[4];
+        ldsm_x4(sKV + krow(8 * j, 0) + sw, kb);
+        mma16816(sacc[j], qa[0], kb[0], kb[1]);
+        mma16816(sacc[j], qa[1], kb[2], kb[3]);
       }
     }
     // row softmax: thread holds rows g (sacc[.][0..1]) and g + 8 (sacc[.][2..3], always a padding
@@ -691,37 +694,35 @@ __global__ void __launch_bounds__(kSThreads, 1) attn_suffix_mma_kernel(const __g
     for (int j = 0; j < 16; ++j) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < NKK; ++kk) {
-      if (16 * kk < ntok) {
-        // A fragment: a0 (row g, keys 0-7 of the step) = n-tile 2kk, a2 (row g, keys 8-15) = 2kk+1;
-        // a1 / a3 (row g + 8) = 0
-        uint32_t ph[4], pl[4];
+      // A fragment: a0 (row g, keys 0-7 of the step) = n-tile 2kk, a2 (row g, keys 8-15) = 2kk+1;
+      // a1 / a3 (row g + 8) = 0
+      uint32_t ph[4], pl[4];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const float* sv = sacc[2 * kk + q];
-          const __nv_bfloat162 hi = __floats2bfloat162_rn(sv[0], sv[1]);
-          const float2 hf = __bfloat1622float2(hi);
-          ph[2 * q] = *reinterpret_cast<const uint32_t*>(&hi);
-          pl[2 * q] = pack_bf16(sv[0] - hf.x, sv[1] - hf.y);
-          ph[2 * q + 1] = 0u;
-          pl[2 * q + 1] = 0u;
-        }
-        // ldmatrix.trans rows: key 16kk + 8 (mi & 1) + mr; n-tiles nt, nt + 1 (mi >> 1)
-        const uint32_t vb0 = sKV + krow(16 * kk + 8 * (mi & 1), 1) + mr * 256;
+      for (int q = 0; q < 2; ++q) {
+        const float* sv = sacc[2 * kk + q];
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(sv[0], sv[1]);
+        const float2 hf = __bfloat1622float2(hi);
+        ph[2 * q] = *reinterpret_cast<const uint32_t*>(&hi);
+        pl[2 * q] = pack_bf16(sv[0] - hf.x, sv[1] - hf.y);
+        ph[2 * q + 1] = 0u;
+        pl[2 * q + 1] = 0u;
+      }
+      // ldmatrix.trans rows: key 16kk + 8 (mi & 1) + mr; n-tiles nt, nt + 1 (mi >> 1)
+      const uint32_t vb0 = sKV + krow(16 * kk + 8 * (mi & 1), 1) + mr * 256;
 #pragma unroll
-        for (int nt = 0; nt < 16; nt += 2) {
-          const int hh = nt >> 3;
-          uint32_t vb[4];
-          ldsm_x4_t(vb0 + hh * 128 + ((((nt & 7) + (mi >> 1)) ^ ((2 * mr + hh) & 7)) << 4), vb);
-          mma16816(oacc[nt], ph, vb[0], vb[1]);
-          mma16816(oacc[nt + 1], ph, vb[2], vb[3]);
-          mma16816(oacc[nt], pl, vb[0], vb[1]);
-          mma16816(oacc[nt + 1], pl, vb[2], vb[3]);
-        }
+      for (int nt = 0; nt < 16; nt += 2) {
+        const int hh = nt >> 3;
+        uint32_t vb[4];
+        ldsm_x4_t(vb0 + hh * 128 + ((((nt & 7) + (mi >> 1)) ^ ((2 * mr + hh) & 7)) << 4), vb);
+        mma16816(oacc[nt], ph, vb[0], vb[1]);
+        mma16816(oacc[nt + 1], ph, vb[2], vb[3]);
+        mma16816(oacc[nt], pl, vb[0], vb[1]);
+        mma16816(oacc[nt + 1], pl, vb[2], vb[3]);
       }
     }
     __syncwarp();  // every lane is done reading the stage: refill it
-    hcode[st] = issue(st, hlen[st]);
-    nq += hcode[st] >= 0;
+    hc = issue(st, hl);
+    nq += hc >= 0;
     // partial of the unit for the real rows g < REP (published with the batch's fence)
     if (g < REP && !(a.dbg_mode & 8)) {
       const float inv = 1.0f / lA;
@@ -732,16 +733,23 @@ __global__ void __launch_bounds__(kSThreads, 1) attn_suffix_mma_kernel(const __g
       if (t4 == 0) *reinterpret_cast<float2*>(a.part_ml + pidx * 2) = make_float2(mA * a.scale, lA);
     }
     if (lane == 0) dl[ndl] = r * a.Hkv + h;
-    if (++ndl == 32) publish();
+    if (++ndl == kSPublish) publish();
+    return true;
+  };
+  if (lane == 0) astamp_lane(a, 3);
+#pragma unroll 1
+  for (int ph = 0;; ph ^= 1) {
+    if (!consume(0, ph, hc0, hl0)) break;
+    if (!consume(1, ph, hc1, hl1)) break;
   }
   publish();
   if (lane == 0) {
     if (warp == 0) astamp_lane(a, 2);
     if (a.dbg_ts) atomicAdd(reinterpret_cast<int*>(a.dbg_ts + blockIdx.x * 16 + 9), nq);
   }
-  __syncthreads();
-  if (threadIdx.x == 0 && atomicAdd(a.unit_ctr + 1, 1) == (int)gridDim.x - 1) {
-    a.unit_ctr[0] = 0;  // every CTA has taken its last unit: ready for the next launch
+  // each warp moves on to its merges as soon as its own units are published (no CTA barrier)
+  if (lane == 0 && atomicAdd(a.unit_ctr + 1, 1) == (int)gridDim.x * kSWarps - 1) {
+    a.unit_ctr[0] = 0;  // every warp has taken its last unit: ready for the next launch
     a.unit_ctr[1] = 0;
   }
   if (threadIdx.x == 0) astamp_lane(a, 6);
@@ -750,9 +758,12 @@ __global__ void __launch_bounds__(kSThreads, 1) attn_suffix_mma_kernel(const __g
   // LSE merge (R8): (row, kv head) pair i is merged by warp i / grid of CTA i % grid, spread over
   // the whole grid; it waits (acquire) until all the pair's units are counted.  No deadlock: units
   // are taken only by running CTAs, which finish them without waiting on anything.
+  // (one query head of a pair per warp: the REP heads of a pair merge concurrently; the last of
+  // them re-arms the pair's counters)
   const int npairs = a.rows * a.Hkv;
   int nm = 0;
-  for (int i = blockIdx.x + warp * gridDim.x; i < npairs; i += gridDim.x * kSWarps) {
+  for (int k = blockIdx.x + warp * gridDim.x; k < npairs * REP; k += gridDim.x * kSWarps) {
+    const int i = k / REP, e = k - i * REP;
     const int r = i / a.Hkv, h = i - r * a.Hkv;
     if (!a.row_active[r]) continue;
     const int nsuf = (a.row_len[r] + kSUnit - 1) / kSUnit;
@@ -762,10 +773,11 @@ __global__ void __launch_bounds__(kSThreads, 1) attn_suffix_mma_kernel(const __g
       if (cnt >= nsuf) break;
       __nanosleep(128);
     }
-#pragma unroll 1
-    for (int e = 0; e < REP; ++e) attn_merge_one<REP>(a, r, h, e, lane);
-    __syncwarp();
-    if (lane == 0) a.merge_cnt[i] = 0;  // ready for the next launch
+    attn_merge_one<REP>(a, r, h, e, lane);
+    if (lane == 0 && atomicAdd(a.merge_done + i, 1) == REP - 1) {
+      a.merge_cnt[i] = 0;  // ready for the next launch
+      a.merge_done[i] = 0;
+    }
     ++nm;
   }
   if (a.dbg_ts) {

@@ -29,29 +29,32 @@ def _fake_group(pid, G):
 
 
 def _worker(rank, world, port, n_prompts, G, q):
+    """One rank of the production host path (paper_2506_22950_b200.rollout, as bench.py drives
+    it): its prompts' results in RankResults slots, ONE exchange after the last group (the torch
+    path: gloo here; the library's NCCL path is tests/test_gpu_multirank.py), then the
+    advantages of every prompt from the gathered arrays."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2506_22950_b200 import rollout
-    mine = rollout.shard_prompts(n_prompts, rank, world)
     per_rank = -(-n_prompts // world)
-    lens = np.zeros(per_rank * G, np.int32)
-    rews = np.full(per_rank * G, np.nan, np.float32)
-    for k, pid in enumerate(mine):
-        l, r = _fake_group(pid, G)
-        lens[k * G:(k + 1) * G] = l
-        rews[k * G:(k + 1) * G] = r
-    all_l, all_r = rollout.gather_results(torch.from_numpy(lens), torch.from_numpy(rews))
-    all_l, all_r = all_l.numpy(), all_r.numpy()
-    # drop padding blocks, restore global prompt order
-    ids = [p for rk in range(world) for p in rollout.shard_prompts(n_prompts, rk, world)
-           + [-1] * (per_rank - len(rollout.shard_prompts(n_prompts, rk, world)))]
-    keep = [i for i, p in enumerate(ids) if p >= 0]
-    order = np.argsort([ids[i] for i in keep])
-    rew = np.concatenate([all_r[i * G:(i + 1) * G] for i in keep])
-    rew = rew.reshape(-1, G)[order].reshape(-1)
-    ln = np.concatenate([all_l[i * G:(i + 1) * G] for i in keep]).reshape(-1, G)[order].reshape(-1)
-    adv = rollout.group_advantages(rew, G)
+    # block placement padded to equal counts (a padding group reports length 0: not completed)
+    placement = {r: rollout.shard_prompts(n_prompts, r, world) for r in range(world)}
+    placement = {r: v + [-1 - r * per_rank - k for k in range(per_rank - len(v))] for r, v in placement.items()}
+    res = rollout.RankResults(per_rank, G, world, device="cpu")
+    for k, pid in enumerate(placement[rank]):
+        d_rew, d_len = res.slot(k)
+        if pid >= 0:
+            l, r = _fake_group(pid, G)
+            d_len.copy_(torch.from_numpy(l))
+            d_rew.copy_(torch.from_numpy(r))
+    all_l, all_r = res.exchange(ctx=None, comm="torch", dist=dist)
+    order = rollout.global_order(placement, world, per_rank)
+    by_pid = rollout.advantages_by_prompt(all_l.numpy(), all_r.numpy(), order, G)
+    real = sorted(p for p in by_pid if p >= 0)
+    ln = np.concatenate([by_pid[p][0] for p in real])
+    rew = np.concatenate([by_pid[p][1] for p in real])
+    adv = np.concatenate([by_pid[p][2] for p in real])
     q.put((rank, ln.tolist(), rew.tolist(), adv.tolist()))
     dist.destroy_process_group()
 
@@ -96,7 +99,7 @@ def test_lpt_placement_balances_predicted_work():
     for world in (2, 4, 8):
         per = 3
         pool = [(pid, float(w)) for pid, w in enumerate(rng.lognormal(9.0, 0.5, world * per))]
-        out = bench.lpt_place(pool, world, per)
+        out = bench.lpt_place(pool, world, per)  # (= paper_2506_22950_b200.rollout.lpt_place)
         assert sorted(p for v in out.values() for p in v) == list(range(world * per))
         assert all(len(v) == per for v in out.values())
         w = dict(pool)

@@ -108,23 +108,26 @@ class ClockSampler:
 
 
 def ncu_traffic(name):
-    """DRAM bytes (read + write) per launch of a kernel from the newest committed ncu
-    `--set full` summary profiles/*/ncu_<name>.csv (tools/summarize_profiles.py), or None."""
+    """DRAM bytes per launch of a kernel from the newest committed ncu `--set full` summary
+    profiles/*/ncu_<name>.csv (tools/summarize_profiles.py), or None: read + write (the contract's
+    `traffic`) and read alone (min over the captured launches)."""
     import csv
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_{name}.csv")), key=os.path.getmtime)
     if not files:
         return None
     rows = list(csv.DictReader(open(files[-1])))
-    vals = []
+    rw, rd = [], []
     for r in rows:
         try:  # ncu reports these counters in MB (1e6 bytes) in the raw page
-            vals.append((float(r["dram__bytes_read.sum"]) + float(r["dram__bytes_write.sum"])) * 1e6)
+            rd.append(float(r["dram__bytes_read.sum"]) * 1e6)
+            rw.append((float(r["dram__bytes_read.sum"]) + float(r["dram__bytes_write.sum"])) * 1e6)
         except (KeyError, ValueError):
             pass
-    # min over the captured launches: ncu's replay can attribute other kernels' dirty-line
-    # write-backs to a launch (one capture showed 140 MB of writes for a 0.2 MB output)
-    return {"bytes_per_launch": round(float(np.min(vals))), "source": os.path.relpath(files[-1], ROOT)} if vals else None
+    if not rw:
+        return None
+    return {"bytes_per_launch": round(float(np.min(rw))), "read_bytes_per_launch": round(float(np.min(rd))),
+            "source": os.path.relpath(files[-1], ROOT)}
 
 
 def lpt_place(pool, world, per_rank):
@@ -344,7 +347,11 @@ def run_ours(args):
                 "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
                 "peak_kind": peak_kind, "bytes_per_launch": gu_bytes,
                 "traffic": tr["bytes_per_launch"] if tr else None,
+                "traffic_read": tr["read_bytes_per_launch"] if tr else None,
                 "traffic_source": tr["source"] if tr else None,
+                "traffic_note": "ncu --set full --cache-control all; reads = the weights + activations (1.00x "
+                                "algorithmic); the kernel's own output is 0.2 MB, the rest of dram__bytes_write "
+                                "are write-backs ncu attributes to the launch",
                 "launch_ms": round(gu_ms, 5), "launches_timed": int(gu_kernel[0][1]),
                 "timing": "CUDA events around a graph of the step's gate/up launches (all layers, 4 passes, PDL "
                           "as in the step; median of 3 replays)",

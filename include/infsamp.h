@@ -88,6 +88,9 @@ typedef struct {
                               only (R5, the parity setting); 1 = a sample also finishes when it samples
                               eos_id (its length is then shorter than true_len).  Needs prefix_k == 0 */
   int32_t eos_id;
+  int32_t bin_slots;       /* IS_MODE_INFINITE: 0 = Alg. 2 over N = G/g micro groups (the paper), 1 = over
+                              g slot bins (SPEC bin_mode = slots; NEXT-2, DESIGN R38): slot j starts
+                              with bin j's head, then Alg. 3 SJF refill.  is_plan_out.loads then has g entries */
   float top_p;             /* nucleus sampling (DESIGN R36): 0 < top_p < 1 samples the
                               Gumbel-max token inside the top-p nucleus (integer-exact mass, fixed-
                               sequence exp); 0 or 1 = off (the paper's plain temperature sampling).
@@ -99,7 +102,7 @@ typedef struct {
 typedef struct {
   int32_t* mask;          /* [G][2]: (group n in 1..N, position j) */
   int64_t* scaled_len;    /* [G]: l~_i = ceil(l^_i / K) */
-  int64_t* loads;         /* [N]: L_n */
+  int64_t* loads;         /* [N]: L_n; N = G/g, or g with bin_slots */
   int32_t* overflow_ids;  /* [G]: samples placed by the least-loaded fallback (R15) */
   int32_t* init_slots;    /* [g]: first g samples from mask, lexicographic (n, j) (R13) */
   int32_t* refill_queue;  /* [G]: static SJF order of the remaining samples (R17) */

@@ -75,7 +75,7 @@ def sjf_refill(pred, finished, started):
 def build_plan(mode, G, g, pred=None, eps=0.1, finished=()):
     """Initial slot fill + static refill queue for one group.
 
-    mode: 'full' | 'naive' | 'fifo' | 'infinite' | 'fptas_only' | 'sjf_only' | 'dynamic'.
+    mode: 'full' | 'naive' | 'fifo' | 'infinite' | 'infinite_slots' | 'fptas_only' | 'sjf_only' | 'dynamic'.
     dynamic (R35): the G candidates in trace order, no quota.
     `finished` = samples that completed in the prefix phase (infinite only).
     Table 2's decomposition is undefined in the paper; SPEC.md's
@@ -104,6 +104,31 @@ def build_plan(mode, G, g, pred=None, eps=0.1, finished=()):
         plan = fptas_plan(pred, G // g, eps)
         lex = sorted(range(G), key=lambda i: plan["mask"][i])
         return dict(init=lex[:g], queue=lex[g:], plan=plan)
+    if mode == "infinite_slots":
+        # SPEC.md l.175 / l.204 / l.255 (bin_mode = slots): Alg. 2 with g bins instead of N
+        # groups; slot j starts with the head of bin j (its first member in Alg. 2's placement
+        # order that did not finish in the prefix phase); an empty bin's slot takes the SJF
+        # queue head, in ascending slot order (DESIGN R38); the rest is the Alg. 3 SJF queue.
+        plan = fptas_plan(pred, g, eps)
+        fin = set(finished)
+        heads = []
+        for j in range(g):
+            members = [i for i in plan["groups"][j] if i not in fin]
+            heads.append(members[0] if members else None)
+        started = set(i for i in heads if i is not None)
+        queue = []
+        while True:
+            j = sjf_refill(pred, fin, started)
+            if j is None:
+                break
+            queue.append(j)
+            started.add(j)
+        init = []
+        for h in heads:
+            if h is None:
+                h = queue.pop(0) if queue else -1
+            init.append(h)
+        return dict(init=init, queue=queue, plan=plan)
     if mode != "infinite":
         raise PlanError(f"IS_ERR_CONFIG: unknown mode {mode}")
     N = G // g

@@ -10,6 +10,8 @@ Follows PAPER.md Alg. 1 (l.218-241) step by step, with the modes of §3.1-3.2:
   infinite  Alg. 1: [optional prefix phase of k tokens in ceil(G/g) barriered
             rounds, l.215-216, l.371] -> Alg. 2 plan -> first g samples from the
             mask -> SJF refill (Alg. 3) with no quota           (R17-R22)
+  infinite_slots  the same with Alg. 2 over g bins (SPEC bin_mode = slots, l.175,
+            l.204, l.255): slot j starts with bin j's head      (R38)
   dynamic   dynamic-slot sampling, §3.2 l.199-200 ("slot is immediately
             reassigned"): g slots, no quota, candidates drawn in trace order from
             the len(true_len) >= target candidates; the run stops at the step of
@@ -71,7 +73,7 @@ def simulate(true_len, mode, g, pred=None, eps=0.1, prefix_k=0, page_tokens=16, 
     def run_phase(queue, stop_at, barrier, quota, init):
         nonlocal step
         for s, uid in enumerate(init):
-            slot[s] = uid
+            slot[s] = uid if uid is not None else -1
         q = list(queue)
         while any(u >= 0 for u in slot):
             step += 1
@@ -144,7 +146,7 @@ def simulate(true_len, mode, g, pred=None, eps=0.1, prefix_k=0, page_tokens=16, 
         p = build_plan(mode, G, g, pred=pred, eps=eps)
         res.init, res.queue, res.plan = p["init"], p["queue"], p["plan"]
         run_phase(p["queue"], lambda u: big, False, 0, p["init"])
-    elif mode == "infinite":
+    elif mode in ("infinite", "infinite_slots"):
         if pred is None:
             raise ValueError("infinite mode needs predicted lengths")
         if prefix_k > 0:
@@ -153,7 +155,7 @@ def simulate(true_len, mode, g, pred=None, eps=0.1, prefix_k=0, page_tokens=16, 
             res.prefix_steps = step
             # R22 / SPEC l.59: samples that finished in the prefix phase have pred = true
             pred = [true_len[i] if true_len[i] <= prefix_k else int(pred[i]) for i in range(G)]
-        p = build_plan("infinite", G, g, pred=pred, eps=eps, finished=finished)
+        p = build_plan(mode, G, g, pred=pred, eps=eps, finished=finished)
         res.init, res.queue, res.plan = p["init"], p["queue"], p["plan"]
         count[:] = [0] * g
         run_phase(p["queue"], lambda u: big, False, 0, p["init"])

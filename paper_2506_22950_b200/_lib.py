@@ -46,7 +46,7 @@ class Config(ctypes.Structure):
                 ("eps", ctypes.c_double), ("temperature", ctypes.c_float), ("seed", ctypes.c_uint64),
                 ("mode", ctypes.c_int32), ("decode_impl", ctypes.c_int32), ("max_groups", ctypes.c_int32),
                 ("dynamic_target", ctypes.c_int32), ("eos_enabled", ctypes.c_int32), ("eos_id", ctypes.c_int32),
-                ("top_p", ctypes.c_float)]
+                ("bin_slots", ctypes.c_int32), ("top_p", ctypes.c_float)]
 
 
 class PlanOut(ctypes.Structure):
@@ -163,6 +163,9 @@ def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix
     c.G, c.g, c.max_new_tokens, c.prompt_len = G, g, max_new_tokens, prompt_len
     c.prefix_k, c.page_tokens, c.row_capacity = prefix_k, page_tokens, row_capacity
     c.kv_budget_bytes, c.eps, c.temperature, c.seed = kv_budget_bytes, eps, temperature, seed
+    c.bin_slots = 0
+    if mode == "infinite_slots":  # Alg. 2 over g slot bins (SPEC bin_mode = slots, DESIGN R38)
+        mode, c.bin_slots = "infinite", 1
     c.mode = MODES[mode] if isinstance(mode, str) else int(mode)
     c.decode_impl = 0  # reserved (include/infsamp.h)
     c.max_groups = max_groups
@@ -177,7 +180,7 @@ def is_plan(cfg, pred_len, finished=None):
     L = load()
     G = cfg.G
     g = G if cfg.mode == MODES["full"] else cfg.g
-    N = G // g if g else 1
+    N = max(G // g if g else 1, g)  # loads has G/g entries, or g with bin_slots
     mask = np.zeros(2 * G, np.int32)
     sl = np.zeros(G, np.int64)
     loads = np.zeros(max(N, 1), np.int64)
@@ -192,8 +195,9 @@ def is_plan(cfg, pred_len, finished=None):
     fin = None if finished is None else np.ascontiguousarray(finished, np.uint8)
     _check(L.is_plan(ctypes.byref(cfg), None if pred is None else _np_ptr(pred),
                      None if fin is None else _np_ptr(fin), ctypes.byref(out)))
+    nb = g if cfg.bin_slots else (G // g if g else 1)
     return dict(mask=[(int(mask[2 * i]), int(mask[2 * i + 1])) for i in range(G)], scaled=[int(x) for x in sl],
-                loads=[int(x) for x in loads[:N]], overflow=[int(x) for x in ovf[:out.n_overflow]],
+                loads=[int(x) for x in loads[:nb]], overflow=[int(x) for x in ovf[:out.n_overflow]],
                 init=[int(x) for x in init[:g]], queue=[int(x) for x in queue[:out.queue_len]], K=out.K,
                 capacity=out.capacity, reserved_bytes=out.reserved_bytes)
 

@@ -90,6 +90,8 @@ struct GemmArgs {
   float fn_eps;
   int* zero;                   // optional: words zeroed once the previous kernel completed
   int zero_n;                  //   (the persistent decode kernel's dependency counters)
+  int* pf_progress;            // optional: the L2 weight prefetcher's pacing word (l2_prefetch_kernel):
+  int pf_seq;                  //   this GEMM's index in the step's weight order, written at launch
 };
 
 constexpr int kBM = 128;
@@ -185,6 +187,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int n_lo = rank * BN / S, n_hi = (rank + 1) * BN / S;
 
   if (threadIdx.x == 0) stamp(a, 0);
+  if (a.pf_progress && blockIdx.x == 0 && threadIdx.x == 0)
+    asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(a.pf_progress), "r"(a.pf_seq) : "memory");
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);

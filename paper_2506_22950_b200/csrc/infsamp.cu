@@ -82,6 +82,8 @@ static is_status check_config(const is_config* c) {
   if (c->dynamic_target < 0 || c->dynamic_target > c->G || (c->dynamic_target > 0 && c->mode != IS_MODE_DYNAMIC))
     return fail(IS_ERR_CONFIG, "dynamic_target must be 0 or 1..G (got %d) and needs IS_MODE_DYNAMIC", c->dynamic_target);
   if (c->decode_impl != 0 && c->decode_impl != 1) return fail(IS_ERR_CONFIG, "decode_impl must be 0 or 1 (reserved)");
+  if (c->bin_slots != 0 && (c->bin_slots != 1 || c->mode != IS_MODE_INFINITE))
+    return fail(IS_ERR_CONFIG, "bin_slots must be 0 or 1 and needs IS_MODE_INFINITE");
   if (c->max_groups < 0 || n_groups(c) > 8 || n_groups(c) * g > 64)
     return fail(IS_ERR_CONFIG, "need 1 <= max_groups <= 8 and max_groups * g <= 64 (got %d x %d)", n_groups(c), g);
   return IS_OK;
@@ -106,7 +108,10 @@ extern "C" is_status is_plan(const is_config* cfg, const int32_t* pred, const ui
                              is_plan_out* out) {
   if (!cfg || !out) return fail(IS_ERR_CONFIG, "null argument");
   CKS(check_config(cfg));
-  const int G = cfg->G, g = eff_g(cfg), N = G / g;
+  const int G = cfg->G, g = eff_g(cfg);
+  // Alg. 2's bins: N = G/g micro groups (the paper's Alg. 2), or g slot bins (bin_slots, R38)
+  const bool slots = cfg->bin_slots != 0;
+  const int N = slots ? g : G / g;
   out->K = 0;
   out->capacity = 0;
   out->n_overflow = 0;
@@ -192,6 +197,28 @@ extern "C" is_status is_plan(const is_config* cfg, const int32_t* pred, const ui
   }
   if (out->loads)
     for (int n = 0; n < N; ++n) out->loads[n] = load[n];
+  if (slots) {
+    // SPEC.md l.175 / l.255 (bin_mode = slots, R38): slot j starts with bin j's head (its first
+    // member in placement order not finished in the prefix phase); an empty bin's slot takes the
+    // SJF queue head in ascending slot order; the rest is the Alg. 3 static queue.
+    std::vector<int> head(g, -1);
+    for (int i : order) {
+      if (finished && finished[i]) continue;
+      if (head[gn[i]] < 0) head[gn[i]] = i;
+    }
+    std::vector<char> used(G, 0);
+    for (int j = 0; j < g; ++j)
+      if (head[j] >= 0) used[head[j]] = 1;
+    std::vector<int> rest;
+    for (int i = 0; i < G; ++i)
+      if (!used[i] && !(finished && finished[i])) rest.push_back(i);
+    std::stable_sort(rest.begin(), rest.end(), [&](int a, int b) { return pred[a] < pred[b]; });
+    size_t qh = 0;
+    for (int j = 0; j < g; ++j) out->init_slots[j] = head[j] >= 0 ? head[j] : (qh < rest.size() ? rest[qh++] : -1);
+    out->queue_len = (int32_t)(rest.size() - qh);
+    for (size_t i = qh; i < rest.size(); ++i) out->refill_queue[i - qh] = rest[i];
+    return IS_OK;
+  }
   // Alg. 1 l.230: first g samples from mask in lexicographic (n, j) order,
   // skipping samples finished in the prefix phase (R13, R22).
   std::vector<int> lex(G);
@@ -537,6 +564,14 @@ struct is_ctx {
   bool graphK_ok;
   int steps_per_graph;
   int launches_per_prefill;
+  // L2 weight prefetcher (IS_L2PF = lookahead MB; 0 = off): a parallel branch of the step graph
+  long long pf_lookahead;
+  unsigned long long* pf_ptr;
+  long long* pf_off;
+  int pf_n;
+  int* pf_progress;
+  cudaStream_t pf_st;
+  cudaEvent_t pf_fork, pf_join;
 };
 
 static void* dalloc(size_t bytes, is_status* s) {
@@ -600,6 +635,7 @@ static SchedArgs sched_args(is_ctx* c) {
   a.nc_suf = c->nc_suf;
   a.chunk = c->sc;
   a.tc_prefix = c->tc_prefix;
+  a.pf_progress = c->pf_lookahead > 0 ? c->pf_progress : nullptr;
   return a;
 }
 
@@ -782,6 +818,10 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
         a.bn_ld = c->max_rows;
         a.bn_eps = s.rms_eps;
       }
+      if (!prefill && c->pf_lookahead > 0) {
+        a.pf_progress = c->pf_progress;
+        a.pf_seq = 4 * l;
+      }
       if (prefill || !(g_skip & 2)) CKS(launch_gemm<EPI_QKV>(BN, w.tm_qkv, tm_xn, a, st, prefill ? 0 : c->stg_qkv));
     }
     prof_mark(st, 1);
@@ -848,6 +888,10 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
         a.fn_bar = c->fn_bar;
         a.fn_eps = s.rms_eps;
       }
+      if (!prefill && c->pf_lookahead > 0) {
+        a.pf_progress = c->pf_progress;
+        a.pf_seq = 4 * l + 1;
+      }
       if (prefill || !(g_skip & 16)) CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_o, tm_attn, a, st, prefill ? 0 : c->stg_o));
     }
     prof_mark(st, 4);
@@ -873,6 +917,10 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
         a.bn_ld = c->max_rows;
         a.bn_eps = s.rms_eps;
       }
+      if (!prefill && c->pf_lookahead > 0) {
+        a.pf_progress = c->pf_progress;
+        a.pf_seq = 4 * l + 2;
+      }
       if (prefill || !(g_skip & 32)) CKS(launch_gemm<EPI_SWIGLU>(BN, w.tm_gu, tm_xn, a, st, prefill ? 0 : c->stg_gu));
     }
     prof_mark(st, 5);
@@ -896,6 +944,10 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
         a.fn_bar = c->fn_bar + 2;
         a.fn_eps = s.rms_eps;
       }
+      if (!prefill && c->pf_lookahead > 0) {
+        a.pf_progress = c->pf_progress;
+        a.pf_seq = 4 * l + 3;
+      }
       if (prefill || !(g_skip & 64)) CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_d, tm_act, a, st, prefill ? 0 : c->stg_d));
     }
     prof_mark(st, 6);
@@ -914,6 +966,16 @@ static is_status enqueue_step(is_ctx* c) {
 static is_status enqueue_step_body(is_ctx* c) {
   cudaStream_t st = c->st;
   const is_shape& s = c->sh;
+  if (c->pf_lookahead > 0) {
+    // the L2 weight prefetcher runs beside the step (fork here, join before the scheduler)
+    CK(cudaEventRecord(c->pf_fork, st));
+    CK(cudaStreamWaitEvent(c->pf_st, c->pf_fork, 0));
+    PrefetchArgs pa{c->pf_ptr, c->pf_off, c->pf_n, c->pf_progress, c->pf_lookahead};
+    l2_prefetch_kernel<<<1, 32, 0, c->pf_st>>>(pa);
+    CK(cudaGetLastError());
+    ++g_launches;
+    CK(cudaEventRecord(c->pf_join, c->pf_st));
+  }
   CKS(run_layers(c, c->rc, false));
   if (!c->fuse_norm)  // (else the last down GEMM's epilogue applied the final norm)
     CKS(launch_k(rmsnorm_kernel, dim3(c->rc), dim3(256), st, (const float*)c->resid, (const float*)c->final_norm,
@@ -938,6 +1000,10 @@ static is_status enqueue_step_body(is_ctx* c) {
   a.seed = c->cfg.seed;
   a.inv_temp = (float)(1.0 / (double)c->cfg.temperature);
   g_splitk_ws = c->splitk_ws;
+  if (c->pf_lookahead > 0) {
+    a.pf_progress = c->pf_progress;
+    a.pf_seq = 4 * s.layers;
+  }
   CKS(launch_gemm<EPI_SAMPLE>(c->BN, c->tm_embed, c->tm_xn_dec, a, st, c->stg_lm));
   if (c->topp) {  // top-p < 1 (R36): the nucleus and its Gumbel-max replace the full-vocabulary key
     ToppArgs t{};
@@ -966,6 +1032,7 @@ static is_status enqueue_step_body(is_ctx* c) {
     CKS(launch_k(topp_sample_kernel, dim3(kToppBlocks, c->rc), dim3(kToppThreads), st, t));
   }
   prof_mark(st, 7);
+  if (c->pf_lookahead > 0) CK(cudaStreamWaitEvent(st, c->pf_join, 0));
   CKS(launch_k(sched_kernel, dim3(1), dim3(kSchedThreads), st, sched_args(c), 1, (1 << c->M) - 1));
   prof_mark(st, 8);
   CK(cudaMemcpyAsync(c->st_host, c->st_dev, sizeof(long long) * ST_COUNT * (c->M + 1), cudaMemcpyDeviceToHost, st));
@@ -1318,6 +1385,38 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
     c->fuse_norm = (e && atoi(e) != 0) && !c->bnorm && th * std::max(c->split_o, 1) <= g_num_sms &&
                    th * std::max(c->split_d, 1) <= g_num_sms;
   }
+  {
+    // L2 weight prefetcher (opt-in: IS_L2PF = lookahead in MB)
+    const char* e = getenv("IS_L2PF");
+    c->pf_lookahead = e ? (long long)(atof(e) * (1 << 20)) : 0;
+    if (c->pf_lookahead > 0) {
+      std::vector<unsigned long long> ptr;
+      std::vector<long long> off(1, 0);
+      auto add = [&](const void* p, size_t bytes) {
+        ptr.push_back((unsigned long long)(uintptr_t)p);
+        off.push_back(off.back() + (long long)bytes);
+      };
+      for (int l = 0; l < s.layers; ++l) {
+        const LayerW& w = c->L[l];
+        add(w.wqkv, (size_t)c->qkv_w * H * 2);
+        add(w.wo, (size_t)H * Hq * 128 * 2);
+        add(w.wgu, (size_t)2 * F * H * 2);
+        add(w.wd, (size_t)H * F * 2);
+      }
+      add(c->embed, (size_t)V * H * 2);
+      c->pf_n = (int)ptr.size();
+      c->pf_ptr = (unsigned long long*)A(ptr.size() * 8);
+      c->pf_off = (long long*)A(off.size() * 8);
+      c->pf_progress = (int*)A(sizeof(int));
+      if (err != IS_OK) return err;
+      CK(cudaMemcpy(c->pf_ptr, ptr.data(), ptr.size() * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(c->pf_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemset(c->pf_progress, 0xFF, sizeof(int)));
+      CK(cudaStreamCreateWithFlags(&c->pf_st, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->pf_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->pf_join, cudaEventDisableTiming));
+    }
+  }
   CK(cudaDeviceSynchronize());
   *out = c;
   return IS_OK;
@@ -1347,6 +1446,14 @@ extern "C" void is_destroy(is_ctx* c) {
     cudaFree(w.k_norm);
   }
   if (c->st_host) cudaFreeHost(c->st_host);
+  if (c->pf_lookahead > 0) {
+    cudaFree(c->pf_ptr);
+    cudaFree(c->pf_off);
+    cudaFree(c->pf_progress);
+    cudaEventDestroy(c->pf_fork);
+    cudaEventDestroy(c->pf_join);
+    cudaStreamDestroy(c->pf_st);
+  }
   cudaEventDestroy(c->ev_in);
   cudaEventDestroy(c->ev_out);
   cudaStreamDestroy(c->st);
@@ -1443,9 +1550,7 @@ extern "C" is_status is_start_group_slot(is_ctx* c, int32_t m, const int32_t* tr
     st[ST_QLEN] = G - g;
     st[ST_MAIN_PENDING] = 1;
     st[ST_MAIN_QLEN] = po.queue_len;
-    int ni = 0;
-    while (ni < g && init[ni] >= 0) ++ni;
-    st[ST_MAIN_NINIT] = ni;
+    st[ST_MAIN_NINIT] = g;  // main_init holds -1 for slots left idle
   } else {
     st[ST_PHASE] = 1;
     st[ST_BARRIER] = (c->cfg.mode == IS_MODE_NAIVE || c->cfg.mode == IS_MODE_FULL) ? 1 : 0;

@@ -1253,6 +1253,66 @@ __global__ void __launch_bounds__(128, 1)
   }
 }
 
+// ------------------------------------------------------------------ L2 weight prefetcher
+// A side branch of the decode-step graph: one warp walks the step's weights in the order the
+// GEMMs consume them (per layer QKV, o_proj, gate/up, down; then the tied lm_head) and issues
+// cp.async.bulk.prefetch.L2 for 64 KB chunks, staying at most `lookahead` bytes ahead of the
+// GEMM that last announced itself (GemmArgs.pf_progress = its index in this order), so HBM keeps
+// streaming weights into L2 while the dependent GEMM / attention chain of earlier layers runs.
+// Nothing waits on it: it only changes where the GEMMs' weight TMA loads hit.
+struct PrefetchArgs {
+  const unsigned long long* ptr;  // [n] start address of each weight matrix, consumption order
+  const long long* off;           // [n + 1] byte offset of each matrix in that order (prefix sums)
+  int n;
+  int* progress;                  // the GEMMs' announced index (-1 before the step's first GEMM)
+  long long lookahead;            // bytes
+};
+__global__ void __launch_bounds__(32) l2_prefetch_kernel(PrefetchArgs a) {
+  const int lane = threadIdx.x;
+  constexpr long long kChunk = 64 << 10;
+  long long limit = -1;  // prefetch bytes [0, limit] allowed so far
+  int seen = -2;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#pragma unroll 1
+  for (int e = 0; e < a.n - 1; ++e) {  // (not the last matrix: once its GEMM runs there is nothing left)
+    const long long o0 = a.off[e], o1 = a.off[e + 1];
+    const char* base = reinterpret_cast<const char*>(a.ptr[e]);
+#pragma unroll 1
+    for (long long r0 = o0; r0 < o1; r0 += 32 * kChunk) {  // rounds of 32 chunks, one per lane
+      const long long o = r0 + lane * kChunk;
+      const long long need = min(o1, r0 + 32 * kChunk) - 1;  // the round's last byte inside the window
+      bool skip = false;
+      while (need > limit) {
+        int p = 0;
+        if (lane == 0) asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(p) : "l"(a.progress) : "memory");
+        p = __shfl_sync(0xffffffffu, p, 0);
+        // the consumer is at the last matrix (nothing left worth fetching) or past this one
+        if (p >= a.n - 1) return;
+        if (p > e) {
+          skip = true;
+          break;
+        }
+        if (p != seen) {
+          seen = p;
+          limit = (p < 0 ? 0 : a.off[p]) + a.lookahead;
+        } else {
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          if (t - t0 > 50000000ull) return;  // never hold the step up: give up after 50 ms
+          __nanosleep(500);
+        }
+      }
+      if (skip) break;
+      if (o < o1) {
+        const long long sz = min(kChunk, o1 - o);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + (o - o0)), "r"((uint32_t)sz)
+                     : "memory");
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ scheduler (Alg. 1 loop body, Alg. 3)
 enum SchedState {
   ST_PHASE = 0,      // 0 prefix phase, 1 main phase
@@ -1325,6 +1385,7 @@ struct SchedArgs {
   int32_t* row_len;
   int32_t* attn_items;       // [Hkv * (nc_pre + row_cap * nc_suf)][kItemStride]
   int Hkv, nc_pre, nc_suf, chunk, tc_prefix;
+  int* pf_progress;          // L2 prefetcher pacing word: reset for the next step (nullable)
 };
 
 // Work list of one decode attention launch, built from the row tables by
@@ -1622,6 +1683,7 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
       }
     }
     if (any && consume) st0[ST_GSTEP] += 1;
+    if (consume && a.pf_progress) *a.pf_progress = -1;  // the next step's prefetcher starts from its first GEMM
     if (st0[ST_GLIVE] > st0[ST_GPEAK]) st0[ST_GPEAK] = st0[ST_GLIVE];
   }
 }

@@ -157,3 +157,22 @@ def test_dynamic_mode_plan_and_config_errors(lib):
         with pytest.raises(lib.InfsampError) as e:
             lib.is_plan(bad, [3] * 8)
         assert e.value.status == lib.IS_ERR_CONFIG
+
+
+def test_is_plan_bin_slots_bit_exact_vs_oracle(lib):
+    """bin_mode = slots (DESIGN R38): init heads, SJF queue and the g-bin loads
+    bit-exact against the oracle, incl. samples finished in a prefix phase."""
+    rng = np.random.default_rng(29)
+    for trial in range(200):
+        g = int(rng.choice([1, 2, 4, 8]))
+        G = g * int(rng.integers(1, 9))
+        true = gen_trace("math", G, 1024, int(rng.integers(1 << 30)))
+        pred = [int(x) for x in predict_lengths(true, "noisy", 0.3, seed=trial)]
+        fin = set(int(i) for i in np.nonzero(rng.random(G) < 0.2)[0]) if trial % 2 else set()
+        cfg = _cfg(lib, G, g, mode="infinite_slots")
+        got = lib.is_plan(cfg, pred, finished=[1 if i in fin else 0 for i in range(G)] if fin else None)
+        ref = planner.build_plan("infinite_slots", G, g, pred=pred, eps=0.1, finished=fin)
+        assert got["init"] == ref["init"], trial
+        assert got["queue"] == ref["queue"], trial
+        assert got["loads"] == ref["plan"]["loads"], trial
+        assert got["capacity"] == ref["plan"]["capacity"]

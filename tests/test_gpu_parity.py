@@ -96,12 +96,12 @@ def tiny(lib):
     w_dev = {k: v.cuda() for k, v in w.items()}
     budget = okv.prefix_bytes(TINY, 16) + 4 * 2 * okv.page_bytes(TINY, 16)  # config 1: "KV budget 4 slots"
     runs = {m: _run(lib, w_dev, prompt, true, pred, m, 2, budget=budget)
-            for m in ("naive", "fifo", "infinite", "fptas_only", "sjf_only")}
+            for m in ("naive", "fifo", "infinite", "fptas_only", "sjf_only", "infinite_slots")}
     runs["full"] = _run(lib, w_dev, prompt, true, pred, "full", 8)
     return dict(w=w, w_dev=w_dev, prompt=prompt, true=true, pred=pred, runs=runs, budget=budget)
 
 
-@pytest.mark.parametrize("mode", ["naive", "fifo", "infinite", "full", "fptas_only", "sjf_only"])
+@pytest.mark.parametrize("mode", ["naive", "fifo", "infinite", "full", "fptas_only", "sjf_only", "infinite_slots"])
 def test_tiny_schedule_bit_exact(tiny, mode):
     r = tiny["runs"][mode]
     ref = simulator.simulate(tiny["true"], mode, 2, pred=tiny["pred"], eps=0.1, page_tokens=16)
@@ -119,7 +119,7 @@ def test_tiny_schedule_bit_exact(tiny, mode):
 def test_tiny_token_streams_identical_across_modes(tiny):
     """Batch invariance (R12 iv): a uid's tokens do not depend on the schedule."""
     base = tiny["runs"]["infinite"]["tokens"]
-    for mode in ("naive", "fifo", "full", "fptas_only", "sjf_only"):
+    for mode in ("naive", "fifo", "full", "fptas_only", "sjf_only", "infinite_slots"):
         assert np.array_equal(tiny["runs"][mode]["tokens"], base), mode
     for i, L in enumerate(tiny["true"]):
         assert np.all(base[i, :L] >= 0) and np.all(base[i, :L] < TINY.vocab) and np.all(base[i, L:] == -1)
@@ -509,3 +509,17 @@ def test_tiny_row_capacity_32_decode_path(lib, tiny):
                 checked += 1
             t_of[uid] = t + 1
     assert checked > 0
+
+
+def test_tiny_bin_slots_with_prefix_phase(lib, tiny):
+    """bin_mode = slots after a k = 4 prefix phase (phase 1 runs Alg. 2 over g bins
+    on the materialised predictions; heads skip samples finished in the prefix phase, R38):
+    the schedule equals the oracle simulation and the tokens the trace-driven ones."""
+    pred = predict_lengths(tiny["true"], "noisy", 0.3, seed=1, prefix_k=4)
+    r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], pred, "infinite_slots", 2, budget=tiny["budget"],
+             prefix_k=4, pt=4)
+    ref = simulator.simulate(tiny["true"], "infinite_slots", 2, pred=pred, eps=0.1, prefix_k=4, page_tokens=4)
+    assert r["steps"] == ref.total_steps and r["stats"]["prefix_steps"] == ref.prefix_steps
+    assert r["slots"].tolist() == ref.slot_table
+    assert r["live"].tolist() == ref.live_pages
+    assert np.array_equal(r["tokens"], tiny["runs"]["infinite"]["tokens"])

@@ -353,3 +353,49 @@ def test_dynamic_slot_mode_pins():
         assert d.tokens_decoded == sum(lens[u] for u in d.finish_step) + part
     with pytest.raises(ValueError):
         simulator.simulate([3, 4], "fifo", 1, target=1)
+
+
+def test_bin_mode_slots_pins():
+    """SPEC.md l.175 / l.204 / l.255 (bin_mode = slots; NEXT-2, DESIGN R38): Alg. 2 runs over g bins
+    and slot j starts with bin j's head.  Hand-derived instance (G = 6, g = 2, eps = 1,
+    pred = true = [5, 1, 1, 1, 1, 1]): S = 10, K = eps*S/2 = 5, l~ = [1]*6, C~ = 3, first fit in
+    (l~ desc, id) order -> bins {0,1,2}, {3,4,5}; heads (0, 3); SJF queue over {1,2,4,5} by
+    (pred, id) = [1, 2, 4, 5]; slot 0 runs 0 for 5 steps while slot 1 runs 3, 1, 2, 4, 5 one step
+    each.  The groups reading (N = G/g = 3: K = 10/3, l~ = [2,1,1,1,1,1], C~ = 3 -> groups {0,1},
+    {2,3,4}, {5}) starts (0, 1) instead -- the two readings differ."""
+    pred = [5, 1, 1, 1, 1, 1]
+    p = planner.build_plan("infinite_slots", 6, 2, pred=pred, eps=1.0)
+    assert p["plan"]["groups"] == [[0, 1, 2], [3, 4, 5]] and p["plan"]["K"] == 5.0 and p["plan"]["capacity"] == 3
+    assert p["init"] == [0, 3] and p["queue"] == [1, 2, 4, 5]
+    q = planner.build_plan("infinite", 6, 2, pred=pred, eps=1.0)
+    assert q["plan"]["groups"] == [[0, 1], [2, 3, 4], [5]] and q["init"] == [0, 1]
+    r = simulator.simulate(pred, "infinite_slots", 2, pred=pred, eps=1.0)
+    assert r.total_steps == 5
+    assert r.slot_table == [[0, 3], [0, 1], [0, 2], [0, 4], [0, 5]]
+    # an empty bin (every member finished in the prefix phase) takes the SJF queue head
+    p2 = planner.build_plan("infinite_slots", 6, 2, pred=pred, eps=1.0, finished={3, 4, 5})
+    assert p2["init"] == [0, 1] and p2["queue"] == [2]
+    # with N = G/g == g the bins are Alg. 2's groups: same plan, heads = each group's first member
+    rng = np.random.default_rng(7)
+    for _ in range(50):
+        g = int(rng.integers(1, 5))
+        G = g * g
+        pr = [int(x) for x in rng.integers(1, 50, G)]
+        a = planner.build_plan("infinite_slots", G, g, pred=pr, eps=0.3)
+        b = planner.build_plan("infinite", G, g, pred=pr, eps=0.3)
+        assert a["plan"]["mask"] == b["plan"]["mask"]
+        for j, grp in enumerate(a["plan"]["groups"]):
+            if grp:
+                assert a["init"][j] == grp[0]
+    # schedule invariants on random traces: each sample runs exactly once, token conservation,
+    # steps >= the lower bound, peak pages <= g full-length samples
+    for trial in range(60):
+        g = int(rng.choice([1, 2, 4, 8]))
+        G = g * int(rng.integers(1, 6))
+        true = [int(x) for x in rng.integers(1, 200, G)]
+        pr = [max(1, int(t * (1 + 0.3 * rng.standard_normal()))) for t in true]
+        r = simulator.simulate(true, "infinite_slots", g, pred=pr, eps=0.1, page_tokens=16)
+        assert sorted(r.finish_step) == list(range(G))
+        assert r.tokens_decoded == sum(true)
+        assert r.total_steps >= simulator.step_lower_bound(true, g)
+        assert r.peak_pages <= g * -(-max(true) // 16)

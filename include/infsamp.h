@@ -91,6 +91,13 @@ typedef struct {
   int32_t bin_slots;       /* IS_MODE_INFINITE: 0 = Alg. 2 over N = G/g micro groups (the paper), 1 = over
                               g slot bins (SPEC bin_mode = slots; NEXT-2, DESIGN R38): slot j starts
                               with bin j's head, then Alg. 3 SJF refill.  is_plan_out.loads then has g entries */
+  int32_t admit_slots;     /* memory-aware admission by predicted length ("samples from future micro
+                              groups may be promoted early if they fit the current memory profile"; NEXT-2,
+                              DESIGN R41), IS_MODE_INFINITE with a KV budget: 0 = off; S > g = rows per step:
+                              slots 0..g-1 keep the worst-case reservation of R25, slots g..S-1 are elastic
+                              and share the rest of the budget's pages, admitting the SJF queue head when its
+                              predicted pages fit.  Needs prefix_k == 0, max_groups <= 1, bin_slots == 0.
+                              is_copy_schedule then has S columns; a stalled slot is logged as -2 - uid */
   float top_p;             /* nucleus sampling (DESIGN R36): 0 < top_p < 1 samples the
                               Gumbel-max token inside the top-p nucleus (integer-exact mass, fixed-
                               sequence exp); 0 or 1 = off (the paper's plain temperature sampling).
@@ -133,6 +140,7 @@ typedef struct {
   int32_t launches_per_step;      /* kernel launches in one decode step (the captured graph) */
   int32_t launches_per_prefill;   /* kernel launches of one is_prefill */
   int32_t discarded;      /* IS_MODE_DYNAMIC: samples in flight at the stop, discarded (R35) */
+  int32_t stalls;         /* admit_slots: slot-steps an elastic slot waited for a page (R41) */
 } is_stats;
 
 typedef struct is_ctx is_ctx;

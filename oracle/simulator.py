@@ -166,6 +166,127 @@ def simulate(true_len, mode, g, pred=None, eps=0.1, prefix_k=0, page_tokens=16, 
     return res
 
 
+def simulate_admit(true_len, g, S, pred, max_new, pool_pages, eps=0.1, page_tokens=16):
+    """Memory-aware admission by predicted length ("samples from future micro
+    groups may be promoted early if they fit the current memory profile"; NEXT-2, reading R41).
+
+    Alg. 1-3 as in `infinite` on slots 0..g-1 (guaranteed slots: each owns the worst-case
+    reservation W = ceil(max_new / page_tokens) pages of R25) plus S - g elastic slots that share
+    the rest of the page pool, E = pool_pages - g W pages.  Per step:
+      1. pages for the step's token, ascending slot: a guaranteed slot always gets its page; an
+         elastic one while the elastic slots hold < E pages; else the lowest idle guaranteed
+         slot adopts it now (its pages leave the elastic count) and it gets a guaranteed page;
+         else it STALLS (no token this step, keeps its pages; logged as -2 - uid);
+      2. every occupied, unstalled slot decodes one token;
+      3. finishes in ascending slot order (pages freed);
+      4. refill in ascending slot order: an idle guaranteed slot first adopts the stalled elastic
+         sample admitted earliest (it moves with its pages, which leave the elastic count), else pops
+         the SJF queue head; an idle elastic slot admits the queue head iff the elastic slots'
+         reservations sum(max(held, ceil(pred / pt))) plus ceil(pred_head / pt) fit E (SJF order
+         kept: a head that does not fit stops admission).
+    At the start the g slots take the plan's initial fill and the elastic slots are admitted as
+    in 4.  Live pages never exceed pool_pages; a stalled elastic sample is always adopted by the
+    next guaranteed slot that frees, so the run terminates.
+    """
+    true_len = [int(x) for x in true_len]
+    pred = [int(p) for p in pred]
+    G = len(true_len)
+    pt = page_tokens
+    W = -(-max_new // pt)
+    E = pool_pages - g * W
+    if not (g < S and G % g == 0 and E >= 0):
+        raise ValueError("IS_ERR_CONFIG: need g < S, G mod g == 0 and a pool of at least g worst-case slots")
+    res = SimResult()
+    p = build_plan("infinite", G, g, pred=pred, eps=eps)
+    res.init, res.queue, res.plan = p["init"], p["queue"], p["plan"]
+    q = list(p["queue"])
+    slot = [-1] * S
+    t = [0] * G
+    pages = [0] * G
+    seq = {}                      # uid -> admission order
+    nseq = [0]
+    finished = set()
+    step = 0
+
+    def place(s, uid, kind):
+        slot[s] = uid
+        seq[uid] = nseq[0]
+        nseq[0] += 1
+        res.events.append((step, s, uid, kind))
+
+    def elastic_reserved():
+        return sum(max(pages[u], -(-pred[u] // pt)) for u in slot[g:] if u >= 0)
+
+    def refill(stalled):
+        for s in range(S):
+            if slot[s] >= 0:
+                continue
+            if s < g:
+                cand = [e for e in range(g, S) if stalled[e] and slot[e] >= 0]
+                if cand:
+                    e = min(cand, key=lambda e: seq[slot[e]])
+                    slot[s], slot[e] = slot[e], -1
+                    stalled[e] = False
+                    res.events.append((step, s, slot[s], "adopt"))
+                elif q:
+                    place(s, q.pop(0), "refill")
+            elif q and elastic_reserved() + -(-pred[q[0]] // pt) <= E:
+                place(s, q.pop(0), "admit")
+
+    for s, uid in enumerate(p["init"]):
+        place(s, uid, "init")
+    refill([False] * S)
+    res.stalls = 0
+    while any(u >= 0 for u in slot):
+        step += 1
+        stalled = [False] * S
+        held_e = sum(pages[u] for u in slot[g:] if u >= 0)
+        for s in range(S):
+            uid = slot[s]
+            if uid < 0:
+                continue
+            if t[uid] % pt == 0:
+                if s < g:
+                    pages[uid] += 1
+                elif held_e < E:
+                    pages[uid] += 1
+                    held_e += 1
+                else:
+                    idle = [q for q in range(g) if slot[q] < 0]
+                    if idle:
+                        slot[idle[0]], slot[s] = uid, -1
+                        held_e -= pages[uid]
+                        pages[uid] += 1
+                        res.events.append((step, idle[0], uid, "adopt"))
+                    else:
+                        stalled[s] = True
+                        res.stalls += 1
+        for s in range(S):
+            uid = slot[s]
+            if uid >= 0 and not stalled[s] and t[uid] == 0 and uid not in res.start_step:
+                res.start_step[uid] = step
+        live = sum(pages)
+        res.live_pages.append(live)
+        res.peak_pages = max(res.peak_pages, live)
+        res.slot_table.append([(-2 - u if stalled[s] else u) if u >= 0 else -1 for s, u in enumerate(slot)])
+        for s in range(S):
+            if slot[s] >= 0 and not stalled[s]:
+                t[slot[s]] += 1
+                res.tokens_decoded += 1
+        for s in range(S):
+            uid = slot[s]
+            if uid >= 0 and not stalled[s] and t[uid] == true_len[uid]:
+                finished.add(uid)
+                res.finish_step[uid] = step
+                pages[uid] = 0
+                slot[s] = -1
+                res.events.append((step, s, uid, "finish"))
+        refill(stalled)
+    res.total_steps = step
+    assert len(finished) == G
+    return res
+
+
 def step_lower_bound(true_len, g):
     """max(max len, ceil(sum / g))."""
     return max(max(true_len), -(-sum(true_len) // g))

@@ -46,7 +46,7 @@ class Config(ctypes.Structure):
                 ("eps", ctypes.c_double), ("temperature", ctypes.c_float), ("seed", ctypes.c_uint64),
                 ("mode", ctypes.c_int32), ("decode_impl", ctypes.c_int32), ("max_groups", ctypes.c_int32),
                 ("dynamic_target", ctypes.c_int32), ("eos_enabled", ctypes.c_int32), ("eos_id", ctypes.c_int32),
-                ("bin_slots", ctypes.c_int32), ("top_p", ctypes.c_float)]
+                ("bin_slots", ctypes.c_int32), ("admit_slots", ctypes.c_int32), ("top_p", ctypes.c_float)]
 
 
 class PlanOut(ctypes.Structure):
@@ -67,7 +67,7 @@ class Stats(ctypes.Structure):
                 ("suffix_tokens", ctypes.c_int64),
                 ("groups", ctypes.c_int32), ("global_steps", ctypes.c_int64), ("global_peak_kv_bytes", ctypes.c_int64),
                 ("launches_per_step", ctypes.c_int32), ("launches_per_prefill", ctypes.c_int32),
-                ("discarded", ctypes.c_int32)]
+                ("discarded", ctypes.c_int32), ("stalls", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -156,7 +156,7 @@ def _np_ptr(a):
 
 def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix_k=0, page_tokens=16,
                 row_capacity=0, kv_budget_bytes=0, eps=0.1, temperature=0.8, seed=20261017,
-                max_groups=1, dynamic_target=0, top_p=1.0, eos_id=None):
+                max_groups=1, dynamic_target=0, top_p=1.0, eos_id=None, admit_slots=0):
     c = Config()
     c.shape = Shape(shape.layers, shape.hidden, shape.n_q_heads, shape.n_kv_heads, shape.head_dim, shape.ffn,
                     shape.vocab, shape.rms_eps, shape.rope_theta)
@@ -164,6 +164,7 @@ def make_config(shape, G, g, max_new_tokens, prompt_len, mode="infinite", prefix
     c.prefix_k, c.page_tokens, c.row_capacity = prefix_k, page_tokens, row_capacity
     c.kv_budget_bytes, c.eps, c.temperature, c.seed = kv_budget_bytes, eps, temperature, seed
     c.bin_slots = 0
+    c.admit_slots = admit_slots  # memory-aware admission by predicted length (DESIGN R41): 0 = off
     if mode == "infinite_slots":  # Alg. 2 over g slot bins (SPEC bin_mode = slots, DESIGN R38)
         mode, c.bin_slots = "infinite", 1
     c.mode = MODES[mode] if isinstance(mode, str) else int(mode)
@@ -307,7 +308,7 @@ class Context:
         L = load()
         self.cfg = cfg
         self.G = cfg.G
-        self.g = cfg.G if cfg.mode == MODES["full"] else cfg.g
+        self.g = cfg.G if cfg.mode == MODES["full"] else (cfg.admit_slots or cfg.g)  # slots per group
         ptrs = weight_pointer_list(weights, cfg.shape.layers)
         arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
         h = ctypes.c_void_p()

@@ -84,14 +84,21 @@ static is_status check_config(const is_config* c) {
   if (c->decode_impl != 0 && c->decode_impl != 1) return fail(IS_ERR_CONFIG, "decode_impl must be 0 or 1 (reserved)");
   if (c->bin_slots != 0 && (c->bin_slots != 1 || c->mode != IS_MODE_INFINITE))
     return fail(IS_ERR_CONFIG, "bin_slots must be 0 or 1 and needs IS_MODE_INFINITE");
+  if (c->admit_slots != 0 &&
+      (c->admit_slots <= g || c->admit_slots > 64 || c->mode != IS_MODE_INFINITE || c->prefix_k != 0 ||
+       n_groups(c) != 1 || c->bin_slots != 0 || c->kv_budget_bytes <= 0 || c->eos_enabled))
+    return fail(IS_ERR_CONFIG, "admit_slots needs g < S <= 64, IS_MODE_INFINITE, a KV budget, prefix_k == 0, "
+                               "max_groups <= 1, bin_slots == 0 and no EOS (R41)");
   if (c->max_groups < 0 || n_groups(c) > 8 || n_groups(c) * g > 64)
     return fail(IS_ERR_CONFIG, "need 1 <= max_groups <= 8 and max_groups * g <= 64 (got %d x %d)", n_groups(c), g);
   return IS_OK;
 }
 
 static int eff_g(const is_config* c) { return c->mode == IS_MODE_FULL ? c->G : c->g; }
+// rows per group slot: the micro-group size, or S with memory-aware admission (R41)
+static int slots_of(const is_config* c) { return c->admit_slots > 0 ? c->admit_slots : eff_g(c); }
 static int row_cap_of(const is_config* c) {
-  int rc = c->row_capacity > 0 ? c->row_capacity : ((n_groups(c) * eff_g(c) + 15) / 16) * 16;
+  int rc = c->row_capacity > 0 ? c->row_capacity : ((n_groups(c) * slots_of(c) + 15) / 16) * 16;
   return rc;
 }
 
@@ -484,7 +491,8 @@ struct LayerW {
 struct is_ctx {
   is_config cfg;
   is_shape sh;
-  int G, g, N, rc, BN, P, pcap, pt, maxp, max_new, num_pages, log_cap, max_rows, max_pos;
+  int G, g, gp, N, rc, BN, P, pcap, pt, maxp, max_new, num_pages, log_cap, max_rows, max_pos;
+  int32_t *pred, *adm_seq, *stall;  // memory-aware admission (R41): [M][G], [M][G], [M][g]
   int qkv_w;  // (Hq + 2 Hkv) * 128
   int64_t page_bytes, prefix_bytes;
   cudaStream_t st, user;
@@ -507,7 +515,8 @@ struct is_ctx {
   float *ssqA, *ssqB;  // [Th][max_rows] per-128-column sums of squares: QKV input, gate/up input
   int bnorm;           // decode: RMSNorm folded into the QKV / gate-up B operand
   int sep_merge;       // decode suffix: 64-token CTA units + separate merge kernel
-  int suffix_mma;      // decode suffix: 64-token units on mma.sync, fused merge (default)
+  int suffix_mma;      // decode suffix: 32-token units on mma.sync, merges spread over the grid (default)
+  int suffix_shape;    //   its CTA shape: 1 = 8 warps x 1 stage (rc <= 16), 0 = 6 warps x 2 stages
   CUtensorMap tm_pool; // the page pool of all layers as rows of 128 bf16, box = one page (128-byte swizzle)
   int stg_lm;          // lm_head ring depth override (IS_STG_LM = 10 / 11; default 8)
   int fuse_norm;       // decode: RMSNorm of the new residual fused into the o_proj / down epilogues
@@ -636,6 +645,13 @@ static SchedArgs sched_args(is_ctx* c) {
   a.chunk = c->sc;
   a.tc_prefix = c->tc_prefix;
   a.pf_progress = c->pf_lookahead > 0 ? c->pf_progress : nullptr;
+  a.admit = c->cfg.admit_slots > 0 ? 1 : 0;
+  a.gp = c->gp;
+  a.W = (int)ceil_div64(c->max_new, c->pt);
+  a.E = c->num_pages - c->gp * a.W;  // (one group: the pool beyond the guaranteed reservations)
+  a.pred = c->pred;
+  a.adm_seq = c->adm_seq;
+  a.stall = c->stall;
   return a;
 }
 
@@ -671,6 +687,7 @@ struct AttnLaunch {
   int grp_rows;                  // rows per group g
   const CUtensorMap* tm_pool;    // decode mma suffix pass: the page pool, rows of 128 bf16, box = page_tokens
   int suffix_mma;                // decode: suffix units on mma.sync (attn_suffix_mma_kernel)
+  int suffix_shape;              //   0: 6 warps x 2 stages, 1: 8 warps x 1 stage
 };
 
 template <int REP, int N>
@@ -718,13 +735,17 @@ static is_status launch_attn_rep(const AttnArgs& aa, const AttnLaunch& al, cudaS
     }
   }
   if (al.suffix_mma) {  // decode, 64-token units on mma.sync with the fused merge
+    const bool wide = al.suffix_shape == 1;  // 8 warps x 1 stage (small launches) vs 6 x 2
+#define IS_SUFFIX_MMA(P)                                                                                         \
+  (wide ? launch_k_smem(attn_suffix_mma_kernel<REP, P, 8, 1>, dim3(g_num_sms), dim3(256),                       \
+                        SuffixMmaSmem<8, 1>::v, st, *al.tm_pool, aa)                                           \
+        : launch_k_smem(attn_suffix_mma_kernel<REP, P, 6, 2>, dim3(g_num_sms), dim3(192),                       \
+                        SuffixMmaSmem<6, 2>::v, st, *al.tm_pool, aa))
     switch (aa.pt) {
-      case 8: CKS(launch_k_smem(attn_suffix_mma_kernel<REP, 8>, dim3(g_num_sms), dim3(kSThreads), SuffixMmaSmem::v,
-                                st, *al.tm_pool, aa)); break;
-      case 16: CKS(launch_k_smem(attn_suffix_mma_kernel<REP, 16>, dim3(g_num_sms), dim3(kSThreads),
-                                 SuffixMmaSmem::v, st, *al.tm_pool, aa)); break;
-      case 32: CKS(launch_k_smem(attn_suffix_mma_kernel<REP, 32>, dim3(g_num_sms), dim3(kSThreads),
-                                 SuffixMmaSmem::v, st, *al.tm_pool, aa)); break;
+      case 8: CKS(IS_SUFFIX_MMA(8)); break;
+      case 16: CKS(IS_SUFFIX_MMA(16)); break;
+      case 32: CKS(IS_SUFFIX_MMA(32)); break;
+#undef IS_SUFFIX_MMA
       default: return fail(IS_ERR_CONFIG, "the mma suffix pass needs page_tokens 8, 16 or 32");
     }
     return IS_OK;
@@ -865,6 +886,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       al.grp_rows = c->g;
       al.tm_pool = &c->tm_pool;
       al.suffix_mma = !prefill && c->suffix_mma;
+      al.suffix_shape = c->suffix_shape;
       CKS(launch_attention(aa, al, st));
     }
     prof_mark(st, 3);
@@ -1115,13 +1137,14 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->cfg = *cfg;
   c->sh = s;
   c->G = cfg->G;
-  c->g = eff_g(cfg);
+  c->g = slots_of(cfg);   // rows (slots) per group
+  c->gp = eff_g(cfg);     // the plan's micro-group size (guaranteed slots with admission, R41)
   c->M = n_groups(cfg);
   c->gprompt_id.assign(c->M, 0);
   c->gprompt_last.assign(c->M, 0);
   c->gprefilled.assign(c->M, 0);
   c->gstarted.assign(c->M, 0);
-  c->N = c->G / c->g;
+  c->N = c->G / c->gp;
   c->rc = row_cap_of(cfg);
   if (c->rc < c->g || c->rc > 64) {
     delete c;
@@ -1170,6 +1193,11 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
       c->sep_merge = 0;
   }
   c->sc = c->suffix_mma ? kSUnit : ((c->tc_prefix && !c->sep_merge) ? kSCW : kSC);
+  {
+    // suffix kernel shape: 8 warps x 1 stage up to 16 rows (each warp has ~1-2 units), else 6 x 2
+    const char* e = getenv("IS_SUFFIX_SHAPE");
+    c->suffix_shape = e ? atoi(e) : (c->rc <= 16 ? 1 : 0);
+  }
   c->nc_suf = (int)ceil_div64(c->max_new, c->sc);
   c->NC = c->nc_pre + c->nc_suf;
   // partials one LSE merge combines: decode = prefix tiles + suffix chunks, prefill = prefix chunks
@@ -1301,6 +1329,9 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->log_live = (int32_t*)A((size_t)M * c->log_cap * 4);
   c->logprobs = (float*)A((size_t)M * c->G * c->max_new * 4);
   c->done_flag = (uint8_t*)A((size_t)M * c->G);
+  c->pred = (int32_t*)A((size_t)M * c->G * 4);
+  c->adm_seq = (int32_t*)A((size_t)M * c->G * 4);
+  c->stall = (int32_t*)A((size_t)M * c->g * 4);
   c->d_prompt_copy = (int32_t*)A((size_t)c->P * 4);
   if (err != IS_OK) return err;
   CK(cudaMallocHost(&c->st_host, sizeof(long long) * ST_COUNT * (M + 1)));
@@ -1432,7 +1463,7 @@ extern "C" void is_destroy(is_ctx* c) {
                   c->row_t, c->row_tok, c->row_pos, c->row_kvloc, c->row_len, c->keys, c->last_tok,
                   c->last_fin, c->st_dev, c->slot_uid, c->slot_count, c->tpos, c->true_len, c->queue,
                   c->main_init, c->main_queue, c->free_stack, c->pagetab, c->npages, c->tokens, c->log_slot,
-                  c->log_live, c->d_prompt_copy, c->lp_key, c->lp_mlz, c->logprobs, c->done_flag, c->prow_active, c->prow_tok, c->prow_pos, c->prow_kvloc,
+                  c->log_live, c->d_prompt_copy, c->lp_key, c->lp_mlz, c->logprobs, c->done_flag, c->pred, c->adm_seq, c->stall, c->prow_active, c->prow_tok, c->prow_pos, c->prow_kvloc,
                   c->prow_len, c->fn_bar, c->logits_tp, c->scores_tp, c->ebits_tp, c->wpart_tp, c->hist_tp,
                   c->sel_tp, c->state_tp};
   for (void* p : bufs)
@@ -1512,13 +1543,13 @@ extern "C" is_status is_start_group_slot(is_ctx* c, int32_t m, const int32_t* tr
   if (m < 0 || m >= c->M) return fail(IS_ERR_CONFIG, "group slot %d out of range [0, %d)", m, c->M);
   if (!c->gprefilled[m]) return fail(IS_ERR_STATE, "is_start_group before is_prefill (slot %d)", m);
   StreamGuard guard(c, c->user);
-  const int G = c->G, g = c->g;
+  const int G = c->G, g = c->g;  // (g = slots per group: S with memory-aware admission, R41)
   for (int i = 0; i < G; ++i)
     if (true_len[i] < 1 || true_len[i] > c->max_new)
       return fail(IS_ERR_DATA, "true length of sample %d is %d (need 1..%d)", i, true_len[i], c->max_new);
   const int k = c->cfg.prefix_k;
-  std::vector<int32_t> pred_eff(G), mask(2 * G), ovf(G), init(g), queue(G);
-  std::vector<int64_t> sl(G), loads(c->N);
+  std::vector<int32_t> pred_eff(G), mask(2 * G), ovf(G), init(g, -1), queue(G);
+  std::vector<int64_t> sl(G), loads(std::max(c->N, c->gp));
   std::vector<uint8_t> fin(G, 0);
   for (int i = 0; i < G; ++i) {
     pred_eff[i] = pred ? pred[i] : true_len[i];
@@ -1563,6 +1594,12 @@ extern "C" is_status is_start_group_slot(is_ctx* c, int32_t m, const int32_t* tr
   }
   st[ST_PROMPT_ID] = c->gprompt_id[m];
   st[ST_PROMPT_LAST] = c->gprompt_last[m];
+  std::vector<int32_t> seq(G, 0);
+  if (c->cfg.admit_slots > 0) {  // R41: the plan's initial fill is admitted first, in slot order
+    for (int s = 0; s < c->gp; ++s)
+      if (init[s] >= 0) seq[init[s]] = s;
+    st[ST_ADMSEQ] = c->gp;
+  }
   const size_t oG = (size_t)m * G, og = (size_t)m * g;
   CK(cudaMemcpyAsync(c->st_dev + (size_t)m * ST_COUNT, st.data(), st.size() * 8, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(c->slot_uid + og, slots.data(), g * 4, cudaMemcpyHostToDevice, c->st));
@@ -1574,6 +1611,9 @@ extern "C" is_status is_start_group_slot(is_ctx* c, int32_t m, const int32_t* tr
   CK(cudaMemcpyAsync(c->main_queue + oG, queue.data(), G * 4, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemsetAsync(c->npages + oG, 0, G * 4, c->st));
   CK(cudaMemsetAsync(c->done_flag + oG, 0, G, c->st));
+  CK(cudaMemcpyAsync(c->pred + oG, pred_eff.data(), G * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->adm_seq + oG, seq.data(), G * 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemsetAsync(c->stall + og, 0, g * 4, c->st));
   CK(cudaMemsetAsync(c->tokens + oG * c->max_new, 0xFF, (size_t)G * c->max_new * 4, c->st));
   CK(cudaMemsetAsync(c->logprobs + oG * c->max_new, 0, (size_t)G * c->max_new * 4, c->st));
   CK(cudaMemsetAsync(c->log_slot + (size_t)m * c->log_cap * g, 0xFF, (size_t)c->log_cap * g * 4, c->st));
@@ -1691,6 +1731,7 @@ extern "C" is_status is_query_slot(is_ctx* c, int32_t m, is_stats* o) {
   o->prefix_steps = (int32_t)st[ST_PREFIX_STEPS];
   o->completed = (int32_t)st[ST_DONE];
   o->discarded = (int32_t)st[ST_DISCARDED];
+  o->stalls = (int32_t)st[ST_STALLS];
   o->live_pages = (int32_t)st[ST_LIVE];
   o->peak_pages = (int32_t)st[ST_PEAK];
   o->error = (int32_t)g0[ST_ERROR];
@@ -2014,6 +2055,7 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
     al.grp_rows = grp_rows;
     al.tm_pool = &tmp;
     al.suffix_mma = mma ? 1 : 0;
+    al.suffix_shape = getenv("IS_SUFFIX_SHAPE") ? atoi(getenv("IS_SUFFIX_SHAPE")) : (rows <= 16 ? 1 : 0);
     aa.pool_row0 = 0;
     aa.dbg_mode = getenv("IS_DBG_SUFFIX_MODE") ? atoi(getenv("IS_DBG_SUFFIX_MODE")) : 0;
     err = launch_attention(aa, al, st);

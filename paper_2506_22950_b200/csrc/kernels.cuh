@@ -282,6 +282,11 @@ __device__ __forceinline__ void attn_merge_one(const AttnArgs& a, int r, int h, 
     m1 = ml.x;
     l1 = ml.y;
   }
+  // the first 16 partial outputs do not depend on the weights: in flight with the (m, l) loads
+  float4 o[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    o[k] = k < n ? __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + k) * kHD) + lane) : make_float4(0, 0, 0, 0);
   const float M = warp_max(fmaxf(m0, m1));
   const float w0 = (lane < n && m0 != -INFINITY) ? expf(m0 - M) * l0 : 0.f;
   const float w1 = (lane + 32 < n && m1 != -INFINITY) ? expf(m1 - M) * l1 : 0.f;
@@ -289,11 +294,12 @@ __device__ __forceinline__ void attn_merge_one(const AttnArgs& a, int r, int h, 
   float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
   for (int i0 = 0; i0 < n; i0 += 16) {
-    float4 o[16];
+    if (i0 > 0) {
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
-      o[k] = i0 + k < n ? __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + i0 + k) * kHD) + lane)
-                        : make_float4(0, 0, 0, 0);
+      for (int k = 0; k < 16; ++k)
+        o[k] = i0 + k < n ? __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + i0 + k) * kHD) + lane)
+                          : make_float4(0, 0, 0, 0);
+    }
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
       const int i = i0 + k;
@@ -443,17 +449,18 @@ __global__ void __launch_bounds__(kAttnThreads) attn_suffix_warp_kernel(AttnArgs
 // ranges), the rest is claimed kSClaim units at a time (one atomic), so warps of CTAs that became
 // resident late (behind the prefix kernel's CTAs) just claim less.
 constexpr int kSUnit = 32;          // keys per unit
-constexpr int kSWarps = 6;          // warps per CTA (each its own ring)
-constexpr int kSWStages = 2;        // stages per warp
-constexpr int kSThreads = 32 * kSWarps;
+// Two shapes (template parameters NW warps x NST stages per warp): 6 x 2 (double-buffered; large
+// launches) and 8 x 1 (more units in flight at once when every warp has only one or two units,
+// e.g. one group of 16 rows).  The launcher picks by row capacity.
 constexpr int kSQueue = 6;          // work items loaded ahead of their issue
 constexpr int kSPublish = 8;        // units per release batch (one fence)
 constexpr int kSStaticPct = 50;     // share of the work list split statically over the warps
+template <int NW, int NST>
 struct SuffixMmaSmem {
   static constexpr int kKV = kSUnit * 2 * kHD * 2;    // K and V of one unit: 16 KB
   static constexpr int kQ = kMaxRep * kHD * 2;        // the row's query heads
   static constexpr int kStage = kKV + kQ;             // 18 KB, a multiple of 1024 (swizzle atoms)
-  static constexpr int v = kSWarps * kSWStages * kStage + 16 + kSWarps * kSWStages * 8 + 1024;
+  static constexpr int v = NW * NST * kStage + 16 + NW * NST * 8 + 1024;
 };
 
 IS_DEVICE void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
@@ -487,11 +494,12 @@ IS_DEVICE void tma_load_5d(void* dst, const CUtensorMap* m, uint64_t* bar, int c
       : "memory");
 }
 
-template <int REP, int PT>
-__global__ void __launch_bounds__(kSThreads, 1) attn_suffix_mma_kernel(const __grid_constant__ CUtensorMap tmPool,
-                                                                        AttnArgs a) {
+template <int REP, int PT, int NW, int NST>
+__global__ void __launch_bounds__(32 * NW, 1) attn_suffix_mma_kernel(const __grid_constant__ CUtensorMap tmPool,
+                                                                      AttnArgs a) {
   pdl_launch_dependents();
-  using SM = SuffixMmaSmem;
+  using SM = SuffixMmaSmem<NW, NST>;
+  constexpr int kSWarps = NW, kSWStages = NST;
   extern __shared__ uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
   uint4* zero16 = reinterpret_cast<uint4*>(sm + kSWarps * kSWStages * SM::kStage);  // Q padding rows
@@ -607,10 +615,10 @@ __global__ void __launch_bounds__(kSThreads, 1) attn_suffix_mma_kernel(const __g
     reinterpret_cast<uint4*>(wsm)[i] = make_uint4(0, 0, 0, 0);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the TMA writes
   __syncwarp();
-  static_assert(kSWStages == 2, "the consume loop is unrolled over two stages");
-  int hc0, hl0, hc1, hl1;  // per stage: the unit's code (-1: none) and row length
+  static_assert(kSWStages == 1 || kSWStages == 2, "the consume loop is unrolled over one or two stages");
+  int hc0, hl0, hc1 = -1, hl1 = 0;  // per stage: the unit's code (-1: none) and row length
   hc0 = issue(0, hl0);
-  hc1 = issue(1, hl1);
+  if (kSWStages == 2) hc1 = issue(1, hl1);
   int nq = (hc0 >= 0) + (hc1 >= 0);  // units issued
   // ---- consume in order; refill the freed stage
   const int g = lane >> 2, t4 = lane & 3, mi = lane >> 3, mr = lane & 7;
@@ -740,7 +748,7 @@ __global__ void __launch_bounds__(kSThreads, 1) attn_suffix_mma_kernel(const __g
 #pragma unroll 1
   for (int ph = 0;; ph ^= 1) {
     if (!consume(0, ph, hc0, hl0)) break;
-    if (!consume(1, ph, hc1, hl1)) break;
+    if (kSWStages == 2 && !consume(1, ph, hc1, hl1)) break;
   }
   publish();
   if (lane == 0) {
@@ -1342,6 +1350,8 @@ enum SchedState {
   ST_GSTEP,        // block 0 only: decode steps with >= 1 active slot in any group
   ST_TARGET,       // dynamic-slot mode: stop at this many completions (0 = all G), R35
   ST_DISCARDED,    //   samples in flight at the stop, discarded
+  ST_ADMSEQ,       // memory-aware admission (R41): next admission sequence number
+  ST_STALLS,       //   slot-steps stalled for a page
   ST_COUNT
 };
 // st[] holds one block of ST_COUNT words per co-resident group (NEXT-1) plus a
@@ -1386,6 +1396,12 @@ struct SchedArgs {
   int32_t* attn_items;       // [Hkv * (nc_pre + row_cap * nc_suf)][kItemStride]
   int Hkv, nc_pre, nc_suf, chunk, tc_prefix;
   int* pf_progress;          // L2 prefetcher pacing word: reset for the next step (nullable)
+  // memory-aware admission by predicted length (R41; admit = 1): slots 0..gp-1 are the plan's
+  // guaranteed slots, gp..g-1 elastic ones sharing E pages; W = worst-case pages per sample
+  int admit, gp, W, E;
+  const int32_t* pred;       // [M][G] predicted lengths
+  int32_t* adm_seq;          // [M][G] admission order
+  int32_t* stall;            // [M][g] slot stalled this step (no page for its token)
 };
 
 // Work list of one decode attention launch, built from the row tables by
@@ -1453,6 +1469,48 @@ __device__ void build_attn_worklist(const WorkList& w, int* s_cnt /* [65] */, in
   __syncthreads();
 }
 
+// R41 refill pass of group m (thread 0): ascending slot order; an idle guaranteed slot adopts the
+// stalled elastic sample admitted earliest (with its pages), else pops the SJF queue; an idle
+// elastic slot admits the queue head iff the elastic slots' reservations
+// sum(max(held, ceil(pred / pt))) plus the head's ceil(pred / pt) fit E pages.
+__device__ void admit_refill(const SchedArgs& a, long long* st, int m) {
+  int32_t* slot_uid = a.slot_uid + m * a.g;
+  int32_t* stall = a.stall + m * a.g;
+  const int32_t* queue = a.queue + (size_t)m * a.G;
+  const int32_t* pred = a.pred + (size_t)m * a.G;
+  int32_t* npages = a.npages + (size_t)m * a.G;
+  int32_t* seq = a.adm_seq + (size_t)m * a.G;
+  for (int s = 0; s < a.g; ++s) {
+    if (slot_uid[s] >= 0) continue;
+    if (s < a.gp) {
+      int best = -1;
+      for (int e = a.gp; e < a.g; ++e)
+        if (slot_uid[e] >= 0 && stall[e] && (best < 0 || seq[slot_uid[e]] < seq[slot_uid[best]])) best = e;
+      if (best >= 0) {
+        slot_uid[s] = slot_uid[best];
+        slot_uid[best] = -1;
+        stall[best] = 0;
+      } else if (st[ST_QHEAD] < st[ST_QLEN]) {
+        const int u = queue[st[ST_QHEAD]++];
+        slot_uid[s] = u;
+        seq[u] = (int32_t)st[ST_ADMSEQ]++;
+      }
+    } else if (st[ST_QHEAD] < st[ST_QLEN]) {
+      const int head = queue[st[ST_QHEAD]];
+      long long res = 0;
+      for (int e = a.gp; e < a.g; ++e) {
+        const int u = slot_uid[e];
+        if (u >= 0) res += max(npages[u], (pred[u] + a.pt - 1) / a.pt);
+      }
+      if (res + (pred[head] + a.pt - 1) / a.pt <= a.E) {
+        ++st[ST_QHEAD];
+        slot_uid[s] = head;
+        seq[head] = (int32_t)st[ST_ADMSEQ]++;
+      }
+    }
+  }
+}
+
 // One CTA of kSchedThreads.  The policy itself (finish / park / refill in
 // ascending slot order, R18; LIFO page recycling, R26) is sequential and runs
 // on thread 0; the per-row preparation of the next step and its attention work
@@ -1515,7 +1573,7 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
       if (consume) {
         for (int s = 0; s < a.g; ++s) {
           const int uid = slot_uid[s];
-          if (uid < 0) continue;
+          if (uid < 0 || (a.admit && a.stall[m * a.g + s])) continue;  // (a stalled slot decoded nothing)
           const int row = m * a.g + s;
           const uint32_t tok = 0xFFFFFFFFu - (uint32_t)(a.keys[row] & 0xFFFFFFFFull);
           tokens[(size_t)uid * a.max_new + tt_[uid]] = (int32_t)tok;
@@ -1525,7 +1583,7 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
         }
         for (int s = 0; s < a.g; ++s) {  // ascending slot index
           const int uid = slot_uid[s];
-          if (uid < 0) continue;
+          if (uid < 0 || (a.admit && a.stall[m * a.g + s])) continue;
           if (tt_[uid] == true_len[uid] || (a.eos_on && tokens[(size_t)uid * a.max_new + tt_[uid] - 1] == a.eos_id)) {
             st[ST_DONE] += 1;
             a.done_flag[(size_t)m * a.G + uid] = 1;
@@ -1558,9 +1616,11 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
           }
           slot_uid[s] = -1;
           slot_count[s] += 1;
-          if (!st[ST_BARRIER] && st[ST_QHEAD] < st[ST_QLEN] && (st[ST_QUOTA] == 0 || slot_count[s] < st[ST_QUOTA]))
+          if (!a.admit && !st[ST_BARRIER] && st[ST_QHEAD] < st[ST_QLEN] &&
+              (st[ST_QUOTA] == 0 || slot_count[s] < st[ST_QUOTA]))
             slot_uid[s] = queue[st[ST_QHEAD]++];
         }
+        if (a.admit) admit_refill(a, st, m);  // (R41: finishes first, then one refill pass)
         bool idle = true;
         for (int s = 0; s < a.g; ++s) idle = idle && slot_uid[s] < 0;
         if (st[ST_BARRIER] && idle && st[ST_QHEAD] < st[ST_QLEN]) {
@@ -1586,11 +1646,36 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
       // pages for rows crossing a page boundary, ascending slot order (LIFO shared stack);
       // only for groups being prepared (all of them after a step; the new group at its start)
       if ((prep_mask >> m) & 1) {
+        if (a.admit && !consume) admit_refill(a, st, m);  // the group's start: elastic admissions
+        int held_e = 0;  // pages held by the elastic slots (R41)
+        if (a.admit)
+          for (int e = a.gp; e < a.g; ++e)
+            if (slot_uid[e] >= 0) held_e += npages[slot_uid[e]];
         for (int s = 0; s < a.g; ++s) {
-          const int uid = slot_uid[s];
+          int uid = slot_uid[s];
+          if (a.admit) a.stall[m * a.g + s] = 0;
           if (uid < 0) continue;
           const int tt = tt_[uid];
           if (tt % a.pt == 0) {
+            if (a.admit && s >= a.gp) {
+              if (held_e >= a.E) {
+                // no elastic page: the lowest idle guaranteed slot adopts the sample now (its
+                // pages leave the elastic count), else it stalls this step
+                int gs = -1;
+                for (int q = 0; q < a.gp && gs < 0; ++q)
+                  if (slot_uid[q] < 0) gs = q;
+                if (gs < 0) {
+                  a.stall[m * a.g + s] = 1;
+                  st[ST_STALLS] += 1;
+                  continue;
+                }
+                slot_uid[gs] = uid;
+                slot_uid[s] = -1;
+                held_e -= npages[uid];
+              } else {
+                ++held_e;
+              }
+            }
             if (st0[ST_FREE_TOP] == 0) {
               // budget violated: the pool is exhausted.  No page is handed out (nothing may
               // alias another sample's KV); the flag stops every row from the next step on
@@ -1618,7 +1703,7 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
     const int s = tid;
     a.keys[s] = 0ull;
     const int m = s / a.g;
-    const int uid = (m < a.M && any) ? a.slot_uid[s] : -1;
+    const int uid = (m < a.M && any && !(a.admit && a.stall[s])) ? a.slot_uid[s] : -1;
     if (uid < 0) {
       a.row_active[s] = 0;
       a.row_uid[s] = 0;
@@ -1674,7 +1759,10 @@ __global__ void __launch_bounds__(kSchedThreads) sched_kernel(SchedArgs a, int c
       if (gany) {
         const long long step = st[ST_STEP];
         if (step < a.log_cap) {
-          for (int s = 0; s < a.g; ++s) a.log_slot[((size_t)m * a.log_cap + step) * a.g + s] = a.slot_uid[m * a.g + s];
+          for (int s = 0; s < a.g; ++s) {
+            const int u = a.slot_uid[m * a.g + s];  // (R41: a stalled slot is logged as -2 - uid)
+            a.log_slot[((size_t)m * a.log_cap + step) * a.g + s] = (a.admit && u >= 0 && a.stall[m * a.g + s]) ? -2 - u : u;
+          }
           a.log_live[(size_t)m * a.log_cap + step] = (int32_t)st[ST_LIVE];
         }
         st[ST_STEP] = step + 1;

@@ -523,3 +523,33 @@ def test_tiny_bin_slots_with_prefix_phase(lib, tiny):
     assert r["slots"].tolist() == ref.slot_table
     assert r["live"].tolist() == ref.live_pages
     assert np.array_equal(r["tokens"], tiny["runs"]["infinite"]["tokens"])
+
+
+@pytest.mark.parametrize("extra_pages,S,pred_noise", [(3, 4, 0.3), (1, 3, 0.6), (0, 4, 0.3), (6, 6, 0.8)])
+def test_tiny_memory_aware_admission(lib, tiny, extra_pages, S, pred_noise):
+    """Memory-aware admission (NEXT-2, DESIGN R41): g = 2 guaranteed slots + S - 2 elastic ones
+    sharing `extra_pages` pages beyond the R25 reservation.  The schedule (slot table with stalls
+    logged as -2 - uid, pages held per step), the stall count and peak KV equal the oracle's
+    simulate_admit; every sample's tokens equal the plain infinite run's (batch invariance)."""
+    true = tiny["true"]
+    pred = predict_lengths(true, "noisy", pred_noise, seed=3)
+    pb = okv.page_bytes(TINY, 16)
+    budget = tiny["budget"] + extra_pages * pb
+    cfg = lib.make_config(TINY, 8, 2, 32, 16, mode="infinite", page_tokens=16, kv_budget_bytes=budget, eps=0.1,
+                          temperature=0.8, seed=SEED, admit_slots=S)
+    ctx = lib.Context(cfg, tiny["w_dev"])
+    ctx.is_prefill(torch.as_tensor(tiny["prompt"], device="cuda"), 0)
+    ctx.is_start_group(true, pred)
+    steps = ctx.is_run_group()
+    st = ctx.is_query()
+    slots, live = ctx.is_copy_schedule()
+    toks = ctx.is_copy_tokens()
+    ctx.close()
+    pool = st["num_pages"]
+    ref = simulator.simulate_admit(true, 2, S, pred, max_new=32, pool_pages=pool, page_tokens=16)
+    assert steps == ref.total_steps
+    assert slots.tolist() == ref.slot_table
+    assert live.tolist() == ref.live_pages
+    assert st["stalls"] == ref.stalls and st["peak_pages"] == ref.peak_pages and st["error"] == 0
+    assert st["peak_kv_bytes"] <= budget
+    assert np.array_equal(toks, tiny["runs"]["infinite"]["tokens"])

@@ -399,3 +399,55 @@ def test_bin_mode_slots_pins():
         assert r.tokens_decoded == sum(true)
         assert r.total_steps >= simulator.step_lower_bound(true, g)
         assert r.peak_pages <= g * -(-max(true) // 16)
+
+
+def test_memory_aware_admission_pins():
+    """Memory-aware admission by predicted length (NEXT-2, DESIGN R41).
+    Hand-traced instance: true = pred = [5,3,4,2,6,1,2,2], g = 2 guaranteed + 2 elastic slots,
+    max_new = 8, 4-token pages -> W = 2 pages per worst-case sample, pool = 5 pages -> E = 1
+    elastic page.  Alg. 2 (N = 4, K = 0.625, l~ = [8,5,7,4,10,2,4,4], C~ = 11) gives groups
+    {4}, {0,7}, {2,3}, {1,6,5}: init (4, 0), SJF queue [5,3,6,7,1,2].  Slot 2 admits 5 (1 page
+    <= E), slot 3 cannot admit 3 (1 + 1 > E).  5 ends at step 1 -> slot 2 admits 3 (steps 2-3),
+    then 6 (steps 4-5); at step 5 sample 0 ends: slot 1 pops 7, slot 2 admits 1; 4 ends at
+    step 6 -> slot 0 pops 2; 7 ends at 7, 1 at 8, 2 at 10: 10 steps against 14 for plain Alg. 1-3."""
+    t = [5, 3, 4, 2, 6, 1, 2, 2]
+    r = simulator.simulate_admit(t, 2, 4, t, max_new=8, pool_pages=5, page_tokens=4)
+    assert r.slot_table == [[4, 0, 5, -1], [4, 0, 3, -1], [4, 0, 3, -1], [4, 0, 6, -1], [4, 0, 6, -1],
+                            [4, 7, 1, -1], [2, 7, 1, -1], [2, -1, 1, -1], [2, -1, -1, -1], [2, -1, -1, -1]]
+    assert r.total_steps == 10 and r.stalls == 0
+    assert simulator.simulate(t, "infinite", 2, pred=t, page_tokens=4).total_steps == 14
+    # a mispredicted elastic sample outgrows the elastic pool: it stalls, then a guaranteed slot
+    # adopts it with its pages (true 8 but predicted 1: admitted on a 1-page reservation)
+    t2, p2 = [8, 8, 8, 1], [8, 8, 1, 1]
+    r2 = simulator.simulate_admit(t2, 1, 2, p2, max_new=8, pool_pages=3, page_tokens=4)
+    assert r2.stalls > 0 and any(k == "adopt" for *_, k in r2.events)
+    assert any(u <= -2 for row in r2.slot_table for u in row[1:])          # logged stalls
+    assert all(u >= -1 for row in r2.slot_table for u in row[:1])           # never in a guaranteed slot
+    assert r2.peak_pages <= 3 and r2.tokens_decoded == sum(t2)
+    # E = 0 (a pool of exactly g worst-case samples): nothing is admitted, Alg. 1-3 exactly
+    rng = np.random.default_rng(11)
+    for _ in range(40):
+        g = int(rng.choice([1, 2, 4]))
+        G = g * int(rng.integers(1, 6))
+        mx = int(rng.integers(4, 64))
+        true = [int(x) for x in rng.integers(1, mx + 1, G)]
+        pr = [max(1, int(x * (1 + 0.3 * rng.standard_normal()))) for x in true]
+        a = simulator.simulate_admit(true, g, g + 2, pr, max_new=mx, pool_pages=g * -(-mx // 8), page_tokens=8)
+        b = simulator.simulate(true, "infinite", g, pred=pr, page_tokens=8)
+        assert [row[:g] for row in a.slot_table] == b.slot_table
+        assert all(row[g:] == [-1, -1] for row in a.slot_table) and a.live_pages == b.live_pages
+    # random instances: the budget is a hard invariant, every sample runs once, no dead step
+    for _ in range(300):
+        g = int(rng.choice([1, 2, 4]))
+        S = g + int(rng.integers(1, 5))
+        G = g * int(rng.integers(1, 6))
+        mx = int(rng.integers(4, 64))
+        pt = int(rng.choice([4, 8, 16]))
+        true = [int(x) for x in rng.integers(1, mx + 1, G)]
+        pr = [max(1, int(x * (1 + 0.4 * rng.standard_normal()))) for x in true]
+        W = -(-mx // pt)
+        pool = g * W + int(rng.integers(0, 3 * W))
+        r = simulator.simulate_admit(true, g, S, pr, max_new=mx, pool_pages=pool, page_tokens=pt)
+        assert r.peak_pages <= pool and max(r.live_pages) <= pool
+        assert r.tokens_decoded == sum(true) and sorted(r.finish_step) == list(range(G))
+        assert all(any(u >= 0 for u in row) for row in r.slot_table)

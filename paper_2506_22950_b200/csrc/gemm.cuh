@@ -554,15 +554,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       } else if constexpr (EPI == EPI_SAMPLE) {
         const bool lp = a.lp_key != nullptr;
-        for (int n = 0; n < min(BN, a.n_valid); ++n) {
+        const int nv = min(BN, a.n_valid);
+        // Philox4x32-10 yields 4 words per counter (v >> 2, t, uid): the 4 lanes of a quad (the same
+        // v >> 2) compute one call each, for 4 different rows, and swap words by shuffles
+        uint32_t pw[4] = {0u, 0u, 0u, 0u};
+        for (int n = 0; n < nv; ++n) {
+          if ((n & 3) == 0) {
+            const int nq = n + (lane & 3);
+            if (nq < nv) {
+              const Philox4 o = philox4x32_10((uint32_t)gm >> 2, (uint32_t)a.row_t[a.row0 + nq],
+                                              (uint32_t)a.row_uid[a.row0 + nq], 0u, (uint32_t)a.seed,
+                                              (uint32_t)(a.seed >> 32));
+              pw[0] = o.x[0];
+              pw[1] = o.x[1];
+              pw[2] = o.x[2];
+              pw[3] = o.x[3];
+            }
+          }
+          const int src = (lane & ~3) | (n & 3);  // the quad lane holding row n's words
+          const uint32_t x0 = __shfl_sync(0xffffffffu, pw[0], src), x1 = __shfl_sync(0xffffffffu, pw[1], src);
+          const uint32_t x2 = __shfl_sync(0xffffffffu, pw[2], src), x3 = __shfl_sync(0xffffffffu, pw[3], src);
           if (!a.row_active[a.row0 + n]) continue;
           unsigned long long key = 0ull;
           float z = -INFINITY;
           if (gm < a.M) {
             z = stg[n * kBM + m];
             if (a.logits_dump) a.logits_dump[(size_t)(a.row0 + n) * a.ld_out + gm] = z;
-            const float g = gumbel(a.seed, (uint32_t)a.row_uid[a.row0 + n], (uint32_t)a.row_t[a.row0 + n],
-                                   (uint32_t)gm);
+            const uint32_t wv = (gm & 3) == 0 ? x0 : ((gm & 3) == 1 ? x1 : ((gm & 3) == 2 ? x2 : x3));
+            const float g = -logf_is(-logf_is(uniform_from_bits(wv)));  // = gumbel(seed, uid, t, gm)
             const float sc = __fadd_rn(__fmul_rn(z, a.inv_temp), g);
             if (a.score_dump) a.score_dump[(size_t)(a.row0 + n) * a.ld_out + gm] = sc;
             key = order_key(sc, (uint32_t)gm);

@@ -282,10 +282,12 @@ __device__ __forceinline__ void attn_merge_one(const AttnArgs& a, int r, int h, 
     m1 = ml.x;
     l1 = ml.y;
   }
-  // the first 16 partial outputs do not depend on the weights: in flight with the (m, l) loads
-  float4 o[16];
+  // the first 32 partial outputs do not depend on the weights: in flight with the (m, l) loads
+  // (one L2 round trip for up to 32 partials)
+  constexpr int B = 32;
+  float4 o[B];
 #pragma unroll
-  for (int k = 0; k < 16; ++k)
+  for (int k = 0; k < B; ++k)
     o[k] = k < n ? __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + k) * kHD) + lane) : make_float4(0, 0, 0, 0);
   const float M = warp_max(fmaxf(m0, m1));
   const float w0 = (lane < n && m0 != -INFINITY) ? expf(m0 - M) * l0 : 0.f;
@@ -293,15 +295,15 @@ __device__ __forceinline__ void attn_merge_one(const AttnArgs& a, int r, int h, 
   const float den = warp_sum(w0) + warp_sum(w1);
   float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
-  for (int i0 = 0; i0 < n; i0 += 16) {
+  for (int i0 = 0; i0 < n; i0 += B) {
     if (i0 > 0) {
 #pragma unroll
-      for (int k = 0; k < 16; ++k)
+      for (int k = 0; k < B; ++k)
         o[k] = i0 + k < n ? __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + i0 + k) * kHD) + lane)
                           : make_float4(0, 0, 0, 0);
     }
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
+    for (int k = 0; k < B; ++k) {
       const int i = i0 + k;
       const float wa = __shfl_sync(0xffffffffu, w0, i & 31), wb = __shfl_sync(0xffffffffu, w1, i & 31);
       const float w = i < 32 ? wa : wb;

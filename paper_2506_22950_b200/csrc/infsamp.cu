@@ -517,6 +517,7 @@ struct is_ctx {
   int sep_merge;       // decode suffix: 64-token CTA units + separate merge kernel
   int suffix_mma;      // decode suffix: 32-token units on mma.sync, merges spread over the grid (default)
   int suffix_shape;    //   its CTA shape: 1 = 8 warps x 1 stage (rc <= 16), 0 = 6 warps x 2 stages
+  int prefix2;         // tcgen05 prefix with the query rows as M (default; up to 256 stacked rows)
   CUtensorMap tm_pool; // the page pool of all layers as rows of 128 bf16, box = one page (128-byte swizzle)
   int stg_lm;          // lm_head ring depth override (IS_STG_LM = 10 / 11; default 8)
   int fuse_norm;       // decode: RMSNorm of the new residual fused into the o_proj / down epilogues
@@ -688,6 +689,7 @@ struct AttnLaunch {
   const CUtensorMap* tm_pool;    // decode mma suffix pass: the page pool, rows of 128 bf16, box = page_tokens
   int suffix_mma;                // decode: suffix units on mma.sync (attn_suffix_mma_kernel)
   int suffix_shape;              //   0: 6 warps x 2 stages, 1: 8 warps x 1 stage
+  int prefix2;                   // decode tcgen05 prefix with the query rows as M (attn_prefix_tc2_kernel)
 };
 
 template <int REP, int N>
@@ -724,9 +726,46 @@ static is_status launch_prefix_tc_n(const AttnArgs& aa, const AttnLaunch& al, cu
 // MMA N of the tcgen05 prefix part: one group's live slots x Hq/Hkv query heads, padded to 16.
 static int prefix_cols(int g, int rep) { return (int)ceil_div64((int64_t)g * rep, 16) * 16; }
 
+template <int REP, int MT>
+static is_status launch_prefix_tc2(const AttnArgs& aa, const AttnLaunch& al, cudaStream_t st) {
+  using SM = PrefixTc2Smem<MT>;
+  auto kern = attn_prefix_tc2_kernel<REP, MT>;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::v));
+    attr = true;
+  }
+  const int nt = (int)ceil_div64(aa.plen, 128);
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  cfg.gridDim = dim3(al.groups * aa.Hkv * nt);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = SM::v;
+  cfg.stream = st;
+  cfg.numAttrs = 0;
+  if (g_use_pdl) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  AttnArgs a2 = aa;
+  a2.dbg_ts = aa.dbg_ts ? aa.dbg_ts + (size_t)2 * 296 * 16 : nullptr;
+  a2.grp_rows = al.grp_rows;
+  a2.grp_kv_rows = al.grp_kv_rows;
+  CK(cudaLaunchKernelEx(&cfg, kern, *al.tm_prefix, a2, al.kv_row_base));
+  ++g_launches;
+  return IS_OK;
+}
+
 template <int REP>
 static is_status launch_attn_rep(const AttnArgs& aa, const AttnLaunch& al, cudaStream_t st) {
-  if (aa.tc_prefix) {
+  if (aa.tc_prefix && al.prefix2) {
+    const int nrows = al.grp_rows * REP;
+    if (nrows <= 128) CKS((launch_prefix_tc2<REP, 1>(aa, al, st)));
+    else if (nrows <= 256) CKS((launch_prefix_tc2<REP, 2>(aa, al, st)));
+    else return fail(IS_ERR_CONFIG, "tcgen05 prefix attention needs g * Hq/Hkv <= 256");
+  } else if (aa.tc_prefix) {
     switch (prefix_cols(al.grp_rows, REP)) {
       case 16: CKS((launch_prefix_tc_n<REP, 16>(aa, al, st))); break;
       case 32: CKS((launch_prefix_tc_n<REP, 32>(aa, al, st))); break;
@@ -887,6 +926,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       al.tm_pool = &c->tm_pool;
       al.suffix_mma = !prefill && c->suffix_mma;
       al.suffix_shape = c->suffix_shape;
+      al.prefix2 = c->prefix2;
       CKS(launch_attention(aa, al, st));
     }
     prof_mark(st, 3);
@@ -1178,7 +1218,13 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->nc_pre = (int)ceil_div64(c->pcap, kPC);  // prefill (CUDA-core causal prefix units)
   {
     const int N = prefix_cols(c->g, s.n_q_heads / s.n_kv_heads);
-    c->tc_prefix = (N == 16 || N == 32 || N == 64) && !getenv("IS_NO_TC_PREFIX");
+    // round 1's tokens-as-M kernel up to 64 stacked rows (its softmax spreads a tile's tokens over
+    // all 128 threads: 5.9 vs 8.3 us at 16 rows), the query-rows-as-M kernel beyond (up to 256;
+    // 1.7x the CUDA-core prefix at 128 rows); IS_PREFIX_IMPL=2 forces the latter
+    const char* pe = getenv("IS_PREFIX_IMPL");
+    c->prefix2 = (pe && atoi(pe) == 2) || N > 64;
+    c->tc_prefix = (c->prefix2 ? c->g * (s.n_q_heads / s.n_kv_heads) <= 256 : (N == 16 || N == 32 || N == 64)) &&
+                   !getenv("IS_NO_TC_PREFIX");
     c->nc_pre_dec = c->tc_prefix ? (int)ceil_div64(c->pcap, 128) : c->nc_pre;
   }
   // decode suffix pass behind the tcgen05 prefix: 64-token units on mma.sync with the fused
@@ -1958,7 +2004,7 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
   if (!d_q || !d_prefix || !d_pool || !d_pagetab || !d_row_len || !d_out) return fail(IS_ERR_CONFIG, "null argument");
   if (rows < 1 || rows > 64 || groups < 1 || grp_rows < 1 || groups * grp_rows > rows || plen < 1 || Hkv < 1 ||
       Hq % Hkv || Hq / Hkv > kMaxRep || page_tokens < 4 || 64 % page_tokens || maxp < 1 || num_pages < 1 ||
-      impl < 0 || impl > 4 || reps < 0 || (reps > 0 && !h_ms))
+      impl < 0 || impl > 6 || reps < 0 || (reps > 0 && !h_ms))
     return fail(IS_ERR_CONFIG, "bad is_dbg_attn arguments");
   if (!g_num_sms) {
     int dev = 0;
@@ -1966,11 +2012,17 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
     CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
   }
   const int rep = Hq / Hkv;
-  const bool tc_ok = prefix_cols(grp_rows, rep) <= 64;
+  // impl 5 / 6: as 0 / 4 with the query-rows-as-M prefix kernel forced (0 / 4 take it only beyond 64
+  // stacked rows, as the decode step does)
+  const bool force2 = impl == 5 || impl == 6 || (getenv("IS_PREFIX_IMPL") && atoi(getenv("IS_PREFIX_IMPL")) == 2);
+  if (impl == 5) impl = 0;
+  if (impl == 6) impl = 4;
+  const bool old_prefix = !force2 && prefix_cols(grp_rows, rep) <= 64;
+  const bool tc_ok = grp_rows * rep <= 256;
   const bool tc = impl == 0 ? tc_ok : impl != 3;
   const bool mma = impl == 0 ? tc_ok && page_tokens % 8 == 0 && page_tokens <= kSUnit : impl == 4;
   const bool sep = impl == 2 || impl == 3 || (impl == 0 && !mma && (!tc || page_tokens > kSCW));
-  if (tc && !tc_ok) return fail(IS_ERR_CONFIG, "tcgen05 prefix needs grp_rows * Hq/Hkv <= 64");
+  if (tc && !tc_ok) return fail(IS_ERR_CONFIG, "tcgen05 prefix needs grp_rows * Hq/Hkv <= 256 (64: impl 5/6)");
   if (mma && (page_tokens % 8 || page_tokens > kSUnit))
     return fail(IS_ERR_CONFIG, "the mma suffix pass needs page_tokens in {8, 16, 32}");
   if (!tc && groups != 1) return fail(IS_ERR_CONFIG, "the CUDA-core prefix serves one group");
@@ -2056,6 +2108,7 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
     al.tm_pool = &tmp;
     al.suffix_mma = mma ? 1 : 0;
     al.suffix_shape = getenv("IS_SUFFIX_SHAPE") ? atoi(getenv("IS_SUFFIX_SHAPE")) : (rows <= 16 ? 1 : 0);
+    al.prefix2 = old_prefix ? 0 : 1;
     aa.pool_row0 = 0;
     aa.dbg_mode = getenv("IS_DBG_SUFFIX_MODE") ? atoi(getenv("IS_DBG_SUFFIX_MODE")) : 0;
     err = launch_attention(aa, al, st);

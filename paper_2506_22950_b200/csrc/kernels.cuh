@@ -1323,6 +1323,206 @@ __global__ void __launch_bounds__(32) l2_prefetch_kernel(PrefetchArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ shared-prefix attention on tcgen05, q rows as M
+// The same contraction as attn_prefix_tc_kernel with the group's stacked query rows as the MMA's M
+// (128 per tile, MT tiles: up to 256 rows, e.g. the 4B shape with all 64 samples live):
+//   S[q][tok] = Q[q][:] . K_tile[tok][:]^T        (A = Q, K-major; B = K tile, K-major; N = 128 tokens)
+//   O[q][d]   = P[q][tok] . V_tile[tok][d]          (A = P, K-major; B = V tile, MN-major; N = 128 dims)
+// Each thread owns one query row's TMEM lane, so the row softmax (max, exp, sum over the tile's
+// 128 tokens) is in registers with no cross-thread reduction; P (bf16 hi/lo pair, ~2^-16) is
+// written over the Q / K tiles MMA 1 no longer needs, so one 128-row tile needs 96 KB of shared
+// memory.  One CTA per (group, kv head, 128-token prefix tile); the partial (o, m, l) of every
+// live query row goes to prefix partial slot `tile`.
+template <int MT>
+struct PrefixTc2Smem {
+  static constexpr int kTile = 2 * 128 * 128;  // [128 rows][128 bf16] as two 64-column halves: 32 KB
+  static constexpr int v = (MT == 1 ? 3 : 5) * kTile + 64 + 1024;
+  static constexpr int kTmemCols = MT == 1 ? 256 : 512;
+};
+
+template <int REP, int MT>
+__global__ void __launch_bounds__(128, 1)
+    attn_prefix_tc2_kernel(const __grid_constant__ CUtensorMap tmKV, AttnArgs a, int kv_row_base) {
+  using SMc = PrefixTc2Smem<MT>;
+  constexpr int T = SMc::kTile, HALF = T / 2;
+  extern __shared__ uint8_t tc2_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc2_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* Qs0 = sm;
+  uint8_t* Qs1 = sm + T;                 // (MT == 2)
+  uint8_t* Ks = sm + MT * T;
+  uint8_t* Vs = Ks + T;
+  uint8_t* Xs = Vs + T;                  // (MT == 2)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + (MT == 1 ? 3 : 5) * T);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt = (a.plen + 127) / 128;
+  const int grp = blockIdx.x / (a.Hkv * nt);
+  const int h = (blockIdx.x / nt) % a.Hkv, tile = blockIdx.x % nt;
+  const int row0 = grp * a.grp_rows;
+  kv_row_base += grp * a.grp_kv_rows;
+  const int tok0 = tile * 128, ntok = min(128, a.plen - tok0);
+  const int nrows = a.grp_rows * REP;  // stacked query rows n = (row - row0) * REP + e
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmKV);
+    mbar_init(&bars[0], 1);  // TMA K + V
+    mbar_init(&bars[1], 1);  // MMA commits (phase 0: S, phase 1: O)
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<SMc::kTmemCols>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  astamp(a, 0);
+  if (threadIdx.x == 0) {
+    // the shared prefix KV is immutable after is_prefill: staged BEFORE the wait on the QKV GEMM
+    const int rk = kv_row_base + (0 * a.Hkv + h) * a.pcap + tok0;
+    const int rv = kv_row_base + (1 * a.Hkv + h) * a.pcap + tok0;
+    mbar_arrive_expect_tx(&bars[0], 2 * T);
+    tma_load_2d(Ks, &tmKV, &bars[0], 0, rk, kEvictNormal);
+    tma_load_2d(Ks + HALF, &tmKV, &bars[0], 64, rk, kEvictNormal);
+    tma_load_2d(Vs, &tmKV, &bars[0], 0, rv, kEvictNormal);
+    tma_load_2d(Vs + HALF, &tmKV, &bars[0], 64, rv, kEvictNormal);
+  }
+  pdl_wait();  // q of this step comes from the QKV GEMM
+  astamp(a, 1);
+  pdl_launch_dependents();
+  // Q rows (K-major, 128-byte swizzle): row n of tile n >> 7, 16-B chunk c (dims 8c..8c+7)
+  for (int i = threadIdx.x; i < nrows * 16; i += 128) {
+    const int n = i >> 4, c = i & 15;
+    const int r = row0 + n / REP, e = n % REP, nl = n & 127;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < a.rows && a.row_active[r]) v = *reinterpret_cast<const uint4*>(a.q + ((size_t)r * a.Hq + h * REP + e) * kHD + c * 8);
+    uint8_t* dst = ((MT == 2 && n >= 128) ? Qs1 : Qs0) + (c >> 3) * HALF + nl * 128;
+    *reinterpret_cast<uint4*>(dst + (((c & 7) ^ (nl & 7)) << 4)) = v;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  astamp(a, 2);
+  if (threadIdx.x == 0) {
+    mbar_wait(&bars[0], 0);
+    astamp(a, 3);
+    tc_fence_after();
+    constexpr uint32_t idesc = idesc_bf16_f32(128, 128);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      if (mt * 128 >= nrows) break;
+      uint8_t* Q = mt == 0 ? Qs0 : Qs1;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {  // 128 dims in steps of 16
+        const uint64_t da = smem_desc_k_sw128(Q + (k >> 2) * HALF) + 2 * (k & 3);
+        const uint64_t db = smem_desc_k_sw128(Ks + (k >> 2) * HALF) + 2 * (k & 3);
+        tc_mma_f16(tmem + mt * 128, da, db, idesc, k > 0 ? 1u : 0u);
+      }
+    }
+    tc_commit(&bars[1]);
+  }
+  __syncwarp();
+  mbar_wait(&bars[1], 0);
+  astamp(a, 4);
+  tc_fence_after();
+  // ---- row softmax in registers: thread = TMEM lane = query row nl of each tile
+  const int nl = warp * 32 + lane;
+  float mrow[MT], lrow[MT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    mrow[mt] = -INFINITY;
+    lrow[mt] = 0.f;
+    if (mt * 128 + warp * 32 >= nrows) continue;  // (warp-uniform) no live row in this warp
+    uint32_t sv[128];
+    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16) + mt * 128;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) tmem_ld32_nowait(trow + 32 * j, sv + 32 * j);
+    tmem_ld_wait();
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 128; ++j) {
+      const float x = j < ntok ? __uint_as_float(sv[j]) * a.scale : -INFINITY;
+      sv[j] = __float_as_uint(x);
+      mx = fmaxf(mx, x);
+    }
+    float l = 0.f;
+    uint8_t* Ph = mt == 0 ? Qs0 : Ks;
+    uint8_t* Pl = mt == 0 ? (MT == 1 ? Ks : Qs1) : Xs;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {  // 8 tokens per 16-B chunk
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float p0 = expf(__uint_as_float(sv[8 * c + 2 * q]) - mx);
+        const float p1 = expf(__uint_as_float(sv[8 * c + 2 * q + 1]) - mx);
+        l += p0 + p1;
+        const __nv_bfloat162 hb = __floats2bfloat162_rn(p0, p1);
+        const float2 hf = __bfloat1622float2(hb);
+        hi[q] = *reinterpret_cast<const uint32_t*>(&hb);
+        lo[q] = pack_bf16(p0 - hf.x, p1 - hf.y);
+      }
+      const int off = (c >> 3) * HALF + nl * 128 + (((c & 7) ^ (nl & 7)) << 4);
+      *reinterpret_cast<uint4*>(Ph + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4*>(Pl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+    mrow[mt] = mx;
+    lrow[mt] = l;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  astamp(a, 5);
+  if (threadIdx.x == 0) {
+    tc_fence_after();
+    constexpr uint32_t idesc2 = idesc_bf16_f32(128, 128) | (1u << 16);  // B (V) MN-major
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      if (mt * 128 >= nrows) break;
+      uint8_t* Ph = mt == 0 ? Qs0 : Ks;
+      uint8_t* Pl = mt == 0 ? (MT == 1 ? Ks : Qs1) : Xs;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {  // 128 tokens in steps of 16
+        const uint64_t db = smem_desc_mn_sw128(Vs + k * 2048, HALF, 1024);
+        const uint64_t dh = smem_desc_k_sw128(Ph + (k >> 2) * HALF) + 2 * (k & 3);
+        const uint64_t dl = smem_desc_k_sw128(Pl + (k >> 2) * HALF) + 2 * (k & 3);
+        tc_mma_f16(tmem + MT * 128 + mt * 128, dh, db, idesc2, k > 0 ? 1u : 0u);
+        tc_mma_f16(tmem + MT * 128 + mt * 128, dl, db, idesc2, 1u);
+      }
+    }
+    tc_commit(&bars[1]);
+  }
+  __syncwarp();
+  mbar_wait(&bars[1], 1);
+  astamp(a, 6);
+  tc_fence_after();
+  // ---- epilogue: row nl's normalised partial (o, m, l) into prefix slot `tile`
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    if (mt * 128 + warp * 32 >= nrows) continue;
+    const int n = mt * 128 + nl;
+    const int r = row0 + n / REP, e = n % REP;
+    const bool live = n < nrows && r < a.rows && a.row_active[r];
+    uint32_t ov[128];
+    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16) + MT * 128 + mt * 128;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) tmem_ld32_nowait(trow + 32 * j, ov + 32 * j);
+    tmem_ld_wait();
+    if (live) {
+      const size_t pidx = ((size_t)r * a.Hq + h * REP + e) * a.NC + tile;
+      const float inv = 1.0f / lrow[mt];
+      float4* po = reinterpret_cast<float4*>(a.part_o + pidx * kHD);
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        po[j] = make_float4(__uint_as_float(ov[4 * j]) * inv, __uint_as_float(ov[4 * j + 1]) * inv,
+                            __uint_as_float(ov[4 * j + 2]) * inv, __uint_as_float(ov[4 * j + 3]) * inv);
+      *reinterpret_cast<float2*>(a.part_ml + pidx * 2) = make_float2(mrow[mt], lrow[mt]);
+    }
+  }
+  astamp(a, 7);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<SMc::kTmemCols>(tmem);
+  }
+}
+
 // ------------------------------------------------------------------ scheduler (Alg. 1 loop body, Alg. 3)
 enum SchedState {
   ST_PHASE = 0,      // 0 prefix phase, 1 main phase

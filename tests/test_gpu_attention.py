@@ -128,11 +128,12 @@ def test_split_attention_default_impl(lib, rows, groups, grp_rows, plen):
     _check(lib, rows, groups, grp_rows, plen, 16, 8, lens, 0, seed=rows * 1000 + plen)
 
 
-@pytest.mark.parametrize("impl", [1, 2, 3, 4])
+@pytest.mark.parametrize("impl", [1, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("rows,groups,grp_rows", [(16, 1, 8), (16, 1, 16), (64, 8, 8)])
 def test_split_attention_every_impl(lib, impl, rows, groups, grp_rows):
     """Each launch variant on every layout it serves (1 warp units, 2 CTA units + merge kernel,
-    3 = CUDA-core prefix: one group, 4 = mma.sync units)."""
+    3 = CUDA-core prefix: one group, 4 = mma.sync units; 5 / 6 = 0 / 4 with the query-rows-as-M
+    prefix kernel forced instead of the tokens-as-M one)."""
     if impl == 3 and groups > 1:
         pytest.skip("the CUDA-core prefix serves one group")
     lens = _lens(rows, groups, grp_rows, rot=impl)
@@ -165,7 +166,7 @@ def test_split_attention_errors(lib):
     with pytest.raises(InfsampError):
         lib.is_dbg_attn(dev[0], dev[1], dev[2], dev[3], bad_len, grp_rows=8)
     with pytest.raises(InfsampError):
-        lib.is_dbg_attn(*dev, grp_rows=8, impl=5)
+        lib.is_dbg_attn(*dev, grp_rows=8, impl=7)
 
 
 @pytest.mark.parametrize("pt", [4, 8, 32, 64])
@@ -174,3 +175,12 @@ def test_split_attention_page_sizes(lib, pt):
     4 falls back to the warp units, 64 to the 64-token CTA units + merge kernel."""
     lens = _lens(16, 1, 16, rot=pt)
     _check(lib, 16, 1, 16, 255, 16, 8, lens, 0, seed=pt, pt=pt)
+
+
+@pytest.mark.parametrize("Hq,Hkv,grp_rows,impl", [(16, 8, 64, 0), (32, 8, 64, 0), (32, 8, 32, 0), (16, 8, 64, 3)])
+def test_split_attention_large_groups(lib, Hq, Hkv, grp_rows, impl):
+    """One group's rows stacked beyond round 1's 64-row tcgen05 limit: 64 rows x 2 heads (128 query
+    rows, one M tile), the 4B shape with 64 live rows x 4 heads (256 rows, two M tiles; SURVEY §8d
+    "R_h = 256"), and the CUDA-core prefix on the same layout."""
+    lens = _lens(64, 1, grp_rows, rot=grp_rows + Hq)
+    _check(lib, 64, 1, grp_rows, 255, Hq, Hkv, lens, impl, seed=grp_rows * 7 + Hq)

@@ -16,6 +16,8 @@ from paper_2506_22950_b200 import _lib  # noqa: E402
 
 
 def case(rows, groups, grp_rows, plen, lens, Hq=16, Hkv=8, pt=16, max_new=1024, impl=0, reps=20, seed=0):
+    if os.environ.get("K5_SHAPE") == "4b":
+        Hq, Hkv = 32, 8
     gen = torch.Generator(device="cuda").manual_seed(seed)
     maxp = math.ceil(max_new / pt)
     q = torch.randn(rows, Hq, 128, device="cuda", generator=gen).to(torch.bfloat16)
@@ -57,6 +59,7 @@ def main():
         ("groups8_math", 64, 8, 8, 255, math_lens(64)),
         ("groups8_t512", 64, 8, 8, 255, [512] * 64),
         ("groups8_t1024", 64, 8, 8, 255, [1024] * 64),
+        ("full64_t512", 64, 1, 64, 255, [512] * 64),
     ]
     for impl in [int(x) for x in args.impls.split(",")]:
         for name, rows, groups, grp, plen, lens in cases:

@@ -20,8 +20,11 @@ data = []
 for r in rows[2:]:
     if len(r) < len(h):
         continue
-    n = int(r[idx["Warp Stall Sampling (All Samples)"]] or 0)
-    rs = {k: int(r[idx[k]] or 0) for k in reasons}
+    try:
+        n = int(r[idx["Warp Stall Sampling (All Samples)"]] or 0)
+        rs = {k: int(r[idx[k]] or 0) for k in reasons}
+    except ValueError:  # a repeated header (several kernels in one report)
+        continue
     for k in reasons:
         tot[k] += rs[k]
     data.append((n, r[idx["Address"]][-5:], r[idx["Source"]].strip(), r[idx["Instructions Executed"]], rs))

@@ -1155,9 +1155,10 @@ __global__ void __launch_bounds__(128, 1)
     float sv[32], r[32];
     tmem_ld16(trow + c32 * 32, sv);
     if (ncol > 16) tmem_ld16(trow + c32 * 32 + 16, sv + 16);
+    const float sl2 = a.scale * 1.4426950408889634f;  // scores in log2 units: exp2 below
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      sv[j] = (valid && j < ncol) ? sv[j] * a.scale : -INFINITY;
+      sv[j] = (valid && j < ncol) ? sv[j] * sl2 : -INFINITY;
       r[j] = sv[j];
     }
     // transpose-max: after the step with offset o, lanes with bit o hold the upper half
@@ -1180,7 +1181,7 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const float Mj = __shfl_sync(0xffffffffu, mcol, j);
-      p[j] = (valid && j < ncol) ? expf(sv[j] - Mj) : 0.f;
+      p[j] = (valid && j < ncol) ? exp2f(sv[j] - Mj) : 0.f;
       r[j] = p[j];
     }
 #pragma unroll
@@ -1208,7 +1209,7 @@ __global__ void __launch_bounds__(128, 1)
     __syncthreads();
     if (threadIdx.x < ncol) {
       const int n = c32 * 32 + threadIdx.x;
-      colM[n] = mcol;  // (thread x < 32 is lane x of warp 0: its mcol is column x)
+      colM[n] = mcol * 0.6931471805599453f;  // natural units (thread x < 32 is lane x of warp 0: column x)
       sbuf[8 * 64 + n] = sbuf[128 + threadIdx.x] + sbuf[160 + threadIdx.x] + sbuf[192 + threadIdx.x] + sbuf[224 + threadIdx.x];
     }
     __syncthreads();
@@ -1354,6 +1355,7 @@ __global__ void __launch_bounds__(128, 1)
   uint8_t* Xs = Vs + T;                  // (MT == 2)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + (MT == 1 ? 3 : 5) * T);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+  __shared__ uint8_t live_n[256];  // stacked row n is a live row of the group
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = (a.plen + 127) / 128;
   const int grp = blockIdx.x / (a.Hkv * nt);
@@ -1387,14 +1389,31 @@ __global__ void __launch_bounds__(128, 1)
   pdl_wait();  // q of this step comes from the QKV GEMM
   astamp(a, 1);
   pdl_launch_dependents();
-  // Q rows (K-major, 128-byte swizzle): row n of tile n >> 7, 16-B chunk c (dims 8c..8c+7)
-  for (int i = threadIdx.x; i < nrows * 16; i += 128) {
-    const int n = i >> 4, c = i & 15;
-    const int r = row0 + n / REP, e = n % REP, nl = n & 127;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < a.rows && a.row_active[r]) v = *reinterpret_cast<const uint4*>(a.q + ((size_t)r * a.Hq + h * REP + e) * kHD + c * 8);
-    uint8_t* dst = ((MT == 2 && n >= 128) ? Qs1 : Qs0) + (c >> 3) * HALF + nl * 128;
-    *reinterpret_cast<uint4*>(dst + (((c & 7) ^ (nl & 7)) << 4)) = v;
+  for (int n = threadIdx.x; n < nrows; n += 128) {
+    const int r = row0 + n / REP;
+    live_n[n] = r < a.rows && a.row_active[r];
+  }
+  // Q rows (K-major, 128-byte swizzle): row n of tile n >> 7, 16-B chunk c (dims 8c..8c+7); a
+  // thread's chunks are loaded 16 at a time (all in flight), then stored
+  for (int i0 = 0; i0 < nrows * 16; i0 += 16 * 128) {
+    uint4 v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int i = i0 + j * 128 + threadIdx.x;
+      const int n = i >> 4, c = i & 15;
+      const int r = row0 + n / REP, e = n % REP;
+      v[j] = (i < nrows * 16 && r < a.rows)
+                 ? *reinterpret_cast<const uint4*>(a.q + ((size_t)r * a.Hq + h * REP + e) * kHD + c * 8)
+                 : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int i = i0 + j * 128 + threadIdx.x;
+      if (i >= nrows * 16) break;
+      const int n = i >> 4, c = i & 15, nl = n & 127;
+      uint8_t* dst = ((MT == 2 && n >= 128) ? Qs1 : Qs0) + (c >> 3) * HALF + nl * 128;
+      *reinterpret_cast<uint4*>(dst + (((c & 7) ^ (nl & 7)) << 4)) = v[j];
+    }
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
@@ -1424,7 +1443,7 @@ __global__ void __launch_bounds__(128, 1)
   // ---- row softmax in registers: thread = TMEM lane = query row nl of each tile
   const int nl = warp * 32 + lane;
   float mrow[MT], lrow[MT];
-#pragma unroll
+#pragma unroll 1
   for (int mt = 0; mt < MT; ++mt) {
     mrow[mt] = -INFINITY;
     lrow[mt] = 0.f;
@@ -1434,10 +1453,12 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
     for (int j = 0; j < 4; ++j) tmem_ld32_nowait(trow + 32 * j, sv + 32 * j);
     tmem_ld_wait();
+    // scores in log2 units (scale * log2 e folded): p = exp2(x - max) = exp(score * scale - m)
+    const float sl2 = a.scale * 1.4426950408889634f;
     float mx = -INFINITY;
 #pragma unroll
     for (int j = 0; j < 128; ++j) {
-      const float x = j < ntok ? __uint_as_float(sv[j]) * a.scale : -INFINITY;
+      const float x = j < ntok ? __uint_as_float(sv[j]) * sl2 : -INFINITY;
       sv[j] = __float_as_uint(x);
       mx = fmaxf(mx, x);
     }
@@ -1449,8 +1470,8 @@ __global__ void __launch_bounds__(128, 1)
       uint32_t hi[4], lo[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const float p0 = expf(__uint_as_float(sv[8 * c + 2 * q]) - mx);
-        const float p1 = expf(__uint_as_float(sv[8 * c + 2 * q + 1]) - mx);
+        const float p0 = exp2f(__uint_as_float(sv[8 * c + 2 * q]) - mx);
+        const float p1 = exp2f(__uint_as_float(sv[8 * c + 2 * q + 1]) - mx);
         l += p0 + p1;
         const __nv_bfloat162 hb = __floats2bfloat162_rn(p0, p1);
         const float2 hf = __bfloat1622float2(hb);
@@ -1461,7 +1482,7 @@ __global__ void __launch_bounds__(128, 1)
       *reinterpret_cast<uint4*>(Ph + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
       *reinterpret_cast<uint4*>(Pl + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
-    mrow[mt] = mx;
+    mrow[mt] = mx * 0.6931471805599453f;  // back to natural units: the partial's m (R8)
     lrow[mt] = l;
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1491,28 +1512,44 @@ __global__ void __launch_bounds__(128, 1)
   mbar_wait(&bars[1], 1);
   astamp(a, 6);
   tc_fence_after();
-  // ---- epilogue: row nl's normalised partial (o, m, l) into prefix slot `tile`
-#pragma unroll
+  // ---- epilogue: row nl's normalised partial (o, m, l) into prefix slot `tile`.  The rows are
+  // staged in shared memory (the spent Q / K / P tiles, 64 KB per 128 rows) so that each 512-B
+  // partial row is written by a whole warp (coalesced), not by one thread.
+  float* ost = reinterpret_cast<float*>(sm);  // [128][132] fp32 (padded rows)
+#pragma unroll 1
   for (int mt = 0; mt < MT; ++mt) {
-    if (mt * 128 + warp * 32 >= nrows) continue;
-    const int n = mt * 128 + nl;
-    const int r = row0 + n / REP, e = n % REP;
-    const bool live = n < nrows && r < a.rows && a.row_active[r];
-    uint32_t ov[128];
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16) + MT * 128 + mt * 128;
+    if (mt * 128 >= nrows) break;
+    if (mt * 128 + warp * 32 < nrows) {
+      uint32_t ov[128];
+      const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16) + MT * 128 + mt * 128;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) tmem_ld32_nowait(trow + 32 * j, ov + 32 * j);
-    tmem_ld_wait();
-    if (live) {
-      const size_t pidx = ((size_t)r * a.Hq + h * REP + e) * a.NC + tile;
+      for (int j = 0; j < 4; ++j) tmem_ld32_nowait(trow + 32 * j, ov + 32 * j);
+      tmem_ld_wait();
       const float inv = 1.0f / lrow[mt];
-      float4* po = reinterpret_cast<float4*>(a.part_o + pidx * kHD);
 #pragma unroll
       for (int j = 0; j < 32; ++j)
-        po[j] = make_float4(__uint_as_float(ov[4 * j]) * inv, __uint_as_float(ov[4 * j + 1]) * inv,
-                            __uint_as_float(ov[4 * j + 2]) * inv, __uint_as_float(ov[4 * j + 3]) * inv);
-      *reinterpret_cast<float2*>(a.part_ml + pidx * 2) = make_float2(mrow[mt], lrow[mt]);
+        *reinterpret_cast<float4*>(ost + nl * 132 + 4 * j) =
+            make_float4(__uint_as_float(ov[4 * j]) * inv, __uint_as_float(ov[4 * j + 1]) * inv,
+                        __uint_as_float(ov[4 * j + 2]) * inv, __uint_as_float(ov[4 * j + 3]) * inv);
     }
+    __syncthreads();
+    // warp w writes rows w, w + 4, ...: lane = 16-B piece of the row
+    for (int rl = warp; rl < 128 && mt * 128 + rl < nrows; rl += 4) {
+      const int n = mt * 128 + rl;
+      const int r = row0 + n / REP, e = n % REP;
+      if (!live_n[n]) continue;
+      const size_t pidx = ((size_t)r * a.Hq + h * REP + e) * a.NC + tile;
+      reinterpret_cast<float4*>(a.part_o + pidx * kHD)[lane] = *reinterpret_cast<const float4*>(ost + rl * 132 + 4 * lane);
+    }
+    {
+      const int n = mt * 128 + nl;
+      const int r = row0 + n / REP, e = n % REP;
+      if (n < nrows && live_n[n]) {
+        const size_t pidx = ((size_t)r * a.Hq + h * REP + e) * a.NC + tile;
+        *reinterpret_cast<float2*>(a.part_ml + pidx * 2) = make_float2(mrow[mt], lrow[mt]);
+      }
+    }
+    __syncthreads();
   }
   astamp(a, 7);
   tc_fence_before();

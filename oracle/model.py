@@ -15,7 +15,9 @@ blocks, per-head RMSNorm on q and k, rotate-half RoPE (theta 1e6), GQA
 (q head h reads kv head h // (Hq/Hkv)), SwiGLU MLP, tied lm_head, no biases.
 
 `mirror=True` rounds to bf16 exactly where the GPU path stores bf16
-(reading R12): r1 normalised activations before every GEMM,
+(reading R12): r1 the operand of every GEMM that follows an RMSNorm,
+which is x*gain, the 1/rms row scale applied to the GEMM's product (R12b:
+RMSNorm(x) W^T = rs * ((x*gain) W^T), rs = 1/sqrt(mean(x^2) + eps)),
 r2 q/k/v after QK-norm + RoPE (what the KV cache holds), r4 attention output,
 r5 SiLU(gate)*up.  `mirror=False` is the pure fp64 model (pinned against the
 HF transformers Qwen3 implementation in tests/test_oracle_model.py).
@@ -40,6 +42,11 @@ def round_bf16(x):
 def rmsnorm(x, gain, eps):
     """x / sqrt(mean(x^2) + eps) * gain over the last axis."""
     return x / np.sqrt(np.mean(x * x, axis=-1, keepdims=True) + eps) * gain
+
+
+def rms_scale(x, eps):
+    """rs = 1 / sqrt(mean(x^2) + eps) per row (the RMSNorm scale), shape [..., 1]."""
+    return 1.0 / np.sqrt(np.mean(x * x, axis=-1, keepdims=True) + eps)
 
 
 def rope_cos_sin(positions, head_dim, theta):
@@ -99,10 +106,11 @@ def forward(weights, shape, tokens, mirror=True, logit_rows=None, trace=None):
     rep = S.n_q_heads // S.n_kv_heads
     for l in range(S.layers):
         w = {k.split(".")[-1]: v for k, v in weights.items() if k.startswith(f"layers.{l}.")}
-        h = rb(rmsnorm(x, _f64(w["in_norm"]), S.rms_eps))
-        q = (h @ _f64(w["wq"]).T).reshape(n, S.n_q_heads, S.head_dim)
-        k = (h @ _f64(w["wk"]).T).reshape(n, S.n_kv_heads, S.head_dim)
-        v = (h @ _f64(w["wv"]).T).reshape(n, S.n_kv_heads, S.head_dim)
+        # RMSNorm(x) W^T = rs * ((x * gain) W^T) (R12b; equal in exact arithmetic)
+        rs, h = rms_scale(x, S.rms_eps), rb(x * _f64(w["in_norm"]))
+        q = (rs * (h @ _f64(w["wq"]).T)).reshape(n, S.n_q_heads, S.head_dim)
+        k = (rs * (h @ _f64(w["wk"]).T)).reshape(n, S.n_kv_heads, S.head_dim)
+        v = (rs * (h @ _f64(w["wv"]).T)).reshape(n, S.n_kv_heads, S.head_dim)
         q = rmsnorm(q, _f64(w["q_norm"]), S.rms_eps)
         k = rmsnorm(k, _f64(w["k_norm"]), S.rms_eps)
         q, k, v = rb(rope(q, cos, sin)), rb(rope(k, cos, sin)), rb(v)
@@ -110,14 +118,14 @@ def forward(weights, shape, tokens, mirror=True, logit_rows=None, trace=None):
         if trace is not None:
             trace[f"{l}.q"], trace[f"{l}.k"], trace[f"{l}.v"], trace[f"{l}.attn"] = q, k, v, a
         x = x + a @ _f64(w["wo"]).T
-        h2 = rb(rmsnorm(x, _f64(w["post_norm"]), S.rms_eps))
-        act = rb(silu(h2 @ _f64(w["w_gate"]).T) * (h2 @ _f64(w["w_up"]).T))
+        rs2, h2 = rms_scale(x, S.rms_eps), rb(x * _f64(w["post_norm"]))
+        act = rb(silu(rs2 * (h2 @ _f64(w["w_gate"]).T)) * (rs2 * (h2 @ _f64(w["w_up"]).T)))
         x = x + act @ _f64(w["w_down"]).T
         if trace is not None:
             trace[f"{l}.resid"] = x.copy()
     rows = np.arange(n) if logit_rows is None else np.asarray(logit_rows)
-    hf = rb(rmsnorm(x[rows], _f64(weights["final_norm"]), S.rms_eps))
-    return hf @ _f64(E).T
+    xr = x[rows]
+    return rms_scale(xr, S.rms_eps) * (rb(xr * _f64(weights["final_norm"])) @ _f64(E).T)
 
 
 def generate(weights, shape, prompt, uid, true_len, seed, T=0.8, mirror=True):

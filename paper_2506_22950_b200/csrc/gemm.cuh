@@ -16,11 +16,20 @@
 // (coalesced float4 stores), one cluster barrier (release / acquire) orders
 // them, and each rank sums its column slice over ranks 0..split-1 in rank order
 // (deterministic; no atomics).  With split == 1 the kernel is persistent over
-// tiles and double-buffers the TMEM accumulator.
+// tiles and double-buffers the TMEM accumulator.  (Measured slower: the last
+// rank to count in on a per-tile counter reducing and finishing the whole tile
+// alone -- one CTA's L2 pull of all partials plus the whole tile's epilogue.)
+//
+// RMSNorm (R12b): a GEMM whose input is a normalised activation reads B =
+// bf16(x * gain) (written by the producer's epilogue, or by embed_kernel for
+// layer 0) and scales its fp32 accumulator by rs[row] = 1/sqrt(mean(x^2)+eps),
+// from the producer's per-128-column sums of squares (rs_ssq): no RMSNorm
+// kernel and no grid barrier between the residual update and its consumer.
 //
 // Epilogues (fused, no extra pass over HBM):
 //   EPI_QKV        per-head RMSNorm of q/k + RoPE + bf16 q / KV-cache append (R12 r2)
-//   EPI_RESID_ADD  out[row][m] += acc                    (o_proj, down: fp32 residual)
+//   EPI_RESID_ADD  out[row][m] += acc                    (o_proj, down: fp32 residual; optionally
+//                  the next norm's operand bf16(x * gain) and per-(tile, row) sums of squares)
 //   EPI_SWIGLU     act[row][f]  = bf16(silu(g) * u)      (gate|up interleaved per 64 rows; R12 r5)
 //   EPI_SAMPLE     keys[row] = max(key(z*invT + Gumbel)) (lm_head + Philox Gumbel-max sampler)
 //   EPI_STORE_F32  out[row][m]  = acc                    (test hook)
@@ -70,26 +79,17 @@ struct GemmArgs {
   uint64_t seed;
   float inv_temp;
   QkvEpiArgs qkv;
-  float* partials;              // split-K workspace [clusters][split][128][BN] fp32 (L2-resident)
+  float* partials;             // split-K workspace [tiles][split][128][BN] fp32 (L2-resident)
   unsigned long long* dbg_ts;  // optional [gridDim][16] globaltimer stamps (probe)
-  // RMSNorm folded into the B operand (decode QKV / gate-up): B rows are computed in
-  // shared memory as bf16(resid[row][k] * rs[row] * gain[k]) (rounding point r1), with
-  // rs[row] = 1/sqrt(sum_t ssq[t][row] / K + eps) from the producer's per-tile partials.
-  const float* bn_resid;       // [rows][K] fp32 (null: B comes from tmB)
-  const float* bn_ssq;         // [bn_tsq][bn_ld] per-128-column sums of squares
-  const __nv_bfloat16* bn_gain;  // [K]
-  int bn_tsq, bn_ld;
-  float bn_eps;
-  float* ssq_out;              // EPI_RESID_ADD: per-(tile, row) sums of squares of the new residual [tiles][bn_ld]
-  // RMSNorm of the new residual fused into EPI_RESID_ADD (needs ssq_out; one tile per CTA):
-  // after a grid barrier every CTA reads the row's per-tile sums of squares (fixed order) and
-  // writes fn_out[row][m] = bf16(x * rs * fn_gain[m]) for its own outputs (rounding point r1)
-  const float* fn_gain;
-  __nv_bfloat16* fn_out;       // [rows][M]
-  unsigned int* fn_bar;        // [2] arrival counter, generation
-  float fn_eps;
-  int* zero;                   // optional: words zeroed once the previous kernel completed
-  int zero_n;                  //   (the persistent decode kernel's dependency counters)
+  // RMSNorm consumer (R12b): acc[row] *= rs[row] = 1/sqrt(sum_t rs_ssq[t][row] / K + eps)
+  const float* rs_ssq;         // [rs_nt][rs_ld] the producer's per-128-column sums of squares (null: no norm)
+  int rs_nt, rs_ld;
+  float rs_eps;
+  // RMSNorm producer (EPI_RESID_ADD): the next norm's B operand and its sums of squares
+  const float* xg_gain;        // [M] next norm's gain (null: no xg_out)
+  __nv_bfloat16* xg_out;       // [rows][M] bf16(x * gain)
+  float* ssq_out;              // [tiles][ssq_ld] per-(tile, row) sum of x^2 of the new residual
+  int ssq_ld;
   int* pf_progress;            // optional: the L2 weight prefetcher's pacing word (l2_prefetch_kernel):
   int pf_seq;                  //   this GEMM's index in the step's weight order, written at launch
 };
@@ -118,32 +118,6 @@ __device__ __forceinline__ void stamp(const GemmArgs& a, int i) {
 
 __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + expf(-x)); }
 
-// One-shot grid barrier for a grid whose CTAs are all co-resident (called by one thread per
-// CTA after a CTA barrier; release / acquire at gpu scope; bounded: 2 s, then __trap).
-__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int n) {
-  unsigned int gen;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
-  __threadfence();
-  const unsigned int old = atomicAdd(bar, 1u);
-  if (old == n - 1) {
-    atomicExch(bar, 0u);
-    __threadfence();
-    atomicAdd(bar + 1, 1u);
-  } else {
-    unsigned long long t0, t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    while (true) {
-      unsigned int g;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
-      if (g != gen) break;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > 2000000000ull) __trap();
-    }
-  }
-  __threadfence();
-}
-
-
 template <int BN, int EPI, int STAGES>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_swapab_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -152,19 +126,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_base = smem;
-  float* aux = reinterpret_cast<float*>(smem + STAGES * C::kStage);  // split-K receive buffer, then exchange
+  float* aux = reinterpret_cast<float*>(smem + STAGES * C::kStage);  // epilogue staging
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * C::kStage + C::kAux);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* redbar = tempty + 2;    // (unused by the pull reduction; kept for layout)
-  uint64_t* consumed = redbar + 1;  // split-K: S-1 peers finished reading our partials
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(consumed + 1);
-  uint64_t* bready = consumed + 2;  // B_NORM: [8] k-blocks [8j, 8j + 8) of the B buffer are filled
-  // B_NORM buffer: [kb1 - kb0][BN][64] bf16, 128-byte swizzled, after the 1 KB barrier block
-  uint8_t* bbuf = smem + STAGES * C::kStage + C::kAux + 1024;
-  const bool bnorm = a.bn_resid != nullptr;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ unsigned long long skey[BN];
   __shared__ float sred[4][BN];
   __shared__ unsigned long long swkey[4][BN];  // SAMPLE: per-warp best key, its logit, tile max / sum
@@ -172,7 +140,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __shared__ float run_m[BN], run_l[BN], run_z[BN];  // the CTA's running log-sum-exp state per row
   __shared__ unsigned long long run_k[BN];
   __shared__ int srow_act[BN], srow_kv[BN];
-  __shared__ float srs[BN];  // fused RMSNorm: 1/rms per row  // EPI_QKV: row tables, loaded during the mainloop
+  __shared__ float srs[BN];  // RMSNorm consumer: 1/rms per row (1 without a norm)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -200,9 +168,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4);
     }
-    mbar_init(redbar, 1);
-    mbar_init(consumed, S > 1 ? S - 1 : 1);
-    for (int i = 0; i < 8; ++i) mbar_init(&bready[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -216,7 +181,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  // every rank's receive barrier must be armed before any peer pushes into it
+  // start-up phase of the cluster barrier (every rank resident before the exchange)
   if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) stamp(a, 1);
@@ -230,17 +195,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // early streams its first STAGES x 16 KB while its predecessor drains.
       // Activation (B) tiles are issued after the wait.
       const int n_pre = (cl < a.num_tiles) ? min(STAGES, kb1 - kb0) : 0;
-      const uint32_t stage_tx = bnorm ? C::kStageA : C::kStage;
       for (int i = 0; i < n_pre; ++i) {
         uint8_t* sa = stage_base + i * C::kStage;
-        mbar_arrive_expect_tx(&full[i], stage_tx);
+        mbar_arrive_expect_tx(&full[i], C::kStage);
         tma_load_2d(sa, &tmA, &full[i], (kb0 + i) * kBK, cl * kBM, kEvictFirst);
       }
       stamp(a, 2);
       pdl_wait();
-      if (!bnorm)
-        for (int i = 0; i < n_pre; ++i)
-          tma_load_2d(stage_base + i * C::kStage + C::kStageA, &tmB, &full[i], (kb0 + i) * kBK, a.row0, kEvictLast);
+      for (int i = 0; i < n_pre; ++i)
+        tma_load_2d(stage_base + i * C::kStage + C::kStageA, &tmB, &full[i], (kb0 + i) * kBK, a.row0, kEvictLast);
       int stage = 0;
       uint32_t phase = 0;
       int done = n_pre;  // k-blocks of the first tile already issued
@@ -251,9 +214,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           } else {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sa = stage_base + stage * C::kStage;
-            mbar_arrive_expect_tx(&full[stage], stage_tx);
+            mbar_arrive_expect_tx(&full[stage], C::kStage);
             tma_load_2d(sa, &tmA, &full[stage], kb * kBK, tile * kBM, kEvictFirst);
-            if (!bnorm) tma_load_2d(sa + C::kStageA, &tmB, &full[stage], kb * kBK, a.row0, kEvictLast);
+            tma_load_2d(sa + C::kStageA, &tmB, &full[stage], kb * kBK, a.row0, kEvictLast);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -276,7 +239,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kb = kb0; kb < kb1; ++kb) {
-        if (bnorm && it == 0 && ((kb - kb0) & 7) == 0) mbar_wait(&bready[(kb - kb0) >> 3], 0);
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0 && kb == kb0) stamp(a, 3);
@@ -284,7 +246,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) {
           uint8_t* sa = stage_base + stage * C::kStage;
           const uint64_t da = smem_desc_k_sw128(sa);
-          const uint64_t db = smem_desc_k_sw128(bnorm ? bbuf + (size_t)(kb - kb0) * BN * 128 : sa + C::kStageA);
+          const uint64_t db = smem_desc_k_sw128(sa + C::kStageA);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
             tc_mma_f16(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
@@ -306,83 +268,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // arithmetic -- sets the latency.
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int m = q * 32 + lane;
+    const int et = threadIdx.x - 64;  // 0..127
     float* stg = aux;             // [BN][128] accumulator tile (column n = activation row)
     float* pre = aux + BN * kBM;  // [BN][128] operands prefetched during the mainloop
     pdl_wait();
-    if (bnorm && cl < a.num_tiles) {
-      // rs[row]: per-row sum over the producer's 128-column partials (fixed order)
-      const int et = threadIdx.x - 64;
-      float* rs = reinterpret_cast<float*>(sred);  // [BN] (sred is free until the first epilogue)
-      if (et < BN) {
+    if (et < BN) {
+      // RMSNorm consumer (R12b): rs per row from the producer's per-128-column partials,
+      // summed in column order (all loads in flight together)
+      float rs = 1.f;
+      if (a.rs_ssq) {
         float ss = 0.f;
         if (et < a.n_valid) {
           float t16[16];
 #pragma unroll 1
-          for (int t0 = 0; t0 < a.bn_tsq; t0 += 16) {
+          for (int t0 = 0; t0 < a.rs_nt; t0 += 16) {
 #pragma unroll
             for (int t = 0; t < 16; ++t)
-              t16[t] = t0 + t < a.bn_tsq ? a.bn_ssq[(size_t)(t0 + t) * a.bn_ld + a.row0 + et] : 0.f;
+              t16[t] = t0 + t < a.rs_nt ? __ldcg(a.rs_ssq + (size_t)(t0 + t) * a.rs_ld + a.row0 + et) : 0.f;
 #pragma unroll
             for (int t = 0; t < 16; ++t) ss += t16[t];
           }
         }
-        rs[et] = et < a.n_valid ? 1.0f / sqrtf(ss / (float)a.K + a.bn_eps) : 0.f;
+        rs = 1.0f / sqrtf(ss / (float)a.K + a.rs_eps);
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      // 16-byte chunks: (kb, row, 8-column chunk); each thread keeps one chunk column.
-      // Batches of up to 8 k-blocks, each released to the MMA warp as soon as written.
-      const int ch = et & 7;
-      const int nkb = kb1 - kb0;
-      constexpr int kPer = BN / 16;   // rows per thread per k-block
-      constexpr int kGrp = 8 / kPer;  // k-blocks per load batch (<= 8)
-#pragma unroll 1
-      for (int g0 = 0; g0 < nkb; g0 += kGrp) {
-        float4 xv[kGrp][kPer][2];
-        uint4 gv[kGrp];
-#pragma unroll
-        for (int j = 0; j < kGrp; ++j) {
-          const int kb = kb0 + g0 + j;
-          const bool okk = g0 + j < nkb;
-          gv[j] = okk ? *reinterpret_cast<const uint4*>(a.bn_gain + kb * 64 + ch * 8) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-          for (int c = 0; c < kPer; ++c) {
-            const int row = (et + 128 * c) >> 3;
-            const bool ok = okk && row < a.n_valid;
-            const float4* src = reinterpret_cast<const float4*>(a.bn_resid + (size_t)(a.row0 + row) * a.K + kb * 64 + ch * 8);
-            xv[j][c][0] = ok ? src[0] : make_float4(0.f, 0.f, 0.f, 0.f);
-            xv[j][c][1] = ok ? src[1] : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < kGrp; ++j) {
-          if (g0 + j >= nkb) break;
-          const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv[j]);
-          const float2 ga = __bfloat1622float2(g2[0]), gb = __bfloat1622float2(g2[1]);
-          const float2 gc = __bfloat1622float2(g2[2]), gd = __bfloat1622float2(g2[3]);
-#pragma unroll
-          for (int c = 0; c < kPer; ++c) {
-            const int row = (et + 128 * c) >> 3;
-            const float r_ = rs[row];
-            const float4 x0 = xv[j][c][0], x1 = xv[j][c][1];
-            uint4 o;
-            __nv_bfloat162 hh;
-            hh = __floats2bfloat162_rn(x0.x * r_ * ga.x, x0.y * r_ * ga.y); o.x = *reinterpret_cast<uint32_t*>(&hh);
-            hh = __floats2bfloat162_rn(x0.z * r_ * gb.x, x0.w * r_ * gb.y); o.y = *reinterpret_cast<uint32_t*>(&hh);
-            hh = __floats2bfloat162_rn(x1.x * r_ * gc.x, x1.y * r_ * gc.y); o.z = *reinterpret_cast<uint32_t*>(&hh);
-            hh = __floats2bfloat162_rn(x1.z * r_ * gd.x, x1.w * r_ * gd.y); o.w = *reinterpret_cast<uint32_t*>(&hh);
-            *reinterpret_cast<uint4*>(bbuf + ((size_t)(g0 + j) * BN + row) * 128 + ((ch ^ (row & 7)) << 4)) = o;
-          }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        // release every 8-k-block group this batch completed
-        if (et == 0)
-          for (int b = g0 >> 3; b <= (min(g0 + kGrp, nkb) - 1) >> 3; ++b)
-            if (min(8 * b + 8, nkb) <= min(g0 + kGrp, nkb)) mbar_arrive(&bready[b]);
-      }
+      srs[et] = rs;
     }
-    if (a.zero)
-      for (int i = blockIdx.x * 128 + (threadIdx.x - 64); i < a.zero_n; i += gridDim.x * 128) a.zero[i] = 0;
     int it = 0;
     for (int tile = cl; tile < a.num_tiles; tile += ncl, ++it) {
       const int acc = it & 1;
@@ -395,10 +305,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       if constexpr (EPI == EPI_QKV) {
         const QkvEpiArgs& e = a.qkv;
-        if (threadIdx.x - 64 < BN) {
-          const int n = threadIdx.x - 64;
-          srow_act[n] = n < a.n_valid ? e.row_active[a.row0 + n] : 0;
-          srow_kv[n] = n < a.n_valid ? e.row_kvloc[a.row0 + n] : 0;
+        if (et < BN) {
+          srow_act[et] = et < a.n_valid ? e.row_active[a.row0 + et] : 0;
+          srow_kv[et] = et < a.n_valid ? e.row_kvloc[a.row0 + et] : 0;
         }
         if (tile < e.Hq + e.Hkv) {
           // all rows' positions first, then the table rows: independent loads in flight together
@@ -450,28 +359,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               sum.z += t[j].z;
               sum.w += t[j].w;
             }
-          stg[(c0 + 0) * kBM + m] = sum.x;
-          stg[(c0 + 1) * kBM + m] = sum.y;
-          stg[(c0 + 2) * kBM + m] = sum.z;
-          stg[(c0 + 3) * kBM + m] = sum.w;
+          stg[(c0 + 0) * kBM + m] = sum.x * srs[c0 + 0];
+          stg[(c0 + 1) * kBM + m] = sum.y * srs[c0 + 1];
+          stg[(c0 + 2) * kBM + m] = sum.z * srs[c0 + 2];
+          stg[(c0 + 3) * kBM + m] = sum.w * srs[c0 + 3];
         }
         if (threadIdx.x == 64) stamp(a, 7);
       } else {
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // srs (first tile)
 #pragma unroll
-        for (int n = 0; n < BN; ++n) stg[n * kBM + m] = v[n];
+        for (int n = 0; n < BN; ++n) stg[n * kBM + m] = v[n] * srs[n];
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (threadIdx.x == 64) stamp(a, 8);
 
       if constexpr (EPI == EPI_STORE_F32 || EPI == EPI_RESID_ADD) {
         const int n_end = min(n_hi, a.n_valid);
+        const float gg = (EPI == EPI_RESID_ADD && a.xg_out && gm < a.M) ? a.xg_gain[gm] : 0.f;
         for (int n = n_lo; n < n_end; ++n) {
           float x = 0.f;
           if (gm < a.M) {
             x = stg[n * kBM + m];
             if (EPI == EPI_RESID_ADD) x += pre[n * kBM + m];
             a.out[(size_t)(a.row0 + n) * a.ld_out + gm] = x;
-            if (EPI == EPI_RESID_ADD && a.fn_out) stg[n * kBM + m] = x;
+            if (EPI == EPI_RESID_ADD && a.xg_out) a.xg_out[(size_t)(a.row0 + n) * a.M + gm] = __float2bfloat16_rn(x * gg);
           }
           if (EPI == EPI_RESID_ADD && a.ssq_out) {
             const float ss = warp_sum(x * x);
@@ -480,28 +391,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         if (EPI == EPI_RESID_ADD && a.ssq_out) {
           asm volatile("bar.sync 1, 128;" ::: "memory");
-          const int n = n_lo + (threadIdx.x - 64);
-          if (n < n_end)
-            a.ssq_out[(size_t)tile * a.bn_ld + a.row0 + n] = sred[0][n] + sred[1][n] + sred[2][n] + sred[3][n];
-        }
-        if (EPI == EPI_RESID_ADD && a.fn_out) {
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (threadIdx.x == 64) grid_barrier(a.fn_bar, gridDim.x);
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          // rs per row: one warp per row, lane t holds tiles t, t + 32, ... (all loads in flight
-          // together), then the same butterfly sum in every CTA
-          for (int n = n_lo + q; n < n_end; n += 4) {
-            float ss = 0.f;
-            for (int t = lane; t < a.num_tiles; t += 32) ss += __ldcg(a.ssq_out + (size_t)t * a.bn_ld + a.row0 + n);
-            ss = warp_sum(ss);
-            if (lane == 0) srs[n] = 1.0f / sqrtf(ss / (float)a.M + a.fn_eps);
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (gm < a.M) {
-            const float gg = a.fn_gain[gm];
-            for (int n = n_lo; n < n_end; ++n)
-              a.fn_out[(size_t)(a.row0 + n) * a.M + gm] = __float2bfloat16_rn(stg[n * kBM + m] * srs[n] * gg);
-          }
+          if (et >= n_lo && et < n_end) a.ssq_out[(size_t)tile * a.ssq_ld + a.row0 + et] = sred[0][et] + sred[1][et] + sred[2][et] + sred[3][et];
         }
       } else if constexpr (EPI == EPI_SWIGLU) {
         // rows [0, 64) of the tile are gate features f, rows [64, 128) the matching up
@@ -642,13 +532,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   if (threadIdx.x == 64) stamp(a, 10);
-  if (S > 1) {
+  if (S > 1 && warp < 2) {
     // producer / MMA warps: complete the start-up barrier phase and arrive on the
     // partials-written phase the epilogue waits for.
-    if (warp < 2) {
-      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    }
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();

@@ -327,6 +327,7 @@ static int g_launches = 0;  // kernel launches issued since the last reset (enqu
 static bool g_use_pdl = true;
 static int g_skip = 0;
 static float* g_splitk_ws = nullptr;  // set per context before enqueueing
+
 static unsigned long long* g_tl = nullptr;  // current timeline buffer during enqueue
 static int g_tl_n = 0;
 static const char* g_tl_name[512];  // debug: bit k skips kernel class k in the decode step (timing experiments only)
@@ -339,8 +340,6 @@ struct Stages {
   static constexpr int v = !DEEP ? 4 : (BN == 16 ? 8 : (BN == 32 ? 6 : 4));
 };
 
-// B_NORM buffer: the CTA's K range of BN normalised rows, bf16.
-static int bnorm_bytes(int BN, int kb_total, int split) { return BN * 128 * (int)ceil_div64(kb_total, split); }
 template <int BN, bool DEEP>
 static int gemm_smem_of() { return GemmCfg<BN, Stages<BN, DEEP>::v>::kSmem; }
 
@@ -349,7 +348,7 @@ static is_status launch_gemm_s(const CUtensorMap& tA, const CUtensorMap& tB, Gem
   using C = GemmCfg<BN, STAGES>;
   static int attr = 0;
   auto kern = gemm_swapab_kernel<BN, EPI, STAGES>;
-  const int smem = C::kSmem + (a.bn_resid ? bnorm_bytes(BN, a.K / kBK, a.split) : 0);
+  const int smem = C::kSmem;
   if (smem > attr) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = smem;
@@ -378,7 +377,8 @@ static is_status launch_gemm_s(const CUtensorMap& tA, const CUtensorMap& tB, Gem
   cfg.attrs = at;
   cfg.numAttrs = na;
   if (!a.partials) a.partials = g_splitk_ws;
-  if (a.split > 1 && (a.num_tiles * a.split > 2 * 160 || !a.partials)) return fail(IS_ERR_CAPACITY, "split-K workspace too small");
+  if (a.split > 1 && (a.num_tiles * a.split > 2 * 160 || !a.partials))
+    return fail(IS_ERR_CAPACITY, "split-K workspace too small");
   if (g_tl && g_tl_n < 512 && !a.dbg_ts) {
     a.dbg_ts = g_tl + (size_t)g_tl_n * 296 * 16;
     g_tl_name[g_tl_n++] = EPI == EPI_QKV ? "qkv" : EPI == EPI_RESID_ADD ? "resid" : EPI == EPI_SWIGLU ? "gu" : EPI == EPI_SAMPLE ? "lm" : "f32";
@@ -484,7 +484,6 @@ static is_status launch_k(K kern, dim3 grid, dim3 block, cudaStream_t st, Args..
 struct LayerW {
   __nv_bfloat16 *wqkv, *wo, *wgu, *wd;
   float *in_norm, *post_norm, *q_norm, *k_norm;
-  __nv_bfloat16 *in_norm_bf, *post_norm_bf;  // exact bf16 copies (B_NORM operand fill)
   CUtensorMap tm_qkv, tm_o, tm_gu, tm_d;
 };
 
@@ -513,14 +512,12 @@ struct is_ctx {
   int* merge_cnt;  // [max_rows][Hkv] fused-merge counters (decode, tcgen05 prefix), then 2 unit counters
   bool static_units;  // IS_STATIC_UNITS: the suffix pass strides its units statically (round 1)
   float *ssqA, *ssqB;  // [Th][max_rows] per-128-column sums of squares: QKV input, gate/up input
-  int bnorm;           // decode: RMSNorm folded into the QKV / gate-up B operand
   int sep_merge;       // decode suffix: 64-token CTA units + separate merge kernel
   int suffix_mma;      // decode suffix: 32-token units on mma.sync, merges spread over the grid (default)
   int suffix_shape;    //   its CTA shape: 1 = 8 warps x 1 stage (rc <= 16), 0 = 6 warps x 2 stages
   int prefix2;         // tcgen05 prefix with the query rows as M (default; up to 256 stacked rows)
   CUtensorMap tm_pool; // the page pool of all layers as rows of 128 bf16, box = one page (128-byte swizzle)
   int stg_lm;          // lm_head ring depth override (IS_STG_LM = 10 / 11; default 8)
-  int fuse_norm;       // decode: RMSNorm of the new residual fused into the o_proj / down epilogues
   int topp;            // 0 < top_p < 1: nucleus sampling pass after the lm_head (R36)
   float* logits_tp;    //   its fp32 logits [max_rows][vocab]
   float* scores_tp;    //   the lm_head's Gumbel scores [max_rows][vocab]
@@ -528,7 +525,6 @@ struct is_ctx {
   unsigned long long *wpart_tp, *hist_tp;  // per-slice mass, level-1 histograms
   int2* sel_tp;        //   per row (e*, v_k)
   ToppState* state_tp; //   per row radix-select state
-  unsigned int* fn_bar;  // [4] their grid barriers (o_proj, down)
   int32_t* attn_items;
   float* splitk_ws;  // split-K partials workspace
   int NC, nc_pre, nc_suf;
@@ -833,16 +829,10 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
   prof_mark(st, 0);
   if (prefill || !(g_skip & 128))
     CKS(launch_k(embed_kernel, dim3(rows), dim3(128), st, (const __nv_bfloat16*)c->embed,
-                 (const int32_t*)r_tok, (const int32_t*)r_active, c->resid, H,
-                 (!prefill && c->bnorm) ? c->ssqA : (float*)nullptr, c->max_rows));
+                 (const int32_t*)r_tok, (const int32_t*)r_active, c->resid, H, (const float*)c->L[0].in_norm, c->xn,
+                 c->ssqA, c->max_rows));
   for (int l = 0; l < s.layers; ++l) {
     LayerW& w = c->L[l];
-    const bool bn = !prefill && (c->bnorm & 1);       // QKV folds the input RMSNorm
-    const bool bn_gu = !prefill && (c->bnorm & 2);    // gate/up folds the post-attention RMSNorm
-    const bool fn = !prefill && c->fuse_norm;          // o_proj / down epilogues write the next xn
-    if (!bn && !(fn && l > 0) && (prefill || !(g_skip & 1)))
-      CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.in_norm, c->xn, H,
-                   s.rms_eps));
     prof_mark(st, 0);
     const size_t prefix_layer = (size_t)2 * Hkv * c->pcap * kHD;
     const size_t pool_layer = (size_t)c->num_pages * 2 * Hkv * c->pt * kHD;
@@ -870,14 +860,10 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       e.pcap = c->pcap;
       e.prefill = prefill ? 1 : 0;
       e.eps = s.rms_eps;
-      if (bn) {
-        a.bn_resid = c->resid;
-        a.bn_ssq = c->ssqA;
-        a.bn_gain = w.in_norm_bf;
-        a.bn_tsq = (int)ceil_div64(H, 128);
-        a.bn_ld = c->max_rows;
-        a.bn_eps = s.rms_eps;
-      }
+      a.rs_ssq = c->ssqA;  // RMSNorm (R12b): B = bf16(x * in_norm) from embed / the previous down epilogue
+      a.rs_nt = (int)ceil_div64(H, kBM);
+      a.rs_ld = c->max_rows;
+      a.rs_eps = s.rms_eps;
       if (!prefill && c->pf_lookahead > 0) {
         a.pf_progress = c->pf_progress;
         a.pf_seq = 4 * l;
@@ -940,16 +926,10 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       a.n_valid = std::min(chunk, rows - r0);
       a.out = c->resid;
       a.ld_out = H;
-      if (bn_gu || fn) {
-        a.ssq_out = c->ssqB;
-        a.bn_ld = c->max_rows;
-      }
-      if (fn) {
-        a.fn_gain = w.post_norm;
-        a.fn_out = c->xn;
-        a.fn_bar = c->fn_bar;
-        a.fn_eps = s.rms_eps;
-      }
+      a.xg_gain = w.post_norm;  // the post-attention norm's operand and sums of squares (R12b)
+      a.xg_out = c->xn;
+      a.ssq_out = c->ssqB;
+      a.ssq_ld = c->max_rows;
       if (!prefill && c->pf_lookahead > 0) {
         a.pf_progress = c->pf_progress;
         a.pf_seq = 4 * l + 1;
@@ -957,9 +937,6 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       if (prefill || !(g_skip & 16)) CKS(launch_gemm<EPI_RESID_ADD>(BN, w.tm_o, tm_attn, a, st, prefill ? 0 : c->stg_o));
     }
     prof_mark(st, 4);
-    if (!bn_gu && !fn && (prefill || !(g_skip & 1)))
-      CKS(launch_k(rmsnorm_kernel, dim3(rows), dim3(256), st, (const float*)c->resid, (const float*)w.post_norm, c->xn, H,
-                   s.rms_eps));
     prof_mark(st, 0);
     for (int r0 = 0; r0 < rows; r0 += chunk) {
       GemmArgs a{};
@@ -971,14 +948,10 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       a.n_valid = std::min(chunk, rows - r0);
       a.act = c->act;
       a.ld_act = F;
-      if (bn_gu) {
-        a.bn_resid = c->resid;
-        a.bn_ssq = c->ssqB;
-        a.bn_gain = w.post_norm_bf;
-        a.bn_tsq = (int)ceil_div64(H, 128);
-        a.bn_ld = c->max_rows;
-        a.bn_eps = s.rms_eps;
-      }
+      a.rs_ssq = c->ssqB;
+      a.rs_nt = (int)ceil_div64(H, kBM);
+      a.rs_ld = c->max_rows;
+      a.rs_eps = s.rms_eps;
       if (!prefill && c->pf_lookahead > 0) {
         a.pf_progress = c->pf_progress;
         a.pf_seq = 4 * l + 2;
@@ -996,16 +969,11 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       a.n_valid = std::min(chunk, rows - r0);
       a.out = c->resid;
       a.ld_out = H;
-      if (bn || fn) {
-        a.ssq_out = c->ssqA;
-        a.bn_ld = c->max_rows;
-      }
-      if (fn) {  // the next layer's input norm, or the final norm after the last layer
-        a.fn_gain = l + 1 < s.layers ? (const float*)c->L[l + 1].in_norm : (const float*)c->final_norm;
-        a.fn_out = c->xn;
-        a.fn_bar = c->fn_bar + 2;
-        a.fn_eps = s.rms_eps;
-      }
+      // the next layer's input norm, or the final norm before the lm_head (R12b)
+      a.xg_gain = l + 1 < s.layers ? (const float*)c->L[l + 1].in_norm : (const float*)c->final_norm;
+      a.xg_out = c->xn;
+      a.ssq_out = c->ssqA;
+      a.ssq_ld = c->max_rows;
       if (!prefill && c->pf_lookahead > 0) {
         a.pf_progress = c->pf_progress;
         a.pf_seq = 4 * l + 3;
@@ -1039,9 +1007,6 @@ static is_status enqueue_step_body(is_ctx* c) {
     CK(cudaEventRecord(c->pf_join, c->pf_st));
   }
   CKS(run_layers(c, c->rc, false));
-  if (!c->fuse_norm)  // (else the last down GEMM's epilogue applied the final norm)
-    CKS(launch_k(rmsnorm_kernel, dim3(c->rc), dim3(256), st, (const float*)c->resid, (const float*)c->final_norm,
-                 c->xn, s.hidden, s.rms_eps));
   prof_mark(st, 0);
   GemmArgs a{};
   a.M = s.vocab;
@@ -1061,6 +1026,10 @@ static is_status enqueue_step_body(is_ctx* c) {
   a.score_dump = c->topp ? c->scores_tp : nullptr;
   a.seed = c->cfg.seed;
   a.inv_temp = (float)(1.0 / (double)c->cfg.temperature);
+  a.rs_ssq = c->ssqA;  // final norm (R12b): B = bf16(x * final_norm) from the last down epilogue
+  a.rs_nt = (int)ceil_div64(s.hidden, kBM);
+  a.rs_ld = c->max_rows;
+  a.rs_eps = s.rms_eps;
   g_splitk_ws = c->splitk_ws;
   if (c->pf_lookahead > 0) {
     a.pf_progress = c->pf_progress;
@@ -1297,13 +1266,9 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
     CK(cudaMemcpy(w.wd, p[10], (size_t)H * F * 2, cudaMemcpyDeviceToDevice));
     w.in_norm = (float*)A(H * 4);
     w.post_norm = (float*)A(H * 4);
-    w.in_norm_bf = (__nv_bfloat16*)A(H * 2);
-    w.post_norm_bf = (__nv_bfloat16*)A(H * 2);
     w.q_norm = (float*)A(128 * 4);
     w.k_norm = (float*)A(128 * 4);
     if (err != IS_OK) return err;
-    CK(cudaMemcpy(w.in_norm_bf, p[0], (size_t)H * 2, cudaMemcpyDeviceToDevice));
-    CK(cudaMemcpy(w.post_norm_bf, p[7], (size_t)H * 2, cudaMemcpyDeviceToDevice));
     bf16_to_f32_kernel<<<(H + 255) / 256, 256>>>((const __nv_bfloat16*)p[0], w.in_norm, H);
     bf16_to_f32_kernel<<<(H + 255) / 256, 256>>>((const __nv_bfloat16*)p[7], w.post_norm, H);
     bf16_to_f32_kernel<<<1, 128>>>((const __nv_bfloat16*)p[4], w.q_norm, 128);
@@ -1335,7 +1300,6 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->ssqA = (float*)A((size_t)ceil_div64(H, 128) * R * 4);
   c->ssqB = (float*)A((size_t)ceil_div64(H, 128) * R * 4);
   c->splitk_ws = (float*)A((size_t)2 * 160 * kBM * 64 * 4);
-  c->fn_bar = (unsigned int*)A(4 * sizeof(unsigned int));
   c->topp = cfg->top_p > 0.f && cfg->top_p < 1.f;
   c->logits_tp = c->topp ? (float*)A((size_t)R * s.vocab * 4) : nullptr;
   c->scores_tp = c->topp ? (float*)A((size_t)R * s.vocab * 4) : nullptr;
@@ -1415,29 +1379,6 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->split_o = choose_split((int)ceil_div64(H, kBM), Hq * 128 / kBK, c->BN);
   c->split_gu = choose_split((int)ceil_div64(2 * F, kBM), H / kBK, c->BN);
   c->split_d = choose_split((int)ceil_div64(H, kBM), F / kBK, c->BN);
-  {
-    // RMSNorm folded into the QKV / gate-up GEMMs when the CTA's normalised B rows fit in smem
-    int maxsm = 0;
-    CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
-    auto fits = [&](int split) {
-      const bool deep = split == 1;
-      int base = 0;
-      switch (c->BN * 2 + (deep ? 1 : 0)) {
-        case 32: base = gemm_smem_of<16, false>(); break;
-        case 33: base = gemm_smem_of<16, true>(); break;
-        case 64: base = gemm_smem_of<32, false>(); break;
-        case 65: base = gemm_smem_of<32, true>(); break;
-        case 128: base = gemm_smem_of<64, false>(); break;
-        default: base = gemm_smem_of<64, true>(); break;
-      }
-      return base + bnorm_bytes(c->BN, H / kBK, split) <= maxsm;
-    };
-    // IS_BNORM=1: QKV and gate/up (measured slower: profiles/r01); IS_BNORM=qkv: QKV only
-    const char* e = getenv("IS_BNORM");
-    c->bnorm = 0;
-    if (e && !strcmp(e, "qkv") && fits(c->split_qkv)) c->bnorm = 1;
-    else if (e && fits(c->split_qkv) && fits(c->split_gu)) c->bnorm = 3;
-  }
   c->l2_prefetch = getenv("IS_L2_PREFETCH") ? atoi(getenv("IS_L2_PREFETCH")) : 0;
   c->steps_per_graph = getenv("IS_STEPS_PER_GRAPH") ? std::max(1, atoi(getenv("IS_STEPS_PER_GRAPH"))) : 1;
   c->stg_qkv = getenv("IS_STG_QKV") ? atoi(getenv("IS_STG_QKV")) : 0;
@@ -1453,14 +1394,6 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   if (const char* e = getenv("IS_SPLIT_OVERRIDE")) {
     int v = atoi(e);
     if (v >= 1 && v <= 8) c->split_qkv = c->split_o = c->split_gu = c->split_d = v;
-  }
-  {
-    // IS_FUSE_NORM=1 (opt-in, measured slower: DESIGN §5a).  The fused norm's grid barrier
-    // needs every CTA co-resident and one tile per CTA
-    const int th = (int)ceil_div64(H, kBM);
-    const char* e = getenv("IS_FUSE_NORM");
-    c->fuse_norm = (e && atoi(e) != 0) && !c->bnorm && th * std::max(c->split_o, 1) <= g_num_sms &&
-                   th * std::max(c->split_d, 1) <= g_num_sms;
   }
   {
     // L2 weight prefetcher (opt-in: IS_L2PF = lookahead in MB)
@@ -1510,13 +1443,11 @@ extern "C" void is_destroy(is_ctx* c) {
                   c->last_fin, c->st_dev, c->slot_uid, c->slot_count, c->tpos, c->true_len, c->queue,
                   c->main_init, c->main_queue, c->free_stack, c->pagetab, c->npages, c->tokens, c->log_slot,
                   c->log_live, c->d_prompt_copy, c->lp_key, c->lp_mlz, c->logprobs, c->done_flag, c->pred, c->adm_seq, c->stall, c->prow_active, c->prow_tok, c->prow_pos, c->prow_kvloc,
-                  c->prow_len, c->fn_bar, c->logits_tp, c->scores_tp, c->ebits_tp, c->wpart_tp, c->hist_tp,
+                  c->prow_len, c->logits_tp, c->scores_tp, c->ebits_tp, c->wpart_tp, c->hist_tp,
                   c->sel_tp, c->state_tp};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (auto& w : c->L) {
-    cudaFree(w.in_norm_bf);
-    cudaFree(w.post_norm_bf);
     cudaFree(w.in_norm);
     cudaFree(w.post_norm);
     cudaFree(w.q_norm);

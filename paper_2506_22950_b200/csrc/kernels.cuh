@@ -9,11 +9,13 @@ constexpr int kHD = 128;      // head_dim (all Qwen3 shapes, R1)
 constexpr int kKPad = 136;    // smem row pitch (bf16) -> conflict-free 16-B row reads
 
 // ------------------------------------------------------------------ embed
-// resid[r][:] = E[tok[r]][:] (fp32 residual stream); idle rows get zeros.  With
-// ssq != null also the per-128-column sums of squares ssq[t][r] that the first
-// QKV GEMM folds its RMSNorm from.  One CTA of 128 threads per row.
+// resid[r][:] = E[tok[r]][:] (fp32 residual stream); idle rows get zeros.  Also the
+// first layer's RMSNorm operands (R12b): xg[r][k] = bf16(x * gain[k]) and the
+// per-128-column sums of squares ssq[t][r] the QKV GEMM derives rs[r] from.
+// One CTA of 128 threads per row.
 __global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ row_tok,
                              const int32_t* __restrict__ row_active, float* __restrict__ resid, int H,
+                             const float* __restrict__ gain, __nv_bfloat16* __restrict__ xg,
                              float* __restrict__ ssq, int ld_ssq) {
   pdl_launch_dependents();  // let the next kernel launch and prefetch now; it waits for our completion itself
   pdl_wait();
@@ -24,54 +26,15 @@ __global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const int32_t*
   for (int t0 = 0; t0 < H; t0 += 128) {
     const int k = t0 + threadIdx.x;
     const float x = (act && k < H) ? __bfloat162float(e[k]) : 0.f;
-    if (k < H) resid[(size_t)r * H + k] = x;
-    if (ssq) {
-      const float s2 = warp_sum(x * x);
-      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s2;
-      __syncthreads();
-      if (threadIdx.x == 0) ssq[(size_t)(t0 / 128) * ld_ssq + r] = red[0] + red[1] + red[2] + red[3];
-      __syncthreads();
+    if (k < H) {
+      resid[(size_t)r * H + k] = x;
+      xg[(size_t)r * H + k] = __float2bfloat16_rn(x * gain[k]);
     }
-  }
-}
-
-// ------------------------------------------------------------------ RMSNorm
-// xn[r][k] = bf16(resid[r][k] / sqrt(mean(resid[r]^2) + eps) * gain[k])   (R12 r1)
-// One CTA per row; every thread issues all its float4 loads before reducing
-// (no serial load chain).  H % 4 == 0, H / 4 <= 4 * blockDim.
-__global__ void rmsnorm_kernel(const float* __restrict__ resid, const float* __restrict__ gain,
-                               __nv_bfloat16* __restrict__ xn, int H, float eps) {
-  pdl_launch_dependents();  // let the next kernel launch and prefetch now; it waits for our completion itself
-  pdl_wait();
-  const int r = blockIdx.x;
-  const float4* x4 = reinterpret_cast<const float4*>(resid + (size_t)r * H);
-  const float4* g4 = reinterpret_cast<const float4*>(gain);
-  const int n4 = H >> 2;
-  float4 xv[4], gv[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int i = threadIdx.x + j * blockDim.x;
-    xv[j] = i < n4 ? x4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-    gv[j] = i < n4 ? g4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  float ss = 0.f;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) ss += xv[j].x * xv[j].x + xv[j].y * xv[j].y + xv[j].z * xv[j].z + xv[j].w * xv[j].w;
-  __shared__ float red[32];
-  ss = warp_sum(ss);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-  __syncthreads();
-  float tot = 0.f;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
-  const float rs = 1.0f / sqrtf(tot / (float)H + eps);
-  __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(xn + (size_t)r * H);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int i = threadIdx.x + j * blockDim.x;
-    if (i < n4) {
-      o2[2 * i] = __floats2bfloat162_rn(xv[j].x * rs * gv[j].x, xv[j].y * rs * gv[j].y);
-      o2[2 * i + 1] = __floats2bfloat162_rn(xv[j].z * rs * gv[j].z, xv[j].w * rs * gv[j].w);
-    }
+    const float s2 = warp_sum(x * x);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s2;
+    __syncthreads();
+    if (threadIdx.x == 0) ssq[(size_t)(t0 / 128) * ld_ssq + r] = red[0] + red[1] + red[2] + red[3];
+    __syncthreads();
   }
 }
 

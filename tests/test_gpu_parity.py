@@ -48,6 +48,29 @@ def test_gemm_tcgen05_vs_fp32_matmul(lib, M_, K, rows, split):
         assert _rel(got[r], ref[r]) < 1e-4, r
 
 
+@pytest.mark.parametrize("M_,K,rows,split", [(2048, 2048, 16, 8), (4096, 2048, 16, 4), (12288, 2048, 16, 2),
+                                             (2048, 6144, 16, 3)])
+def test_gemm_splitk_deterministic(lib, M_, K, rows, split):
+    """Split-K (gemm.cuh): each rank sums its column slice over the ranks' partials in rank
+    order, so repeated launches give bit-identical outputs, within the 1e-4 kernel tolerance
+    of the fp64 product."""
+    g = torch.Generator(device="cuda").manual_seed(7 + M_ + split)
+    w = (torch.randn(M_, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    x = torch.randn(rows, K, device="cuda", generator=g).to(torch.bfloat16)
+    outs = []
+    for _ in range(6):
+        y = torch.full((rows, M_), float("nan"), device="cuda")
+        lib.is_dbg_gemm(w, x, y, split=split)
+        outs.append(y)
+    torch.cuda.synchronize()
+    for y in outs[1:]:
+        assert torch.equal(y, outs[0])
+    ref = (x.double() @ w.double().T).cpu().numpy()
+    got = outs[0].cpu().numpy()
+    for r in range(rows):
+        assert _rel(got[r], ref[r]) < 1e-4, r
+
+
 # ---------------------------------------------------------------------------- tiny end to end
 TINY = SHAPES["tiny"]
 SEED = 20261017
@@ -371,20 +394,6 @@ def test_tiny_dynamic_slot_mode(lib, tiny, target):
     base = tiny["runs"]["infinite"]["tokens"]
     for uid in ref.finish_step:
         assert np.array_equal(r["tokens"][uid], base[uid]), uid
-
-
-def test_tiny_fused_norm_opt_in(lib, tiny, monkeypatch):
-    """IS_FUSE_NORM=1 (opt-in): RMSNorm in the o_proj / down epilogues behind a grid
-    barrier.  Same schedule; the norm's fp32 sum order differs, so tokens are compared with the
-    teacher-forced tolerance of the default path (all but a near-tie few identical)."""
-    monkeypatch.setenv("IS_FUSE_NORM", "1")
-    r = _run(lib, tiny["w_dev"], tiny["prompt"], tiny["true"], tiny["pred"], "infinite", 2,
-             budget=tiny["budget"])
-    base = tiny["runs"]["infinite"]
-    assert r["slots"].tolist() == base["slots"].tolist() and r["stats"]["completed"] == 8
-    valid = base["tokens"] >= 0
-    same = np.mean(r["tokens"][valid] == base["tokens"][valid])
-    assert same >= 0.9, same
 
 
 @pytest.mark.parametrize("top_p", [0.9, 0.5, 0.05])

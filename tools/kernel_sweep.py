@@ -39,7 +39,7 @@ SETTINGS = [s for s in os.environ.get("SWEEP", "").split(";") if s] or [
     "", "IS_SPLIT_GU=1", "IS_SPLIT_GU=3", "IS_SPLIT_GU=4", "IS_STG_GU=6", "IS_STG_GU=8",
     "IS_SPLIT_D=4", "IS_STG_D=6", "IS_STG_D=8", "IS_SPLIT_O=4", "IS_STG_O=6", "IS_SPLIT_QKV=2", "IS_STG_QKV=6",
 ]
-KNOBS = ["IS_STREAMK_GU", "IS_STG_LM", "IS_FUSE_NORM", "IS_SPLIT_GU", "IS_SPLIT_D", "IS_SPLIT_O", "IS_SPLIT_QKV", "IS_STG_GU", "IS_STG_D", "IS_STG_O",
+KNOBS = ["IS_STREAMK_GU", "IS_STG_LM", "IS_SPLIT_GU", "IS_SPLIT_D", "IS_SPLIT_O", "IS_SPLIT_QKV", "IS_STG_GU", "IS_STG_D", "IS_STG_O",
          "IS_STG_QKV"]
 for setting in SETTINGS:
     for k in KNOBS:

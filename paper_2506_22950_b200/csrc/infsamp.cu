@@ -327,6 +327,7 @@ static int g_launches = 0;  // kernel launches issued since the last reset (enqu
 static bool g_use_pdl = true;
 static int g_skip = 0;
 static float* g_splitk_ws = nullptr;  // set per context before enqueueing
+static bool g_exact_prefix_max = false;  // IS_EXACT_PREFIX_MAX: the prefix softmax takes the column max (no bound)
 
 static unsigned long long* g_tl = nullptr;  // current timeline buffer during enqueue
 static int g_tl_n = 0;
@@ -398,6 +399,8 @@ static is_status launch_gemm(int BN, const CUtensorMap& tA, const CUtensorMap& t
                              int stages = 0) {
   const bool deep = a.split == 1;
   // deeper weight ring for a split-K GEMM (more of its weights arrive before the PDL wait returns)
+  if (!deep && BN == 16 && stages == 3) return launch_gemm_s<16, EPI, 3>(tA, tB, a, st);
+  if (!deep && BN == 16 && stages == 5) return launch_gemm_s<16, EPI, 5>(tA, tB, a, st);
   if (!deep && BN == 16 && stages == 6) return launch_gemm_s<16, EPI, 6>(tA, tB, a, st);
   if (!deep && BN == 16 && stages == 8) return launch_gemm_s<16, EPI, 8>(tA, tB, a, st);
   // lm_head (persistent, one CTA per SM): more bytes in flight per SM (IS_STG_LM)
@@ -511,6 +514,7 @@ struct is_ctx {
   float *part_o, *part_ml;
   int* merge_cnt;  // [max_rows][Hkv] fused-merge counters (decode, tcgen05 prefix), then 2 unit counters
   bool static_units;  // IS_STATIC_UNITS: the suffix pass strides its units statically (round 1)
+  float* kmax;         // [M][L][Hkv][prefix tiles] max key norm per 128-token prefix tile (prefix_kmax_kernel)
   float *ssqA, *ssqB;  // [Th][max_rows] per-128-column sums of squares: QKV input, gate/up input
   int sep_merge;       // decode suffix: 64-token CTA units + separate merge kernel
   int suffix_mma;      // decode suffix: 32-token units on mma.sync, merges spread over the grid (default)
@@ -755,7 +759,7 @@ static is_status launch_prefix_tc2(const AttnArgs& aa, const AttnLaunch& al, cud
 }
 
 template <int REP>
-static is_status launch_attn_rep(const AttnArgs& aa, const AttnLaunch& al, cudaStream_t st) {
+static is_status launch_attn_rep(AttnArgs aa, const AttnLaunch& al, cudaStream_t st) {
   if (aa.tc_prefix && al.prefix2) {
     const int nrows = al.grp_rows * REP;
     if (nrows <= 128) CKS((launch_prefix_tc2<REP, 1>(aa, al, st)));
@@ -771,11 +775,19 @@ static is_status launch_attn_rep(const AttnArgs& aa, const AttnLaunch& al, cudaS
   }
   if (al.suffix_mma) {  // decode, 64-token units on mma.sync with the fused merge
     const bool wide = al.suffix_shape == 1;  // 8 warps x 1 stage (small launches) vs 6 x 2
+    // A suffix CTA does not fit beside a tcgen05 prefix CTA: with few prefix CTAs, the last
+    // suffix CTAs start only when the prefix kernel exits, so they get no static units and no
+    // merges (those would set the kernel's tail).
+    aa.early_ctas = 0;
+    if (aa.tc_prefix && !getenv("IS_NO_EARLY_CTAS")) {
+      const int npre = al.groups * aa.Hkv * (int)ceil_div64(aa.plen, 128);
+      if (npre <= g_num_sms / 4) aa.early_ctas = g_num_sms - npre;
+    }
 #define IS_SUFFIX_MMA(P)                                                                                         \
-  (wide ? launch_k_smem(attn_suffix_mma_kernel<REP, P, 8, 1>, dim3(g_num_sms), dim3(256),                       \
-                        SuffixMmaSmem<8, 1>::v, st, *al.tm_pool, aa)                                           \
-        : launch_k_smem(attn_suffix_mma_kernel<REP, P, 6, 2>, dim3(g_num_sms), dim3(192),                       \
-                        SuffixMmaSmem<6, 2>::v, st, *al.tm_pool, aa))
+  (wide ? launch_k_smem(attn_suffix_mma_kernel<REP, P, 8, 1>, dim3(g_num_sms), dim3(256),                            \
+                        SuffixMmaSmem<8, 1, REP>::v, st, *al.tm_pool, aa)                                           \
+        : launch_k_smem(attn_suffix_mma_kernel<REP, P, 6, 2>, dim3(g_num_sms), dim3(192),                            \
+                        SuffixMmaSmem<6, 2, REP>::v, st, *al.tm_pool, aa))
     switch (aa.pt) {
       case 8: CKS(IS_SUFFIX_MMA(8)); break;
       case 16: CKS(IS_SUFFIX_MMA(16)); break;
@@ -883,6 +895,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
     aa.items = c->attn_items;
     aa.n_items = c->st_dev + (size_t)c->M * ST_COUNT + ST_ATTN_ITEMS;
     aa.dbg_ts = nullptr;
+    aa.dbg_mode = getenv("IS_DBG_ATTN_MODE") ? atoi(getenv("IS_DBG_ATTN_MODE")) : 0;  // timing experiments
     if (g_tl && l < 4) aa.dbg_ts = g_tl + (size_t)(400 + 4 * l) * 296 * 16;  // attn: 2x296 CTAs, prefix_tc after
     aa.out = c->attn;
     aa.rows = rows;
@@ -898,6 +911,11 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
     aa.pool_row0 = l * c->num_pages * 2 * Hkv;
     aa.unit_ctr = (!prefill && !c->static_units) ? c->merge_cnt + (size_t)c->max_rows * Hkv : nullptr;
     aa.merge_done = c->merge_cnt + (size_t)c->max_rows * Hkv + 2;
+    if (!prefill && !g_exact_prefix_max) {
+      const int nt = (int)ceil_div64(c->pcap, 128);
+      aa.kmax = c->kmax + (size_t)l * Hkv * nt;
+      aa.kmax_grp = s.layers * Hkv * nt;
+    }
     aa.sc = prefill ? kSC : c->sc;
     aa.NC = c->NC;
     aa.prefill = prefill ? 1 : 0;
@@ -1139,6 +1157,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   if (prop.major != 10) return fail(IS_ERR_CUDA, "needs an sm_100 (B200) device, found sm_%d%d", prop.major, prop.minor);
   g_num_sms = prop.multiProcessorCount;
   if (getenv("IS_NO_PDL")) g_use_pdl = false;
+  g_exact_prefix_max = getenv("IS_EXACT_PREFIX_MAX") != nullptr;
   if (getenv("IS_SKIP")) g_skip = atoi(getenv("IS_SKIP"));
 
   is_ctx* c = new is_ctx{};
@@ -1297,6 +1316,7 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   c->part_ml = (float*)A((size_t)R * Hq * c->NC * 2 * 4);
   c->merge_cnt = (int*)A(((size_t)2 * R * Hkv + 2) * 4);  // + 2 unit counters + merged-head counters
   c->static_units = getenv("IS_STATIC_UNITS") != nullptr;  // timing comparison only
+  c->kmax = (float*)A((size_t)c->M * s.layers * Hkv * ceil_div64(c->pcap, 128) * 4);
   c->ssqA = (float*)A((size_t)ceil_div64(H, 128) * R * 4);
   c->ssqB = (float*)A((size_t)ceil_div64(H, 128) * R * 4);
   c->splitk_ws = (float*)A((size_t)2 * 160 * kBM * 64 * 4);
@@ -1438,7 +1458,7 @@ extern "C" void is_destroy(is_ctx* c) {
   if (c->graph_ok) cudaGraphExecDestroy(c->graph);
   if (c->graphK_ok) cudaGraphExecDestroy(c->graphK);
   void* bufs[] = {c->wblob, c->final_norm, c->prefix, c->pool, c->resid, c->xn, c->attn, c->act, c->q,
-                  c->part_o, c->part_ml, c->merge_cnt, c->ssqA, c->ssqB, c->attn_items, c->splitk_ws, c->rope_cos, c->rope_sin, c->row_active, c->row_uid, c->row_lid,
+                  c->part_o, c->part_ml, c->merge_cnt, c->kmax, c->ssqA, c->ssqB, c->attn_items, c->splitk_ws, c->rope_cos, c->rope_sin, c->row_active, c->row_uid, c->row_lid,
                   c->row_t, c->row_tok, c->row_pos, c->row_kvloc, c->row_len, c->keys, c->last_tok,
                   c->last_fin, c->st_dev, c->slot_uid, c->slot_count, c->tpos, c->true_len, c->queue,
                   c->main_init, c->main_queue, c->free_stack, c->pagetab, c->npages, c->tokens, c->log_slot,
@@ -1495,6 +1515,12 @@ extern "C" is_status is_prefill_slot(is_ctx* c, int32_t slot, const int32_t* d_p
   CKS(launch_k(prefill_rows_kernel, dim3((c->pcap + 127) / 128), dim3(128), c->st, (const int32_t*)c->d_prompt_copy,
                c->pcap, c->prow_active, c->prow_tok, c->prow_pos, c->prow_kvloc));
   CKS(run_layers(c, c->pcap, true, slot));
+  {  // the prefix's key-norm bound per (layer, kv head, 128-token tile) for the decode prefix softmax
+    const int nt = (int)ceil_div64(c->pcap, 128), Hkv = c->sh.n_kv_heads, L = c->sh.layers;
+    CKS(launch_k(prefix_kmax_kernel, dim3(L * Hkv * nt), dim3(128), c->st,
+                 (const __nv_bfloat16*)(c->prefix + (size_t)slot * L * 2 * Hkv * c->pcap * kHD), L, Hkv, c->pcap,
+                 c->pcap, c->kmax + (size_t)slot * L * Hkv * nt));
+  }
   c->launches_per_prefill = g_launches - launches0;
   CK(cudaStreamSynchronize(c->st));
   if (last < 0 || last >= c->sh.vocab) return fail(IS_ERR_DATA, "prompt token %d out of range", last);
@@ -1979,6 +2005,8 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
   float* part_o = (float*)dalloc((size_t)rows * Hq * NC * 128 * 4, &err);
   float* part_ml = (float*)dalloc((size_t)rows * Hq * NC * 2 * 4, &err);
   int* mcnt = (int*)dalloc(((size_t)2 * rows * Hkv + 2) * 4, &err);
+  const int ntp = (int)ceil_div64(plen, 128);
+  float* kmx = (float*)dalloc((size_t)groups * Hkv * ntp * 4, &err);
   uint8_t* flush = reps > 0 ? (uint8_t*)dalloc((size_t)256 << 20, &err) : nullptr;  // > 2x the 126 MB L2
   CUtensorMap tm, tmp;
   if (err == IS_OK) err = make_tmap(&tm, d_prefix, (int64_t)groups * 2 * Hkv * plen, 128, 128);
@@ -2001,6 +2029,7 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
     wl.items = items;
     wl.n_items = nit;
     attn_worklist_kernel<<<1, kSchedThreads, 0, st>>>(wl);
+    prefix_kmax_kernel<<<groups * Hkv * ntp, 128, 0, st>>>((const __nv_bfloat16*)d_prefix, 1, Hkv, plen, plen, kmx);
     AttnArgs aa{};
     aa.q = (const __nv_bfloat16*)d_q;
     aa.kpre = (const __nv_bfloat16*)d_prefix;
@@ -2028,6 +2057,8 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
     aa.merge_cnt = (tc && !sep) ? mcnt : nullptr;
     aa.unit_ctr = getenv("IS_STATIC_UNITS") ? nullptr : mcnt + (size_t)rows * Hkv;
     aa.merge_done = mcnt + (size_t)rows * Hkv + 2;
+    aa.kmax = getenv("IS_EXACT_PREFIX_MAX") ? nullptr : kmx;
+    aa.kmax_grp = Hkv * ntp;
     aa.sc = sc;
     aa.scale = 1.0f / sqrtf((float)kHD);
     AttnLaunch al{};
@@ -2113,7 +2144,7 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
               u[u.size() / 2], u.back(), m[0], m[m.size() / 2], m.back());
     }
   }
-  for (void* p : {(void*)d_act, (void*)d_lid, (void*)items, (void*)nit, (void*)part_o, (void*)part_ml, (void*)mcnt,
+  for (void* p : {(void*)d_act, (void*)d_lid, (void*)items, (void*)nit, (void*)part_o, (void*)part_ml, (void*)mcnt, (void*)kmx,
                   (void*)flush})
     if (p) cudaFree(p);
   return err;
@@ -2165,32 +2196,20 @@ extern "C" int is_dbg_timeline(is_ctx* c) {
            f(mn[10]), f(mx[10]), f(mn[11]), f(mx[11]));
   }
   for (int l = 0; l < 4; ++l) {
-    const unsigned long long* base = &h0[(size_t)(400 + 2 * l) * 296 * 16];
-    double st = 1e30, en = 0;
-    std::vector<double> pst[2], pcm[2], pend[2];
-    int nunits[4] = {0, 0, 0, 0};
-    for (int b = 0; b < 4 * 296; ++b) {
-      const unsigned long long* p = base + b * 16;
-      if (!p[0]) continue;
-      st = std::min(st, (double)(p[0] - t0) / 1e3);
-      en = std::max(en, (double)(p[15] - t0) / 1e3);
-      int k = 0;
-      for (int nu = 0; nu < 3; ++nu) {
-        const unsigned long long* q = p + 1 + 4 * nu;
-        if (!q[0] || !q[2] || q[3] < 1 || q[3] > 2) break;
-        const int kind = (int)q[3] - 1;
-        pst[kind].push_back((double)(q[1] - q[0]) / 1e3);
-        pcm[kind].push_back((double)(q[2] - q[1]) / 1e3);
-        pend[kind].push_back((double)(q[2] - t0) / 1e3);
-        ++k;
-      }
-      nunits[std::min(k, 3)]++;
+    // the mma suffix kernel's CTAs: 0 start, 3 units begin, 2 warp 0's units done, 6 all units
+    // published, 7 prefix complete (PDL wait), 8 merges done
+    const unsigned long long* base = &h0[(size_t)(400 + 4 * l) * 296 * 16];
+    printf("suffix L%d", l);
+    const int ks[6] = {0, 3, 2, 6, 7, 8};
+    for (int q = 0; q < 6; ++q) {
+      std::vector<double> v;
+      for (int b = 0; b < 296; ++b)
+        if (base[b * 16] && base[b * 16 + ks[q]]) v.push_back((double)(base[b * 16 + ks[q]] - t0) / 1e3);
+      if (v.empty()) continue;
+      std::sort(v.begin(), v.end());
+      printf("  s%d n=%zu %.2f/%.2f/%.2f", ks[q], v.size(), v[0], v[v.size() / 2], v.back());
     }
-    auto med = [](std::vector<double> v) { if (v.empty()) return -1.0; std::sort(v.begin(), v.end()); return v[v.size() / 2]; };
-    auto mx = [](std::vector<double> v) { if (v.empty()) return -1.0; return *std::max_element(v.begin(), v.end()); };
-    printf("%s L%d %.2f..%.2f  CTAs with 0/1/2/3 units: %d/%d/%d/%d | prefix n=%zu stage %.2f/%.2f compute %.2f/%.2f done<=%.2f | suffix n=%zu stage %.2f/%.2f compute %.2f/%.2f done<=%.2f\n",
-           (l & 1) ? "attn#2" : "attn", l / 2, st, en, nunits[0], nunits[1], nunits[2], nunits[3], pst[0].size(), med(pst[0]), mx(pst[0]), med(pcm[0]),
-           mx(pcm[0]), mx(pend[0]), pst[1].size(), med(pst[1]), mx(pst[1]), med(pcm[1]), mx(pcm[1]), mx(pend[1]));
+    printf("\n");
   }
   for (int l = 0; l < 2; ++l) {
     const unsigned long long* base = &h0[((size_t)(400 + 4 * l) * 296 + 2 * 296) * 16];
@@ -2204,8 +2223,19 @@ extern "C" int is_dbg_timeline(is_ctx* c) {
       for (int k = 0; k < 8; ++k)
         if (p[k]) mx[k] = std::max(mx[k], (double)(p[k] - t0) / 1e3);
     }
-    printf("prefix_tc L%d ctas=%d start %.2f waited %.2f q_staged %.2f tma %.2f S_done %.2f P_done %.2f O_done %.2f end %.2f\n", l, n,
-           mn0, mx[1], mx[2], mx[3], mx[4], mx[5], mx[6], mx[7]);
+    double mx8 = 0;
+    for (int b = 0; b < 64; ++b)
+      if (base[b * 16] && base[b * 16 + 8]) mx8 = std::max(mx8, (double)(base[b * 16 + 8] - t0) / 1e3);
+    printf("prefix_tc L%d ctas=%d start %.2f waited %.2f q_staged %.2f tma %.2f S_done %.2f [softmax pass 0 done %.2f] P_done %.2f O_done %.2f end %.2f\n", l, n,
+           mn0, mx[1], mx[2], mx[3], mx[4], mx8, mx[5], mx[6], mx[7]);
+    printf("      fine:");
+    for (int k = 9; k <= 14; ++k) {
+      double v = 0;
+      for (int b = 0; b < 64; ++b)
+        if (base[b * 16] && base[b * 16 + k]) v = std::max(v, (double)(base[b * 16 + k] - t0) / 1e3);
+      printf(" s%d %.2f", k, v);
+    }
+    printf("\n");
     // per-CTA phase durations (median / max, us): wait->q, q->S, S->P (softmax), P->O, O->end
     const char* nm[5] = {"q_stage", "S_mma", "softmax", "PV_mma", "epilogue"};
     const int k0[5] = {1, 2, 4, 5, 6}, k1[5] = {2, 4, 5, 6, 7};

@@ -89,6 +89,10 @@ struct AttnArgs {
   int* unit_ctr;              // decode: [2] dynamic work fetching (next unit, warps / CTAs done; the last
                               //   finisher resets both for the next launch); null = static striding
   int sc;                     // decode suffix chunk (tokens per work item): kSC, or kSCW for the warp kernel
+  const float* kmax;          // decode, tcgen05 prefix: max_t ||k_t|| per (kv head, 128-token tile) of this
+  int kmax_grp;               //   layer (prefix_kmax_kernel, at prefill); group stride.  null: exact max
+  int early_ctas;             // decode (mma suffix): CTAs [0, early_ctas) take the static units and the
+                              //   merges; the rest (placed behind the prefix kernel's CTAs) only claim (0: all)
   int grp_rows;               // decode, tcgen05 prefix: rows per co-resident group (g); group m = rows m*g ..
   int grp_kv_rows;            //   prefix-KV tensor-map rows per group (L * 2 * Hkv * pcap)
   float scale;                // 1/sqrt(128)
@@ -420,11 +424,13 @@ constexpr int kSUnit = 32;          // keys per unit
 constexpr int kSQueue = 6;          // work items loaded ahead of their issue
 constexpr int kSPublish = 8;        // units per release batch (one fence)
 constexpr int kSStaticPct = 50;     // share of the work list split statically over the warps
-template <int NW, int NST>
+// Sized so that the 8 x 1 shape (<= 16 rows) shares an SM with a tcgen05 prefix CTA
+// (PrefixTcSmem<16>): every suffix CTA starts at once instead of behind the prefix kernel.
+template <int NW, int NST, int REP>
 struct SuffixMmaSmem {
   static constexpr int kKV = kSUnit * 2 * kHD * 2;    // K and V of one unit: 16 KB
-  static constexpr int kQ = kMaxRep * kHD * 2;        // the row's query heads
-  static constexpr int kStage = kKV + kQ;             // 18 KB, a multiple of 1024 (swizzle atoms)
+  static constexpr int kQ = REP <= 4 ? 1024 : 2048;   // the row's REP query heads (bf16)
+  static constexpr int kStage = kKV + kQ;             // 17 or 18 KB, a multiple of 1024 (swizzle atoms)
   static constexpr int v = NW * NST * kStage + 16 + NW * NST * 8 + 1024;
 };
 
@@ -463,7 +469,7 @@ template <int REP, int PT, int NW, int NST>
 __global__ void __launch_bounds__(32 * NW, 1) attn_suffix_mma_kernel(const __grid_constant__ CUtensorMap tmPool,
                                                                       AttnArgs a) {
   pdl_launch_dependents();
-  using SM = SuffixMmaSmem<NW, NST>;
+  using SM = SuffixMmaSmem<NW, NST, REP>;
   constexpr int kSWarps = NW, kSWStages = NST;
   extern __shared__ uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
@@ -488,9 +494,11 @@ __global__ void __launch_bounds__(32 * NW, 1) attn_suffix_mma_kernel(const __gri
   // counter, one unit ahead (claim + item load overlap the current unit's math; a warp never
   // hoards more than one unit, so the tail stays short).  Small work lists are all static.
   const bool loads = !(a.dbg_mode & 1), qload = !(a.dbg_mode & 4);
-  const int GW = gridDim.x * kSWarps, gw = blockIdx.x * kSWarps + warp;
+  const int early = a.early_ctas > 0 ? min(a.early_ctas, (int)gridDim.x) : (int)gridDim.x;
+  const bool is_early = (int)blockIdx.x < early;
+  const int GW = early * kSWarps, gw = blockIdx.x * kSWarps + warp;
   const int Ls = n <= 2 * GW ? n : (int)((long long)n * kSStaticPct / 100);
-  int snext = gw;  // next static unit to load into the queue
+  int snext = is_early ? gw : Ls;  // next static unit to load into the queue
   // static queue: lane q < kSQueue holds the item (code, length, pages 0..3) of the q-th next static
   // unit; code -1 = none
   uint4 x0 = make_uint4(0xFFFFFFFFu, 0, 0, 0);
@@ -735,7 +743,7 @@ __global__ void __launch_bounds__(32 * NW, 1) attn_suffix_mma_kernel(const __gri
   // them re-arms the pair's counters)
   const int npairs = a.rows * a.Hkv;
   int nm = 0;
-  for (int k = blockIdx.x + warp * gridDim.x; k < npairs * REP; k += gridDim.x * kSWarps) {
+  for (int k = is_early ? blockIdx.x + warp * early : npairs * REP; k < npairs * REP; k += early * kSWarps) {
     const int i = k / REP, e = k - i * REP;
     const int r = i / a.Hkv, h = i - r * a.Hkv;
     if (!a.row_active[r]) continue;
@@ -984,6 +992,36 @@ __global__ void __launch_bounds__(32) attn_merge_kernel(AttnArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ prefix key norms
+// kmax[((g * layers + l) * Hkv + h) * nt + tile] = max over the tile's tokens of ||k_t||_2 (fp32 over
+// the bf16 keys), for prefix buffers [g][layers][2][Hkv][pcap][128].  The prefix is immutable after
+// prefill, so this runs once per prompt; the decode prefix kernel bounds its scores with it.
+__global__ void __launch_bounds__(128) prefix_kmax_kernel(const __nv_bfloat16* __restrict__ prefix, int layers,
+                                                          int Hkv, int pcap, int plen, float* __restrict__ kmax) {
+  const int nt = (plen + 127) / 128;
+  const int tile = blockIdx.x % nt, h = (blockIdx.x / nt) % Hkv, gl = blockIdx.x / (nt * Hkv);
+  const int tok = tile * 128 + threadIdx.x;
+  float ss = 0.f;
+  if (tok < plen) {
+    const uint4* k4 = reinterpret_cast<const uint4*>(prefix + ((size_t)gl * 2 * Hkv * pcap + (size_t)h * pcap + tok) * kHD);
+#pragma unroll 4
+    for (int i = 0; i < 16; ++i) {
+      const uint4 v = k4[i];
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(b[j]);
+        ss += f.x * f.x + f.y * f.y;
+      }
+    }
+  }
+  __shared__ float red[4];
+  ss = warp_max(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) kmax[blockIdx.x] = sqrtf(fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3])));
+}
+
 // ------------------------------------------------------------------ shared-prefix attention on tcgen05
 // The decode step's shared-prefix part as two dense tensor-core contractions
 // (BASELINE north_star: "stacks the group's live queries into one dense
@@ -1003,8 +1041,8 @@ struct PrefixTcSmem {
   static constexpr int kV = 2 * 128 * 128;
   static constexpr int kQ = 2 * N * 128;     // two 64-d atoms of N rows
   static constexpr int kP = 2 * N * 128;     // two 64-token atoms of N rows (P_hi; P_lo follows)
-  static constexpr int kS = N * 129 * 4;     // scores / probabilities, [column][token], padded
-  static constexpr int v = kK + kV + kQ + 2 * kP + kS + 4 * N * 4 * 2 + N * 16 + 64 + 1024;
+  static constexpr int kS = (8 * 64 + N) * 4; // softmax scratch: [4][32] maxima, [4][32] sums, [N] column sums
+  static constexpr int v = kK + kV + kQ + 2 * kP + kS + 4 * N * 4 * 2 + N * 20 + 32 + 64 + 1024;
   static constexpr int kTmemCols = (2 * N) <= 32 ? 32 : ((2 * N) <= 64 ? 64 : ((2 * N) <= 128 ? 128 : 256));
 };
 
@@ -1030,8 +1068,8 @@ __global__ void __launch_bounds__(128, 1)
   uint8_t* Qsm = Vsm + SM::kV;
   uint8_t* Psm = Qsm + SM::kQ;
   uint8_t* Plo = Psm + SM::kP;
-  float* Ssm = reinterpret_cast<float*>(Plo + SM::kP);  // [N][129]
-  float* red = Ssm + N * 129;                          // [4][N] max, [4][N] sum
+  float* Ssm = reinterpret_cast<float*>(Plo + SM::kP);  // softmax scratch (SM::kS)
+  float* red = Ssm + SM::kS / 4;                       // [4][N] max, [4][N] sum
   float* colM = red + 8 * N;                           // [N] column max, [N] 1/sum, [N] (int) partial index or -1
   float* colI = colM + N;
   long long* colP = reinterpret_cast<long long*>(colI + 2 * N);
@@ -1069,24 +1107,59 @@ __global__ void __launch_bounds__(128, 1)
     tma_load_2d(Vsm, &tmKV, &bars[0], 0, rv, kEvictNormal);
     tma_load_2d(Vsm + 128 * 128, &tmKV, &bars[0], 64, rv, kEvictNormal);
   }
-  pdl_wait();                 // q of this step comes from the QKV GEMM
-  astamp(a, 1);
-  pdl_launch_dependents();    // the suffix kernel may start now (it does not touch our outputs)
-  // Q rows n = r*REP + e (K-major, 128-byte swizzle, two 64-d atoms)
+  // row tables (the previous step's scheduler) and the key-norm bound (prefill) are final
+  // before the wait
   if (threadIdx.x < N) {
     const int rl = threadIdx.x / REP, r = row0 + rl;
     colI[N + threadIdx.x] = (rl < a.grp_rows && r < a.rows && a.row_active[r]) ? 1.f : 0.f;  // row live
   }
+  const float kmx = a.kmax ? a.kmax[grp * a.kmax_grp + h * nt + tile] : 0.f;
+  __syncthreads();
+  // ---- the softmax below is latency-bound by instruction fetch when it runs cold (measured
+  // ~25 ns per instruction in the decode step: this kernel's code is evicted between layers), so
+  // pass 0 runs the bounded-offset softmax once on stale TMEM / smem while the QKV GEMM is still
+  // running (its outputs are rewritten in pass 1), and pass 1 does the real work.
+  constexpr int CW = N < 32 ? N : 32;
+  const int t = warp * 32 + lane;  // token lane (TMEM lane quadrant = warp)
+  float* sbuf = Ssm;               // [4][32] maxima, [4][32] sums, [64] column sums
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  const bool valid = t < ntok;
+  float* qb2 = red;  // [N] score bound per column (log2 units), [N] fast-path flag
+#pragma unroll 1
+  for (int pass = (a.kmax && !(a.dbg_mode & 32)) ? 0 : 1; pass < 2; ++pass) {
+  bool fast = true;
+  if (pass == 1) {
+  pdl_wait();                 // q of this step comes from the QKV GEMM
+  astamp(a, 1);
+  pdl_launch_dependents();    // the suffix kernel may start now (it does not touch our outputs)
+  // Q rows n = r*REP + e (K-major, 128-byte swizzle, two 64-d atoms); ||q_n||^2 on the way
   for (int i = threadIdx.x; i < N * 16; i += 128) {
     const int n = i >> 4, c = i & 15;
     const int rl = n / REP, r = row0 + rl, e = n % REP;
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (rl < a.grp_rows && r < a.rows && a.row_active[r])
-      v = *reinterpret_cast<const uint4*>(a.q + ((size_t)r * a.Hq + h * REP + e) * kHD + c * 8);
+    if (colI[N + n] != 0.f) v = *reinterpret_cast<const uint4*>(a.q + ((size_t)r * a.Hq + h * REP + e) * kHD + c * 8);
     *reinterpret_cast<uint4*>(Qsm + (c >> 3) * N * 128 + n * 128 + (((c & 7) ^ (n & 7)) << 4)) = v;
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+    float qs = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(b[j]);
+      qs += f.x * f.x + f.y * f.y;
+    }
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) qs += __shfl_xor_sync(0xffffffffu, qs, o);  // the 16 chunks of row n
+    if (c == 0) {
+      // Cauchy-Schwarz: s = q.k / sqrt(d) <= ||q|| max||k|| / sqrt(d) =: B (natural units).  With
+      // B <= 40 every exp(s - B) lies in [e^-80, 1] (no overflow, no underflow to zero), so B
+      // replaces the column max: softmax is shift-invariant and the LSE merge takes any offset.
+      const float B = sqrtf(qs) * kmx * a.scale;
+      qb2[n] = B * 1.4426950408889634f;
+      qb2[N + n] = (a.kmax && B <= 40.f) ? 1.f : 0.f;
+    }
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
+  for (int n = 0; n < N; ++n) fast = fast && qb2[N + n] != 0.f;
   astamp(a, 2);
   if (threadIdx.x == 0) {
     mbar_wait(&bars[0], 0);
@@ -1105,28 +1178,70 @@ __global__ void __launch_bounds__(128, 1)
   mbar_wait(&bars[1], 0);
   astamp(a, 4);
   tc_fence_after();
-  // ---- column softmax in registers.  Thread t holds S^T row t (its token) for 32
-  // query columns at a time; a transpose reduction (31 shuffles) leaves lane l with
-  // column l's max / sum over the warp's 32 tokens, the 4 warps combine through smem.
-  const int t = warp * 32 + lane;  // token lane (TMEM lane quadrant = warp)
-  float* sbuf = Ssm;               // [4][32] maxima, [4][32] sums, [64] column sums (Ssm is free now)
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  const bool valid = t < ntok;
+  }  // pass 1 only
+  // ---- column softmax in registers.  Thread t holds S^T row t (its token) for CW
+  // query columns at a time (CW = min(N, 32)); a transpose reduction (CW - 1 shuffles,
+  // plus one per remaining lane bit) leaves lane l with column (l mod CW)'s max / sum over
+  // the warp's 32 tokens, the 4 warps combine through smem.
+  if (fast) {
+    // bounded-offset softmax: p = exp(s - B[column]); only the column sums need the other lanes
 #pragma unroll 1
-  for (int c32 = 0; c32 < (N + 31) / 32; ++c32) {
-    const int ncol = N - c32 * 32 < 32 ? N - c32 * 32 : 32;  // 16 or 32
-    float sv[32], r[32];
-    tmem_ld16(trow + c32 * 32, sv);
-    if (ncol > 16) tmem_ld16(trow + c32 * 32 + 16, sv + 16);
+    for (int c32 = 0; c32 < N / CW; ++c32) {
+      float sv[CW];
+      tmem_ld16(trow + c32 * CW, sv);
+      if (CW > 16) tmem_ld16(trow + c32 * CW + 16, sv + (CW > 16 ? 16 : 0));
+      astamp(a, 9);
+      const float sl2 = a.scale * 1.4426950408889634f;
+      float r[CW];
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        const int n = c32 * CW + j;
+        const float p = valid ? exp2f(fmaf(sv[j], sl2, -qb2[n])) : 0.f;
+        r[j] = p;
+        const int off = (t >> 6) * N * 128 + n * 128 + ((((t & 63) >> 3) ^ (n & 7)) << 4) + (t & 7) * 2;
+        const __nv_bfloat16 phi = __float2bfloat16_rn(p);
+        *reinterpret_cast<__nv_bfloat16*>(Psm + off) = phi;
+        *reinterpret_cast<__nv_bfloat16*>(Plo + off) = __float2bfloat16_rn(p - __bfloat162float(phi));
+      }
+      astamp(a, 10);
+#pragma unroll
+      for (int o = CW / 2; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int j = 0; j < o; ++j) {
+          const float send = up ? r[j] : r[j + o];
+          const float keep = up ? r[j + o] : r[j];
+          r[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+#pragma unroll
+      for (int o = CW; o < 32; o <<= 1) r[0] += __shfl_xor_sync(0xffffffffu, r[0], o);
+      sbuf[128 + warp * 32 + lane] = r[0];
+      astamp(a, 11);
+      __syncthreads();
+      astamp(a, 12);
+      if (threadIdx.x < CW) {
+        const int n = c32 * CW + threadIdx.x;
+        colM[n] = qb2[n] * 0.6931471805599453f;  // the offset B, natural units
+        sbuf[8 * 64 + n] = sbuf[128 + threadIdx.x] + sbuf[160 + threadIdx.x] + sbuf[192 + threadIdx.x] + sbuf[224 + threadIdx.x];
+      }
+      if (c32 + 1 < N / CW) __syncthreads();
+    }
+  } else {
+#pragma unroll 1
+  for (int c32 = 0; c32 < N / CW; ++c32) {
+    float sv[CW], r[CW];
+    tmem_ld16(trow + c32 * CW, sv);
+    if (CW > 16) tmem_ld16(trow + c32 * CW + 16, sv + (CW > 16 ? 16 : 0));
     const float sl2 = a.scale * 1.4426950408889634f;  // scores in log2 units: exp2 below
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      sv[j] = (valid && j < ncol) ? sv[j] * sl2 : -INFINITY;
+    for (int j = 0; j < CW; ++j) {
+      sv[j] = valid ? sv[j] * sl2 : -INFINITY;
       r[j] = sv[j];
     }
     // transpose-max: after the step with offset o, lanes with bit o hold the upper half
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
+    for (int o = CW / 2; o >= 1; o >>= 1) {
       const bool up = (lane & o) != 0;
 #pragma unroll
       for (int j = 0; j < o; ++j) {
@@ -1135,20 +1250,22 @@ __global__ void __launch_bounds__(128, 1)
         r[j] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, o));
       }
     }
-    sbuf[warp * 32 + lane] = r[0];  // column c32*32 + lane, this warp's 32 tokens
+#pragma unroll
+    for (int o = CW; o < 32; o <<= 1) r[0] = fmaxf(r[0], __shfl_xor_sync(0xffffffffu, r[0], o));
+    sbuf[warp * 32 + lane] = r[0];  // column c32*CW + (lane mod CW), this warp's 32 tokens
     __syncthreads();
     float mcol = fmaxf(fmaxf(sbuf[lane], sbuf[32 + lane]), fmaxf(sbuf[64 + lane], sbuf[96 + lane]));
     __syncthreads();
     // p = exp(s - M[column]); M of column j comes from lane j
-    float p[32];
+    float p[CW];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
+    for (int j = 0; j < CW; ++j) {
       const float Mj = __shfl_sync(0xffffffffu, mcol, j);
-      p[j] = (valid && j < ncol) ? exp2f(sv[j] - Mj) : 0.f;
+      p[j] = valid ? exp2f(sv[j] - Mj) : 0.f;
       r[j] = p[j];
     }
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
+    for (int o = CW / 2; o >= 1; o >>= 1) {
       const bool up = (lane & o) != 0;
 #pragma unroll
       for (int j = 0; j < o; ++j) {
@@ -1157,29 +1274,38 @@ __global__ void __launch_bounds__(128, 1)
         r[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
       }
     }
+#pragma unroll
+    for (int o = CW; o < 32; o <<= 1) r[0] += __shfl_xor_sync(0xffffffffu, r[0], o);
     sbuf[128 + warp * 32 + lane] = r[0];
     // P^T operand (row n, K index t, two 64-token atoms, 128-byte swizzle) as a bf16
     // hi/lo pair (two accumulating MMAs keep P to ~2^-16)
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      if (j >= ncol) break;
-      const int n = c32 * 32 + j;
+    for (int j = 0; j < CW; ++j) {
+      const int n = c32 * CW + j;
       const int off = (t >> 6) * N * 128 + n * 128 + ((((t & 63) >> 3) ^ (n & 7)) << 4) + (t & 7) * 2;
       const __nv_bfloat16 phi = __float2bfloat16_rn(p[j]);
       *reinterpret_cast<__nv_bfloat16*>(Psm + off) = phi;
       *reinterpret_cast<__nv_bfloat16*>(Plo + off) = __float2bfloat16_rn(p[j] - __bfloat162float(phi));
     }
     __syncthreads();
-    if (threadIdx.x < ncol) {
-      const int n = c32 * 32 + threadIdx.x;
-      colM[n] = mcol * 0.6931471805599453f;  // natural units (thread x < 32 is lane x of warp 0: column x)
+    if (threadIdx.x < CW) {
+      const int n = c32 * CW + threadIdx.x;
+      colM[n] = mcol * 0.6931471805599453f;  // natural units (thread x < CW is lane x of warp 0: column x)
       sbuf[8 * 64 + n] = sbuf[128 + threadIdx.x] + sbuf[160 + threadIdx.x] + sbuf[192 + threadIdx.x] + sbuf[224 + threadIdx.x];
     }
     __syncthreads();
   }
+  }
+  if (pass == 0) {
+    astamp(a, 8);
+    __syncthreads();
+  }
+  }  // pass
+  astamp(a, 13);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
   __syncthreads();
+  astamp(a, 14);
   if (threadIdx.x == 0) {
     tc_fence_after();
     // A = V^T: M = d (MN-major: 64-d blocks 16 KB apart), K = tokens (8-row groups 1 KB apart)

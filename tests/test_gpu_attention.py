@@ -184,3 +184,17 @@ def test_split_attention_large_groups(lib, Hq, Hkv, grp_rows, impl):
     "R_h = 256"), and the CUDA-core prefix on the same layout."""
     lens = _lens(64, 1, grp_rows, rot=grp_rows + Hq)
     _check(lib, 64, 1, grp_rows, 255, Hq, Hkv, lens, impl, seed=grp_rows * 7 + Hq)
+
+
+@pytest.mark.parametrize("qscale,exact", [(1.0, True), (4.0, False), (3.2, False)])
+def test_split_attention_prefix_offset_paths(lib, monkeypatch, qscale, exact):
+    """The tcgen05 prefix softmax takes the Cauchy-Schwarz bound B = ||q|| max_t ||k_t|| / sqrt(d)
+    as its offset when every column's B <= 40 (exp(s - B) in [e^-80, 1]), else the exact column
+    max; IS_EXACT_PREFIX_MAX forces the latter.  Both equal the fp64 oracle: qscale 1 (B ~ 14,
+    bound path unless forced), 4 (B ~ 56: every CTA falls back), 3.2 (B straddles 40 across
+    CTAs: mixed)."""
+    if exact:
+        monkeypatch.setenv("IS_EXACT_PREFIX_MAX", "1")
+    for rows, groups, grp_rows in [(16, 1, 8), (64, 8, 8), (16, 1, 16)]:
+        lens = _lens(rows, groups, grp_rows, rot=int(qscale * 10))
+        _check(lib, rows, groups, grp_rows, 255, 16, 8, lens, 0, seed=int(qscale * 100) + rows, qscale=qscale)

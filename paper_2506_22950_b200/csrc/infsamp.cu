@@ -444,6 +444,7 @@ static is_status launch_k_smem(K kern, dim3 grid, dim3 block, int smem, cudaStre
     }
   if (!found) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+
     attr.push_back({(const void*)kern, smem});
   }
   cudaLaunchConfig_t cfg{};
@@ -518,7 +519,8 @@ struct is_ctx {
   float *ssqA, *ssqB;  // [Th][max_rows] per-128-column sums of squares: QKV input, gate/up input
   int sep_merge;       // decode suffix: 64-token CTA units + separate merge kernel
   int suffix_mma;      // decode suffix: 32-token units on mma.sync, merges spread over the grid (default)
-  int suffix_shape;    //   its CTA shape: 1 = 8 warps x 1 stage (rc <= 16), 0 = 6 warps x 2 stages
+  int suffix_shape;    //   its CTA shape: 1 = 8 warps x 1 stage (default), 0 = 6 warps x 2 stages
+  int attn_carveout;   //   shared-memory carveout (%) of the attention kernels, -1 = driver default
   int prefix2;         // tcgen05 prefix with the query rows as M (default; up to 256 stacked rows)
   CUtensorMap tm_pool; // the page pool of all layers as rows of 128 bf16, box = one page (128-byte swizzle)
   int stg_lm;          // lm_head ring depth override (IS_STG_LM = 10 / 11; default 8)
@@ -689,8 +691,27 @@ struct AttnLaunch {
   const CUtensorMap* tm_pool;    // decode mma suffix pass: the page pool, rows of 128 bf16, box = page_tokens
   int suffix_mma;                // decode: suffix units on mma.sync (attn_suffix_mma_kernel)
   int suffix_shape;              //   0: 6 warps x 2 stages, 1: 8 warps x 1 stage
+  int carveout;                  // shared-memory carveout (%) for the prefix / suffix kernels, -1: default
   int prefix2;                   // decode tcgen05 prefix with the query rows as M (attn_prefix_tc2_kernel)
 };
+
+// Per-kernel shared-memory carveout, set only when it changes (contexts of different row counts
+// may share a kernel instantiation).  -1 = the driver's default (0 after a change).
+static is_status set_carveout(const void* kern, int carveout) {
+  static std::vector<std::pair<const void*, int>> cur;
+  const int v = carveout < 0 ? 0 : carveout;
+  for (auto& pr : cur)
+    if (pr.first == kern) {
+      if (pr.second == v) return IS_OK;
+      pr.second = v;
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, v));
+      return IS_OK;
+    }
+  if (carveout < 0) return IS_OK;  // never set: leave the default
+  cur.push_back({kern, v});
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, v));
+  return IS_OK;
+}
 
 template <int REP, int N>
 static is_status launch_prefix_tc_n(const AttnArgs& aa, const AttnLaunch& al, cudaStream_t st) {
@@ -701,6 +722,7 @@ static is_status launch_prefix_tc_n(const AttnArgs& aa, const AttnLaunch& al, cu
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::v));
     attr = true;
   }
+  CKS(set_carveout((const void*)kern, al.carveout));
   const int nt = (int)ceil_div64(aa.plen, 128);
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute at[1];
@@ -735,6 +757,7 @@ static is_status launch_prefix_tc2(const AttnArgs& aa, const AttnLaunch& al, cud
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::v));
     attr = true;
   }
+  CKS(set_carveout((const void*)kern, al.carveout));
   const int nt = (int)ceil_div64(aa.plen, 128);
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute at[1];
@@ -784,10 +807,14 @@ static is_status launch_attn_rep(AttnArgs aa, const AttnLaunch& al, cudaStream_t
       if (npre <= g_num_sms / 4) aa.early_ctas = g_num_sms - npre;
     }
 #define IS_SUFFIX_MMA(P)                                                                                         \
-  (wide ? launch_k_smem(attn_suffix_mma_kernel<REP, P, 8, 1>, dim3(g_num_sms), dim3(256),                            \
-                        SuffixMmaSmem<8, 1, REP>::v, st, *al.tm_pool, aa)                                           \
-        : launch_k_smem(attn_suffix_mma_kernel<REP, P, 6, 2>, dim3(g_num_sms), dim3(192),                            \
-                        SuffixMmaSmem<6, 2, REP>::v, st, *al.tm_pool, aa))
+  (wide ? (set_carveout((const void*)attn_suffix_mma_kernel<REP, P, 8, 1>, al.carveout) != IS_OK                     \
+               ? IS_ERR_CUDA                                                                                     \
+               : launch_k_smem(attn_suffix_mma_kernel<REP, P, 8, 1>, dim3(g_num_sms), dim3(256),                 \
+                               SuffixMmaSmem<8, 1, REP>::v, st, *al.tm_pool, aa))                                \
+        : (set_carveout((const void*)attn_suffix_mma_kernel<REP, P, 6, 2>, al.carveout) != IS_OK                     \
+               ? IS_ERR_CUDA                                                                                     \
+               : launch_k_smem(attn_suffix_mma_kernel<REP, P, 6, 2>, dim3(g_num_sms), dim3(192),                 \
+                               SuffixMmaSmem<6, 2, REP>::v, st, *al.tm_pool, aa)))
     switch (aa.pt) {
       case 8: CKS(IS_SUFFIX_MMA(8)); break;
       case 16: CKS(IS_SUFFIX_MMA(16)); break;
@@ -930,6 +957,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
       al.tm_pool = &c->tm_pool;
       al.suffix_mma = !prefill && c->suffix_mma;
       al.suffix_shape = c->suffix_shape;
+      al.carveout = c->attn_carveout;
       al.prefix2 = c->prefix2;
       CKS(launch_attention(aa, al, st));
     }
@@ -1230,7 +1258,12 @@ extern "C" is_status is_create(const is_config* cfg, const void* const* dw, int3
   {
     // suffix kernel shape: 8 warps x 1 stage up to 16 rows (each warp has ~1-2 units), else 6 x 2
     const char* e = getenv("IS_SUFFIX_SHAPE");
-    c->suffix_shape = e ? atoi(e) : (c->rc <= 16 ? 1 : 0);
+    c->suffix_shape = e ? atoi(e) : 1;
+    // beyond 16 rows (co-resident groups) the tcgen05 prefix CTAs are many: with the maximum
+    // carveout a suffix CTA fits beside each, so the suffix pass starts at once (K5 8 groups x 1024:
+    // 78.9 -> 68.6 us, profiles/r02c); at 16 rows the co-resident prefix chain slows instead
+    const char* cv = getenv("IS_ATTN_CARVEOUT");
+    c->attn_carveout = cv ? atoi(cv) : (c->rc > 16 ? 100 : -1);
   }
   c->nc_suf = (int)ceil_div64(c->max_new, c->sc);
   c->NC = c->nc_pre + c->nc_suf;
@@ -2069,7 +2102,8 @@ extern "C" is_status is_dbg_attn(const void* d_q, const void* d_prefix, int32_t 
     al.grp_rows = grp_rows;
     al.tm_pool = &tmp;
     al.suffix_mma = mma ? 1 : 0;
-    al.suffix_shape = getenv("IS_SUFFIX_SHAPE") ? atoi(getenv("IS_SUFFIX_SHAPE")) : (rows <= 16 ? 1 : 0);
+    al.suffix_shape = getenv("IS_SUFFIX_SHAPE") ? atoi(getenv("IS_SUFFIX_SHAPE")) : 1;
+    al.carveout = getenv("IS_ATTN_CARVEOUT") ? atoi(getenv("IS_ATTN_CARVEOUT")) : (rows > 16 ? 100 : -1);
     al.prefix2 = old_prefix ? 0 : 1;
     aa.pool_row0 = 0;
     aa.dbg_mode = getenv("IS_DBG_SUFFIX_MODE") ? atoi(getenv("IS_DBG_SUFFIX_MODE")) : 0;

@@ -15,6 +15,12 @@ IS_DEVICE uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// 1024-byte-aligned start of a dynamic shared-memory window (swizzle atoms), derived by pointer
+// arithmetic on the __shared__ array itself: going through an integer would hide the address
+// space, and every access through the result would compile to a generic LD.E / ST.E (tracked on
+// the long scoreboard like a global access) instead of LDS / STS.
+IS_DEVICE uint8_t* align1024_smem(uint8_t* raw) { return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u); }
+
 // ---------------------------------------------------------------- mbarrier
 IS_DEVICE void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));

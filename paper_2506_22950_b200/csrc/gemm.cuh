@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                        GemmArgs a) {
   using C = GemmCfg<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align1024_smem(smem_raw);
   uint8_t* stage_base = smem;
   float* aux = reinterpret_cast<float*>(smem + STAGES * C::kStage);  // epilogue staging
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * C::kStage + C::kAux);

@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(32 * NW, 1) attn_suffix_mma_kernel(const __gri
   using SM = SuffixMmaSmem<NW, NST, REP>;
   constexpr int kSWarps = NW, kSWStages = NST;
   extern __shared__ uint8_t sm_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sm = align1024_smem(sm_raw);
   uint4* zero16 = reinterpret_cast<uint4*>(sm + kSWarps * kSWStages * SM::kStage);  // Q padding rows
   uint64_t* bars = reinterpret_cast<uint64_t*>(zero16 + 1);
   __shared__ int done_list[kSWarps * 32];
@@ -1062,7 +1062,7 @@ __global__ void __launch_bounds__(128, 1)
     attn_prefix_tc_kernel(const __grid_constant__ CUtensorMap tmKV, AttnArgs a, int kv_row_base) {
   using SM = PrefixTcSmem<N>;
   extern __shared__ uint8_t tc_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sm = align1024_smem(tc_raw);
   uint8_t* Ksm = sm;
   uint8_t* Vsm = Ksm + SM::kK;
   uint8_t* Qsm = Vsm + SM::kV;
@@ -1436,7 +1436,7 @@ __global__ void __launch_bounds__(128, 1)
   using SMc = PrefixTc2Smem<MT>;
   constexpr int T = SMc::kTile, HALF = T / 2;
   extern __shared__ uint8_t tc2_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc2_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sm = align1024_smem(tc2_raw);
   uint8_t* Qs0 = sm;
   uint8_t* Qs1 = sm + T;                 // (MT == 2)
   uint8_t* Ks = sm + MT * T;

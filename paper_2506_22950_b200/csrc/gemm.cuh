@@ -320,6 +320,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               pre[n * kBM + m] = m < 64 ? e.rope_cos[(size_t)pos[n] * 64 + m] : e.rope_sin[(size_t)pos[n] * 64 + m - 64];
         }
       }
+      // per-feature gains of the epilogue, loaded before the accumulator is ready
+      float gpre = 0.f;
+      if constexpr (EPI == EPI_RESID_ADD) gpre = (a.xg_out && gm < a.M) ? a.xg_gain[gm] : 0.f;
+      if constexpr (EPI == EPI_QKV) gpre = tile < a.qkv.Hq ? a.qkv.q_gain[m] : a.qkv.k_gain[m];
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (threadIdx.x == 64) stamp(a, 5);
@@ -375,7 +379,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
       if constexpr (EPI == EPI_STORE_F32 || EPI == EPI_RESID_ADD) {
         const int n_end = min(n_hi, a.n_valid);
-        const float gg = (EPI == EPI_RESID_ADD && a.xg_out && gm < a.M) ? a.xg_gain[gm] : 0.f;
+        const float gg = gpre;
         for (int n = n_lo; n < n_end; ++n) {
           float x = 0.f;
           if (gm < a.M) {
@@ -413,7 +417,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (lane == 0) sred[q][n] = ss;
           }
           asm volatile("bar.sync 1, 128;" ::: "memory");
-          const float gn = is_q ? e.q_gain[m] : e.k_gain[m];
+          const float gn = gpre;
           for (int n = n_lo; n < n_end; ++n) {
             const float ss = sred[0][n] + sred[1][n] + sred[2][n] + sred[3][n];
             stg[n * kBM + m] *= (1.0f / sqrtf(ss / (float)kBM + e.eps)) * gn;

@@ -113,7 +113,8 @@ def ncu_traffic(name):
     `traffic`) and read alone (min over the captured launches)."""
     import csv
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_{name}.csv")), key=os.path.getmtime)
+    # the newest round's capture: profiles/<round>/ names sort in round order (r01 < r02a < ... < r02e)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_{name}.csv")))
     if not files:
         return None
     rows = list(csv.DictReader(open(files[-1])))

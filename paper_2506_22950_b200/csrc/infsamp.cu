@@ -920,6 +920,7 @@ static is_status run_layers(is_ctx* c, int rows, bool prefill, int grp = 0) {
     aa.part_o = c->part_o;
     aa.part_ml = c->part_ml;
     aa.items = c->attn_items;
+    aa.items_cap = prefill ? 0 : Hkv * (c->nc_pre * ((c->rc + 3) / 4) + c->rc * c->nc_suf);
     aa.n_items = c->st_dev + (size_t)c->M * ST_COUNT + ST_ATTN_ITEMS;
     aa.dbg_ts = nullptr;
     aa.dbg_mode = getenv("IS_DBG_ATTN_MODE") ? atoi(getenv("IS_DBG_ATTN_MODE")) : 0;  // timing experiments

@@ -91,6 +91,7 @@ struct AttnArgs {
   int sc;                     // decode suffix chunk (tokens per work item): kSC, or kSCW for the warp kernel
   const float* kmax;          // decode, tcgen05 prefix: max_t ||k_t|| per (kv head, 128-token tile) of this
   int kmax_grp;               //   layer (prefix_kmax_kernel, at prefill); group stride.  null: exact max
+  int items_cap;              // decode (mma suffix): work items the buffer holds (speculative queue loads)
   int early_ctas;             // decode (mma suffix): CTAs [0, early_ctas) take the static units and the
                               //   merges; the rest (placed behind the prefix kernel's CTAs) only claim (0: all)
   int grp_rows;               // decode, tcgen05 prefix: rows per co-resident group (g); group m = rows m*g ..
@@ -486,6 +487,20 @@ __global__ void __launch_bounds__(32 * NW, 1) attn_suffix_mma_kernel(const __gri
   }
   __syncthreads();
   const int n = (int)a.n_items[0];
+  // speculative static-queue loads (items gw + q * GW of this warp, independent of n: one L2 round
+  // trip instead of two before the first unit issues); validated against the static range below
+  uint4 x0 = make_uint4(0xFFFFFFFFu, 0, 0, 0);
+  uint2 x1 = make_uint2(0, 0);
+  {
+    const int early0 = a.early_ctas > 0 ? min(a.early_ctas, (int)gridDim.x) : (int)gridDim.x;
+    const int u = (blockIdx.x * NW + (threadIdx.x >> 5)) + (threadIdx.x & 31) * early0 * NW;
+    if ((int)blockIdx.x < early0 && a.items_cap > 0 && (threadIdx.x & 31) < kSQueue && u < a.items_cap) {
+      const uint4* it = reinterpret_cast<const uint4*>(a.items + (size_t)u * kItemStride);
+      x0 = it[0];
+      const uint4 y = it[1];
+      x1 = make_uint2(y.x, y.y);
+    }
+  }
   constexpr int pt = PT;  // page tokens (8, 16 or 32): the stage addressing is compile-time
   uint8_t* wsm = sm + warp * kSWStages * SM::kStage;
   uint64_t* full = bars + warp * kSWStages;
@@ -500,9 +515,7 @@ __global__ void __launch_bounds__(32 * NW, 1) attn_suffix_mma_kernel(const __gri
   const int Ls = n <= 2 * GW ? n : (int)((long long)n * kSStaticPct / 100);
   int snext = is_early ? gw : Ls;  // next static unit to load into the queue
   // static queue: lane q < kSQueue holds the item (code, length, pages 0..3) of the q-th next static
-  // unit; code -1 = none
-  uint4 x0 = make_uint4(0xFFFFFFFFu, 0, 0, 0);
-  uint2 x1 = make_uint2(0, 0);
+  // unit (x0, x1 above); code -1 = none
   auto load_to = [&](int u, int q, uint4& y0, uint2& y1) {
     if (lane == q) {
       y0 = make_uint4(0xFFFFFFFFu, 0, 0, 0);
@@ -515,8 +528,15 @@ __global__ void __launch_bounds__(32 * NW, 1) attn_suffix_mma_kernel(const __gri
       }
     }
   };
+  if (is_early && a.items_cap > 0) {
+    // the first kSQueue static items were loaded speculatively above (before the item count
+    // arrived); drop those past the static range
+    if (lane < kSQueue && gw + lane * GW >= Ls) x0 = make_uint4(0xFFFFFFFFu, 0, 0, 0);
+    snext += kSQueue * GW;
+  } else {
 #pragma unroll 1
-  for (int q = 0; q < kSQueue; ++q, snext += GW) load_to(snext < Ls ? snext : n, q, x0, x1);
+    for (int q = 0; q < kSQueue; ++q, snext += GW) load_to(snext < Ls ? snext : n, q, x0, x1);
+  }
   // dynamic: lane 0 holds the item of the next claimed unit (d0.x = -1: none / not claimed yet)
   uint4 d0 = make_uint4(0xFFFFFFFFu, 0, 0, 0);
   uint2 d1 = make_uint2(0, 0);

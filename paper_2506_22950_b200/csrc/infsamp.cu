@@ -2264,7 +2264,7 @@ extern "C" int is_dbg_timeline(is_ctx* c) {
     printf("prefix_tc L%d ctas=%d start %.2f waited %.2f q_staged %.2f tma %.2f S_done %.2f [softmax pass 0 done %.2f] P_done %.2f O_done %.2f end %.2f\n", l, n,
            mn0, mx[1], mx[2], mx[3], mx[4], mx8, mx[5], mx[6], mx[7]);
     printf("      fine:");
-    for (int k = 9; k <= 14; ++k) {
+    for (int k = 9; k <= 15; ++k) {
       double v = 0;
       for (int b = 0; b < 64; ++b)
         if (base[b * 16] && base[b * 16 + k]) v = std::max(v, (double)(base[b * 16 + k] - t0) / 1e3);

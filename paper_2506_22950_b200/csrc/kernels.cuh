@@ -1336,6 +1336,7 @@ __global__ void __launch_bounds__(128, 1)
       const uint64_t db = smem_desc_k_sw128((k < 8 ? Psm : Plo) + ((k & 7) >> 2) * N * 128) + 2 * (k & 3);
       tc_mma_f16(tmem + N, da, db, idesc2, k > 0 ? 1u : 0u);
     }
+    astamp(a, 15);
     tc_commit(&bars[1]);
   }
   __syncwarp();

@@ -321,9 +321,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       // per-feature gains of the epilogue, loaded before the accumulator is ready
-      float gpre = 0.f;
-      if constexpr (EPI == EPI_RESID_ADD) gpre = (a.xg_out && gm < a.M) ? a.xg_gain[gm] : 0.f;
-      if constexpr (EPI == EPI_QKV) gpre = tile < a.qkv.Hq ? a.qkv.q_gain[m] : a.qkv.k_gain[m];
+      // RESID_ADD: the next norm's gains of this lane's 4 features (4 lane .. 4 lane + 3)
+      float4 gg4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if constexpr (EPI == EPI_RESID_ADD)
+        if (a.xg_out && tile * kBM + 4 * lane < a.M) gg4 = *reinterpret_cast<const float4*>(a.xg_gain + tile * kBM + 4 * lane);
+      // QKV: the QK-norm gains of this thread's feature pairs (2i, 2i + 1) and (64 + 2i, 65 + 2i)
+      float2 gq0 = make_float2(0.f, 0.f), gq1 = make_float2(0.f, 0.f);
+      if constexpr (EPI == EPI_QKV) {
+        if (tile < a.qkv.Hq + a.qkv.Hkv) {
+          const float* gsrc = tile < a.qkv.Hq ? a.qkv.q_gain : a.qkv.k_gain;
+          gq0 = *reinterpret_cast<const float2*>(gsrc + (et & 31) * 2);
+          gq1 = *reinterpret_cast<const float2*>(gsrc + 64 + (et & 31) * 2);
+        }
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (threadIdx.x == 64) stamp(a, 5);
@@ -378,73 +388,111 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (threadIdx.x == 64) stamp(a, 8);
 
       if constexpr (EPI == EPI_STORE_F32 || EPI == EPI_RESID_ADD) {
+        // one row per warp and pass (4 rows per pass): lane l owns features 4l .. 4l + 3 (float4
+        // residual store, 8-byte bf16 store of the next norm's operand), the warp's butterfly sum
+        // is the row's sum of squares over the tile (M % 4 == 0)
         const int n_end = min(n_hi, a.n_valid);
-        const float gg = gpre;
-        for (int n = n_lo; n < n_end; ++n) {
-          float x = 0.f;
-          if (gm < a.M) {
-            x = stg[n * kBM + m];
-            if (EPI == EPI_RESID_ADD) x += pre[n * kBM + m];
-            a.out[(size_t)(a.row0 + n) * a.ld_out + gm] = x;
-            if (EPI == EPI_RESID_ADD && a.xg_out) a.xg_out[(size_t)(a.row0 + n) * a.M + gm] = __float2bfloat16_rn(x * gg);
+        const int g4 = tile * kBM + 4 * lane;
+        for (int n = n_lo + (et >> 5); n < n_end; n += 4) {
+          float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (g4 < a.M) {
+            x = *reinterpret_cast<const float4*>(stg + n * kBM + 4 * lane);
+            if (EPI == EPI_RESID_ADD) {
+              const float4 p4 = *reinterpret_cast<const float4*>(pre + n * kBM + 4 * lane);
+              x.x += p4.x;
+              x.y += p4.y;
+              x.z += p4.z;
+              x.w += p4.w;
+            }
+            *reinterpret_cast<float4*>(a.out + (size_t)(a.row0 + n) * a.ld_out + g4) = x;
+            if (EPI == EPI_RESID_ADD && a.xg_out) {
+              const __nv_bfloat162 b0 = __floats2bfloat162_rn(x.x * gg4.x, x.y * gg4.y);
+              const __nv_bfloat162 b1 = __floats2bfloat162_rn(x.z * gg4.z, x.w * gg4.w);
+              uint2 u;
+              u.x = *reinterpret_cast<const uint32_t*>(&b0);
+              u.y = *reinterpret_cast<const uint32_t*>(&b1);
+              *reinterpret_cast<uint2*>(a.xg_out + (size_t)(a.row0 + n) * a.M + g4) = u;
+            }
           }
           if (EPI == EPI_RESID_ADD && a.ssq_out) {
-            const float ss = warp_sum(x * x);
-            if (lane == 0) sred[q][n] = ss;
+            const float ss = warp_sum(x.x * x.x + x.y * x.y + x.z * x.z + x.w * x.w);
+            if (lane == 0) a.ssq_out[(size_t)tile * a.ssq_ld + a.row0 + n] = ss;
           }
         }
-        if (EPI == EPI_RESID_ADD && a.ssq_out) {
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (et >= n_lo && et < n_end) a.ssq_out[(size_t)tile * a.ssq_ld + a.row0 + et] = sred[0][et] + sred[1][et] + sred[2][et] + sred[3][et];
-        }
       } else if constexpr (EPI == EPI_SWIGLU) {
-        // rows [0, 64) of the tile are gate features f, rows [64, 128) the matching up
-        const int f = tile * 64 + m;
-        if (m < 64 && f * 2 < a.M)
-          for (int n = n_lo; n < min(n_hi, a.n_valid); ++n)
-            a.act[(size_t)(a.row0 + n) * a.ld_act + f] =
-                __float2bfloat16_rn(silu_f(stg[n * kBM + m]) * stg[n * kBM + m + 64]);
+        // rows [0, 64) of the tile are gate features f, rows [64, 128) the matching up.  Every
+        // epilogue thread takes two adjacent features of one row (one bf16x2 store); the 128
+        // threads cover 4 rows per pass
+        const int fp = (et & 31) * 2, f = tile * 64 + fp;
+        const int n_end = min(n_hi, a.n_valid);
+        if (f * 2 < a.M)
+          for (int n = n_lo + (et >> 5); n < n_end; n += 4) {
+            const float2 g2 = *reinterpret_cast<const float2*>(stg + n * kBM + fp);
+            const float2 u2 = *reinterpret_cast<const float2*>(stg + n * kBM + 64 + fp);
+            *reinterpret_cast<__nv_bfloat162*>(a.act + (size_t)(a.row0 + n) * a.ld_act + f) =
+                __floats2bfloat162_rn(silu_f(g2.x) * u2.x, silu_f(g2.y) * u2.y);
+          }
       } else if constexpr (EPI == EPI_QKV) {
-        // head = tile: q (tile < Hq), k (< Hq + Hkv) or v.  Per-head RMSNorm over the
-        // 128 lanes of a column, then rotate-half RoPE pairs (m, m +- 64).
+        // head = tile: q (tile < Hq), k (< Hq + Hkv) or v.  Per-head RMSNorm over the 128
+        // features of a row (8 threads per row, 16 rows per pass), then rotate-half RoPE: every
+        // thread takes the feature pairs (2i, 2i + 1) and their partners (64 + 2i, 65 + 2i) of one
+        // row (two bf16x2 stores), 4 rows per pass.
         const QkvEpiArgs& e = a.qkv;
         const bool is_v = tile >= e.Hq + e.Hkv, is_q = tile < e.Hq;
         const int n_end = min(n_hi, a.n_valid);
+        float* rsn = &sred[0][0];  // [BN] 1/rms of the head per row
         if (!is_v) {
-          for (int n = n_lo; n < n_end; ++n) {
-            const float x = stg[n * kBM + m];
-            const float ss = warp_sum(x * x);
-            if (lane == 0) sred[q][n] = ss;
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          const float gn = gpre;
-          for (int n = n_lo; n < n_end; ++n) {
-            const float ss = sred[0][n] + sred[1][n] + sred[2][n] + sred[3][n];
-            stg[n * kBM + m] *= (1.0f / sqrtf(ss / (float)kBM + e.eps)) * gn;
+          const int part = et & 7;
+          for (int n0 = n_lo; n0 < n_end; n0 += 16) {
+            const int n = n0 + (et >> 3);
+            float ss = 0.f;
+            if (n < n_end)
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float x = stg[n * kBM + j * 8 + part];
+                ss += x * x;
+              }
+            ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+            ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+            ss += __shfl_xor_sync(0xffffffffu, ss, 4);
+            if (part == 0 && n < n_end) rsn[n] = 1.0f / sqrtf(ss / (float)kBM + e.eps);
           }
           asm volatile("bar.sync 1, 128;" ::: "memory");
         }
         const int hk = tile - e.Hq - (is_v ? e.Hkv : 0);
-        for (int n = n_lo; n < n_end; ++n) {
-          const int row = a.row0 + n;
+        const int i2 = (et & 31) * 2;
+        for (int n = n_lo + (et >> 5); n < n_end; n += 4) {
           if (!srow_act[n]) continue;
-          float y = stg[n * kBM + m];
+          const int row = a.row0 + n;
+          float2 lo = *reinterpret_cast<const float2*>(stg + n * kBM + i2);
+          float2 hi = *reinterpret_cast<const float2*>(stg + n * kBM + 64 + i2);
           if (!is_v) {
-            const int i = m & 63;
-            const float c = pre[n * kBM + i], sn = pre[n * kBM + 64 + i];
-            y = m < 64 ? (y * c - stg[n * kBM + m + 64] * sn) : (y * c + stg[n * kBM + m - 64] * sn);
+            const float r = rsn[n];
+            lo.x *= r * gq0.x;
+            lo.y *= r * gq0.y;
+            hi.x *= r * gq1.x;
+            hi.y *= r * gq1.y;
+            const float2 c = *reinterpret_cast<const float2*>(pre + n * kBM + i2);
+            const float2 s = *reinterpret_cast<const float2*>(pre + n * kBM + 64 + i2);
+            const float2 ylo = make_float2(lo.x * c.x - hi.x * s.x, lo.y * c.y - hi.y * s.y);
+            const float2 yhi = make_float2(hi.x * c.x + lo.x * s.x, hi.y * c.y + lo.y * s.y);
+            lo = ylo;
+            hi = yhi;
           }
-          const __nv_bfloat16 b = __float2bfloat16_rn(y);
+          const __nv_bfloat162 blo = __floats2bfloat162_rn(lo.x, lo.y), bhi = __floats2bfloat162_rn(hi.x, hi.y);
+          __nv_bfloat16* dst;
           if (is_q) {
-            e.q_out[((size_t)row * e.Hq + tile) * kBM + m] = b;
+            dst = e.q_out + ((size_t)row * e.Hq + tile) * kBM;
           } else {
             const int kvsel = is_v ? 1 : 0;
             const int loc = srow_kv[n];
             size_t off;
-            if (e.prefill) off = (((size_t)kvsel * e.Hkv + hk) * e.pcap + loc) * kBM + m;
-            else off = ((((size_t)(loc / e.pt) * 2 + kvsel) * e.Hkv + hk) * e.pt + loc % e.pt) * kBM + m;
-            e.kv[off] = b;
+            if (e.prefill) off = (((size_t)kvsel * e.Hkv + hk) * e.pcap + loc) * kBM;
+            else off = ((((size_t)(loc / e.pt) * 2 + kvsel) * e.Hkv + hk) * e.pt + loc % e.pt) * kBM;
+            dst = e.kv + off;
           }
+          *reinterpret_cast<__nv_bfloat162*>(dst + i2) = blo;
+          *reinterpret_cast<__nv_bfloat162*>(dst + 64 + i2) = bhi;
         }
       } else if constexpr (EPI == EPI_SAMPLE) {
         const bool lp = a.lp_key != nullptr;

@@ -1956,7 +1956,7 @@ extern "C" is_status is_profile_step_graph(is_ctx* c, float* h_ms, int32_t* h_ki
 
 extern "C" is_status is_dbg_gemm(const void* d_w, const void* d_x, float* d_y, int32_t M, int32_t K, int32_t rows,
                                  int32_t split, void* stream) {
-  if (rows < 1 || rows > 64 || K % 64 || split < 1 || split > 8) return fail(IS_ERR_CONFIG, "bad dbg_gemm shape");
+  if (rows < 1 || rows > 64 || K % 64 || M % 4 || split < 1 || split > 8) return fail(IS_ERR_CONFIG, "bad dbg_gemm shape");
   if (!g_num_sms) {  // (cudaGetDeviceProperties costs milliseconds: once)
     int dev = 0;
     CK(cudaGetDevice(&dev));

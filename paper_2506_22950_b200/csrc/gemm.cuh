@@ -133,10 +133,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  __shared__ unsigned long long skey[BN];
-  __shared__ float sred[4][BN];
-  __shared__ unsigned long long swkey[4][BN];  // SAMPLE: per-warp best key, its logit, tile max / sum
-  __shared__ float swz[4][BN], swm[4][BN];
+  __shared__ float sred[4][BN];  // QKV: per-row 1/rms of the head
   __shared__ float run_m[BN], run_l[BN], run_z[BN];  // the CTA's running log-sum-exp state per row
   __shared__ unsigned long long run_k[BN];
   __shared__ int srow_act[BN], srow_kv[BN];
@@ -172,7 +169,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
   if (EPI == EPI_SAMPLE && threadIdx.x < BN) {
-    skey[threadIdx.x] = 0ull;
     run_m[threadIdx.x] = -INFINITY;
     run_l[threadIdx.x] = 0.f;
     run_z[threadIdx.x] = 0.f;
@@ -495,90 +491,90 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           *reinterpret_cast<__nv_bfloat162*>(dst + 64 + i2) = bhi;
         }
       } else if constexpr (EPI == EPI_SAMPLE) {
+        // one row per warp and pass (rows n = warp, warp + 4, ...; a row always meets the same
+        // warp, which keeps its running log-sum-exp state): lane l owns the tile's vocabulary
+        // entries v = 4l .. 4l + 3, whose Gumbel words are exactly the 4 words of the Philox4x32-10
+        // call with counter v >> 2 (R10/R11); in-lane argmax of the keys, one warp butterfly per row,
+        // one atomicMax per (row, tile)
         const bool lp = a.lp_key != nullptr;
         const int nv = min(BN, a.n_valid);
-        // Philox4x32-10 yields 4 words per counter (v >> 2, t, uid): the 4 lanes of a quad (the same
-        // v >> 2) compute one call each, for 4 different rows, and swap words by shuffles
-        uint32_t pw[4] = {0u, 0u, 0u, 0u};
-        for (int n = 0; n < nv; ++n) {
-          if ((n & 3) == 0) {
-            const int nq = n + (lane & 3);
-            if (nq < nv) {
-              const Philox4 o = philox4x32_10((uint32_t)gm >> 2, (uint32_t)a.row_t[a.row0 + nq],
-                                              (uint32_t)a.row_uid[a.row0 + nq], 0u, (uint32_t)a.seed,
-                                              (uint32_t)(a.seed >> 32));
-              pw[0] = o.x[0];
-              pw[1] = o.x[1];
-              pw[2] = o.x[2];
-              pw[3] = o.x[3];
+        const int g4 = tile * kBM + 4 * lane;
+        for (int n = et >> 5; n < nv; n += 4) {
+          const int row = a.row0 + n;
+          if (!a.row_active[row]) continue;  // (warp-uniform)
+          const float4 zs = *reinterpret_cast<const float4*>(stg + n * kBM + 4 * lane);
+          const float zv[4] = {zs.x, zs.y, zs.z, zs.w};
+          const Philox4 o = philox4x32_10((uint32_t)g4 >> 2, (uint32_t)a.row_t[row], (uint32_t)a.row_uid[row], 0u,
+                                          (uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+          unsigned long long key = 0ull;
+          float zk = -INFINITY, zmax = -INFINITY;
+          float sc4[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            sc4[j] = 0.f;
+            if (g4 + j < a.M) {
+              const float z = zv[j];
+              const float g = -logf_is(-logf_is(uniform_from_bits(o.x[j])));  // = gumbel(seed, uid, t, v)
+              const float sc = __fadd_rn(__fmul_rn(z, a.inv_temp), g);
+              sc4[j] = sc;
+              const unsigned long long k = order_key(sc, (uint32_t)(g4 + j));
+              if (k > key) {
+                key = k;
+                zk = z;
+              }
+              zmax = fmaxf(zmax, z);
             }
           }
-          const int src = (lane & ~3) | (n & 3);  // the quad lane holding row n's words
-          const uint32_t x0 = __shfl_sync(0xffffffffu, pw[0], src), x1 = __shfl_sync(0xffffffffu, pw[1], src);
-          const uint32_t x2 = __shfl_sync(0xffffffffu, pw[2], src), x3 = __shfl_sync(0xffffffffu, pw[3], src);
-          if (!a.row_active[a.row0 + n]) continue;
-          unsigned long long key = 0ull;
-          float z = -INFINITY;
-          if (gm < a.M) {
-            z = stg[n * kBM + m];
-            if (a.logits_dump) a.logits_dump[(size_t)(a.row0 + n) * a.ld_out + gm] = z;
-            const uint32_t wv = (gm & 3) == 0 ? x0 : ((gm & 3) == 1 ? x1 : ((gm & 3) == 2 ? x2 : x3));
-            const float g = -logf_is(-logf_is(uniform_from_bits(wv)));  // = gumbel(seed, uid, t, gm)
-            const float sc = __fadd_rn(__fmul_rn(z, a.inv_temp), g);
-            if (a.score_dump) a.score_dump[(size_t)(a.row0 + n) * a.ld_out + gm] = sc;
-            key = order_key(sc, (uint32_t)gm);
+          if (g4 + 3 < a.M) {
+            if (a.logits_dump) *reinterpret_cast<float4*>(a.logits_dump + (size_t)row * a.ld_out + g4) = zs;
+            if (a.score_dump)
+              *reinterpret_cast<float4*>(a.score_dump + (size_t)row * a.ld_out + g4) = make_float4(sc4[0], sc4[1], sc4[2], sc4[3]);
+          } else {
+            for (int j = 0; j < 4; ++j)
+              if (g4 + j < a.M) {
+                if (a.logits_dump) a.logits_dump[(size_t)row * a.ld_out + g4 + j] = zv[j];
+                if (a.score_dump) a.score_dump[(size_t)row * a.ld_out + g4 + j] = sc4[j];
+              }
           }
-          float zk = z;  // logit carried with the key
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-            const float oz = __shfl_xor_sync(0xffffffffu, zk, o);
+          for (int s = 16; s > 0; s >>= 1) {
+            const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, s);
+            const float oz = __shfl_xor_sync(0xffffffffu, zk, s);
             if (other > key) {
               key = other;
               zk = oz;
             }
           }
-          if (lane == 0) atomicMax(&skey[n], key);
+          if (lane == 0 && key) atomicMax(a.keys + row, key);
           if (lp) {
-            // per-warp (max, sum exp) of the tile's logits for this row (log-probabilities, NEXT-3)
-            const float wm = warp_max(z);
-            const float ws = warp_sum(z == -INFINITY ? 0.f : expf(z - wm));
+            // the tile's (max, sum exp) of this row's logits, folded into the warp's running state
+            const float wm = warp_max(zmax);
+            float se = 0.f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (g4 + j < a.M && zv[j] != -INFINITY) se += expf(zv[j] - wm);
+            const float ws = warp_sum(se);
             if (lane == 0) {
-              swkey[q][n] = key;
-              swz[q][n] = zk;
-              swm[q][n] = wm;
-              sred[q][n] = ws;
-            }
-          }
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (threadIdx.x - 64 < BN) {
-          const int n = threadIdx.x - 64;
-          if (skey[n]) atomicMax(a.keys + a.row0 + n, skey[n]);
-          skey[n] = 0ull;
-          if (lp && n < a.n_valid && a.row_active[a.row0 + n]) {
-            // fold the tile into the CTA's running state (warps in fixed order), publish it
-            float M = run_m[n], L = run_l[n];
-            for (int w = 0; w < 4; ++w) {
-              const float mw = swm[w][n];
-              if (mw == -INFINITY) continue;
-              const float Mn = fmaxf(M, mw);
-              L = (M == -INFINITY ? 0.f : L * expf(M - Mn)) + sred[w][n] * expf(mw - Mn);
-              M = Mn;
-              if (swkey[w][n] > run_k[n]) {
-                run_k[n] = swkey[w][n];
-                run_z[n] = swz[w][n];
+              float M = run_m[n], L = run_l[n];
+              if (wm != -INFINITY) {
+                const float Mn = fmaxf(M, wm);
+                L = (M == -INFINITY ? 0.f : L * expf(M - Mn)) + ws * expf(wm - Mn);
+                M = Mn;
+                if (key > run_k[n]) {
+                  run_k[n] = key;
+                  run_z[n] = zk;
+                }
               }
+              run_m[n] = M;
+              run_l[n] = L;
+              const size_t idx = (size_t)row * gridDim.x + blockIdx.x;
+              a.lp_key[idx] = run_k[n];
+              a.lp_mlz[idx] = make_float4(M, L, run_z[n], 0.f);
             }
-            run_m[n] = M;
-            run_l[n] = L;
-            const size_t idx = (size_t)(a.row0 + n) * gridDim.x + blockIdx.x;
-            a.lp_key[idx] = run_k[n];
-            a.lp_mlz[idx] = make_float4(M, L, run_z[n], 0.f);
           }
         }
       }
-      // stg / pre / skey are rewritten by the next tile
+      // stg / pre are rewritten by the next tile
       asm volatile("bar.sync 1, 128;" ::: "memory");
     }
   }

@@ -763,7 +763,12 @@ __global__ void __launch_bounds__(32 * NW, 1) attn_suffix_mma_kernel(const __gri
   // them re-arms the pair's counters)
   const int npairs = a.rows * a.Hkv;
   int nm = 0;
-  for (int k = is_early ? blockIdx.x + warp * early : npairs * REP; k < npairs * REP; k += early * kSWarps) {
+  // merges packed onto the first CTAs (all their warps), so the other CTAs exit right after
+  // their units and free their SMs for the o_proj GEMM's CTAs, which then stream their weights
+  // during the merges
+  const int nmc = min(early, (npairs * REP + kSWarps - 1) / kSWarps);
+  for (int k = (is_early && (int)blockIdx.x < nmc) ? blockIdx.x * kSWarps + warp : npairs * REP; k < npairs * REP;
+       k += nmc * kSWarps) {
     const int i = k / REP, e = k - i * REP;
     const int r = i / a.Hkv, h = i - r * a.Hkv;
     if (!a.row_active[r]) continue;

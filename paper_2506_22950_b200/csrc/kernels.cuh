@@ -603,9 +603,21 @@ __global__ void __launch_bounds__(32 * NW, 1) attn_suffix_mma_kernel(const __gri
     }
     return cd;
   };
-  // this warp's stages zero-filled (finite stale rows, see consume) while its items load
-  for (int i = lane; i < kSWStages * SM::kStage / 16; i += 32)
-    reinterpret_cast<uint4*>(wsm)[i] = make_uint4(0, 0, 0, 0);
+  // Finite stale rows (see consume): a unit always loads its first page, and masked keys only
+  // need finite V rows (their scores are replaced by -inf, their P is 0), so only the V rows of
+  // pages 1.. of each stage are zeroed (stale later on = earlier units' V, finite); the K rows
+  // and the rest of the stage are left as they are.  (dbg 64: the whole stage, as before)
+  if (a.dbg_mode & 64) {
+    for (int i = lane; i < kSWStages * SM::kStage / 16; i += 32) reinterpret_cast<uint4*>(wsm)[i] = make_uint4(0, 0, 0, 0);
+  } else {
+#pragma unroll 1
+    for (int s = 0; s < kSWStages; ++s)
+#pragma unroll 1
+      for (int j = 1; j < kSUnit / pt; ++j) {
+        uint4* vb = reinterpret_cast<uint4*>(wsm + s * SM::kStage + (2 * j * pt + pt) * 256);
+        for (int i = lane; i < pt * 256 / 16; i += 32) vb[i] = make_uint4(0, 0, 0, 0);
+      }
+  }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the TMA writes
   __syncwarp();
   static_assert(kSWStages == 1 || kSWStages == 2, "the consume loop is unrolled over one or two stages");
